@@ -1,0 +1,186 @@
+"""rqb / rsvd / rpca / rrpca, step by step in the paper's order (oracle, FP64).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+``oracle_rsvd`` follows Alg. 4 ``rqb``, Alg. 2
+``sub_iterations`` and Alg. 5 ``rsvd``:
+
+  (1) l = k + p                      (Alg. 4 step 1; clamp l <= min(m,n), reading R10)
+  (2) Omega = rnorm(n, l)            (step 2; counter spec, oracle/philox.py)
+  (3) Y = A Omega                    (step 3, Eq. YAQ)
+  (4) for j = 1..q:                  (Alg. 2)
+        [Q,~] = qr(Y); [Q,~] = qr(A^T Q); Y = A Q
+  (9) [Q,~] = qr(Y)                  (step 9; reading R3: the last QR follows the loop)
+  (10) B = Q^T A                     (step 10, Eq. BQA) -- formed as B^T = A^T Q
+  Alg. 5 (2) [U~, Sigma, V] = svd(B)  (economic; jacobi_svd_bt on B^T)
+  Alg. 5 (3) U = Q U~                (Eq. UQU)
+  return U(:,1:nu), d = diag(Sigma)(1:k), V(:,1:nv)
+  plus the sign convention of reading R9 (largest-|.| entry of each V column >= 0).
+
+Matrix products use numpy's ``@`` (a library primitive, as the task allows);
+the QR and SVD are written out in oracle/linalg.py.
+"""
+import numpy as np
+
+from .linalg import hqr, jacobi_svd_bt, soft_threshold
+from .philox import omega
+
+
+def resolve_params(m, n, k, nu=None, nv=None, p=10, q=2):
+    """Parameter resolution (step a1; readings R10, R11).
+
+    1 <= k <= min(m, n) else ValueError; p >= 0, q >= 0; l = min(k+p, min(m,n));
+    nu, nv default k, values > k are clamped to k, 0 means "not formed".
+    """
+    mn = min(m, n)
+    if not (1 <= k <= mn):
+        raise ValueError("k must satisfy 1 <= k <= min(m, n)")
+    if p < 0 or q < 0:
+        raise ValueError("p and q must be >= 0")
+    nu = k if nu is None else min(max(int(nu), 0), k)
+    nv = k if nv is None else min(max(int(nv), 0), k)
+    l = min(k + p, mn)
+    return k, nu, nv, l
+
+
+def sign_fix(U, V):
+    """Reading R9: for every column i, if the largest-|.| entry of V(:,i)
+    (lowest index on ties) is negative, negate V(:,i) and U(:,i)."""
+    U = U.copy()
+    V = V.copy()
+    for i in range(V.shape[1]):
+        idx = int(np.argmax(np.abs(V[:, i])))
+        if V[idx, i] < 0:
+            V[:, i] = -V[:, i]
+            if U is not None and i < U.shape[1]:
+                U[:, i] = -U[:, i]
+    return U, V
+
+
+def _prepare(A, center=False, scale=False):
+    """Upcast exactly to FP64; optional column centring/scaling (Alg. 6)."""
+    X = np.array(A, dtype=np.float64)
+    m = X.shape[0]
+    c = None
+    s = None
+    if center:
+        c = X.sum(axis=0) / m
+        X = X - c[None, :]
+    if scale:
+        s = np.sqrt((X * X).sum(axis=0) / (m - 1))
+        s = np.where(s > 0, s, 1.0)
+        X = X / s[None, :]
+    return X, c, s
+
+
+def oracle_rqb(A, l, q=2, sdist="normal", seed=0, stream=0, omega_dtype=np.float64):
+    """Alg. 4 rqb with Alg. 2 sub_iterations: returns Q (m x l), B^T (n x l)."""
+    X = np.asarray(A, dtype=np.float64)
+    m, n = X.shape
+    Om = omega(n, l, sdist, seed, stream, dtype=omega_dtype)   # step (2)
+    Y = X @ Om                                                  # step (3)
+    for _ in range(q):                                          # step (4), Alg. 2
+        Q, _r = hqr(Y)                                          #   (2)
+        Qz, _r = hqr(X.T @ Q)                                   #   (3)
+        Y = X @ Qz                                              #   (4)
+    Q, _r = hqr(Y)                                              # step (9)
+    Bt = X.T @ Q                                                # step (10), B^T = A^T Q
+    return Q, Bt
+
+
+def oracle_rsvd(A, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0,
+                stream=0, center=False, scale=False, full=False):
+    """Alg. 5 rsvd with the interface of P:708.
+
+    Returns dict(d, u, v, l, center, scale) -- d: (k,), u: m x nu, v: n x nv.
+    ``full=True`` additionally returns the untruncated l-column factors.
+    FP32 ``A`` -> Omega rounded to FP32 (reading R12), arithmetic in FP64.
+    """
+    A = np.asarray(A)
+    omega_dtype = np.float32 if A.dtype == np.float32 else np.float64
+    X, c, s = _prepare(A, center, scale)
+    m, n = X.shape
+    k, nu, nv, l = resolve_params(m, n, k, nu, nv, p, q)
+    transposed = m < n
+    W = X.T if transposed else X
+    Q, Bt = oracle_rqb(W, l, q, sdist, seed, stream, omega_dtype)
+    sigma, Ut, V, sweeps = jacobi_svd_bt(Bt)                    # Alg. 5 (2)
+    U = Q @ Ut                                                  # Alg. 5 (3), Eq. UQU
+    if transposed:
+        U, V = V, U
+    U, V = sign_fix(U, V)
+    out = dict(d=sigma[:k].copy(), u=U[:, :nu].copy(), v=V[:, :nv].copy(), l=l,
+               center=c, scale=s, sweeps=sweeps)
+    if full:
+        out.update(d_full=sigma, u_full=U, v_full=V)
+    return out
+
+
+def oracle_rpca(A, k, center=True, scale=False, retx=True, p=10, q=2,
+                sdist="normal", seed=0, stream=0):
+    """Alg. 6 rpca / interface P:1381-1398.
+
+    rsvd on the centred (and optionally scaled) X; eigenvalues
+    Lambda = Sigma^2 / (m-1) (Eq. P:1322), rotation = V, sdev = sqrt(Lambda),
+    scores x = U Sigma (= X V).
+    """
+    r = oracle_rsvd(A, k, p=p, q=q, sdist=sdist, seed=seed, stream=stream,
+                    center=center, scale=scale)
+    m = np.asarray(A).shape[0]
+    eig = r["d"] ** 2 / (m - 1)
+    out = dict(rotation=r["v"], eigvals=eig, sdev=np.sqrt(eig), center=r["center"],
+               scale=r["scale"], d=r["d"])
+    if retx:
+        out["x"] = r["u"] * r["d"][None, :]
+    return out
+
+
+def oracle_rrpca(A, lam=None, maxiter=100, tol=1e-7, k=20, p=10, q=2,
+                 sdist="normal", seed=0, trace=False):
+    """Alg. 7 rrpca, the inexact ALM loop, readings R17-R23.
+
+    lambda = max(m,n)^-1/2;  ||A||_2 = sigma_1 of rsvd(A, 1, p, q,
+    stream 0) (R18);  mu_0 = 1.25 / ||A||_2 (R17);  Z = A / J(A) with
+    J(A) = max(||A||_2, ||A||_max / lambda) (R19);  S = 0.  Then repeat:
+      (6)  [U, Sigma, V] = rsvd(A - S + Z/mu, k, p, q)   (fresh Omega: stream t, R23)
+      (7)  l = #{sigma_i > 1/mu}                         (fixed k, R22)
+      (8)  Sigma_l = soft_thres(sigma(1:l), 1/mu)
+      (9)  L = U(:,1:l) Sigma_l V(:,1:l)^T
+      (10) S = soft_thres(A - L + Z/mu, lambda/mu)
+      (11) Z = Z + (A - L - S) mu
+      (12) mu = min(1.5 mu, 1e7 mu_0)                    (R20)
+      until ||A - L - S||_F / ||A||_F < tol  (R21; evaluated after step 11)
+    Returns dict(L, S, iters, residual, trace=[(res, l, mu)...]).
+    """
+    A = np.asarray(A, dtype=np.float64)
+    m, n = A.shape
+    if lam is None or lam <= 0:
+        lam = 1.0 / np.sqrt(max(m, n))
+    norm2 = oracle_rsvd(A, 1, p=p, q=q, sdist=sdist, seed=seed, stream=0)["d"][0]
+    mu0 = 1.25 / norm2
+    mu = mu0
+    dual = max(norm2, np.max(np.abs(A)) / lam)
+    Z = A / dual
+    S = np.zeros_like(A)
+    normF = np.sqrt(np.sum(A * A))
+    hist = []
+    L = np.zeros_like(A)
+    res = np.inf
+    it = 0
+    for it in range(1, maxiter + 1):
+        M = A - S + Z / mu
+        r = oracle_rsvd(M, k, p=p, q=q, sdist=sdist, seed=seed, stream=it)
+        d = r["d"]
+        nl = int(np.sum(d > 1.0 / mu))
+        dl = soft_threshold(d[:nl], 1.0 / mu)
+        L = (r["u"][:, :nl] * dl[None, :]) @ r["v"][:, :nl].T
+        S = soft_threshold(A - L + Z / mu, lam / mu)
+        E = A - L - S
+        Z = Z + E * mu
+        res = np.sqrt(np.sum(E * E)) / normF
+        hist.append((res, nl, mu))
+        mu = min(1.5 * mu, 1e7 * mu0)
+        if res < tol:
+            break
+    return dict(L=L, S=S, iters=it, residual=res, trace=hist, lam=lam, mu0=mu0,
+                norm2=norm2)
