@@ -1,0 +1,174 @@
+/*
+ * rsvd_b200.h -- C ABI of the B200-native randomized SVD hot path
+ * (arXiv 1608.02148, the `rsvd` package).  sm_100a only.
+ *
+ * Everything here is plain C: pointers (host or device, as stated per
+ * argument) and sizes.  No torch types.  The Python binding
+ * (paper_1608_02148_b200/__init__.py) marshals arguments only.
+ *
+ * Conventions common to every entry point
+ * ---------------------------------------
+ *  * Matrices are ROW-MAJOR with an explicit leading dimension (elements, not
+ *    bytes): element (i, j) of X lives at X[i*ldx + j], ldx >= #columns.
+ *  * "device" = memory of the context's CUDA device (cudaMalloc / torch).
+ *    The library never frees caller memory; it owns only its workspace.
+ *  * All work is enqueued on the context's stream (the one given to
+ *    rsvd_create).  Calls that return a status read a small device status
+ *    word at the end (one stream synchronisation); outputs are valid when
+ *    the call returns RSVD_OK.
+ *  * Validation errors (RSVD_EINVAL / RSVD_EUNSUPPORTED) are returned BEFORE
+ *    any launch and write nothing.  rsvd_last_error() gives the message for
+ *    the last non-OK status, or a warning (e.g. nu > k clamped).
+ *  * dtype RSVD_F64: A, u, d, v are double.  RSVD_F32: A, u, d, v are float;
+ *    the power-scheme panels, the small SVD and the orthonormalisations run
+ *    in FP64 (reading R12).
+ *  * Distributed mode (after rsvd_comm_init with nranks > 1): A is row-sharded,
+ *    this rank holds rows [row_offset, row_offset + m_local) of the m_global x n
+ *    matrix; u returns this rank's rows, d and v are replicated.  Requires
+ *    m_global >= n.  Collectives: NCCL allreduce(sum) of the n x l partials
+ *    (Z = A^T Q, B^T = A^T Q), of l x l Gram matrices and of column sums.
+ */
+#ifndef RSVD_B200_H
+#define RSVD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RSVD_OK = 0,
+  RSVD_EINVAL = 1,        /* bad argument (nothing launched, nothing written) */
+  RSVD_ENOMEM = 2,        /* workspace allocation failed                      */
+  RSVD_ECUDA = 3,         /* CUDA runtime error (message in rsvd_last_error)  */
+  RSVD_ENCCL = 4,         /* NCCL error                                       */
+  RSVD_ENUMERIC = 5,      /* non-finite intermediate or Jacobi sweep cap hit  */
+  RSVD_EUNSUPPORTED = 6   /* valid request outside this build's envelope      */
+} rsvd_status;
+
+/* Random test matrix distributions, PAPER.md:417-430 (§2.3) and the
+ * `sdist = c("normal", "unif", "rademacher")` argument. */
+typedef enum { RSVD_NORMAL = 0, RSVD_UNIF = 1, RSVD_RADEMACHER = 2 } rsvd_sdist;
+typedef enum { RSVD_F64 = 0, RSVD_F32 = 1 } rsvd_dtype;
+
+typedef struct rsvd_ctx rsvd_ctx;   /* opaque: device, stream, workspace, comm */
+
+/* Create a context bound to `device` and `cuda_stream` (a cudaStream_t; NULL
+ * = legacy default stream).  The stream must outlive the context. */
+rsvd_status rsvd_create(rsvd_ctx** ctx, int device, void* cuda_stream);
+rsvd_status rsvd_destroy(rsvd_ctx* ctx);
+const char* rsvd_last_error(const rsvd_ctx* ctx);
+const char* rsvd_version(void);
+
+/* NCCL plumbing (multi-GPU, one process per GPU).  rank 0 calls
+ * rsvd_nccl_unique_id (writes 128 bytes to host memory `out`), the caller
+ * broadcasts them (e.g. torch.distributed), and every rank calls
+ * rsvd_comm_init.  nranks == 1 is accepted and means single-GPU. */
+rsvd_status rsvd_nccl_unique_id(void* out128);
+rsvd_status rsvd_comm_init(rsvd_ctx* ctx, const void* nccl_unique_id128, int nranks, int rank);
+
+/* Input matrix descriptor.  `A` is caller-owned DEVICE memory, read-only,
+ * row-major m_local x n with leading dimension lda >= n; it must stay valid
+ * until the call returns.  Single GPU: m_global == m_local, row_offset == 0. */
+typedef struct {
+  int32_t dtype;          /* rsvd_dtype */
+  const void* A;
+  int64_t m_local, n, lda;
+  int64_t m_global, row_offset;
+} rsvd_matrix;
+
+/* rsvd parameters: rsvd(A, k, nu = NULL, nv = NULL, p = 10, q = 2,
+ * sdist = "normal") (§3.6).
+ *   k      target rank, 1 <= k <= min(m, n) (reading R10)
+ *   nu,nv  number of left/right singular vectors to return; values
+ *          > k are clamped to k with a warning; 0 = not formed
+ *   p      oversampling, l = min(k + p, min(m, n)) (Alg. 4 step 1)
+ *   q      subspace iterations (Alg. 2)
+ *   seed, stream  counter-based Omega (reading R1)
+ *   center  1 = implicit column centring of A (rpca, Alg. 6)
+ *   scale   1 = implicit column scaling by the (centred) column s.d. */
+typedef struct {
+  int32_t k, nu, nv, p, q;
+  int32_t sdist;          /* rsvd_sdist */
+  uint64_t seed, stream;
+  int32_t center, scale;
+} rsvd_params;
+
+/* Fill the defaults of P:708: nu = nv = k, p = 10, q = 2, normal, seed 0,
+ * stream 0, no centring/scaling. */
+void rsvd_params_default(rsvd_params* prm, int32_t k);
+
+/* Randomized SVD, Alg. 5 on top of Alg. 4 rqb.
+ *   u  DEVICE, m_local x nu, row-major, ldu >= nu (NULL iff nu == 0): this
+ *      rank's rows of U(:, 1:nu)
+ *   d  DEVICE, k values of the dtype of A, descending (replicated)
+ *   v  DEVICE, n x nv, row-major, ldv >= nv (NULL iff nv == 0); V is NOT
+ *      transposed (replicated)
+ * Sign convention (reading R9): the largest-|.| entry of each V column is
+ * positive; the same flip is applied to U. */
+rsvd_status rsvd_run(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm,
+                     void* u, int64_t ldu, void* d, void* v, int64_t ldv);
+
+/* Randomized QB decomposition, Alg. 4, with the final QR
+ * of reading R3.  Q: DEVICE m_local x l (ldq >= l), this rank's rows;
+ * Bt: DEVICE n x l (ldb >= l), B^T = A^T Q, replicated.  l = min(k+p, min(m,n)).
+ * Results in the dtype of A. */
+rsvd_status rsvd_rqb(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm,
+                     void* Q, int64_t ldq, void* Bt, int64_t ldb);
+
+/* Randomized PCA, Alg. 6, interface P:1381-1398:
+ * rsvd on X = (A - 1 c^T) diag(1/s) (centring/scaling never materialised).
+ *   rotation DEVICE n x k (ldr >= k)       = V
+ *   eigvals  DEVICE k                      = d^2 / (m - 1)   (Eq. P:1322)
+ *   x        DEVICE m_local x k (ldx >= k) = U diag(d) scores, NULL = retx FALSE
+ *   center   DEVICE n column means (NULL = not returned; prm->center selects)
+ *   scale    DEVICE n column s.d. (NULL = not returned)
+ * Outputs in the dtype of A. */
+rsvd_status rsvd_rpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm,
+                      void* rotation, int64_t ldr, void* eigvals, void* x, int64_t ldx,
+                      void* center, void* scale);
+
+/* Randomized robust PCA by inexact ALM, Alg. 7, with the
+ * readings R17-R23 of DESIGN.md (mu_0 = 1.25/||A||_2, fixed target rank k,
+ * fresh Omega stream t per iteration, mu <- min(1.5 mu, 1e7 mu_0)).
+ *   lambda  <= 0 selects max(m, n)^-1/2
+ *   tol     stop when ||A - L - S||_F / ||A||_F < tol
+ * FP64 only.  L, S: DEVICE m_local x n (ld >= n), caller-owned.
+ *   iters, final_residual: HOST out-params (nullable)
+ *   trace: HOST, nullable, 3*maxiter doubles (residual, l, mu) per iteration */
+typedef struct {
+  double lambda, tol;
+  int32_t maxiter;
+  int32_t k, p, q;
+  int32_t sdist;
+  uint64_t seed;
+} rsvd_rrpca_params;
+void rsvd_rrpca_params_default(rsvd_rrpca_params* prm);
+rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_rrpca_params* prm,
+                       void* L, void* S, int64_t ld, int32_t* iters, double* final_residual,
+                       double* trace);
+
+/* Random test matrix alone (K1): writes the n x l matrix
+ * Omega to DEVICE `out` (row-major, ldo >= l) in `dtype` (FP32 = round to
+ * nearest of the FP64 value).  Exposed for bit-exact parity tests. */
+rsvd_status rsvd_omega(rsvd_ctx* ctx, int64_t n, int64_t l, int32_t sdist, uint64_t seed,
+                       uint64_t stream, int32_t dtype, void* out, int64_t ldo);
+
+/* Per-kernel timing of the last calls (CUDA events on the context stream,
+ * enabled by rsvd_set_profiling(ctx, 1)).  kind: 0 = sketch/power pass A.X,
+ * 1 = transposed pass A^T.X (incl. its split reduction), 2 = panel
+ * orthonormalisation, 3 = small SVD, 4 = other.  Returns accumulated
+ * milliseconds and launch count since the last reset (HOST out-params). */
+rsvd_status rsvd_set_profiling(rsvd_ctx* ctx, int enable);
+rsvd_status rsvd_profile(rsvd_ctx* ctx, int kind, double* total_ms, int64_t* count,
+                         double* bytes);
+rsvd_status rsvd_profile_reset(rsvd_ctx* ctx);
+/* Number of kernels this library launched since the last reset. */
+int64_t rsvd_launch_count(const rsvd_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSVD_B200_H */

@@ -1,0 +1,316 @@
+"""B200-native randomized SVD (arXiv 1608.02148, the `rsvd` package) -- Python binding.
+
+Thin ctypes binding of the C ABI in ``include/rsvd_b200.h``: argument
+marshalling only.  Every step of the hot path (Omega, the passes over A, the
+panel orthonormalisations, the Jacobi SVD, the IALM updates) runs in the CUDA
+kernels of ``csrc/``; torch is used for device memory, streams and process
+groups.  There is no CPU fallback: if the extension is missing this module
+raises on import of the library.
+
+Paper interfaces mirrored:
+  rsvd(A, k, nu=NULL, nv=NULL, p=10, q=2, sdist="normal")     P:708   (§3.6)
+  rpca(A, k, center=TRUE, scale=TRUE, retx=TRUE, p=10, q=2)   P:1381  (§4.4)
+  rrpca(A, lambda=NULL, maxiter=50, tol=1e-5, p=10, q=2, ...) P:1736  (§5.4)
+  rqb(A, k, p, q)                                             Alg. 4
+"""
+import ctypes
+import os
+from collections import namedtuple
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "librsvd_b200.so")
+
+SDIST = {"normal": 0, "unif": 1, "rademacher": 2}
+STATUS = {0: "RSVD_OK", 1: "RSVD_EINVAL", 2: "RSVD_ENOMEM", 3: "RSVD_ECUDA", 4: "RSVD_ENCCL",
+          5: "RSVD_ENUMERIC", 6: "RSVD_EUNSUPPORTED"}
+EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_last_error", "rsvd_version", "rsvd_nccl_unique_id",
+           "rsvd_comm_init", "rsvd_params_default", "rsvd_run", "rsvd_rqb", "rsvd_rpca",
+           "rsvd_rrpca_params_default", "rsvd_rrpca", "rsvd_omega", "rsvd_set_profiling", "rsvd_profile",
+           "rsvd_profile_reset", "rsvd_launch_count"]
+
+
+class RsvdError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("%s: %s" % (STATUS.get(status, status), msg))
+        self.status = status
+
+
+class Matrix(ctypes.Structure):
+    _fields_ = [("dtype", ctypes.c_int32), ("A", ctypes.c_void_p), ("m_local", ctypes.c_int64),
+                ("n", ctypes.c_int64), ("lda", ctypes.c_int64), ("m_global", ctypes.c_int64),
+                ("row_offset", ctypes.c_int64)]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("nu", ctypes.c_int32), ("nv", ctypes.c_int32), ("p", ctypes.c_int32),
+                ("q", ctypes.c_int32), ("sdist", ctypes.c_int32), ("seed", ctypes.c_uint64),
+                ("stream", ctypes.c_uint64), ("center", ctypes.c_int32), ("scale", ctypes.c_int32)]
+
+
+class RrpcaParams(ctypes.Structure):
+    _fields_ = [("lam", ctypes.c_double), ("tol", ctypes.c_double), ("maxiter", ctypes.c_int32),
+                ("k", ctypes.c_int32), ("p", ctypes.c_int32), ("q", ctypes.c_int32), ("sdist", ctypes.c_int32),
+                ("seed", ctypes.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load the C-ABI library (built in-tree by build.py).  Raises if missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError("rsvd_b200 CUDA extension not built (%s); run __graft_entry__.build()" % LIB_PATH)
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, u64, dp = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+    MP, PP = ctypes.POINTER(Matrix), ctypes.POINTER(Params)
+    sig = {
+        "rsvd_create": ([ctypes.POINTER(vp), ctypes.c_int, vp], ctypes.c_int),
+        "rsvd_destroy": ([vp], ctypes.c_int),
+        "rsvd_last_error": ([vp], ctypes.c_char_p),
+        "rsvd_version": ([], ctypes.c_char_p),
+        "rsvd_nccl_unique_id": ([vp], ctypes.c_int),
+        "rsvd_comm_init": ([vp, vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+        "rsvd_params_default": ([PP, i32], None),
+        "rsvd_run": ([vp, MP, PP, vp, i64, vp, vp, i64], ctypes.c_int),
+        "rsvd_rqb": ([vp, MP, PP, vp, i64, vp, i64], ctypes.c_int),
+        "rsvd_rpca": ([vp, MP, PP, vp, i64, vp, vp, i64, vp, vp], ctypes.c_int),
+        "rsvd_rrpca_params_default": ([ctypes.POINTER(RrpcaParams)], None),
+        "rsvd_rrpca": ([vp, MP, ctypes.POINTER(RrpcaParams), vp, vp, i64, ctypes.POINTER(i32),
+                        ctypes.POINTER(dp), ctypes.POINTER(dp)], ctypes.c_int),
+        "rsvd_omega": ([vp, i64, i64, i32, u64, u64, i32, vp, i64], ctypes.c_int),
+        "rsvd_set_profiling": ([vp, ctypes.c_int], ctypes.c_int),
+        "rsvd_profile": ([vp, ctypes.c_int, ctypes.POINTER(dp), ctypes.POINTER(i64), ctypes.POINTER(dp)],
+                         ctypes.c_int),
+        "rsvd_profile_reset": ([vp], ctypes.c_int),
+        "rsvd_launch_count": ([vp], i64),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+class Context:
+    """A library context bound to one CUDA device and stream (default: torch's
+    current stream on that device)."""
+
+    def __init__(self, device=None, stream=None):
+        L = lib()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        h = ctypes.c_void_p()
+        st = L.rsvd_create(ctypes.byref(h), self.device.index or 0, ctypes.c_void_p(stream.cuda_stream))
+        if st != 0:
+            raise RsvdError(st, "rsvd_create failed")
+        self.h = h
+        self.rank, self.world = 0, 1
+
+    def check(self, st):
+        if st != 0:
+            raise RsvdError(st, lib().rsvd_last_error(self.h).decode())
+
+    def last_error(self):
+        return lib().rsvd_last_error(self.h).decode()
+
+    def init_comm(self, rank, world, group=None):
+        """NCCL communicator owned by the library: rank 0 makes the unique id,
+        torch.distributed broadcasts it (any backend), every rank joins."""
+        import torch.distributed as dist
+        buf = ctypes.create_string_buffer(128)
+        if rank == 0:
+            self.check(lib().rsvd_nccl_unique_id(buf))
+        obj = [bytes(buf.raw)]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        raw = ctypes.create_string_buffer(obj[0], 128)
+        self.check(lib().rsvd_comm_init(self.h, raw, world, rank))
+        self.rank, self.world = rank, world
+
+    def set_profiling(self, on=True):
+        self.check(lib().rsvd_set_profiling(self.h, 1 if on else 0))
+
+    def profile(self, kind):
+        ms, cnt, by = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
+        self.check(lib().rsvd_profile(self.h, kind, ctypes.byref(ms), ctypes.byref(cnt), ctypes.byref(by)))
+        return ms.value, cnt.value, by.value
+
+    def profile_reset(self):
+        self.check(lib().rsvd_profile_reset(self.h))
+
+    def launch_count(self):
+        return int(lib().rsvd_launch_count(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().rsvd_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx = {}
+
+
+def default_context(device=None):
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    if key not in _default_ctx:
+        _default_ctx[key] = Context(dev, torch.cuda.current_stream(dev))
+    return _default_ctx[key]
+
+
+def _matrix(A, m_global=None, row_offset=0):
+    if not A.is_cuda:
+        raise ValueError("A must be a CUDA tensor (use the *_host helpers for host buffers)")
+    if A.dim() != 2 or A.stride(1) != 1:
+        raise ValueError("A must be a 2-D row-major tensor with unit column stride")
+    if A.dtype == torch.float64:
+        dt = 0
+    elif A.dtype == torch.float32:
+        dt = 1
+    else:
+        raise ValueError("A must be float64 or float32")
+    m, n = A.shape
+    return Matrix(dt, A.data_ptr(), m, n, A.stride(0), m if m_global is None else m_global, row_offset)
+
+
+def _params(k, nu, nv, p, q, sdist, seed, stream, center=0, scale=0):
+    prm = Params()
+    lib().rsvd_params_default(ctypes.byref(prm), int(k))
+    prm.nu = int(k) if nu is None else int(nu)
+    prm.nv = int(k) if nv is None else int(nv)
+    prm.p, prm.q = int(p), int(q)
+    prm.sdist = SDIST[sdist] if isinstance(sdist, str) else int(sdist)
+    prm.seed, prm.stream = int(seed), int(stream)
+    prm.center, prm.scale = int(bool(center)), int(bool(scale))
+    return prm
+
+
+RsvdResult = namedtuple("RsvdResult", ["d", "u", "v"])
+
+
+def rsvd(A, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None,
+         m_global=None, row_offset=0, out=None):
+    """Randomized SVD (Alg. 5; interface P:708).
+
+    A: CUDA tensor (m x n, float64 or float32, row-major).  Returns (d, u, v)
+    with d (k,), u (m x nu) and v (n x nv, not transposed).  In distributed
+    mode (ctx.init_comm) A holds this rank's rows and u this rank's rows.
+    """
+    ctx = ctx or default_context(A.device)
+    mat = _matrix(A, m_global, row_offset)
+    mg = mat.m_global
+    kk = int(k)
+    nu_ = kk if nu is None else min(int(nu), kk)
+    nv_ = kk if nv is None else min(int(nv), kk)
+    prm = _params(k, nu, nv, p, q, sdist, seed, stream)
+    if not (1 <= kk <= min(mg, A.shape[1])):
+        raise RsvdError(1, "k must satisfy 1 <= k <= min(m, n)")
+    if out is None:
+        d = torch.empty(kk, dtype=A.dtype, device=A.device)
+        u = torch.empty(A.shape[0], max(nu_, 0), dtype=A.dtype, device=A.device)
+        v = torch.empty(A.shape[1], max(nv_, 0), dtype=A.dtype, device=A.device)
+    else:
+        d, u, v = out
+    ctx.check(lib().rsvd_run(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(u) if nu_ else ctypes.c_void_p(0),
+                             max(nu_, 1), _ptr(d), _ptr(v) if nv_ else ctypes.c_void_p(0), max(nv_, 1)))
+    return RsvdResult(d, u, v)
+
+
+def rsvd_host(A_host, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None,
+              device="cuda", staging=None):
+    """End-to-end call on a HOST matrix: H2D copy of A, rsvd, D2H of (d, u, v)."""
+    ctx = ctx or default_context(device)
+    if staging is None or staging.shape != A_host.shape or staging.dtype != A_host.dtype:
+        staging = torch.empty(A_host.shape, dtype=A_host.dtype, device=device)
+    staging.copy_(A_host, non_blocking=True)
+    r = rsvd(staging, k, nu, nv, p, q, sdist, seed, stream, ctx=ctx)
+    return RsvdResult(r.d.to("cpu", non_blocking=False), r.u.to("cpu"), r.v.to("cpu"))
+
+
+def rqb(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None, m_global=None, row_offset=0):
+    """Randomized QB (Alg. 4): returns (Q (m x l), B (l x n))."""
+    ctx = ctx or default_context(A.device)
+    mat = _matrix(A, m_global, row_offset)
+    l = min(int(k) + int(p), min(mat.m_global, A.shape[1]))
+    Q = torch.empty(A.shape[0], l, dtype=A.dtype, device=A.device)
+    Bt = torch.empty(A.shape[1], l, dtype=A.dtype, device=A.device)
+    prm = _params(k, 0, 0, p, q, sdist, seed, stream)
+    ctx.check(lib().rsvd_rqb(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(Q), l, _ptr(Bt), l))
+    return Q, Bt.T
+
+
+def rpca(A, k, center=True, scale=False, retx=True, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None,
+         m_global=None, row_offset=0):
+    """Randomized PCA (Alg. 6; interface P:1381-1398)."""
+    ctx = ctx or default_context(A.device)
+    mat = _matrix(A, m_global, row_offset)
+    m, n = A.shape
+    kk = int(k)
+    rot = torch.empty(n, kk, dtype=A.dtype, device=A.device)
+    eig = torch.empty(kk, dtype=A.dtype, device=A.device)
+    x = torch.empty(m, kk, dtype=A.dtype, device=A.device) if retx else None
+    c = torch.empty(n, dtype=A.dtype, device=A.device) if center else None
+    s = torch.empty(n, dtype=A.dtype, device=A.device) if scale else None
+    prm = _params(k, k, k, p, q, sdist, seed, stream, center, scale)
+    ctx.check(lib().rsvd_rpca(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(rot), kk, _ptr(eig), _ptr(x), kk,
+                              _ptr(c), _ptr(s)))
+    return dict(rotation=rot, eigvals=eig, sdev=eig.sqrt(), x=x, center=c, scale=s)
+
+
+def rrpca(A, lam=None, maxiter=50, tol=1e-5, p=10, q=2, k=20, sdist="normal", seed=0, trace=False, ctx=None,
+          m_global=None, row_offset=0):
+    """Randomized robust PCA by inexact ALM (Alg. 7; interface P:1736)."""
+    ctx = ctx or default_context(A.device)
+    mat = _matrix(A, m_global, row_offset)
+    prm = RrpcaParams()
+    lib().rsvd_rrpca_params_default(ctypes.byref(prm))
+    prm.lam = 0.0 if lam is None else float(lam)
+    prm.tol, prm.maxiter, prm.k, prm.p, prm.q = float(tol), int(maxiter), int(k), int(p), int(q)
+    prm.sdist = SDIST[sdist] if isinstance(sdist, str) else int(sdist)
+    prm.seed = int(seed)
+    L = torch.empty_like(A)
+    S = torch.empty_like(A)
+    it = ctypes.c_int32()
+    res = ctypes.c_double()
+    tr = (ctypes.c_double * (3 * int(maxiter)))()
+    ctx.check(lib().rsvd_rrpca(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(L), _ptr(S), A.shape[1],
+                               ctypes.byref(it), ctypes.byref(res), tr))
+    hist = [(tr[3 * i], int(tr[3 * i + 1]), tr[3 * i + 2]) for i in range(it.value)]
+    out = dict(L=L, S=S, iters=it.value, residual=res.value)
+    if trace:
+        out["trace"] = hist
+    return out
+
+
+def omega(n, l, sdist="normal", seed=0, stream=0, dtype=torch.float64, device="cuda", ctx=None):
+    """The random test matrix Omega (n x l) from the device generator (K1)."""
+    ctx = ctx or default_context(device)
+    out = torch.empty(n, l, dtype=dtype, device=device)
+    sd = SDIST[sdist] if isinstance(sdist, str) else int(sdist)
+    ctx.check(lib().rsvd_omega(ctx.h, n, l, sd, int(seed), int(stream), 1 if dtype == torch.float32 else 0,
+                               _ptr(out), l))
+    return out
+
+
+def version():
+    return lib().rsvd_version().decode()

@@ -1,0 +1,847 @@
+// api.cu -- C ABI (include/rsvd_b200.h) and the host orchestrator of the
+// randomized SVD hot path.  Host code only; every numerical step runs in the
+// kernels of gemm_pass.cu / omega.cu / panel.cu / ialm.cu on ctx->stream.
+//
+// Pass schedule of one rsvd (Alg. 4 + Alg. 2 + Alg. 5):
+//   K1 Omega -> X                                   (Alg. 4 step 2)
+//   K2 Y = A X                                      (step 3; pass 1)
+//   q x [ orth(Y) -> Q ; K3 Z = A^T Q (+allreduce) ; orth(Z) ; K2 Y = A Z ]   (Alg. 2)
+//   orth(Y) -> Q ; K3 B^T = A^T Q (+allreduce)      (steps 9, 10; pass 2q+2)
+//   orth(B^T) -> Q_B, R_B ; Jacobi(R_B^T) -> Sigma, U~ (= W), J
+//   V = Q_B J ; signs from V (reading R9) ; U = Q (U~ diag(sgn))   (Alg. 5 steps 2-3)
+// orth = CholeskyQR2 (Gram by K3, l x l Cholesky, Y R^-1 by K2) with a
+// breakdown flag, or Householder (one CTA) when the panel fits in shared
+// memory, or TSQR (Householder leaves + combine) in robust mode.  A CholQR2
+// breakdown anywhere re-runs the whole call in robust mode (one status read
+// per call, no per-panel host synchronisation).
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/rsvd_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace rsvd;
+
+namespace {
+
+constexpr int kFlagCholBreak = 1, kFlagJacobiCap = 2, kFlagNonFinite = 4;
+constexpr int kMaxL = 120;       // Jacobi + leaf QR shared-memory envelope
+
+struct ProfRec { int kind; double bytes; cudaEvent_t a, b; };
+
+}  // namespace
+
+struct rsvd_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  std::string err;
+  // workspace (grown on demand; kept between calls)
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  char* ws2 = nullptr;            // robust-mode TSQR stacks / rrpca buffers
+  size_t ws2_bytes = 0;
+  int* flags_dev = nullptr;
+  int* flags_host = nullptr;      // pinned
+  int* sweeps_dev = nullptr;
+  double* hbuf = nullptr;         // pinned host scratch (small D2H/H2D transfers)
+  char* ws3 = nullptr;            // rrpca buffers
+  size_t ws3_bytes = 0;
+  // comm
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  // profiling
+  bool prof = false;
+  std::vector<ProfRec> pending;
+  std::vector<cudaEvent_t> pool;
+  double prof_ms[5] = {0, 0, 0, 0, 0};
+  double prof_bytes[5] = {0, 0, 0, 0, 0};
+  int64_t prof_count[5] = {0, 0, 0, 0, 0};
+  int64_t launches = 0;
+};
+
+namespace {
+
+rsvd_status fail(rsvd_ctx* c, rsvd_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+#define CK(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, RSVD_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+#define CKS(expr)                         \
+  do {                                    \
+    rsvd_status s_ = (expr);              \
+    if (s_ != RSVD_OK) return s_;         \
+  } while (0)
+
+cudaEvent_t take_event(rsvd_ctx* c) {
+  if (!c->pool.empty()) {
+    cudaEvent_t e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct Prof {
+  rsvd_ctx* c; int kind; double bytes; cudaEvent_t a = nullptr;
+  Prof(rsvd_ctx* c_, int k, double b) : c(c_), kind(k), bytes(b) {
+    if (c->prof) { a = take_event(c); cudaEventRecord(a, c->stream); }
+  }
+  ~Prof() {
+    if (c->prof) {
+      cudaEvent_t b2 = take_event(c);
+      cudaEventRecord(b2, c->stream);
+      c->pending.push_back({kind, bytes, a, b2});
+    }
+  }
+};
+
+void prof_collect(rsvd_ctx* c) {
+  for (auto& r : c->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      c->prof_ms[r.kind] += ms;
+      c->prof_bytes[r.kind] += r.bytes;
+      c->prof_count[r.kind] += 1;
+    }
+    c->pool.push_back(r.a);
+    c->pool.push_back(r.b);
+  }
+  c->pending.clear();
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ----------------------------------------------------------------- workspace plan
+struct Plan {
+  int64_t M, n;      // local rows, columns (after the m < n transpose swap: M x n "A")
+  int l, Np;         // sketch width, padded width (multiple of 8)
+  bool f32;
+  bool trans_input;  // single-GPU m < n: work on A^T without copying
+  bool scaled = false;  // implicit column scaling active (rpca scale = TRUE)
+  const void* A; int64_t lda;
+  int64_t m_global;
+  // workspace offsets
+  size_t oX, oY, oT, oZ, oPart, oSmall, oColc, oColr, oColp, total;
+  size_t part_bytes;
+  // small-buffer offsets (doubles from oSmall)
+  double *X, *Y, *T, *Z, *part, *G, *Rinv, *R1, *R2, *RB, *W, *J, *sigma, *sgn, *colc, *colr, *cols, *colp, *Rsm;
+};
+
+bool small_panel(int64_t rows, int l) { return rows <= leaf_rows_cap(l); }
+
+size_t plan_bytes(rsvd_ctx* ctx, Plan& p) {
+  const int Np = p.Np;
+  size_t part = 0;
+  auto upd = [&](int64_t M, int64_t K, int N) {
+    const int s = gemm_choose_splits(M, K, ctx->num_sms);
+    part = std::max(part, gemm_partial_bytes(M, N, s));
+  };
+  upd(p.M, p.n, Np);       // Y = A X
+  upd(p.n, p.M, Np);       // Z = A^T Q
+  upd(Np, p.M, Np);        // Gram of Y
+  upd(Np, p.n, Np);        // Gram of Z
+  upd(p.M, Np, Np);        // Y R^-1
+  upd(p.n, Np, Np);        // Z R^-1
+  p.part_bytes = part;
+  const int64_t big = std::max(p.M, p.n);
+  size_t o = 0;
+  p.oX = o; o = align256(o + (size_t)p.n * Np * 8);
+  p.oY = o; o = align256(o + (size_t)p.M * Np * 8);
+  p.oT = o; o = align256(o + (size_t)big * Np * 8);
+  p.oZ = o; o = align256(o + (size_t)p.n * Np * 8);
+  p.oPart = o; o = align256(o + part);
+  p.oSmall = o; o = align256(o + (size_t)(9 * Np * Np + 4 * Np) * 8);
+  p.oColc = o; o = align256(o + (size_t)p.n * 8);
+  p.oColr = o; o = align256(o + (size_t)p.n * 16);
+  p.oColp = o; o = align256(o + colsum_partial_bytes(p.M, p.n) + 256);
+  p.total = o;
+  return o;
+}
+
+rsvd_status ensure_ws(rsvd_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->ws_bytes) return RSVD_OK;
+  if (ctx->ws) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->ws); ctx->ws = nullptr; ctx->ws_bytes = 0; }
+  if (cudaMalloc(&ctx->ws, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, RSVD_ENOMEM, "workspace allocation of %zu bytes failed", bytes);
+  }
+  ctx->ws_bytes = bytes;
+  return RSVD_OK;
+}
+
+rsvd_status ensure_ws2(rsvd_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->ws2_bytes) return RSVD_OK;
+  if (ctx->ws2) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->ws2); ctx->ws2 = nullptr; ctx->ws2_bytes = 0; }
+  if (cudaMalloc(&ctx->ws2, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, RSVD_ENOMEM, "workspace allocation of %zu bytes failed", bytes);
+  }
+  ctx->ws2_bytes = bytes;
+  return RSVD_OK;
+}
+
+void bind(rsvd_ctx* ctx, Plan& p) {
+  char* b = ctx->ws;
+  const int Np = p.Np;
+  p.X = (double*)(b + p.oX); p.Y = (double*)(b + p.oY); p.T = (double*)(b + p.oT);
+  p.Z = (double*)(b + p.oZ); p.part = (double*)(b + p.oPart);
+  double* s = (double*)(b + p.oSmall);
+  p.G = s; s += Np * Np; p.Rinv = s; s += Np * Np; p.R1 = s; s += Np * Np; p.R2 = s; s += Np * Np;
+  p.RB = s; s += Np * Np; p.W = s; s += Np * Np; p.J = s; s += Np * Np; p.Rsm = s; s += 2 * Np * Np;
+  p.sigma = s; s += Np; p.sgn = s; s += Np;
+  p.colc = (double*)(b + p.oColc); p.colr = (double*)(b + p.oColr); p.cols = p.colr + p.n; p.colp = (double*)(b + p.oColp);
+}
+
+// ----------------------------------------------------------------- collectives
+rsvd_status allreduce_sum(rsvd_ctx* ctx, double* buf, size_t count) {
+  if (ctx->nranks <= 1 || count == 0) return RSVD_OK;
+  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream);
+  if (r != ncclSuccess) return fail(ctx, RSVD_ENCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
+  return RSVD_OK;
+}
+
+rsvd_status allgather(rsvd_ctx* ctx, const double* send, double* recv, size_t count) {
+  ncclResult_t r = ncclAllGather(send, recv, count, ncclDouble, ctx->comm, ctx->stream);
+  if (r != ncclSuccess) return fail(ctx, RSVD_ENCCL, "ncclAllGather: %s", ncclGetErrorString(r));
+  return RSVD_OK;
+}
+
+// ----------------------------------------------------------------- passes over A
+// Y (M x Np) = f(A) X  (K2).   With trans_input the stored matrix is A^T (n x M
+// row-major), so this is the TN form of the stored matrix.
+rsvd_status pass_ax(rsvd_ctx* ctx, Plan& p, const double* X, double* Y, bool centred) {
+  GemmCall g{};
+  g.A = p.A; g.lda = p.lda; g.a_f32 = p.f32; g.trans = p.trans_input;
+  g.B = X; g.ldb = p.Np; g.C = Y; g.ldc = p.Np; g.P = p.part;
+  g.center = centred ? p.colc : nullptr;
+  g.rscale = p.scaled ? p.colr : nullptr;
+  g.M = p.M; g.K = p.n; g.N = p.Np; g.Nout = p.Np;
+  g.splits = gemm_choose_splits(g.M, g.K, ctx->num_sms);
+  const double bytes = (double)p.M * p.n * (p.f32 ? 4 : 8);
+  Prof pr(ctx, 0, bytes);
+  CK(gemm_pass(g, ctx->stream, nullptr));
+  return RSVD_OK;
+}
+
+// Z (n x Np) = f(A)^T Q (K3), then allreduce over ranks.
+rsvd_status pass_atx(rsvd_ctx* ctx, Plan& p, const double* Q, double* Z, bool centred) {
+  GemmCall g{};
+  g.A = p.A; g.lda = p.lda; g.a_f32 = p.f32; g.trans = !p.trans_input;
+  g.B = Q; g.ldb = p.Np; g.C = Z; g.ldc = p.Np; g.P = p.part;
+  g.center = centred ? p.colc : nullptr;
+  g.rscale = p.scaled ? p.colr : nullptr;
+  g.M = p.n; g.K = p.M; g.N = p.Np; g.Nout = p.Np;
+  g.splits = gemm_choose_splits(g.M, g.K, ctx->num_sms);
+  const double bytes = (double)p.M * p.n * (p.f32 ? 4 : 8);
+  {
+    Prof pr(ctx, 1, bytes);
+    CK(gemm_pass(g, ctx->stream, nullptr));
+  }
+  return allreduce_sum(ctx, Z, (size_t)p.n * p.Np);
+}
+
+// C (rows x Nout) = S (rows x Np) * Bsm (Np x Np) (small-K product, K2 kernel)
+rsvd_status small_k(rsvd_ctx* ctx, Plan& p, const double* S, int64_t rows, const double* Bsm, double* C,
+                    int64_t ldc, int Nout) {
+  GemmCall g{};
+  g.A = S; g.lda = p.Np; g.a_f32 = false; g.trans = false;
+  g.B = Bsm; g.ldb = p.Np; g.C = C; g.ldc = ldc; g.P = p.part;
+  g.M = rows; g.K = p.Np; g.N = p.Np; g.Nout = Nout;
+  g.splits = gemm_choose_splits(g.M, g.K, ctx->num_sms);
+  CK(gemm_pass(g, ctx->stream, nullptr));
+  return RSVD_OK;
+}
+
+// G (Np x Np) = S^T S (K3 kernel), allreduce when the rows are distributed.
+rsvd_status gram(rsvd_ctx* ctx, Plan& p, const double* S, int64_t rows, bool dist) {
+  GemmCall g{};
+  g.A = S; g.lda = p.Np; g.a_f32 = false; g.trans = true;
+  g.B = S; g.ldb = p.Np; g.C = p.G; g.ldc = p.Np; g.P = p.part;
+  g.M = p.Np; g.K = rows; g.N = p.Np; g.Nout = p.Np;
+  g.splits = gemm_choose_splits(g.M, g.K, ctx->num_sms);
+  CK(gemm_pass(g, ctx->stream, nullptr));
+  if (dist) return allreduce_sum(ctx, p.G, (size_t)p.Np * p.Np);
+  return RSVD_OK;
+}
+
+// TSQR on `rows` x l panel S (ld Np), single device; R (l x l, ld l) to Rout.
+rsvd_status tsqr_local(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, double* Rout) {
+  const int l = p.l;
+  const int cap = leaf_rows_cap(l);
+  struct Lev { double* buf; int64_t ld, M, P; };
+  std::vector<Lev> levs;
+  // stack sizes
+  size_t need = 0;
+  {
+    int64_t Mc = rows;
+    while (Mc > cap) {
+      int64_t P = ceil_div(Mc, cap);
+      if (Mc / P < l) P = Mc / l;
+      need += (size_t)P * l * l * 8 + 256;
+      Mc = P * l;
+    }
+  }
+  CKS(ensure_ws2(ctx, need + 256));
+  char* wp = ctx->ws2;
+  double* cur = S;
+  int64_t ld = p.Np, Mc = rows;
+  while (Mc > cap) {
+    int64_t P = ceil_div(Mc, cap);
+    if (Mc / P < l) P = Mc / l;
+    double* stack = (double*)wp;
+    wp += align256((size_t)P * l * l * 8);
+    CK(launch_hqr_leaves(cur, ld, Mc, l, P, stack, ctx->stream));
+    levs.push_back({cur, ld, Mc, P});
+    cur = stack; ld = l; Mc = P * l;
+  }
+  CK(launch_hqr_leaves(cur, ld, Mc, l, 1, Rout, ctx->stream));
+  for (int i = (int)levs.size() - 1; i >= 0; --i) {
+    const double* Sq = (i + 1 < (int)levs.size()) ? levs[i + 1].buf : cur;
+    CK(launch_tsqr_combine(levs[i].buf, levs[i].ld, levs[i].M, l, levs[i].P, Sq, l, ctx->stream));
+  }
+  return RSVD_OK;
+}
+
+// Orthonormalise the first l columns of S (rows x Np, ld Np) in place.
+// dist: rows are distributed over ranks.  R (l x l, ld Np) to Rout if non-null.
+rsvd_status orth(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool dist, bool robust, double* Rout) {
+  const int l = p.l, Np = p.Np;
+  Prof pr(ctx, 2, (double)rows * Np * 8 * 4);
+  if (!dist && small_panel(rows, l)) {
+    CK(launch_hqr_leaves(S, Np, rows, l, 1, p.Rsm, ctx->stream));
+    if (Rout) { CK(launch_copy_out(p.Rsm, l, l, l, Rout, Np, false, nullptr, ctx->stream));  }
+    return RSVD_OK;
+  }
+  if (!robust) {
+    // CholeskyQR2
+    CKS(gram(ctx, p, S, rows, dist));
+    CK(launch_chol_inv(p.G, Np, l, Np, p.R1, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream));
+    CKS(small_k(ctx, p, S, rows, p.Rinv, p.T, Np, Np));
+    CKS(gram(ctx, p, p.T, rows, dist));
+    CK(launch_chol_inv(p.G, Np, l, Np, p.R2, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream));
+    CKS(small_k(ctx, p, p.T, rows, p.Rinv, S, Np, Np));
+    if (Rout) { CK(launch_small_matmul(p.R2, p.R1, Rout, l, Np, ctx->stream));  }
+    return RSVD_OK;
+  }
+  // robust: TSQR (local), then across ranks
+  if (rows < l) return fail(ctx, RSVD_EUNSUPPORTED, "robust panel QR needs >= l rows per rank");
+  CKS(tsqr_local(ctx, p, S, rows, p.Rsm));
+  if (dist) {
+    // allgather the local R factors, QR of the stack (redundant per rank), combine
+    const size_t rr = (size_t)l * l;
+    const int64_t srows = (int64_t)ctx->nranks * l;
+    // reuse T as the gathered stack (big enough: max(M, n) * Np >= nranks * l * l? check)
+    if ((size_t)srows * l > (size_t)std::max(p.M, p.n) * Np)
+      return fail(ctx, RSVD_EUNSUPPORTED, "too many ranks for the robust panel QR workspace");
+    double* stack = p.T;
+    CKS(allgather(ctx, p.Rsm, stack, rr));
+    double* Rg = p.Rsm + rr;
+    if (srows <= leaf_rows_cap(l)) {
+      CK(launch_hqr_leaves(stack, l, srows, l, 1, Rg, ctx->stream));
+    } else {
+      Plan q = p; q.Np = l;
+      CKS(tsqr_local(ctx, q, stack, srows, Rg));
+    }
+    // local Q <- local Q * S_rank : treat the local panel as nleaves = 1 block
+    // (combine kernel reads S rows [leaf*l, ...) so offset the pointer)
+    const int64_t nleaves = std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 256), 1));
+    CK(launch_tsqr_combine(S, Np, rows, l, nleaves, stack + (size_t)ctx->rank * l * l, l, ctx->stream));
+    if (Rout) { CK(launch_copy_out(Rg, l, l, l, Rout, Np, false, nullptr, ctx->stream));  }
+  } else if (Rout) {
+    CK(launch_copy_out(p.Rsm, l, l, l, Rout, Np, false, nullptr, ctx->stream));
+  }
+  return RSVD_OK;
+}
+
+rsvd_status validate(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, int64_t* m_out,
+                     int64_t* n_out) {
+  if (!ctx) return RSVD_EINVAL;
+  if (!A || !prm) return fail(ctx, RSVD_EINVAL, "null argument");
+  if (A->dtype != RSVD_F64 && A->dtype != RSVD_F32) return fail(ctx, RSVD_EINVAL, "dtype must be F64 or F32");
+  if (!A->A) return fail(ctx, RSVD_EINVAL, "A is null");
+  if (A->m_local < 1 || A->n < 1 || A->lda < A->n) return fail(ctx, RSVD_EINVAL, "bad shape or lda < n");
+  const int64_t mg = ctx->nranks > 1 ? A->m_global : A->m_local;
+  if (ctx->nranks > 1) {
+    if (A->m_global < A->m_local || A->row_offset < 0 || A->row_offset + A->m_local > A->m_global)
+      return fail(ctx, RSVD_EINVAL, "bad distributed row range");
+    if (mg < A->n) return fail(ctx, RSVD_EUNSUPPORTED, "distributed mode needs m_global >= n");
+  }
+  const int64_t mn = std::min(mg, A->n);
+  if (prm->k < 1 || prm->k > mn) return fail(ctx, RSVD_EINVAL, "k must satisfy 1 <= k <= min(m, n)");
+  if (prm->p < 0 || prm->q < 0) return fail(ctx, RSVD_EINVAL, "p and q must be >= 0");
+  if (prm->sdist < 0 || prm->sdist > 2) return fail(ctx, RSVD_EINVAL, "sdist must be normal, unif or rademacher");
+  if (prm->nu < 0 || prm->nv < 0) return fail(ctx, RSVD_EINVAL, "nu, nv must be >= 0");
+  *m_out = mg;
+  *n_out = A->n;
+  return RSVD_OK;
+}
+
+// Core of rsvd: fills p.Y (= Q, M x Np), p.X (= V, n x Np, sign-fixed),
+// p.W (= U~ diag(sgn), Np x Np), p.sigma.  Returns flags via ctx->flags_dev.
+rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool robust, bool want_svd) {
+  const int l = p.l, Np = p.Np;
+  const bool dist = ctx->nranks > 1;
+  const bool centred = prm->center != 0 || prm->scale != 0;
+  CK(cudaMemsetAsync(ctx->flags_dev, 0, sizeof(int) * 4, ctx->stream));
+  p.scaled = prm->scale != 0;
+  if (centred || p.scaled) {
+    // column means c (and 1/s.d. for scaling): Alg. 6, "center and scale"
+    if (centred) {
+      CK(launch_colsum(p.A, p.lda, p.f32, p.M, p.n, 0, nullptr, p.colp, p.colc, ctx->stream, nullptr));
+      CKS(allreduce_sum(ctx, p.colc, (size_t)p.n));
+      CK(launch_colstat_finish(p.colc, p.n, (double)p.m_global, 0, nullptr, ctx->stream));
+    } else {
+      CK(launch_fill(p.colc, p.n, 0.0, ctx->stream));
+    }
+    if (p.scaled) {
+      CK(launch_colsum(p.A, p.lda, p.f32, p.M, p.n, 1, p.colc, p.colp, p.colr, ctx->stream, nullptr));
+      CKS(allreduce_sum(ctx, p.colr, (size_t)p.n));
+      CK(launch_colstat_finish(p.colr, p.n, (double)p.m_global, 1, p.cols, ctx->stream));
+    }
+  }
+  {
+    Prof pr(ctx, 4, 0);
+    CK(launch_omega(p.n, l, Np, Np, prm->sdist, prm->seed, prm->stream, p.f32, false, p.X, ctx->stream));
+  }
+  CKS(pass_ax(ctx, p, p.X, p.Y, centred));                          // Y = A Omega
+  for (int j = 0; j < prm->q; ++j) {                                 // Alg. 2
+    CKS(orth(ctx, p, p.Y, p.M, dist, robust, nullptr));             //   [Q,~] = qr(Y)
+    CKS(pass_atx(ctx, p, p.Y, p.Z, centred));                        //   A^T Q
+    CKS(orth(ctx, p, p.Z, p.n, false, robust, nullptr));            //   [Q,~] = qr(A^T Q)
+    CKS(pass_ax(ctx, p, p.Z, p.Y, centred));                         //   Y = A Q
+  }
+  CKS(orth(ctx, p, p.Y, p.M, dist, robust, nullptr));               // Alg. 4 step 9
+  CKS(pass_atx(ctx, p, p.Y, p.Z, centred));                          // step 10: B^T = A^T Q
+  if (!want_svd) return RSVD_OK;
+  // economic SVD of B via B^T = Q_B R_B and Jacobi on R_B^T (Alg. 5 step 2)
+  CKS(orth(ctx, p, p.Z, p.n, false, robust, p.RB));
+  {
+    Prof pr(ctx, 3, 0);
+    CK(launch_jacobi(p.RB, Np, l, p.sigma, p.W, p.J, Np, ctx->flags_dev, ctx->sweeps_dev, ctx->stream));
+  }
+  CK(launch_zero_cols(p.J, Np, l, l, Np, ctx->stream));       // keep padding exact zeros
+  CK(launch_fill(p.J + (size_t)l * Np, (int64_t)(Np - l) * Np, 0.0, ctx->stream));
+  CK(launch_zero_cols(p.W, Np, l, l, Np, ctx->stream));
+  CK(launch_fill(p.W + (size_t)l * Np, (int64_t)(Np - l) * Np, 0.0, ctx->stream));
+  // V = Q_B J  (n x Np) into X
+  CKS(small_k(ctx, p, p.Z, p.n, p.J, p.X, Np, Np));
+  if (!p.trans_input) {
+    // reading R9: signs from V; U = Q (U~ diag(sgn)) is formed by the caller-facing step
+    CK(launch_sign_from_v(p.X, Np, p.n, l, p.sgn, ctx->stream));
+    CK(launch_scale_cols(p.X, Np, p.n, l, p.sgn, ctx->stream));
+    CK(launch_scale_cols(p.W, Np, l, l, p.sgn, ctx->stream));
+  } else {
+    // worked on A^T: the V of A is U' = Q U~ (M x Np, into T); signs from it
+    CKS(small_k(ctx, p, p.Y, p.M, p.W, p.T, Np, Np));
+    CK(launch_sign_from_v(p.T, Np, p.M, l, p.sgn, ctx->stream));
+    CK(launch_scale_cols(p.T, Np, p.M, l, p.sgn, ctx->stream));
+    CK(launch_scale_cols(p.X, Np, p.n, l, p.sgn, ctx->stream));
+  }
+  CK(launch_check_finite(p.sigma, l, ctx->flags_dev, ctx->stream));
+  return RSVD_OK;
+}
+
+rsvd_status finish_flags(rsvd_ctx* ctx, int* flags) {
+  CK(cudaMemcpyAsync(ctx->flags_host, ctx->flags_dev, sizeof(int) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->prof) prof_collect(ctx);
+  *flags = ctx->flags_host[0];
+  return RSVD_OK;
+}
+
+// Build the plan for A (handles the single-GPU m < n case by working on A^T).
+rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bool center_or_scale, Plan& p) {
+  const int64_t mg = ctx->nranks > 1 ? A->m_global : A->m_local;
+  p.f32 = A->dtype == RSVD_F32;
+  p.A = A->A; p.lda = A->lda;
+  p.trans_input = (ctx->nranks <= 1) && (A->m_local < A->n);
+  if (p.trans_input && center_or_scale)
+    return fail(ctx, RSVD_EUNSUPPORTED, "centring/scaling needs m >= n");
+  if (p.trans_input) { p.M = A->n; p.n = A->m_local; p.m_global = A->n; }
+  else { p.M = A->m_local; p.n = A->n; p.m_global = mg; }
+  const int64_t mn = std::min(mg, A->n);
+  p.l = (int)std::min<int64_t>((int64_t)k + p_over, mn);
+  p.Np = (int)round_up(p.l, 8);
+  if (p.l > kMaxL) return fail(ctx, RSVD_EUNSUPPORTED, "l = k + p = %d exceeds this build's limit %d", p.l, kMaxL);
+  if (ctx->nranks > 1 && p.M < p.l)
+    return fail(ctx, RSVD_EUNSUPPORTED, "each rank needs at least l = %d rows", p.l);
+  const size_t bytes = plan_bytes(ctx, p);
+  CKS(ensure_ws(ctx, bytes));
+  bind(ctx, p);
+  return RSVD_OK;
+}
+
+rsvd_status run_with_retry(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool want_svd) {
+  int flags = 0;
+  CKS(rsvd_core(ctx, p, prm, false, want_svd));
+  CKS(finish_flags(ctx, &flags));
+  if (flags & kFlagCholBreak) {
+    CKS(rsvd_core(ctx, p, prm, true, want_svd));
+    CKS(finish_flags(ctx, &flags));
+  }
+  if (flags & kFlagNonFinite) return fail(ctx, RSVD_ENUMERIC, "non-finite intermediate (input contains Inf/NaN?)");
+  if (flags & kFlagJacobiCap) return fail(ctx, RSVD_ENUMERIC, "one-sided Jacobi hit the 30-sweep cap");
+  return RSVD_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* rsvd_version(void) { return "rsvd_b200 0.1 (sm_100a)"; }
+
+rsvd_status rsvd_create(rsvd_ctx** out, int device, void* stream) {
+  if (!out) return RSVD_EINVAL;
+  *out = nullptr;
+  rsvd_ctx* ctx = new rsvd_ctx();
+  ctx->device = device;
+  ctx->stream = (cudaStream_t)stream;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->flags_dev, 16 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->flags_host, 16 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->hbuf, 1024 * sizeof(double));
+  if (e == cudaSuccess) ctx->sweeps_dev = ctx->flags_dev + 8;
+  if (e != cudaSuccess) {
+    delete ctx;
+    return RSVD_ECUDA;
+  }
+  *out = ctx;
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_destroy(rsvd_ctx* ctx) {
+  if (!ctx) return RSVD_EINVAL;
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  for (auto& r : ctx->pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : ctx->pool) cudaEventDestroy(e);
+  cudaFree(ctx->ws);
+  cudaFree(ctx->ws2);
+  cudaFree(ctx->flags_dev);
+  cudaFreeHost(ctx->flags_host);
+  cudaFreeHost(ctx->hbuf);
+  cudaFree(ctx->ws3);
+  delete ctx;
+  return RSVD_OK;
+}
+
+const char* rsvd_last_error(const rsvd_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+rsvd_status rsvd_nccl_unique_id(void* out128) {
+  if (!out128) return RSVD_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return RSVD_ENCCL;
+  memcpy(out128, &id, sizeof id);
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_comm_init(rsvd_ctx* ctx, const void* id128, int nranks, int rank) {
+  if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, RSVD_EINVAL, "bad comm args");
+  if (nranks == 1) { ctx->nranks = 1; ctx->rank = 0; return RSVD_OK; }
+  if (!id128) return fail(ctx, RSVD_EINVAL, "null unique id");
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof id);
+  cudaSetDevice(ctx->device);
+  ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
+  if (r != ncclSuccess) return fail(ctx, RSVD_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  return RSVD_OK;
+}
+
+void rsvd_params_default(rsvd_params* prm, int32_t k) {
+  if (!prm) return;
+  memset(prm, 0, sizeof *prm);
+  prm->k = k; prm->nu = k; prm->nv = k; prm->p = 10; prm->q = 2;
+  prm->sdist = RSVD_NORMAL;
+}
+
+void rsvd_rrpca_params_default(rsvd_rrpca_params* prm) {
+  if (!prm) return;
+  memset(prm, 0, sizeof *prm);
+  prm->lambda = 0.0; prm->tol = 1e-5; prm->maxiter = 50; prm->k = 20; prm->p = 10; prm->q = 2;
+  prm->sdist = RSVD_NORMAL;
+}
+
+rsvd_status rsvd_run(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm_in, void* u, int64_t ldu,
+                     void* d, void* v, int64_t ldv) {
+  int64_t mg, n;
+  CKS(validate(ctx, A, prm_in, &mg, &n));
+  rsvd_params prm = *prm_in;
+  ctx->err.clear();
+  if (prm.nu > prm.k || prm.nv > prm.k) {
+    prm.nu = std::min(prm.nu, prm.k);
+    prm.nv = std::min(prm.nv, prm.k);
+    ctx->err = "warning: nu/nv > k clamped to k";
+  }
+  if (!d) return fail(ctx, RSVD_EINVAL, "d is null");
+  if (prm.nu > 0 && (!u || ldu < prm.nu)) return fail(ctx, RSVD_EINVAL, "u null or ldu < nu");
+  if (prm.nv > 0 && (!v || ldv < prm.nv)) return fail(ctx, RSVD_EINVAL, "v null or ldv < nv");
+  CK(cudaSetDevice(ctx->device));
+  Plan p{};
+  CKS(make_plan(ctx, A, prm.k, prm.p, prm.center || prm.scale, p));
+  CKS(run_with_retry(ctx, p, &prm, true));
+  const bool f32 = p.f32;
+  const int Np = p.Np;
+  // outputs: U = Q (U~ diag sgn), V (sign-fixed), d = sigma(1:k)
+  int nu = prm.nu, nv = prm.nv;
+  double* Uo = p.T;      // M x Np scratch
+  if (!p.trans_input) {
+    if (nu > 0) {
+      if (!f32) { CKS(small_k(ctx, p, p.Y, p.M, p.W, (double*)u, ldu, nu)); }
+      else {
+        CKS(small_k(ctx, p, p.Y, p.M, p.W, Uo, Np, nu));
+        CK(launch_copy_out(Uo, Np, p.M, nu, u, ldu, true, nullptr, ctx->stream));
+      }
+    }
+    if (nv > 0) CK(launch_copy_out(p.X, Np, p.n, nv, v, ldv, f32, nullptr, ctx->stream));
+  } else {
+    // worked on A^T = U' S V'^T  =>  A = V' S U'^T: u <- V' (n_eff rows), v <- U'
+    (void)Uo;
+    if (nu > 0) CK(launch_copy_out(p.X, Np, p.n, nu, u, ldu, f32, nullptr, ctx->stream));
+    if (nv > 0) CK(launch_copy_out(p.T, Np, p.M, nv, v, ldv, f32, nullptr, ctx->stream));
+  }
+  CK(launch_copy_out(p.sigma, 1, prm.k, 1, d, 1, f32, nullptr, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->prof) prof_collect(ctx);
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_rqb(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, void* Q, int64_t ldq, void* Bt,
+                     int64_t ldb) {
+  int64_t mg, n;
+  CKS(validate(ctx, A, prm, &mg, &n));
+  if (prm->center) return fail(ctx, RSVD_EUNSUPPORTED, "rqb with centring: use rsvd_rpca");
+  CK(cudaSetDevice(ctx->device));
+  Plan p{};
+  CKS(make_plan(ctx, A, prm->k, prm->p, prm->center || prm->scale, p));
+  if (p.trans_input) return fail(ctx, RSVD_EUNSUPPORTED, "rqb needs m >= n");
+  if (!Q || !Bt || ldq < p.l || ldb < p.l) return fail(ctx, RSVD_EINVAL, "Q/Bt null or ld < l");
+  CKS(run_with_retry(ctx, p, prm, false));
+  CK(launch_copy_out(p.Y, p.Np, p.M, p.l, Q, ldq, p.f32, nullptr, ctx->stream));
+  CK(launch_copy_out(p.Z, p.Np, p.n, p.l, Bt, ldb, p.f32, nullptr, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_rpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm_in, void* rotation, int64_t ldr,
+                      void* eigvals, void* x, int64_t ldx, void* center, void* scale) {
+  int64_t mg, n;
+  CKS(validate(ctx, A, prm_in, &mg, &n));
+  rsvd_params prm = *prm_in;
+  if (!rotation || ldr < prm.k || !eigvals) return fail(ctx, RSVD_EINVAL, "rotation/eigvals null or ldr < k");
+  if (x && ldx < prm.k) return fail(ctx, RSVD_EINVAL, "ldx < k");
+  CK(cudaSetDevice(ctx->device));
+  Plan p{};
+  CKS(make_plan(ctx, A, prm.k, prm.p, prm.center || prm.scale, p));
+  if (p.trans_input) return fail(ctx, RSVD_EUNSUPPORTED, "rpca needs m >= n");
+  CKS(run_with_retry(ctx, p, &prm, true));
+  const int k = prm.k, Np = p.Np;
+  CK(launch_copy_out(p.X, Np, p.n, k, rotation, ldr, p.f32, nullptr, ctx->stream));
+  CK(launch_pca_eig(p.sigma, k, (double)p.m_global, eigvals, p.f32, ctx->stream));
+  if (x) {
+    CKS(small_k(ctx, p, p.Y, p.M, p.W, p.T, Np, k));
+    CK(launch_copy_out(p.T, Np, p.M, k, x, ldx, p.f32, p.sigma, ctx->stream));   // scores U diag(d)
+  }
+  if (center && prm.center) CK(launch_copy_out(p.colc, 1, p.n, 1, center, 1, p.f32, nullptr, ctx->stream));
+  if (scale && prm.scale) CK(launch_copy_out(p.cols, 1, p.n, 1, scale, 1, p.f32, nullptr, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_omega(rsvd_ctx* ctx, int64_t n, int64_t l, int32_t sdist, uint64_t seed, uint64_t stream,
+                       int32_t dtype, void* out, int64_t ldo) {
+  if (!ctx) return RSVD_EINVAL;
+  if (n < 1 || l < 1 || ldo < l || !out || sdist < 0 || sdist > 2) return fail(ctx, RSVD_EINVAL, "bad omega args");
+  CK(cudaSetDevice(ctx->device));
+  const bool f32 = dtype == RSVD_F32;
+  CK(launch_omega(n, l, ldo, l, sdist, seed, stream, f32, f32, out, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_set_profiling(rsvd_ctx* ctx, int enable) {
+  if (!ctx) return RSVD_EINVAL;
+  ctx->prof = enable != 0;
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_profile(rsvd_ctx* ctx, int kind, double* total_ms, int64_t* count, double* bytes) {
+  if (!ctx || kind < 0 || kind > 4) return RSVD_EINVAL;
+  if (!ctx->pending.empty()) {
+    cudaStreamSynchronize(ctx->stream);
+    prof_collect(ctx);
+  }
+  if (total_ms) *total_ms = ctx->prof_ms[kind];
+  if (count) *count = ctx->prof_count[kind];
+  if (bytes) *bytes = ctx->prof_bytes[kind];
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_profile_reset(rsvd_ctx* ctx) {
+  if (!ctx) return RSVD_EINVAL;
+  if (!ctx->pending.empty()) { cudaStreamSynchronize(ctx->stream); prof_collect(ctx); }
+  for (int i = 0; i < 5; ++i) { ctx->prof_ms[i] = 0; ctx->prof_bytes[i] = 0; ctx->prof_count[i] = 0; }
+  rsvd::g_kernel_launches = 0;
+  return RSVD_OK;
+}
+
+int64_t rsvd_launch_count(const rsvd_ctx* ctx) { return ctx ? rsvd::g_kernel_launches : 0; }
+
+}  // extern "C"
+
+// =================================================================== rrpca (Alg. 7)
+namespace {
+
+rsvd_status rsvd_device(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, double* U, int64_t ldu,
+                        double* d, double* V, int64_t ldv) {
+  int64_t mg, n;
+  CKS(validate(ctx, A, prm, &mg, &n));
+  Plan p{};
+  CKS(make_plan(ctx, A, prm->k, prm->p, false, p));
+  if (p.trans_input) return fail(ctx, RSVD_EUNSUPPORTED, "rrpca needs m >= n");
+  CKS(run_with_retry(ctx, p, prm, true));
+  if (U) CKS(small_k(ctx, p, p.Y, p.M, p.W, U, ldu, prm->k));
+  if (V) CK(launch_copy_out(p.X, p.Np, p.n, prm->k, V, ldv, false, nullptr, ctx->stream));
+  CK(launch_copy_out(p.sigma, 1, prm->k, 1, d, 1, false, nullptr, ctx->stream));
+  return RSVD_OK;
+}
+
+rsvd_status allreduce_max(rsvd_ctx* ctx, double* buf, size_t count) {
+  if (ctx->nranks <= 1) return RSVD_OK;
+  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclMax, ctx->comm, ctx->stream);
+  if (r != ncclSuccess) return fail(ctx, RSVD_ENCCL, "ncclAllReduce(max): %s", ncclGetErrorString(r));
+  return RSVD_OK;
+}
+
+}  // namespace
+
+extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_rrpca_params* prm, void* Lout,
+                                  void* Sout, int64_t ld, int32_t* iters_out, double* res_out, double* trace) {
+  if (!ctx) return RSVD_EINVAL;
+  if (!A || !prm || !Lout || !Sout) return fail(ctx, RSVD_EINVAL, "null argument");
+  if (A->dtype != RSVD_F64) return fail(ctx, RSVD_EUNSUPPORTED, "rrpca is FP64 only");
+  if (ld < A->n) return fail(ctx, RSVD_EINVAL, "ld < n");
+  if (A->lda != A->n || ld != A->n)
+    return fail(ctx, RSVD_EUNSUPPORTED, "rrpca needs contiguous A, L, S (lda == ld == n)");
+  if (prm->maxiter < 1 || prm->k < 1 || prm->k > 32 || !(prm->tol > 0)) return fail(ctx, RSVD_EINVAL, "bad rrpca params (1 <= k <= 32, maxiter >= 1, tol > 0)");
+  rsvd_params rp;
+  rsvd_params_default(&rp, prm->k);
+  rp.p = prm->p; rp.q = prm->q; rp.sdist = prm->sdist; rp.seed = prm->seed;
+  int64_t mg, n;
+  CKS(validate(ctx, A, &rp, &mg, &n));
+  CK(cudaSetDevice(ctx->device));
+  const int64_t m = A->m_local;
+  const int k = prm->k;
+  const double lam = prm->lambda > 0 ? prm->lambda : 1.0 / sqrt((double)std::max(mg, n));
+  const double* Ad = (const double*)A->A;
+  double* S = (double*)Sout;
+  double* Lm = (double*)Lout;
+  // rrpca buffers: Z, M (m x n, ld n), U (m x k), V (n x k), d, dl, partials
+  const int nb = ialm_blocks();
+  size_t o = 0;
+  const size_t oZ = o; o = align256(o + (size_t)m * n * 8);
+  const size_t oM = o; o = align256(o + (size_t)m * n * 8);
+  const size_t oU = o; o = align256(o + (size_t)m * k * 8);
+  const size_t oV = o; o = align256(o + (size_t)n * k * 8);
+  const size_t od = o; o = align256(o + 64 * 8);
+  const size_t odl = o; o = align256(o + 64 * 8);
+  const size_t oP = o; o = align256(o + (size_t)2 * nb * 8 + 64);
+  if (o > ctx->ws3_bytes) {
+    if (ctx->ws3) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->ws3); ctx->ws3 = nullptr; ctx->ws3_bytes = 0; }
+    if (cudaMalloc(&ctx->ws3, o) != cudaSuccess) { cudaGetLastError(); return fail(ctx, RSVD_ENOMEM, "rrpca workspace"); }
+    ctx->ws3_bytes = o;
+  }
+  double* Z = (double*)(ctx->ws3 + oZ);
+  double* M = (double*)(ctx->ws3 + oM);
+  double* U = (double*)(ctx->ws3 + oU);
+  double* V = (double*)(ctx->ws3 + oV);
+  double* dd = (double*)(ctx->ws3 + od);
+  double* dl = (double*)(ctx->ws3 + odl);
+  double* part = (double*)(ctx->ws3 + oP);
+  double* scal = part + 2 * nb;   // [0] = sum, [1] = max
+  double* h = ctx->hbuf;
+
+  // ||A||_2 = sigma_1 of rsvd(A, 1, p, q) with Omega stream 0 (reading R18)
+  rsvd_params r1 = rp;
+  r1.k = 1; r1.nu = 0; r1.nv = 0; r1.stream = 0;
+  CKS(rsvd_device(ctx, A, &r1, nullptr, 0, dd, nullptr, 0));
+  // ||A||_F^2 and max|A|
+  CK(launch_ialm_init(Ad, A->lda, m, n, part, part + nb, nb, ctx->stream));
+  CK(launch_reduce_blocks(part, nb, 0, scal, ctx->stream));
+  CK(launch_reduce_blocks(part + nb, nb, 1, scal + 1, ctx->stream));
+  CKS(allreduce_sum(ctx, scal, 1));
+  CKS(allreduce_max(ctx, scal + 1, 1));
+  CK(cudaMemcpyAsync(h, dd, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(h + 1, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const double norm2 = h[0], normF = sqrt(h[1]), maxabs = h[2];
+  if (!(norm2 > 0) || !std::isfinite(norm2)) return fail(ctx, RSVD_ENUMERIC, "||A||_2 is zero or non-finite");
+  const double mu0 = 1.25 / norm2;                         // reading R17
+  double mu = mu0;
+  const double dual = std::max(norm2, maxabs / lam);       // reading R19
+  CK(launch_scale_copy(Ad, A->lda, m, n, dual, Z, ctx->stream));   // Z = A / J(A)
+  CK(cudaMemset2DAsync(S, ld * 8, 0, n * 8, m, ctx->stream));       // S = 0
+  CK(launch_ialm_form_m(Ad, S, Z, n, m, n, 1.0 / mu, M, ctx->stream));
+  rsvd_matrix Mdesc = *A;
+  Mdesc.A = M;
+  Mdesc.lda = n;
+  int it = 0;
+  double res = INFINITY;
+  int nl = 0;
+  for (it = 1; it <= prm->maxiter; ++it) {
+    rsvd_params ri = rp;
+    ri.stream = (uint64_t)it;                               // fresh Omega per iteration (R23)
+    CKS(rsvd_device(ctx, &Mdesc, &ri, U, k, dd, V, k));      // step (6)
+    CK(cudaMemcpyAsync(h, dd, k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    nl = 0;
+    for (int i = 0; i < k; ++i) if (h[i] > 1.0 / mu) ++nl;  // step (7), fixed k (R22)
+    for (int i = 0; i < k; ++i) h[64 + i] = (i < nl) ? h[i] - 1.0 / mu : 0.0;   // step (8)
+    CK(cudaMemcpyAsync(dl, h + 64, k * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    const double mu_next = std::min(1.5 * mu, 1e7 * mu0);  // step (12), R20
+    CK(launch_ialm_update(Ad, S, Z, M, n, m, n, U, k, V, k, dl, nl, 1.0 / mu, mu, lam, 1.0 / mu_next, part, nb,
+                          ctx->stream));                   // steps (9)-(11) fused
+    CK(launch_reduce_blocks(part, nb, 0, scal, ctx->stream));
+    CKS(allreduce_sum(ctx, scal, 1));
+    CK(cudaMemcpyAsync(h + 128, scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    res = sqrt(h[128]) / normF;
+    if (trace) { trace[3 * (it - 1)] = res; trace[3 * (it - 1) + 1] = nl; trace[3 * (it - 1) + 2] = mu; }
+    mu = mu_next;
+    if (res < prm->tol) break;
+  }
+  if (it > prm->maxiter) it = prm->maxiter;
+  CK(launch_lowrank_materialise(U, k, V, k, dl, nl, m, n, Lm, ld, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (iters_out) *iters_out = it;
+  if (res_out) *res_out = res;
+  return RSVD_OK;
+}

@@ -1,0 +1,317 @@
+// gemm_pass.cu -- the streaming tall-skinny passes over A.
+//
+//   NN form (K2):  C (M x N) = Aop (M x K) * B (K x N),  Aop(m,k) = f(A[m*lda + k])
+//                  used for the sketch Y = A Omega (Eq. YAQ; Alg. 4
+//                  step 3), the power pass Y = A Q (Alg. 2 step 4),
+//                  and the small-K products Y R^-1, Q U~, Q_B J (Eq. UQU).
+//   TN form (K3):  C (M x N) = Aop^T ...  Aop(m,k) = f(A[k*lda + m])
+//                  used for Z = A^T Q (Alg. 2 step 3), B^T = A^T Q
+//                  (Eq. BQA; Alg. 4 step 10) and Gram Y^T Y.
+//   f(a) = (a - c[col]) * rs[col] with col = the column index of A (implicit
+//   centring/scaling for rpca, Alg. 6), identity when c, rs are null.
+//
+// Design (B200, FP64): tcgen05 has no f64 kind, so the MMA is the warp-level
+// DMMA (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4), 37 TFLOP/s measured on this
+// pool (profiles/peaks_box.json).  A CTA owns BM = 128 rows of C and all N <= 128
+// columns; 8 warps = 4 (M, 32 rows each) x 2 (N halves).  A and B tiles of
+// BK = 16 are staged in shared memory by a 4-stage cp.async (LDGSTS) ring with
+// zero-fill for ragged edges; padding strides keep the fragment loads at the
+// minimum two shared-memory wavefronts.  A is read from HBM exactly once per
+// pass; B (Omega / Q, <= 5 MB) is re-read from L2 by every row block.  The
+// contraction may be split over `splits` CTAs (grid.y); the partials land in a
+// workspace and are summed in a fixed order by gemm_reduce (deterministic, no
+// FP64 atomics: SURVEY H4).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rsvd {
+
+constexpr int BM = 128, BK = 16, STAGES = 4, GEMM_THREADS = 256;
+constexpr int A_NN_LD = BK + 4;      // [BM][BK+4]  (row = m)
+constexpr int A_TN_LD = BM + 8;      // [BK][BM+8]  (row = k)
+constexpr int B_PAD = 8;             // [BK][N+8]
+constexpr int NMAX = 128;
+
+template <typename TA>
+struct GemmSmem {
+  static constexpr int a_stage_elems_nn = BM * A_NN_LD;
+  static constexpr int a_stage_elems_tn = BK * A_TN_LD;
+  static constexpr int a_stage_elems = a_stage_elems_nn > a_stage_elems_tn ? a_stage_elems_nn : a_stage_elems_tn;
+  static constexpr int b_stage_elems = BK * (NMAX + B_PAD);
+  static constexpr size_t bytes =
+      (size_t)STAGES * (a_stage_elems * sizeof(TA) + b_stage_elems * sizeof(double) + 2 * BK * sizeof(double));
+};
+
+struct GemmArgs {
+  const void* A; int64_t lda;
+  const double* B; int64_t ldb;
+  double* C; int64_t ldc;           // final output (splits == 1)
+  double* P;                        // partials [splits][M][N] (splits > 1)
+  const double* c; const double* rs;
+  int64_t M, K; int N, Nout;
+  int splits; int64_t ktiles_per_split;
+  bool a_vec;                       // A rows 16-byte aligned (vector cp.async)
+};
+
+template <typename TA, bool TRANS, int TMAX>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  using S = GemmSmem<TA>;
+  TA* As = reinterpret_cast<TA*>(smem_raw);
+  double* Bs = reinterpret_cast<double*>(smem_raw + (size_t)STAGES * S::a_stage_elems * sizeof(TA));
+  double* Cs = Bs + (size_t)STAGES * S::b_stage_elems;       // per-stage centring: c then rs (BK each)
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int split = blockIdx.y;
+  const int N = g.N;
+  const int ldbs = (N % 16 == 0) ? N + B_PAD : N;   // keeps B fragment loads at 2 wavefronts
+  const int T = N >> 3;                      // n8 tiles
+  const int T0 = (T + 1) >> 1;
+  const int tile_begin = wn == 0 ? 0 : T0;
+  const int ntiles = wn == 0 ? T0 : T - T0;
+  const int64_t KT = ceil_div(g.K, BK);
+  const int64_t kt_begin = (int64_t)split * g.ktiles_per_split;
+  int64_t kt_end = kt_begin + g.ktiles_per_split;
+  if (kt_end > KT) kt_end = KT;
+  const int64_t nkt = kt_end > kt_begin ? kt_end - kt_begin : 0;
+  const TA* A = reinterpret_cast<const TA*>(g.A);
+  const bool centre = g.c != nullptr;
+  const bool scale = g.rs != nullptr;
+  const bool avec = g.a_vec;
+
+  auto load_stage = [&](int stage, int64_t kt) {
+    const int64_t k0 = kt * BK;
+    TA* as = As + stage * S::a_stage_elems;
+    double* bs = Bs + stage * S::b_stage_elems;
+    constexpr int EPC = 16 / sizeof(TA);     // elements per 16-byte chunk
+    if (!avec) {
+      // unaligned rows: element-wise cp.async (same results, slower)
+      for (int e = tid; e < BM * BK; e += GEMM_THREADS) {
+        int r, cc; int64_t gm, gk;
+        if (!TRANS) { r = e / BK; cc = e % BK; gm = m0 + r; gk = k0 + cc; }
+        else { r = e / BM; cc = e % BM; gk = k0 + r; gm = m0 + cc; }
+        const bool ok = gm < g.M && gk < g.K;
+        const TA* src = ok ? (TRANS ? A + gk * g.lda + gm : A + gm * g.lda + gk) : A;
+        TA* dst = TRANS ? as + r * A_TN_LD + cc : as + r * A_NN_LD + cc;
+        if (sizeof(TA) == 8) cp_async8(dst, src, ok ? 8 : 0);
+        else cp_async4(dst, src, ok ? 4 : 0);
+      }
+    } else if (!TRANS) {
+      // BM rows x BK cols of A (row m, contiguous k)
+      constexpr int CPR = BK / EPC;          // chunks per row
+      for (int ch = tid; ch < BM * CPR; ch += GEMM_THREADS) {
+        const int r = ch / CPR, cc = (ch % CPR) * EPC;
+        const int64_t gm = m0 + r, gk = k0 + cc;
+        int valid = 0;
+        if (gm < g.M && gk < g.K) valid = (int)((g.K - gk) < EPC ? (g.K - gk) : EPC);
+        const TA* src = valid ? A + gm * g.lda + gk : A;
+        cp_async16(as + r * A_NN_LD + cc, src, valid * (int)sizeof(TA));
+      }
+    } else {
+      // BK rows (k) x BM cols (m) of A, contiguous along m
+      constexpr int CPR = BM / EPC;
+      for (int ch = tid; ch < BK * CPR; ch += GEMM_THREADS) {
+        const int r = ch / CPR, cc = (ch % CPR) * EPC;
+        const int64_t gk = k0 + r, gm = m0 + cc;
+        int valid = 0;
+        if (gk < g.K && gm < g.M) valid = (int)((g.M - gm) < EPC ? (g.M - gm) : EPC);
+        const TA* src = valid ? A + gk * g.lda + gm : A;
+        cp_async16(as + r * A_TN_LD + cc, src, valid * (int)sizeof(TA));
+      }
+    }
+    // B: BK rows x N cols (N multiple of 8, ldb even => 16-byte chunks of 2 doubles)
+    const int CPRB = N >> 1;
+    for (int ch = tid; ch < BK * CPRB; ch += GEMM_THREADS) {
+      const int r = ch / CPRB, cc = (ch % CPRB) * 2;
+      const int64_t gk = k0 + r;
+      const bool ok = gk < g.K;
+      cp_async16(bs + r * ldbs + cc, ok ? g.B + gk * g.ldb + cc : g.B, ok ? 16 : 0);
+    }
+    if (!TRANS && (centre || scale)) {
+      double* cs = Cs + stage * 2 * BK;
+      if (tid < BK) {
+        const int64_t gk = k0 + tid;
+        cs[tid] = (centre && gk < g.K) ? g.c[gk] : 0.0;
+        cs[BK + tid] = (scale && gk < g.K) ? g.rs[gk] : 1.0;
+      }
+    }
+  };
+
+  double acc[4][TMAX][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < TMAX; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // TN centring: c / rs depend on the output row (= column of A)
+  double crow[4], srow[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gm = m0 + wm * 32 + i * 8 + gq;
+    crow[i] = (TRANS && centre && gm < g.M) ? g.c[gm] : 0.0;
+    srow[i] = (TRANS && scale && gm < g.M) ? g.rs[gm] : 1.0;
+  }
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nkt) load_stage(s, kt_begin + s);
+    cp_async_commit();
+  }
+
+  for (int64_t it = 0; it < nkt; ++it) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int64_t pf = it + STAGES - 1;
+      if (pf < nkt) load_stage((int)(pf % STAGES), kt_begin + pf);
+      cp_async_commit();
+    }
+    const int stage = (int)(it % STAGES);
+    const TA* as = As + stage * S::a_stage_elems;
+    const double* bs = Bs + stage * S::b_stage_elems;
+    const double* cs = Cs + stage * 2 * BK;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = wm * 32 + i * 8 + gq;
+        if (!TRANS) {
+          double v = (double)as[r * A_NN_LD + kk + tq];
+          if (centre) v -= cs[kk + tq];
+          if (scale) v *= cs[BK + kk + tq];
+          a[i] = v;
+        } else {
+          double v = (double)as[(kk + tq) * A_TN_LD + r];
+          if (centre) v -= crow[i];
+          if (scale) v *= srow[i];
+          a[i] = v;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < TMAX; ++j) {
+        if (j < ntiles) {
+          const double b = bs[(kk + tq) * ldbs + (tile_begin + j) * 8 + gq];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[i], b);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: out-of-range rows are masked; padded B columns give zeros.
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gm = m0 + wm * 32 + i * 8 + gq;
+    if (gm >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < TMAX; ++j) {
+      if (j >= ntiles) continue;
+      const int col = (tile_begin + j) * 8 + 2 * tq;
+      if (g.splits == 1) {
+        if (col < g.Nout) g.C[gm * g.ldc + col] = acc[i][j][0];
+        if (col + 1 < g.Nout) g.C[gm * g.ldc + col + 1] = acc[i][j][1];
+      } else {
+        double* p = g.P + ((int64_t)split * g.M + gm) * N + col;
+        *reinterpret_cast<double2*>(p) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    }
+  }
+}
+
+// Fixed-order sum of the split partials: C[m][n] = sum_s P[s][m][n], n < Nout.
+__global__ void gemm_reduce_kernel(const double* __restrict__ P, int splits, int64_t M, int N,
+                                   double* __restrict__ C, int64_t ldc, int Nout) {
+  const int64_t total = M * (int64_t)Nout;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = e / Nout;
+    const int n = (int)(e % Nout);
+    double s = 0.0;
+    for (int t = 0; t < splits; ++t) s += P[((int64_t)t * M + m) * N + n];
+    C[m * ldc + n] = s;
+  }
+}
+
+template <typename TA, bool TRANS, int TMAX>
+static cudaError_t launch_one(const GemmArgs& g, dim3 grid, cudaStream_t st) {
+  auto kfn = gemm_pass_kernel<TA, TRANS, TMAX>;
+  const size_t smem = GemmSmem<TA>::bytes;
+  static bool attr_set = false;   // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  kfn<<<grid, GEMM_THREADS, smem, st>>>(g); ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+template <typename TA, bool TRANS>
+static cudaError_t dispatch_tmax(const GemmArgs& g, dim3 grid, cudaStream_t st) {
+  const int T = g.N / 8, T0 = (T + 1) / 2;
+  switch (T0) {
+    case 1: return launch_one<TA, TRANS, 1>(g, grid, st);
+    case 2: return launch_one<TA, TRANS, 2>(g, grid, st);
+    case 3: return launch_one<TA, TRANS, 3>(g, grid, st);
+    case 4: return launch_one<TA, TRANS, 4>(g, grid, st);
+    case 5: return launch_one<TA, TRANS, 5>(g, grid, st);
+    case 6: return launch_one<TA, TRANS, 6>(g, grid, st);
+    case 7: return launch_one<TA, TRANS, 7>(g, grid, st);
+    case 8: return launch_one<TA, TRANS, 8>(g, grid, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int gemm_choose_splits(int64_t M, int64_t K, int num_sms) {
+  const int64_t mblocks = ceil_div(M, BM);
+  const int64_t KT = ceil_div(K, BK);
+  const int64_t target = 2LL * num_sms;
+  if (mblocks >= num_sms) return 1;
+  int64_t s = ceil_div(target, mblocks);
+  const int64_t maxs = KT / 4 > 0 ? KT / 4 : 1;   // keep >= 4 k-tiles per split
+  if (s > maxs) s = maxs;
+  if (s < 1) s = 1;
+  return (int)s;
+}
+
+size_t gemm_partial_bytes(int64_t M, int N, int splits) {
+  return splits > 1 ? (size_t)splits * (size_t)M * (size_t)N * sizeof(double) : 0;
+}
+
+cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st, int* launches) {
+  if (c.N % 8 != 0 || c.N > NMAX || c.N < 8 || (c.ldb & 1)) return cudaErrorInvalidValue;
+  GemmArgs g;
+  g.A = c.A; g.lda = c.lda; g.B = c.B; g.ldb = c.ldb; g.C = c.C; g.ldc = c.ldc; g.P = c.P;
+  g.c = c.center; g.rs = c.rscale; g.M = c.M; g.K = c.K; g.N = c.N; g.Nout = c.Nout;
+  g.splits = c.splits < 1 ? 1 : c.splits;
+  {
+    const size_t es = c.a_f32 ? 4 : 8;
+    g.a_vec = ((uintptr_t)c.A % 16 == 0) && ((c.lda * es) % 16 == 0);
+  }
+  const int64_t KT = ceil_div(c.K, BK);
+  g.ktiles_per_split = ceil_div(KT, g.splits);
+  g.splits = (int)ceil_div(KT, g.ktiles_per_split);
+  if (g.splits < 1) g.splits = 1;
+  if (g.splits > 1 && c.P == nullptr) return cudaErrorInvalidValue;
+  dim3 grid((unsigned)ceil_div(c.M, BM), (unsigned)g.splits);
+  cudaError_t e;
+  if (c.a_f32) e = c.trans ? dispatch_tmax<float, true>(g, grid, st) : dispatch_tmax<float, false>(g, grid, st);
+  else e = c.trans ? dispatch_tmax<double, true>(g, grid, st) : dispatch_tmax<double, false>(g, grid, st);
+  if (e != cudaSuccess) return e;
+  if (g.splits > 1) {
+    const int64_t total = c.M * (int64_t)c.Nout;
+    int blocks = (int)ceil_div(total, 256);
+    if (blocks > 4 * 148) blocks = 4 * 148;
+    if (blocks < 1) blocks = 1;
+    gemm_reduce_kernel<<<blocks, 256, 0, st>>>(c.P, g.splits, c.M, c.N, c.C, c.ldc, c.Nout); ++g_kernel_launches;
+      e = cudaGetLastError();
+  }
+  return e;
+}
+
+}  // namespace rsvd

@@ -1,0 +1,106 @@
+// kernels.h -- internal launchers of the B200 rsvd library (host-callable).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace rsvd {
+
+// Kernels launched by this library (all launchers add to it).
+extern int64_t g_kernel_launches;
+
+// ---- K2/K3 streaming passes (gemm_pass.cu)
+struct GemmCall {
+  const void* A; int64_t lda; bool a_f32; bool trans;
+  const double* B; int64_t ldb;          // K x N, N % 8 == 0, zero-padded columns
+  double* C; int64_t ldc;                // output M x Nout
+  double* P;                             // split partials (>= gemm_partial_bytes)
+  const double* center;                  // per A-column mean (nullable)
+  const double* rscale;                  // per A-column 1/s.d. (nullable)
+  int64_t M, K; int N, Nout; int splits;
+};
+int gemm_choose_splits(int64_t M, int64_t K, int num_sms);
+size_t gemm_partial_bytes(int64_t M, int N, int splits);
+cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st, int* launches);
+
+// ---- K1 Omega (omega.cu)
+cudaError_t launch_omega(int64_t n, int64_t l, int64_t ldo, int64_t ncols_zero, int sdist,
+                         uint64_t seed, uint64_t stream, bool f32_round, bool out_f32, void* out,
+                         cudaStream_t st);
+
+// ---- small / panel kernels (panel.cu)
+// Column sums of A (m x n): out[j] = sum_i f(A[i][j]) with f = identity (mode 0)
+// or (a - c_j)^2 (mode 1).  Deterministic two-level reduction.
+cudaError_t launch_colsum(const void* A, int64_t lda, bool a_f32, int64_t m, int64_t n, int mode,
+                          const double* c, double* partial, double* out, cudaStream_t st, int* launches);
+size_t colsum_partial_bytes(int64_t m, int64_t n);
+// c = sum / m  (mode 0); rs = 1/sqrt(sumsq/(m-1)) and s (mode 1)
+cudaError_t launch_colstat_finish(double* v, int64_t n, double m_global, int mode, double* s_out,
+                                  cudaStream_t st);
+
+// Cholesky of the l x l Gram G (ld ldg): R upper with G = R^T R, Rinv = R^-1 into
+// ldr x ldr buffers (zero padded to npad); flag |= 1 on breakdown.
+cudaError_t launch_chol_inv(const double* G, int ldg, int l, int npad, double* R, double* Rinv,
+                            int* flag, int flag_bit, cudaStream_t st);
+// C (l x l) = A (l x l) * B (l x l), all ld = lda; single CTA.
+cudaError_t launch_small_matmul(const double* A, const double* B, double* C, int l, int ld,
+                                cudaStream_t st);
+// Householder leaves: rows [leaf*rows_base + min(leaf, rem) ...] of Y (ld ldy, l
+// columns).  Explicit Q overwrites the leaf rows; R (l x l, diag >= 0) goes to
+// Rstack + leaf*l*l (ld l).
+int leaf_rows_cap(int l);
+cudaError_t launch_hqr_leaves(double* Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
+                              double* Rstack, cudaStream_t st);
+// Q rows of each leaf <- Q rows * S_leaf, S_leaf = rows [leaf*l, leaf*l+l) of S (ld lds).
+cudaError_t launch_tsqr_combine(double* Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
+                                const double* S, int64_t lds, cudaStream_t st);
+
+// One-sided Jacobi SVD of X = R^T (R upper l x l, ld ldr): X J = W Sigma.
+// Outputs: sigma (l, descending), W (l x l, ld ldo) = U~, J (l x l, ld ldo).
+// flag |= 2 if the sweep cap was hit, 4 on non-finite input.
+cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double* W, double* J,
+                          int ldo, int* flag, int* sweeps, cudaStream_t st);
+
+// Sign convention (reading R9): sgn[i] = -1 iff the largest-|.| entry of V(:,i)
+// (lowest index on ties) is negative.
+cudaError_t launch_sign_from_v(const double* V, int64_t ldv, int64_t n, int l, double* sgn,
+                               cudaStream_t st);
+// X(:, j) *= sgn[j] for j < l (rows r, ld ldx)
+cudaError_t launch_scale_cols(double* X, int64_t ldx, int64_t rows, int l, const double* sgn,
+                              cudaStream_t st);
+// dst (rows x cols, ldd, f32 or f64) = src (ld lds) ; optional per-column factor
+cudaError_t launch_copy_out(const double* src, int64_t lds, int64_t rows, int cols, void* dst,
+                            int64_t ldd, bool dst_f32, const double* colfac, cudaStream_t st);
+cudaError_t launch_fill(double* p, int64_t count, double v, cudaStream_t st);
+// Y (rows x ld) columns [l, npad) set to zero
+cudaError_t launch_zero_cols(double* Y, int64_t ld, int64_t rows, int l, int npad, cudaStream_t st);
+// rpca: eig[i] = d[i]^2 / (m-1)
+cudaError_t launch_pca_eig(const double* d, int k, double m, void* eig, bool f32, cudaStream_t st);
+// Finite check of flags: flag |= 4 if any non-finite among v[0..n)
+cudaError_t launch_check_finite(const double* v, int64_t n, int* flag, cudaStream_t st);
+
+// ---- IALM (ialm.cu), FP64, reading R17-R23 of DESIGN.md
+// M = A - S + Z * inv_mu ;  optional: norms of A (||A||_F^2 partials, max|A|)
+cudaError_t launch_ialm_form_m(const double* A, const double* S, const double* Z, int64_t ld,
+                               int64_t m, int64_t n, double inv_mu, double* M, cudaStream_t st);
+// Fused update with L = U diag(dl) V^T (rank r <= 32, never materialised):
+//   S = shrink(A - L + Z inv_mu, lam inv_mu);  E = A - L - S;  Z += mu E;
+//   M_next = A - S + Z * inv_mu_next;  partial[b] = sum E^2 (per block).
+cudaError_t launch_ialm_update(const double* A, double* S, double* Z, double* Mnext, int64_t ld,
+                               int64_t m, int64_t n, const double* U, int64_t ldu,
+                               const double* V, int64_t ldv, const double* dl, int r,
+                               double inv_mu, double mu, double lam, double inv_mu_next,
+                               double* partial, int nblocks, cudaStream_t st);
+// L = U diag(dl) V^T materialised (final output)
+cudaError_t launch_lowrank_materialise(const double* U, int64_t ldu, const double* V, int64_t ldv,
+                                       const double* dl, int r, int64_t m, int64_t n, double* L,
+                                       int64_t ldl, cudaStream_t st);
+// Z = A / dual ; partials of ||A||_F^2 and max|A| (per block)
+cudaError_t launch_ialm_init(const double* A, int64_t ld, int64_t m, int64_t n, double* sumsq_part,
+                             double* max_part, int nblocks, cudaStream_t st);
+cudaError_t launch_scale_copy(const double* A, int64_t ld, int64_t m, int64_t n, double f,
+                              double* Z, cudaStream_t st);
+cudaError_t launch_reduce_blocks(const double* part, int nb, int op_max, double* out, cudaStream_t st);
+int ialm_blocks();
+
+}  // namespace rsvd

@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same
+seeded inputs.  Tolerances (BASELINE.json north_star):
+singular values relative 1e-10 (FP64) / 1e-4 (FP32); reconstruction error
+<= 1.0001 x the oracle's + 1e-13 floor (reading R24); ||U^T U - I||_max,
+||V^T V - I||_max <= 1e-12 (FP64) / 1e-5 (FP32); Omega bit-exact for
+uniform / Rademacher, <= 4 ulp for normal."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthetic
+
+pytestmark = pytest.mark.gpu
+
+SD = ["normal", "unif", "rademacher"]
+
+
+@pytest.fixture(scope="module")
+def rb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1608_02148_b200 as rb
+    return rb
+
+
+def _np(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def _recon_err(A, d, U, V):
+    return np.linalg.norm(A - (U * d) @ V.T) / np.linalg.norm(A)
+
+
+def _cos_cols(X, Y):
+    return np.abs(np.sum(X * Y, axis=0)) / (np.linalg.norm(X, axis=0) * np.linalg.norm(Y, axis=0))
+
+
+def _check_parity(A, r, o, k, tol_d=1e-10, tol_orth=1e-12, floor=1e-13, gap_tol=1e-6):
+    d, U, V = _np(r.d), _np(r.u), _np(r.v)
+    assert np.all(np.isfinite(d)) and np.all(np.isfinite(U)) and np.all(np.isfinite(V))
+    rel = np.abs(d - o["d"]) / np.maximum(np.abs(o["d"]), 1e-300)
+    assert rel.max() <= tol_d, "singular values: max rel err %.3e" % rel.max()
+    if U.shape[1]:
+        assert np.abs(U.T @ U - np.eye(U.shape[1])).max() <= tol_orth
+    if V.shape[1]:
+        assert np.abs(V.T @ V - np.eye(V.shape[1])).max() <= tol_orth
+    if U.shape[1] == k and V.shape[1] == k:
+        e_gpu = _recon_err(A, d, U, V)
+        e_or = _recon_err(A, o["d"], o["u"], o["v"])
+        assert e_gpu <= 1.0001 * e_or + floor, (e_gpu, e_or)
+    # singular vectors: column-wise where the spectrum is separated (reading R29)
+    dd = o["d"]
+    sep = np.ones(len(dd), dtype=bool)
+    for i in range(len(dd)):
+        for j in range(len(dd)):
+            if i != j and abs(dd[i] - dd[j]) <= gap_tol * dd[0]:
+                sep[i] = False
+    nv = min(V.shape[1], o["v"].shape[1])
+    if nv:
+        c = _cos_cols(V[:, :nv], o["v"][:, :nv])[sep[:nv]]
+        assert np.all(c > 1 - 1e-8), c.min()
+        # sign convention (R9): same signs as the oracle for separated columns
+        s = np.sign(np.sum(V[:, :nv] * o["v"][:, :nv], axis=0))[sep[:nv]]
+        assert np.all(s > 0)
+
+
+# ----------------------------------------------------------------------------- Omega (K1)
+@pytest.mark.parametrize("sdist", SD)
+@pytest.mark.parametrize("n,l", [(1, 1), (777, 13), (5000, 60)])
+def test_omega_bits(rb, sdist, n, l):
+    seed, stream = 0x0123456789ABCDEF, 0x00000002_00000007
+    g = _np(rb.omega(n, l, sdist, seed, stream))
+    o = oracle.omega(n, l, sdist, seed, stream)
+    if sdist == "normal":
+        ulp = np.abs(g - o) / np.spacing(np.maximum(np.abs(o), 1e-300))
+        assert ulp.max() <= 4
+    else:
+        assert np.array_equal(g, o)
+    g32 = rb.omega(n, l, sdist, seed, stream, dtype=torch.float32).cpu().numpy()
+    o32 = oracle.omega(n, l, sdist, seed, stream, dtype=np.float32)
+    if sdist == "normal":
+        assert np.abs(g32.astype(np.float64) - o32).max() <= 2 * np.spacing(np.abs(o32).max())
+    else:
+        assert np.array_equal(g32.astype(np.float64), o32)
+
+
+# ----------------------------------------------------------------------------- rsvd
+def test_config1_exact_rank(rb):
+    """Config 1 (J:7): exact rank 10, recovered singular values to 1e-12."""
+    A, meta = synthetic.make_config(1)
+    An = A.numpy()
+    Ad = A.cuda()
+    r = rb.rsvd(Ad, 10, p=10, q=2, sdist="normal", seed=meta["seed_omega"])
+    s = meta["s"].numpy()
+    assert np.max(np.abs(_np(r.d) - s) / s) <= 1e-12
+    o = oracle.oracle_rsvd(An, 10, p=10, q=2, sdist="normal", seed=meta["seed_omega"])
+    _check_parity(An, r, o, 10)
+
+
+CASES = [
+    # m, n, k, p, q, sdist, nu, nv
+    (300, 200, 10, 10, 2, "normal", None, None),
+    (1000, 257, 17, 5, 1, "unif", 5, 17),
+    (2049, 300, 50, 10, 2, "rademacher", None, None),
+    (4000, 1500, 40, 20, 3, "normal", None, 0),
+    (173, 531, 12, 8, 2, "normal", None, None),         # wide: works on A^T
+    (120, 90, 90, 10, 1, "unif", None, None),           # l = min(m,n): exact SVD
+    (5000, 64, 1, 10, 0, "rademacher", None, None),     # k = 1, q = 0
+    (3001, 777, 100, 20, 2, "unif", None, None),        # l = 120 (the build limit)
+]
+
+
+def _decay_matrix(m, n, seed, noise=1e-8):
+    k = min(m, n)
+    s = np.exp(-np.arange(k) / 15.0)
+    A, _ = synthetic.lowrank(m, n, torch.as_tensor(s), noise=noise, seed=seed)
+    return A
+
+
+@pytest.mark.parametrize("m,n,k,p,q,sdist,nu,nv", CASES)
+def test_rsvd_parity_cases(rb, m, n, k, p, q, sdist, nu, nv):
+    A = _decay_matrix(m, n, seed=m + n)
+    An = A.numpy()
+    r = rb.rsvd(A.cuda(), k, nu=nu, nv=nv, p=p, q=q, sdist=sdist, seed=77, stream=3)
+    o = oracle.oracle_rsvd(An, k, nu=nu, nv=nv, p=p, q=q, sdist=sdist, seed=77, stream=3)
+    _check_parity(An, r, o, k)
+
+
+def test_rsvd_unaligned_lda(rb):
+    """Odd leading dimension (non-16-byte rows) takes the element-wise staging path."""
+    A = _decay_matrix(1001, 301, seed=5)
+    big = torch.zeros(1001, 303, dtype=torch.float64)
+    big[:, :301] = A
+    view = big.cuda()[:, :301]
+    r = rb.rsvd(view, 20, p=10, q=2, seed=1)
+    o = oracle.oracle_rsvd(A.numpy(), 20, p=10, q=2, seed=1)
+    _check_parity(A.numpy(), r, o, 20)
+
+
+def test_rsvd_fp32(rb):
+    A = _decay_matrix(3000, 700, seed=9).to(torch.float32)
+    An = A.numpy()
+    r = rb.rsvd(A.cuda(), 30, p=10, q=2, seed=4)
+    assert r.d.dtype == torch.float32
+    o = oracle.oracle_rsvd(An, 30, p=10, q=2, seed=4)
+    _check_parity(An.astype(np.float64), r, o, 30, tol_d=1e-4, tol_orth=1e-5, floor=1e-6)
+
+
+def test_rsvd_rank_deficient_large_panel(rb):
+    """Exactly rank-5 input with a panel too tall for one CTA: CholeskyQR2 breaks
+    down and the TSQR (Householder leaves) path must take over."""
+    A, s = synthetic.lowrank(6000, 400, torch.as_tensor(10.0 ** (-np.arange(5) / 2)), seed=3)
+    An = A.numpy()
+    r = rb.rsvd(A.cuda(), 5, p=15, q=2, seed=2)
+    assert np.max(np.abs(_np(r.d) - s.numpy()) / s.numpy()) <= 1e-11
+    o = oracle.oracle_rsvd(An, 5, p=15, q=2, seed=2)
+    _check_parity(An, r, o, 5)
+
+
+def test_rsvd_deterministic(rb):
+    A = _decay_matrix(2000, 500, seed=1).cuda()
+    r1 = rb.rsvd(A, 20, seed=5)
+    r2 = rb.rsvd(A, 20, seed=5)
+    assert torch.equal(r1.d, r2.d) and torch.equal(r1.u, r2.u) and torch.equal(r1.v, r2.v)
+
+
+def test_rsvd_errors(rb):
+    A = torch.randn(50, 40, dtype=torch.float64, device="cuda")
+    for bad in (0, 41):
+        with pytest.raises(rb.RsvdError) as ei:
+            rb.rsvd(A, bad)
+        assert ei.value.status == 1
+    r = rb.rsvd(A, 5, nu=9, nv=9)           # clamped to k with a warning
+    assert r.u.shape == (50, 5) and r.v.shape == (40, 5)
+
+
+def test_config2_full_size(rb):
+    """Config 2 (J:8) at full size: 10000 x 5000, k=50, p=10, q=2, Rademacher."""
+    A, meta = synthetic.make_config(2)
+    An = A.numpy()
+    r = rb.rsvd(A.cuda(), 50, p=10, q=2, sdist="rademacher", seed=meta["seed_omega"])
+    o = oracle.oracle_rsvd(An, 50, p=10, q=2, sdist="rademacher", seed=meta["seed_omega"])
+    _check_parity(An, r, o, 50)
+
+
+# ----------------------------------------------------------------------------- rqb
+def test_rqb_parity(rb):
+    A = _decay_matrix(2500, 400, seed=11)
+    An = A.numpy()
+    Q, B = rb.rqb(A.cuda(), 20, p=10, q=1, sdist="unif", seed=6)
+    Qo, Bto = oracle.oracle_rqb(An, 30, 1, "unif", 6)
+    Q, B = _np(Q), _np(B)
+    assert np.abs(Q.T @ Q - np.eye(30)).max() < 1e-12
+    # same projector Q Q^T A (and, for a full-rank sketch, the same Q up to rounding)
+    assert np.linalg.norm(Q @ B - Qo @ Bto.T) / np.linalg.norm(An) < 1e-11
+    assert np.abs(Q - Qo).max() < 1e-8
+
+
+# ----------------------------------------------------------------------------- rpca
+@pytest.mark.parametrize("scale", [False, True])
+def test_rpca_parity(rb, scale):
+    A = _decay_matrix(4000, 300, seed=21) + 3.0 * torch.arange(300, dtype=torch.float64)[None, :] / 300
+    An = A.numpy()
+    out = rb.rpca(A.cuda(), 25, center=True, scale=scale, p=10, q=2, sdist="unif", seed=8)
+    o = oracle.oracle_rpca(An, 25, center=True, scale=scale, p=10, q=2, sdist="unif", seed=8)
+    ev = _np(out["eigvals"])
+    assert np.max(np.abs(ev - o["eigvals"]) / o["eigvals"]) < 1e-10
+    assert np.abs(_np(out["center"]) - o["center"]).max() < 1e-13
+    if scale:
+        assert np.max(np.abs(_np(out["scale"]) - o["scale"]) / o["scale"]) < 1e-13
+    c = _cos_cols(_np(out["rotation"]), o["rotation"])
+    assert np.all(c > 1 - 1e-8)
+    x = _np(out["x"])
+    assert np.linalg.norm(x - o["x"]) / np.linalg.norm(o["x"]) < 1e-9
+
+
+def test_rpca_large_offset_centring(rb):
+    """In-tile centring keeps explicit-centring accuracy for large column means
+    (offsets 1e2..1e4 x the rms)."""
+    A = _decay_matrix(3000, 200, seed=2) * 1e-2 + 1e2
+    An = A.numpy()
+    out = rb.rpca(A.cuda(), 10, center=True, p=10, q=2, seed=3)
+    o = oracle.oracle_rpca(An, 10, center=True, p=10, q=2, seed=3)
+    ev = _np(out["eigvals"])
+    assert np.max(np.abs(ev - o["eigvals"]) / o["eigvals"]) < 1e-9
+
+
+# ----------------------------------------------------------------------------- rrpca
+def test_rrpca_parity_small(rb):
+    A, L0, S0 = synthetic.sparse_plus_lowrank(4000, 300, rank=5, frac=0.05, seed=12)
+    An = A.numpy()
+    out = rb.rrpca(A.cuda(), k=10, p=10, q=2, tol=1e-7, maxiter=100, seed=3, trace=True)
+    o = oracle.oracle_rrpca(An, k=10, p=10, q=2, tol=1e-7, maxiter=100, seed=3)
+    assert abs(out["iters"] - o["iters"]) <= 1
+    L, S = _np(out["L"]), _np(out["S"])
+    if out["iters"] == o["iters"]:
+        assert np.linalg.norm(L - o["L"]) / np.linalg.norm(o["L"]) < 1e-10
+        assert np.linalg.norm(S - o["S"]) / np.linalg.norm(o["S"]) < 1e-10
+    L0n, S0n = L0.numpy(), S0.numpy()
+    assert np.linalg.norm(L - L0n) / np.linalg.norm(L0n) < 1e-6
+    assert ((np.abs(S) > 1e-6) == (S0n != 0)).mean() > 0.999
+    assert out["residual"] < 1e-7
