@@ -168,6 +168,12 @@ rsvd_status rsvd_profile_reset(rsvd_ctx* ctx);
 /* Number of kernels this library launched since the last reset. */
 int64_t rsvd_launch_count(const rsvd_ctx* ctx);
 
+/* Diagnostics of the last rsvd-family call (HOST out-param, n <= 3 slots):
+ * out[0] = one-sided Jacobi sweeps, out[1] = 1 if the CholeskyQR2 breakdown
+ * re-run in robust (Householder / TSQR) mode was taken, out[2] = kernel
+ * launches since the last rsvd_profile_reset. */
+rsvd_status rsvd_stats(const rsvd_ctx* ctx, int64_t* out, int n);
+
 #ifdef __cplusplus
 }
 #endif

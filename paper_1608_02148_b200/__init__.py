@@ -28,7 +28,7 @@ STATUS = {0: "RSVD_OK", 1: "RSVD_EINVAL", 2: "RSVD_ENOMEM", 3: "RSVD_ECUDA", 4: 
 EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_last_error", "rsvd_version", "rsvd_nccl_unique_id",
            "rsvd_comm_init", "rsvd_params_default", "rsvd_run", "rsvd_rqb", "rsvd_rpca",
            "rsvd_rrpca_params_default", "rsvd_rrpca", "rsvd_omega", "rsvd_set_profiling", "rsvd_profile",
-           "rsvd_profile_reset", "rsvd_launch_count"]
+           "rsvd_profile_reset", "rsvd_launch_count", "rsvd_stats"]
 
 
 class RsvdError(RuntimeError):
@@ -88,6 +88,7 @@ def lib():
                          ctypes.c_int),
         "rsvd_profile_reset": ([vp], ctypes.c_int),
         "rsvd_launch_count": ([vp], i64),
+        "rsvd_stats": ([vp, ctypes.POINTER(i64), ctypes.c_int], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -154,6 +155,12 @@ class Context:
 
     def launch_count(self):
         return int(lib().rsvd_launch_count(self.h))
+
+    def stats(self):
+        """(Jacobi sweeps, robust re-run taken, kernel launches) of the last call."""
+        buf = (ctypes.c_int64 * 3)()
+        self.check(lib().rsvd_stats(self.h, buf, 3))
+        return dict(jacobi_sweeps=int(buf[0]), robust_rerun=bool(buf[1]), launches=int(buf[2]))
 
     def close(self):
         if getattr(self, "h", None):

@@ -67,6 +67,8 @@ struct rsvd_ctx {
   double prof_bytes[5] = {0, 0, 0, 0, 0};
   int64_t prof_count[5] = {0, 0, 0, 0, 0};
   int64_t launches = 0;
+  int last_sweeps = 0;
+  int last_robust = 0;
 };
 
 namespace {
@@ -467,10 +469,11 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool robus
 }
 
 rsvd_status finish_flags(rsvd_ctx* ctx, int* flags) {
-  CK(cudaMemcpyAsync(ctx->flags_host, ctx->flags_dev, sizeof(int) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->flags_host, ctx->flags_dev, sizeof(int) * 16, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (ctx->prof) prof_collect(ctx);
   *flags = ctx->flags_host[0];
+  ctx->last_sweeps = ctx->flags_host[8];
   return RSVD_OK;
 }
 
@@ -486,7 +489,7 @@ rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bo
   else { p.M = A->m_local; p.n = A->n; p.m_global = mg; }
   const int64_t mn = std::min(mg, A->n);
   p.l = (int)std::min<int64_t>((int64_t)k + p_over, mn);
-  p.Np = (int)round_up(p.l, 8);
+  p.Np = (int)round_up(p.l, 16);      // GEMM N granularity: two warps x n8 tiles
   if (p.l > kMaxL) return fail(ctx, RSVD_EUNSUPPORTED, "l = k + p = %d exceeds this build's limit %d", p.l, kMaxL);
   if (ctx->nranks > 1 && p.M < p.l)
     return fail(ctx, RSVD_EUNSUPPORTED, "each rank needs at least l = %d rows", p.l);
@@ -498,9 +501,11 @@ rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bo
 
 rsvd_status run_with_retry(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool want_svd) {
   int flags = 0;
+  ctx->last_robust = 0;
   CKS(rsvd_core(ctx, p, prm, false, want_svd));
   CKS(finish_flags(ctx, &flags));
   if (flags & kFlagCholBreak) {
+    ctx->last_robust = 1;
     CKS(rsvd_core(ctx, p, prm, true, want_svd));
     CKS(finish_flags(ctx, &flags));
   }
@@ -714,6 +719,13 @@ rsvd_status rsvd_profile_reset(rsvd_ctx* ctx) {
 }
 
 int64_t rsvd_launch_count(const rsvd_ctx* ctx) { return ctx ? rsvd::g_kernel_launches : 0; }
+
+rsvd_status rsvd_stats(const rsvd_ctx* ctx, int64_t* out, int n) {
+  if (!ctx || !out || n < 0) return RSVD_EINVAL;
+  const int64_t v[3] = {ctx->last_sweeps, ctx->last_robust, rsvd::g_kernel_launches};
+  for (int i = 0; i < n && i < 3; ++i) out[i] = v[i];
+  return RSVD_OK;
+}
 
 }  // extern "C"
 

@@ -28,8 +28,8 @@ namespace rsvd {
 
 constexpr int BM = 128, BK = 16, STAGES = 4, GEMM_THREADS = 256;
 constexpr int A_NN_LD = BK + 4;      // [BM][BK+4]  (row = m)
-constexpr int A_TN_LD = BM + 8;      // [BK][BM+8]  (row = k)
-constexpr int B_PAD = 8;             // [BK][N+8]
+constexpr int A_TN_LD = BM + 4;      // [BK][BM+4]  (row = k); stride = 4 (mod 16) doubles
+constexpr int B_LDMAX = 132;         // [BK][N + pad], N + pad = 4 (mod 16)
 constexpr int NMAX = 128;
 
 template <typename TA>
@@ -37,7 +37,7 @@ struct GemmSmem {
   static constexpr int a_stage_elems_nn = BM * A_NN_LD;
   static constexpr int a_stage_elems_tn = BK * A_TN_LD;
   static constexpr int a_stage_elems = a_stage_elems_nn > a_stage_elems_tn ? a_stage_elems_nn : a_stage_elems_tn;
-  static constexpr int b_stage_elems = BK * (NMAX + B_PAD);
+  static constexpr int b_stage_elems = BK * B_LDMAX;
   static constexpr size_t bytes =
       (size_t)STAGES * (a_stage_elems * sizeof(TA) + b_stage_elems * sizeof(double) + 2 * BK * sizeof(double));
 };
@@ -67,11 +67,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
   const int64_t m0 = (int64_t)blockIdx.x * BM;
   const int split = blockIdx.y;
   const int N = g.N;
-  const int ldbs = (N % 16 == 0) ? N + B_PAD : N;   // keeps B fragment loads at 2 wavefronts
-  const int T = N >> 3;                      // n8 tiles
-  const int T0 = (T + 1) >> 1;
-  const int tile_begin = wn == 0 ? 0 : T0;
-  const int ntiles = wn == 0 ? T0 : T - T0;
+  // 64-bit fragment loads are served per half-warp (16 lanes x 8 B): a row stride of
+  // 4 (mod 16) doubles makes the 4 x 4 (row, column) lanes of a half-warp hit 16
+  // distinct bank pairs (one wavefront per half-warp).
+  const int ldbs = N + ((4 - N) & 15);
+  const int tile_begin = wn * TMAX;          // N = 16 * TMAX: each warp owns TMAX n8 tiles
   const int64_t KT = ceil_div(g.K, BK);
   const int64_t kt_begin = (int64_t)split * g.ktiles_per_split;
   int64_t kt_end = kt_begin + g.ktiles_per_split;
@@ -82,11 +82,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
   const bool scale = g.rs != nullptr;
   const bool avec = g.a_vec;
 
+  // Per-thread cp.async chunk descriptors, computed once: a thread always moves
+  // the same (row, column) chunk slots of a stage; only the k offset advances.
+  constexpr int EPC = 16 / sizeof(TA);                       // elements per 16-byte chunk
+  constexpr int A_CHUNKS = (BM * BK / EPC) / GEMM_THREADS;   // 4 (double) or 2 (float)
+  const int a_cpr = TRANS ? BM / EPC : BK / EPC;             // chunks per smem row
+  int a_r[A_CHUNKS], a_c[A_CHUNKS];
+#pragma unroll
+  for (int c = 0; c < A_CHUNKS; ++c) {
+    const int id = tid + c * GEMM_THREADS;
+    a_r[c] = id / a_cpr;
+    a_c[c] = (id % a_cpr) * EPC;
+  }
+
   auto load_stage = [&](int stage, int64_t kt) {
     const int64_t k0 = kt * BK;
     TA* as = As + stage * S::a_stage_elems;
     double* bs = Bs + stage * S::b_stage_elems;
-    constexpr int EPC = 16 / sizeof(TA);     // elements per 16-byte chunk
     if (!avec) {
       // unaligned rows: element-wise cp.async (same results, slower)
       for (int e = tid; e < BM * BK; e += GEMM_THREADS) {
@@ -99,33 +111,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
         if (sizeof(TA) == 8) cp_async8(dst, src, ok ? 8 : 0);
         else cp_async4(dst, src, ok ? 4 : 0);
       }
-    } else if (!TRANS) {
-      // BM rows x BK cols of A (row m, contiguous k)
-      constexpr int CPR = BK / EPC;          // chunks per row
-      for (int ch = tid; ch < BM * CPR; ch += GEMM_THREADS) {
-        const int r = ch / CPR, cc = (ch % CPR) * EPC;
-        const int64_t gm = m0 + r, gk = k0 + cc;
-        int valid = 0;
-        if (gm < g.M && gk < g.K) valid = (int)((g.K - gk) < EPC ? (g.K - gk) : EPC);
-        const TA* src = valid ? A + gm * g.lda + gk : A;
-        cp_async16(as + r * A_NN_LD + cc, src, valid * (int)sizeof(TA));
-      }
     } else {
-      // BK rows (k) x BM cols (m) of A, contiguous along m
-      constexpr int CPR = BM / EPC;
-      for (int ch = tid; ch < BK * CPR; ch += GEMM_THREADS) {
-        const int r = ch / CPR, cc = (ch % CPR) * EPC;
-        const int64_t gk = k0 + r, gm = m0 + cc;
+#pragma unroll
+      for (int c = 0; c < A_CHUNKS; ++c) {
+        int64_t gm, gk;
+        int64_t lim;
+        if (!TRANS) { gm = m0 + a_r[c]; gk = k0 + a_c[c]; lim = g.K - gk; }
+        else { gk = k0 + a_r[c]; gm = m0 + a_c[c]; lim = g.M - gm; }
         int valid = 0;
-        if (gk < g.K && gm < g.M) valid = (int)((g.M - gm) < EPC ? (g.M - gm) : EPC);
-        const TA* src = valid ? A + gk * g.lda + gm : A;
-        cp_async16(as + r * A_TN_LD + cc, src, valid * (int)sizeof(TA));
+        if (gm < g.M && gk < g.K) valid = (int)(lim < EPC ? lim : EPC);
+        const TA* src = valid ? A + (TRANS ? gk * g.lda + gm : gm * g.lda + gk) : A;
+        cp_async16(as + a_r[c] * (TRANS ? A_TN_LD : A_NN_LD) + a_c[c], src, valid * (int)sizeof(TA));
       }
     }
-    // B: BK rows x N cols (N multiple of 8, ldb even => 16-byte chunks of 2 doubles)
+    // B: BK rows x N cols (N % 16 == 0, ldb even => 16-byte chunks of 2 doubles)
     const int CPRB = N >> 1;
     for (int ch = tid; ch < BK * CPRB; ch += GEMM_THREADS) {
-      const int r = ch / CPRB, cc = (ch % CPRB) * 2;
+      const int r = ch / CPRB, cc = (ch - r * CPRB) * 2;
       const int64_t gk = k0 + r;
       const bool ok = gk < g.K;
       cp_async16(bs + r * ldbs + cc, ok ? g.B + gk * g.ldb + cc : g.B, ok ? 16 : 0);
@@ -191,14 +193,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
           a[i] = v;
         }
       }
+      double b[TMAX];
 #pragma unroll
-      for (int j = 0; j < TMAX; ++j) {
-        if (j < ntiles) {
-          const double b = bs[(kk + tq) * ldbs + (tile_begin + j) * 8 + gq];
+      for (int j = 0; j < TMAX; ++j) b[j] = bs[(kk + tq) * ldbs + (tile_begin + j) * 8 + gq];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[i], b);
-        }
-      }
+      for (int j = 0; j < TMAX; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
   cp_async_wait<0>();
@@ -210,7 +211,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
     if (gm >= g.M) continue;
 #pragma unroll
     for (int j = 0; j < TMAX; ++j) {
-      if (j >= ntiles) continue;
       const int col = (tile_begin + j) * 8 + 2 * tq;
       if (g.splits == 1) {
         if (col < g.Nout) g.C[gm * g.ldc + col] = acc[i][j][0];
@@ -253,8 +253,7 @@ static cudaError_t launch_one(const GemmArgs& g, dim3 grid, cudaStream_t st) {
 
 template <typename TA, bool TRANS>
 static cudaError_t dispatch_tmax(const GemmArgs& g, dim3 grid, cudaStream_t st) {
-  const int T = g.N / 8, T0 = (T + 1) / 2;
-  switch (T0) {
+  switch (g.N / 16) {
     case 1: return launch_one<TA, TRANS, 1>(g, grid, st);
     case 2: return launch_one<TA, TRANS, 2>(g, grid, st);
     case 3: return launch_one<TA, TRANS, 3>(g, grid, st);
@@ -284,7 +283,7 @@ size_t gemm_partial_bytes(int64_t M, int N, int splits) {
 }
 
 cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st, int* launches) {
-  if (c.N % 8 != 0 || c.N > NMAX || c.N < 8 || (c.ldb & 1)) return cudaErrorInvalidValue;
+  if (c.N % 16 != 0 || c.N > NMAX || c.N < 16 || (c.ldb & 1)) return cudaErrorInvalidValue;
   GemmArgs g;
   g.A = c.A; g.lda = c.lda; g.B = c.B; g.ldb = c.ldb; g.C = c.C; g.ldc = c.ldc; g.P = c.P;
   g.c = c.center; g.rs = c.rscale; g.M = c.M; g.K = c.K; g.N = c.N; g.Nout = c.Nout;

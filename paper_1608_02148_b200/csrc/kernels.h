@@ -12,7 +12,7 @@ extern int64_t g_kernel_launches;
 // ---- K2/K3 streaming passes (gemm_pass.cu)
 struct GemmCall {
   const void* A; int64_t lda; bool a_f32; bool trans;
-  const double* B; int64_t ldb;          // K x N, N % 8 == 0, zero-padded columns
+  const double* B; int64_t ldb;          // K x N, N % 16 == 0, zero-padded columns
   double* C; int64_t ldc;                // output M x Nout
   double* P;                             // split partials (>= gemm_partial_bytes)
   const double* center;                  // per A-column mean (nullable)

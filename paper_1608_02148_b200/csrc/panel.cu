@@ -24,8 +24,20 @@ namespace rsvd {
 
 constexpr int SMEM_OPTIN = 232448;   // B200 per-block opt-in shared memory (profiles/peaks_box.json)
 
+// cudaFuncSetAttribute is a slow host call: raise each kernel's dynamic
+// shared-memory limit to the opt-in maximum once, on first use.
 static cudaError_t set_smem(const void* fn, size_t bytes) {
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  static const void* done[32];
+  static int ndone = 0;
+  for (int i = 0; i < ndone; ++i)
+    if (done[i] == fn) return cudaSuccess;
+  (void)bytes;
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_OPTIN - (int)fa.sharedSizeBytes);
+  if (e == cudaSuccess && ndone < 32) done[ndone++] = fn;
+  return e;
 }
 
 // ------------------------------------------------------------------ column statistics
@@ -98,67 +110,110 @@ cudaError_t launch_colstat_finish(double* v, int64_t n, double m_global, int mod
 }
 
 // ------------------------------------------------------------------ Cholesky + inverse
-__global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ G, int ldg, int l,
-                                                        int npad, double* __restrict__ R,
-                                                        double* __restrict__ Rinv, int* flag,
-                                                        int flag_bit) {
+template <int NY>
+__global__ void __launch_bounds__(32 * NY, 1) chol_inv_kernel(const double* __restrict__ G, int ldg, int l, int npad,
+                                                              double* __restrict__ R, double* __restrict__ Rinv,
+                                                              int* flag, int flag_bit) {
+  // l <= 120, 32 x NY threads; thread (tx, ty) owns the elements (a, b) with
+  // a = ty (mod NY) and b = tx (mod 32) (at most MR x 4 of them).
+  // Gs (l x l) becomes R (upper) in place by a right-looking Cholesky; Xs
+  // accumulates R^-1 by a right-looking bottom-up back substitution.  Every
+  // update step loads its operands into registers before storing (no
+  // load-after-store serialisation through shared memory); 2 barriers per step.
+  constexpr int MR = (128 + NY - 1) / NY;
   extern __shared__ double sm[];
-  double* Gs = sm;                 // l x l (ld l), becomes R (upper) in place
-  double* d0 = Gs + l * l;         // original diagonal
+  const int ld = l;
+  double* Gs = sm;
+  double* Xs = Gs + l * ld;
   __shared__ int bad;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ double d0[128];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  constexpr int nthr = 32 * NY;
   if (tid == 0) bad = 0;
-  for (int e = tid; e < l * l; e += nt) Gs[e] = G[(e / l) * ldg + (e % l)];
-  __syncthreads();
-  for (int j = tid; j < l; j += nt) d0[j] = Gs[j * l + j];
+  for (int a = ty; a < l; a += NY)
+    for (int b = tx; b < l; b += 32) {
+      Gs[a * ld + b] = G[a * ldg + b];
+      Xs[a * ld + b] = 0.0;
+    }
+  for (int a = tid; a < l; a += nthr) d0[a] = G[a * ldg + a];
   __syncthreads();
   for (int j = 0; j < l; ++j) {
-    const double d = Gs[j * l + j];
+    const double d = Gs[j * ld + j];
     const bool brk = !(d > 1e-13 * d0[j]) || !isfinite(d);
     const double r = brk ? 1.0 : sqrt(d);
+    const double ir = 1.0 / r;
+    __syncthreads();                                     // pivot read by all
+    if (tid == 0) { Gs[j * ld + j] = r; if (brk) bad = 1; }
+    for (int b = j + 1 + tid; b < l; b += nthr) Gs[j * ld + b] = brk ? 0.0 : Gs[j * ld + b] * ir;
     __syncthreads();
-    if (tid == 0) {
-      if (brk) bad = 1;
-      Gs[j * l + j] = r;
+    // trailing update G[a][b] -= R[j][a] R[j][b], j < a <= b
+    double rb[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { const int b = tx + 32 * c; rb[c] = (b < l) ? Gs[j * ld + b] : 0.0; }
+#pragma unroll
+    for (int rr = 0; rr < MR; ++rr) {
+      const int a = ty + NY * rr;
+      if (a > j && a < l) {
+        const double ra = Gs[j * ld + a];
+        double g[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { const int b = tx + 32 * c; g[c] = (b >= a && b < l) ? Gs[a * ld + b] : 0.0; }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { const int b = tx + 32 * c; if (b >= a && b < l) Gs[a * ld + b] = fma(-ra, rb[c], g[c]); }
+      }
     }
-    for (int c = j + 1 + tid; c < l; c += nt) Gs[j * l + c] = brk ? 0.0 : Gs[j * l + c] / r;
+    __syncthreads();                                     // next pivot is read after the update
+  }
+  // bottom-up: X[k][j] = (delta_kj - S[k][j]) / R[k][k], j >= k ; S[i][j] += R[i][k] X[k][j], i < k <= j
+  for (int k = l - 1; k >= 0; --k) {
+    const double rkk = Gs[k * ld + k];
+    for (int j = k + tid; j < l; j += nthr) Xs[k * ld + j] = ((j == k ? 1.0 : 0.0) - Xs[k * ld + j]) / rkk;
     __syncthreads();
-    const int rem = l - j - 1;
-    for (int e = tid; e < rem * rem; e += nt) {
-      const int a = j + 1 + e / rem, b = j + 1 + e % rem;
-      if (b >= a) Gs[a * l + b] -= Gs[j * l + a] * Gs[j * l + b];
+    double xk[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { const int j = tx + 32 * c; xk[c] = (j >= k && j < l) ? Xs[k * ld + j] : 0.0; }
+#pragma unroll
+    for (int rr = 0; rr < MR; ++rr) {
+      const int i = ty + NY * rr;
+      if (i < k) {
+        const double rik = Gs[i * ld + k];
+        double x[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { const int j = tx + 32 * c; x[c] = (j >= k && j < l) ? Xs[i * ld + j] : 0.0; }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { const int j = tx + 32 * c; if (j >= k && j < l) Xs[i * ld + j] = fma(rik, xk[c], x[c]); }
+      }
     }
     __syncthreads();
   }
-  // R (upper, zero-padded to npad) and its inverse by column back-substitution:
-  // one warp per column c of X = R^-1: X[i][c] = (delta_ic - sum_{k>i} R[i][k] X[k][c]) / R[i][i]
-  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  for (int e = tid; e < npad * npad; e += nt) {
-    const int a = e / npad, b = e % npad;
-    if (R) R[e] = (a < l && b < l && b >= a) ? Gs[a * l + b] : 0.0;
-    Rinv[e] = 0.0;
+  for (int e = tid; e < npad * npad; e += nthr) {
+    const int r2 = e / npad, c = e - r2 * npad;
+    const bool in = r2 < l && c < l && c >= r2;
+    if (R) R[e] = in ? Gs[r2 * ld + c] : 0.0;
+    Rinv[e] = in ? Xs[r2 * ld + c] : 0.0;
   }
-  __syncthreads();
-  for (int c = warp; c < l; c += nw) {
-    for (int i = c; i >= 0; --i) {
-      double s = 0.0;
-      for (int k = i + 1 + lane; k <= c; k += 32) s += Gs[i * l + k] * Rinv[k * npad + c];
-      s = warp_sum(s);
-      if (lane == 0) Rinv[i * npad + c] = ((i == c ? 1.0 : 0.0) - s) / Gs[i * l + i];
-      __syncwarp();
-    }
-  }
-  __syncthreads();
   if (tid == 0 && bad) atomicOr(flag, flag_bit);
 }
 
+int g_chol_ny = 16;  // thread-block rows (32 x ny threads); tools/bench_small
+
 cudaError_t launch_chol_inv(const double* G, int ldg, int l, int npad, double* R, double* Rinv, int* flag,
                             int flag_bit, cudaStream_t st) {
-  const size_t smem = ((size_t)l * l + l) * sizeof(double);
-  if (smem > (size_t)SMEM_OPTIN - 1024) return cudaErrorInvalidValue;
-  cudaError_t e = set_smem((const void*)chol_inv_kernel, smem);
-  if (e != cudaSuccess) return e;
-  chol_inv_kernel<<<1, 1024, smem, st>>>(G, ldg, l, npad, R, Rinv, flag, flag_bit); ++g_kernel_launches;
+  const size_t smem = 2 * (size_t)l * l * sizeof(double);
+  if (l > 120 || smem > (size_t)SMEM_OPTIN - 2048) return cudaErrorInvalidValue;
+  cudaError_t e;
+#define RSVD_CHOL(NY)                                                                      \
+  e = set_smem((const void*)chol_inv_kernel<NY>, smem);                                   \
+  if (e != cudaSuccess) return e;                                                         \
+  chol_inv_kernel<NY><<<1, dim3(32, NY), smem, st>>>(G, ldg, l, npad, R, Rinv, flag, flag_bit);
+  switch (g_chol_ny) {
+    case 4: RSVD_CHOL(4) break;
+    case 8: RSVD_CHOL(8) break;
+    case 32: RSVD_CHOL(32) break;
+    default: RSVD_CHOL(16) break;
+  }
+#undef RSVD_CHOL
+  ++g_kernel_launches;
   return cudaGetLastError();
 }
 
@@ -321,106 +376,182 @@ cudaError_t launch_tsqr_combine(double* Y, int64_t ldy, int64_t M, int l, int64_
 }
 
 // ------------------------------------------------------------------ one-sided Jacobi
-__global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__ R, int ldr, int l,
-                                                      double* __restrict__ sigma, double* __restrict__ Wo,
-                                                      double* __restrict__ Jo, int ldo, int* flag,
-                                                      int* sweeps_out) {
+#ifndef JPROBE
+#define JPROBE(k)
+#endif
+template <int GL, bool FASTT>
+__global__ void __launch_bounds__(1024, 1) jacobi_kernel(const double* __restrict__ R, int ldr, int l,
+                                                         double* __restrict__ sigma, double* __restrict__ Wo,
+                                                         double* __restrict__ Jo, int ldo, int* flag,
+                                                         int* sweeps_out) {
+  // One-sided Jacobi on X = R^T: a pair (p, q) of columns is handled by a
+  // group of GL lanes (32/GL pairs per warp), so the per-step instruction
+  // count grows with the matrix work, not with the number of pairs.
   extern __shared__ double sm[];
   double* X = sm;                  // X[p*l + i] = column p of X = R^T  (= row p of R)
   double* J = X + l * l;           // J[p*l + i] = column p of J
   __shared__ int rotated, bad;
   __shared__ double sg[128];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int gsub = lane % GL, gid = warp * (32 / GL) + lane / GL, ngroups = nw * (32 / GL);
   if (tid == 0) { rotated = 0; bad = 0; }
+  __syncthreads();
   for (int e = tid; e < l * l; e += nt) {
-    const int p = e / l, i = e % l;
+    const int p = e / l, i = e - p * l;
     const double v = (i >= p) ? R[p * ldr + i] : 0.0;   // R upper: row p, col i
     if (!isfinite(v)) bad = 1;
     X[e] = v;
     J[e] = (p == i) ? 1.0 : 0.0;
   }
   __syncthreads();
-  const double tol = (double)l * 0x1.0p-52;
-  const int L = l + (l & 1);
+  const double tol = (double)l * 0x1.0p-52, tol2 = tol * tol;
+  const int L = l + (l & 1);       // round-robin over L players (a dummy when l is odd)
+  const int half = L / 2, Lm1 = L - 1;
   int sweeps = 0;
   bool converged = (bad != 0);
   for (int sweep = 0; sweep <= 30 && !converged; ++sweep) {
-    __syncthreads();
-    if (tid == 0) rotated = 0;
-    __syncthreads();
-    for (int s = 0; s < L - 1; ++s) {
-      for (int pi = warp; pi < L / 2; pi += nw) {
-        // round-robin (circle) pairing: index 0 fixed, others rotate
-        const int a = (pi == 0) ? 0 : ((pi - 1 + s) % (L - 1)) + 1;
-        const int bq = ((L - 2 - pi + s) % (L - 1)) + 1;
-        const int p = a < bq ? a : bq, q = a < bq ? bq : a;
-        if (q >= l) continue;
+    for (int s = 0; s < Lm1; ++s) {
+      for (int pb = 0; pb < half; pb += ngroups) {          // warp-uniform trip count
+        const int pi = pb + gid;
+        int p = 0, q = 0;
+        bool act = pi < half;
+        if (act) {
+          // circle method: player 0 fixed, players 1..L-1 rotate with s
+          int x1 = pi - 1 + s; if (x1 >= Lm1) x1 -= Lm1;
+          int x2 = Lm1 - 1 - pi + s; if (x2 >= Lm1) x2 -= Lm1;
+          const int a = (pi == 0) ? 0 : 1 + x1, bq = 1 + x2;
+          p = a < bq ? a : bq;
+          q = a < bq ? bq : a;
+          act = q < l;                                     // dummy player
+        }
+        JPROBE(0)
+        double al = 0.0, be = 0.0, ga = 0.0;
         double* xp = X + p * l;
         double* xq = X + q * l;
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < l; i += 32) {
-          const double u = xp[i], v = xq[i];
-          al += u * u; be += v * v; ga += u * v;
+        if (act) {
+          for (int i = gsub; i < l; i += GL) {
+            const double u = xp[i], v = xq[i];
+            al = fma(u, u, al); be = fma(v, v, be); ga = fma(u, v, ga);
+          }
         }
-        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-        if (fabs(ga) > tol * sqrt(al * be)) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
-          for (int i = lane; i < l; i += 32) {
+#pragma unroll
+        for (int o = GL / 2; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        JPROBE(1)
+        if (act && ga * ga > tol2 * (al * be)) {
+          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga), written as
+          // t = 2 ga sgn(be - al) / (|be - al| + sqrt((be - al)^2 + 4 ga^2)): one sqrt, one div.
+          const double dlt = be - al;
+          double t, c;
+          if (FASTT) {
+            // The angle only steers convergence; orthogonality of the rotation comes from
+            // c^2 + s^2 = 1, so t may be computed in FP32 (on operands scaled to O(1))
+            // while c = (1 + t^2)^-1/2 is refined to full FP64 precision by Newton steps.
+            const double mx = fmax(fabs(dlt), fabs(2.0 * ga));
+            const int ex = ilogb(mx);
+            const float df = (float)scalbn(dlt, -ex), gf = (float)scalbn(2.0 * ga, -ex);
+            const float tf = (df >= 0.f ? gf : -gf) / (fabsf(df) + sqrtf(fmaf(df, df, gf * gf)));
+            t = (double)tf;
+            const double x = fma(t, t, 1.0);
+            double c0 = (double)rsqrtf((float)x);
+            c0 = c0 * fma(-0.5 * x * c0, c0, 1.5);
+            c0 = c0 * fma(-0.5 * x * c0, c0, 1.5);
+            c = c0;
+          } else {
+            t = (dlt >= 0.0 ? 2.0 * ga : -2.0 * ga) / (fabs(dlt) + sqrt(fma(dlt, dlt, 4.0 * ga * ga)));
+            c = rsqrt(fma(t, t, 1.0));
+          }
+          const double sn = c * t;
+          JPROBE(2)
+          double* jp = J + p * l;
+          double* jq = J + q * l;
+          for (int i = gsub; i < l; i += GL) {
             const double u = xp[i], v = xq[i];
             xp[i] = c * u - sn * v;
             xq[i] = sn * u + c * v;
+            const double ju = jp[i], jv = jq[i];
+            jp[i] = c * ju - sn * jv;
+            jq[i] = sn * ju + c * jv;
           }
-          double* jp = J + p * l;
-          double* jq = J + q * l;
-          for (int i = lane; i < l; i += 32) {
-            const double u = jp[i], v = jq[i];
-            jp[i] = c * u - sn * v;
-            jq[i] = sn * u + c * v;
-          }
-          if (lane == 0) rotated = 1;
+          if (gsub == 0) rotated = 1;
         }
+        JPROBE(3)
       }
       __syncthreads();
+      JPROBE(4)
     }
-    if (!rotated) converged = true;
+    const bool any = rotated != 0;
+    __syncthreads();
+    if (tid == 0) rotated = 0;
+    if (!any) converged = true;
     else ++sweeps;
+    __syncthreads();
   }
-  __syncthreads();
   // sigma, stable descending order
   for (int p = warp; p < l; p += nw) {
     double s = 0.0;
-    for (int i = lane; i < l; i += 32) s += X[p * l + i] * X[p * l + i];
+    for (int i = lane; i < l; i += 32) s = fma(X[p * l + i], X[p * l + i], s);
     s = warp_sum(s);
     if (lane == 0) sg[p] = sqrt(s);
   }
   __syncthreads();
-  for (int p = tid; p < l; p += nt) {
+  for (int p = warp; p < l; p += nw) {
     int rank = 0;
     const double sp = sg[p];
-    for (int q = 0; q < l; ++q) rank += (sg[q] > sp) || (sg[q] == sp && q < p);
-    sigma[rank] = sp;
+    for (int q = lane; q < l; q += 32) rank += (sg[q] > sp) || (sg[q] == sp && q < p);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (lane == 0) sigma[rank] = sp;
     const double inv = sp > 0.0 ? 1.0 / sp : 1.0;
-    for (int i = 0; i < l; ++i) {
+    for (int i = lane; i < l; i += 32) {
       Wo[i * ldo + rank] = X[p * l + i] * inv;
       Jo[i * ldo + rank] = J[p * l + i];
     }
   }
   if (tid == 0) {
-    if (sweeps > 30 || (!converged)) atomicOr(flag, 2);
+    if (!converged) atomicOr(flag, 2);
     if (bad) atomicOr(flag, 4);
     if (sweeps_out) *sweeps_out = sweeps;
   }
 }
 
+int g_jacobi_lanes = 16;  // lanes per column pair (tunable; tools/bench_small)
+bool g_jacobi_fastt = true;
+
 cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double* W, double* J, int ldo,
                           int* flag, int* sweeps, cudaStream_t st) {
   const size_t smem = 2 * (size_t)l * l * sizeof(double);
   if (l > 120 || smem > (size_t)SMEM_OPTIN - 2048) return cudaErrorInvalidValue;
-  cudaError_t e = set_smem((const void*)jacobi_kernel, smem);
-  if (e != cudaSuccess) return e;
-  jacobi_kernel<<<1, 1024, smem, st>>>(R, ldr, l, sigma, W, J, ldo, flag, sweeps); ++g_kernel_launches;
+  const int L = l + (l & 1);
+  const int gl = g_jacobi_lanes;
+  const int groups_per_warp = 32 / gl;
+  int warps = (int)ceil_div(L / 2, groups_per_warp);
+  if (warps < 1) warps = 1;
+  if (warps > 32) warps = 32;
+  cudaError_t e;
+#define RSVD_JAC(G)                                                                          \
+  if (g_jacobi_fastt) {                                                                     \
+    e = set_smem((const void*)jacobi_kernel<G, true>, smem);                                \
+    if (e != cudaSuccess) return e;                                                         \
+    jacobi_kernel<G, true><<<1, 32 * warps, smem, st>>>(R, ldr, l, sigma, W, J, ldo, flag, sweeps); \
+  } else {                                                                                  \
+    e = set_smem((const void*)jacobi_kernel<G, false>, smem);                               \
+    if (e != cudaSuccess) return e;                                                         \
+    jacobi_kernel<G, false><<<1, 32 * warps, smem, st>>>(R, ldr, l, sigma, W, J, ldo, flag, sweeps); \
+  }
+  switch (gl) {
+    case 1: RSVD_JAC(1) break;
+    case 2: RSVD_JAC(2) break;
+    case 4: RSVD_JAC(4) break;
+    case 8: RSVD_JAC(8) break;
+    case 16: RSVD_JAC(16) break;
+    default: RSVD_JAC(32) break;
+  }
+#undef RSVD_JAC
+  ++g_kernel_launches;
   return cudaGetLastError();
 }
 
