@@ -26,7 +26,7 @@
 
 namespace rsvd {
 
-constexpr int BM = 128, BK = 16, STAGES = 4, GEMM_THREADS = 256;
+constexpr int BM = 128, BK = 32, STAGES = 3, GEMM_THREADS = 256;
 constexpr int A_NN_LD = BK + 4;      // [BM][BK+4]  (row = m)
 constexpr int A_TN_LD = BM + 4;      // [BK][BM+4]  (row = k); stride = 4 (mod 16) doubles
 constexpr int B_LDMAX = 132;         // [BK][N + pad], N + pad = 4 (mod 16)
@@ -53,7 +53,7 @@ struct GemmArgs {
   bool a_vec;                       // A rows 16-byte aligned (vector cp.async)
 };
 
-template <typename TA, bool TRANS, int TMAX>
+template <typename TA, bool TRANS, int TMAX, bool CENT>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   using S = GemmSmem<TA>;
@@ -78,8 +78,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
   if (kt_end > KT) kt_end = KT;
   const int64_t nkt = kt_end > kt_begin ? kt_end - kt_begin : 0;
   const TA* A = reinterpret_cast<const TA*>(g.A);
-  const bool centre = g.c != nullptr;
-  const bool scale = g.rs != nullptr;
+  const bool centre = CENT && g.c != nullptr;
+  const bool scale = CENT && g.rs != nullptr;
   const bool avec = g.a_vec;
 
   // Per-thread cp.async chunk descriptors, computed once: a thread always moves
@@ -175,31 +175,40 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
     const TA* as = As + stage * S::a_stage_elems;
     const double* bs = Bs + stage * S::b_stage_elems;
     const double* cs = Cs + stage * 2 * BK;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double a[4];
+    // fragments for k-step kk + 4 are loaded (into the other register set)
+    // before the DMMAs of k-step kk are issued: no register reuse stalls
+    double af[2][4], bf[2][TMAX];
+    auto load_frags = [&](int buf, int kk) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int r = wm * 32 + i * 8 + gq;
+        double v;
         if (!TRANS) {
-          double v = (double)as[r * A_NN_LD + kk + tq];
-          if (centre) v -= cs[kk + tq];
-          if (scale) v *= cs[BK + kk + tq];
-          a[i] = v;
+          v = (double)as[r * A_NN_LD + kk + tq];
+          if (CENT) {
+            if (centre) v -= cs[kk + tq];
+            if (scale) v *= cs[BK + kk + tq];
+          }
         } else {
-          double v = (double)as[(kk + tq) * A_TN_LD + r];
-          if (centre) v -= crow[i];
-          if (scale) v *= srow[i];
-          a[i] = v;
+          v = (double)as[(kk + tq) * A_TN_LD + r];
+          if (CENT) {
+            if (centre) v -= crow[i];
+            if (scale) v *= srow[i];
+          }
         }
+        af[buf][i] = v;
       }
-      double b[TMAX];
 #pragma unroll
-      for (int j = 0; j < TMAX; ++j) b[j] = bs[(kk + tq) * ldbs + (tile_begin + j) * 8 + gq];
+      for (int j = 0; j < TMAX; ++j) bf[buf][j] = bs[(kk + tq) * ldbs + (tile_begin + j) * 8 + gq];
+    };
+    load_frags(0, 0);
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      if (ks + 1 < BK / 4) load_frags((ks + 1) & 1, (ks + 1) * 4);
 #pragma unroll
       for (int j = 0; j < TMAX; ++j)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int i = 0; i < 4; ++i) dmma884(acc[i][j][0], acc[i][j][1], af[ks & 1][i], bf[ks & 1][j]);
     }
   }
   cp_async_wait<0>();
@@ -239,13 +248,14 @@ __global__ void gemm_reduce_kernel(const double* __restrict__ P, int splits, int
 
 template <typename TA, bool TRANS, int TMAX>
 static cudaError_t launch_one(const GemmArgs& g, dim3 grid, cudaStream_t st) {
-  auto kfn = gemm_pass_kernel<TA, TRANS, TMAX>;
+  const bool cent = g.c != nullptr || g.rs != nullptr;
+  auto kfn = cent ? gemm_pass_kernel<TA, TRANS, TMAX, true> : gemm_pass_kernel<TA, TRANS, TMAX, false>;
   const size_t smem = GemmSmem<TA>::bytes;
-  static bool attr_set = false;   // per instantiation
-  if (!attr_set) {
+  static bool attr_set[2] = {false, false};   // per instantiation (centred or not)
+  if (!attr_set[cent]) {
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[cent] = true;
   }
   kfn<<<grid, GEMM_THREADS, smem, st>>>(g); ++g_kernel_launches;
   return cudaGetLastError();
