@@ -160,8 +160,7 @@ size_t plan_bytes(rsvd_ctx* ctx, Plan& p) {
   const int Np = p.Np;
   size_t part = 0;
   auto upd = [&](int64_t M, int64_t K, int N) {
-    const int s = gemm_choose_splits(M, K, ctx->num_sms);
-    part = std::max(part, gemm_partial_bytes(M, N, s));
+    part = std::max(part, gemm_partial_bytes(N, gemm_choose_grid(M, K, ctx->num_sms)));
   };
   upd(p.M, p.n, Np);       // Y = A X
   upd(p.n, p.M, Np);       // Z = A^T Q
@@ -243,10 +242,10 @@ rsvd_status pass_ax(rsvd_ctx* ctx, Plan& p, const double* X, double* Y, bool cen
   g.center = centred ? p.colc : nullptr;
   g.rscale = p.scaled ? p.colr : nullptr;
   g.M = p.M; g.K = p.n; g.N = p.Np; g.Nout = p.Np;
-  g.splits = gemm_choose_splits(g.M, g.K, ctx->num_sms);
+  g.grid = ctx->num_sms;
   const double bytes = (double)p.M * p.n * (p.f32 ? 4 : 8);
   Prof pr(ctx, 0, bytes);
-  CK(gemm_pass(g, ctx->stream, nullptr));
+  CK(gemm_pass(g, ctx->stream));
   return RSVD_OK;
 }
 
@@ -258,11 +257,11 @@ rsvd_status pass_atx(rsvd_ctx* ctx, Plan& p, const double* Q, double* Z, bool ce
   g.center = centred ? p.colc : nullptr;
   g.rscale = p.scaled ? p.colr : nullptr;
   g.M = p.n; g.K = p.M; g.N = p.Np; g.Nout = p.Np;
-  g.splits = gemm_choose_splits(g.M, g.K, ctx->num_sms);
+  g.grid = ctx->num_sms;
   const double bytes = (double)p.M * p.n * (p.f32 ? 4 : 8);
   {
     Prof pr(ctx, 1, bytes);
-    CK(gemm_pass(g, ctx->stream, nullptr));
+    CK(gemm_pass(g, ctx->stream));
   }
   return allreduce_sum(ctx, Z, (size_t)p.n * p.Np);
 }
@@ -274,8 +273,8 @@ rsvd_status small_k(rsvd_ctx* ctx, Plan& p, const double* S, int64_t rows, const
   g.A = S; g.lda = p.Np; g.a_f32 = false; g.trans = false;
   g.B = Bsm; g.ldb = p.Np; g.C = C; g.ldc = ldc; g.P = p.part;
   g.M = rows; g.K = p.Np; g.N = p.Np; g.Nout = Nout;
-  g.splits = gemm_choose_splits(g.M, g.K, ctx->num_sms);
-  CK(gemm_pass(g, ctx->stream, nullptr));
+  g.grid = ctx->num_sms;
+  CK(gemm_pass(g, ctx->stream));
   return RSVD_OK;
 }
 
@@ -285,8 +284,8 @@ rsvd_status gram(rsvd_ctx* ctx, Plan& p, const double* S, int64_t rows, bool dis
   g.A = S; g.lda = p.Np; g.a_f32 = false; g.trans = true;
   g.B = S; g.ldb = p.Np; g.C = p.G; g.ldc = p.Np; g.P = p.part;
   g.M = p.Np; g.K = rows; g.N = p.Np; g.Nout = p.Np;
-  g.splits = gemm_choose_splits(g.M, g.K, ctx->num_sms);
-  CK(gemm_pass(g, ctx->stream, nullptr));
+  g.grid = ctx->num_sms;
+  CK(gemm_pass(g, ctx->stream));
   if (dist) return allreduce_sum(ctx, p.G, (size_t)p.Np * p.Np);
   return RSVD_OK;
 }

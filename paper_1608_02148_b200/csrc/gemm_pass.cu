@@ -12,23 +12,25 @@
 //
 // Design (B200, FP64): tcgen05 has no f64 kind, so the MMA is the warp-level
 // DMMA (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4), 37 TFLOP/s measured on this
-// pool (profiles/peaks_box.json).  A CTA owns BM = 128 rows of C and all N <= 128
-// columns; 8 warps = 4 (M, 32 rows each) x 2 (N halves).  A and B tiles of
-// BK = 16 are staged in shared memory by a 4-stage cp.async (LDGSTS) ring with
-// zero-fill for ragged edges; padding strides keep the fragment loads at the
-// minimum two shared-memory wavefronts.  A is read from HBM exactly once per
-// pass; B (Omega / Q, <= 5 MB) is re-read from L2 by every row block.  The
-// contraction may be split over `splits` CTAs (grid.y); the partials land in a
-// workspace and are summed in a fixed order by gemm_reduce (deterministic, no
-// FP64 atomics: SURVEY H4).
+// pool (profiles/peaks_box.json).  A work unit is (row block of BM = 128 rows
+// of C, k-tile of BK = 32); the units are split evenly over a persistent grid
+// of one CTA per SM ("stream-K"), so there is no wave quantisation whatever
+// the shape.  A CTA streams its contiguous range of units through a 3-stage
+// cp.async (LDGSTS) shared-memory ring with zero-fill for ragged edges; the 8
+// warps = 4 (M, 32 rows) x 2 (N halves) keep all N <= 128 columns of C in
+// registers and double-buffer their DMMA fragments.  A row block finished
+// entirely inside one CTA is written directly; a row block shared by several
+// CTAs leaves per-CTA partials that gemm_streamk_fixup sums in CTA order
+// (deterministic, no FP64 atomics: SURVEY H4).  A is read from HBM exactly
+// once per pass; B (Omega / Q, <= 5 MB) is re-read from L2.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace rsvd {
 
 constexpr int BM = 128, BK = 32, STAGES = 3, GEMM_THREADS = 256;
-constexpr int A_NN_LD = BK + 4;      // [BM][BK+4]  (row = m)
-constexpr int A_TN_LD = BM + 4;      // [BK][BM+4]  (row = k); stride = 4 (mod 16) doubles
+constexpr int A_NN_LD = BK + 4;      // [BM][BK+4]  (row = m); stride = 4 (mod 16) doubles
+constexpr int A_TN_LD = BM + 4;      // [BK][BM+4]  (row = k)
 constexpr int B_LDMAX = 132;         // [BK][N + pad], N + pad = 4 (mod 16)
 constexpr int NMAX = 128;
 
@@ -45,13 +47,20 @@ struct GemmSmem {
 struct GemmArgs {
   const void* A; int64_t lda;
   const double* B; int64_t ldb;
-  double* C; int64_t ldc;           // final output (splits == 1)
-  double* P;                        // partials [splits][M][N] (splits > 1)
+  double* C; int64_t ldc;           // final output
+  double* P;                        // stream-K partials [grid][2][BM][N]
   const double* c; const double* rs;
   int64_t M, K; int N, Nout;
-  int splits; int64_t ktiles_per_split;
+  int64_t KT, units;                // k-tiles per row block, total units
+  int grid;
   bool a_vec;                       // A rows 16-byte aligned (vector cp.async)
 };
+
+// first unit of CTA c when `units` are split evenly over `grid` CTAs
+// (units * grid < 2^63 for every shape this library accepts)
+__host__ __device__ inline int64_t unit_lo(int64_t units, int grid, int c) {
+  return (units * (int64_t)c) / grid;
+}
 
 template <typename TA, bool TRANS, int TMAX, bool CENT>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) {
@@ -64,28 +73,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 3, wn = warp >> 2;
   const int gq = lane >> 2, tq = lane & 3;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int split = blockIdx.y;
   const int N = g.N;
   // 64-bit fragment loads are served per half-warp (16 lanes x 8 B): a row stride of
   // 4 (mod 16) doubles makes the 4 x 4 (row, column) lanes of a half-warp hit 16
   // distinct bank pairs (one wavefront per half-warp).
   const int ldbs = N + ((4 - N) & 15);
   const int tile_begin = wn * TMAX;          // N = 16 * TMAX: each warp owns TMAX n8 tiles
-  const int64_t KT = ceil_div(g.K, BK);
-  const int64_t kt_begin = (int64_t)split * g.ktiles_per_split;
-  int64_t kt_end = kt_begin + g.ktiles_per_split;
-  if (kt_end > KT) kt_end = KT;
-  const int64_t nkt = kt_end > kt_begin ? kt_end - kt_begin : 0;
+  const int64_t KT = g.KT;
+  const int64_t u_lo = unit_lo(g.units, g.grid, blockIdx.x);
+  const int64_t u_hi = unit_lo(g.units, g.grid, blockIdx.x + 1);
+  const int64_t nun = u_hi - u_lo;
   const TA* A = reinterpret_cast<const TA*>(g.A);
   const bool centre = CENT && g.c != nullptr;
   const bool scale = CENT && g.rs != nullptr;
   const bool avec = g.a_vec;
 
   // Per-thread cp.async chunk descriptors, computed once: a thread always moves
-  // the same (row, column) chunk slots of a stage; only the k offset advances.
+  // the same (row, column) chunk slots of a stage; only the tile offsets advance.
   constexpr int EPC = 16 / sizeof(TA);                       // elements per 16-byte chunk
-  constexpr int A_CHUNKS = (BM * BK / EPC) / GEMM_THREADS;   // 4 (double) or 2 (float)
+  constexpr int A_CHUNKS = (BM * BK / EPC) / GEMM_THREADS;
   const int a_cpr = TRANS ? BM / EPC : BK / EPC;             // chunks per smem row
   int a_r[A_CHUNKS], a_c[A_CHUNKS];
 #pragma unroll
@@ -95,8 +101,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
     a_c[c] = (id % a_cpr) * EPC;
   }
 
-  auto load_stage = [&](int stage, int64_t kt) {
-    const int64_t k0 = kt * BK;
+  auto load_stage = [&](int stage, int64_t u) {
+    const int64_t mb = u / KT, kt = u - mb * KT;
+    const int64_t m0 = mb * BM, k0 = kt * BK;
     TA* as = As + stage * S::a_stage_elems;
     double* bs = Bs + stage * S::b_stage_elems;
     if (!avec) {
@@ -114,8 +121,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
     } else {
 #pragma unroll
       for (int c = 0; c < A_CHUNKS; ++c) {
-        int64_t gm, gk;
-        int64_t lim;
+        int64_t gm, gk, lim;
         if (!TRANS) { gm = m0 + a_r[c]; gk = k0 + a_c[c]; lim = g.K - gk; }
         else { gk = k0 + a_r[c]; gm = m0 + a_c[c]; lim = g.M - gm; }
         int valid = 0;
@@ -132,7 +138,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
       const bool ok = gk < g.K;
       cp_async16(bs + r * ldbs + cc, ok ? g.B + gk * g.ldb + cc : g.B, ok ? 16 : 0);
     }
-    if (!TRANS && (centre || scale)) {
+    if (!TRANS && CENT) {
       double* cs = Cs + stage * 2 * BK;
       if (tid < BK) {
         const int64_t gk = k0 + tid;
@@ -150,25 +156,52 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
 
   // TN centring: c / rs depend on the output row (= column of A)
   double crow[4], srow[4];
+  auto set_rows = [&](int64_t m0) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t gm = m0 + wm * 32 + i * 8 + gq;
-    crow[i] = (TRANS && centre && gm < g.M) ? g.c[gm] : 0.0;
-    srow[i] = (TRANS && scale && gm < g.M) ? g.rs[gm] : 1.0;
-  }
+    for (int i = 0; i < 4; ++i) {
+      const int64_t gm = m0 + wm * 32 + i * 8 + gq;
+      crow[i] = (TRANS && centre && gm < g.M) ? g.c[gm] : 0.0;
+      srow[i] = (TRANS && scale && gm < g.M) ? g.rs[gm] : 1.0;
+    }
+  };
+
+  auto epilogue = [&](int64_t mb, bool full, int slot) {
+    const int64_t m0 = mb * BM;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rloc = wm * 32 + i * 8 + gq;
+      const int64_t gm = m0 + rloc;
+#pragma unroll
+      for (int j = 0; j < TMAX; ++j) {
+        const int col = (tile_begin + j) * 8 + 2 * tq;
+        if (full) {
+          if (gm < g.M) {
+            if (col < g.Nout) g.C[gm * g.ldc + col] = acc[i][j][0];
+            if (col + 1 < g.Nout) g.C[gm * g.ldc + col + 1] = acc[i][j][1];
+          }
+        } else {
+          double* p = g.P + (((int64_t)blockIdx.x * 2 + slot) * BM + rloc) * N + col;
+          *reinterpret_cast<double2*>(p) = make_double2(acc[i][j][0], acc[i][j][1]);
+        }
+        acc[i][j][0] = acc[i][j][1] = 0.0;
+      }
+    }
+  };
+
+  if (CENT && TRANS && nun > 0) set_rows((u_lo / KT) * BM);
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nkt) load_stage(s, kt_begin + s);
+    if (s < nun) load_stage(s, u_lo + s);
     cp_async_commit();
   }
 
-  for (int64_t it = 0; it < nkt; ++it) {
+  for (int64_t it = 0; it < nun; ++it) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
       const int64_t pf = it + STAGES - 1;
-      if (pf < nkt) load_stage((int)(pf % STAGES), kt_begin + pf);
+      if (pf < nun) load_stage((int)(pf % STAGES), u_lo + pf);
       cp_async_commit();
     }
     const int stage = (int)(it % STAGES);
@@ -210,44 +243,67 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
 #pragma unroll
         for (int i = 0; i < 4; ++i) dmma884(acc[i][j][0], acc[i][j][1], af[ks & 1][i], bf[ks & 1][j]);
     }
-  }
-  cp_async_wait<0>();
-
-  // Epilogue: out-of-range rows are masked; padded B columns give zeros.
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t gm = m0 + wm * 32 + i * 8 + gq;
-    if (gm >= g.M) continue;
-#pragma unroll
-    for (int j = 0; j < TMAX; ++j) {
-      const int col = (tile_begin + j) * 8 + 2 * tq;
-      if (g.splits == 1) {
-        if (col < g.Nout) g.C[gm * g.ldc + col] = acc[i][j][0];
-        if (col + 1 < g.Nout) g.C[gm * g.ldc + col + 1] = acc[i][j][1];
-      } else {
-        double* p = g.P + ((int64_t)split * g.M + gm) * N + col;
-        *reinterpret_cast<double2*>(p) = make_double2(acc[i][j][0], acc[i][j][1]);
-      }
+    // end of a row-block segment: write it out (directly if this CTA covered
+    // all of its k-tiles, else as a partial for the fix-up)
+    const int64_t u = u_lo + it;
+    const int64_t mb = u / KT, kt = u - mb * KT;
+    if (kt == KT - 1 || it == nun - 1) {
+      const int64_t seg_start = (mb * KT > u_lo) ? mb * KT : u_lo;
+      const bool full = (seg_start == mb * KT) && (kt == KT - 1);
+      const int slot = (mb == u_lo / KT) ? 0 : 1;
+      epilogue(mb, full, slot);
+      if (CENT && TRANS && it + 1 < nun) set_rows((mb + 1) * BM);
     }
   }
+  cp_async_wait<0>();
 }
 
-// Fixed-order sum of the split partials: C[m][n] = sum_s P[s][m][n], n < Nout.
-__global__ void gemm_reduce_kernel(const double* __restrict__ P, int splits, int64_t M, int N,
-                                   double* __restrict__ C, int64_t ldc, int Nout) {
-  const int64_t total = M * (int64_t)Nout;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = e / Nout;
-    const int n = (int)(e % Nout);
+// Stream-K fix-up: for every row block split between CTAs, sum the partials
+// of the CTAs that touched it and write C.  Block column b-1 handles the
+// boundary at the start of CTA b (only the first boundary inside a row block
+// does the work).  T consecutive lanes share one output element, each summing
+// a strided subset of the contributors, then a fixed xor-shuffle tree
+// combines them: the summation order depends only on the shape
+// (deterministic), and every lane has only a few independent loads in flight.
+__global__ void gemm_streamk_fixup(GemmArgs g, int T) {
+  __shared__ int s_first, s_last;
+  __shared__ unsigned char s_slot[1024];
+  const int b = blockIdx.x + 1;
+  const int64_t ub = unit_lo(g.units, g.grid, b);
+  if (ub >= g.units || ub % g.KT == 0) return;                 // boundary on a row-block edge
+  const int64_t mb = ub / g.KT;
+  if (unit_lo(g.units, g.grid, b - 1) > mb * g.KT) return;     // not the first boundary in mb
+  if (threadIdx.x == 0) {
+    int c_last = b;
+    const int64_t last_unit = (mb + 1) * g.KT - 1;
+    while (c_last + 1 < g.grid && unit_lo(g.units, g.grid, c_last + 1) <= last_unit) ++c_last;
+    s_first = b - 1;
+    s_last = c_last;
+  }
+  __syncthreads();
+  const int c_first = s_first, c_last = s_last;
+  for (int c = c_first + threadIdx.x; c <= c_last; c += blockDim.x)
+    s_slot[c - c_first] = (mb == unit_lo(g.units, g.grid, c) / g.KT) ? 0 : 1;
+  __syncthreads();
+  const int N = g.N;
+  const int64_t m0 = mb * BM;
+  const int E = BM * N, epb = blockDim.x / T;
+  const int t = threadIdx.x % T;
+  for (int e0 = blockIdx.y * epb; e0 < E; e0 += gridDim.y * epb) {   // warp-uniform trip count
+    const int e = e0 + threadIdx.x / T;
+    const int r = e / N, col = e - r * N;
+    const bool ok = e < E && m0 + r < g.M && col < g.Nout;
     double s = 0.0;
-    for (int t = 0; t < splits; ++t) s += P[((int64_t)t * M + m) * N + n];
-    C[m * ldc + n] = s;
+    if (ok)
+      for (int c = c_first + t; c <= c_last; c += T)
+        s += g.P[(((int64_t)c * 2 + s_slot[c - c_first]) * BM + r) * N + col];
+    for (int o = T >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (ok && t == 0) g.C[(m0 + r) * g.ldc + col] = s;
   }
 }
 
 template <typename TA, bool TRANS, int TMAX>
-static cudaError_t launch_one(const GemmArgs& g, dim3 grid, cudaStream_t st) {
+static cudaError_t launch_one(const GemmArgs& g, cudaStream_t st) {
   const bool cent = g.c != nullptr || g.rs != nullptr;
   auto kfn = cent ? gemm_pass_kernel<TA, TRANS, TMAX, true> : gemm_pass_kernel<TA, TRANS, TMAX, false>;
   const size_t smem = GemmSmem<TA>::bytes;
@@ -257,68 +313,70 @@ static cudaError_t launch_one(const GemmArgs& g, dim3 grid, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_set[cent] = true;
   }
-  kfn<<<grid, GEMM_THREADS, smem, st>>>(g); ++g_kernel_launches;
+  kfn<<<g.grid, GEMM_THREADS, smem, st>>>(g);
   return cudaGetLastError();
 }
 
 template <typename TA, bool TRANS>
-static cudaError_t dispatch_tmax(const GemmArgs& g, dim3 grid, cudaStream_t st) {
+static cudaError_t dispatch_tmax(const GemmArgs& g, cudaStream_t st) {
   switch (g.N / 16) {
-    case 1: return launch_one<TA, TRANS, 1>(g, grid, st);
-    case 2: return launch_one<TA, TRANS, 2>(g, grid, st);
-    case 3: return launch_one<TA, TRANS, 3>(g, grid, st);
-    case 4: return launch_one<TA, TRANS, 4>(g, grid, st);
-    case 5: return launch_one<TA, TRANS, 5>(g, grid, st);
-    case 6: return launch_one<TA, TRANS, 6>(g, grid, st);
-    case 7: return launch_one<TA, TRANS, 7>(g, grid, st);
-    case 8: return launch_one<TA, TRANS, 8>(g, grid, st);
+    case 1: return launch_one<TA, TRANS, 1>(g, st);
+    case 2: return launch_one<TA, TRANS, 2>(g, st);
+    case 3: return launch_one<TA, TRANS, 3>(g, st);
+    case 4: return launch_one<TA, TRANS, 4>(g, st);
+    case 5: return launch_one<TA, TRANS, 5>(g, st);
+    case 6: return launch_one<TA, TRANS, 6>(g, st);
+    case 7: return launch_one<TA, TRANS, 7>(g, st);
+    case 8: return launch_one<TA, TRANS, 8>(g, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-int gemm_choose_splits(int64_t M, int64_t K, int num_sms) {
+// persistent grid: one CTA per SM, but at least kMinUnits k-tiles per CTA so
+// that the pipeline fill and the partial write-out stay amortised
+constexpr int64_t kMinUnits = 8;
+int gemm_choose_grid(int64_t M, int64_t K, int num_sms) {
   const int64_t mblocks = ceil_div(M, BM);
-  const int64_t KT = ceil_div(K, BK);
-  const int64_t target = 2LL * num_sms;
-  if (mblocks >= num_sms) return 1;
-  int64_t s = ceil_div(target, mblocks);
-  const int64_t maxs = KT / 4 > 0 ? KT / 4 : 1;   // keep >= 4 k-tiles per split
-  if (s > maxs) s = maxs;
-  if (s < 1) s = 1;
-  return (int)s;
+  const int64_t units = mblocks * ceil_div(K, BK);
+  int64_t gsz = units / kMinUnits;
+  if (gsz < mblocks) gsz = mblocks;                          // short K: one row block per CTA
+  if (gsz > num_sms) gsz = num_sms;
+  if (gsz < 1) gsz = 1;
+  return (int)gsz;
 }
 
-size_t gemm_partial_bytes(int64_t M, int N, int splits) {
-  return splits > 1 ? (size_t)splits * (size_t)M * (size_t)N * sizeof(double) : 0;
-}
+size_t gemm_partial_bytes(int N, int grid) { return (size_t)grid * 2 * BM * (size_t)N * sizeof(double); }
 
-cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st, int* launches) {
+cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st) {
   if (c.N % 16 != 0 || c.N > NMAX || c.N < 16 || (c.ldb & 1)) return cudaErrorInvalidValue;
+  if (c.M <= 0 || c.K <= 0) return cudaErrorInvalidValue;
   GemmArgs g;
   g.A = c.A; g.lda = c.lda; g.B = c.B; g.ldb = c.ldb; g.C = c.C; g.ldc = c.ldc; g.P = c.P;
   g.c = c.center; g.rs = c.rscale; g.M = c.M; g.K = c.K; g.N = c.N; g.Nout = c.Nout;
-  g.splits = c.splits < 1 ? 1 : c.splits;
+  g.KT = ceil_div(c.K, BK);
+  g.units = ceil_div(c.M, BM) * g.KT;
+  g.grid = gemm_choose_grid(c.M, c.K, c.grid > 0 ? c.grid : 148);
   {
     const size_t es = c.a_f32 ? 4 : 8;
     g.a_vec = ((uintptr_t)c.A % 16 == 0) && ((c.lda * es) % 16 == 0);
   }
-  const int64_t KT = ceil_div(c.K, BK);
-  g.ktiles_per_split = ceil_div(KT, g.splits);
-  g.splits = (int)ceil_div(KT, g.ktiles_per_split);
-  if (g.splits < 1) g.splits = 1;
-  if (g.splits > 1 && c.P == nullptr) return cudaErrorInvalidValue;
-  dim3 grid((unsigned)ceil_div(c.M, BM), (unsigned)g.splits);
+  if (g.grid > 1 && c.P == nullptr) return cudaErrorInvalidValue;
   cudaError_t e;
-  if (c.a_f32) e = c.trans ? dispatch_tmax<float, true>(g, grid, st) : dispatch_tmax<float, false>(g, grid, st);
-  else e = c.trans ? dispatch_tmax<double, true>(g, grid, st) : dispatch_tmax<double, false>(g, grid, st);
+  if (c.a_f32) e = c.trans ? dispatch_tmax<float, true>(g, st) : dispatch_tmax<float, false>(g, st);
+  else e = c.trans ? dispatch_tmax<double, true>(g, st) : dispatch_tmax<double, false>(g, st);
+  ++g_kernel_launches;
   if (e != cudaSuccess) return e;
-  if (g.splits > 1) {
-    const int64_t total = c.M * (int64_t)c.Nout;
-    int blocks = (int)ceil_div(total, 256);
-    if (blocks > 4 * 148) blocks = 4 * 148;
-    if (blocks < 1) blocks = 1;
-    gemm_reduce_kernel<<<blocks, 256, 0, st>>>(c.P, g.splits, c.M, c.N, c.C, c.ldc, c.Nout); ++g_kernel_launches;
-      e = cudaGetLastError();
+  if (g.grid > 1) {
+    // contributors per split row block -> lanes per output element (<= 4 loads each)
+    const int64_t contributors = ceil_div(g.KT * (int64_t)g.grid, g.units) + 1;
+    int T = 1;
+    while (T < 32 && T * 4 < contributors) T <<= 1;
+    const int epb = 256 / T;
+    int ych = (int)ceil_div((int64_t)BM * g.N, epb);
+    if (ych > 64) ych = 64;
+    gemm_streamk_fixup<<<dim3(g.grid - 1, ych), 256, 0, st>>>(g, T);
+    ++g_kernel_launches;
+    e = cudaGetLastError();
   }
   return e;
 }

@@ -17,11 +17,12 @@ struct GemmCall {
   double* P;                             // split partials (>= gemm_partial_bytes)
   const double* center;                  // per A-column mean (nullable)
   const double* rscale;                  // per A-column 1/s.d. (nullable)
-  int64_t M, K; int N, Nout; int splits;
+  int64_t M, K; int N, Nout;
+  int grid;                              // persistent stream-K grid (<= #SMs)
 };
-int gemm_choose_splits(int64_t M, int64_t K, int num_sms);
-size_t gemm_partial_bytes(int64_t M, int N, int splits);
-cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st, int* launches);
+int gemm_choose_grid(int64_t M, int64_t K, int num_sms);
+size_t gemm_partial_bytes(int N, int grid);
+cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st);
 
 // ---- K1 Omega (omega.cu)
 cudaError_t launch_omega(int64_t n, int64_t l, int64_t ldo, int64_t ncols_zero, int sdist,
