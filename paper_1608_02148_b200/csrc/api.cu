@@ -330,12 +330,23 @@ rsvd_status tsqr_local(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, double* 
 
 // Orthonormalise the first l columns of S (rows x Np, ld Np) in place.
 // dist: rows are distributed over ranks.  R (l x l, ld Np) to Rout if non-null.
-rsvd_status orth(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool dist, bool robust, double* Rout) {
+rsvd_status orth(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool dist, bool robust, double* Rout,
+                 bool exact = true) {
   const int l = p.l, Np = p.Np;
   Prof pr(ctx, 2, (double)rows * Np * 8 * 4);
   if (!dist && small_panel(rows, l)) {
     CK(launch_hqr_leaves(S, Np, rows, l, 1, p.Rsm, ctx->stream));
     if (Rout) { CK(launch_copy_out(p.Rsm, l, l, l, Rout, Np, false, nullptr, ctx->stream));  }
+    return RSVD_OK;
+  }
+  if (!robust && !exact) {
+    // intermediate subspace-iteration basis (Alg. 2 steps 2-3): only span(Y)
+    // matters downstream, so one CholeskyQR pass suffices (breakdown-checked)
+    CKS(gram(ctx, p, S, rows, dist));
+    CK(launch_chol_inv(p.G, Np, l, Np, p.R1, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream));
+    // in place: each output row of S R^-1 depends only on the same input row,
+    // and stream-K writes a shared row block only in the fix-up after all reads
+    CKS(small_k(ctx, p, S, rows, p.Rinv, S, Np, Np));
     return RSVD_OK;
   }
   if (!robust) {
@@ -431,9 +442,9 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool robus
   }
   CKS(pass_ax(ctx, p, p.X, p.Y, centred));                          // Y = A Omega
   for (int j = 0; j < prm->q; ++j) {                                 // Alg. 2
-    CKS(orth(ctx, p, p.Y, p.M, dist, robust, nullptr));             //   [Q,~] = qr(Y)
+    CKS(orth(ctx, p, p.Y, p.M, dist, robust, nullptr, false));      //   [Q,~] = qr(Y)
     CKS(pass_atx(ctx, p, p.Y, p.Z, centred));                        //   A^T Q
-    CKS(orth(ctx, p, p.Z, p.n, false, robust, nullptr));            //   [Q,~] = qr(A^T Q)
+    CKS(orth(ctx, p, p.Z, p.n, false, robust, nullptr, false));     //   [Q,~] = qr(A^T Q)
     CKS(pass_ax(ctx, p, p.Z, p.Y, centred));                         //   Y = A Q
   }
   CKS(orth(ctx, p, p.Y, p.M, dist, robust, nullptr));               // Alg. 4 step 9

@@ -110,109 +110,186 @@ cudaError_t launch_colstat_finish(double* v, int64_t n, double m_global, int mod
 }
 
 // ------------------------------------------------------------------ Cholesky + inverse
-template <int NY>
-__global__ void __launch_bounds__(32 * NY, 1) chol_inv_kernel(const double* __restrict__ G, int ldg, int l, int npad,
-                                                              double* __restrict__ R, double* __restrict__ Rinv,
-                                                              int* flag, int flag_bit) {
-  // l <= 120, 32 x NY threads; thread (tx, ty) owns the elements (a, b) with
-  // a = ty (mod NY) and b = tx (mod 32) (at most MR x 4 of them).
-  // Gs (l x l) becomes R (upper) in place by a right-looking Cholesky; Xs
-  // accumulates R^-1 by a right-looking bottom-up back substitution.  Every
-  // update step loads its operands into registers before storing (no
-  // load-after-store serialisation through shared memory); 2 barriers per step.
-  constexpr int MR = (128 + NY - 1) / NY;
+// Blocked Cholesky + triangular inverse, NB x NB blocks, 256 threads.
+// Only the NB-column diagonal factorisations and the NB x NB diagonal-block
+// inverses are sequential, and they run warp-synchronously (no CTA barrier);
+// the block-row solves, trailing updates and off-diagonal inverse blocks are
+// CTA-parallel with 3 (Cholesky) / 2 (inverse) barriers per block.
+constexpr int CHOL_NB = 16, CHOL_THREADS = 256;
+#ifndef CPROBE
+#define CPROBE(k)
+#endif
+
+__global__ void __launch_bounds__(CHOL_THREADS, 1) chol_inv_kernel(const double* __restrict__ G, int ldg, int l,
+                                                                   int npad, double* __restrict__ R,
+                                                                   double* __restrict__ Rinv, int* flag,
+                                                                   int flag_bit) {
+  constexpr int NB = CHOL_NB;
   extern __shared__ double sm[];
-  const int ld = l;
-  double* Gs = sm;
-  double* Xs = Gs + l * ld;
+  double* Gs = sm;                 // l x l, becomes R (upper)
+  double* Xs = Gs + l * l;         // l x l, R^-1 (upper)
+  __shared__ double d0[120], rdiag[120];
   __shared__ int bad;
-  __shared__ double d0[128];
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
-  constexpr int nthr = 32 * NY;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+  CPROBE(0)
   if (tid == 0) bad = 0;
-  for (int a = ty; a < l; a += NY)
-    for (int b = tx; b < l; b += 32) {
-      Gs[a * ld + b] = G[a * ldg + b];
-      Xs[a * ld + b] = 0.0;
-    }
-  for (int a = tid; a < l; a += nthr) d0[a] = G[a * ldg + a];
+  for (int e = tid; e < l * l; e += nthr) {
+    const int a = e / l, b = e - (e / l) * l;
+    const double g = G[a * ldg + b];
+    Gs[e] = g;
+    Xs[e] = 0.0;
+    if (a == b) d0[a] = g;
+  }
   __syncthreads();
-  for (int j = 0; j < l; ++j) {
-    const double d = Gs[j * ld + j];
-    const bool brk = !(d > 1e-13 * d0[j]) || !isfinite(d);
-    const double r = brk ? 1.0 : sqrt(d);
-    const double ir = 1.0 / r;
-    __syncthreads();                                     // pivot read by all
-    if (tid == 0) { Gs[j * ld + j] = r; if (brk) bad = 1; }
-    for (int b = j + 1 + tid; b < l; b += nthr) Gs[j * ld + b] = brk ? 0.0 : Gs[j * ld + b] * ir;
-    __syncthreads();
-    // trailing update G[a][b] -= R[j][a] R[j][b], j < a <= b
-    double rb[4];
+  CPROBE(1)
+  // ---------------- Cholesky G = R^T R, right-looking by NB-column blocks
+  for (int k0 = 0; k0 < l; k0 += NB) {
+    const int kb = min(NB, l - k0), ke = k0 + kb;
+    if (warp == 0) {                                   // (1) diagonal block, warp-synchronous
+      for (int c = k0; c < ke; ++c) {
+        const double d = Gs[c * l + c];
+        const bool brk = !(d > 1e-13 * d0[c]) || !isfinite(d);
+        const double ir = brk ? 1.0 : rsqrt(d);       // one long-latency op per pivot
+        const double r = brk ? 1.0 : d * ir;
+        __syncwarp();
+        if (lane == 0) { Gs[c * l + c] = r; rdiag[c] = ir; if (brk) bad = 1; }
+        const int b = c + 1 + (lane & 15);
+        if (lane < 16 && b < ke) Gs[c * l + b] = brk ? 0.0 : Gs[c * l + b] * ir;
+        __syncwarp();
+        // in-block trailing update, lane = (row parity, column); all operands are
+        // loaded into registers before the stores (no load-after-store chains)
+        if (b < ke) {
+          const double rcb = Gs[c * l + b];
+          double rca[NB / 2], gg[NB / 2];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) { const int b = tx + 32 * c; rb[c] = (b < l) ? Gs[j * ld + b] : 0.0; }
+          for (int t = 0; t < NB / 2; ++t) {
+            const int a = c + 1 + (lane >> 4) + 2 * t;
+            rca[t] = (a <= b) ? Gs[c * l + a] : 0.0;
+            gg[t] = (a <= b) ? Gs[a * l + b] : 0.0;
+          }
 #pragma unroll
-    for (int rr = 0; rr < MR; ++rr) {
-      const int a = ty + NY * rr;
-      if (a > j && a < l) {
-        const double ra = Gs[j * ld + a];
-        double g[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { const int b = tx + 32 * c; g[c] = (b >= a && b < l) ? Gs[a * ld + b] : 0.0; }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { const int b = tx + 32 * c; if (b >= a && b < l) Gs[a * ld + b] = fma(-ra, rb[c], g[c]); }
-      }
-    }
-    __syncthreads();                                     // next pivot is read after the update
-  }
-  // bottom-up: X[k][j] = (delta_kj - S[k][j]) / R[k][k], j >= k ; S[i][j] += R[i][k] X[k][j], i < k <= j
-  for (int k = l - 1; k >= 0; --k) {
-    const double rkk = Gs[k * ld + k];
-    for (int j = k + tid; j < l; j += nthr) Xs[k * ld + j] = ((j == k ? 1.0 : 0.0) - Xs[k * ld + j]) / rkk;
-    __syncthreads();
-    double xk[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) { const int j = tx + 32 * c; xk[c] = (j >= k && j < l) ? Xs[k * ld + j] : 0.0; }
-#pragma unroll
-    for (int rr = 0; rr < MR; ++rr) {
-      const int i = ty + NY * rr;
-      if (i < k) {
-        const double rik = Gs[i * ld + k];
-        double x[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { const int j = tx + 32 * c; x[c] = (j >= k && j < l) ? Xs[i * ld + j] : 0.0; }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { const int j = tx + 32 * c; if (j >= k && j < l) Xs[i * ld + j] = fma(rik, xk[c], x[c]); }
+          for (int t = 0; t < NB / 2; ++t) {
+            const int a = c + 1 + (lane >> 4) + 2 * t;
+            if (a <= b) Gs[a * l + b] = fma(-rca[t], rcb, gg[t]);
+          }
+        }
+        __syncwarp();
       }
     }
     __syncthreads();
+    CPROBE(2)
+    // (2) block row: R[k0:ke][j] = R_kk^-T G[k0:ke][j]  (forward substitution per column j)
+    for (int j = ke + tid; j < l; j += nthr) {
+      double x[NB];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        if (i < kb) {
+          double s = Gs[(k0 + i) * l + j];
+#pragma unroll
+          for (int p = 0; p < NB; ++p)
+            if (p < i) s -= Gs[(k0 + p) * l + k0 + i] * x[p];
+          x[i] = s * rdiag[k0 + i];
+          Gs[(k0 + i) * l + j] = x[i];
+        }
+      }
+    }
+    __syncthreads();
+    CPROBE(3)
+    // (3) trailing update: G[i][j] -= sum_p R[p][i] R[p][j], ke <= i <= j
+    const int tr = l - ke;
+    for (int i = ke + (tid >> 4); i < l; i += (nthr >> 4)) {
+      double ri[NB];
+#pragma unroll
+      for (int p = 0; p < NB; ++p) ri[p] = (p < kb) ? Gs[(k0 + p) * l + i] : 0.0;
+      for (int j = i + (tid & 15); j < l; j += 16) {
+        double s = 0.0;
+#pragma unroll
+        for (int p = 0; p < NB; ++p) if (p < kb) s = fma(ri[p], Gs[(k0 + p) * l + j], s);
+        Gs[i * l + j] -= s;
+      }
+    }
+    (void)tr;
+    __syncthreads();
+    CPROBE(4)
   }
+  // ---------------- X = R^-1
+  const int nblk = (l + NB - 1) / NB;
+  // (1) diagonal blocks, one warp per block, one lane per column (back substitution)
+  for (int kbk = warp; kbk < nblk; kbk += nthr / 32) {
+    const int k0 = kbk * NB, kb = min(NB, l - k0);
+    if (lane < kb) {
+      const int c = lane;
+      double x[NB];
+#pragma unroll
+      for (int ii = NB - 1; ii >= 0; --ii) {
+        if (ii <= c) {
+          double s = 0.0;
+#pragma unroll
+          for (int p = 0; p < NB; ++p)
+            if (p > ii && p <= c) s = fma(Gs[(k0 + ii) * l + k0 + p], x[p], s);
+          x[ii] = (ii == c) ? rdiag[k0 + c] : -s * rdiag[k0 + ii];
+          Xs[(k0 + ii) * l + k0 + c] = x[ii];
+        } else {
+          x[ii] = 0.0;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  CPROBE(5)
+  // (2) off-diagonal blocks, block rows bottom-up:
+  //     T[I][j] = sum_{p >= i0+kb} R[I][p] X[p][j];  X[I][j] = -X_II T[I][j]
+  for (int ib = nblk - 2; ib >= 0; --ib) {
+    const int i0 = ib * NB, kb = min(NB, l - i0), je = i0 + kb;
+    const int ncols = l - je;
+    for (int e = tid; e < kb * ncols; e += nthr) {
+      const int ii = e / ncols, j = je + e % ncols;
+      double s0 = 0.0, s1 = 0.0;
+      int p = je;
+      for (; p + 1 <= j; p += 2) {
+        s0 = fma(Gs[(i0 + ii) * l + p], Xs[p * l + j], s0);
+        s1 = fma(Gs[(i0 + ii) * l + p + 1], Xs[(p + 1) * l + j], s1);
+      }
+      if (p <= j) s0 = fma(Gs[(i0 + ii) * l + p], Xs[p * l + j], s0);
+      Xs[(i0 + ii) * l + j] = s0 + s1;                 // T, in place (rows i0..je of column j)
+    }
+    __syncthreads();
+    for (int j = je + tid; j < l; j += nthr) {
+      double t[NB];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) t[q] = (q < kb) ? Xs[(i0 + q) * l + j] : 0.0;
+#pragma unroll
+      for (int ii = 0; ii < NB; ++ii) {
+        if (ii < kb) {
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < NB; ++q) if (q >= ii && q < kb) s = fma(Xs[(i0 + ii) * l + i0 + q], t[q], s);
+          Xs[(i0 + ii) * l + j] = -s;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  CPROBE(6)
   for (int e = tid; e < npad * npad; e += nthr) {
     const int r2 = e / npad, c = e - r2 * npad;
     const bool in = r2 < l && c < l && c >= r2;
-    if (R) R[e] = in ? Gs[r2 * ld + c] : 0.0;
-    Rinv[e] = in ? Xs[r2 * ld + c] : 0.0;
+    if (R) R[e] = in ? Gs[r2 * l + c] : 0.0;
+    Rinv[e] = in ? Xs[r2 * l + c] : 0.0;
   }
   if (tid == 0 && bad) atomicOr(flag, flag_bit);
+  CPROBE(7)
 }
 
-int g_chol_ny = 16;  // thread-block rows (32 x ny threads); tools/bench_small
+int g_chol_ny = 16;  // (unused; kept for tools/bench_small)
 
 cudaError_t launch_chol_inv(const double* G, int ldg, int l, int npad, double* R, double* Rinv, int* flag,
                             int flag_bit, cudaStream_t st) {
-  const size_t smem = 2 * (size_t)l * l * sizeof(double);
+  const size_t smem = 2 * (size_t)l * l * sizeof(double);   // + ~2 KB static: fits up to l = 120
   if (l > 120 || smem > (size_t)SMEM_OPTIN - 2048) return cudaErrorInvalidValue;
-  cudaError_t e;
-#define RSVD_CHOL(NY)                                                                      \
-  e = set_smem((const void*)chol_inv_kernel<NY>, smem);                                   \
-  if (e != cudaSuccess) return e;                                                         \
-  chol_inv_kernel<NY><<<1, dim3(32, NY), smem, st>>>(G, ldg, l, npad, R, Rinv, flag, flag_bit);
-  switch (g_chol_ny) {
-    case 4: RSVD_CHOL(4) break;
-    case 8: RSVD_CHOL(8) break;
-    case 32: RSVD_CHOL(32) break;
-    default: RSVD_CHOL(16) break;
-  }
-#undef RSVD_CHOL
+  cudaError_t e = set_smem((const void*)chol_inv_kernel, smem);
+  if (e != cudaSuccess) return e;
+  chol_inv_kernel<<<1, CHOL_THREADS, smem, st>>>(G, ldg, l, npad, R, Rinv, flag, flag_bit);
   ++g_kernel_launches;
   return cudaGetLastError();
 }

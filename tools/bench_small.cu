@@ -6,6 +6,9 @@
 #include <vector>
 __device__ long long g_probe[8];
 __device__ long long g_probe_last;
+__device__ long long c_probe[8];
+__device__ long long c_probe_last;
+#define CPROBE(k) if (threadIdx.x == 0) { long long _t = clock64(); if (k > 0) c_probe[k] += _t - c_probe_last; c_probe_last = _t; }
 #define JPROBE(k) if (threadIdx.x == 0) { long long _t = clock64(); if (k > 0) g_probe[k] += _t - g_probe_last; g_probe_last = _t; }
 #include "../paper_1608_02148_b200/csrc/panel.cu"
 namespace rsvd { int64_t g_kernel_launches = 0; }
@@ -32,7 +35,7 @@ int main() {
     CK(cudaMalloc(&dR, l*l*8)); CK(cudaMalloc(&dG, l*l*8)); CK(cudaMalloc(&dR1, np*np*8)); CK(cudaMalloc(&dRi, np*np*8));
     CK(cudaMalloc(&sig, np*8)); CK(cudaMalloc(&W, np*np*8)); CK(cudaMalloc(&Jm, np*np*8));
     CK(cudaMemcpy(dR, R.data(), l*l*8, cudaMemcpyHostToDevice)); CK(cudaMemcpy(dG, G.data(), l*l*8, cudaMemcpyHostToDevice));
-    for (int ny : {4, 8, 16, 32}) {
+    for (int ny : {16}) {
       rsvd::g_chol_ny = ny;
       float t1 = timeit([&]{ launch_chol_inv(dG, l, l, np, dR1, dRi, flag, 1, 0); }, 20);
       printf("      chol_inv ny=%2d: %8.2f us\n", ny, t1);
@@ -48,6 +51,8 @@ int main() {
       double s = 0; for (int k = 0; k < l; ++k) s += R1[i*np+k]*Ri[k*np+j];
       e2 = std::fmax(e2, std::fabs(s - (i == j)));
     }
+    { long long pr[8]; cudaMemcpyFromSymbol(pr, c_probe, sizeof pr); long long z[8] = {0}; cudaMemcpyToSymbol(c_probe, z, sizeof z);
+      printf("      chol probe (all runs): load %lld diag %lld rowsolve %lld trail %lld invdiag %lld invoff %lld store %lld\n", pr[1], pr[2], pr[3], pr[4], pr[5], pr[6], pr[7]); }
     printf("l=%3d chol_inv %8.2f us (|R1-R| %.1e, |R R^-1 - I| %.1e)\n", l, tc, e1, e2);
     for (int cfg = 0; cfg < 8; ++cfg) {
       const int gls[4] = {4, 8, 16, 32};
