@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -208,9 +208,16 @@ def main():
     u = torch.empty(m_loc, k, dtype=A.dtype, device=dev)
     v = torch.empty(n, k, dtype=A.dtype, device=dev)
     center = meta["center"]
+    is_rrpca = bool(meta.get("rrpca"))
+    rr_state = {}
 
     def step():
-        if center:
+        if is_rrpca:
+            out = rb.rrpca(A, k=k, p=p, q=q, tol=meta["tol"], maxiter=100, sdist=meta["sdist"],
+                           seed=meta["seed_omega"], ctx=ctx, m_global=m, row_offset=meta["row_offset"])
+            rr_state["iters"] = out["iters"]
+            rr_state["residual"] = out["residual"]
+        elif center:
             rb.rpca(A, k, center=True, p=p, q=q, sdist=meta["sdist"], seed=meta["seed_omega"], ctx=ctx,
                     m_global=m, row_offset=meta["row_offset"])
         else:
@@ -252,7 +259,14 @@ def main():
     ms = float(t.item())
     passes = 2 * q + 2
     a_bytes = m * n * es
-    value = passes * a_bytes / (ms * 1e-3) / 1e9
+    if is_rrpca:
+        # per IALM iteration: one rsvd (2q+2 passes over M) + the fused update
+        # (reads A, S, Z; writes S, Z, M = 6 m x n arrays); plus the ||A||_2 rsvd
+        it = rr_state.get("iters", 1)
+        step_bytes = (it + 1) * passes * a_bytes + it * 6 * a_bytes
+    else:
+        step_bytes = passes * a_bytes + (a_bytes if center else 0)     # + the column-mean pass
+    value = step_bytes / (ms * 1e-3) / 1e9
 
     # roofline of the dominant kernel (the streaming passes; kinds 0 = A.X, 1 = A^T.X)
     hbm_peak, hbm_src, fp64_peak, fp64_src = peaks()
@@ -290,14 +304,16 @@ def main():
             "data": "synthetic",
             "config": {"workload": meta["name"], "m": m, "n": n, "k": k, "p": p, "q": q, "l": l,
                        "sdist": meta["sdist"], "center": bool(center), "passes_per_step": passes,
-                       "A_bytes": a_bytes, "l2_policy": "A (%d MB) > L2 (126 MB): no flush" % (a_bytes >> 20)
+                       "A_bytes": a_bytes, "bytes_per_step": step_bytes,
+                       "rrpca_iters": rr_state.get("iters"), "rrpca_residual": rr_state.get("residual"),
+                       "l2_policy": "A (%d MB) > L2 (126 MB): no flush" % (a_bytes >> 20)
                        if a_bytes > 126e6 else "A L2-resident (latency-bound config)",
                        "parallelism": "row-sharded dp%d" % world},
             "roofline": roof, "gpu_launches": int(launches), "clocks": clocks,
             "diagnostics": ctx.stats()}
 
     # end-to-end: host A (pinned) -> device, rsvd, d/u/v -> host, through the same API
-    if not args.no_e2e and world == 1 and not center:
+    if not args.no_e2e and world == 1 and not center and not is_rrpca:
         A_host = A.cpu().pin_memory()
         stage = torch.empty_like(A)
         d_h = torch.empty(k, dtype=A.dtype).pin_memory()
@@ -326,7 +342,7 @@ def main():
                        "h2d_bytes_per_step": int(a_bytes),
                        "d2h_bytes_per_step": int((k + m_loc * k + n * k) * es)}
 
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not is_rrpca and m * n <= 2e8:
         t_cpu, b_cpu, reps, shape = cpu_baseline_run(A.cpu().numpy(), meta)
         line["cpu_baseline"] = {"value": round(b_cpu / t_cpu / 1e9, 4), "unit": "GB/s",
                                 "cores": os.cpu_count(), "kind": "oracle",

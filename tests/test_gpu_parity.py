@@ -241,3 +241,38 @@ def test_rrpca_parity_small(rb):
     assert np.linalg.norm(L - L0n) / np.linalg.norm(L0n) < 1e-6
     assert ((np.abs(S) > 1e-6) == (S0n != 0)).mean() > 0.999
     assert out["residual"] < 1e-7
+
+
+# ----------------------------------------------------------------------------- full-size configs 3, 5
+def test_config3_full_size_rpca(rb):
+    """Config 3 (J:9): 200000 x 4000 column-centred PCA, k=100, p=20, q=2, uniform Omega."""
+    A, meta = synthetic.make_config(3)
+    out = rb.rpca(A.cuda(), 100, center=True, p=20, q=2, sdist="unif", seed=meta["seed_omega"])
+    An = A.numpy()
+    o = oracle.oracle_rpca(An, 100, center=True, p=20, q=2, sdist="unif", seed=meta["seed_omega"])
+    ev = _np(out["eigvals"])
+    assert np.max(np.abs(ev - o["eigvals"]) / o["eigvals"]) < 2e-10       # d^2: twice the d tolerance
+    assert np.abs(_np(out["center"]) - o["center"]).max() < 1e-12
+    rot = _np(out["rotation"])
+    assert np.abs(rot.T @ rot - np.eye(100)).max() < 1e-12
+    # separated eigenpairs agree column-wise with the oracle
+    dd = np.sqrt(o["eigvals"])
+    sep = np.array([min([abs(dd[i] - dd[j]) for j in range(100) if j != i]) > 1e-6 * dd[0] for i in range(100)])
+    c = _cos_cols(rot, o["rotation"])[sep]
+    assert np.all(c > 1 - 1e-8)
+
+
+def test_config5_full_size_rrpca(rb):
+    """Config 5 (J:11): 100000 x 1000 robust PCA by IALM, rsvd(k=20, p=10, q=2), tol 1e-7."""
+    A, meta = synthetic.make_config(5)
+    out = rb.rrpca(A.cuda(), k=20, p=10, q=2, tol=1e-7, maxiter=100, seed=meta["seed_omega"], trace=True)
+    L, S = _np(out["L"]), _np(out["S"])
+    L0, S0 = meta["L0"].numpy(), meta["S0"].numpy()
+    assert out["residual"] < 1e-7
+    assert np.linalg.norm(L - L0) / np.linalg.norm(L0) < 1e-6                  # ground truth (R21, X5)
+    assert ((np.abs(S) > 1e-6) == (S0 != 0)).mean() > 0.999
+    o = oracle.oracle_rrpca(A.numpy(), k=20, p=10, q=2, tol=1e-7, maxiter=100, seed=meta["seed_omega"])
+    assert abs(out["iters"] - o["iters"]) <= 1
+    if out["iters"] == o["iters"]:
+        assert np.linalg.norm(L - o["L"]) / np.linalg.norm(o["L"]) < 1e-10
+        assert np.linalg.norm(S - o["S"]) / np.linalg.norm(o["S"]) < 1e-10
