@@ -18,6 +18,7 @@
 #include <nccl.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -68,6 +69,7 @@ struct rsvd_ctx {
   int64_t prof_count[5] = {0, 0, 0, 0, 0};
   int64_t launches = 0;
   int last_sweeps = 0;
+  bool fp32_tcgen05 = true;       // RSVD_FP32_PATH=dmma selects the FP64-DMMA path for FP32 inputs
   int last_robust = 0;
 };
 
@@ -148,7 +150,9 @@ struct Plan {
   const void* A; int64_t lda;
   int64_t m_global;
   // workspace offsets
-  size_t oX, oY, oT, oZ, oPart, oSmall, oColc, oColr, oColp, total;
+  size_t oX, oY, oT, oZ, oPart, oSmall, oColc, oColr, oColp, oSplit, total;
+  bool use_tf32 = false;          // FP32 A on tcgen05 (3-term TF32 split)
+  float* split = nullptr;
   size_t part_bytes;
   // small-buffer offsets (doubles from oSmall)
   double *X, *Y, *T, *Z, *part, *G, *Rinv, *R1, *R2, *RB, *W, *J, *sigma, *sgn, *colc, *colr, *cols, *colp, *Rsm;
@@ -168,6 +172,7 @@ size_t plan_bytes(rsvd_ctx* ctx, Plan& p) {
   upd(Np, p.n, Np);        // Gram of Z
   upd(p.M, Np, Np);        // Y R^-1
   upd(p.n, Np, Np);        // Z R^-1
+  if (p.use_tf32) part = std::max(part, gemm_partial_bytes(tf32_n(Np), ctx->num_sms));
   p.part_bytes = part;
   const int64_t big = std::max(p.M, p.n);
   size_t o = 0;
@@ -180,6 +185,7 @@ size_t plan_bytes(rsvd_ctx* ctx, Plan& p) {
   p.oColc = o; o = align256(o + (size_t)p.n * 8);
   p.oColr = o; o = align256(o + (size_t)p.n * 16);
   p.oColp = o; o = align256(o + colsum_partial_bytes(p.M, p.n) + 256);
+  p.oSplit = o; o = align256(o + (p.use_tf32 ? tf32_split_bytes(big, Np) : 0));
   p.total = o;
   return o;
 }
@@ -216,6 +222,7 @@ void bind(rsvd_ctx* ctx, Plan& p) {
   p.RB = s; s += Np * Np; p.W = s; s += Np * Np; p.J = s; s += Np * Np; p.Rsm = s; s += 2 * Np * Np;
   p.sigma = s; s += Np; p.sgn = s; s += Np;
   p.colc = (double*)(b + p.oColc); p.colr = (double*)(b + p.oColr); p.cols = p.colr + p.n; p.colp = (double*)(b + p.oColp);
+  p.split = (float*)(b + p.oSplit);
 }
 
 // ----------------------------------------------------------------- collectives
@@ -235,7 +242,20 @@ rsvd_status allgather(rsvd_ctx* ctx, const double* send, double* recv, size_t co
 // ----------------------------------------------------------------- passes over A
 // Y (M x Np) = f(A) X  (K2).   With trans_input the stored matrix is A^T (n x M
 // row-major), so this is the TN form of the stored matrix.
+rsvd_status pass_tf32(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, double* C, int64_t M, int64_t K) {
+  Tf32Call t{};
+  t.A = (const float*)p.A; t.lda = p.lda; t.trans = trans;
+  t.B = B; t.ldb = p.Np; t.C = C; t.ldc = p.Np; t.P = p.part; t.split = p.split;
+  t.M = M; t.K = K; t.N = p.Np; t.Nout = p.Np; t.grid = ctx->num_sms;
+  CK(tf32_pass(t, ctx->stream));
+  return RSVD_OK;
+}
+
 rsvd_status pass_ax(rsvd_ctx* ctx, Plan& p, const double* X, double* Y, bool centred) {
+  if (p.use_tf32 && !centred) {
+    Prof pr(ctx, 0, (double)p.M * p.n * 4);
+    return pass_tf32(ctx, p, p.trans_input, X, Y, p.M, p.n);
+  }
   GemmCall g{};
   g.A = p.A; g.lda = p.lda; g.a_f32 = p.f32; g.trans = p.trans_input;
   g.B = X; g.ldb = p.Np; g.C = Y; g.ldc = p.Np; g.P = p.part;
@@ -251,6 +271,13 @@ rsvd_status pass_ax(rsvd_ctx* ctx, Plan& p, const double* X, double* Y, bool cen
 
 // Z (n x Np) = f(A)^T Q (K3), then allreduce over ranks.
 rsvd_status pass_atx(rsvd_ctx* ctx, Plan& p, const double* Q, double* Z, bool centred) {
+  if (p.use_tf32 && !centred) {
+    {
+      Prof pr(ctx, 1, (double)p.M * p.n * 4);
+      CKS(pass_tf32(ctx, p, !p.trans_input, Q, Z, p.n, p.M));
+    }
+    return allreduce_sum(ctx, Z, (size_t)p.n * p.Np);
+  }
   GemmCall g{};
   g.A = p.A; g.lda = p.lda; g.a_f32 = p.f32; g.trans = !p.trans_input;
   g.B = Q; g.ldb = p.Np; g.C = Z; g.ldc = p.Np; g.P = p.part;
@@ -500,6 +527,7 @@ rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bo
   const int64_t mn = std::min(mg, A->n);
   p.l = (int)std::min<int64_t>((int64_t)k + p_over, mn);
   p.Np = (int)round_up(p.l, 16);      // GEMM N granularity: two warps x n8 tiles
+  p.use_tf32 = p.f32 && !center_or_scale && ctx->fp32_tcgen05 && tf32_pass_supported(p.A, p.lda);
   if (p.l > kMaxL) return fail(ctx, RSVD_EUNSUPPORTED, "l = k + p = %d exceeds this build's limit %d", p.l, kMaxL);
   if (ctx->nranks > 1 && p.M < p.l)
     return fail(ctx, RSVD_EUNSUPPORTED, "each rank needs at least l = %d rows", p.l);
@@ -543,6 +571,10 @@ rsvd_status rsvd_create(rsvd_ctx** out, int device, void* stream) {
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->flags_host, 16 * sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->hbuf, 1024 * sizeof(double));
   if (e == cudaSuccess) ctx->sweeps_dev = ctx->flags_dev + 8;
+  {
+    const char* fp = getenv("RSVD_FP32_PATH");
+    if (fp && strcmp(fp, "dmma") == 0) ctx->fp32_tcgen05 = false;
+  }
   if (e != cudaSuccess) {
     delete ctx;
     return RSVD_ECUDA;

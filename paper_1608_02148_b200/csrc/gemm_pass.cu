@@ -302,6 +302,22 @@ __global__ void gemm_streamk_fixup(GemmArgs g, int T) {
   }
 }
 
+// fix-up for partials produced by another pass kernel with the same stream-K
+// partition (the tcgen05 FP32 path)
+cudaError_t gemm_streamk_fixup_launch(double* C, int64_t ldc, double* P, int64_t M, int N, int Nout, int64_t KT,
+                                      int64_t units, int grid, cudaStream_t st) {
+  GemmArgs g{};
+  g.C = C; g.ldc = ldc; g.P = P; g.M = M; g.N = N; g.Nout = Nout; g.KT = KT; g.units = units; g.grid = grid;
+  const int64_t contributors = ceil_div(KT * (int64_t)grid, units) + 1;
+  int T = 1;
+  while (T < 32 && T * 4 < contributors) T <<= 1;
+  int ych = (int)ceil_div((int64_t)BM * N, 256 / T);
+  if (ych > 64) ych = 64;
+  gemm_streamk_fixup<<<dim3(grid - 1, ych), 256, 0, st>>>(g, T);
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
 template <typename TA, bool TRANS, int TMAX>
 static cudaError_t launch_one(const GemmArgs& g, cudaStream_t st) {
   const bool cent = g.c != nullptr || g.rs != nullptr;

@@ -24,6 +24,23 @@ int gemm_choose_grid(int64_t M, int64_t K, int num_sms);
 size_t gemm_partial_bytes(int N, int grid);
 cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st);
 
+cudaError_t gemm_streamk_fixup_launch(double* C, int64_t ldc, double* P, int64_t M, int N, int Nout, int64_t KT,
+                                      int64_t units, int grid, cudaStream_t st);
+
+// ---- FP32 A on tcgen05 (pass_tf32.cu): 3-term TF32 split, TMEM accumulators
+struct Tf32Call {
+  const float* A; int64_t lda; bool trans;   // A row-major FP32 (16-byte aligned rows)
+  const double* B; int64_t ldb;              // K x N panel, FP64 (split to TF32 hi/lo inside)
+  double* C; int64_t ldc;                    // M x Nout output, FP64
+  double* P;                                 // stream-K partials (grid * 2 * 128 * tf32_n(N) doubles)
+  float* split;                              // 2 * K * tf32_n(N) floats scratch
+  int64_t M, K; int N, Nout; int grid;
+};
+bool tf32_pass_supported(const void* A, int64_t lda);
+int tf32_n(int Np);
+size_t tf32_split_bytes(int64_t K, int Np);
+cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st);
+
 // ---- K1 Omega (omega.cu)
 cudaError_t launch_omega(int64_t n, int64_t l, int64_t ldo, int64_t ncols_zero, int sdist,
                          uint64_t seed, uint64_t stream, bool f32_round, bool out_f32, void* out,

@@ -1,0 +1,409 @@
+// pass_tf32.cu -- the passes over an FP32 A (config 4) on the 5th-generation
+// tensor cores: tcgen05.mma kind::tf32 with a 3-term split, TMEM accumulators,
+// TMA-fed shared-memory ring, warp-specialised roles, stream-K partition.
+//
+//   NN:  C (M x N) = A (M x K) X (K x N)      (sketch / power pass, Alg. 4 step 3, Alg. 2 step 4)
+//   TN:  C (M x N) = A^T (M x K) Q (K x N)    (A^T Q passes, Alg. 2 step 3, Alg. 4 step 10)
+//
+// Precision (reading R12): every FP32 operand x is
+// split as x = hi + lo with hi = x truncated to TF32 (the bits kind::tf32
+// consumes) and lo = rna_tf32(x - hi) (x - hi is exact in FP32); the product is
+// A_hi B_hi + A_lo B_hi + A_hi B_lo, accumulated in FP32 in TMEM for one
+// row-block segment and then summed across segments in FP64.  The panel (X or
+// Q) is split once per pass into global hi/lo FP32 copies by prep_split_b;
+// the A tile is split in shared memory by the 4 epilogue warps.
+//
+// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one
+// thread), warp 2 = TMEM allocator, warps 4..7 = A-tile split + epilogue
+// (warp w reads TMEM lanes 32*(w%4)..+32).  Shared memory per stage:
+// A (16 KB, SWIZZLE_128B; K-major for NN, MN-major for TN), A_lo (16 KB),
+// B_hi, B_lo (N/32 boxes of 4 KB, MN-major).  3 stages.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rsvd {
+namespace tf32 {
+
+constexpr int BM = 128, BK = 32, STAGES = 3, THREADS = 256;
+constexpr int A_BYTES = BM * BK * 4;          // 16 KB
+constexpr int B_BOX_BYTES = 32 * BK * 4;      // 4 KB per 32-column box
+
+struct Args {
+  double* C; int64_t ldc;
+  double* P;
+  int64_t M, K; int N, Nout;
+  int64_t KT, units;
+  int grid;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = smem_u32(b);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory matrix descriptor (Blackwell version 1).  layout 2 =
+// SWIZZLE_128B (K-major operands); layout 1 = SWIZZLE_128B_BASE32B, the only
+// swizzled layout tcgen05 accepts for MN-major 32-bit (tf32) operands; its TMA
+// counterpart is CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B (4-row 512 B K atoms).
+constexpr uint32_t LAYOUT_SW128 = 2, LAYOUT_SW128_BASE32B = 1;
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout = LAYOUT_SW128) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;                   // version = 1 (tcgen05)
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"l"(static_cast<uint64_t>(__cvta_generic_to_shared(bar))) : "memory");
+}
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+#define TMEM_LD32(taddr, v)                                                                                  \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
+               "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                     \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),          \
+                 "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),      \
+                 "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),   \
+                 "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),   \
+                 "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                          \
+               : "r"(taddr))
+
+// tcgen05.wait::ld with the loaded registers as in/out operands, so that no use
+// of them can be scheduled before the wait
+#define TMEM_WAIT_LD(v)                                                                                      \
+  asm volatile("tcgen05.wait::ld.sync.aligned;"                                                               \
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]),         \
+                 "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]),     \
+                 "+r"(v[14]), "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]),  \
+                 "+r"(v[21]), "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]),  \
+                 "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31])                                         \
+               :                                                                                              \
+               : "memory")
+
+__host__ __device__ inline int64_t unit_lo(int64_t units, int grid, int c) { return (units * (int64_t)c) / grid; }
+
+#ifndef TF32_DEBUG_SPLIT
+#define TF32_DEBUG_SPLIT
+#endif
+template <bool TRANS>
+__global__ void __launch_bounds__(THREADS, 1)
+pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBhi,
+                 const __grid_constant__ CUtensorMap mapBlo, Args g) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte aligned carve-up (SWIZZLE_128B atoms)
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nbox = g.N / 32;
+  const int b_bytes = nbox * B_BOX_BYTES;
+  const int stage_bytes = 2 * A_BYTES + 2 * b_bytes;
+  __shared__ uint64_t full[STAGES], splitd[STAGES], empty_[STAGES], accf, acce;
+  __shared__ uint32_t tmem_base;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t KT = g.KT;
+  const int64_t u_lo = unit_lo(g.units, g.grid, blockIdx.x);
+  const int64_t u_hi = unit_lo(g.units, g.grid, blockIdx.x + 1);
+  const int64_t nun = u_hi - u_lo;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&splitd[s], 4); mbar_init(&empty_[s], 1); }
+    mbar_init(&accf, 1);
+    mbar_init(&acce, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+
+  auto stageA = [&](int s) { return base + (size_t)s * stage_bytes; };
+  auto stageAlo = [&](int s) { return base + (size_t)s * stage_bytes + A_BYTES; };
+  auto stageBhi = [&](int s) { return base + (size_t)s * stage_bytes + 2 * A_BYTES; };
+  auto stageBlo = [&](int s) { return base + (size_t)s * stage_bytes + 2 * A_BYTES + b_bytes; };
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      for (int64_t it = 0; it < nun; ++it) {
+        const int s = (int)(it % STAGES);
+        const uint32_t ph = (uint32_t)((it / STAGES) & 1);
+        mbar_wait(&empty_[s], ph ^ 1);
+        const int64_t u = u_lo + it, mb = u / KT, kt = u - mb * KT;
+        const int m0 = (int)(mb * BM), k0 = (int)(kt * BK);
+        mbar_expect_tx(&full[s], (uint32_t)(A_BYTES + 2 * b_bytes));
+        if (!TRANS) {
+          tma_2d(stageA(s), &mapA, k0, m0, &full[s]);                       // box {32 k, 128 rows}
+        } else {
+          for (int j = 0; j < 4; ++j) tma_2d(stageA(s) + j * B_BOX_BYTES, &mapA, m0 + 32 * j, k0, &full[s]);
+        }
+        for (int j = 0; j < nbox; ++j) {
+          tma_2d(stageBhi(s) + j * B_BOX_BYTES, &mapBhi, 32 * j, k0, &full[s]);
+          tma_2d(stageBlo(s) + j * B_BOX_BYTES, &mapBlo, 32 * j, k0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((TRANS ? 1u : 0u) << 15) | (1u << 16) |
+                             ((uint32_t)(g.N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      int64_t seg = 0;
+      bool first_in_seg = true;
+      for (int64_t it = 0; it < nun; ++it) {
+        const int s = (int)(it % STAGES);
+        const uint32_t ph = (uint32_t)((it / STAGES) & 1);
+        const int64_t u = u_lo + it, mb = u / KT, kt = u - mb * KT;
+        if (first_in_seg && seg > 0) { mbar_wait(&acce, (uint32_t)((seg - 1) & 1)); tc_fence_after(); }
+        mbar_wait(&splitd[s], ph);
+        tc_fence_after();
+        const uint32_t aH = smem_u32(stageA(s)), aL = smem_u32(stageAlo(s));
+        const uint32_t bH = smem_u32(stageBhi(s)), bL = smem_u32(stageBlo(s));
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          uint64_t dAh, dAl;
+          if (!TRANS) {   // K-major A: advance 32 B per 8-wide k step inside the 128 B swizzle row
+            dAh = sdesc(aH + kk * 32, 16, 1024);
+            dAl = sdesc(aL + kk * 32, 16, 1024);
+          } else {        // MN-major A: 8 k rows (1 KB) per k step; 512 B k atoms; 32-column boxes 4 KB apart
+            dAh = sdesc(aH + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
+            dAl = sdesc(aL + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
+          }
+          const uint64_t dBh = sdesc(bH + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
+          const uint64_t dBl = sdesc(bL + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
+          const uint32_t acc0 = (first_in_seg && kk == 0) ? 0u : 1u;
+          mma_tf32(tmem, dAh, dBh, idesc, acc0);
+          mma_tf32(tmem, dAl, dBh, idesc, 1u);
+          mma_tf32(tmem, dAh, dBl, idesc, 1u);
+        }
+        mma_commit(&empty_[s]);                       // smem stage free when these MMAs complete
+        first_in_seg = false;
+        if (kt == KT - 1 || it == nun - 1) {
+          mma_commit(&accf);                          // accumulator of this segment complete
+          ++seg;
+          first_in_seg = true;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- A-tile split + epilogue (warps 4..7)
+    const int et = tid - 128;                         // 0..127
+    int64_t seg = 0;
+    for (int64_t it = 0; it < nun; ++it) {
+      const int s = (int)(it % STAGES);
+      const uint32_t ph = (uint32_t)((it / STAGES) & 1);
+      mbar_wait(&full[s], ph);
+      float4* a4 = reinterpret_cast<float4*>(stageA(s));
+      float4* l4 = reinterpret_cast<float4*>(stageAlo(s));
+#pragma unroll 4
+      for (int q = et; q < A_BYTES / 16; q += 128) {
+        float4 a = a4[q], hi, lo;
+        hi.x = tf32_trunc(a.x); lo.x = tf32_rna(a.x - hi.x);
+        hi.y = tf32_trunc(a.y); lo.y = tf32_rna(a.y - hi.y);
+        hi.z = tf32_trunc(a.z); lo.z = tf32_rna(a.z - hi.z);
+        hi.w = tf32_trunc(a.w); lo.w = tf32_rna(a.w - hi.w);
+        a4[q] = hi;
+        l4[q] = lo;
+      }
+      TF32_DEBUG_SPLIT
+      fence_proxy_async();                            // generic-proxy writes -> async proxy (MMA)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&splitd[s]);
+      const int64_t u = u_lo + it, mb = u / KT, kt = u - mb * KT;
+      if (kt == KT - 1 || it == nun - 1) {
+        mbar_wait(&accf, (uint32_t)(seg & 1));
+        tc_fence_after();
+        const int64_t seg_start = (mb * KT > u_lo) ? mb * KT : u_lo;
+        const bool fullseg = (seg_start == mb * KT) && (kt == KT - 1);
+        const int slot = (mb == u_lo / KT) ? 0 : 1;
+        const int row = 32 * (warp & 3) + lane;
+        const int64_t gm = mb * BM + row;
+        for (int c0 = 0; c0 < g.N; c0 += 32) {
+          uint32_t v[32];
+          const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)c0;
+          TMEM_LD32(taddr, v);
+          TMEM_WAIT_LD(v);    // the registers are defined only after wait::ld
+          if (fullseg) {
+            if (gm < g.M) {
+              double* dst = g.C + gm * g.ldc + c0;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (c0 + j < g.Nout) dst[j] = (double)__uint_as_float(v[j]);
+            }
+          } else {
+            double* dst = g.P + (((int64_t)blockIdx.x * 2 + slot) * BM + row) * g.N + c0;
+#pragma unroll
+            for (int j = 0; j < 32; j += 2)
+              *reinterpret_cast<double2*>(dst + j) = make_double2((double)__uint_as_float(v[j]),
+                                                                  (double)__uint_as_float(v[j + 1]));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acce);
+        ++seg;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(128));
+  }
+}
+
+// X (K x Np, FP64, ld ldx) -> Xhi, Xlo (K x N, FP32, row-major, zero-padded columns)
+__global__ void prep_split_b(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, int N,
+                             float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t total = K * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / N;
+    const int n = (int)(e - k * N);
+    const float x = (n < Np) ? (float)X[k * ldx + n] : 0.0f;
+    const float h = tf32_trunc(x);
+    hi[e] = h;
+    lo[e] = tf32_rna(x - h);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D FP32 row-major tensor (rows x cols, ld elements), box {box_cols, box_rows};
+// SWIZZLE_128B for K-major use, SWIZZLE_128B_ATOM_32B for MN-major use
+static bool make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+                     int box_rows, bool mn_major) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace tf32
+
+bool tf32_pass_supported(const void* A, int64_t lda) {
+  return ((uintptr_t)A % 16 == 0) && ((lda * 4) % 16 == 0) && tf32::get_encode() != nullptr;
+}
+
+int tf32_n(int Np) { return (int)round_up(Np, 32); }
+
+size_t tf32_split_bytes(int64_t K, int Np) { return 2 * (size_t)K * tf32_n(Np) * sizeof(float); }
+
+cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st) {
+  using namespace tf32;
+  const int N = tf32_n(c.N);
+  if (N > 128 || c.M <= 0 || c.K <= 0) return cudaErrorInvalidValue;
+  // 1) panel split into FP32 hi / lo (K x N, row-major)
+  float* hi = c.split;
+  float* lo = c.split + (size_t)c.K * N;
+  {
+    int64_t total = c.K * N;
+    int blocks = (int)ceil_div(total, 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    prep_split_b<<<blocks, 256, 0, st>>>(c.B, c.ldb, c.K, c.N, N, hi, lo);
+    ++g_kernel_launches;
+  }
+  // 2) tensor maps
+  CUtensorMap mA, mBh, mBl;
+  bool ok;
+  if (!c.trans) ok = make_map(&mA, c.A, c.M, c.K, c.lda, 32, BM, false);     // A: M rows x K cols (K-major)
+  else ok = make_map(&mA, c.A, c.K, c.M, c.lda, 32, BK, true);               // A: K rows x M cols (MN-major)
+  ok = ok && make_map(&mBh, hi, c.K, N, N, 32, BK, true) && make_map(&mBl, lo, c.K, N, N, 32, BK, true);
+  if (!ok) return cudaErrorInvalidValue;
+  Args g;
+  g.C = c.C; g.ldc = c.ldc; g.P = c.P; g.M = c.M; g.K = c.K; g.N = N; g.Nout = c.Nout;
+  g.KT = ceil_div(c.K, BK);
+  const int64_t mblocks = ceil_div(c.M, BM);
+  g.units = mblocks * g.KT;
+  int64_t grid = g.units / 8;
+  if (grid < mblocks) grid = mblocks;
+  if (grid > c.grid) grid = c.grid;
+  if (grid < 1) grid = 1;
+  g.grid = (int)grid;
+  const size_t smem = (size_t)STAGES * (2 * A_BYTES + 2 * (N / 32) * B_BOX_BYTES) + 1024;
+  cudaError_t e;
+  if (!c.trans) {
+    e = cudaFuncSetAttribute(pass_tf32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    pass_tf32_kernel<false><<<g.grid, THREADS, smem, st>>>(mA, mBh, mBl, g);
+  } else {
+    e = cudaFuncSetAttribute(pass_tf32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    pass_tf32_kernel<true><<<g.grid, THREADS, smem, st>>>(mA, mBh, mBl, g);
+  }
+  ++g_kernel_launches;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (g.grid > 1) e = gemm_streamk_fixup_launch(c.C, c.ldc, c.P, c.M, N, c.Nout, g.KT, g.units, g.grid, st);
+  return e;
+}
+
+}  // namespace rsvd
