@@ -168,11 +168,8 @@ size_t plan_bytes(rsvd_ctx* ctx, Plan& p) {
   };
   upd(p.M, p.n, Np);       // Y = A X
   upd(p.n, p.M, Np);       // Z = A^T Q
-  upd(Np, p.M, Np);        // Gram of Y
-  upd(Np, p.n, Np);        // Gram of Z
-  upd(p.M, Np, Np);        // Y R^-1
-  upd(p.n, Np, Np);        // Z R^-1
   if (p.use_tf32) part = std::max(part, gemm_partial_bytes(tf32_n(Np), ctx->num_sms));
+  part = std::max(part, gram_partial_bytes(Np, ctx->num_sms));
   p.part_bytes = part;
   const int64_t big = std::max(p.M, p.n);
   size_t o = 0;
@@ -293,26 +290,17 @@ rsvd_status pass_atx(rsvd_ctx* ctx, Plan& p, const double* Q, double* Z, bool ce
   return allreduce_sum(ctx, Z, (size_t)p.n * p.Np);
 }
 
-// C (rows x Nout) = S (rows x Np) * Bsm (Np x Np) (small-K product, K2 kernel)
+// C (rows x Nout) = S (rows x Np) * Bsm (Np x Np) (small-K product, panel_apply)
 rsvd_status small_k(rsvd_ctx* ctx, Plan& p, const double* S, int64_t rows, const double* Bsm, double* C,
-                    int64_t ldc, int Nout) {
-  GemmCall g{};
-  g.A = S; g.lda = p.Np; g.a_f32 = false; g.trans = false;
-  g.B = Bsm; g.ldb = p.Np; g.C = C; g.ldc = ldc; g.P = p.part;
-  g.M = rows; g.K = p.Np; g.N = p.Np; g.Nout = Nout;
-  g.grid = ctx->num_sms;
-  CK(gemm_pass(g, ctx->stream));
+                    int64_t ldc, int Nout, bool upper = false) {
+  CK(launch_panel_apply(S, p.Np, rows, p.Np, Bsm, p.Np, C, ldc, Nout, upper, ctx->num_sms, ctx->stream));
   return RSVD_OK;
 }
 
-// G (Np x Np) = S^T S (K3 kernel), allreduce when the rows are distributed.
+// G (Np x Np) = S^T S (gram_partial + fixed-order reduce), allreduce when the
+// rows are distributed.
 rsvd_status gram(rsvd_ctx* ctx, Plan& p, const double* S, int64_t rows, bool dist) {
-  GemmCall g{};
-  g.A = S; g.lda = p.Np; g.a_f32 = false; g.trans = true;
-  g.B = S; g.ldb = p.Np; g.C = p.G; g.ldc = p.Np; g.P = p.part;
-  g.M = p.Np; g.K = rows; g.N = p.Np; g.Nout = p.Np;
-  g.grid = ctx->num_sms;
-  CK(gemm_pass(g, ctx->stream));
+  CK(launch_gram(S, p.Np, rows, p.Np, p.part, p.G, p.Np, ctx->num_sms, ctx->stream));
   if (dist) return allreduce_sum(ctx, p.G, (size_t)p.Np * p.Np);
   return RSVD_OK;
 }
@@ -370,21 +358,21 @@ rsvd_status orth(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool dist, boo
     // intermediate subspace-iteration basis (Alg. 2 steps 2-3): only span(Y)
     // matters downstream, so one CholeskyQR pass suffices (breakdown-checked)
     CKS(gram(ctx, p, S, rows, dist));
-    CK(launch_chol_inv(p.G, Np, l, Np, p.R1, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream));
+    CK(launch_chol_aug(p.G, Np, l, Np, p.R1, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream));
     // in place: each output row of S R^-1 depends only on the same input row,
     // and stream-K writes a shared row block only in the fix-up after all reads
-    CKS(small_k(ctx, p, S, rows, p.Rinv, S, Np, Np));
+    CKS(small_k(ctx, p, S, rows, p.Rinv, S, Np, Np, true));
     return RSVD_OK;
   }
   if (!robust) {
     // CholeskyQR2
     CKS(gram(ctx, p, S, rows, dist));
-    CK(launch_chol_inv(p.G, Np, l, Np, p.R1, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream));
-    CKS(small_k(ctx, p, S, rows, p.Rinv, p.T, Np, Np));
+    CK(launch_chol_aug(p.G, Np, l, Np, p.R1, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream));
+    CKS(small_k(ctx, p, S, rows, p.Rinv, p.T, Np, Np, true));
     CKS(gram(ctx, p, p.T, rows, dist));
-    CK(launch_chol_inv(p.G, Np, l, Np, p.R2, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream));
-    CKS(small_k(ctx, p, p.T, rows, p.Rinv, S, Np, Np));
-    if (Rout) { CK(launch_small_matmul(p.R2, p.R1, Rout, l, Np, ctx->stream));  }
+    CK(launch_chol_aug(p.G, Np, l, Np, p.R2, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream));
+    CKS(small_k(ctx, p, p.T, rows, p.Rinv, S, Np, Np, true));
+    if (Rout) { CK(launch_panel_apply(p.R2, Np, Np, Np, p.R1, Np, Rout, Np, Np, true, ctx->num_sms, ctx->stream));  }
     return RSVD_OK;
   }
   // robust: TSQR (local), then across ranks

@@ -41,6 +41,23 @@ int tf32_n(int Np);
 size_t tf32_split_bytes(int64_t K, int Np);
 cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st);
 
+// ---- CholeskyQR panel path (cholqr.cu)
+// G (Np x Np, ld ldg) = S^T S for S (rows x Np, ld lds): gram_partial over
+// gram_ctas() row chunks into `partial` (>= gram_partial_bytes) + fixed-order reduce.
+int gram_ctas(int64_t rows, int num_sms);
+size_t gram_partial_bytes(int Np, int num_sms);
+cudaError_t launch_gram(const double* S, int64_t lds, int64_t rows, int Np, double* partial, double* G, int ldg,
+                        int num_sms, cudaStream_t st);
+// G = R^T R (l x l leading block of G, ld ldg) and R^-1, by symmetric elimination
+// on [G | I]; R, Rinv npad x npad (ld npad, zero padded; R nullable); flag |= flag_bit
+// on breakdown (pivot <= 1e-13 of its original diagonal, or non-finite).
+cudaError_t launch_chol_aug(const double* G, int ldg, int l, int npad, double* R, double* Rinv, int* flag,
+                            int flag_bit, cudaStream_t st);
+// C (rows x Nout, ld ldc) = S (rows x Np, ld lds) * T (Np x Np, ld ldt); C may alias S.
+// upper: T is upper triangular (skips the zero blocks).
+cudaError_t launch_panel_apply(const double* S, int64_t lds, int64_t rows, int Np, const double* T, int64_t ldt,
+                               double* C, int64_t ldc, int Nout, bool upper, int num_sms, cudaStream_t st);
+
 // ---- K1 Omega (omega.cu)
 cudaError_t launch_omega(int64_t n, int64_t l, int64_t ldo, int64_t ncols_zero, int sdist,
                          uint64_t seed, uint64_t stream, bool f32_round, bool out_f32, void* out,
