@@ -150,9 +150,10 @@ struct Plan {
   const void* A; int64_t lda;
   int64_t m_global;
   // workspace offsets
-  size_t oX, oY, oT, oZ, oPart, oSmall, oColc, oColr, oColp, oSplit, total;
+  size_t oX, oY, oT, oZ, oPart, oSmall, oColc, oColr, oColp, oSplit, oJlog, total;
   bool use_tf32 = false;          // FP32 A on tcgen05 (3-term TF32 split)
   float* split = nullptr;
+  void* jlog = nullptr;
   size_t part_bytes;
   // small-buffer offsets (doubles from oSmall)
   double *X, *Y, *T, *Z, *part, *G, *Rinv, *R1, *R2, *RB, *W, *J, *sigma, *sgn, *colc, *colr, *cols, *colp, *Rsm;
@@ -183,6 +184,7 @@ size_t plan_bytes(rsvd_ctx* ctx, Plan& p) {
   p.oColr = o; o = align256(o + (size_t)p.n * 16);
   p.oColp = o; o = align256(o + colsum_partial_bytes(p.M, p.n) + 256);
   p.oSplit = o; o = align256(o + (p.use_tf32 ? tf32_split_bytes(big, Np) : 0));
+  p.oJlog = o; o = align256(o + jacobi_scratch_bytes(p.l));
   p.total = o;
   return o;
 }
@@ -220,6 +222,7 @@ void bind(rsvd_ctx* ctx, Plan& p) {
   p.sigma = s; s += Np; p.sgn = s; s += Np;
   p.colc = (double*)(b + p.oColc); p.colr = (double*)(b + p.oColr); p.cols = p.colr + p.n; p.colp = (double*)(b + p.oColp);
   p.split = (float*)(b + p.oSplit);
+  p.jlog = (void*)(b + p.oJlog);
 }
 
 // ----------------------------------------------------------------- collectives
@@ -469,7 +472,7 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool robus
   CKS(orth(ctx, p, p.Z, p.n, false, robust, p.RB));
   {
     Prof pr(ctx, 3, 0);
-    CK(launch_jacobi(p.RB, Np, l, p.sigma, p.W, p.J, Np, ctx->flags_dev, ctx->sweeps_dev, ctx->stream));
+    CK(launch_jacobi(p.RB, Np, l, p.sigma, p.W, p.J, Np, ctx->flags_dev, ctx->sweeps_dev, p.jlog, ctx->stream));
   }
   CK(launch_zero_cols(p.J, Np, l, l, Np, ctx->stream));       // keep padding exact zeros
   CK(launch_fill(p.J + (size_t)l * Np, (int64_t)(Np - l) * Np, 0.0, ctx->stream));

@@ -1,0 +1,299 @@
+// jacobi.cu -- economic SVD of the l x l factor (Alg. 5 step 2):
+// one-sided (Hestenes) Jacobi on X = R_B^T, X J = W Sigma (reading R7/R8 of
+// rotate iff |gamma| > tau sqrt(alpha beta), tau = l 2^-52, stop
+// after a sweep without rotation, cap 30 sweeps).
+//
+// B200 design.  The columns are padded to L = 2^ceil(log2 l) (zero columns
+// never rotate).  A sweep is L - 1 parallel steps of L/2 disjoint pairs in a
+// recursive "stationary / travelling" order: at level d the columns form
+// blocks of B = L / 2^d; in step s the k-th column of a block's first half
+// (stationary, kept in registers for the whole level) meets column (k + s) mod
+// B/2 of its second half (travelling, read from and written back to shared
+// memory).  Every pair meets exactly once per sweep (at the level of their
+// highest differing index bit), and only half of X crosses shared memory per
+// step.  Four lanes own a pair.
+//
+// J is not accumulated here: each step's rotations (c, s) go to a log in
+// global memory, and jacobi_apply_j replays the log on the rows of J (rows
+// are independent: the rotations act on columns) in parallel across CTAs, so
+// the sequential kernel moves only X.
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rsvd {
+
+namespace {
+
+__host__ __device__ inline int jac_L(int l) {
+  int L = 2;
+  while (L < l) L <<= 1;
+  return L;
+}
+
+// (stationary p, travelling q) of pair k at a level with half-block h = 2^lh, step s
+__device__ __forceinline__ void jac_pair(int lh, int s, int k, int& p, int& q) {
+  const int h = 1 << lh;
+  const int kk = k & (h - 1), base = (k >> lh) << (lh + 1);
+  p = base + kk;
+  q = base + h + ((kk + s) & (h - 1));
+}
+
+// Rotation (c, s) annihilating gamma for column norms alpha, beta:
+// t = 2 ga sgn(be - al) / (|be - al| + sqrt((be - al)^2 + 4 ga^2)) (the oracle's zeta
+// formula rewritten).  The angle only steers convergence (orthogonality of the
+// rotation comes from c^2 + s^2 = 1), so t is formed in FP32 on operands scaled
+// by a power of two to O(1), and c = (1 + t^2)^-1/2 is refined to FP64 by Newton.
+__device__ __forceinline__ void jac_rot(double al, double be, double ga, double& c, double& sn) {
+  const double dlt = be - al, g2 = 2.0 * ga;
+  const double mx = fmax(fabs(dlt), fabs(g2));
+  const long long ex = (__double_as_longlong(mx) >> 52) & 0x7ff;          // biased exponent
+  const double scale = __longlong_as_double((2046 - ex) << 52);           // ~ 1 / mx (power of two)
+  const float df = (float)(dlt * scale), gf = (float)(g2 * scale);
+  const float tf = __fdividef(df >= 0.f ? gf : -gf, fabsf(df) + sqrtf(fmaf(df, df, gf * gf)));
+  const double t = (double)tf;
+  const double x = fma(t, t, 1.0);
+  double c0 = (double)rsqrtf((float)x);
+  c0 = c0 * fma(-0.5 * x * c0, c0, 1.5);
+  c0 = c0 * fma(-0.5 * x * c0, c0, 1.5);
+  c = c0;
+  sn = c0 * t;
+}
+}  // namespace
+
+size_t jacobi_log_bytes(int l) {
+  const int L = jac_L(l);
+  return (size_t)31 * (L - 1) * (L / 2) * 2 * sizeof(double);
+}
+
+// JG lanes own a column pair; EPL = elements of a column per lane (l <= JG * EPL)
+template <int JG, int EPL>
+__global__ void __launch_bounds__(512, 1)
+jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict__ sigma, double* __restrict__ Wo,
+                int ldo, double2* __restrict__ rlog, int* __restrict__ rank_out, int* flag, int* sweeps_out) {
+  extern __shared__ __align__(16) double Xs[];           // L columns x LDX (column p: Xs + p * LDX)
+  const int L = jac_L(l);
+  constexpr int LDX = JG * EPL + 4;                      // consecutive columns 4 doubles apart mod 32 banks
+  __shared__ int rotated, bad;
+  __shared__ double sg[128];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int npairs = L / 2;
+  const bool act = tid / JG < npairs;                    // lanes beyond the last pair mirror it
+  const int k = act ? tid / JG : npairs - 1, gs = tid % JG;   // pair slot, lane within the pair
+  if (tid == 0) { rotated = 0; bad = 0; }
+  __syncthreads();
+  // X = R^T: column p of X = row p of R (upper: entries i >= p); rows/columns >= l are zero
+  for (int e = tid; e < L * LDX; e += nt) {
+    const int p = e / LDX, i = e - p * LDX;
+    double v = 0.0;
+    if (p < l && i < l && i >= p) v = R[p * ldr + i];
+    if (!isfinite(v)) bad = 1;
+    Xs[e] = v;
+  }
+  __syncthreads();
+  const double tol = (double)l * 0x1.0p-52, tol2 = tol * tol;
+  int levels = 0;
+  while ((1 << levels) < L) ++levels;
+  int sweeps = 0;
+  bool converged = bad != 0;
+  int64_t gstep = 0;                                     // global step index into the log
+  for (int sweep = 0; sweep <= 30 && !converged; ++sweep) {
+    for (int d = 0; d < levels; ++d) {
+      const int lh = levels - 1 - d, h = 1 << lh;
+      int p = 0, q = 0;
+      double xs[EPL], xt[EPL];
+      {
+        jac_pair(lh, 0, k, p, q);
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) xs[e] = Xs[p * LDX + gs + JG * e];
+      }
+      for (int s = 0; s < h; ++s, ++gstep) {
+        double c = 1.0, sn = 0.0;
+        {
+          jac_pair(lh, s, k, p, q);
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) xt[e] = Xs[q * LDX + gs + JG * e];
+          constexpr int NCH = EPL >= 4 ? 4 : EPL;        // independent accumulation chains
+          double a[NCH], b[NCH], g[NCH];
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) a[c] = b[c] = g[c] = 0.0;
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) {
+            a[e % NCH] = fma(xs[e], xs[e], a[e % NCH]);
+            b[e % NCH] = fma(xt[e], xt[e], b[e % NCH]);
+            g[e % NCH] = fma(xs[e], xt[e], g[e % NCH]);
+          }
+#pragma unroll
+          for (int c = 1; c < NCH; ++c) { a[0] += a[c]; b[0] += b[c]; g[0] += g[c]; }
+          double al = a[0], be = b[0], ga = g[0];
+#pragma unroll
+          for (int o = JG / 2; o > 0; o >>= 1) {
+            al += __shfl_xor_sync(0xffffffffu, al, o);
+            be += __shfl_xor_sync(0xffffffffu, be, o);
+            ga += __shfl_xor_sync(0xffffffffu, ga, o);
+          }
+          if (ga * ga > tol2 * (al * be)) {
+            jac_rot(al, be, ga, c, sn);
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) {
+              const double u = xs[e], v = xt[e];
+              xs[e] = c * u - sn * v;
+              xt[e] = sn * u + c * v;
+            }
+            if (gs == 0 && act) rotated = 1;
+          }
+          if (act) {
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) Xs[q * LDX + gs + JG * e] = xt[e];
+            if (gs == 0) rlog[gstep * npairs + k] = make_double2(c, sn);
+          }
+        }
+        __syncthreads();                                 // travelling columns published
+      }
+      if (act) {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) Xs[p * LDX + gs + JG * e] = xs[e];
+      }
+      __syncthreads();
+    }
+    const bool any = rotated != 0;
+    __syncthreads();
+    if (tid == 0) rotated = 0;
+    if (!any) converged = true;
+    else ++sweeps;
+    __syncthreads();
+  }
+  // sigma_p = ||x_p||, stable descending ranks, W(:, rank) = x_p / sigma_p
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  for (int p = warp; p < l; p += nw) {
+    double s = 0.0;
+    for (int i = lane; i < l; i += 32) s = fma(Xs[p * LDX + i], Xs[p * LDX + i], s);
+    s = warp_sum(s);
+    if (lane == 0) sg[p] = sqrt(s);
+  }
+  __syncthreads();
+  for (int p = warp; p < l; p += nw) {
+    int rk = 0;
+    const double sp = sg[p];
+    for (int q = lane; q < l; q += 32) rk += (sg[q] > sp) || (sg[q] == sp && q < p);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
+    if (lane == 0) { sigma[rk] = sp; rank_out[p] = rk; }
+    const double inv = sp > 0.0 ? 1.0 / sp : 1.0;
+    for (int i = lane; i < l; i += 32) Wo[i * ldo + rk] = Xs[p * LDX + i] * inv;
+  }
+  if (tid == 0) {
+    if (!converged) atomicOr(flag, 2);
+    if (bad) atomicOr(flag, 4);
+    if (sweeps_out) *sweeps_out = sweeps;
+    rank_out[128] = sweeps;                              // rotations logged for `sweeps` sweeps
+  }
+}
+
+// J = product of the logged rotations (identity start), one warp per row of J
+// (4 rows per CTA); the log is staged through shared memory in chunks of
+// JA_CH steps (cp.async, double-buffered) shared by the CTA's warps.
+// Jo(i, rank[p]) = J(i, p).
+constexpr int JA_CH = 16;
+
+__global__ void __launch_bounds__(128)
+jacobi_apply_j(const double2* __restrict__ rlog, const int* __restrict__ rank, int l, double* __restrict__ Jo,
+               int ldo) {
+  __shared__ double rows[4][129];
+  __shared__ __align__(16) double2 buf[2][JA_CH * 64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 4 + warp;
+  const int L = jac_L(l), npairs = L / 2;
+  double* row = rows[warp];
+  for (int p = lane; p < L; p += 32) row[p] = (p == i) ? 1.0 : 0.0;
+  const int nsweeps = rank[128];
+  int levels = 0;
+  while ((1 << levels) < L) ++levels;
+  const int64_t total = (int64_t)nsweeps * (L - 1);
+  const int64_t nch = ceil_div(total, JA_CH);
+  auto load = [&](int b, int64_t ch) {
+    const int64_t s0 = ch * JA_CH;
+    const int64_t n = min((int64_t)JA_CH, total - s0) * npairs;
+    const double2* src = rlog + s0 * npairs;
+    for (int e = threadIdx.x; e < n; e += 128) cp_async16(&buf[b][e], src + e, 16);
+  };
+  if (nch > 0) load(0, 0);
+  cp_async_commit();
+  int lh = levels - 1, s = 0;
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) load((int)((ch + 1) & 1), ch + 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double2* cb = buf[ch & 1];
+    const int nst = (int)min((int64_t)JA_CH, total - ch * JA_CH);
+    for (int st = 0; st < nst; ++st) {
+      for (int k = lane; k < npairs; k += 32) {
+        int p, q;
+        jac_pair(lh, s, k, p, q);
+        const double2 cs = cb[st * npairs + k];
+        const double u = row[p], v = row[q];
+        row[p] = cs.x * u - cs.y * v;
+        row[q] = cs.y * u + cs.x * v;
+      }
+      __syncwarp();
+      if (++s == (1 << lh)) {
+        s = 0;
+        if (--lh < 0) lh = levels - 1;
+      }
+    }
+    __syncthreads();                                     // buffer reused by chunk ch + 2
+  }
+  cp_async_wait<0>();
+  if (i < l)
+    for (int p = lane; p < l; p += 32) Jo[i * ldo + rank[p]] = row[p];
+}
+
+int g_jacobi_lanes = 0;   // lanes per column pair (4, 8, 16; 0: 4 for L <= 64, else 8; tools/bench_jacobi)
+
+cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double* W, double* J, int ldo,
+                          int* flag, int* sweeps, void* scratch, cudaStream_t st) {
+  if (l < 1 || l > 128) return cudaErrorInvalidValue;
+  const int L = jac_L(l);
+  double2* rlog = reinterpret_cast<double2*>(scratch);
+  int* rank = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + jacobi_log_bytes(l));
+  const int JGv = g_jacobi_lanes ? g_jacobi_lanes : (L <= 64 ? 4 : 8);
+  const int threads = (int)round_up((int64_t)(L / 2) * JGv, 32);
+  const int epl_need = (l + JGv - 1) / JGv;
+  cudaError_t e = cudaSuccess;
+#define RSVD_JX(JG, EPL)                                                                                   \
+  {                                                                                                       \
+    const int ldx = JG * EPL + 4;                                                                         \
+    const size_t smem = (size_t)L * ldx * sizeof(double);                                                 \
+    static bool attr = false;                                                                             \
+    if (!attr) {                                                                                          \
+      e = cudaFuncSetAttribute(jacobi_x_kernel<JG, EPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+      if (e != cudaSuccess) return e;                                                                     \
+      attr = true;                                                                                        \
+    }                                                                                                     \
+    jacobi_x_kernel<JG, EPL><<<1, threads, smem, st>>>(R, ldr, l, sigma, W, ldo, rlog, rank, flag, sweeps); \
+  }
+#define RSVD_JX_EPL(JG)                  \
+  if (epl_need <= 1) RSVD_JX(JG, 1)      \
+  else if (epl_need <= 2) RSVD_JX(JG, 2) \
+  else if (epl_need <= 4) RSVD_JX(JG, 4) \
+  else if (epl_need <= 8) RSVD_JX(JG, 8) \
+  else if (epl_need <= 16) RSVD_JX(JG, 16) \
+  else RSVD_JX(JG, 32)
+  if (JGv == 4) { RSVD_JX_EPL(4) }
+  else if (JGv == 16) { RSVD_JX_EPL(16) }
+  else { RSVD_JX_EPL(8) }
+#undef RSVD_JX_EPL
+#undef RSVD_JX
+  ++g_kernel_launches;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  jacobi_apply_j<<<(unsigned)ceil_div(l, 4), 128, 0, st>>>(rlog, rank, l, J, ldo);
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+size_t jacobi_scratch_bytes(int l) { return jacobi_log_bytes(l) + 256 * sizeof(int); }
+
+}  // namespace rsvd

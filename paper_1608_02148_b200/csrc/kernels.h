@@ -90,11 +90,13 @@ cudaError_t launch_hqr_leaves(double* Y, int64_t ldy, int64_t M, int l, int64_t 
 cudaError_t launch_tsqr_combine(double* Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
                                 const double* S, int64_t lds, cudaStream_t st);
 
-// One-sided Jacobi SVD of X = R^T (R upper l x l, ld ldr): X J = W Sigma.
+// One-sided Jacobi SVD of X = R^T (R upper l x l, ld ldr): X J = W Sigma (jacobi.cu).
 // Outputs: sigma (l, descending), W (l x l, ld ldo) = U~, J (l x l, ld ldo).
-// flag |= 2 if the sweep cap was hit, 4 on non-finite input.
+// flag |= 2 if the sweep cap was hit, 4 on non-finite input.  scratch: device
+// buffer of jacobi_scratch_bytes(l) (rotation log + ranks).
+size_t jacobi_scratch_bytes(int l);
 cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double* W, double* J,
-                          int ldo, int* flag, int* sweeps, cudaStream_t st);
+                          int ldo, int* flag, int* sweeps, void* scratch, cudaStream_t st);
 
 // Sign convention (reading R9): sgn[i] = -1 iff the largest-|.| entry of V(:,i)
 // (lowest index on ties) is negative.

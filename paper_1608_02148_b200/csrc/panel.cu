@@ -10,10 +10,6 @@
 //                single-CTA panel QR for small panels and the leaves of TSQR.
 //                Robust for exactly rank-deficient panels (config 1).
 //  * tsqr_combine: Q_leaf <- Q_leaf * S_leaf, the downward sweep of TSQR.
-//  * jacobi:     one-sided (Hestenes) Jacobi SVD of R_B^T in shared memory,
-//                parallel round-robin ordering, one warp per column pair with
-//                warp-shuffle dot products; economic SVD of B (Alg. 5 step 2,
-//                P:628) via B^T = Q_B R_B.
 //  * sign / copy / column statistics helpers.
 #include <math.h>
 
@@ -449,186 +445,6 @@ cudaError_t launch_tsqr_combine(double* Y, int64_t ldy, int64_t M, int l, int64_
   cudaError_t e = set_smem((const void*)tsqr_combine_kernel, smem);
   if (e != cudaSuccess) return e;
   tsqr_combine_kernel<<<(unsigned)nleaves, 512, smem, st>>>(Y, ldy, M, l, nleaves, S, lds); ++g_kernel_launches;
-  return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------ one-sided Jacobi
-#ifndef JPROBE
-#define JPROBE(k)
-#endif
-template <int GL, bool FASTT>
-__global__ void __launch_bounds__(1024, 1) jacobi_kernel(const double* __restrict__ R, int ldr, int l,
-                                                         double* __restrict__ sigma, double* __restrict__ Wo,
-                                                         double* __restrict__ Jo, int ldo, int* flag,
-                                                         int* sweeps_out) {
-  // One-sided Jacobi on X = R^T: a pair (p, q) of columns is handled by a
-  // group of GL lanes (32/GL pairs per warp), so the per-step instruction
-  // count grows with the matrix work, not with the number of pairs.
-  extern __shared__ double sm[];
-  double* X = sm;                  // X[p*l + i] = column p of X = R^T  (= row p of R)
-  double* J = X + l * l;           // J[p*l + i] = column p of J
-  __shared__ int rotated, bad;
-  __shared__ double sg[128];
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  const int gsub = lane % GL, gid = warp * (32 / GL) + lane / GL, ngroups = nw * (32 / GL);
-  if (tid == 0) { rotated = 0; bad = 0; }
-  __syncthreads();
-  for (int e = tid; e < l * l; e += nt) {
-    const int p = e / l, i = e - p * l;
-    const double v = (i >= p) ? R[p * ldr + i] : 0.0;   // R upper: row p, col i
-    if (!isfinite(v)) bad = 1;
-    X[e] = v;
-    J[e] = (p == i) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  const double tol = (double)l * 0x1.0p-52, tol2 = tol * tol;
-  const int L = l + (l & 1);       // round-robin over L players (a dummy when l is odd)
-  const int half = L / 2, Lm1 = L - 1;
-  int sweeps = 0;
-  bool converged = (bad != 0);
-  for (int sweep = 0; sweep <= 30 && !converged; ++sweep) {
-    for (int s = 0; s < Lm1; ++s) {
-      for (int pb = 0; pb < half; pb += ngroups) {          // warp-uniform trip count
-        const int pi = pb + gid;
-        int p = 0, q = 0;
-        bool act = pi < half;
-        if (act) {
-          // circle method: player 0 fixed, players 1..L-1 rotate with s
-          int x1 = pi - 1 + s; if (x1 >= Lm1) x1 -= Lm1;
-          int x2 = Lm1 - 1 - pi + s; if (x2 >= Lm1) x2 -= Lm1;
-          const int a = (pi == 0) ? 0 : 1 + x1, bq = 1 + x2;
-          p = a < bq ? a : bq;
-          q = a < bq ? bq : a;
-          act = q < l;                                     // dummy player
-        }
-        JPROBE(0)
-        double al = 0.0, be = 0.0, ga = 0.0;
-        double* xp = X + p * l;
-        double* xq = X + q * l;
-        if (act) {
-          for (int i = gsub; i < l; i += GL) {
-            const double u = xp[i], v = xq[i];
-            al = fma(u, u, al); be = fma(v, v, be); ga = fma(u, v, ga);
-          }
-        }
-#pragma unroll
-        for (int o = GL / 2; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          ga += __shfl_xor_sync(0xffffffffu, ga, o);
-        }
-        JPROBE(1)
-        if (act && ga * ga > tol2 * (al * be)) {
-          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga), written as
-          // t = 2 ga sgn(be - al) / (|be - al| + sqrt((be - al)^2 + 4 ga^2)): one sqrt, one div.
-          const double dlt = be - al;
-          double t, c;
-          if (FASTT) {
-            // The angle only steers convergence; orthogonality of the rotation comes from
-            // c^2 + s^2 = 1, so t may be computed in FP32 (on operands scaled to O(1))
-            // while c = (1 + t^2)^-1/2 is refined to full FP64 precision by Newton steps.
-            const double mx = fmax(fabs(dlt), fabs(2.0 * ga));
-            const int ex = ilogb(mx);
-            const float df = (float)scalbn(dlt, -ex), gf = (float)scalbn(2.0 * ga, -ex);
-            const float tf = (df >= 0.f ? gf : -gf) / (fabsf(df) + sqrtf(fmaf(df, df, gf * gf)));
-            t = (double)tf;
-            const double x = fma(t, t, 1.0);
-            double c0 = (double)rsqrtf((float)x);
-            c0 = c0 * fma(-0.5 * x * c0, c0, 1.5);
-            c0 = c0 * fma(-0.5 * x * c0, c0, 1.5);
-            c = c0;
-          } else {
-            t = (dlt >= 0.0 ? 2.0 * ga : -2.0 * ga) / (fabs(dlt) + sqrt(fma(dlt, dlt, 4.0 * ga * ga)));
-            c = rsqrt(fma(t, t, 1.0));
-          }
-          const double sn = c * t;
-          JPROBE(2)
-          double* jp = J + p * l;
-          double* jq = J + q * l;
-          for (int i = gsub; i < l; i += GL) {
-            const double u = xp[i], v = xq[i];
-            xp[i] = c * u - sn * v;
-            xq[i] = sn * u + c * v;
-            const double ju = jp[i], jv = jq[i];
-            jp[i] = c * ju - sn * jv;
-            jq[i] = sn * ju + c * jv;
-          }
-          if (gsub == 0) rotated = 1;
-        }
-        JPROBE(3)
-      }
-      __syncthreads();
-      JPROBE(4)
-    }
-    const bool any = rotated != 0;
-    __syncthreads();
-    if (tid == 0) rotated = 0;
-    if (!any) converged = true;
-    else ++sweeps;
-    __syncthreads();
-  }
-  // sigma, stable descending order
-  for (int p = warp; p < l; p += nw) {
-    double s = 0.0;
-    for (int i = lane; i < l; i += 32) s = fma(X[p * l + i], X[p * l + i], s);
-    s = warp_sum(s);
-    if (lane == 0) sg[p] = sqrt(s);
-  }
-  __syncthreads();
-  for (int p = warp; p < l; p += nw) {
-    int rank = 0;
-    const double sp = sg[p];
-    for (int q = lane; q < l; q += 32) rank += (sg[q] > sp) || (sg[q] == sp && q < p);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
-    if (lane == 0) sigma[rank] = sp;
-    const double inv = sp > 0.0 ? 1.0 / sp : 1.0;
-    for (int i = lane; i < l; i += 32) {
-      Wo[i * ldo + rank] = X[p * l + i] * inv;
-      Jo[i * ldo + rank] = J[p * l + i];
-    }
-  }
-  if (tid == 0) {
-    if (!converged) atomicOr(flag, 2);
-    if (bad) atomicOr(flag, 4);
-    if (sweeps_out) *sweeps_out = sweeps;
-  }
-}
-
-int g_jacobi_lanes = 16;  // lanes per column pair (tunable; tools/bench_small)
-bool g_jacobi_fastt = true;
-
-cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double* W, double* J, int ldo,
-                          int* flag, int* sweeps, cudaStream_t st) {
-  const size_t smem = 2 * (size_t)l * l * sizeof(double);
-  if (l > 120 || smem > (size_t)SMEM_OPTIN - 2048) return cudaErrorInvalidValue;
-  const int L = l + (l & 1);
-  const int gl = g_jacobi_lanes;
-  const int groups_per_warp = 32 / gl;
-  int warps = (int)ceil_div(L / 2, groups_per_warp);
-  if (warps < 1) warps = 1;
-  if (warps > 32) warps = 32;
-  cudaError_t e;
-#define RSVD_JAC(G)                                                                          \
-  if (g_jacobi_fastt) {                                                                     \
-    e = set_smem((const void*)jacobi_kernel<G, true>, smem);                                \
-    if (e != cudaSuccess) return e;                                                         \
-    jacobi_kernel<G, true><<<1, 32 * warps, smem, st>>>(R, ldr, l, sigma, W, J, ldo, flag, sweeps); \
-  } else {                                                                                  \
-    e = set_smem((const void*)jacobi_kernel<G, false>, smem);                               \
-    if (e != cudaSuccess) return e;                                                         \
-    jacobi_kernel<G, false><<<1, 32 * warps, smem, st>>>(R, ldr, l, sigma, W, J, ldo, flag, sweeps); \
-  }
-  switch (gl) {
-    case 1: RSVD_JAC(1) break;
-    case 2: RSVD_JAC(2) break;
-    case 4: RSVD_JAC(4) break;
-    case 8: RSVD_JAC(8) break;
-    case 16: RSVD_JAC(16) break;
-    default: RSVD_JAC(32) break;
-  }
-#undef RSVD_JAC
-  ++g_kernel_launches;
   return cudaGetLastError();
 }
 

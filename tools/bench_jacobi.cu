@@ -1,0 +1,67 @@
+// Microbenchmark + self-check of the one-sided Jacobi SVD (jacobi.cu):
+// X = R^T, X J = W Sigma.  Checks W^T W = I, J^T J = I, X J = W Sigma, sorted
+// sigma.  Not product code.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude -o tools/bench_jacobi tools/bench_jacobi.cu
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include "../paper_1608_02148_b200/csrc/jacobi.cu"
+namespace rsvd { int64_t g_kernel_launches = 0; }
+using namespace rsvd;
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s @%d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
+
+template <typename F> float timeit(F f, int reps) {
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  f(); CK(cudaDeviceSynchronize());
+  cudaEventRecord(a); for (int r = 0; r < reps; ++r) f(); cudaEventRecord(b); cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b); CK(cudaGetLastError()); return ms * 1000.f / reps;
+}
+
+int main() {
+  int* flag; CK(cudaMalloc(&flag, 64));
+  int* sw; CK(cudaMalloc(&sw, 64));
+  for (int l : {1, 2, 7, 20, 30, 60, 64, 100, 120, 128}) {
+    const int ld = (l + 15) / 16 * 16;
+    std::vector<double> R(ld * ld, 0.0);
+    srand(l);
+    for (int i = 0; i < l; ++i)
+      for (int j = i; j < l; ++j)
+        R[i * ld + j] = (i == j) ? std::exp(-i / 20.0) : 0.3 * ((rand() % 2001) / 1000.0 - 1.0) * std::exp(-i / 20.0);
+    double *dR, *sig, *W, *J; void* scr;
+    CK(cudaMalloc(&dR, ld * ld * 8)); CK(cudaMalloc(&sig, ld * 8)); CK(cudaMalloc(&W, ld * ld * 8));
+    CK(cudaMalloc(&J, ld * ld * 8)); CK(cudaMalloc(&scr, jacobi_scratch_bytes(l)));
+    CK(cudaMemcpy(dR, R.data(), ld * ld * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemset(flag, 0, 64));
+    for (int jg : {4, 8}) {
+      g_jacobi_lanes = jg;
+      float tj = timeit([&] { launch_jacobi(dR, ld, l, sig, W, J, ld, flag, sw, scr, 0); }, 10);
+      printf("    lanes/pair %2d: %8.2f us\n", jg, tj);
+    }
+    g_jacobi_lanes = 0;
+    float t = timeit([&] { launch_jacobi(dR, ld, l, sig, W, J, ld, flag, sw, scr, 0); }, 10);
+    int sweeps, fl;
+    CK(cudaMemcpy(&sweeps, sw, 4, cudaMemcpyDeviceToHost)); CK(cudaMemcpy(&fl, flag, 4, cudaMemcpyDeviceToHost));
+    std::vector<double> hs(ld), hW(ld * ld), hJ(ld * ld);
+    CK(cudaMemcpy(hs.data(), sig, ld * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hW.data(), W, ld * ld * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hJ.data(), J, ld * ld * 8, cudaMemcpyDeviceToHost));
+    double ew = 0, ej = 0, er = 0, srt = 0;
+    for (int a = 0; a < l; ++a)
+      for (int b = 0; b < l; ++b) {
+        double sw_ = 0, sj = 0;
+        for (int i = 0; i < l; ++i) { sw_ += hW[i * ld + a] * hW[i * ld + b]; sj += hJ[i * ld + a] * hJ[i * ld + b]; }
+        ew = std::fmax(ew, std::fabs(sw_ - (a == b))); ej = std::fmax(ej, std::fabs(sj - (a == b)));
+      }
+    for (int i = 0; i < l; ++i)            // X J = W Sigma, X = R^T: X[i][p] = R[p][i]
+      for (int c = 0; c < l; ++c) {
+        double s = 0; for (int p = 0; p < l; ++p) s += R[p * ld + i] * hJ[p * ld + c];
+        er = std::fmax(er, std::fabs(s - hW[i * ld + c] * hs[c]));
+      }
+    for (int i = 1; i < l; ++i) if (hs[i] > hs[i - 1]) srt = 1;
+    printf("l %3d: jacobi %8.2f us  sweeps %d flag %d | |WtW-I| %.1e |JtJ-I| %.1e |XJ-WS| %.1e unsorted %d s0 %.6f s_l %.3e\n",
+           l, t, sweeps, fl, ew, ej, er, (int)srt, hs[0], hs[l - 1]);
+    cudaFree(dR); cudaFree(sig); cudaFree(W); cudaFree(J); cudaFree(scr);
+  }
+  return 0;
+}
