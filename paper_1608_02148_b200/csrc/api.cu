@@ -71,6 +71,8 @@ struct rsvd_ctx {
   int last_sweeps = 0;
   bool fp32_tcgen05 = true;       // RSVD_FP32_PATH=dmma selects the FP64-DMMA path for FP32 inputs
   int last_robust = 0;
+  unsigned* gemm_flags = nullptr; // stream-K fix-up flags (kMaxGrid, zeroed at creation)
+  unsigned gemm_epoch = 0;
 };
 
 namespace {
@@ -247,6 +249,7 @@ rsvd_status pass_tf32(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, doubl
   t.A = (const float*)p.A; t.lda = p.lda; t.trans = trans;
   t.B = B; t.ldb = p.Np; t.C = C; t.ldc = p.Np; t.P = p.part; t.split = p.split;
   t.M = M; t.K = K; t.N = p.Np; t.Nout = p.Np; t.grid = ctx->num_sms;
+  t.flags = ctx->gemm_flags; t.epoch = ++ctx->gemm_epoch;
   CK(tf32_pass(t, ctx->stream));
   return RSVD_OK;
 }
@@ -263,6 +266,7 @@ rsvd_status pass_ax(rsvd_ctx* ctx, Plan& p, const double* X, double* Y, bool cen
   g.rscale = p.scaled ? p.colr : nullptr;
   g.M = p.M; g.K = p.n; g.N = p.Np; g.Nout = p.Np;
   g.grid = ctx->num_sms;
+  g.flags = ctx->gemm_flags; g.epoch = ++ctx->gemm_epoch;
   const double bytes = (double)p.M * p.n * (p.f32 ? 4 : 8);
   Prof pr(ctx, 0, bytes);
   CK(gemm_pass(g, ctx->stream));
@@ -285,6 +289,7 @@ rsvd_status pass_atx(rsvd_ctx* ctx, Plan& p, const double* Q, double* Z, bool ce
   g.rscale = p.scaled ? p.colr : nullptr;
   g.M = p.n; g.K = p.M; g.N = p.Np; g.Nout = p.Np;
   g.grid = ctx->num_sms;
+  g.flags = ctx->gemm_flags; g.epoch = ++ctx->gemm_epoch;
   const double bytes = (double)p.M * p.n * (p.f32 ? 4 : 8);
   {
     Prof pr(ctx, 1, bytes);
@@ -562,6 +567,8 @@ rsvd_status rsvd_create(rsvd_ctx** out, int device, void* stream) {
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->flags_host, 16 * sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->hbuf, 1024 * sizeof(double));
   if (e == cudaSuccess) ctx->sweeps_dev = ctx->flags_dev + 8;
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->gemm_flags, 4096 * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(ctx->gemm_flags, 0, 4096 * sizeof(unsigned));
   {
     const char* fp = getenv("RSVD_FP32_PATH");
     if (fp && strcmp(fp, "dmma") == 0) ctx->fp32_tcgen05 = false;
@@ -586,6 +593,7 @@ rsvd_status rsvd_destroy(rsvd_ctx* ctx) {
   cudaFreeHost(ctx->flags_host);
   cudaFreeHost(ctx->hbuf);
   cudaFree(ctx->ws3);
+  cudaFree(ctx->gemm_flags);
   delete ctx;
   return RSVD_OK;
 }

@@ -15,13 +15,14 @@
 // pool (profiles/peaks_box.json).  A work unit is (row block of BM = 128 rows
 // of C, k-tile of BK = 32); the units are split evenly over a persistent grid
 // of one CTA per SM ("stream-K"), so there is no wave quantisation whatever
-// the shape.  A CTA streams its contiguous range of units through a 3-stage
+// the shape; row blocks split between CTAs are summed inside the kernel.  A CTA streams its contiguous range of units through a 3-stage
 // cp.async (LDGSTS) shared-memory ring with zero-fill for ragged edges; the 8
 // warps = 4 (M, 32 rows) x 2 (N halves) keep all N <= 128 columns of C in
 // registers and double-buffer their DMMA fragments.  A row block finished
 // entirely inside one CTA is written directly; a row block shared by several
-// CTAs leaves per-CTA partials that gemm_streamk_fixup sums in CTA order
-// (deterministic, no FP64 atomics: SURVEY H4).  A is read from HBM exactly
+// CTAs is summed in CTA order by the CTA holding its first k-tile, from
+// partials the later CTAs publish with release/acquire flags (deterministic,
+// no FP64 atomics: SURVEY H4).  A is read from HBM exactly
 // once per pass; B (Omega / Q, <= 5 MB) is re-read from L2.
 #include "common.cuh"
 #include "kernels.h"
@@ -48,7 +49,8 @@ struct GemmArgs {
   const void* A; int64_t lda;
   const double* B; int64_t ldb;
   double* C; int64_t ldc;           // final output
-  double* P;                        // stream-K partials [grid][2][BM][N]
+  double* P;                        // stream-K partials [grid][BM][N] (a CTA's leading segment)
+  unsigned* flags; unsigned epoch;  // per-CTA "partial published" flags (value = launch epoch)
   const double* c; const double* rs;
   int64_t M, K; int N, Nout;
   int64_t KT, units;                // k-tiles per row block, total units
@@ -165,8 +167,54 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
     }
   };
 
-  auto epilogue = [&](int64_t mb, bool full, int slot) {
+  // In-kernel stream-K fix-up (deterministic, no FP64 atomics: SURVEY H4).  A
+  // row-block segment is (i) the whole row block -> written directly; (ii) a
+  // continuation (starts after the row block's first k-tile; always the CTA's
+  // first segment) -> partial P[cta] + release flag; (iii) the head of a row
+  // block that continues into later CTAs (always the CTA's last segment) ->
+  // acquire the later CTAs' partials in CTA order, add, write.  Waits only
+  // point to higher CTAs, which publish their partial first: no deadlock with
+  // the whole grid resident (grid <= #SMs, one CTA per SM).
+  auto epilogue = [&](int64_t mb, int64_t seg_start, int64_t seg_end) {
     const int64_t m0 = mb * BM;
+    const int64_t rb_lo = mb * KT, rb_hi = rb_lo + KT;
+    if (seg_start > rb_lo) {
+      double* pb = g.P + (int64_t)blockIdx.x * BM * N;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int rloc = wm * 32 + i * 8 + gq;
+#pragma unroll
+        for (int j = 0; j < TMAX; ++j) {
+          const int col = (tile_begin + j) * 8 + 2 * tq;
+          *reinterpret_cast<double2*>(pb + rloc * N + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+          acc[i][j][0] = acc[i][j][1] = 0.0;
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(g.epoch) : "memory");
+      return;
+    }
+    if (seg_end < rb_hi) {
+      for (int c = blockIdx.x + 1; c < g.grid && unit_lo(g.units, g.grid, c) < rb_hi; ++c) {
+        unsigned f;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(g.flags + c) : "memory");
+        } while (f != g.epoch);
+        const double* pb = g.P + (int64_t)c * BM * N;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rloc = wm * 32 + i * 8 + gq;
+#pragma unroll
+          for (int j = 0; j < TMAX; ++j) {
+            const int col = (tile_begin + j) * 8 + 2 * tq;
+            const double2 v = *reinterpret_cast<const double2*>(pb + rloc * N + col);
+            acc[i][j][0] += v.x;
+            acc[i][j][1] += v.y;
+          }
+        }
+      }
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int rloc = wm * 32 + i * 8 + gq;
@@ -174,14 +222,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
 #pragma unroll
       for (int j = 0; j < TMAX; ++j) {
         const int col = (tile_begin + j) * 8 + 2 * tq;
-        if (full) {
-          if (gm < g.M) {
-            if (col < g.Nout) g.C[gm * g.ldc + col] = acc[i][j][0];
-            if (col + 1 < g.Nout) g.C[gm * g.ldc + col + 1] = acc[i][j][1];
-          }
-        } else {
-          double* p = g.P + (((int64_t)blockIdx.x * 2 + slot) * BM + rloc) * N + col;
-          *reinterpret_cast<double2*>(p) = make_double2(acc[i][j][0], acc[i][j][1]);
+        if (gm < g.M) {
+          if (col < g.Nout) g.C[gm * g.ldc + col] = acc[i][j][0];
+          if (col + 1 < g.Nout) g.C[gm * g.ldc + col + 1] = acc[i][j][1];
         }
         acc[i][j][0] = acc[i][j][1] = 0.0;
       }
@@ -249,73 +292,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
     const int64_t mb = u / KT, kt = u - mb * KT;
     if (kt == KT - 1 || it == nun - 1) {
       const int64_t seg_start = (mb * KT > u_lo) ? mb * KT : u_lo;
-      const bool full = (seg_start == mb * KT) && (kt == KT - 1);
-      const int slot = (mb == u_lo / KT) ? 0 : 1;
-      epilogue(mb, full, slot);
+      epilogue(mb, seg_start, u + 1);
       if (CENT && TRANS && it + 1 < nun) set_rows((mb + 1) * BM);
     }
   }
   cp_async_wait<0>();
-}
-
-// Stream-K fix-up: for every row block split between CTAs, sum the partials
-// of the CTAs that touched it and write C.  Block column b-1 handles the
-// boundary at the start of CTA b (only the first boundary inside a row block
-// does the work).  T consecutive lanes share one output element, each summing
-// a strided subset of the contributors, then a fixed xor-shuffle tree
-// combines them: the summation order depends only on the shape
-// (deterministic), and every lane has only a few independent loads in flight.
-__global__ void gemm_streamk_fixup(GemmArgs g, int T) {
-  __shared__ int s_first, s_last;
-  __shared__ unsigned char s_slot[1024];
-  const int b = blockIdx.x + 1;
-  const int64_t ub = unit_lo(g.units, g.grid, b);
-  if (ub >= g.units || ub % g.KT == 0) return;                 // boundary on a row-block edge
-  const int64_t mb = ub / g.KT;
-  if (unit_lo(g.units, g.grid, b - 1) > mb * g.KT) return;     // not the first boundary in mb
-  if (threadIdx.x == 0) {
-    int c_last = b;
-    const int64_t last_unit = (mb + 1) * g.KT - 1;
-    while (c_last + 1 < g.grid && unit_lo(g.units, g.grid, c_last + 1) <= last_unit) ++c_last;
-    s_first = b - 1;
-    s_last = c_last;
-  }
-  __syncthreads();
-  const int c_first = s_first, c_last = s_last;
-  for (int c = c_first + threadIdx.x; c <= c_last; c += blockDim.x)
-    s_slot[c - c_first] = (mb == unit_lo(g.units, g.grid, c) / g.KT) ? 0 : 1;
-  __syncthreads();
-  const int N = g.N;
-  const int64_t m0 = mb * BM;
-  const int E = BM * N, epb = blockDim.x / T;
-  const int t = threadIdx.x % T;
-  for (int e0 = blockIdx.y * epb; e0 < E; e0 += gridDim.y * epb) {   // warp-uniform trip count
-    const int e = e0 + threadIdx.x / T;
-    const int r = e / N, col = e - r * N;
-    const bool ok = e < E && m0 + r < g.M && col < g.Nout;
-    double s = 0.0;
-    if (ok)
-      for (int c = c_first + t; c <= c_last; c += T)
-        s += g.P[(((int64_t)c * 2 + s_slot[c - c_first]) * BM + r) * N + col];
-    for (int o = T >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (ok && t == 0) g.C[(m0 + r) * g.ldc + col] = s;
-  }
-}
-
-// fix-up for partials produced by another pass kernel with the same stream-K
-// partition (the tcgen05 FP32 path)
-cudaError_t gemm_streamk_fixup_launch(double* C, int64_t ldc, double* P, int64_t M, int N, int Nout, int64_t KT,
-                                      int64_t units, int grid, cudaStream_t st) {
-  GemmArgs g{};
-  g.C = C; g.ldc = ldc; g.P = P; g.M = M; g.N = N; g.Nout = Nout; g.KT = KT; g.units = units; g.grid = grid;
-  const int64_t contributors = ceil_div(KT * (int64_t)grid, units) + 1;
-  int T = 1;
-  while (T < 32 && T * 4 < contributors) T <<= 1;
-  int ych = (int)ceil_div((int64_t)BM * N, 256 / T);
-  if (ych > 64) ych = 64;
-  gemm_streamk_fixup<<<dim3(grid - 1, ych), 256, 0, st>>>(g, T);
-  ++g_kernel_launches;
-  return cudaGetLastError();
 }
 
 template <typename TA, bool TRANS, int TMAX>
@@ -361,7 +342,7 @@ int gemm_choose_grid(int64_t M, int64_t K, int num_sms) {
   return (int)gsz;
 }
 
-size_t gemm_partial_bytes(int N, int grid) { return (size_t)grid * 2 * BM * (size_t)N * sizeof(double); }
+size_t gemm_partial_bytes(int N, int grid) { return (size_t)grid * BM * (size_t)N * sizeof(double); }
 
 cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st) {
   if (c.N % 16 != 0 || c.N > NMAX || c.N < 16 || (c.ldb & 1)) return cudaErrorInvalidValue;
@@ -369,6 +350,7 @@ cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st) {
   GemmArgs g;
   g.A = c.A; g.lda = c.lda; g.B = c.B; g.ldb = c.ldb; g.C = c.C; g.ldc = c.ldc; g.P = c.P;
   g.c = c.center; g.rs = c.rscale; g.M = c.M; g.K = c.K; g.N = c.N; g.Nout = c.Nout;
+  g.flags = c.flags; g.epoch = c.epoch;
   g.KT = ceil_div(c.K, BK);
   g.units = ceil_div(c.M, BM) * g.KT;
   g.grid = gemm_choose_grid(c.M, c.K, c.grid > 0 ? c.grid : 148);
@@ -376,24 +358,12 @@ cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st) {
     const size_t es = c.a_f32 ? 4 : 8;
     g.a_vec = ((uintptr_t)c.A % 16 == 0) && ((c.lda * es) % 16 == 0);
   }
-  if (g.grid > 1 && c.P == nullptr) return cudaErrorInvalidValue;
+  if (g.grid > 1 && (c.P == nullptr || c.flags == nullptr)) return cudaErrorInvalidValue;
   cudaError_t e;
   if (c.a_f32) e = c.trans ? dispatch_tmax<float, true>(g, st) : dispatch_tmax<float, false>(g, st);
   else e = c.trans ? dispatch_tmax<double, true>(g, st) : dispatch_tmax<double, false>(g, st);
   ++g_kernel_launches;
   if (e != cudaSuccess) return e;
-  if (g.grid > 1) {
-    // contributors per split row block -> lanes per output element (<= 4 loads each)
-    const int64_t contributors = ceil_div(g.KT * (int64_t)g.grid, g.units) + 1;
-    int T = 1;
-    while (T < 32 && T * 4 < contributors) T <<= 1;
-    const int epb = 256 / T;
-    int ych = (int)ceil_div((int64_t)BM * g.N, epb);
-    if (ych > 64) ych = 64;
-    gemm_streamk_fixup<<<dim3(g.grid - 1, ych), 256, 0, st>>>(g, T);
-    ++g_kernel_launches;
-    e = cudaGetLastError();
-  }
   return e;
 }
 

@@ -15,6 +15,7 @@ struct GemmCall {
   const double* B; int64_t ldb;          // K x N, N % 16 == 0, zero-padded columns
   double* C; int64_t ldc;                // output M x Nout
   double* P;                             // split partials (>= gemm_partial_bytes)
+  unsigned* flags; unsigned epoch;       // >= grid flags, zero-initialised once; epoch unique per launch
   const double* center;                  // per A-column mean (nullable)
   const double* rscale;                  // per A-column 1/s.d. (nullable)
   int64_t M, K; int N, Nout;
@@ -24,15 +25,14 @@ int gemm_choose_grid(int64_t M, int64_t K, int num_sms);
 size_t gemm_partial_bytes(int N, int grid);
 cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st);
 
-cudaError_t gemm_streamk_fixup_launch(double* C, int64_t ldc, double* P, int64_t M, int N, int Nout, int64_t KT,
-                                      int64_t units, int grid, cudaStream_t st);
 
 // ---- FP32 A on tcgen05 (pass_tf32.cu): 3-term TF32 split, TMEM accumulators
 struct Tf32Call {
   const float* A; int64_t lda; bool trans;   // A row-major FP32 (16-byte aligned rows)
   const double* B; int64_t ldb;              // K x N panel, FP64 (split to TF32 hi/lo inside)
   double* C; int64_t ldc;                    // M x Nout output, FP64
-  double* P;                                 // stream-K partials (grid * 2 * 128 * tf32_n(N) doubles)
+  double* P;                                 // stream-K partials (grid * 128 * tf32_n(N) doubles)
+  unsigned* flags; unsigned epoch;           // as GemmCall
   float* split;                              // 2 * K * tf32_n(N) floats scratch
   int64_t M, K; int N, Nout; int grid;
 };

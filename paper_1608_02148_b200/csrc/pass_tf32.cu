@@ -32,7 +32,8 @@ constexpr int B_BOX_BYTES = 32 * BK * 4;      // 4 KB per 32-column box
 
 struct Args {
   double* C; int64_t ldc;
-  double* P;
+  double* P;                                  // [grid][BM][N] partial of a CTA's leading segment
+  unsigned* flags; unsigned epoch;
   int64_t M, K; int N, Nout;
   int64_t KT, units;
   int grid;
@@ -258,9 +259,12 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       if (kt == KT - 1 || it == nun - 1) {
         mbar_wait(&accf, (uint32_t)(seg & 1));
         tc_fence_after();
-        const int64_t seg_start = (mb * KT > u_lo) ? mb * KT : u_lo;
-        const bool fullseg = (seg_start == mb * KT) && (kt == KT - 1);
-        const int slot = (mb == u_lo / KT) ? 0 : 1;
+        // in-kernel stream-K fix-up (see gemm_pass.cu): continuation -> partial +
+        // release flag; head of a spanning row block -> acquire later partials
+        const int64_t rb_lo = mb * KT, rb_hi = rb_lo + KT;
+        const int64_t seg_start = (rb_lo > u_lo) ? rb_lo : u_lo;
+        const bool cont = seg_start > rb_lo;
+        const bool head = !cont && (u + 1 < rb_hi);
         const int row = 32 * (warp & 3) + lane;
         const int64_t gm = mb * BM + row;
         for (int c0 = 0; c0 < g.N; c0 += 32) {
@@ -268,20 +272,43 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)c0;
           TMEM_LD32(taddr, v);
           TMEM_WAIT_LD(v);    // the registers are defined only after wait::ld
-          if (fullseg) {
-            if (gm < g.M) {
-              double* dst = g.C + gm * g.ldc + c0;
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (c0 + j < g.Nout) dst[j] = (double)__uint_as_float(v[j]);
-            }
-          } else {
-            double* dst = g.P + (((int64_t)blockIdx.x * 2 + slot) * BM + row) * g.N + c0;
+          if (cont) {
+            double* dst = g.P + ((int64_t)blockIdx.x * BM + row) * g.N + c0;
 #pragma unroll
             for (int j = 0; j < 32; j += 2)
               *reinterpret_cast<double2*>(dst + j) = make_double2((double)__uint_as_float(v[j]),
                                                                   (double)__uint_as_float(v[j + 1]));
+          } else {
+            double a[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) a[j] = (double)__uint_as_float(v[j]);
+            if (head) {
+              for (int c = blockIdx.x + 1; c < g.grid && unit_lo(g.units, g.grid, c) < rb_hi; ++c) {
+                unsigned f;
+                do {
+                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(g.flags + c) : "memory");
+                } while (f != g.epoch);
+                const double* src = g.P + ((int64_t)c * BM + row) * g.N + c0;
+#pragma unroll
+                for (int j = 0; j < 32; j += 2) {
+                  const double2 pv = *reinterpret_cast<const double2*>(src + j);
+                  a[j] += pv.x;
+                  a[j + 1] += pv.y;
+                }
+              }
+            }
+            if (gm < g.M) {
+              double* dst = g.C + gm * g.ldc + c0;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (c0 + j < g.Nout) dst[j] = a[j];
+            }
           }
+        }
+        if (cont) {
+          __threadfence();
+          asm volatile("bar.sync 1, 128;" ::: "memory");     // the four epilogue warps
+          if (et == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(g.epoch) : "memory");
         }
         tc_fence_before();
         __syncwarp();
@@ -380,6 +407,8 @@ cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st) {
   if (!ok) return cudaErrorInvalidValue;
   Args g;
   g.C = c.C; g.ldc = c.ldc; g.P = c.P; g.M = c.M; g.K = c.K; g.N = N; g.Nout = c.Nout;
+  g.flags = c.flags; g.epoch = c.epoch;
+  if (c.flags == nullptr) return cudaErrorInvalidValue;
   g.KT = ceil_div(c.K, BK);
   const int64_t mblocks = ceil_div(c.M, BM);
   g.units = mblocks * g.KT;
@@ -400,10 +429,7 @@ cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st) {
     pass_tf32_kernel<true><<<g.grid, THREADS, smem, st>>>(mA, mBh, mBl, g);
   }
   ++g_kernel_launches;
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  if (g.grid > 1) e = gemm_streamk_fixup_launch(c.C, c.ldc, c.P, c.M, N, c.Nout, g.KT, g.units, g.grid, st);
-  return e;
+  return cudaGetLastError();
 }
 
 }  // namespace rsvd
