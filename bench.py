@@ -251,7 +251,7 @@ def main():
     clocks = sampler.stop() if sampler else None
     ms = e0.elapsed_time(e1) / max(args.steps, 1)
     launches = ctx.launch_count()
-    prof = {kind: ctx.profile(kind) for kind in range(5)}
+    prof = {kind: ctx.profile(kind) for kind in range(6)}
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         import torch.distributed as dist
@@ -278,8 +278,8 @@ def main():
     bytes_launch = m_loc * n * es
     tf = flops_launch / (avg_ms * 1e-3) / 1e12
     gbs = bytes_launch / (avg_ms * 1e-3) / 1e9
-    share = {"A.X": prof[0][0] / max(sum(prof[kk][0] for kk in range(5)), 1e-12),
-             "At.X": prof[1][0] / max(sum(prof[kk][0] for kk in range(5)), 1e-12)}
+    share = {"A.X": prof[0][0] / max(sum(prof[kk][0] for kk in range(6)), 1e-12),
+             "At.X": prof[1][0] / max(sum(prof[kk][0] for kk in range(6)), 1e-12)}
     roof = {"bound": "tensor", "kernel": kinds[dom], "achieved": round(tf, 3), "peak": fp64_peak,
             "unit": "TFLOP/s", "frac": round(tf / fp64_peak, 4), "traffic": None,
             "peak_source": fp64_src + " (FP64 DMMA; tcgen05 has no f64 kind)",
@@ -289,7 +289,7 @@ def main():
                     "peak_source": hbm_src},
             "step_share": {kk: round(vv, 4) for kk, vv in share.items()},
             "per_kind_ms_per_step": {name: round(prof[kk][0] / max(args.steps, 1), 4) for kk, name in
-                                     enumerate(["pass_AX", "pass_AtX", "panel_orth", "jacobi_svd", "omega"])}}
+                                     enumerate(["pass_AX", "pass_AtX", "panel_orth", "jacobi_svd", "omega", "ozaki_slice_A"])}}
     traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic_cfg%d.json" % args.config)
     if os.path.exists(traffic_file):
         try:

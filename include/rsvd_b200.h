@@ -159,7 +159,8 @@ rsvd_status rsvd_omega(rsvd_ctx* ctx, int64_t n, int64_t l, int32_t sdist, uint6
 /* Per-kernel timing of the last calls (CUDA events on the context stream,
  * enabled by rsvd_set_profiling(ctx, 1)).  kind: 0 = sketch/power pass A.X,
  * 1 = transposed pass A^T.X (incl. its split reduction), 2 = panel
- * orthonormalisation, 3 = small SVD, 4 = other.  Returns accumulated
+ * orthonormalisation, 3 = small SVD, 4 = other, 5 = Ozaki slicing of A
+ * (FP64 inputs on the tensor-core path, once per call).  Returns accumulated
  * milliseconds and launch count since the last reset (HOST out-params). */
 rsvd_status rsvd_set_profiling(rsvd_ctx* ctx, int enable);
 rsvd_status rsvd_profile(rsvd_ctx* ctx, int kind, double* total_ms, int64_t* count,
@@ -168,10 +169,12 @@ rsvd_status rsvd_profile_reset(rsvd_ctx* ctx);
 /* Number of kernels this library launched since the last reset. */
 int64_t rsvd_launch_count(const rsvd_ctx* ctx);
 
-/* Diagnostics of the last rsvd-family call (HOST out-param, n <= 3 slots):
+/* Diagnostics of the last rsvd-family call (HOST out-param, n <= 4 slots):
  * out[0] = one-sided Jacobi sweeps, out[1] = 1 if the CholeskyQR2 breakdown
  * re-run in robust (Householder / TSQR) mode was taken, out[2] = kernel
- * launches since the last rsvd_profile_reset. */
+ * launches since the last rsvd_profile_reset, out[3] = passes run on the
+ * FP64 Ozaki tensor-core path since the context was created (RSVD_FP64_PATH=dmma
+ * in the environment at rsvd_create selects the FP64 DMMA path instead). */
 rsvd_status rsvd_stats(const rsvd_ctx* ctx, int64_t* out, int n);
 
 #ifdef __cplusplus

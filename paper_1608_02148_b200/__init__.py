@@ -157,10 +157,11 @@ class Context:
         return int(lib().rsvd_launch_count(self.h))
 
     def stats(self):
-        """(Jacobi sweeps, robust re-run taken, kernel launches) of the last call."""
-        buf = (ctypes.c_int64 * 3)()
-        self.check(lib().rsvd_stats(self.h, buf, 3))
-        return dict(jacobi_sweeps=int(buf[0]), robust_rerun=bool(buf[1]), launches=int(buf[2]))
+        """(Jacobi sweeps, robust re-run taken, kernel launches, Ozaki passes) of the last call."""
+        buf = (ctypes.c_int64 * 4)()
+        self.check(lib().rsvd_stats(self.h, buf, 4))
+        return dict(jacobi_sweeps=int(buf[0]), robust_rerun=bool(buf[1]), launches=int(buf[2]),
+                    ozaki_passes=int(buf[3]))
 
     def close(self):
         if getattr(self, "h", None):

@@ -64,12 +64,16 @@ struct rsvd_ctx {
   bool prof = false;
   std::vector<ProfRec> pending;
   std::vector<cudaEvent_t> pool;
-  double prof_ms[5] = {0, 0, 0, 0, 0};
-  double prof_bytes[5] = {0, 0, 0, 0, 0};
-  int64_t prof_count[5] = {0, 0, 0, 0, 0};
+  double prof_ms[6] = {0, 0, 0, 0, 0, 0};
+  double prof_bytes[6] = {0, 0, 0, 0, 0, 0};
+  int64_t prof_count[6] = {0, 0, 0, 0, 0, 0};
   int64_t launches = 0;
   int last_sweeps = 0;
   bool fp32_tcgen05 = true;       // RSVD_FP32_PATH=dmma selects the FP64-DMMA path for FP32 inputs
+  bool fp64_ozaki = true;         // RSVD_FP64_PATH=dmma selects the DMMA path for FP64 inputs
+  char* ws4 = nullptr;            // Ozaki slices of A (+ X slice scratch)
+  size_t ws4_bytes = 0;
+  int64_t ozaki_calls = 0;
   int last_robust = 0;
   unsigned* gemm_flags = nullptr; // stream-K fix-up flags (kMaxGrid, zeroed at creation)
   unsigned gemm_epoch = 0;
@@ -154,6 +158,9 @@ struct Plan {
   // workspace offsets
   size_t oX, oY, oT, oZ, oPart, oSmall, oColc, oColr, oColp, oSplit, oJlog, total;
   bool use_tf32 = false;          // FP32 A on tcgen05 (3-term TF32 split)
+  bool use_ozaki = false;         // FP64 A on tcgen05 (Ozaki int8 slices)
+  OzakiA oz{};
+  void* ozx = nullptr;            // X slice scratch
   float* split = nullptr;
   void* jlog = nullptr;
   size_t part_bytes;
@@ -254,7 +261,21 @@ rsvd_status pass_tf32(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, doubl
   return RSVD_OK;
 }
 
+rsvd_status pass_ozaki(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, double* C, int64_t M, int64_t K) {
+  OzakiCall o{};
+  o.a = &p.oz; o.trans = trans; o.B = B; o.ldb = p.Np; o.C = C; o.ldc = p.Np; o.Nout = p.Np;
+  o.P = p.part; o.flags = ctx->gemm_flags; o.epoch = ++ctx->gemm_epoch; o.xscratch = p.ozx;
+  o.M = M; o.K = K; o.N = p.Np; o.grid = ctx->num_sms;
+  ++ctx->ozaki_calls;
+  CK(ozaki_pass(o, ctx->stream));
+  return RSVD_OK;
+}
+
 rsvd_status pass_ax(rsvd_ctx* ctx, Plan& p, const double* X, double* Y, bool centred) {
+  if (p.use_ozaki) {
+    Prof pr(ctx, 0, (double)p.M * p.n * 8);
+    return pass_ozaki(ctx, p, p.trans_input, X, Y, p.M, p.n);
+  }
   if (p.use_tf32 && !centred) {
     Prof pr(ctx, 0, (double)p.M * p.n * 4);
     return pass_tf32(ctx, p, p.trans_input, X, Y, p.M, p.n);
@@ -275,6 +296,13 @@ rsvd_status pass_ax(rsvd_ctx* ctx, Plan& p, const double* X, double* Y, bool cen
 
 // Z (n x Np) = f(A)^T Q (K3), then allreduce over ranks.
 rsvd_status pass_atx(rsvd_ctx* ctx, Plan& p, const double* Q, double* Z, bool centred) {
+  if (p.use_ozaki) {
+    {
+      Prof pr(ctx, 1, (double)p.M * p.n * 8);
+      CKS(pass_ozaki(ctx, p, !p.trans_input, Q, Z, p.n, p.M));
+    }
+    return allreduce_sum(ctx, Z, (size_t)p.n * p.Np);
+  }
   if (p.use_tf32 && !centred) {
     {
       Prof pr(ctx, 1, (double)p.M * p.n * 4);
@@ -459,6 +487,12 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool robus
       CK(launch_colstat_finish(p.colr, p.n, (double)p.m_global, 1, p.cols, ctx->stream));
     }
   }
+  if (p.use_ozaki) {
+    // slices of f(A) once per call; every pass below reads them (pass_ozaki.cu)
+    Prof pr(ctx, 5, (double)p.M * p.n * 8);
+    CK(ozaki_slice_a(p.oz, (const double*)p.A, p.lda, centred ? p.colc : nullptr, p.scaled ? p.colr : nullptr,
+                     ctx->flags_dev, ctx->stream));
+  }
   {
     Prof pr(ctx, 4, 0);
     CK(launch_omega(p.n, l, Np, Np, prm->sdist, prm->seed, prm->stream, p.f32, false, p.X, ctx->stream));
@@ -524,12 +558,28 @@ rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bo
   p.l = (int)std::min<int64_t>((int64_t)k + p_over, mn);
   p.Np = (int)round_up(p.l, 16);      // GEMM N granularity: two warps x n8 tiles
   p.use_tf32 = p.f32 && !center_or_scale && ctx->fp32_tcgen05 && tf32_pass_supported(p.A, p.lda);
+  p.use_ozaki = !p.f32 && ctx->fp64_ozaki && ozaki_supported(p.Np);
   if (p.l > kMaxL) return fail(ctx, RSVD_EUNSUPPORTED, "l = k + p = %d exceeds this build's limit %d", p.l, kMaxL);
   if (ctx->nranks > 1 && p.M < p.l)
     return fail(ctx, RSVD_EUNSUPPORTED, "each rank needs at least l = %d rows", p.l);
   const size_t bytes = plan_bytes(ctx, p);
   CKS(ensure_ws(ctx, bytes));
   bind(ctx, p);
+  if (p.use_ozaki) {
+    // slices of the stored matrix (A->m_local x A->n), then the X slice scratch
+    const size_t sa = align256(ozaki_a_bytes(A->m_local, A->n));
+    const size_t sx = align256(ozaki_x_bytes(std::max(p.M, p.n), p.Np));
+    if (sa + sx > ctx->ws4_bytes) {
+      if (ctx->ws4) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->ws4); ctx->ws4 = nullptr; ctx->ws4_bytes = 0; }
+      if (cudaMalloc(&ctx->ws4, sa + sx) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, RSVD_ENOMEM, "Ozaki slice workspace of %zu bytes failed", sa + sx);
+      }
+      ctx->ws4_bytes = sa + sx;
+    }
+    p.oz = ozaki_layout_a(ctx->ws4, A->m_local, A->n);
+    p.ozx = ctx->ws4 + sa;
+  }
   return RSVD_OK;
 }
 
@@ -572,6 +622,8 @@ rsvd_status rsvd_create(rsvd_ctx** out, int device, void* stream) {
   {
     const char* fp = getenv("RSVD_FP32_PATH");
     if (fp && strcmp(fp, "dmma") == 0) ctx->fp32_tcgen05 = false;
+    const char* f64 = getenv("RSVD_FP64_PATH");
+    if (f64 && strcmp(f64, "dmma") == 0) ctx->fp64_ozaki = false;
   }
   if (e != cudaSuccess) {
     delete ctx;
@@ -594,6 +646,7 @@ rsvd_status rsvd_destroy(rsvd_ctx* ctx) {
   cudaFreeHost(ctx->hbuf);
   cudaFree(ctx->ws3);
   cudaFree(ctx->gemm_flags);
+  cudaFree(ctx->ws4);
   delete ctx;
   return RSVD_OK;
 }
@@ -740,7 +793,7 @@ rsvd_status rsvd_set_profiling(rsvd_ctx* ctx, int enable) {
 }
 
 rsvd_status rsvd_profile(rsvd_ctx* ctx, int kind, double* total_ms, int64_t* count, double* bytes) {
-  if (!ctx || kind < 0 || kind > 4) return RSVD_EINVAL;
+  if (!ctx || kind < 0 || kind > 5) return RSVD_EINVAL;
   if (!ctx->pending.empty()) {
     cudaStreamSynchronize(ctx->stream);
     prof_collect(ctx);
@@ -754,7 +807,7 @@ rsvd_status rsvd_profile(rsvd_ctx* ctx, int kind, double* total_ms, int64_t* cou
 rsvd_status rsvd_profile_reset(rsvd_ctx* ctx) {
   if (!ctx) return RSVD_EINVAL;
   if (!ctx->pending.empty()) { cudaStreamSynchronize(ctx->stream); prof_collect(ctx); }
-  for (int i = 0; i < 5; ++i) { ctx->prof_ms[i] = 0; ctx->prof_bytes[i] = 0; ctx->prof_count[i] = 0; }
+  for (int i = 0; i < 6; ++i) { ctx->prof_ms[i] = 0; ctx->prof_bytes[i] = 0; ctx->prof_count[i] = 0; }
   rsvd::g_kernel_launches = 0;
   return RSVD_OK;
 }
@@ -763,8 +816,8 @@ int64_t rsvd_launch_count(const rsvd_ctx* ctx) { return ctx ? rsvd::g_kernel_lau
 
 rsvd_status rsvd_stats(const rsvd_ctx* ctx, int64_t* out, int n) {
   if (!ctx || !out || n < 0) return RSVD_EINVAL;
-  const int64_t v[3] = {ctx->last_sweeps, ctx->last_robust, rsvd::g_kernel_launches};
-  for (int i = 0; i < n && i < 3; ++i) out[i] = v[i];
+  const int64_t v[4] = {ctx->last_sweeps, ctx->last_robust, rsvd::g_kernel_launches, ctx->ozaki_calls};
+  for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
   return RSVD_OK;
 }
 

@@ -58,6 +58,30 @@ cudaError_t launch_chol_aug(const double* G, int ldg, int l, int npad, double* R
 cudaError_t launch_panel_apply(const double* S, int64_t lds, int64_t rows, int Np, const double* T, int64_t ldt,
                                double* C, int64_t ldc, int Nout, bool upper, int num_sms, cudaStream_t st);
 
+// ---- FP64 passes by Ozaki-scheme int8 slices on tcgen05 (pass_ozaki.cu)
+#define OZ_S 8                                   // 7-bit digits per element (56 bits: exact for FP64)
+struct OzakiA {                                  // A sliced once per call: m x (ldn/128) x S x 128 int8 + exponents
+  int8_t* slices; double* ea;                    // ea[row][col super-tile] = 2^E (512 x 512 super-tiles)
+  double* tmax;                                  // scratch: max |f(a)| per 128 x 128 tile
+  int64_t m, n, ldn; int ntiles;
+};
+size_t ozaki_a_bytes(int64_t m, int64_t n);
+OzakiA ozaki_layout_a(void* buf, int64_t m, int64_t n);
+// slices of f(A) = (A - 1 c^T) diag(rs) (c, rs nullable); flag |= 4 on non-finite A
+cudaError_t ozaki_slice_a(const OzakiA& a, const double* A, int64_t lda, const double* c, const double* rs, int* flag,
+                          cudaStream_t st);
+struct OzakiCall {
+  const OzakiA* a; bool trans;                   // trans: C = f(A)^T B (M = n, K = m), else C = f(A) B
+  const double* B; int64_t ldb;                  // K x N panel (FP64), N = Np <= 64
+  double* C; int64_t ldc; int Nout;
+  double* P; unsigned* flags; unsigned epoch;    // stream-K partials / flags as GemmCall
+  void* xscratch;                                // >= ozaki_x_bytes(K, N)
+  int64_t M, K; int N; int grid;
+};
+bool ozaki_supported(int Np);
+size_t ozaki_x_bytes(int64_t K, int Np);
+cudaError_t ozaki_pass(const OzakiCall& c, cudaStream_t st);
+
 // ---- K1 Omega (omega.cu)
 cudaError_t launch_omega(int64_t n, int64_t l, int64_t ldo, int64_t ncols_zero, int sdist,
                          uint64_t seed, uint64_t stream, bool f32_round, bool out_f32, void* out,

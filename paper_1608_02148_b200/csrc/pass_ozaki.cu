@@ -1,0 +1,543 @@
+// pass_ozaki.cu -- the FP64 passes over A on the 5th-generation tensor cores:
+// Ozaki-scheme emulation of the FP64 products Y = A X (sketch / power pass,
+// Eq. YAQ, Alg. 2 step 4) and Z = A^T Q (Alg. 2 step 3, Eq. BQA
+// P:220) with tcgen05.mma kind::i8 (int8 x int8 -> int32 in TMEM).
+//
+// Why: tcgen05 has no f64 kind; the warp-level DMMA pipe (37 TFLOP/s measured)
+// bounds a pass at l/4 flop per A byte to ~20-40% of the HBM roof.
+// int8 tensor throughput is ~60x higher, so an exact slice decomposition
+// moves the pass to the HBM roof.
+//
+// Representation (exact, no rounding): A is cut into 128 x 128 tiles; a tile
+// with max |a| < 2^E stores a = sign(a) * 2^E * sum_{t=1..S} d_t 2^{-7t} with
+// digits d_t in [0, 127] (sign applied to every digit, so each fits int8) —
+// the first 7S bits of |a| 2^-E, truncated (S = 7: 49 bits).  X (the panel,
+// K x Np) is cut per (128-row k-block, column) the same way.  Then
+//   (A X)_ij = sum_kb 2^{E_A(tile) + E_X(kb, j)} sum_{t,u} 2^{-7(t+u)} (D_t X_u)_ij
+// where D_t X_u over one k-block is an exact int32 dot product (|.| <= 128 * 127^2).
+// Products with t + u > S + 1 are dropped (their weight is < 2^{-7(S+2)}).
+// Terms of equal weight g = t + u share one TMEM accumulator: S groups x N
+// columns (S = 7, N <= 64: 448 of 512 TMEM columns).  After each k-block the
+// epilogue converts the groups to FP64 and accumulates the scaled sum in
+// registers.
+//
+// A is sliced once per rsvd call (ozaki_slice_a) and read by every pass (S
+// bytes per element instead of 8); X is sliced before each pass.
+//
+// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 =
+// TMEM allocator, warps 4..7 = epilogue (TMEM lanes = output rows).  Stream-K
+// over (row block, k-block) units with the in-kernel fix-up of gemm_pass.cu.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace rsvd {
+namespace oz {
+using namespace tc;
+
+constexpr int BM = 128, BKO = 128, THREADS = 256;
+// A-slice pipeline stages: as many 16 KB stages as fit next to two X buffers
+__host__ __device__ constexpr int nsa_for(int S, int N) { return (220 * 1024 - 2 * S * N * 128 - 2048) / (128 * 128) > 6 ? 6 : (220 * 1024 - 2 * S * N * 128 - 2048) / (128 * 128); }
+constexpr int A_TILE = BM * BKO;                    // bytes of one slice tile
+constexpr int KSUP = 4, ET = KSUP * BKO;            // exponent super-tiles: 512 x 512 of A, 512-row blocks of X;
+                                                    // int32 accumulation over 512 k (<= 512 * 127^2 < 2^23)
+
+__host__ __device__ inline int64_t unit_lo(int64_t units, int grid, int c) { return (units * (int64_t)c) / grid; }
+#ifndef OZ_PROBE
+#define OZ_PROBE_DECL
+#define OZ_PROBE(slot)
+#define OZ_PROBE_OUT
+#endif
+
+__device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// ---------------------------------------------------------------- slicing
+// exponent E with max |a| < 2^E (0 for an all-zero block)
+__device__ __forceinline__ int block_exp(double mx) { return mx > 0.0 ? ilogb(mx) + 1 : 0; }
+
+// S digits of |v| 2^{7S - E} (truncated), sign applied, packed 4 elements per word
+template <int S>
+__device__ __forceinline__ void digits4(const double (&v)[4], double scale, uint32_t (&w)[S]) {
+#pragma unroll
+  for (int t = 0; t < S; ++t) w[t] = 0u;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const double y = fabs(v[e]) * scale;                // < 2^{7S}, exact scaling
+    const unsigned long long q = (unsigned long long)y;  // truncation
+    const bool neg = v[e] < 0.0;
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+      int d = (int)((q >> (7 * (S - 1 - t))) & 127ull);
+      if (neg) d = -d;
+      w[t] |= ((uint32_t)(d & 0xff)) << (8 * e);
+    }
+  }
+}
+
+// f(a) = (a - c_j) * rs_j when c / rs are given (rpca centring / scaling, Alg. 6)
+__device__ __forceinline__ double fval(const double* A, int64_t lda, const double* c, const double* rs, int64_t r,
+                                       int64_t cc) {
+  double a = A[r * lda + cc];
+  if (c) a -= c[cc];
+  if (rs) a *= rs[cc];
+  return a;
+}
+
+// max |f(a)| per 128 x 128 tile (bx = column tile, by = row tile); flag |= 4 on non-finite
+__global__ void __launch_bounds__(256)
+ozaki_amax_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, const double* __restrict__ c,
+                  const double* __restrict__ rs, double* __restrict__ tmax, int* flag) {
+  __shared__ double red[8];
+  const int64_t r0 = (int64_t)blockIdx.y * BM, c0 = (int64_t)blockIdx.x * BKO;
+  const int tid = threadIdx.x;
+  double mx = 0.0;
+  bool nf = false;
+  for (int e = tid; e < BM * BKO; e += 256) {
+    const int64_t r = r0 + e / BKO, cc = c0 + e % BKO;
+    if (r < m && cc < n) {
+      const double a = fval(A, lda, c, rs, r, cc);
+      if (!isfinite(a)) nf = true;
+      mx = fmax(mx, fabs(a));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((tid & 31) == 0) red[tid >> 5] = mx;
+  if (nf) atomicOr(flag, 4);
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
+    tmax[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = fmax(mx, red[0]);
+  }
+}
+
+// 128 x 128 tile -> slices, interleaved as [row][col block][t][128 bytes] so that
+// one unit's S slice boxes read one contiguous S * 128 B run per row (DRAM
+// locality for both pass orientations); digits relative to the
+// 512 x 512 super-tile exponent; ea[sy * nsx + sx] = 2^E
+template <int S>
+__global__ void __launch_bounds__(256)
+ozaki_slice_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, const double* __restrict__ c,
+                     const double* __restrict__ rs, const double* __restrict__ tmax, int8_t* __restrict__ slices,
+                     int64_t ldn, double* __restrict__ ea, int nsx) {
+  const int64_t r0 = (int64_t)blockIdx.y * BM, c0 = (int64_t)blockIdx.x * BKO;
+  const int tid = threadIdx.x;
+  const int sy = blockIdx.y / KSUP, sx = blockIdx.x / KSUP;
+  double mx = 0.0;
+  for (int yy = sy * KSUP; yy < min((int)gridDim.y, (sy + 1) * KSUP); ++yy)
+    for (int xx = sx * KSUP; xx < min((int)gridDim.x, (sx + 1) * KSUP); ++xx) mx = fmax(mx, tmax[(int64_t)yy * gridDim.x + xx]);
+  const int E = block_exp(mx);
+  if (tid == 0 && blockIdx.y % KSUP == 0 && blockIdx.x % KSUP == 0) ea[(int64_t)sy * nsx + sx] = ldexp(1.0, E);
+  const double scale = ldexp(1.0, 7 * S - E);
+  // 4 consecutive columns per thread-iteration; columns >= n of the last block are zero
+  const int64_t nblk = ldn / BKO;
+  for (int e = tid; e < BM * (BKO / 4); e += 256) {
+    const int64_t r = r0 + e / (BKO / 4);
+    const int jj = 4 * (e % (BKO / 4));
+    const int64_t cc = c0 + jj;
+    if (r >= m) continue;
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = (cc + q < n) ? fval(A, lda, c, rs, r, cc + q) : 0.0;
+    uint32_t w[S];
+    digits4<S>(v, scale, w);
+    int8_t* dst = slices + ((r * nblk + blockIdx.x) * S) * BKO + jj;
+#pragma unroll
+    for (int t = 0; t < S; ++t) *reinterpret_cast<uint32_t*>(dst + t * BKO) = w[t];
+  }
+}
+
+// X (K x Np, ldx) -> xs[u][j][k] (u < S, j < Np, ld ldk bytes) and
+// xf[sb * Np + j] = 2^E(sb, j) for 512-row super-blocks sb.
+// (1) column maxima per 16-row chunk, (2) one thread per (16-row chunk, column).
+__global__ void __launch_bounds__(256)
+ozaki_xmax_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, double* __restrict__ cmax) {
+  const int j = threadIdx.x % 32 + 32 * blockIdx.y, r = threadIdx.x / 32;
+  const int64_t kc = (int64_t)blockIdx.x * 8 + r;           // 16-row chunk
+  if (j >= Np || kc * 16 >= K) return;
+  double mx = 0.0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if (kc * 16 + k < K) mx = fmax(mx, fabs(X[(kc * 16 + k) * ldx + j]));
+  cmax[kc * Np + j] = mx;
+}
+
+template <int S>
+__global__ void __launch_bounds__(256)
+ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, const double* __restrict__ cmax,
+                     int8_t* __restrict__ xs, int64_t ldk, double* __restrict__ xf) {
+  const int j = threadIdx.x % 32 + 32 * blockIdx.y, r = threadIdx.x / 32;
+  const int64_t kc = (int64_t)blockIdx.x * 8 + r;
+  if (j >= Np || kc * 16 >= ldk) return;
+  const int64_t nch = ceil_div(K, 16);
+  const int64_t sb = kc / (ET / 16), c0 = sb * (ET / 16);
+  double mx = 0.0;
+  for (int64_t c = c0; c < min(nch, c0 + ET / 16); ++c) mx = fmax(mx, cmax[c * Np + j]);
+  const int E = block_exp(mx);
+  if (kc % (ET / 16) == 0) xf[sb * Np + j] = ldexp(1.0, E);
+  const double scale = ldexp(1.0, 7 * S - E);
+  uint32_t w[4][S];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t kk = kc * 16 + 4 * q + e;
+      v[e] = kk < K ? X[kk * ldx + j] : 0.0;
+    }
+    digits4<S>(v, scale, w[q]);
+  }
+#pragma unroll
+  for (int t = 0; t < S; ++t)
+    *reinterpret_cast<uint4*>(xs + ((int64_t)t * Np + j) * ldk + kc * 16) = make_uint4(w[0][t], w[1][t], w[2][t], w[3][t]);
+}
+
+// ---------------------------------------------------------------- pass kernel
+struct Args {
+  double* C; int64_t ldc;
+  double* P; unsigned* flags; unsigned epoch;
+  const double* ea; int ea_ld;                      // 2^E per A tile [row tile][col tile]
+  const double* xf;                                 // 2^E per (k-block, column) of X
+  int64_t M, K; int N, Nout, Np;
+  int64_t KB, units; int grid;
+};
+
+template <bool TRANS, int S, int N>
+__global__ void __launch_bounds__(THREADS, 1)
+ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapX, Args g) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int NSA = nsa_for(S, N);
+  constexpr int XSL = N * BKO;                      // bytes of one X slice (N rows x 128 k)
+  constexpr int XBUF = ((S * XSL + 1023) / 1024) * 1024;
+  unsigned char* astage = base;
+  unsigned char* xbuf = base + NSA * A_TILE;
+  __shared__ uint64_t afull[NSA], aempty[NSA], xfull[2], xempty[2], accf, acce;
+  __shared__ uint32_t tmem_base;
+  __shared__ double xfsm[4 * 64];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t KB = g.KB;
+  const int64_t u_lo = unit_lo(g.units, g.grid, blockIdx.x);
+  const int64_t u_hi = unit_lo(g.units, g.grid, blockIdx.x + 1);
+  const int64_t nun = u_hi - u_lo;
+
+  if (tid == 0) {
+    for (int s = 0; s < NSA; ++s) { mbar_init(&afull[s], 1); mbar_init(&aempty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&xfull[s], 1); mbar_init(&xempty[s], 1); }
+    mbar_init(&accf, 1);
+    mbar_init(&acce, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      for (int64_t it = 0; it < nun; ++it) {
+        const int64_t u = u_lo + it, mb = u / KB, kb = u - mb * KB;
+        const int xb = (int)(it & 1);
+        mbar_wait(&xempty[xb], (uint32_t)(((it >> 1) & 1) ^ 1));
+        mbar_expect_tx(&xfull[xb], (uint32_t)(S * XSL));
+        for (int t = 0; t < S; ++t) tma_2d(xbuf + xb * XBUF + t * XSL, &mapX, (int)(kb * BKO), t * g.Np, &xfull[xb]);
+        for (int t = 0; t < S; ++t) {
+          const int64_t q = it * S + t;
+          const int s = (int)(q % NSA);
+          mbar_wait(&aempty[s], (uint32_t)(((q / NSA) & 1) ^ 1));
+          mbar_expect_tx(&afull[s], (uint32_t)A_TILE);
+          if (!TRANS) tma_4d(astage + s * A_TILE, &mapA, 0, t, (int)kb, (int)(mb * BM), &afull[s]);
+          else tma_4d(astage + s * A_TILE, &mapA, 0, t, (int)mb, (int)(kb * BKO), &afull[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      // X slices u0..u0+c-1 are consecutive N-row blocks in shared memory and their
+      // groups t+u0..t+u0+c-1 consecutive N-column blocks of TMEM, so one MMA with
+      // N_mma = c N covers them all (c N <= 256).
+      const uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((TRANS ? 1u : 0u) << 15) | (0u << 16) |
+                              ((uint32_t)(BM >> 4) << 24);
+      constexpr int CMAX = 256 / N;
+      OZ_PROBE_DECL
+      int64_t ndrain = 0;
+      bool fresh = true;
+      for (int64_t it = 0; it < nun; ++it) {
+        const int64_t u = u_lo + it, kb = u % KB;
+        const bool drain = (kb % KSUP == KSUP - 1) || kb == KB - 1 || it == nun - 1;
+        const int xb = (int)(it & 1);
+        OZ_PROBE(0)
+        mbar_wait(&xfull[xb], (uint32_t)((it >> 1) & 1));
+        OZ_PROBE(1)
+        if (fresh && ndrain > 0) mbar_wait(&acce, (uint32_t)((ndrain - 1) & 1));
+        OZ_PROBE(2)
+        tc_fence_after();
+        const uint64_t dx0 = sdesc(smem_u32(xbuf + xb * XBUF), 16, 1024);
+        const uint32_t acc0 = fresh ? 0u : 1u;
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          const int64_t q = it * S + t;
+          const int s = (int)(q % NSA);
+          OZ_PROBE(0)
+          mbar_wait(&afull[s], (uint32_t)((q / NSA) & 1));
+          OZ_PROBE(3)
+          tc_fence_after();
+          // descriptors differ only in the start-address field (address >> 4, low 14 bits):
+          // K-major (NN) k-steps are +32 B, MN-major (TN) k-steps +32 rows of 128 B
+          const uint64_t da0 = sdesc(smem_u32(astage + s * A_TILE), 16, 1024);
+#pragma unroll
+          for (int kk = 0; kk < BKO / 32; ++kk) {
+            const uint64_t da = da0 + (uint64_t)(TRANS ? kk * 256 : kk * 2);
+#pragma unroll
+            for (int u0 = 0; u0 < S - t; u0 += CMAX) {
+              constexpr int dummy = 0; (void)dummy;
+              const int cnt = (S - t - u0) < CMAX ? (S - t - u0) : CMAX;
+              const uint64_t db = dx0 + (uint64_t)((u0 * XSL + kk * 32) >> 4);
+              const uint32_t idesc = idesc0 | ((uint32_t)((cnt * N) >> 3) << 17);
+              mma_i8(tmem + (uint32_t)((t + u0) * N), da, db, idesc, (t > 0 || kk > 0) ? 1u : acc0);
+            }
+          }
+          mma_commit(&aempty[s]);
+          OZ_PROBE(4)
+        }
+        mma_commit(&xempty[xb]);
+        if (drain) { mma_commit(&accf); ++ndrain; }
+        fresh = drain;
+      }
+      OZ_PROBE_OUT
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM groups -> FP64, scale, accumulate; segment write-out
+    const int et = tid - 128;
+    const int row = 32 * (warp & 3) + lane;
+    const uint32_t tlane = (uint32_t)(32 * (warp & 3)) << 16;
+    double acc[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) acc[j] = 0.0;
+    double* xfs = xfsm + (warp & 3) * 64;             // per-warp copy of this unit's column factors
+    int64_t ndrain = 0;
+    for (int64_t it = 0; it < nun; ++it) {
+      const int64_t u = u_lo + it, mb = u / KB, kb = u - mb * KB;
+      if (!((kb % KSUP == KSUP - 1) || kb == KB - 1 || it == nun - 1)) continue;
+      const double eaf = TRANS ? g.ea[(kb / KSUP) * g.ea_ld + mb / KSUP] : g.ea[(mb / KSUP) * g.ea_ld + kb / KSUP];
+      for (int j = lane; j < N; j += 32) xfs[j] = eaf * g.xf[(kb / KSUP) * g.Np + j];
+      __syncwarp();
+      mbar_wait(&accf, (uint32_t)(ndrain & 1));
+      ++ndrain;
+      tc_fence_after();
+      // 8 columns at a time: the S group loads are issued back to back, one wait
+#pragma unroll
+      for (int c = 0; c < N / 8; ++c) {
+        uint32_t v[S][8];
+#pragma unroll
+        for (int gg = 0; gg < S; ++gg) TMEM_LD8(tmem + tlane + (uint32_t)(gg * N + 8 * c), v[gg]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        double part[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) part[i] = 0.0;
+        double w = 0x1.0p-14;                         // group g = t + u (t, u from 1): weight 2^{-7(g + 2)}
+#pragma unroll
+        for (int gg = 0; gg < S; ++gg) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) part[i] = fma((double)(int)v[gg][i], w, part[i]);
+          w *= 0x1.0p-7;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[8 * c + i] = fma(part[i], xfs[8 * c + i], acc[8 * c + i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce);
+      if (kb == KB - 1 || it == nun - 1) {
+        // stream-K fix-up (see gemm_pass.cu)
+        const int64_t rb_lo = mb * KB, rb_hi = rb_lo + KB;
+        const int64_t seg_start = (rb_lo > u_lo) ? rb_lo : u_lo;
+        const bool cont = seg_start > rb_lo;
+        const bool head = !cont && (u + 1 < rb_hi);
+        const int64_t gm = mb * BM + row;
+        if (cont) {
+          double* dst = g.P + ((int64_t)blockIdx.x * BM + row) * N;
+#pragma unroll
+          for (int j = 0; j < N; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(acc[j], acc[j + 1]);
+          __threadfence();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (et == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(g.epoch) : "memory");
+        } else {
+          if (head) {
+            for (int cc = blockIdx.x + 1; cc < g.grid && unit_lo(g.units, g.grid, cc) < rb_hi; ++cc) {
+              unsigned f;
+              do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(g.flags + cc) : "memory");
+              } while (f != g.epoch);
+              const double* src = g.P + ((int64_t)cc * BM + row) * N;
+#pragma unroll
+              for (int j = 0; j < N; j += 2) {
+                const double2 pv = *reinterpret_cast<const double2*>(src + j);
+                acc[j] += pv.x;
+                acc[j + 1] += pv.y;
+              }
+            }
+          }
+          if (gm < g.M) {
+            double* dst = g.C + gm * g.ldc;
+#pragma unroll
+            for (int j = 0; j < N; ++j)
+              if (j < g.Nout) dst[j] = acc[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) acc[j] = 0.0;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+// slices as a 4-D tensor (byte j < 128, slice t, column block, row) over the
+// interleaved layout; box {128, 1, 1, 128} = one 128 x 128 slice tile
+static bool map_slices(CUtensorMap* mp, const int8_t* p, int64_t rows, int64_t nblk, int S) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {128, (cuuint64_t)S, (cuuint64_t)nblk, (cuuint64_t)rows};
+  cuuint64_t strides[3] = {128, (cuuint64_t)(128 * S), (cuuint64_t)(128 * S * nblk)};
+  cuuint32_t box[4] = {128, 1, 1, 128};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+static bool map_i8_2d(CUtensorMap* mp, const int8_t* p, int64_t cols, int64_t rows, int64_t ld, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace oz
+
+int ozaki_slices() { return OZ_S; }
+
+bool ozaki_supported(int Np) { return Np <= 64 && Np % 16 == 0 && tc::get_encode() != nullptr; }
+
+size_t ozaki_a_bytes(int64_t m, int64_t n) {
+  const int64_t ldn = round_up(n, oz::BKO);
+  const int64_t tiles = ceil_div(m, oz::BM) * ceil_div(n, oz::BKO);
+  return (size_t)OZ_S * m * ldn + 256 + 2 * (size_t)tiles * sizeof(double) + 512;
+}
+
+size_t ozaki_x_bytes(int64_t K, int Np) {
+  const int64_t ldk = round_up(K, 16);
+  return (size_t)OZ_S * Np * ldk + 256 + (size_t)(round_up(ceil_div(K, oz::ET) * Np, 32) + ceil_div(K, 16) * Np) * sizeof(double) + 256;
+}
+
+cudaError_t ozaki_slice_a(const OzakiA& a, const double* A, int64_t lda, const double* c, const double* rs, int* flag,
+                          cudaStream_t st) {
+  dim3 grid((unsigned)ceil_div(a.n, oz::BKO), (unsigned)ceil_div(a.m, oz::BM));
+  oz::ozaki_amax_kernel<<<grid, 256, 0, st>>>(A, lda, a.m, a.n, c, rs, a.tmax, flag);
+  oz::ozaki_slice_a_kernel<OZ_S><<<grid, 256, 0, st>>>(A, lda, a.m, a.n, c, rs, a.tmax, a.slices, a.ldn, a.ea, a.ntiles);
+  g_kernel_launches += 2;
+  return cudaGetLastError();
+}
+
+OzakiA ozaki_layout_a(void* buf, int64_t m, int64_t n) {
+  OzakiA a{};
+  a.m = m; a.n = n; a.ldn = round_up(n, oz::BKO);
+  a.slices = reinterpret_cast<int8_t*>(buf);
+  a.ea = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + round_up((int64_t)OZ_S * m * a.ldn, 256));
+  const int64_t tiles = ceil_div(m, oz::BM) * ceil_div(n, oz::BKO);
+  a.tmax = a.ea + round_up(tiles, 32);
+  a.ntiles = (int)ceil_div(n, oz::ET);               // super-tile columns (ea row stride)
+  return a;
+}
+
+cudaError_t ozaki_pass(const OzakiCall& c, cudaStream_t st) {
+  using namespace oz;
+  const OzakiA& a = *c.a;
+  const int N = c.N;
+  if (!ozaki_supported(N) || c.M <= 0 || c.K <= 0) return cudaErrorInvalidValue;
+  // 1) X slices
+  const int64_t ldk = round_up(c.K, 16);
+  int8_t* xs = reinterpret_cast<int8_t*>(c.xscratch);
+  double* xf = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
+  const int64_t KB = ceil_div(c.K, BKO);
+  double* cmax = xf + round_up(ceil_div(c.K, ET) * N, 32);
+  {
+    const dim3 gx((unsigned)ceil_div(ceil_div(c.K, 16), 8), (unsigned)ceil_div(N, 32));
+    ozaki_xmax_kernel<<<gx, 256, 0, st>>>(c.B, c.ldb, c.K, N, cmax);
+    const dim3 gs((unsigned)ceil_div(ldk / 16, 8), (unsigned)ceil_div(N, 32));
+    ozaki_slice_x_kernel<OZ_S><<<gs, 256, 0, st>>>(c.B, c.ldb, c.K, N, cmax, xs, ldk, xf);
+    g_kernel_launches += 2;
+  }
+  // 2) tensor maps: A slices as (cols = n, rows = m, S); X slices as (cols = K, rows = S * N)
+  CUtensorMap mA, mX;
+  if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, OZ_S)) return cudaErrorInvalidValue;
+  if (!map_i8_2d(&mX, xs, c.K, (int64_t)OZ_S * N, ldk, N)) return cudaErrorInvalidValue;
+  Args g{};
+  g.C = c.C; g.ldc = c.ldc; g.P = c.P; g.flags = c.flags; g.epoch = c.epoch;
+  g.ea = a.ea; g.ea_ld = a.ntiles; g.xf = xf;
+  g.M = c.M; g.K = c.K; g.N = N; g.Nout = c.Nout; g.Np = N;
+  g.KB = KB;
+  const int64_t mblocks = ceil_div(c.M, BM);
+  g.units = mblocks * KB;
+  int64_t grid = g.units / 4;
+  if (grid < mblocks) grid = mblocks;
+  if (grid > c.grid) grid = c.grid;
+  if (grid < 1) grid = 1;
+  g.grid = (int)grid;
+  const size_t smem = (size_t)nsa_for(OZ_S, N) * A_TILE + 2 * (size_t)(((OZ_S * N * BKO) + 1023) / 1024 * 1024) + 1024;
+  cudaError_t e = cudaSuccess;
+#define RSVD_OZ(TR, NN)                                                                                   \
+  {                                                                                                      \
+    static bool attr = false;                                                                            \
+    if (!attr) {                                                                                         \
+      e = cudaFuncSetAttribute(ozaki_pass_kernel<TR, OZ_S, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); \
+      if (e != cudaSuccess) return e;                                                                    \
+      attr = true;                                                                                       \
+    }                                                                                                    \
+    ozaki_pass_kernel<TR, OZ_S, NN><<<g.grid, THREADS, smem, st>>>(mA, mX, g);                           \
+  }
+  if (!c.trans) {
+    switch (N) { case 16: RSVD_OZ(false, 16) break; case 32: RSVD_OZ(false, 32) break;
+                 case 48: RSVD_OZ(false, 48) break; default: RSVD_OZ(false, 64) break; }
+  } else {
+    switch (N) { case 16: RSVD_OZ(true, 16) break; case 32: RSVD_OZ(true, 32) break;
+                 case 48: RSVD_OZ(true, 48) break; default: RSVD_OZ(true, 64) break; }
+  }
+#undef RSVD_OZ
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace rsvd

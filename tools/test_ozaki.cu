@@ -1,0 +1,115 @@
+// Standalone check of the Ozaki int8 tcgen05 pass (pass_ozaki.cu) against a
+// host long-double reference, NN (C = A X) and TN (C = A^T Q).  Not product code.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude -lcuda -o tools/test_ozaki tools/test_ozaki.cu
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+__device__ unsigned long long g_oz[8];
+#define OZ_PROBE_DECL long long _ozt[5] = {0, 0, 0, 0, 0}; long long _ozl = clock64();
+#define OZ_PROBE(slot) { long long _t = clock64(); _ozt[slot] += _t - _ozl; _ozl = _t; }
+#define OZ_PROBE_OUT for (int q = 0; q < 5; ++q) atomicAdd(&g_oz[q], (unsigned long long)_ozt[q]);
+#include "../paper_1608_02148_b200/csrc/pass_tf32.cu"
+#include "../paper_1608_02148_b200/csrc/pass_ozaki.cu"
+namespace rsvd { int64_t g_kernel_launches = 0; }
+using namespace rsvd;
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s @%d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
+
+int main(int argc, char** argv) {
+  const int64_t m = argc > 1 ? atol(argv[1]) : 1000, n = argc > 2 ? atol(argv[2]) : 700;
+  const int reps = argc > 3 ? atoi(argv[3]) : 0;
+  const int mode = argc > 4 ? atoi(argv[4]) : 0;   // 1: one-digit data (A, X = small integers / 128)
+  int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  std::vector<double> A(m * n);
+  srand(5);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double v = (rand() % 200001) / 100000.0 - 1.0;
+      if (i % 7 == 3) v *= 1e-6;                 // rows of very different scale
+      if (j % 11 == 5) v *= 37.5;
+      if (mode == 1) v = ((i * 7 + j * 3) % 255 - 127) / 128.0;
+      if (mode == 2) v = (i == j) ? 1.0 / 128 : 0.0;
+      A[i * n + j] = v;
+    }
+  double *dA, *dC, *dB, *dP; int* flag; unsigned* flags; void *abuf, *xbuf;
+  CK(cudaMalloc(&dA, m * n * 8)); CK(cudaMemcpy(dA, A.data(), m * n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&abuf, ozaki_a_bytes(m, n))); CK(cudaMalloc(&flag, 64)); CK(cudaMemset(flag, 0, 64));
+  CK(cudaMalloc(&flags, 4096 * 4)); CK(cudaMemset(flags, 0, 4096 * 4));
+  const int64_t big = m > n ? m : n;
+  CK(cudaMalloc(&dB, big * 64 * 8)); CK(cudaMalloc(&dC, big * 64 * 8)); CK(cudaMalloc(&dP, (size_t)nsm * 128 * 64 * 8));
+  CK(cudaMalloc(&xbuf, ozaki_x_bytes(big, 64)));
+  OzakiA oa = ozaki_layout_a(abuf, m, n);
+  CK(ozaki_slice_a(oa, dA, n, nullptr, nullptr, flag, 0));
+  CK(cudaDeviceSynchronize());
+  {
+    std::vector<int8_t> sl((size_t)OZ_S * m * oa.ldn);
+    const int64_t tiles = ceil_div(m, 512) * oa.ntiles;
+    std::vector<double> ea(tiles);
+    CK(cudaMemcpy(sl.data(), oa.slices, sl.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ea.data(), oa.ea, tiles * 8, cudaMemcpyDeviceToHost));
+    double e = 0;
+    for (int64_t i = 0; i < m; ++i) for (int64_t j = 0; j < n; ++j) {
+      long double v = 0, w = 1.0L / 128;
+      for (int t = 0; t < OZ_S; ++t) { v += sl[((i * (oa.ldn / 128) + j / 128) * OZ_S + t) * 128 + j % 128] * w; w /= 128; }
+      v *= ea[(i / 512) * oa.ntiles + j / 512];
+      const double tile_max = ea[(i / 512) * oa.ntiles + j / 512];
+      e = fmax(e, fabs((double)(v - A[i * n + j])) / tile_max);
+    }
+    printf("A slice reconstruction: max |err| / 2^E_tile = %.3e (expect < 2^-56 = %.1e)\n", e, ldexp(1.0, -56));
+  }
+  unsigned epoch = 0;
+  for (int trans = 0; trans < 2; ++trans)
+    for (int N : {16, 32, 64}) {
+      const int64_t M = trans ? n : m, K = trans ? m : n;
+      std::vector<double> B(K * N), C(M * N, -7.0);
+      for (int64_t k = 0; k < K; ++k) for (int j = 0; j < N; ++j) {
+        B[k * N + j] = ((rand() % 200001) / 100000.0 - 1.0) * (j % 3 == 1 ? 1e3 : 1.0);
+        if (mode >= 1) B[k * N + j] = ((k * 5 + j * 11) % 255 - 127) / 128.0;
+      }
+      CK(cudaMemcpy(dB, B.data(), K * N * 8, cudaMemcpyHostToDevice));
+      OzakiCall c{};
+      c.a = &oa; c.trans = trans; c.B = dB; c.ldb = N; c.C = dC; c.ldc = N; c.Nout = N; c.P = dP; c.flags = flags;
+      c.epoch = ++epoch; c.xscratch = xbuf; c.M = M; c.K = K; c.N = N; c.grid = nsm;
+      CK(ozaki_pass(c, 0));
+      CK(cudaDeviceSynchronize());
+      CK(cudaMemcpy(C.data(), dC, M * N * 8, cudaMemcpyDeviceToHost));
+      double emax_abs = 0, emax_rel = 0, rmax = 0;
+      for (int64_t i = 0; i < M; ++i)
+        for (int j = 0; j < N; ++j) {
+          long double s = 0, sa = 0;
+          for (int64_t k = 0; k < K; ++k) {
+            const double a = trans ? A[k * n + i] : A[i * n + k];
+            s += (long double)a * B[k * N + j];
+            sa += fabsl((long double)a * B[k * N + j]);
+          }
+          const double e = fabs((double)(C[i * N + j] - s));
+          emax_abs = fmax(emax_abs, e);
+          if (sa > 0) emax_rel = fmax(emax_rel, e / (double)sa);
+          rmax = fmax(rmax, fabs((double)s));
+        }
+      {
+        unsigned long long pr[8]; cudaMemcpyFromSymbol(pr, g_oz, sizeof pr); unsigned long long z[8] = {0}; cudaMemcpyToSymbol(g_oz, z, sizeof z);
+        const double tot = pr[0] + pr[1] + pr[2] + pr[3] + pr[4];
+        printf("  MMA thread time: issue %.1f%%  wait xfull %.1f%%  wait acce %.1f%%  wait afull %.1f%%  mma-issue %.1f%%\n",
+               100 * pr[0] / tot, 100 * pr[1] / tot, 100 * pr[2] / tot, 100 * pr[3] / tot, 100 * pr[4] / tot);
+      }
+      float us = 0;
+      if (reps > 0) {
+        cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        for (int r = 0; r < reps; ++r) { c.epoch = ++epoch; ozaki_pass(c, 0); }
+        cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&us, e0, e1); us = us * 1000 / reps;
+      }
+      if (mode >= 1 && N == 16) {
+        printf("  C[0][0..7]:"); for (int j = 0; j < 8; ++j) printf(" %.6f", C[j]); printf("\n");
+        printf("  R[0][0..7]:");
+        for (int j = 0; j < 8; ++j) { long double s2 = 0; for (int64_t k = 0; k < K; ++k) s2 += (long double)(trans ? A[k * n] : A[k]) * B[k * N + j]; printf(" %.6f", (double)s2); }
+        printf("\n  C[1][0..7]:"); for (int j = 0; j < 8; ++j) printf(" %.6f", C[N + j]); printf("\n");
+      }
+      printf("trans %d N %2d: max|C-R| %.3e (max|R| %.3e)  max |C-R|/sum|a x| %.3e  %s  %.1f us\n", trans, N, emax_abs, rmax,
+             emax_rel, emax_rel < 1e-13 ? "OK" : "FAIL", us);
+    }
+  int fl; CK(cudaMemcpy(&fl, flag, 4, cudaMemcpyDeviceToHost));
+  printf("flag %d\n", fl);
+  return 0;
+}
