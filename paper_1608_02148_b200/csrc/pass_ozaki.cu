@@ -41,14 +41,20 @@ constexpr int BM = 128, BKO = 128, THREADS = 256;
 // A-slice pipeline stages: as many 16 KB stages as fit next to two X buffers
 __host__ __device__ constexpr int nsa_for(int S, int N) { return (220 * 1024 - 2 * S * N * 128 - 2048) / (128 * 128) > 6 ? 6 : (220 * 1024 - 2 * S * N * 128 - 2048) / (128 * 128); }
 constexpr int A_TILE = BM * BKO;                    // bytes of one slice tile
-constexpr int KSUP = 4, ET = KSUP * BKO;            // exponent super-tiles: 512 x 512 of A, 512-row blocks of X;
-                                                    // int32 accumulation over 512 k (<= 512 * 127^2 < 2^23)
+constexpr int KSUP = 8, ET = KSUP * BKO;            // exponent super-tiles: 1024 x 1024 of A, 1024-row blocks of X;
+                                                    // int32 accumulation over 1024 k: <= 8 pairs * 1024 * 127^2 < 2^27
 
 __host__ __device__ inline int64_t unit_lo(int64_t units, int grid, int c) { return (units * (int64_t)c) / grid; }
 #ifndef OZ_PROBE
 #define OZ_PROBE_DECL
 #define OZ_PROBE(slot)
 #define OZ_PROBE_OUT
+#define OZ_PROBE2_DECL
+#define OZ_PROBE2(slot)
+#define OZ_PROBE2_OUT
+#define OZ_PROBE3_DECL
+#define OZ_PROBE3(slot)
+#define OZ_PROBE3_OUT
 #endif
 
 __device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
@@ -255,21 +261,39 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
+      OZ_PROBE2_DECL
       for (int64_t it = 0; it < nun; ++it) {
         const int64_t u = u_lo + it, mb = u / KB, kb = u - mb * KB;
         const int xb = (int)(it & 1);
+        OZ_PROBE2(0)
         mbar_wait(&xempty[xb], (uint32_t)(((it >> 1) & 1) ^ 1));
+        OZ_PROBE2(1)
+#ifdef OZ_SKIP_X
+        mbar_arrive(&xfull[xb]);
+#else
         mbar_expect_tx(&xfull[xb], (uint32_t)(S * XSL));
         for (int t = 0; t < S; ++t) tma_2d(xbuf + xb * XBUF + t * XSL, &mapX, (int)(kb * BKO), t * g.Np, &xfull[xb]);
+#endif
         for (int t = 0; t < S; ++t) {
           const int64_t q = it * S + t;
           const int s = (int)(q % NSA);
+          OZ_PROBE2(0)
           mbar_wait(&aempty[s], (uint32_t)(((q / NSA) & 1) ^ 1));
+          OZ_PROBE2(2)
+#ifndef OZ_SKIP_A
           mbar_expect_tx(&afull[s], (uint32_t)A_TILE);
+#endif
+#ifdef OZ_SKIP_A
+          mbar_arrive(&afull[s]);
+          (void)mb;
+#else
           if (!TRANS) tma_4d(astage + s * A_TILE, &mapA, 0, t, (int)kb, (int)(mb * BM), &afull[s]);
           else tma_4d(astage + s * A_TILE, &mapA, 0, t, (int)mb, (int)(kb * BKO), &afull[s]);
+#endif
         }
       }
+      OZ_PROBE2(0)
+      OZ_PROBE2_OUT
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer
@@ -315,7 +339,9 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
               const int cnt = (S - t - u0) < CMAX ? (S - t - u0) : CMAX;
               const uint64_t db = dx0 + (uint64_t)((u0 * XSL + kk * 32) >> 4);
               const uint32_t idesc = idesc0 | ((uint32_t)((cnt * N) >> 3) << 17);
+#ifndef OZ_SKIP_MMA
               mma_i8(tmem + (uint32_t)((t + u0) * N), da, db, idesc, (t > 0 || kk > 0) ? 1u : acc0);
+#endif
             }
           }
           mma_commit(&aempty[s]);
@@ -337,13 +363,16 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
     for (int j = 0; j < N; ++j) acc[j] = 0.0;
     double* xfs = xfsm + (warp & 3) * 64;             // per-warp copy of this unit's column factors
     int64_t ndrain = 0;
+    OZ_PROBE3_DECL
     for (int64_t it = 0; it < nun; ++it) {
       const int64_t u = u_lo + it, mb = u / KB, kb = u - mb * KB;
       if (!((kb % KSUP == KSUP - 1) || kb == KB - 1 || it == nun - 1)) continue;
       const double eaf = TRANS ? g.ea[(kb / KSUP) * g.ea_ld + mb / KSUP] : g.ea[(mb / KSUP) * g.ea_ld + kb / KSUP];
       for (int j = lane; j < N; j += 32) xfs[j] = eaf * g.xf[(kb / KSUP) * g.Np + j];
       __syncwarp();
+      OZ_PROBE3(0)
       mbar_wait(&accf, (uint32_t)(ndrain & 1));
+      OZ_PROBE3(1)
       ++ndrain;
       tc_fence_after();
       // 8 columns at a time: the S group loads are issued back to back, one wait
@@ -369,6 +398,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acce);
+      OZ_PROBE3(2)
       if (kb == KB - 1 || it == nun - 1) {
         // stream-K fix-up (see gemm_pass.cu)
         const int64_t rb_lo = mb * KB, rb_hi = rb_lo + KB;
@@ -409,7 +439,10 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
 #pragma unroll
         for (int j = 0; j < N; ++j) acc[j] = 0.0;
       }
+      OZ_PROBE3(3)
     }
+    OZ_PROBE3(0)
+    OZ_PROBE3_OUT
   }
   tc_fence_before();
   __syncthreads();

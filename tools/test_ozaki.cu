@@ -9,6 +9,13 @@ __device__ unsigned long long g_oz[8];
 #define OZ_PROBE_DECL long long _ozt[5] = {0, 0, 0, 0, 0}; long long _ozl = clock64();
 #define OZ_PROBE(slot) { long long _t = clock64(); _ozt[slot] += _t - _ozl; _ozl = _t; }
 #define OZ_PROBE_OUT for (int q = 0; q < 5; ++q) atomicAdd(&g_oz[q], (unsigned long long)_ozt[q]);
+__device__ unsigned long long g_oz2[4], g_oz3[4];
+#define OZ_PROBE2_DECL long long _p2[3] = {0, 0, 0}; long long _p2l = clock64();
+#define OZ_PROBE2(slot) { long long _t = clock64(); _p2[slot] += _t - _p2l; _p2l = _t; }
+#define OZ_PROBE2_OUT for (int q = 0; q < 3; ++q) atomicAdd(&g_oz2[q], (unsigned long long)_p2[q]);
+#define OZ_PROBE3_DECL long long _p3[4] = {0, 0, 0, 0}; long long _p3l = clock64();
+#define OZ_PROBE3(slot) if (lane == 0) { long long _t = clock64(); _p3[slot] += _t - _p3l; _p3l = _t; }
+#define OZ_PROBE3_OUT if (lane == 0) for (int q = 0; q < 4; ++q) atomicAdd(&g_oz3[q], (unsigned long long)_p3[q]);
 #include "../paper_1608_02148_b200/csrc/pass_tf32.cu"
 #include "../paper_1608_02148_b200/csrc/pass_ozaki.cu"
 namespace rsvd { int64_t g_kernel_launches = 0; }
@@ -43,7 +50,7 @@ int main(int argc, char** argv) {
   CK(cudaDeviceSynchronize());
   {
     std::vector<int8_t> sl((size_t)OZ_S * m * oa.ldn);
-    const int64_t tiles = ceil_div(m, 512) * oa.ntiles;
+    const int64_t tiles = ceil_div(m, 1024) * oa.ntiles;
     std::vector<double> ea(tiles);
     CK(cudaMemcpy(sl.data(), oa.slices, sl.size(), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(ea.data(), oa.ea, tiles * 8, cudaMemcpyDeviceToHost));
@@ -51,8 +58,8 @@ int main(int argc, char** argv) {
     for (int64_t i = 0; i < m; ++i) for (int64_t j = 0; j < n; ++j) {
       long double v = 0, w = 1.0L / 128;
       for (int t = 0; t < OZ_S; ++t) { v += sl[((i * (oa.ldn / 128) + j / 128) * OZ_S + t) * 128 + j % 128] * w; w /= 128; }
-      v *= ea[(i / 512) * oa.ntiles + j / 512];
-      const double tile_max = ea[(i / 512) * oa.ntiles + j / 512];
+      v *= ea[(i / 1024) * oa.ntiles + j / 1024];
+      const double tile_max = ea[(i / 1024) * oa.ntiles + j / 1024];
       e = fmax(e, fabs((double)(v - A[i * n + j])) / tile_max);
     }
     printf("A slice reconstruction: max |err| / 2^E_tile = %.3e (expect < 2^-56 = %.1e)\n", e, ldexp(1.0, -56));
@@ -92,6 +99,11 @@ int main(int argc, char** argv) {
         const double tot = pr[0] + pr[1] + pr[2] + pr[3] + pr[4];
         printf("  MMA thread time: issue %.1f%%  wait xfull %.1f%%  wait acce %.1f%%  wait afull %.1f%%  mma-issue %.1f%%\n",
                100 * pr[0] / tot, 100 * pr[1] / tot, 100 * pr[2] / tot, 100 * pr[3] / tot, 100 * pr[4] / tot);
+        unsigned long long p2[4], p3[4]; cudaMemcpyFromSymbol(p2, g_oz2, sizeof p2); cudaMemcpyFromSymbol(p3, g_oz3, sizeof p3);
+        cudaMemcpyToSymbol(g_oz2, z, sizeof z); cudaMemcpyToSymbol(g_oz3, z, sizeof z);
+        const double t2 = p2[0] + p2[1] + p2[2], t3 = p3[0] + p3[1] + p3[2] + p3[3];
+        printf("  producer: issue %.1f%%  wait xempty %.1f%%  wait aempty %.1f%% | epilogue: other %.1f%%  wait accf %.1f%%  drain %.1f%%  write-out %.1f%%\n",
+               100 * p2[0] / t2, 100 * p2[1] / t2, 100 * p2[2] / t2, 100 * p3[0] / t3, 100 * p3[1] / t3, 100 * p3[2] / t3, 100 * p3[3] / t3);
       }
       float us = 0;
       if (reps > 0) {
