@@ -222,29 +222,33 @@ struct Args {
   int64_t KB, units; int grid;
 };
 
+// One unit = (128-row output block, 64-k block): 8 A-slice tiles (128 x 64 B)
+// + the S X-slice tiles (N x 64 B), 64 + 8N KB, loaded as one transaction
+// into one of two unit buffers, so the whole next unit streams in while the
+// current one is multiplied.
+constexpr int BKU = 64;                             // k per unit
+constexpr int KSU = ET / BKU;                       // units per exponent super-block (16)
+constexpr int A_UT = BM * BKU;                      // bytes of one A-slice tile of a unit
+
 template <bool TRANS, int S, int N>
 __global__ void __launch_bounds__(THREADS, 1)
 ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapX, Args g) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int NSA = nsa_for(S, N);
-  constexpr int XSL = N * BKO;                      // bytes of one X slice (N rows x 128 k)
-  constexpr int XBUF = ((S * XSL + 1023) / 1024) * 1024;
-  unsigned char* astage = base;
-  unsigned char* xbuf = base + NSA * A_TILE;
-  __shared__ uint64_t afull[NSA], aempty[NSA], xfull[2], xempty[2], accf, acce;
+  constexpr int XSL = N * BKU;                      // bytes of one X slice tile (N rows x 64 k)
+  constexpr int UBUF = ((S * A_UT + S * XSL) + 1023) / 1024 * 1024;
+  __shared__ uint64_t ufull[2], uempty[2], accf, acce;
   __shared__ uint32_t tmem_base;
   __shared__ double xfsm[4 * 64];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t KB = g.KB;
+  const int64_t KB = g.KB;                          // 64-k blocks
   const int64_t u_lo = unit_lo(g.units, g.grid, blockIdx.x);
   const int64_t u_hi = unit_lo(g.units, g.grid, blockIdx.x + 1);
   const int64_t nun = u_hi - u_lo;
 
   if (tid == 0) {
-    for (int s = 0; s < NSA; ++s) { mbar_init(&afull[s], 1); mbar_init(&aempty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&xfull[s], 1); mbar_init(&xempty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&ufull[s], 1); mbar_init(&uempty[s], 1); }
     mbar_init(&accf, 1);
     mbar_init(&acce, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -259,38 +263,23 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   const uint32_t tmem = tmem_base;
 
   if (warp == 0) {
-    // ---------------- TMA producer
+    // ---------------- TMA producer: one transaction per unit
     if (lane == 0) {
       OZ_PROBE2_DECL
       for (int64_t it = 0; it < nun; ++it) {
         const int64_t u = u_lo + it, mb = u / KB, kb = u - mb * KB;
-        const int xb = (int)(it & 1);
+        const int ub = (int)(it & 1);
+        unsigned char* ubuf = base + ub * UBUF;
         OZ_PROBE2(0)
-        mbar_wait(&xempty[xb], (uint32_t)(((it >> 1) & 1) ^ 1));
+        mbar_wait(&uempty[ub], (uint32_t)(((it >> 1) & 1) ^ 1));
         OZ_PROBE2(1)
-#ifdef OZ_SKIP_X
-        mbar_arrive(&xfull[xb]);
-#else
-        mbar_expect_tx(&xfull[xb], (uint32_t)(S * XSL));
-        for (int t = 0; t < S; ++t) tma_2d(xbuf + xb * XBUF + t * XSL, &mapX, (int)(kb * BKO), t * g.Np, &xfull[xb]);
-#endif
+        mbar_expect_tx(&ufull[ub], (uint32_t)(S * A_UT + S * XSL));
         for (int t = 0; t < S; ++t) {
-          const int64_t q = it * S + t;
-          const int s = (int)(q % NSA);
-          OZ_PROBE2(0)
-          mbar_wait(&aempty[s], (uint32_t)(((q / NSA) & 1) ^ 1));
-          OZ_PROBE2(2)
-#ifndef OZ_SKIP_A
-          mbar_expect_tx(&afull[s], (uint32_t)A_TILE);
-#endif
-#ifdef OZ_SKIP_A
-          mbar_arrive(&afull[s]);
-          (void)mb;
-#else
-          if (!TRANS) tma_4d(astage + s * A_TILE, &mapA, 0, t, (int)kb, (int)(mb * BM), &afull[s]);
-          else tma_4d(astage + s * A_TILE, &mapA, 0, t, (int)mb, (int)(kb * BKO), &afull[s]);
-#endif
+          if (!TRANS) tma_4d(ubuf + t * A_UT, &mapA, (int)((kb & 1) * BKU), t, (int)(kb >> 1), (int)(mb * BM), &ufull[ub]);
+          else tma_4d(ubuf + t * A_UT, &mapA, 0, t, (int)mb, (int)(kb * BKU), &ufull[ub]);
         }
+        for (int t = 0; t < S; ++t) tma_2d(ubuf + S * A_UT + t * XSL, &mapX, (int)(kb * BKU), t * g.Np, &ufull[ub]);
+        OZ_PROBE2(2)
       }
       OZ_PROBE2(0)
       OZ_PROBE2_OUT
@@ -298,9 +287,8 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   } else if (warp == 1) {
     // ---------------- MMA issuer
     if (lane == 0) {
-      // X slices u0..u0+c-1 are consecutive N-row blocks in shared memory and their
-      // groups t+u0..t+u0+c-1 consecutive N-column blocks of TMEM, so one MMA with
-      // N_mma = c N covers them all (c N <= 256).
+      // X slices u0..u0+c-1 are consecutive N-row tiles and their groups t+u0..t+u0+c-1
+      // consecutive N-column blocks of TMEM: one MMA with N_mma = c N covers them (<= 256)
       const uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((TRANS ? 1u : 0u) << 15) | (0u << 16) |
                               ((uint32_t)(BM >> 4) << 24);
       constexpr int CMAX = 256 / N;
@@ -309,33 +297,26 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       bool fresh = true;
       for (int64_t it = 0; it < nun; ++it) {
         const int64_t u = u_lo + it, kb = u % KB;
-        const bool drain = (kb % KSUP == KSUP - 1) || kb == KB - 1 || it == nun - 1;
-        const int xb = (int)(it & 1);
+        const bool drain = (kb % KSU == KSU - 1) || kb == KB - 1 || it == nun - 1;
+        const int ub = (int)(it & 1);
         OZ_PROBE(0)
-        mbar_wait(&xfull[xb], (uint32_t)((it >> 1) & 1));
-        OZ_PROBE(1)
+        mbar_wait(&ufull[ub], (uint32_t)((it >> 1) & 1));
+        OZ_PROBE(3)
         if (fresh && ndrain > 0) mbar_wait(&acce, (uint32_t)((ndrain - 1) & 1));
         OZ_PROBE(2)
         tc_fence_after();
-        const uint64_t dx0 = sdesc(smem_u32(xbuf + xb * XBUF), 16, 1024);
+        const uint32_t ua = smem_u32(base + ub * UBUF);
+        const uint64_t dx0 = sdesc(ua + S * A_UT, 16, 512, LAYOUT_SW64);
         const uint32_t acc0 = fresh ? 0u : 1u;
 #pragma unroll
         for (int t = 0; t < S; ++t) {
-          const int64_t q = it * S + t;
-          const int s = (int)(q % NSA);
-          OZ_PROBE(0)
-          mbar_wait(&afull[s], (uint32_t)((q / NSA) & 1));
-          OZ_PROBE(3)
-          tc_fence_after();
-          // descriptors differ only in the start-address field (address >> 4, low 14 bits):
-          // K-major (NN) k-steps are +32 B, MN-major (TN) k-steps +32 rows of 128 B
-          const uint64_t da0 = sdesc(smem_u32(astage + s * A_TILE), 16, 1024);
+          // NN: A tile K-major, 64 B rows (SW64, k-step +32 B); TN: MN-major, 128 B rows (SW128, k-step +32 rows)
+          const uint64_t da0 = TRANS ? sdesc(ua + t * A_UT, 16, 1024, LAYOUT_SW128) : sdesc(ua + t * A_UT, 16, 512, LAYOUT_SW64);
 #pragma unroll
-          for (int kk = 0; kk < BKO / 32; ++kk) {
+          for (int kk = 0; kk < BKU / 32; ++kk) {
             const uint64_t da = da0 + (uint64_t)(TRANS ? kk * 256 : kk * 2);
 #pragma unroll
             for (int u0 = 0; u0 < S - t; u0 += CMAX) {
-              constexpr int dummy = 0; (void)dummy;
               const int cnt = (S - t - u0) < CMAX ? (S - t - u0) : CMAX;
               const uint64_t db = dx0 + (uint64_t)((u0 * XSL + kk * 32) >> 4);
               const uint32_t idesc = idesc0 | ((uint32_t)((cnt * N) >> 3) << 17);
@@ -344,10 +325,9 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
 #endif
             }
           }
-          mma_commit(&aempty[s]);
-          OZ_PROBE(4)
         }
-        mma_commit(&xempty[xb]);
+        OZ_PROBE(4)
+        mma_commit(&uempty[ub]);
         if (drain) { mma_commit(&accf); ++ndrain; }
         fresh = drain;
       }
@@ -361,14 +341,15 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
     double acc[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) acc[j] = 0.0;
-    double* xfs = xfsm + (warp & 3) * 64;             // per-warp copy of this unit's column factors
+    double* xfs = xfsm + (warp & 3) * 64;             // per-warp copy of this super-block's column factors
     int64_t ndrain = 0;
     OZ_PROBE3_DECL
     for (int64_t it = 0; it < nun; ++it) {
       const int64_t u = u_lo + it, mb = u / KB, kb = u - mb * KB;
-      if (!((kb % KSUP == KSUP - 1) || kb == KB - 1 || it == nun - 1)) continue;
-      const double eaf = TRANS ? g.ea[(kb / KSUP) * g.ea_ld + mb / KSUP] : g.ea[(mb / KSUP) * g.ea_ld + kb / KSUP];
-      for (int j = lane; j < N; j += 32) xfs[j] = eaf * g.xf[(kb / KSUP) * g.Np + j];
+      if (!((kb % KSU == KSU - 1) || kb == KB - 1 || it == nun - 1)) continue;
+      const int64_t sb = kb / KSU, sm_ = mb * BM / ET;      // super-block along k, super-tile along m
+      const double eaf = TRANS ? g.ea[sb * g.ea_ld + sm_] : g.ea[sm_ * g.ea_ld + sb];
+      for (int j = lane; j < N; j += 32) xfs[j] = eaf * g.xf[sb * g.Np + j];
       __syncwarp();
       OZ_PROBE3(0)
       mbar_wait(&accf, (uint32_t)(ndrain & 1));
@@ -454,27 +435,29 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
 
 // ---------------------------------------------------------------- host side
 // slices as a 4-D tensor (byte j < 128, slice t, column block, row) over the
-// interleaved layout; box {128, 1, 1, 128} = one 128 x 128 slice tile
-static bool map_slices(CUtensorMap* mp, const int8_t* p, int64_t rows, int64_t nblk, int S) {
+// interleaved layout.  NN unit tile: 128 rows x 64 B (box {64, 1, 1, 128},
+// SW64, K-major); TN unit tile: 64 rows x 128 B (box {128, 1, 1, 64}, SW128,
+// MN-major operand).
+static bool map_slices(CUtensorMap* mp, const int8_t* p, int64_t rows, int64_t nblk, int S, bool trans) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[4] = {128, (cuuint64_t)S, (cuuint64_t)nblk, (cuuint64_t)rows};
   cuuint64_t strides[3] = {128, (cuuint64_t)(128 * S), (cuuint64_t)(128 * S * nblk)};
-  cuuint32_t box[4] = {128, 1, 1, 128};
+  cuuint32_t box[4] = {trans ? 128u : 64u, 1, 1, trans ? 64u : 128u};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(p), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             CU_TENSOR_MAP_INTERLEAVE_NONE, trans ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 static bool map_i8_2d(CUtensorMap* mp, const int8_t* p, int64_t cols, int64_t rows, int64_t ld, int box_rows) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld};
-  cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   return enc(mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(p), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -535,21 +518,21 @@ cudaError_t ozaki_pass(const OzakiCall& c, cudaStream_t st) {
   }
   // 2) tensor maps: A slices as (cols = n, rows = m, S); X slices as (cols = K, rows = S * N)
   CUtensorMap mA, mX;
-  if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, OZ_S)) return cudaErrorInvalidValue;
+  if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, OZ_S, c.trans)) return cudaErrorInvalidValue;
   if (!map_i8_2d(&mX, xs, c.K, (int64_t)OZ_S * N, ldk, N)) return cudaErrorInvalidValue;
   Args g{};
   g.C = c.C; g.ldc = c.ldc; g.P = c.P; g.flags = c.flags; g.epoch = c.epoch;
   g.ea = a.ea; g.ea_ld = a.ntiles; g.xf = xf;
   g.M = c.M; g.K = c.K; g.N = N; g.Nout = c.Nout; g.Np = N;
-  g.KB = KB;
+  g.KB = ceil_div(c.K, BKU);
   const int64_t mblocks = ceil_div(c.M, BM);
-  g.units = mblocks * KB;
+  g.units = mblocks * g.KB;
   int64_t grid = g.units / 4;
   if (grid < mblocks) grid = mblocks;
   if (grid > c.grid) grid = c.grid;
   if (grid < 1) grid = 1;
   g.grid = (int)grid;
-  const size_t smem = (size_t)nsa_for(OZ_S, N) * A_TILE + 2 * (size_t)(((OZ_S * N * BKO) + 1023) / 1024 * 1024) + 1024;
+  const size_t smem = 2 * (size_t)((OZ_S * A_UT + OZ_S * N * BKU + 1023) / 1024 * 1024) + 1024;
   cudaError_t e = cudaSuccess;
 #define RSVD_OZ(TR, NN)                                                                                   \
   {                                                                                                      \

@@ -41,7 +41,7 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 // SWIZZLE_128B (K-major operands); layout 1 = SWIZZLE_128B_BASE32B, the only
 // swizzled layout tcgen05 accepts for MN-major 32-bit (tf32) operands; its TMA
 // counterpart is CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B (4-row 512 B K atoms).
-constexpr uint32_t LAYOUT_SW128 = 2, LAYOUT_SW128_BASE32B = 1;
+constexpr uint32_t LAYOUT_SW128 = 2, LAYOUT_SW128_BASE32B = 1, LAYOUT_SW64 = 4;
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout = LAYOUT_SW128) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFF);
