@@ -264,7 +264,8 @@ rsvd_status pass_tf32(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, doubl
 rsvd_status pass_ozaki(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, double* C, int64_t M, int64_t K) {
   OzakiCall o{};
   o.a = &p.oz; o.trans = trans; o.B = B; o.ldb = p.Np; o.C = C; o.ldc = p.Np; o.Nout = p.Np;
-  o.P = p.part; o.flags = ctx->gemm_flags; o.epoch = ++ctx->gemm_epoch; o.xscratch = p.ozx;
+  o.P = p.part; o.flags = ctx->gemm_flags; o.epoch = ++ctx->gemm_epoch; o.epoch2 = ++ctx->gemm_epoch;
+  o.xscratch = p.ozx;
   o.M = M; o.K = K; o.N = p.Np; o.grid = ctx->num_sms;
   ++ctx->ozaki_calls;
   CK(ozaki_pass(o, ctx->stream));
@@ -568,7 +569,7 @@ rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bo
   if (p.use_ozaki) {
     // slices of the stored matrix (A->m_local x A->n), then the X slice scratch
     const size_t sa = align256(ozaki_a_bytes(A->m_local, A->n));
-    const size_t sx = align256(ozaki_x_bytes(std::max(p.M, p.n), p.Np));
+    const size_t sx = align256(ozaki_x_bytes(std::max(p.M, p.n), std::min(p.Np, 64)));
     if (sa + sx > ctx->ws4_bytes) {
       if (ctx->ws4) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->ws4); ctx->ws4 = nullptr; ctx->ws4_bytes = 0; }
       if (cudaMalloc(&ctx->ws4, sa + sx) != cudaSuccess) {

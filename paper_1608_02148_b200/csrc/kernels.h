@@ -72,9 +72,10 @@ cudaError_t ozaki_slice_a(const OzakiA& a, const double* A, int64_t lda, const d
                           cudaStream_t st);
 struct OzakiCall {
   const OzakiA* a; bool trans;                   // trans: C = f(A)^T B (M = n, K = m), else C = f(A) B
-  const double* B; int64_t ldb;                  // K x N panel (FP64), N = Np <= 64
+  const double* B; int64_t ldb;                  // K x N panel (FP64), N = Np <= 128 (two launches above 64)
   double* C; int64_t ldc; int Nout;
   double* P; unsigned* flags; unsigned epoch;    // stream-K partials / flags as GemmCall
+  unsigned epoch2;                               // second column block (N > 64)
   void* xscratch;                                // >= ozaki_x_bytes(K, N)
   int64_t M, K; int N; int grid;
 };

@@ -168,10 +168,13 @@ ozaki_slice_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64
 }
 
 // X (K x Np, ldx) -> xs[u][j][k] (u < S, j < Np, ld ldk bytes) and
-// xf[sb * Np + j] = 2^E(sb, j) for 512-row super-blocks sb.
-// (1) column maxima per 16-row chunk, (2) one thread per (16-row chunk, column).
+// xf[sb * Np + j] = 2^E(sb, j) for 1024-row super-blocks sb.
+// (1) column maxima per super-block: one thread per (16-row chunk, column),
+// combined with an integer atomicMax on the bit pattern (monotone for
+// non-negative doubles, order-independent => deterministic) into a zeroed
+// array; (2) one thread per (16-row chunk, column) slices.
 __global__ void __launch_bounds__(256)
-ozaki_xmax_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, double* __restrict__ cmax) {
+ozaki_xmax_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, double* __restrict__ smax) {
   const int j = threadIdx.x % 32 + 32 * blockIdx.y, r = threadIdx.x / 32;
   const int64_t kc = (int64_t)blockIdx.x * 8 + r;           // 16-row chunk
   if (j >= Np || kc * 16 >= K) return;
@@ -179,7 +182,8 @@ ozaki_xmax_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, 
 #pragma unroll
   for (int k = 0; k < 16; ++k)
     if (kc * 16 + k < K) mx = fmax(mx, fabs(X[(kc * 16 + k) * ldx + j]));
-  cmax[kc * Np + j] = mx;
+  atomicMax(reinterpret_cast<unsigned long long*>(smax) + (kc * 16 / ET) * Np + j,
+            (unsigned long long)__double_as_longlong(mx));
 }
 
 template <int S>
@@ -189,11 +193,8 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
   const int j = threadIdx.x % 32 + 32 * blockIdx.y, r = threadIdx.x / 32;
   const int64_t kc = (int64_t)blockIdx.x * 8 + r;
   if (j >= Np || kc * 16 >= ldk) return;
-  const int64_t nch = ceil_div(K, 16);
-  const int64_t sb = kc / (ET / 16), c0 = sb * (ET / 16);
-  double mx = 0.0;
-  for (int64_t c = c0; c < min(nch, c0 + ET / 16); ++c) mx = fmax(mx, cmax[c * Np + j]);
-  const int E = block_exp(mx);
+  const int64_t sb = kc / (ET / 16);
+  const int E = block_exp(cmax[sb * Np + j]);
   if (kc % (ET / 16) == 0) xf[sb * Np + j] = ldexp(1.0, E);
   const double scale = ldexp(1.0, 7 * S - E);
   uint32_t w[4][S];
@@ -465,7 +466,9 @@ static bool map_i8_2d(CUtensorMap* mp, const int8_t* p, int64_t cols, int64_t ro
 
 int ozaki_slices() { return OZ_S; }
 
-bool ozaki_supported(int Np) { return Np <= 64 && Np % 16 == 0 && tc::get_encode() != nullptr; }
+// Np <= 64 in one launch; 64 < Np <= 128 as two column blocks (64, Np - 64),
+// each its own launch over the same A slices (TMEM holds 8 groups x 64 columns)
+bool ozaki_supported(int Np) { return Np <= 128 && Np % 16 == 0 && tc::get_encode() != nullptr; }
 
 size_t ozaki_a_bytes(int64_t m, int64_t n) {
   const int64_t ldn = round_up(n, oz::BKO);
@@ -498,11 +501,25 @@ OzakiA ozaki_layout_a(void* buf, int64_t m, int64_t n) {
   return a;
 }
 
+static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st);
+
 cudaError_t ozaki_pass(const OzakiCall& c, cudaStream_t st) {
+  if (!ozaki_supported(c.N) || c.M <= 0 || c.K <= 0) return cudaErrorInvalidValue;
+  if (c.N <= 64) return ozaki_pass_cols(c, st);
+  OzakiCall h = c;                                   // columns [0, 64): B, C with their own leading dimensions
+  h.N = 64; h.Nout = c.Nout < 64 ? c.Nout : 64;
+  cudaError_t e = ozaki_pass_cols(h, st);
+  if (e != cudaSuccess) return e;
+  h = c;                                             // columns [64, N)
+  h.B = c.B + 64; h.C = c.C + 64; h.N = c.N - 64; h.Nout = c.Nout - 64; h.epoch = c.epoch2;
+  if (h.Nout <= 0) return cudaSuccess;
+  return ozaki_pass_cols(h, st);
+}
+
+static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
   using namespace oz;
   const OzakiA& a = *c.a;
   const int N = c.N;
-  if (!ozaki_supported(N) || c.M <= 0 || c.K <= 0) return cudaErrorInvalidValue;
   // 1) X slices
   const int64_t ldk = round_up(c.K, 16);
   int8_t* xs = reinterpret_cast<int8_t*>(c.xscratch);
@@ -510,16 +527,25 @@ cudaError_t ozaki_pass(const OzakiCall& c, cudaStream_t st) {
   const int64_t KB = ceil_div(c.K, BKO);
   double* cmax = xf + round_up(ceil_div(c.K, ET) * N, 32);
   {
+    cudaMemsetAsync(cmax, 0, (size_t)ceil_div(c.K, ET) * N * sizeof(double), st);
     const dim3 gx((unsigned)ceil_div(ceil_div(c.K, 16), 8), (unsigned)ceil_div(N, 32));
     ozaki_xmax_kernel<<<gx, 256, 0, st>>>(c.B, c.ldb, c.K, N, cmax);
     const dim3 gs((unsigned)ceil_div(ldk / 16, 8), (unsigned)ceil_div(N, 32));
     ozaki_slice_x_kernel<OZ_S><<<gs, 256, 0, st>>>(c.B, c.ldb, c.K, N, cmax, xs, ldk, xf);
+#ifdef OZ_DEBUG
+    { cudaError_t ee = cudaGetLastError(); if (ee) printf("x slicing: %s (N %d K %lld gx %u %u gs %u %u)\n", cudaGetErrorString(ee), N, (long long)c.K, gx.x, gx.y, gs.x, gs.y); }
+#endif
     g_kernel_launches += 2;
   }
   // 2) tensor maps: A slices as (cols = n, rows = m, S); X slices as (cols = K, rows = S * N)
   CUtensorMap mA, mX;
   if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, OZ_S, c.trans)) return cudaErrorInvalidValue;
-  if (!map_i8_2d(&mX, xs, c.K, (int64_t)OZ_S * N, ldk, N)) return cudaErrorInvalidValue;
+  if (!map_i8_2d(&mX, xs, c.K, (int64_t)OZ_S * N, ldk, N)) {
+#ifdef OZ_DEBUG
+    printf("map X failed: xs %p K %lld rows %lld ldk %lld box %d\n", (void*)xs, (long long)c.K, (long long)OZ_S * N, (long long)ldk, N);
+#endif
+    return cudaErrorInvalidValue;
+  }
   Args g{};
   g.C = c.C; g.ldc = c.ldc; g.P = c.P; g.flags = c.flags; g.epoch = c.epoch;
   g.ea = a.ea; g.ea_ld = a.ntiles; g.xf = xf;

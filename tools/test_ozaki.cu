@@ -43,7 +43,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&abuf, ozaki_a_bytes(m, n))); CK(cudaMalloc(&flag, 64)); CK(cudaMemset(flag, 0, 64));
   CK(cudaMalloc(&flags, 4096 * 4)); CK(cudaMemset(flags, 0, 4096 * 4));
   const int64_t big = m > n ? m : n;
-  CK(cudaMalloc(&dB, big * 64 * 8)); CK(cudaMalloc(&dC, big * 64 * 8)); CK(cudaMalloc(&dP, (size_t)nsm * 128 * 64 * 8));
+  CK(cudaMalloc(&dB, big * 128 * 8)); CK(cudaMalloc(&dC, big * 128 * 8)); CK(cudaMalloc(&dP, (size_t)nsm * 128 * 64 * 8));
   CK(cudaMalloc(&xbuf, ozaki_x_bytes(big, 64)));
   OzakiA oa = ozaki_layout_a(abuf, m, n);
   CK(ozaki_slice_a(oa, dA, n, nullptr, nullptr, flag, 0));
@@ -66,7 +66,7 @@ int main(int argc, char** argv) {
   }
   unsigned epoch = 0;
   for (int trans = 0; trans < 2; ++trans)
-    for (int N : {16, 32, 64}) {
+    for (int N : {16, 32, 64, 96, 128}) {
       const int64_t M = trans ? n : m, K = trans ? m : n;
       std::vector<double> B(K * N), C(M * N, -7.0);
       for (int64_t k = 0; k < K; ++k) for (int j = 0; j < N; ++j) {
@@ -76,8 +76,8 @@ int main(int argc, char** argv) {
       CK(cudaMemcpy(dB, B.data(), K * N * 8, cudaMemcpyHostToDevice));
       OzakiCall c{};
       c.a = &oa; c.trans = trans; c.B = dB; c.ldb = N; c.C = dC; c.ldc = N; c.Nout = N; c.P = dP; c.flags = flags;
-      c.epoch = ++epoch; c.xscratch = xbuf; c.M = M; c.K = K; c.N = N; c.grid = nsm;
-      CK(ozaki_pass(c, 0));
+      c.epoch = ++epoch; c.epoch2 = ++epoch; c.xscratch = xbuf; c.M = M; c.K = K; c.N = N; c.grid = nsm;
+      { cudaError_t e0 = ozaki_pass(c, 0); cudaError_t e1 = cudaDeviceSynchronize(); if (e0 || e1) { printf("ozaki_pass N=%d trans=%d: ret %s sync %s\n", N, trans, cudaGetErrorString(e0), cudaGetErrorString(e1)); continue; } }
       CK(cudaDeviceSynchronize());
       CK(cudaMemcpy(C.data(), dC, M * N * 8, cudaMemcpyDeviceToHost));
       double emax_abs = 0, emax_rel = 0, rmax = 0;
@@ -100,7 +100,7 @@ int main(int argc, char** argv) {
         printf("  MMA thread time: issue %.1f%%  wait xfull %.1f%%  wait acce %.1f%%  wait afull %.1f%%  mma-issue %.1f%%\n",
                100 * pr[0] / tot, 100 * pr[1] / tot, 100 * pr[2] / tot, 100 * pr[3] / tot, 100 * pr[4] / tot);
         unsigned long long p2[4], p3[4]; cudaMemcpyFromSymbol(p2, g_oz2, sizeof p2); cudaMemcpyFromSymbol(p3, g_oz3, sizeof p3);
-        cudaMemcpyToSymbol(g_oz2, z, sizeof z); cudaMemcpyToSymbol(g_oz3, z, sizeof z);
+        cudaMemcpyToSymbol(g_oz2, z, sizeof(g_oz2)); cudaMemcpyToSymbol(g_oz3, z, sizeof(g_oz3));
         const double t2 = p2[0] + p2[1] + p2[2], t3 = p3[0] + p3[1] + p3[2] + p3[3];
         printf("  producer: issue %.1f%%  wait xempty %.1f%%  wait aempty %.1f%% | epilogue: other %.1f%%  wait accf %.1f%%  drain %.1f%%  write-out %.1f%%\n",
                100 * p2[0] / t2, 100 * p2[1] / t2, 100 * p2[2] / t2, 100 * p3[0] / t3, 100 * p3[1] / t3, 100 * p3[2] / t3, 100 * p3[3] / t3);
@@ -109,7 +109,7 @@ int main(int argc, char** argv) {
       if (reps > 0) {
         cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        for (int r = 0; r < reps; ++r) { c.epoch = ++epoch; ozaki_pass(c, 0); }
+        for (int r = 0; r < reps; ++r) { c.epoch = ++epoch; c.epoch2 = ++epoch; ozaki_pass(c, 0); }
         cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&us, e0, e1); us = us * 1000 / reps;
       }
       if (mode >= 1 && N == 16) {
