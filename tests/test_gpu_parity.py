@@ -288,3 +288,45 @@ def test_rsvd_fp32_tcgen05_parity(rb, m, n, k, p, q):
     r = rb.rsvd(A.cuda(), k, p=p, q=q, seed=12)
     o = oracle.oracle_rsvd(An, k, p=p, q=q, seed=12)
     _check_parity(An.astype(np.float64), r, o, k, tol_d=1e-4, tol_orth=1e-5, floor=1e-6, gap_tol=1e-3, cos_tol=1e-5)
+
+
+# ----------------------------------------------------------------------------- FP64 pass paths
+def _ctx_with_path(rb, path):
+    import os
+    old = os.environ.get("RSVD_FP64_PATH")
+    os.environ["RSVD_FP64_PATH"] = path
+    try:
+        return rb.Context(0)
+    finally:
+        if old is None:
+            del os.environ["RSVD_FP64_PATH"]
+        else:
+            os.environ["RSVD_FP64_PATH"] = old
+
+
+@pytest.mark.parametrize("m,n,k,p", [(3000, 1100, 50, 10), (2500, 900, 100, 20)])
+def test_ozaki_and_dmma_paths_agree(rb, m, n, k, p):
+    """The Ozaki int8 tensor-core passes and the FP64 DMMA passes compute the
+    same products to FP64 accuracy: both match the oracle and each other."""
+    A = _decay_matrix(m, n, seed=21)
+    Ad = A.cuda()
+    c_oz, c_dm = _ctx_with_path(rb, "ozaki"), _ctx_with_path(rb, "dmma")
+    r_oz = rb.rsvd(Ad, k, p=p, q=2, seed=4, ctx=c_oz)
+    r_dm = rb.rsvd(Ad, k, p=p, q=2, seed=4, ctx=c_dm)
+    assert c_oz.stats()["ozaki_passes"] > 0 and c_dm.stats()["ozaki_passes"] == 0
+    d_oz, d_dm = _np(r_oz.d), _np(r_dm.d)
+    assert np.max(np.abs(d_oz - d_dm) / d_dm) <= 1e-11
+    o = oracle.oracle_rsvd(A.numpy(), k, p=p, q=2, seed=4)
+    _check_parity(A.numpy(), r_oz, o, k)
+    _check_parity(A.numpy(), r_dm, o, k)
+
+
+def test_rsvd_heterogeneous_row_scales(rb):
+    """Rows spanning six decades inside one exponent super-tile of the Ozaki
+    slices (the exponent is shared by 1024 x 1024 elements): parity holds."""
+    A = _decay_matrix(2200, 800, seed=33).numpy()
+    rng = np.random.default_rng(7)
+    A = A * (10.0 ** rng.uniform(-6, 0, size=(A.shape[0], 1)))
+    r = rb.rsvd(torch.from_numpy(A).cuda(), 30, p=10, q=2, seed=9)
+    o = oracle.oracle_rsvd(A, 30, p=10, q=2, seed=9)
+    _check_parity(A, r, o, 30)
