@@ -131,13 +131,21 @@ rsvd_status rsvd_rpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* pr
                       void* center, void* scale);
 
 /* Randomized robust PCA by inexact ALM, Alg. 7, with the
- * readings R17-R23 of DESIGN.md (mu_0 = 1.25/||A||_2, fixed target rank k,
- * fresh Omega stream t per iteration, mu <- min(1.5 mu, 1e7 mu_0)).
+ * readings R17-R23, R30 of DESIGN.md (mu_0 = 1.25/||A||_2, fresh Omega stream t per
+ * iteration, mu <- min(1.5 mu, 1e7 mu_0)).
  *   lambda  <= 0 selects max(m, n)^-1/2
  *   tol     stop when ||A - L - S||_F / ||A||_F < tol
- * FP64 only.  L, S: DEVICE m_local x n (ld >= n), caller-owned.
+ *   k       > 0: fixed target rank k (R22), needs k <= min(m, n), k + p <= 120;
+ *           0: adaptive target rank -- k = 2 at step (1), then step (7)
+ *           predict_rank (Remark 1): l = max(1, #{sigma_i > 1/mu}),
+ *           k <- l + 1 if l < k else min(l + ceil(0.05 min(m, n)), min(m, n)),
+ *           capped at min(min(m, n), 120 - p) (no deterministic-SVD switch, R30)
+ * FP64 only.  L, S: DEVICE m_local x n (ld == n), caller-owned; A contiguous.
  *   iters, final_residual: HOST out-params (nullable)
- *   trace: HOST, nullable, 3*maxiter doubles (residual, l, mu) per iteration */
+ *   trace: HOST, nullable, 4*maxiter doubles per iteration: (residual, l, mu,
+ *          target rank k used by that iteration's rsvd)
+ * Errors: RSVD_EINVAL (null, k < 0, maxiter < 1, tol <= 0), RSVD_EUNSUPPORTED
+ * (FP32, strided A/L/S, k beyond the envelope), RSVD_ENUMERIC (||A||_2 = 0). */
 typedef struct {
   double lambda, tol;
   int32_t maxiter;

@@ -135,25 +135,48 @@ def oracle_rpca(A, k, center=True, scale=False, retx=True, p=10, q=2,
     return out
 
 
+def predict_rank(d, mu_inv, k, minmn):
+    """Alg. 7 step (7) "k, l = predict_rank(Sigma, mu^-1)"; the paper
+    defers the rule to Lin et al. (Remark 1).  Reading R30:
+      l = max(1, #{d_i > mu^-1})
+      k_next = l + 1                                if l < k
+               min(l + ceil(0.05 minmn), minmn)    otherwise
+    Returns (k_next, l)."""
+    l = max(1, int(np.sum(np.asarray(d) > mu_inv)))
+    if l < k:
+        return l + 1, l
+    return min(l + int(np.ceil(0.05 * minmn)), minmn), l
+
+
 def oracle_rrpca(A, lam=None, maxiter=100, tol=1e-7, k=20, p=10, q=2,
-                 sdist="normal", seed=0, trace=False):
-    """Alg. 7 rrpca, the inexact ALM loop, readings R17-R23.
+                 sdist="normal", seed=0, trace=False, kmax=None, det_switch=True):
+    """Alg. 7 rrpca, the inexact ALM loop, readings R17-R23, R30.
 
     lambda = max(m,n)^-1/2;  ||A||_2 = sigma_1 of rsvd(A, 1, p, q,
     stream 0) (R18);  mu_0 = 1.25 / ||A||_2 (R17);  Z = A / J(A) with
     J(A) = max(||A||_2, ||A||_max / lambda) (R19);  S = 0.  Then repeat:
       (6)  [U, Sigma, V] = rsvd(A - S + Z/mu, k, p, q)   (fresh Omega: stream t, R23)
-      (7)  l = #{sigma_i > 1/mu}                         (fixed k, R22)
+      (7)  l = #{sigma_i > 1/mu}                         (fixed k > 0, R22)
+           k, l = predict_rank(Sigma, 1/mu)              (k = 0: adaptive, k starts at 2, R30)
       (8)  Sigma_l = soft_thres(sigma(1:l), 1/mu)
       (9)  L = U(:,1:l) Sigma_l V(:,1:l)^T
       (10) S = soft_thres(A - L + Z/mu, lambda/mu)
       (11) Z = Z + (A - L - S) mu
       (12) mu = min(1.5 mu, 1e7 mu_0)                    (R20)
       until ||A - L - S||_F / ||A||_F < tol  (R21; evaluated after step 11)
-    Returns dict(L, S, iters, residual, trace=[(res, l, mu)...]).
+    Adaptive mode: predicted k is capped at kmax (default min(m, n)); with
+    det_switch the truncated SVD of step (6) is the deterministic one (numpy
+    SVD) whenever k > min(m, n)/4 (Remark 2).
+    Returns dict(L, S, iters, residual, trace=[(res, l, mu, k)...]).
     """
     A = np.asarray(A, dtype=np.float64)
     m, n = A.shape
+    minmn = min(m, n)
+    adaptive = k == 0
+    if kmax is None:
+        kmax = minmn
+    if adaptive:
+        k = min(2, kmax)
     if lam is None or lam <= 0:
         lam = 1.0 / np.sqrt(max(m, n))
     norm2 = oracle_rsvd(A, 1, p=p, q=q, sdist=sdist, seed=seed, stream=0)["d"][0]
@@ -169,16 +192,24 @@ def oracle_rrpca(A, lam=None, maxiter=100, tol=1e-7, k=20, p=10, q=2,
     it = 0
     for it in range(1, maxiter + 1):
         M = A - S + Z / mu
-        r = oracle_rsvd(M, k, p=p, q=q, sdist=sdist, seed=seed, stream=it)
+        if adaptive and det_switch and k > minmn / 4:
+            uu, dd, vt = np.linalg.svd(M, full_matrices=False)
+            r = dict(u=uu[:, :k], d=dd[:k], v=vt[:k].T)
+        else:
+            r = oracle_rsvd(M, k, p=p, q=q, sdist=sdist, seed=seed, stream=it)
         d = r["d"]
         nl = int(np.sum(d > 1.0 / mu))
+        kused = k
+        if adaptive:
+            k, _ = predict_rank(d, 1.0 / mu, k, minmn)
+            k = min(k, kmax)
         dl = soft_threshold(d[:nl], 1.0 / mu)
         L = (r["u"][:, :nl] * dl[None, :]) @ r["v"][:, :nl].T
         S = soft_threshold(A - L + Z / mu, lam / mu)
         E = A - L - S
         Z = Z + E * mu
         res = np.sqrt(np.sum(E * E)) / normF
-        hist.append((res, nl, mu))
+        hist.append((res, nl, mu, kused))
         mu = min(1.5 * mu, 1e7 * mu0)
         if res < tol:
             break

@@ -287,7 +287,11 @@ def rpca(A, k, center=True, scale=False, retx=True, p=10, q=2, sdist="normal", s
 
 def rrpca(A, lam=None, maxiter=50, tol=1e-5, p=10, q=2, k=20, sdist="normal", seed=0, trace=False, ctx=None,
           m_global=None, row_offset=0):
-    """Randomized robust PCA by inexact ALM (Alg. 7; interface P:1736)."""
+    """Randomized robust PCA by inexact ALM (Alg. 7; interface P:1736).
+
+    k > 0 fixes the target rank; k = 0 selects the adaptive target rank of
+    Alg. 7 steps (1) and (7) (k = 2, then predict_rank; R30).
+    trace: per iteration (residual, l, mu, k)."""
     ctx = ctx or default_context(A.device)
     mat = _matrix(A, m_global, row_offset)
     prm = RrpcaParams()
@@ -300,10 +304,10 @@ def rrpca(A, lam=None, maxiter=50, tol=1e-5, p=10, q=2, k=20, sdist="normal", se
     S = torch.empty_like(A)
     it = ctypes.c_int32()
     res = ctypes.c_double()
-    tr = (ctypes.c_double * (3 * int(maxiter)))()
+    tr = (ctypes.c_double * (4 * int(maxiter)))()
     ctx.check(lib().rsvd_rrpca(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(L), _ptr(S), A.shape[1],
                                ctypes.byref(it), ctypes.byref(res), tr))
-    hist = [(tr[3 * i], int(tr[3 * i + 1]), tr[3 * i + 2]) for i in range(it.value)]
+    hist = [(tr[4 * i], int(tr[4 * i + 1]), tr[4 * i + 2], int(tr[4 * i + 3])) for i in range(it.value)]
     out = dict(L=L, S=S, iters=it.value, residual=res.value)
     if trace:
         out["trace"] = hist

@@ -858,28 +858,39 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
   if (ld < A->n) return fail(ctx, RSVD_EINVAL, "ld < n");
   if (A->lda != A->n || ld != A->n)
     return fail(ctx, RSVD_EUNSUPPORTED, "rrpca needs contiguous A, L, S (lda == ld == n)");
-  if (prm->maxiter < 1 || prm->k < 1 || prm->k > 32 || !(prm->tol > 0)) return fail(ctx, RSVD_EINVAL, "bad rrpca params (1 <= k <= 32, maxiter >= 1, tol > 0)");
+  if (prm->maxiter < 1 || prm->k < 0 || !(prm->tol > 0))
+    return fail(ctx, RSVD_EINVAL, "bad rrpca params (k >= 0, maxiter >= 1, tol > 0)");
+  const bool adaptive = prm->k == 0;   // Alg. 7 steps (1), (7): k = 2, predict_rank (reading R30)
   rsvd_params rp;
-  rsvd_params_default(&rp, prm->k);
+  rsvd_params_default(&rp, adaptive ? 1 : prm->k);
   rp.p = prm->p; rp.q = prm->q; rp.sdist = prm->sdist; rp.seed = prm->seed;
   int64_t mg, n;
   CKS(validate(ctx, A, &rp, &mg, &n));
   CK(cudaSetDevice(ctx->device));
   const int64_t m = A->m_local;
-  const int k = prm->k;
+  const int64_t minmn = std::min(mg, n);
+  // library envelope: l = k + p <= kMaxL (the deterministic-SVD switch of
+  // Remark 2, is not part of this library; R30)
+  const int kcap = (int)std::min<int64_t>(minmn, kMaxL - rp.p);
+  if (kcap < 1) return fail(ctx, RSVD_EUNSUPPORTED, "p = %d leaves no room for k under l <= %d", rp.p, kMaxL);
+  if (!adaptive && prm->k > kcap)
+    return fail(ctx, RSVD_EUNSUPPORTED, "k = %d exceeds min(m, n) or l = k + p <= %d", prm->k, kMaxL);
+  int k = adaptive ? std::min(2, kcap) : prm->k;
+  const int kbuf = adaptive ? kcap : prm->k;
   const double lam = prm->lambda > 0 ? prm->lambda : 1.0 / sqrt((double)std::max(mg, n));
   const double* Ad = (const double*)A->A;
   double* S = (double*)Sout;
   double* Lm = (double*)Lout;
-  // rrpca buffers: Z, M (m x n, ld n), U (m x k), V (n x k), d, dl, partials
+  // rrpca buffers: Z, M (m x n, ld n), U (m x kbuf), V (n x kbuf), d, dl, partials
   const int nb = ialm_blocks();
+  const int npart = ialm_partials(n, nb);
   size_t o = 0;
   const size_t oZ = o; o = align256(o + (size_t)m * n * 8);
   const size_t oM = o; o = align256(o + (size_t)m * n * 8);
-  const size_t oU = o; o = align256(o + (size_t)m * k * 8);
-  const size_t oV = o; o = align256(o + (size_t)n * k * 8);
-  const size_t od = o; o = align256(o + 64 * 8);
-  const size_t odl = o; o = align256(o + 64 * 8);
+  const size_t oU = o; o = align256(o + (size_t)m * kbuf * 8);
+  const size_t oV = o; o = align256(o + (size_t)n * kbuf * 8);
+  const size_t od = o; o = align256(o + 128 * 8);
+  const size_t odl = o; o = align256(o + 128 * 8);
   const size_t oP = o; o = align256(o + (size_t)2 * nb * 8 + 64);
   if (o > ctx->ws3_bytes) {
     if (ctx->ws3) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->ws3); ctx->ws3 = nullptr; ctx->ws3_bytes = 0; }
@@ -893,7 +904,7 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
   double* dd = (double*)(ctx->ws3 + od);
   double* dl = (double*)(ctx->ws3 + odl);
   double* part = (double*)(ctx->ws3 + oP);
-  double* scal = part + 2 * nb;   // [0] = sum, [1] = max
+  double* scal = part + 2 * nb;   // [0] = sum, [1] = max, [2] = l
   double* h = ctx->hbuf;
 
   // ||A||_2 = sigma_1 of rsvd(A, 1, p, q) with Omega stream 0 (reading R18)
@@ -922,31 +933,37 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
   Mdesc.lda = n;
   int it = 0;
   double res = INFINITY;
-  int nl = 0;
+  int kused = k;
   for (it = 1; it <= prm->maxiter; ++it) {
     rsvd_params ri = rp;
+    ri.k = ri.nu = ri.nv = k;
     ri.stream = (uint64_t)it;                               // fresh Omega per iteration (R23)
     CKS(rsvd_device(ctx, &Mdesc, &ri, U, k, dd, V, k));      // step (6)
-    CK(cudaMemcpyAsync(h, dd, k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    nl = 0;
-    for (int i = 0; i < k; ++i) if (h[i] > 1.0 / mu) ++nl;  // step (7), fixed k (R22)
-    for (int i = 0; i < k; ++i) h[64 + i] = (i < nl) ? h[i] - 1.0 / mu : 0.0;   // step (8)
-    CK(cudaMemcpyAsync(dl, h + 64, k * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(launch_ialm_threshold(dd, k, 1.0 / mu, dl, scal + 2, ctx->stream));   // steps (7)-(8)
     const double mu_next = std::min(1.5 * mu, 1e7 * mu0);  // step (12), R20
-    CK(launch_ialm_update(Ad, S, Z, M, n, m, n, U, k, V, k, dl, nl, 1.0 / mu, mu, lam, 1.0 / mu_next, part, nb,
+    CK(launch_ialm_update(Ad, S, Z, M, n, m, n, U, k, V, k, dl, k, 1.0 / mu, mu, lam, 1.0 / mu_next, part, nb,
                           ctx->stream));                   // steps (9)-(11) fused
-    CK(launch_reduce_blocks(part, nb, 0, scal, ctx->stream));
+    CK(launch_reduce_blocks(part, npart, 0, scal, ctx->stream));
     CKS(allreduce_sum(ctx, scal, 1));
-    CK(cudaMemcpyAsync(h + 128, scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(h + 128, scal, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     res = sqrt(h[128]) / normF;
-    if (trace) { trace[3 * (it - 1)] = res; trace[3 * (it - 1) + 1] = nl; trace[3 * (it - 1) + 2] = mu; }
+    const int nl = (int)h[130];
+    kused = k;
+    if (trace) {
+      double* tr = trace + 4 * (it - 1);
+      tr[0] = res; tr[1] = nl; tr[2] = mu; tr[3] = k;
+    }
+    if (adaptive) {                                         // step (7) predict_rank (R30)
+      const int l1 = std::max(nl, 1);
+      int64_t kn = l1 < k ? l1 + 1 : std::min<int64_t>(l1 + (int64_t)ceil(0.05 * (double)minmn), minmn);
+      k = (int)std::min<int64_t>(kn, kcap);
+    }
     mu = mu_next;
     if (res < prm->tol) break;
   }
   if (it > prm->maxiter) it = prm->maxiter;
-  CK(launch_lowrank_materialise(U, k, V, k, dl, nl, m, n, Lm, ld, ctx->stream));
+  CK(launch_lowrank_materialise(U, kused, V, kused, dl, kused, m, n, Lm, ld, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (iters_out) *iters_out = it;
   if (res_out) *res_out = res;

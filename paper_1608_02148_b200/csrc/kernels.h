@@ -145,7 +145,7 @@ cudaError_t launch_check_finite(const double* v, int64_t n, int* flag, cudaStrea
 // M = A - S + Z * inv_mu ;  optional: norms of A (||A||_F^2 partials, max|A|)
 cudaError_t launch_ialm_form_m(const double* A, const double* S, const double* Z, int64_t ld,
                                int64_t m, int64_t n, double inv_mu, double* M, cudaStream_t st);
-// Fused update with L = U diag(dl) V^T (rank r <= 32, never materialised):
+// Fused update with L = U diag(dl) V^T (rank r <= 128, never materialised):
 //   S = shrink(A - L + Z inv_mu, lam inv_mu);  E = A - L - S;  Z += mu E;
 //   M_next = A - S + Z * inv_mu_next;  partial[b] = sum E^2 (per block).
 cudaError_t launch_ialm_update(const double* A, double* S, double* Z, double* Mnext, int64_t ld,
@@ -164,5 +164,10 @@ cudaError_t launch_scale_copy(const double* A, int64_t ld, int64_t m, int64_t n,
                               double* Z, cudaStream_t st);
 cudaError_t launch_reduce_blocks(const double* part, int nb, int op_max, double* out, cudaStream_t st);
 int ialm_blocks();
+// number of partials launch_ialm_update writes for n columns and nblocks (<= nblocks)
+int ialm_partials(int64_t n, int nblocks);
+// dl_t = max(d_t - inv_mu, 0) for t < k (d descending); *l_out = #{d_t > inv_mu}
+cudaError_t launch_ialm_threshold(const double* d, int k, double inv_mu, double* dl, double* l_out,
+                                  cudaStream_t st);
 
 }  // namespace rsvd

@@ -243,6 +243,32 @@ def test_rrpca_parity_small(rb):
     assert out["residual"] < 1e-7
 
 
+@pytest.mark.parametrize("m,n,rank,k", [(4000, 300, 5, 0), (3000, 400, 40, 0), (3000, 400, 40, 60)])
+def test_rrpca_adaptive_and_large_rank_parity(rb, m, n, rank, k):
+    """Alg. 7 with the adaptive target rank of steps (1), (7) (k = 0, R30) and a
+    fixed rank above 32 (the R = 64 update kernel): the rank trajectory (l, k)
+    per iteration matches the oracle's exactly, L and S within 1e-10 when the
+    iteration counts agree, and the planted L0, S0 are recovered."""
+    A, L0, S0 = synthetic.sparse_plus_lowrank(m, n, rank=rank, frac=0.05, seed=rank + 11)
+    An = A.numpy()
+    out = rb.rrpca(A.cuda(), k=k, p=10, q=2, tol=1e-7, maxiter=100, seed=4, trace=True)
+    o = oracle.oracle_rrpca(An, k=k, p=10, q=2, tol=1e-7, maxiter=100, seed=4, kmax=min(m, n, 110))
+    assert all(t[3] <= min(m, n) / 4 for t in o["trace"])          # no Remark-2 switch on either side
+    nt = min(out["iters"], o["iters"])
+    assert [(t[1], t[3]) for t in out["trace"][:nt]] == [(t[1], t[3]) for t in o["trace"][:nt]]
+    if k == 0:
+        assert out["trace"][0][3] == 2 and out["trace"][-1][3] == rank + 1
+    assert abs(out["iters"] - o["iters"]) <= 1
+    L, S = _np(out["L"]), _np(out["S"])
+    if out["iters"] == o["iters"]:
+        assert np.linalg.norm(L - o["L"]) / np.linalg.norm(o["L"]) < 1e-10
+        assert np.linalg.norm(S - o["S"]) / np.linalg.norm(o["S"]) < 1e-10
+    L0n, S0n = L0.numpy(), S0.numpy()
+    assert np.linalg.norm(L - L0n) / np.linalg.norm(L0n) < 1e-6
+    assert ((np.abs(S) > 1e-6) == (S0n != 0)).mean() > 0.999
+    assert out["residual"] < 1e-7
+
+
 # ----------------------------------------------------------------------------- full-size configs 3, 5
 def test_config3_full_size_rpca(rb):
     """Config 3 (J:9): 200000 x 4000 column-centred PCA, k=100, p=20, q=2, uniform Omega."""

@@ -14,7 +14,7 @@ import pytest
 import oracle
 from oracle.linalg import hqr, jacobi_svd_bt, soft_threshold
 from oracle.philox import omega, omega_words, philox4x32_10
-from oracle.rsvd import oracle_rpca, oracle_rqb, oracle_rrpca, oracle_rsvd, resolve_params
+from oracle.rsvd import oracle_rpca, oracle_rqb, oracle_rrpca, oracle_rsvd, predict_rank, resolve_params
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = json.load(open(os.path.join(HERE, "golden", "worked_examples.json")))
@@ -343,3 +343,31 @@ def test_rrpca_recovers_planted_low_rank_plus_sparse():
     supp = (np.abs(out["S"]) > 1e-6) == (S0 != 0)
     assert supp.mean() > 0.999
     assert abs(out["lam"] - 1 / np.sqrt(2000)) < 1e-16
+
+
+def test_predict_rank_rule():
+    """Alg. 7 step (7) predict_rank (Remark 1 P:1716), reading R30:
+    worked cases of the stated rule (SPEC predict_rank examples)."""
+    assert predict_rank([5, 3, 0.1], 1.0, 2, 100) == (7, 2)       # l == k: grow by ceil(5% of 100)
+    assert predict_rank([0.5, 0.2], 1.0, 2, 100) == (2, 1)        # nothing above 1/mu: l floored to 1
+    assert predict_rank([5, 3, 0.1], 1.0, 10, 100) == (3, 2)      # l < k: shrink to l + 1
+    assert predict_rank([9, 8, 7], 1.0, 3, 3) == (3, 3)           # growth capped at min(m, n)
+    assert predict_rank([9, 8, 7], 1.0, 3, 41) == (6, 3)          # ceil(0.05 * 41) = 3
+    assert predict_rank([2.0, 1.0], 1.0, 2, 10) == (2, 1)         # strict '>' at the threshold
+
+
+def test_rrpca_adaptive_rank_settles_at_rank_plus_one():
+    """k = 0: k starts at 2 (step (1)) and predict_rank grows it until the
+    thresholded rank l stops at the planted rank 5, after which k = l + 1 = 6;
+    the planted L0, S0 are recovered (ground truth, not the oracle itself)."""
+    import synthetic
+    A, L0, S0 = synthetic.sparse_plus_lowrank(2000, 200, rank=5, frac=0.05, seed=31)
+    A, L0, S0 = A.numpy(), L0.numpy(), S0.numpy()
+    out = oracle_rrpca(A, k=0, p=10, q=2, tol=1e-7, maxiter=100, seed=5)
+    tr = out["trace"]
+    assert tr[0][3] == 2                                   # step (1): k = 2
+    assert all(t[3] <= 200 // 4 for t in tr)               # stays randomized (Remark 2)
+    assert tr[-1][1] == 5 and tr[-1][3] == 6               # l = rank, k = l + 1
+    assert out["residual"] < 1e-7
+    assert np.linalg.norm(out["L"] - L0) / np.linalg.norm(L0) < 1e-5
+    assert ((np.abs(out["S"]) > 1e-6) == (S0 != 0)).mean() > 0.999
