@@ -59,7 +59,7 @@ cudaError_t launch_panel_apply(const double* S, int64_t lds, int64_t rows, int N
                                double* C, int64_t ldc, int Nout, bool upper, int num_sms, cudaStream_t st);
 
 // ---- FP64 passes by Ozaki-scheme int8 slices on tcgen05 (pass_ozaki.cu)
-#define OZ_S 8                                   // 7-bit digits per element (56 bits: exact for FP64)
+#define OZ_S 7                                   // 8-bit digits per element (A: 56-bit two's complement, X: 54-bit balanced)
 struct OzakiA {                                  // A sliced once per call: m x (ldn/128) x S x 128 int8 + exponents
   int8_t* slices; double* ea;                    // ea[row][col super-tile] = 2^E (512 x 512 super-tiles)
   double* tmax;                                  // scratch: max |f(a)| per 128 x 128 tile

@@ -8,18 +8,23 @@
 // int8 tensor throughput is ~60x higher, so an exact slice decomposition
 // moves the pass to the HBM roof.
 //
-// Representation (exact, no rounding): A is cut into 128 x 128 tiles; a tile
-// with max |a| < 2^E stores a = sign(a) * 2^E * sum_{t=1..S} d_t 2^{-7t} with
-// digits d_t in [0, 127] (sign applied to every digit, so each fits int8) —
-// the first 7S bits of |a| 2^-E, truncated (S = 7: 49 bits).  X (the panel,
-// K x Np) is cut per (128-row k-block, column) the same way.  Then
-//   (A X)_ij = sum_kb 2^{E_A(tile) + E_X(kb, j)} sum_{t,u} 2^{-7(t+u)} (D_t X_u)_ij
-// where D_t X_u over one k-block is an exact int32 dot product (|.| <= 128 * 127^2).
-// Products with t + u > S + 1 are dropped (their weight is < 2^{-7(S+2)}).
+// Representation: A is cut into 1024 x 1024 super-tiles; with max |a| < 2^E
+// over the super-tile, a is rounded to the 56-bit integer N = rn(a 2^{55-E})
+// (exact for every a >= 2^{E-3}; error <= 2^{E-56} otherwise) and N is stored
+// as S = 7 two's-complement bytes: digit 0 signed (s8), digits 1..6 unsigned
+// (u8), weight of digit t = 2^{E-7-8t}.  X (the panel, K x Np) is cut per
+// (1024-row block, column) with exponent F into S balanced signed digits
+// (s8, N = rn(x 2^{54-F}) < 2^54 in magnitude, weight of digit u = 2^{F-6-8u}).
+// Then
+//   (A X)_ij = sum_sb 2^{E + F} sum_{t,u} 2^{-13-8(t+u)} (D_t X_u)_ij
+// where D_t X_u over one super-block is an exact int32 dot product
+// (|.| <= 1024 * 255 * 128 < 2^25).  Products with t + u > S - 1 are dropped
+// (weight <= 2^{-69} relative to 2^{E+F}: below FP64 rounding of the sum).
 // Terms of equal weight g = t + u share one TMEM accumulator: S groups x N
-// columns (S = 7, N <= 64: 448 of 512 TMEM columns).  After each k-block the
-// epilogue converts the groups to FP64 and accumulates the scaled sum in
-// registers.
+// columns (N <= 64: 448 of 512 TMEM columns); the t = 0 MMAs run as s8 x s8,
+// the others as u8 x s8 (kind::i8 takes the operand signedness per
+// instruction).  After each super-block the epilogue converts the groups to
+// FP64 and accumulates the scaled sum in registers.
 //
 // A is sliced once per rsvd call (ozaki_slice_a) and read by every pass (S
 // bytes per element instead of 8); X is sliced before each pass.
@@ -38,11 +43,9 @@ namespace oz {
 using namespace tc;
 
 constexpr int BM = 128, BKO = 128, THREADS = 256;
-// A-slice pipeline stages: as many 16 KB stages as fit next to two X buffers
-__host__ __device__ constexpr int nsa_for(int S, int N) { return (220 * 1024 - 2 * S * N * 128 - 2048) / (128 * 128) > 6 ? 6 : (220 * 1024 - 2 * S * N * 128 - 2048) / (128 * 128); }
 constexpr int A_TILE = BM * BKO;                    // bytes of one slice tile
 constexpr int KSUP = 8, ET = KSUP * BKO;            // exponent super-tiles: 1024 x 1024 of A, 1024-row blocks of X;
-                                                    // int32 accumulation over 1024 k: <= 8 pairs * 1024 * 127^2 < 2^27
+                                                    // int32 accumulation over 1024 k: <= 7 pairs * 1024 * 255 * 128 < 2^28
 
 __host__ __device__ inline int64_t unit_lo(int64_t units, int grid, int c) { return (units * (int64_t)c) / grid; }
 #ifndef OZ_PROBE
@@ -75,22 +78,37 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t a, uint64_t b, ui
 // exponent E with max |a| < 2^E (0 for an all-zero block)
 __device__ __forceinline__ int block_exp(double mx) { return mx > 0.0 ? ilogb(mx) + 1 : 0; }
 
-// S digits of |v| 2^{7S - E} (truncated), sign applied, packed 4 elements per word
+// A digits: N = rn(v 2^{8S-1-E}) (|N| < 2^{8S-1}) as S two's-complement bytes,
+// most significant first (byte 0 read as s8, the others as u8); packed 4
+// elements per word
 template <int S>
-__device__ __forceinline__ void digits4(const double (&v)[4], double scale, uint32_t (&w)[S]) {
+__device__ __forceinline__ void digits_a4(const double (&v)[4], double scale, uint32_t (&w)[S]) {
 #pragma unroll
   for (int t = 0; t < S; ++t) w[t] = 0u;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const double y = fabs(v[e]) * scale;                // < 2^{7S}, exact scaling
-    const unsigned long long q = (unsigned long long)y;  // truncation
-    const bool neg = v[e] < 0.0;
+    const long long q = __double2ll_rn(v[e] * scale);   // exact power-of-two scaling, then round
 #pragma unroll
-    for (int t = 0; t < S; ++t) {
-      int d = (int)((q >> (7 * (S - 1 - t))) & 127ull);
-      if (neg) d = -d;
-      w[t] |= ((uint32_t)(d & 0xff)) << (8 * e);
+    for (int t = 0; t < S; ++t) w[t] |= ((uint32_t)(q >> (8 * (S - 1 - t))) & 0xffu) << (8 * e);
+  }
+}
+
+// X digits: N = rn(v 2^{8S-2-F}) (|N| < 2^{8S-2}) as S balanced signed bytes
+// d_u in [-128, 127] (d_0 in [-64, 64]), N = sum_u d_u 256^{S-1-u}
+template <int S>
+__device__ __forceinline__ void digits_x4(const double (&v)[4], double scale, uint32_t (&w)[S]) {
+#pragma unroll
+  for (int t = 0; t < S; ++t) w[t] = 0u;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    long long q = __double2ll_rn(v[e] * scale);
+#pragma unroll
+    for (int t = S - 1; t >= 1; --t) {
+      const int d = (int)(signed char)(q & 0xff);
+      q = (q - d) >> 8;                                   // exact
+      w[t] |= ((uint32_t)d & 0xffu) << (8 * e);
     }
+    w[0] |= ((uint32_t)q & 0xffu) << (8 * e);
   }
 }
 
@@ -134,7 +152,7 @@ ozaki_amax_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t 
 // 128 x 128 tile -> slices, interleaved as [row][col block][t][128 bytes] so that
 // one unit's S slice boxes read one contiguous S * 128 B run per row (DRAM
 // locality for both pass orientations); digits relative to the
-// 512 x 512 super-tile exponent; ea[sy * nsx + sx] = 2^E
+// 1024 x 1024 super-tile exponent; ea[sy * nsx + sx] = 2^E
 template <int S>
 __global__ void __launch_bounds__(256)
 ozaki_slice_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, const double* __restrict__ c,
@@ -148,7 +166,7 @@ ozaki_slice_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64
     for (int xx = sx * KSUP; xx < min((int)gridDim.x, (sx + 1) * KSUP); ++xx) mx = fmax(mx, tmax[(int64_t)yy * gridDim.x + xx]);
   const int E = block_exp(mx);
   if (tid == 0 && blockIdx.y % KSUP == 0 && blockIdx.x % KSUP == 0) ea[(int64_t)sy * nsx + sx] = ldexp(1.0, E);
-  const double scale = ldexp(1.0, 7 * S - E);
+  const double scale = ldexp(1.0, 8 * S - 1 - E);
   // 4 consecutive columns per thread-iteration; columns >= n of the last block are zero
   const int64_t nblk = ldn / BKO;
   for (int e = tid; e < BM * (BKO / 4); e += 256) {
@@ -160,7 +178,7 @@ ozaki_slice_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64
 #pragma unroll
     for (int q = 0; q < 4; ++q) v[q] = (cc + q < n) ? fval(A, lda, c, rs, r, cc + q) : 0.0;
     uint32_t w[S];
-    digits4<S>(v, scale, w);
+    digits_a4<S>(v, scale, w);
     int8_t* dst = slices + ((r * nblk + blockIdx.x) * S) * BKO + jj;
 #pragma unroll
     for (int t = 0; t < S; ++t) *reinterpret_cast<uint32_t*>(dst + t * BKO) = w[t];
@@ -196,7 +214,7 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
   const int64_t sb = kc / (ET / 16);
   const int E = block_exp(cmax[sb * Np + j]);
   if (kc % (ET / 16) == 0) xf[sb * Np + j] = ldexp(1.0, E);
-  const double scale = ldexp(1.0, 7 * S - E);
+  const double scale = ldexp(1.0, 8 * S - 2 - E);
   uint32_t w[4][S];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -206,7 +224,7 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
       const int64_t kk = kc * 16 + 4 * q + e;
       v[e] = kk < K ? X[kk * ldx + j] : 0.0;
     }
-    digits4<S>(v, scale, w[q]);
+    digits_x4<S>(v, scale, w[q]);
   }
 #pragma unroll
   for (int t = 0; t < S; ++t)
@@ -230,6 +248,8 @@ struct Args {
 constexpr int BKU = 64;                             // k per unit
 constexpr int KSU = ET / BKU;                       // units per exponent super-block (16)
 constexpr int A_UT = BM * BKU;                      // bytes of one A-slice tile of a unit
+__host__ __device__ constexpr int oz_ubuf(int S, int N) { return (S * A_UT + S * N * BKU + 1023) / 1024 * 1024; }
+__host__ __device__ constexpr int oz_nbuf(int S, int N) { return 3 * oz_ubuf(S, N) + 1024 <= 219 * 1024 ? 3 : 2; }
 
 template <bool TRANS, int S, int N>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -238,7 +258,8 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int XSL = N * BKU;                      // bytes of one X slice tile (N rows x 64 k)
   constexpr int UBUF = ((S * A_UT + S * XSL) + 1023) / 1024 * 1024;
-  __shared__ uint64_t ufull[2], uempty[2], accf, acce;
+  constexpr int NB = oz_nbuf(S, N);                 // unit buffers (3 when they fit, else 2)
+  __shared__ uint64_t ufull[3], uempty[3], accf, acce;
   __shared__ uint32_t tmem_base;
   __shared__ double xfsm[4 * 64];
 
@@ -249,7 +270,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   const int64_t nun = u_hi - u_lo;
 
   if (tid == 0) {
-    for (int s = 0; s < 2; ++s) { mbar_init(&ufull[s], 1); mbar_init(&uempty[s], 1); }
+    for (int s = 0; s < NB; ++s) { mbar_init(&ufull[s], 1); mbar_init(&uempty[s], 1); }
     mbar_init(&accf, 1);
     mbar_init(&acce, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -269,10 +290,10 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       OZ_PROBE2_DECL
       for (int64_t it = 0; it < nun; ++it) {
         const int64_t u = u_lo + it, mb = u / KB, kb = u - mb * KB;
-        const int ub = (int)(it & 1);
+        const int ub = (int)(it % NB);
         unsigned char* ubuf = base + ub * UBUF;
         OZ_PROBE2(0)
-        mbar_wait(&uempty[ub], (uint32_t)(((it >> 1) & 1) ^ 1));
+        mbar_wait(&uempty[ub], (uint32_t)(((it / NB) & 1) ^ 1));
         OZ_PROBE2(1)
         mbar_expect_tx(&ufull[ub], (uint32_t)(S * A_UT + S * XSL));
         for (int t = 0; t < S; ++t) {
@@ -290,7 +311,8 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
     if (lane == 0) {
       // X slices u0..u0+c-1 are consecutive N-row tiles and their groups t+u0..t+u0+c-1
       // consecutive N-column blocks of TMEM: one MMA with N_mma = c N covers them (<= 256)
-      const uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((TRANS ? 1u : 0u) << 15) | (0u << 16) |
+      // D s32; B s8; A s8 for digit 0, u8 for the others (bits 7-9, set per t)
+      const uint32_t idesc0 = (2u << 4) | (1u << 10) | ((TRANS ? 1u : 0u) << 15) | (0u << 16) |
                               ((uint32_t)(BM >> 4) << 24);
       constexpr int CMAX = 256 / N;
       OZ_PROBE_DECL
@@ -299,9 +321,9 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       for (int64_t it = 0; it < nun; ++it) {
         const int64_t u = u_lo + it, kb = u % KB;
         const bool drain = (kb % KSU == KSU - 1) || kb == KB - 1 || it == nun - 1;
-        const int ub = (int)(it & 1);
+        const int ub = (int)(it % NB);
         OZ_PROBE(0)
-        mbar_wait(&ufull[ub], (uint32_t)((it >> 1) & 1));
+        mbar_wait(&ufull[ub], (uint32_t)((it / NB) & 1));
         OZ_PROBE(3)
         if (fresh && ndrain > 0) mbar_wait(&acce, (uint32_t)((ndrain - 1) & 1));
         OZ_PROBE(2)
@@ -320,7 +342,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
             for (int u0 = 0; u0 < S - t; u0 += CMAX) {
               const int cnt = (S - t - u0) < CMAX ? (S - t - u0) : CMAX;
               const uint64_t db = dx0 + (uint64_t)((u0 * XSL + kk * 32) >> 4);
-              const uint32_t idesc = idesc0 | ((uint32_t)((cnt * N) >> 3) << 17);
+              const uint32_t idesc = idesc0 | ((t == 0 ? 1u : 0u) << 7) | ((uint32_t)((cnt * N) >> 3) << 17);
 #ifndef OZ_SKIP_MMA
               mma_i8(tmem + (uint32_t)((t + u0) * N), da, db, idesc, (t > 0 || kk > 0) ? 1u : acc0);
 #endif
@@ -367,12 +389,12 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         double part[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) part[i] = 0.0;
-        double w = 0x1.0p-14;                         // group g = t + u (t, u from 1): weight 2^{-7(g + 2)}
+        double w = 0x1.0p-13;                         // group g = t + u: weight 2^{-13-8g}
 #pragma unroll
         for (int gg = 0; gg < S; ++gg) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) part[i] = fma((double)(int)v[gg][i], w, part[i]);
-          w *= 0x1.0p-7;
+          w *= 0x1.0p-8;
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[8 * c + i] = fma(part[i], xfs[8 * c + i], acc[8 * c + i]);
@@ -558,7 +580,8 @@ static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
   if (grid > c.grid) grid = c.grid;
   if (grid < 1) grid = 1;
   g.grid = (int)grid;
-  const size_t smem = 2 * (size_t)((OZ_S * A_UT + OZ_S * N * BKU + 1023) / 1024 * 1024) + 1024;
+  const int nbuf = N <= 16 ? oz_nbuf(OZ_S, 16) : N <= 32 ? oz_nbuf(OZ_S, 32) : N <= 48 ? oz_nbuf(OZ_S, 48) : oz_nbuf(OZ_S, 64);
+  const size_t smem = (size_t)nbuf * oz_ubuf(OZ_S, N <= 16 ? 16 : N <= 32 ? 32 : N <= 48 ? 48 : 64) + 1024;
   cudaError_t e = cudaSuccess;
 #define RSVD_OZ(TR, NN)                                                                                   \
   {                                                                                                      \

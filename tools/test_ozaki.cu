@@ -56,8 +56,12 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(ea.data(), oa.ea, tiles * 8, cudaMemcpyDeviceToHost));
     double e = 0;
     for (int64_t i = 0; i < m; ++i) for (int64_t j = 0; j < n; ++j) {
-      long double v = 0, w = 1.0L / 128;
-      for (int t = 0; t < OZ_S; ++t) { v += sl[((i * (oa.ldn / 128) + j / 128) * OZ_S + t) * 128 + j % 128] * w; w /= 128; }
+      long double v = 0, w = 1.0L / 128;      // digit 0 s8 (weight 2^-7), digits t >= 1 u8 (weight 2^{-7-8t})
+      for (int t = 0; t < OZ_S; ++t) {
+        const int8_t d = sl[((i * (oa.ldn / 128) + j / 128) * OZ_S + t) * 128 + j % 128];
+        v += (t == 0 ? (long double)d : (long double)(uint8_t)d) * w;
+        w /= 256;
+      }
       v *= ea[(i / 1024) * oa.ntiles + j / 1024];
       const double tile_max = ea[(i / 1024) * oa.ntiles + j / 1024];
       e = fmax(e, fabs((double)(v - A[i * n + j])) / tile_max);
@@ -67,6 +71,7 @@ int main(int argc, char** argv) {
   unsigned epoch = 0;
   for (int trans = 0; trans < 2; ++trans)
     for (int N : {16, 32, 64, 96, 128}) {
+      if (argc > 5 && N != atoi(argv[5])) continue;
       const int64_t M = trans ? n : m, K = trans ? m : n;
       std::vector<double> B(K * N), C(M * N, -7.0);
       for (int64_t k = 0; k < K; ++k) for (int j = 0; j < N; ++j) {
@@ -81,7 +86,8 @@ int main(int argc, char** argv) {
       CK(cudaDeviceSynchronize());
       CK(cudaMemcpy(C.data(), dC, M * N * 8, cudaMemcpyDeviceToHost));
       double emax_abs = 0, emax_rel = 0, rmax = 0;
-      for (int64_t i = 0; i < M; ++i)
+      const int64_t istep = M > 2000 ? M / 499 : 1;   // sampled rows for large problems
+      for (int64_t i = 0; i < M; i += istep)
         for (int j = 0; j < N; ++j) {
           long double s = 0, sa = 0;
           for (int64_t k = 0; k < K; ++k) {
