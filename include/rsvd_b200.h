@@ -88,12 +88,18 @@ typedef struct {
  *   q      subspace iterations (Alg. 2)
  *   seed, stream  counter-based Omega (reading R1)
  *   center  1 = implicit column centring of A (rpca, Alg. 6)
- *   scale   1 = implicit column scaling by the (centred) column s.d. */
+ *   scale   1 = implicit column scaling by the (centred) column s.d.
+ *   power   power scheme between the sketch and the final QR: 0 = subspace
+ *           iterations with QR (Alg. 2, default), 1 = the direct
+ *           scheme Y = (A A^T)^q A Omega without normalisation (Alg. 1,
+ *           P:343-362; "not recommended in practice"); RSVD_EINVAL
+ *           otherwise */
 typedef struct {
   int32_t k, nu, nv, p, q;
   int32_t sdist;          /* rsvd_sdist */
   uint64_t seed, stream;
   int32_t center, scale;
+  int32_t power;
 } rsvd_params;
 
 /* Fill the defaults of P:708: nu = nv = k, p = 10, q = 2, normal, seed 0,

@@ -73,14 +73,21 @@ def _prepare(A, center=False, scale=False):
     return X, c, s
 
 
-def oracle_rqb(A, l, q=2, sdist="normal", seed=0, stream=0, omega_dtype=np.float64):
-    """Alg. 4 rqb with Alg. 2 sub_iterations: returns Q (m x l), B^T (n x l)."""
+def oracle_rqb(A, l, q=2, sdist="normal", seed=0, stream=0, omega_dtype=np.float64,
+               power="subspace"):
+    """Alg. 4 rqb with Alg. 2 sub_iterations (power="subspace") or the direct
+    power scheme of Alg. 1 (power="direct"): returns Q (m x l),
+    B^T (n x l)."""
     X = np.asarray(A, dtype=np.float64)
     m, n = X.shape
     Om = omega(n, l, sdist, seed, stream, dtype=omega_dtype)   # step (2)
     Y = X @ Om                                                  # step (3)
-    for _ in range(q):                                          # step (4), Alg. 2
-        Q, _r = hqr(Y)                                          #   (2)
+    for _ in range(q):                                          # step (4)
+        if power == "direct":                                   # Alg. 1
+            Y = X.T @ Y                                         #   (2)
+            Y = X @ Y                                           #   (3)
+            continue
+        Q, _r = hqr(Y)                                          # Alg. 2 (2)
         Qz, _r = hqr(X.T @ Q)                                   #   (3)
         Y = X @ Qz                                              #   (4)
     Q, _r = hqr(Y)                                              # step (9)
@@ -89,7 +96,7 @@ def oracle_rqb(A, l, q=2, sdist="normal", seed=0, stream=0, omega_dtype=np.float
 
 
 def oracle_rsvd(A, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0,
-                stream=0, center=False, scale=False, full=False):
+                stream=0, center=False, scale=False, full=False, power="subspace"):
     """Alg. 5 rsvd with the interface of P:708.
 
     Returns dict(d, u, v, l, center, scale) -- d: (k,), u: m x nu, v: n x nv.
@@ -103,7 +110,7 @@ def oracle_rsvd(A, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0,
     k, nu, nv, l = resolve_params(m, n, k, nu, nv, p, q)
     transposed = m < n
     W = X.T if transposed else X
-    Q, Bt = oracle_rqb(W, l, q, sdist, seed, stream, omega_dtype)
+    Q, Bt = oracle_rqb(W, l, q, sdist, seed, stream, omega_dtype, power=power)
     sigma, Ut, V, sweeps = jacobi_svd_bt(Bt)                    # Alg. 5 (2)
     U = Q @ Ut                                                  # Alg. 5 (3), Eq. UQU
     if transposed:

@@ -46,7 +46,10 @@ class Matrix(ctypes.Structure):
 class Params(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("nu", ctypes.c_int32), ("nv", ctypes.c_int32), ("p", ctypes.c_int32),
                 ("q", ctypes.c_int32), ("sdist", ctypes.c_int32), ("seed", ctypes.c_uint64),
-                ("stream", ctypes.c_uint64), ("center", ctypes.c_int32), ("scale", ctypes.c_int32)]
+                ("stream", ctypes.c_uint64), ("center", ctypes.c_int32), ("scale", ctypes.c_int32),
+                ("power", ctypes.c_int32)]
+
+POWER = {"subspace": 0, "direct": 1}
 
 
 class RrpcaParams(ctypes.Structure):
@@ -201,7 +204,7 @@ def _matrix(A, m_global=None, row_offset=0):
     return Matrix(dt, A.data_ptr(), m, n, A.stride(0), m if m_global is None else m_global, row_offset)
 
 
-def _params(k, nu, nv, p, q, sdist, seed, stream, center=0, scale=0):
+def _params(k, nu, nv, p, q, sdist, seed, stream, center=0, scale=0, power="subspace"):
     prm = Params()
     lib().rsvd_params_default(ctypes.byref(prm), int(k))
     prm.nu = int(k) if nu is None else int(nu)
@@ -210,6 +213,7 @@ def _params(k, nu, nv, p, q, sdist, seed, stream, center=0, scale=0):
     prm.sdist = SDIST[sdist] if isinstance(sdist, str) else int(sdist)
     prm.seed, prm.stream = int(seed), int(stream)
     prm.center, prm.scale = int(bool(center)), int(bool(scale))
+    prm.power = POWER[power] if isinstance(power, str) else int(power)
     return prm
 
 
@@ -217,9 +221,10 @@ RsvdResult = namedtuple("RsvdResult", ["d", "u", "v"])
 
 
 def rsvd(A, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None,
-         m_global=None, row_offset=0, out=None):
+         m_global=None, row_offset=0, out=None, power="subspace"):
     """Randomized SVD (Alg. 5; interface P:708).
 
+    power: "subspace" (Alg. 2, QR between passes) or "direct" (Alg. 1).
     A: CUDA tensor (m x n, float64 or float32, row-major).  Returns (d, u, v)
     with d (k,), u (m x nu) and v (n x nv, not transposed).  In distributed
     mode (ctx.init_comm) A holds this rank's rows and u this rank's rows.
@@ -230,7 +235,7 @@ def rsvd(A, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0, stream=0, ct
     kk = int(k)
     nu_ = kk if nu is None else min(int(nu), kk)
     nv_ = kk if nv is None else min(int(nv), kk)
-    prm = _params(k, nu, nv, p, q, sdist, seed, stream)
+    prm = _params(k, nu, nv, p, q, sdist, seed, stream, power=power)
     if not (1 <= kk <= min(mg, A.shape[1])):
         raise RsvdError(1, "k must satisfy 1 <= k <= min(m, n)")
     if out is None:

@@ -22,6 +22,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -460,6 +461,7 @@ rsvd_status validate(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm
   if (prm->p < 0 || prm->q < 0) return fail(ctx, RSVD_EINVAL, "p and q must be >= 0");
   if (prm->sdist < 0 || prm->sdist > 2) return fail(ctx, RSVD_EINVAL, "sdist must be normal, unif or rademacher");
   if (prm->nu < 0 || prm->nv < 0) return fail(ctx, RSVD_EINVAL, "nu, nv must be >= 0");
+  if (prm->power < 0 || prm->power > 1) return fail(ctx, RSVD_EINVAL, "power must be 0 (Alg. 2) or 1 (Alg. 1)");
   *m_out = mg;
   *n_out = A->n;
   return RSVD_OK;
@@ -499,11 +501,16 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool robus
     CK(launch_omega(p.n, l, Np, Np, prm->sdist, prm->seed, prm->stream, p.f32, false, p.X, ctx->stream));
   }
   CKS(pass_ax(ctx, p, p.X, p.Y, centred));                          // Y = A Omega
-  for (int j = 0; j < prm->q; ++j) {                                 // Alg. 2
-    CKS(orth(ctx, p, p.Y, p.M, dist, robust, nullptr, false));      //   [Q,~] = qr(Y)
+  for (int j = 0; j < prm->q; ++j) {
+    if (prm->power == 1) {                                           // Alg. 1 (direct)
+      CKS(pass_atx(ctx, p, p.Y, p.Z, centred));                      //   (2) Y = A^T Y
+      CKS(pass_ax(ctx, p, p.Z, p.Y, centred));                       //   (3) Y = A Y
+      continue;
+    }
+    CKS(orth(ctx, p, p.Y, p.M, dist, robust, nullptr, false));      // Alg. 2 (2) [Q,~] = qr(Y)
     CKS(pass_atx(ctx, p, p.Y, p.Z, centred));                        //   A^T Q
-    CKS(orth(ctx, p, p.Z, p.n, false, robust, nullptr, false));     //   [Q,~] = qr(A^T Q)
-    CKS(pass_ax(ctx, p, p.Z, p.Y, centred));                         //   Y = A Q
+    CKS(orth(ctx, p, p.Z, p.n, false, robust, nullptr, false));     //   (3) [Q,~] = qr(A^T Q)
+    CKS(pass_ax(ctx, p, p.Z, p.Y, centred));                         //   (4) Y = A Q
   }
   CKS(orth(ctx, p, p.Y, p.M, dist, robust, nullptr));               // Alg. 4 step 9
   CKS(pass_atx(ctx, p, p.Y, p.Z, centred));                          // step 10: B^T = A^T Q
@@ -584,14 +591,20 @@ rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bo
   return RSVD_OK;
 }
 
-rsvd_status run_with_retry(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool want_svd) {
+// The caller's output kernels (`emit`) are enqueued right behind the core, so
+// the one host synchronisation per call (reading the status word) also covers
+// them; on a CholeskyQR breakdown the robust core and the outputs run again.
+rsvd_status run_with_retry(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool want_svd,
+                           const std::function<rsvd_status()>& emit = nullptr) {
   int flags = 0;
   ctx->last_robust = 0;
   CKS(rsvd_core(ctx, p, prm, false, want_svd));
+  if (emit) CKS(emit());
   CKS(finish_flags(ctx, &flags));
   if (flags & kFlagCholBreak) {
     ctx->last_robust = 1;
     CKS(rsvd_core(ctx, p, prm, true, want_svd));
+    if (emit) CKS(emit());
     CKS(finish_flags(ctx, &flags));
   }
   if (flags & kFlagNonFinite) return fail(ctx, RSVD_ENUMERIC, "non-finite intermediate (input contains Inf/NaN?)");
@@ -707,30 +720,30 @@ rsvd_status rsvd_run(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm
   CK(cudaSetDevice(ctx->device));
   Plan p{};
   CKS(make_plan(ctx, A, prm.k, prm.p, prm.center || prm.scale, p));
-  CKS(run_with_retry(ctx, p, &prm, true));
   const bool f32 = p.f32;
   const int Np = p.Np;
+  const int nu = prm.nu, nv = prm.nv;
   // outputs: U = Q (U~ diag sgn), V (sign-fixed), d = sigma(1:k)
-  int nu = prm.nu, nv = prm.nv;
-  double* Uo = p.T;      // M x Np scratch
-  if (!p.trans_input) {
-    if (nu > 0) {
-      if (!f32) { CKS(small_k(ctx, p, p.Y, p.M, p.W, (double*)u, ldu, nu)); }
-      else {
-        CKS(small_k(ctx, p, p.Y, p.M, p.W, Uo, Np, nu));
-        CK(launch_copy_out(Uo, Np, p.M, nu, u, ldu, true, nullptr, ctx->stream));
+  auto emit = [&]() -> rsvd_status {
+    double* Uo = p.T;      // M x Np scratch
+    if (!p.trans_input) {
+      if (nu > 0) {
+        if (!f32) { CKS(small_k(ctx, p, p.Y, p.M, p.W, (double*)u, ldu, nu)); }
+        else {
+          CKS(small_k(ctx, p, p.Y, p.M, p.W, Uo, Np, nu));
+          CK(launch_copy_out(Uo, Np, p.M, nu, u, ldu, true, nullptr, ctx->stream));
+        }
       }
+      if (nv > 0) CK(launch_copy_out(p.X, Np, p.n, nv, v, ldv, f32, nullptr, ctx->stream));
+    } else {
+      // worked on A^T = U' S V'^T  =>  A = V' S U'^T: u <- V' (n_eff rows), v <- U'
+      if (nu > 0) CK(launch_copy_out(p.X, Np, p.n, nu, u, ldu, f32, nullptr, ctx->stream));
+      if (nv > 0) CK(launch_copy_out(p.T, Np, p.M, nv, v, ldv, f32, nullptr, ctx->stream));
     }
-    if (nv > 0) CK(launch_copy_out(p.X, Np, p.n, nv, v, ldv, f32, nullptr, ctx->stream));
-  } else {
-    // worked on A^T = U' S V'^T  =>  A = V' S U'^T: u <- V' (n_eff rows), v <- U'
-    (void)Uo;
-    if (nu > 0) CK(launch_copy_out(p.X, Np, p.n, nu, u, ldu, f32, nullptr, ctx->stream));
-    if (nv > 0) CK(launch_copy_out(p.T, Np, p.M, nv, v, ldv, f32, nullptr, ctx->stream));
-  }
-  CK(launch_copy_out(p.sigma, 1, prm.k, 1, d, 1, f32, nullptr, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  if (ctx->prof) prof_collect(ctx);
+    CK(launch_copy_out(p.sigma, 1, prm.k, 1, d, 1, f32, nullptr, ctx->stream));
+    return RSVD_OK;
+  };
+  CKS(run_with_retry(ctx, p, &prm, true, emit));
   return RSVD_OK;
 }
 

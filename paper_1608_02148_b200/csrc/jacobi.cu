@@ -22,6 +22,12 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef JAC_PROBE
+#define JAC_PROBE_DECL
+#define JAC_PROBE(slot)
+#define JAC_PROBE_OUT
+#endif
+
 namespace rsvd {
 
 namespace {
@@ -43,18 +49,33 @@ __device__ __forceinline__ void jac_pair(int lh, int s, int k, int& p, int& q) {
 // Rotation (c, s) annihilating gamma for column norms alpha, beta:
 // t = 2 ga sgn(be - al) / (|be - al| + sqrt((be - al)^2 + 4 ga^2)) (the oracle's zeta
 // formula rewritten).  The angle only steers convergence (orthogonality of the
-// rotation comes from c^2 + s^2 = 1), so t is formed in FP32 on operands scaled
-// by a power of two to O(1), and c = (1 + t^2)^-1/2 is refined to FP64 by Newton.
+// rotation comes from c^2 + s^2 = 1), so t is formed from the hardware FP64
+// reciprocal / rsqrt approximations (one Newton step each, ~2^-40) on operands
+// scaled by a power of two to O(1), and c = (1 + t^2)^-1/2 is refined to FP64
+// by Newton.  No FP32 round trips (each F2F conversion sits on the per-step
+// critical path).
+__device__ __forceinline__ double rcp_nr1(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y * fma(-x, y, 2.0);
+}
+__device__ __forceinline__ double rsqrt_approx(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
 __device__ __forceinline__ void jac_rot(double al, double be, double ga, double& c, double& sn) {
   const double dlt = be - al, g2 = 2.0 * ga;
   const double mx = fmax(fabs(dlt), fabs(g2));
   const long long ex = (__double_as_longlong(mx) >> 52) & 0x7ff;          // biased exponent
   const double scale = __longlong_as_double((2046 - ex) << 52);           // ~ 1 / mx (power of two)
-  const float df = (float)(dlt * scale), gf = (float)(g2 * scale);
-  const float tf = __fdividef(df >= 0.f ? gf : -gf, fabsf(df) + sqrtf(fmaf(df, df, gf * gf)));
-  const double t = (double)tf;
+  const double df = dlt * scale, gf = g2 * scale;                          // exact
+  const double h = fma(df, df, gf * gf);
+  double r = rsqrt_approx(h);
+  r = r * fma(-0.5 * h * r, r, 1.5);
+  const double t = (df >= 0.0 ? gf : -gf) * rcp_nr1(fabs(df) + h * r);
   const double x = fma(t, t, 1.0);
-  double c0 = (double)rsqrtf((float)x);
+  double c0 = rsqrt_approx(x);
   c0 = c0 * fma(-0.5 * x * c0, c0, 1.5);
   c0 = c0 * fma(-0.5 * x * c0, c0, 1.5);
   c = c0;
@@ -98,6 +119,7 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
   int sweeps = 0;
   bool converged = bad != 0;
   int64_t gstep = 0;                                     // global step index into the log
+  JAC_PROBE_DECL
   for (int sweep = 0; sweep <= 30 && !converged; ++sweep) {
     for (int d = 0; d < levels; ++d) {
       const int lh = levels - 1 - d, h = 1 << lh;
@@ -112,12 +134,13 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
         double c = 1.0, sn = 0.0;
         {
           jac_pair(lh, s, k, p, q);
+          JAC_PROBE(0)
 #pragma unroll
           for (int e = 0; e < EPL; ++e) xt[e] = Xs[q * LDX + gs + JG * e];
           constexpr int NCH = EPL >= 4 ? 4 : EPL;        // independent accumulation chains
           double a[NCH], b[NCH], g[NCH];
 #pragma unroll
-          for (int c = 0; c < NCH; ++c) a[c] = b[c] = g[c] = 0.0;
+          for (int w = 0; w < NCH; ++w) a[w] = b[w] = g[w] = 0.0;
 #pragma unroll
           for (int e = 0; e < EPL; ++e) {
             a[e % NCH] = fma(xs[e], xs[e], a[e % NCH]);
@@ -125,7 +148,7 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
             g[e % NCH] = fma(xs[e], xt[e], g[e % NCH]);
           }
 #pragma unroll
-          for (int c = 1; c < NCH; ++c) { a[0] += a[c]; b[0] += b[c]; g[0] += g[c]; }
+          for (int w = 1; w < NCH; ++w) { a[0] += a[w]; b[0] += b[w]; g[0] += g[w]; }
           double al = a[0], be = b[0], ga = g[0];
 #pragma unroll
           for (int o = JG / 2; o > 0; o >>= 1) {
@@ -133,8 +156,10 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
             be += __shfl_xor_sync(0xffffffffu, be, o);
             ga += __shfl_xor_sync(0xffffffffu, ga, o);
           }
+          JAC_PROBE(1)
           if (ga * ga > tol2 * (al * be)) {
             jac_rot(al, be, ga, c, sn);
+            JAC_PROBE(2)
 #pragma unroll
             for (int e = 0; e < EPL; ++e) {
               const double u = xs[e], v = xt[e];
@@ -148,8 +173,10 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
             for (int e = 0; e < EPL; ++e) Xs[q * LDX + gs + JG * e] = xt[e];
             if (gs == 0) rlog[gstep * npairs + k] = make_double2(c, sn);
           }
+          JAC_PROBE(3)
         }
         __syncthreads();                                 // travelling columns published
+        JAC_PROBE(4)
       }
       if (act) {
 #pragma unroll
@@ -164,6 +191,7 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
     else ++sweeps;
     __syncthreads();
   }
+  JAC_PROBE_OUT
   // sigma_p = ||x_p||, stable descending ranks, W(:, rank) = x_p / sigma_p
   const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   for (int p = warp; p < l; p += nw) {

@@ -226,6 +226,29 @@ def test_rpca_large_offset_centring(rb):
     assert np.max(np.abs(ev - o["eigvals"]) / o["eigvals"]) < 1e-9
 
 
+@pytest.mark.parametrize("q", [1, 2])
+def test_rsvd_direct_power_scheme_parity(rb, q):
+    """Alg. 1 direct power scheme (power="direct") against the
+    oracle's Alg. 1 on the same Omega: d within 1e-10 relative, V columns
+    parallel, U orthonormal."""
+    A = _decay_matrix(3000, 700, seed=41 + q, noise=1e-6)
+    An = A.numpy()
+    r = rb.rsvd(A.cuda(), 20, p=10, q=q, seed=5, power="direct")
+    o = oracle.oracle_rsvd(An, 20, p=10, q=q, seed=5, power="direct")
+    d = _np(r.d)
+    assert np.max(np.abs(d - o["d"]) / o["d"]) < 1e-10
+    c = _cos_cols(_np(r.v), o["v"])
+    assert np.all(c[:15] > 1 - 1e-8)
+    u = _np(r.u)
+    assert np.abs(u.T @ u - np.eye(20)).max() < 1e-12
+
+
+def test_rsvd_power_param_rejected(rb):
+    A = torch.randn(50, 40, dtype=torch.float64).cuda()
+    with pytest.raises(rb.RsvdError):
+        rb.rsvd(A, 5, power=2)
+
+
 # ----------------------------------------------------------------------------- rrpca
 def test_rrpca_parity_small(rb):
     A, L0, S0 = synthetic.sparse_plus_lowrank(4000, 300, rank=5, frac=0.05, seed=12)

@@ -263,6 +263,28 @@ def test_rsvd_power_scheme_matches_Aq_sketch():
     assert np.abs(Bt - A.T @ Q).max() < 1e-13
 
 
+def test_direct_power_scheme_is_Aq_sketch():
+    """Alg. 1 (direct): the sketch after q iterations is exactly
+    A^(q) Omega = U S^(2q+1) V^T Omega (Eq. Aq), and on a
+    well-conditioned input the whole rsvd agrees with the Alg. 2 path."""
+    rng = np.random.default_rng(19)
+    m, n, l, q = 90, 60, 8, 2
+    U, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    s = np.linspace(2.0, 1.0, n)
+    A = (U * s) @ V.T
+    Aq = (U * s ** (2 * q + 1)) @ V.T
+    Om = omega(n, l, "normal", seed=6)
+    Qd, _ = np.linalg.qr(Aq @ Om)
+    Q, Bt = oracle_rqb(A, l, q, "normal", seed=6, power="direct")
+    assert np.linalg.svd(Qd.T @ Q, compute_uv=False).min() > 1 - 1e-12
+    assert np.abs(Bt - A.T @ Q).max() < 1e-13
+    r1 = oracle_rsvd(A, 5, p=3, q=q, seed=6, power="direct")
+    r2 = oracle_rsvd(A, 5, p=3, q=q, seed=6)
+    assert np.abs(r1["d"] - r2["d"]).max() < 1e-12
+    assert np.abs(np.abs(np.sum(r1["v"] * r2["v"], axis=0)) - 1).max() < 1e-9
+
+
 def test_rsvd_wide_input_transposes():
     A = np.random.default_rng(4).standard_normal((30, 70))
     r = oracle_rsvd(A, 5, nu=5, nv=3, p=5, q=1, seed=2)

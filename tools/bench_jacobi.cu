@@ -6,6 +6,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+__device__ unsigned long long g_jp[6];
+#define JAC_PROBE
+#define JAC_PROBE_DECL long long _jt[5] = {0, 0, 0, 0, 0}; long long _jl = clock64();
+#define JAC_PROBE(slot) if (threadIdx.x == 0) { long long _t = clock64(); _jt[slot] += _t - _jl; _jl = _t; }
+#define JAC_PROBE_OUT if (threadIdx.x == 0) { for (int q = 0; q < 5; ++q) atomicAdd(&g_jp[q], (unsigned long long)_jt[q]); atomicAdd(&g_jp[5], (unsigned long long)gstep); }
 #include "../paper_1608_02148_b200/csrc/jacobi.cu"
 namespace rsvd { int64_t g_kernel_launches = 0; }
 using namespace rsvd;
@@ -35,10 +40,13 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&J, ld * ld * 8)); CK(cudaMalloc(&scr, jacobi_scratch_bytes(l)));
     CK(cudaMemcpy(dR, R.data(), ld * ld * 8, cudaMemcpyHostToDevice));
     CK(cudaMemset(flag, 0, 64));
-    for (int jg : {4}) {
+    for (int jg : {4, 8}) {
       g_jacobi_lanes = jg;
       float tj = timeit([&] { launch_jacobi(dR, ld, l, sig, W, J, ld, flag, sw, scr, 0); }, 10);
-      printf("    lanes/pair %2d: %8.2f us\n", jg, tj);
+      unsigned long long pr[6]; cudaMemcpyFromSymbol(pr, g_jp, sizeof pr); unsigned long long z[6] = {0}; cudaMemcpyToSymbol(g_jp, z, sizeof z);
+      const double st = pr[5] > 0 ? (double)pr[5] : 1.0;
+      printf("    lanes/pair %2d: %8.2f us | cycles/step (thread 0): ld->reduced %.0f  rot %.0f  apply+store %.0f  barrier %.0f  (other %.0f)\n", jg, tj,
+             pr[1] / st, pr[2] / st, pr[3] / st, pr[4] / st, pr[0] / st);
     }
     g_jacobi_lanes = 0;
     float t = timeit([&] { launch_jacobi(dR, ld, l, sig, W, J, ld, flag, sw, scr, 0); }, 10);
