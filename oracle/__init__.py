@@ -19,6 +19,7 @@ Passages followed (PAPER.md line numbers, "P:n"):
   * ``rsvd()`` interface           P:706-724 (§3.6)
   * Alg. 6 ``rpca``                P:1336-1361, Eq. P:1322 (§4.2)
   * Alg. 7 ``rrpca`` (IALM)        P:1655-1723 (§5.3)
+  * Alg. id / rid / rcur           P:2059-2127, Alg. rcur P:1975-2010 (§6)
 
 Pins: every function here is pinned by ``tests/test_oracle_pins.py`` against
 closed forms, textbook special cases, an independent Philox implementation
@@ -27,7 +28,7 @@ inputs.  Parity unpinned: the paper's printed Table 1-3 numbers (their datasets
 are not available), see DESIGN.md §Readings.
 """
 from .philox import philox4x32_10, omega, u01
-from .linalg import hqr, jacobi_svd_bt, soft_threshold
+from .linalg import hqr, jacobi_svd_bt, qrcp, soft_threshold
 from .rsvd import (oracle_rqb, oracle_rsvd, oracle_rpca, oracle_rrpca,
                    resolve_params, sign_fix)
 

@@ -9,6 +9,10 @@
   economic SVD" (reading R7).
 * ``soft_threshold``: shrink(x, tau) = sign(x) max(|x| - tau, 0)
   (Alg. 7 steps (8) and (10)).
+* ``qrcp``: QR with column pivoting, "[~, S, P] = qr(A)  pivoted QR
+  decomposition" (Alg. id step (1); "stopped after k iterations to
+  obtain only the k dominant pivots"): Businger-Golub largest
+  remaining column norm, ties to the lowest index (reading R31).
 
 Plain loops over columns / column pairs with numpy vector operations; no
 blocking, no reordering beyond the textbook algorithms.
@@ -126,3 +130,38 @@ def soft_threshold(x, tau):
     """shrink(x, tau) = sign(x) * max(|x| - tau, 0), entrywise (P:1691, P:1698)."""
     x = np.asarray(x, dtype=np.float64)
     return np.sign(x) * np.maximum(np.abs(x) - tau, 0.0)
+
+
+def qrcp(A, steps=None):
+    """Householder QR with column pivoting (Businger-Golub), `steps` pivots.
+
+    At step j the column with the largest 2-norm of rows j.. among the not yet
+    pivoted columns is swapped to position j (first one on ties, reading R31),
+    then reflected with the hqr convention (alpha = -sign(x_0) ||x||,
+    H = I - 2 v v^T / v^T v).  Returns S (min(m, steps) x n, upper trapezoidal
+    in the pivoted column order; rows >= steps hold the un-reduced remainder
+    when steps < min(m, n)) and the permutation P (column j of S is column
+    P[j] of A)."""
+    R = np.array(A, dtype=np.float64)
+    m, n = R.shape
+    steps = min(m, n) if steps is None else min(int(steps), m, n)
+    P = np.arange(n)
+    for j in range(steps):
+        norms = np.sum(R[j:, j:] * R[j:, j:], axis=0)
+        pj = j + int(np.argmax(norms))
+        if pj != j:
+            R[:, [j, pj]] = R[:, [pj, j]]
+            P[[j, pj]] = P[[pj, j]]
+        x = R[j:, j]
+        nx = np.sqrt(np.dot(x, x))
+        if nx == 0.0:
+            continue
+        alpha = -_sign(x[0]) * nx
+        v = x.copy()
+        v[0] -= alpha
+        vtv = np.dot(v, v)
+        w = v @ R[j:, j + 1:]
+        R[j:, j + 1:] -= np.outer(v, w) * (2.0 / vtv)
+        R[j + 1:, j] = 0.0
+        R[j, j] = alpha
+    return R, P

@@ -22,7 +22,7 @@ the QR and SVD are written out in oracle/linalg.py.
 """
 import numpy as np
 
-from .linalg import hqr, jacobi_svd_bt, soft_threshold
+from .linalg import hqr, jacobi_svd_bt, qrcp, soft_threshold
 from .philox import omega
 
 
@@ -222,3 +222,63 @@ def oracle_rrpca(A, lam=None, maxiter=100, tol=1e-7, k=20, p=10, q=2,
             break
     return dict(L=L, S=S, iters=it, residual=res, trace=hist, lam=lam, mu0=mu0,
                 norm2=norm2)
+
+
+def _triu_solve(S, B):
+    """X = S^-1 B for upper-triangular nonsingular S (back substitution)."""
+    k = S.shape[0]
+    X = np.zeros_like(B, dtype=np.float64)
+    for i in range(k - 1, -1, -1):
+        X[i] = (B[i] - S[i, i + 1:] @ X[i + 1:]) / S[i, i]
+    return X
+
+
+def oracle_id(A, k):
+    """Alg. id, column interpolative decomposition A ~ C Z:
+      (1) [~, S, P] = qr(A)  pivoted QR, k steps
+      (2) S^+ = pinv(S(1:k, 1:k))      -- S(1:k,1:k) is upper triangular; for
+                                         rank >= k it is invertible and pinv = the
+                                         inverse (back substitution, reading R31)
+      (3) T = S^+ S(1:k, (k+1):n)
+      (4)-(5) Z = 0 (k x n); Z(:, P) = [I_k, T]
+      (6) J = P(1:k);  (7) C = A(:, J)
+    Returns dict(C, Z, J, S, P)."""
+    A = np.asarray(A, dtype=np.float64)
+    m, n = A.shape
+    S, P = qrcp(A, k)
+    T = _triu_solve(S[:k, :k], S[:k, k:])
+    Z = np.zeros((k, n))
+    Z[:, P] = np.hstack([np.eye(k), T])
+    J = P[:k].copy()
+    return dict(C=A[:, J].copy(), Z=Z, J=J, S=S, P=P)
+
+
+def oracle_rid(A, k, p=10, q=2, sdist="normal", seed=0, stream=0):
+    """Alg. rid (P:2100-2127): (1) [~, B] = rqb(A, k, q, p) (Alg. 4; the
+    argument order in the listing is a typo, reading R27); (2) [~, Z, J] =
+    id(B, k); (3) C = A(:, J).  Returns dict(C, Z, J)."""
+    A = np.asarray(A, dtype=np.float64)
+    m, n = A.shape
+    k, _, _, l = resolve_params(m, n, k, 0, 0, p, q)
+    Q, Bt = oracle_rqb(A, l, q, sdist, seed, stream)
+    r = oracle_id(Bt.T, k)
+    return dict(C=A[:, r["J"]].copy(), Z=r["Z"], J=r["J"])
+
+
+def oracle_rcur(A, k, p=10, q=2, sdist="normal", seed=0, stream=0):
+    """Alg. rcur (P:1975-2010):
+      (1) [C, Z, J] = rid(A, k, p, q)
+      (2) [~, S, P] = qr(C^T)  pivoted QR;  (3) I = P(1:k)
+      (4) R = A(I, :);  (5) R^+ = pinv(R);  (6) U = Z R^+
+    pinv(R) for the full-row-rank R (k x n): R^+ = Q_R S_R^-T from the
+    Householder QR R^T = Q_R S_R (reading R31).  Returns dict(C, U, R, J, I)."""
+    A = np.asarray(A, dtype=np.float64)
+    r = oracle_rid(A, k, p, q, sdist, seed, stream)
+    k = r["C"].shape[1]
+    _S, P = qrcp(r["C"].T, k)
+    I = P[:k].copy()
+    R = A[I, :].copy()
+    Qr, Sr = hqr(R.T)
+    Rpinv = Qr @ _triu_solve(Sr, np.eye(k)).T          # Q_R S_R^-T
+    U = r["Z"] @ Rpinv
+    return dict(C=r["C"], U=U, R=R, J=r["J"], I=I, Z=r["Z"])

@@ -106,27 +106,28 @@ gram_partial_kernel(const double* __restrict__ S, int64_t lds, int64_t rows, int
     }
 }
 
-// G (Np x Np, ld ldg) = sum_{p < P} partial_p (Ng x Ng), fixed order: T lanes per
-// element each sum p = t, t+T, ... ascending, then a fixed xor tree.
+// upper triangle of G (Np x Np, ld ldg) = sum_{p < P} partial_p (Ng x Ng), fixed order: T lanes per
+// element each sum p = t, t+T, ... ascending (loads issued in batches of 8 so
+// they are in flight together), then a fixed xor tree.
 __global__ void gram_reduce_kernel(const double* __restrict__ partial, int P, int Ng, int Np,
                                    double* __restrict__ G, int ldg) {
-  constexpr int T = 8;
+  constexpr int T = 8, B = 8;
   const int e = blockIdx.x * (blockDim.x / T) + threadIdx.x / T;
   const int t = threadIdx.x % T;
   const int r = e / Np, c = e - (e / Np) * Np;
-  const bool ok = e < Np * Np;
-  double s0 = 0.0, s1 = 0.0;
+  const bool ok = e < Np * Np && r <= c;                  // upper triangle (all chol_aug reads)
+  double s = 0.0;
   if (ok) {
-    const double* p = partial + (r <= c ? r * Ng + c : c * Ng + r);   // upper blocks hold G
+    const double* p = partial + r * Ng + c;                          // upper blocks hold G
     const int64_t step = (int64_t)Ng * Ng;
-    int q = t;
-    for (; q + T < P; q += 2 * T) {
-      s0 += p[q * step];
-      s1 += p[(q + T) * step];
+    for (int q0 = t; q0 < P; q0 += T * B) {
+      double v[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) v[b] = (q0 + b * T < P) ? __ldcg(p + (q0 + b * T) * step) : 0.0;
+#pragma unroll
+      for (int b = 0; b < B; ++b) s += v[b];
     }
-    if (q < P) s0 += p[q * step];
   }
-  double s = s0 + s1;
 #pragma unroll
   for (int o = T / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (ok && t == 0) G[r * ldg + c] = s;

@@ -393,3 +393,58 @@ def test_rrpca_adaptive_rank_settles_at_rank_plus_one():
     assert out["residual"] < 1e-7
     assert np.linalg.norm(out["L"] - L0) / np.linalg.norm(L0) < 1e-5
     assert ((np.abs(out["S"]) > 1e-6) == (S0 != 0)).mean() > 0.999
+
+
+# ----------------------------------------------------------------------------- id / rid / rcur (§8(f) f3)
+def test_qrcp_matches_lapack_geqp3():
+    """Pivoted QR (Alg. id step (1)) against LAPACK's geqp3 (scipy):
+    same pivot order on inputs with distinct column norms, |diag S| equal,
+    and A(:, P) = Q S reconstructed with the oracle's own factor."""
+    import scipy.linalg as sl
+    from oracle.linalg import qrcp
+    rng = np.random.default_rng(21)
+    for m, n in [(40, 30), (25, 60), (9, 9)]:
+        A = rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 10.0)[None, :]
+        S, P = qrcp(A)
+        _q, R, P2 = sl.qr(A, pivoting=True)
+        assert (P == P2).all()
+        r = min(m, n)
+        assert np.abs(np.abs(np.diag(S[:r, :r])) - np.abs(np.diag(R[:r, :r]))).max() < 1e-12
+        assert np.abs(np.tril(S[:r, :r], -1)).max() == 0.0
+        # orthogonal invariance: S^T S = A(:,P)^T A(:,P)
+        assert np.abs(S.T @ S - A[:, P].T @ A[:, P]).max() < 1e-12 * np.abs(A).max() ** 2 * m
+
+
+def test_id_worked_example_and_exact_rank():
+    """Alg. id.  Hand case: diag(1, 3, 2) pivots the columns by
+    norm (P = [1, 2, 0]), k = 2 gives J = [1, 2] and Z = [[0, 1, 0], [0, 0, 1]].
+    Exact rank k: C Z = A (the ID is exact), Z(:, J) = I_k."""
+    from oracle.rsvd import oracle_id
+    r = oracle_id(np.diag([1.0, 3.0, 2.0]), 2)
+    assert list(r["J"]) == [1, 2]
+    assert np.abs(r["Z"] - np.array([[0.0, 1.0, 0.0], [0.0, 0.0, 1.0]])).max() < 1e-15
+    rng = np.random.default_rng(22)
+    A = rng.standard_normal((150, 9)) @ rng.standard_normal((9, 80))
+    r = oracle_id(A, 9)
+    assert np.abs(r["C"] @ r["Z"] - A).max() < 1e-12 * np.abs(A).max()
+    assert np.abs(r["Z"][:, r["J"]] - np.eye(9)).max() < 1e-15
+    assert np.abs(r["C"] - A[:, r["J"]]).max() == 0.0
+
+
+def test_rid_rcur_exact_rank_reconstruct():
+    """Alg. rid and rcur on an exactly rank-k
+    input: C Z = A and C U R = A to rounding (C and R span the column and row
+    spaces), the randomized ID picks the same columns as the deterministic ID
+    of A when l = min(m, n) (Q Q^T A = A, so B = Q^T A has A's pivots)."""
+    from oracle.rsvd import oracle_id, oracle_rid, oracle_rcur
+    rng = np.random.default_rng(23)
+    A = rng.standard_normal((300, 12)) @ rng.standard_normal((12, 90))
+    r = oracle_rid(A, 12, p=6, q=1, seed=3)
+    assert np.abs(r["C"] @ r["Z"] - A).max() < 1e-11 * np.abs(A).max()
+    c = oracle_rcur(A, 12, p=6, q=1, seed=3)
+    assert np.abs(c["C"] @ c["U"] @ c["R"] - A).max() < 1e-10 * np.abs(A).max()
+    assert np.abs(c["R"] - A[c["I"], :]).max() == 0.0
+    small = rng.standard_normal((40, 25))
+    full = oracle_rid(small, 5, p=20, q=0, seed=1)     # l = 25 = min(m, n)
+    det = oracle_id(small, 5)
+    assert list(full["J"]) == list(det["J"])
