@@ -124,6 +124,28 @@ rsvd_status rsvd_run(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm
 rsvd_status rsvd_rqb(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm,
                      void* Q, int64_t ldq, void* Bt, int64_t ldb);
 
+/* Randomized column interpolative decomposition, Alg. rid
+ * with Alg. id applied to B = Q^T A of rqb (reading R31):
+ * A ~ C Z with C = A(:, J), Z(:, J) = I_k.  Pivots: Businger-Golub pivoted QR
+ * of B stopped after k steps.  FP64, m >= n; rows may be
+ * distributed (C holds this rank's rows, Z and J are replicated).
+ *   C  DEVICE m_local x k (ldc >= k)   skeleton columns
+ *   Z  DEVICE k x n (ldz >= n)         interpolation matrix
+ *   J  DEVICE int64 k                  column indices, in pivot order
+ * RSVD_ENUMERIC if the numerical rank of B is < k (S(1:k,1:k) singular). */
+rsvd_status rsvd_rid(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm,
+                     void* C, int64_t ldc, void* Z, int64_t ldz, int64_t* J);
+
+/* Randomized CUR decomposition, Alg. rcur: rid, then the
+ * pivoted QR of C^T gives the row indices I = P(1:k); R = A(I, :) and
+ * U = Z pinv(R) with pinv(R) = Q_R S_R^-T from the Householder QR R^T =
+ * Q_R S_R (reading R31).  A ~ C U R.  FP64, single GPU, m >= n.
+ *   C  DEVICE m x k (ldc >= k);  U  DEVICE k x k (ldu >= k);
+ *   R  DEVICE k x n (ldr >= n);  J, I  DEVICE int64 k (column / row indices) */
+rsvd_status rsvd_rcur(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm,
+                      void* C, int64_t ldc, void* U, int64_t ldu, void* R, int64_t ldr,
+                      int64_t* J, int64_t* I);
+
 /* Randomized PCA, Alg. 6, interface P:1381-1398:
  * rsvd on X = (A - 1 c^T) diag(1/s) (centring/scaling never materialised).
  *   rotation DEVICE n x k (ldr >= k)       = V
@@ -171,10 +193,13 @@ rsvd_status rsvd_omega(rsvd_ctx* ctx, int64_t n, int64_t l, int32_t sdist, uint6
                        uint64_t stream, int32_t dtype, void* out, int64_t ldo);
 
 /* Per-kernel timing of the last calls (CUDA events on the context stream,
- * enabled by rsvd_set_profiling(ctx, 1)).  kind: 0 = sketch/power pass A.X,
+ * enabled by rsvd_set_profiling(ctx, 1); 2 = only the pass kernels, kinds
+ * 0, 1, 6, for the least event overhead).  kind: 0 = sketch/power pass A.X,
  * 1 = transposed pass A^T.X (incl. its split reduction), 2 = panel
  * orthonormalisation, 3 = small SVD, 4 = other, 5 = Ozaki slicing of A
- * (FP64 inputs on the tensor-core path, once per call).  Returns accumulated
+ * (FP64 inputs on the tensor-core path, once per call), 6 = Ozaki slicing of
+ * the panel X before each pass (kinds 0 / 1 then time the pass kernels
+ * alone).  Returns accumulated
  * milliseconds and launch count since the last reset (HOST out-params). */
 rsvd_status rsvd_set_profiling(rsvd_ctx* ctx, int enable);
 rsvd_status rsvd_profile(rsvd_ctx* ctx, int kind, double* total_ms, int64_t* count,

@@ -29,7 +29,7 @@ are not available), see DESIGN.md §Readings.
 """
 from .philox import philox4x32_10, omega, u01
 from .linalg import hqr, jacobi_svd_bt, qrcp, soft_threshold
-from .rsvd import (oracle_rqb, oracle_rsvd, oracle_rpca, oracle_rrpca,
+from .rsvd import (oracle_rqb, oracle_rsvd, oracle_rpca, oracle_rrpca, oracle_id, oracle_rid, oracle_rcur, predict_rank,
                    resolve_params, sign_fix)
 
 __all__ = ["philox4x32_10", "omega", "u01", "hqr", "jacobi_svd_bt",

@@ -246,6 +246,9 @@ def oracle_id(A, k):
     A = np.asarray(A, dtype=np.float64)
     m, n = A.shape
     S, P = qrcp(A, k)
+    d = np.abs(np.diag(S[:k, :k]))
+    if not d[0] > 0 or np.any(d[1:] <= m * 2.0 ** -52 * d[0]):
+        raise ValueError("numerical rank < k: S(1:k,1:k) singular (reading R31)")
     T = _triu_solve(S[:k, :k], S[:k, k:])
     Z = np.zeros((k, n))
     Z[:, P] = np.hstack([np.eye(k), T])

@@ -28,7 +28,7 @@ STATUS = {0: "RSVD_OK", 1: "RSVD_EINVAL", 2: "RSVD_ENOMEM", 3: "RSVD_ECUDA", 4: 
 EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_last_error", "rsvd_version", "rsvd_nccl_unique_id",
            "rsvd_comm_init", "rsvd_params_default", "rsvd_run", "rsvd_rqb", "rsvd_rpca",
            "rsvd_rrpca_params_default", "rsvd_rrpca", "rsvd_omega", "rsvd_set_profiling", "rsvd_profile",
-           "rsvd_profile_reset", "rsvd_launch_count", "rsvd_stats"]
+           "rsvd_profile_reset", "rsvd_launch_count", "rsvd_stats", "rsvd_rid", "rsvd_rcur"]
 
 
 class RsvdError(RuntimeError):
@@ -83,6 +83,8 @@ def lib():
         "rsvd_rqb": ([vp, MP, PP, vp, i64, vp, i64], ctypes.c_int),
         "rsvd_rpca": ([vp, MP, PP, vp, i64, vp, vp, i64, vp, vp], ctypes.c_int),
         "rsvd_rrpca_params_default": ([ctypes.POINTER(RrpcaParams)], None),
+        "rsvd_rid": ([vp, MP, PP, vp, i64, vp, i64, vp], i32),
+        "rsvd_rcur": ([vp, MP, PP, vp, i64, vp, i64, vp, i64, vp, vp], i32),
         "rsvd_rrpca": ([vp, MP, ctypes.POINTER(RrpcaParams), vp, vp, i64, ctypes.POINTER(i32),
                         ctypes.POINTER(dp), ctypes.POINTER(dp)], ctypes.c_int),
         "rsvd_omega": ([vp, i64, i64, i32, u64, u64, i32, vp, i64], ctypes.c_int),
@@ -146,7 +148,9 @@ class Context:
         self.rank, self.world = rank, world
 
     def set_profiling(self, on=True):
-        self.check(lib().rsvd_set_profiling(self.h, 1 if on else 0))
+        """on: False/0 off, True/1 every kind, 2 = the pass kernels only."""
+        level = (1 if on else 0) if isinstance(on, bool) else int(on)
+        self.check(lib().rsvd_set_profiling(self.h, level))
 
     def profile(self, kind):
         ms, cnt, by = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
@@ -270,6 +274,39 @@ def rqb(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None, m_global=No
     prm = _params(k, 0, 0, p, q, sdist, seed, stream)
     ctx.check(lib().rsvd_rqb(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(Q), l, _ptr(Bt), l))
     return Q, Bt.T
+
+
+def rid(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None, m_global=None, row_offset=0):
+    """Randomized column ID (Alg. rid; Alg. id):
+    returns dict(C (m x k) = A[:, J], Z (k x n), J (k,) int64 pivot order)."""
+    ctx = ctx or default_context(A.device)
+    mat = _matrix(A, m_global, row_offset)
+    m, n = A.shape
+    kk = int(k)
+    C = torch.empty(m, kk, dtype=A.dtype, device=A.device)
+    Z = torch.empty(kk, n, dtype=A.dtype, device=A.device)
+    J = torch.empty(kk, dtype=torch.int64, device=A.device)
+    prm = _params(k, 0, 0, p, q, sdist, seed, stream)
+    ctx.check(lib().rsvd_rid(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(C), kk, _ptr(Z), n, _ptr(J)))
+    return dict(C=C, Z=Z, J=J)
+
+
+def rcur(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None):
+    """Randomized CUR (Alg. rcur): A ~ C U R; returns
+    dict(C (m x k), U (k x k), R (k x n), J (column indices), I (row indices))."""
+    ctx = ctx or default_context(A.device)
+    mat = _matrix(A, None, 0)
+    m, n = A.shape
+    kk = int(k)
+    C = torch.empty(m, kk, dtype=A.dtype, device=A.device)
+    U = torch.empty(kk, kk, dtype=A.dtype, device=A.device)
+    R = torch.empty(kk, n, dtype=A.dtype, device=A.device)
+    J = torch.empty(kk, dtype=torch.int64, device=A.device)
+    I = torch.empty(kk, dtype=torch.int64, device=A.device)
+    prm = _params(k, 0, 0, p, q, sdist, seed, stream)
+    ctx.check(lib().rsvd_rcur(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(C), kk, _ptr(U), kk, _ptr(R), n,
+                              _ptr(J), _ptr(I)))
+    return dict(C=C, U=U, R=R, J=J, I=I)
 
 
 def rpca(A, k, center=True, scale=False, retx=True, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None,

@@ -35,7 +35,7 @@ using namespace rsvd;
 
 namespace {
 
-constexpr int kFlagCholBreak = 1, kFlagJacobiCap = 2, kFlagNonFinite = 4;
+constexpr int kFlagCholBreak = 1, kFlagJacobiCap = 2, kFlagNonFinite = 4, kFlagRankDef = 8;
 constexpr int kMaxL = 120;       // Jacobi + leaf QR shared-memory envelope
 
 struct ProfRec { int kind; double bytes; cudaEvent_t a, b; };
@@ -62,12 +62,12 @@ struct rsvd_ctx {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   // profiling
-  bool prof = false;
+  int prof = 0;                   // 0 off, 1 every kind, 2 the pass kernels only (kinds 0, 1, 6)
   std::vector<ProfRec> pending;
   std::vector<cudaEvent_t> pool;
-  double prof_ms[6] = {0, 0, 0, 0, 0, 0};
-  double prof_bytes[6] = {0, 0, 0, 0, 0, 0};
-  int64_t prof_count[6] = {0, 0, 0, 0, 0, 0};
+  double prof_ms[7] = {0, 0, 0, 0, 0, 0, 0};
+  double prof_bytes[7] = {0, 0, 0, 0, 0, 0, 0};
+  int64_t prof_count[7] = {0, 0, 0, 0, 0, 0, 0};
   int64_t launches = 0;
   int last_sweeps = 0;
   bool fp32_tcgen05 = true;       // RSVD_FP32_PATH=dmma selects the FP64-DMMA path for FP32 inputs
@@ -120,10 +120,11 @@ cudaEvent_t take_event(rsvd_ctx* c) {
 struct Prof {
   rsvd_ctx* c; int kind; double bytes; cudaEvent_t a = nullptr;
   Prof(rsvd_ctx* c_, int k, double b) : c(c_), kind(k), bytes(b) {
-    if (c->prof) { a = take_event(c); cudaEventRecord(a, c->stream); }
+    if (on()) { a = take_event(c); cudaEventRecord(a, c->stream); }
   }
+  bool on() const { return c->prof == 1 || (c->prof == 2 && (kind == 0 || kind == 1 || kind == 6)); }
   ~Prof() {
-    if (c->prof) {
+    if (on()) {
       cudaEvent_t b2 = take_event(c);
       cudaEventRecord(b2, c->stream);
       c->pending.push_back({kind, bytes, a, b2});
@@ -162,6 +163,7 @@ struct Plan {
   bool use_ozaki = false;         // FP64 A on tcgen05 (Ozaki int8 slices)
   OzakiA oz{};
   void* ozx = nullptr;            // X slice scratch
+  void* ozx2 = nullptr;           // second 64-column block (Np > 64)
   float* split = nullptr;
   void* jlog = nullptr;
   size_t part_bytes;
@@ -262,22 +264,31 @@ rsvd_status pass_tf32(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, doubl
   return RSVD_OK;
 }
 
-rsvd_status pass_ozaki(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, double* C, int64_t M, int64_t K) {
+// One Ozaki pass: profile kind 6 = X slicing, `kind` (0 / 1) = the pass kernel(s)
+rsvd_status pass_ozaki(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, double* C, int64_t M, int64_t K,
+                       int kind) {
   OzakiCall o{};
   o.a = &p.oz; o.trans = trans; o.B = B; o.ldb = p.Np; o.C = C; o.ldc = p.Np; o.Nout = p.Np;
   o.P = p.part; o.flags = ctx->gemm_flags; o.epoch = ++ctx->gemm_epoch; o.epoch2 = ++ctx->gemm_epoch;
-  o.xscratch = p.ozx;
+  o.xscratch = p.ozx; o.xscratch2 = p.ozx2;
   o.M = M; o.K = K; o.N = p.Np; o.grid = ctx->num_sms;
   ++ctx->ozaki_calls;
+  if (!ctx->prof) {
+    CK(ozaki_pass(o, ctx->stream));
+    return RSVD_OK;
+  }
+  cudaEvent_t e0 = take_event(ctx), e1 = take_event(ctx), e1b = take_event(ctx), e2 = take_event(ctx);
+  cudaEventRecord(e0, ctx->stream);
+  o.mark = e1; o.mark2 = e1b;
   CK(ozaki_pass(o, ctx->stream));
+  cudaEventRecord(e2, ctx->stream);
+  ctx->pending.push_back({6, 0.0, e0, e1});
+  ctx->pending.push_back({kind, (double)p.M * p.n * 8, e1b, e2});
   return RSVD_OK;
 }
 
 rsvd_status pass_ax(rsvd_ctx* ctx, Plan& p, const double* X, double* Y, bool centred) {
-  if (p.use_ozaki) {
-    Prof pr(ctx, 0, (double)p.M * p.n * 8);
-    return pass_ozaki(ctx, p, p.trans_input, X, Y, p.M, p.n);
-  }
+  if (p.use_ozaki) return pass_ozaki(ctx, p, p.trans_input, X, Y, p.M, p.n, 0);
   if (p.use_tf32 && !centred) {
     Prof pr(ctx, 0, (double)p.M * p.n * 4);
     return pass_tf32(ctx, p, p.trans_input, X, Y, p.M, p.n);
@@ -299,10 +310,7 @@ rsvd_status pass_ax(rsvd_ctx* ctx, Plan& p, const double* X, double* Y, bool cen
 // Z (n x Np) = f(A)^T Q (K3), then allreduce over ranks.
 rsvd_status pass_atx(rsvd_ctx* ctx, Plan& p, const double* Q, double* Z, bool centred) {
   if (p.use_ozaki) {
-    {
-      Prof pr(ctx, 1, (double)p.M * p.n * 8);
-      CKS(pass_ozaki(ctx, p, !p.trans_input, Q, Z, p.n, p.M));
-    }
+    CKS(pass_ozaki(ctx, p, !p.trans_input, Q, Z, p.n, p.M, 1));
     return allreduce_sum(ctx, Z, (size_t)p.n * p.Np);
   }
   if (p.use_tf32 && !centred) {
@@ -577,16 +585,18 @@ rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bo
     // slices of the stored matrix (A->m_local x A->n), then the X slice scratch
     const size_t sa = align256(ozaki_a_bytes(A->m_local, A->n));
     const size_t sx = align256(ozaki_x_bytes(std::max(p.M, p.n), std::min(p.Np, 64)));
-    if (sa + sx > ctx->ws4_bytes) {
+    const size_t nx = p.Np > 64 ? 2 : 1;
+    if (sa + nx * sx > ctx->ws4_bytes) {
       if (ctx->ws4) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->ws4); ctx->ws4 = nullptr; ctx->ws4_bytes = 0; }
-      if (cudaMalloc(&ctx->ws4, sa + sx) != cudaSuccess) {
+      if (cudaMalloc(&ctx->ws4, sa + nx * sx) != cudaSuccess) {
         cudaGetLastError();
-        return fail(ctx, RSVD_ENOMEM, "Ozaki slice workspace of %zu bytes failed", sa + sx);
+        return fail(ctx, RSVD_ENOMEM, "Ozaki slice workspace of %zu bytes failed", sa + nx * sx);
       }
-      ctx->ws4_bytes = sa + sx;
+      ctx->ws4_bytes = sa + nx * sx;
     }
     p.oz = ozaki_layout_a(ctx->ws4, A->m_local, A->n);
     p.ozx = ctx->ws4 + sa;
+    p.ozx2 = nx > 1 ? ctx->ws4 + sa + sx : nullptr;
   }
   return RSVD_OK;
 }
@@ -764,6 +774,82 @@ rsvd_status rsvd_rqb(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm
   return RSVD_OK;
 }
 
+// Alg. rid: [~, B] = rqb(A, k, p, q); [~, Z, J] = id(B, k) (Alg. id,
+// P:2059-2095) by the pivoted QR of B (qrcp.cu, on B^T = A^T Q as computed);
+// C = A(:, J).  Reading R31.
+rsvd_status rsvd_rid(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, void* C, int64_t ldc, void* Z,
+                     int64_t ldz, int64_t* J) {
+  int64_t mg, n;
+  CKS(validate(ctx, A, prm, &mg, &n));
+  if (A->dtype != RSVD_F64) return fail(ctx, RSVD_EUNSUPPORTED, "rid is FP64 only");
+  if (prm->center || prm->scale) return fail(ctx, RSVD_EUNSUPPORTED, "rid has no centring / scaling");
+  const int k = prm->k;
+  if (!C || !Z || !J || ldc < k || ldz < n) return fail(ctx, RSVD_EINVAL, "C/Z/J null or ldc < k or ldz < n");
+  CK(cudaSetDevice(ctx->device));
+  Plan p{};
+  CKS(make_plan(ctx, A, k, prm->p, false, p));
+  if (p.trans_input) return fail(ctx, RSVD_EUNSUPPORTED, "rid needs m >= n");
+  if (p.l > 128) return fail(ctx, RSVD_EUNSUPPORTED, "rid needs l <= 128");
+  auto emit = [&]() -> rsvd_status {
+    CKS(ensure_ws2(ctx, qrcp_scratch_bytes(p.n, k, ctx->num_sms)));
+    CK(launch_qrcp(p.Z, p.Np, p.l, p.n, k, J, (double*)Z, ldz, ctx->ws2, ctx->flags_dev, kFlagRankDef,
+                   ctx->num_sms, ctx->stream));
+    CK(launch_gather_cols((const double*)A->A, A->lda, A->m_local, J, k, (double*)C, ldc, ctx->stream));
+    return RSVD_OK;
+  };
+  CKS(run_with_retry(ctx, p, prm, false, emit));
+  if (ctx->flags_host[0] & kFlagRankDef) return fail(ctx, RSVD_ENUMERIC, "pivoted QR: numerical rank of B < k");
+  return RSVD_OK;
+}
+
+// Alg. rcur: [C, Z, J] = rid(A, k, p, q); [~, S, P] = qr(C^T)
+// pivoted (k pivots over the m columns of C^T = rows of C); I = P(1:k);
+// R = A(I, :); U = Z pinv(R) with pinv(R) = Q_R S_R^-T from the Householder
+// TSQR of R^T (reading R31).
+rsvd_status rsvd_rcur(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, void* C, int64_t ldc, void* U,
+                      int64_t ldu, void* R, int64_t ldr, int64_t* J, int64_t* I) {
+  int64_t mg, n;
+  CKS(validate(ctx, A, prm, &mg, &n));
+  if (A->dtype != RSVD_F64) return fail(ctx, RSVD_EUNSUPPORTED, "rcur is FP64 only");
+  if (ctx->nranks > 1) return fail(ctx, RSVD_EUNSUPPORTED, "rcur is single-GPU (pivoted QR over distributed rows)");
+  if (prm->center || prm->scale) return fail(ctx, RSVD_EUNSUPPORTED, "rcur has no centring / scaling");
+  const int k = prm->k;
+  if (!C || !U || !R || !J || !I || ldc < k || ldu < k || ldr < n)
+    return fail(ctx, RSVD_EINVAL, "C/U/R/J/I null or ldc < k, ldu < k, ldr < n");
+  CK(cudaSetDevice(ctx->device));
+  Plan p{};
+  CKS(make_plan(ctx, A, k, prm->p, false, p));
+  if (p.trans_input) return fail(ctx, RSVD_EUNSUPPORTED, "rcur needs m >= n");
+  if (p.l > 128) return fail(ctx, RSVD_EUNSUPPORTED, "rcur needs l <= 128");
+  const int64_t m = A->m_local;
+  const double* Ad = (const double*)A->A;
+  const int Np2 = (int)round_up(k, 16);
+  double* Zs = p.X;                        // k x n, ld n (p.X is n x Np >= k x n)
+  double* Ct = p.T;                        // m x k copy of C for the pivoted QR of C^T
+  double* Rt = p.Y;                        // n x Np2 panel R^T -> Q_R
+  double* Sr = p.RB;                       // S_R (k x k, ld Np2)
+  auto emit = [&]() -> rsvd_status {
+    CKS(ensure_ws2(ctx, std::max(qrcp_scratch_bytes(p.n, k, ctx->num_sms), qrcp_scratch_bytes(m, k, ctx->num_sms))));
+    CK(launch_qrcp(p.Z, p.Np, p.l, p.n, k, J, Zs, p.n, ctx->ws2, ctx->flags_dev, kFlagRankDef, ctx->num_sms,
+                   ctx->stream));                                        // rid: Z, J
+    CK(launch_gather_cols(Ad, A->lda, m, J, k, (double*)C, ldc, ctx->stream));   // C = A(:, J)
+    CK(launch_gather_cols(Ad, A->lda, m, J, k, Ct, k, ctx->stream));
+    CK(launch_qrcp(Ct, k, k, m, k, I, nullptr, 0, ctx->ws2, ctx->flags_dev, kFlagRankDef, ctx->num_sms,
+                   ctx->stream));                                        // I = P(1:k) of qr(C^T)
+    CK(cudaMemsetAsync(Rt, 0, (size_t)p.n * Np2 * sizeof(double), ctx->stream));
+    CK(launch_gather_rows(Ad, A->lda, p.n, I, k, (double*)R, ldr, Rt, Np2, ctx->stream));   // R = A(I, :), R^T
+    Plan q = p;
+    q.l = k; q.Np = Np2;
+    CKS(orth(ctx, q, Rt, p.n, false, true, Sr));                         // R^T = Q_R S_R (TSQR)
+    CK(launch_zq(Zs, p.n, Rt, Np2, p.n, k, p.part, p.G, k, ctx->num_sms, ctx->stream));   // W = Z Q_R
+    CK(launch_rtsolve(p.G, k, Sr, Np2, k, (double*)U, ldu, ctx->stream));              // U = W S_R^-T
+    return RSVD_OK;
+  };
+  CKS(run_with_retry(ctx, p, prm, false, emit));
+  if (ctx->flags_host[0] & kFlagRankDef) return fail(ctx, RSVD_ENUMERIC, "pivoted QR: numerical rank < k");
+  return RSVD_OK;
+}
+
 rsvd_status rsvd_rpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm_in, void* rotation, int64_t ldr,
                       void* eigvals, void* x, int64_t ldx, void* center, void* scale) {
   int64_t mg, n;
@@ -802,12 +888,12 @@ rsvd_status rsvd_omega(rsvd_ctx* ctx, int64_t n, int64_t l, int32_t sdist, uint6
 
 rsvd_status rsvd_set_profiling(rsvd_ctx* ctx, int enable) {
   if (!ctx) return RSVD_EINVAL;
-  ctx->prof = enable != 0;
+  ctx->prof = enable == 2 ? 2 : (enable != 0 ? 1 : 0);
   return RSVD_OK;
 }
 
 rsvd_status rsvd_profile(rsvd_ctx* ctx, int kind, double* total_ms, int64_t* count, double* bytes) {
-  if (!ctx || kind < 0 || kind > 5) return RSVD_EINVAL;
+  if (!ctx || kind < 0 || kind > 6) return RSVD_EINVAL;
   if (!ctx->pending.empty()) {
     cudaStreamSynchronize(ctx->stream);
     prof_collect(ctx);
@@ -821,7 +907,7 @@ rsvd_status rsvd_profile(rsvd_ctx* ctx, int kind, double* total_ms, int64_t* cou
 rsvd_status rsvd_profile_reset(rsvd_ctx* ctx) {
   if (!ctx) return RSVD_EINVAL;
   if (!ctx->pending.empty()) { cudaStreamSynchronize(ctx->stream); prof_collect(ctx); }
-  for (int i = 0; i < 6; ++i) { ctx->prof_ms[i] = 0; ctx->prof_bytes[i] = 0; ctx->prof_count[i] = 0; }
+  for (int i = 0; i < 7; ++i) { ctx->prof_ms[i] = 0; ctx->prof_bytes[i] = 0; ctx->prof_count[i] = 0; }
   rsvd::g_kernel_launches = 0;
   return RSVD_OK;
 }

@@ -76,8 +76,10 @@ struct OzakiCall {
   double* C; int64_t ldc; int Nout;
   double* P; unsigned* flags; unsigned epoch;    // stream-K partials / flags as GemmCall
   unsigned epoch2;                               // second column block (N > 64)
-  void* xscratch;                                // >= ozaki_x_bytes(K, N)
+  void* xscratch;                                // >= ozaki_x_bytes(K, min(N, 64))
+  void* xscratch2;                               // second column block (N > 64), same size
   int64_t M, K; int N; int grid;
+  cudaEvent_t mark, mark2;                       // nullable: both recorded after X slicing, before the pass kernel(s)
 };
 bool ozaki_supported(int Np);
 size_t ozaki_x_bytes(int64_t K, int Np);
@@ -140,6 +142,24 @@ cudaError_t launch_zero_cols(double* Y, int64_t ld, int64_t rows, int l, int npa
 cudaError_t launch_pca_eig(const double* d, int k, double m, void* eig, bool f32, cudaStream_t st);
 // Finite check of flags: flag |= 4 if any non-finite among v[0..n)
 cudaError_t launch_check_finite(const double* v, int64_t n, int* flag, cudaStream_t st);
+
+// ---- pivoted QR / interpolative decomposition (qrcp.cu), Alg. id / rid / rcur, reading R31
+// Column-contiguous W (column c = rows doubles at W + c*ld), `steps` Businger-Golub
+// pivots into perm; W is overwritten.  Z != null: Z (steps x ncols, ld ldz) = the
+// ID interpolation matrix (Z(:, P) = [I, S_kk^-1 S_12]); flag |= flag_bit if S_kk
+// is singular (rank < steps).  Cooperative launch, one CTA per SM.
+size_t qrcp_scratch_bytes(int64_t ncols, int steps, int num_sms);
+cudaError_t launch_qrcp(double* W, int64_t ld, int rows, int64_t ncols, int steps, int64_t* perm, double* Z,
+                        int64_t ldz, void* scratch, int* flag, int flag_bit, int num_sms, cudaStream_t st);
+cudaError_t launch_gather_cols(const double* A, int64_t lda, int64_t m, const int64_t* J, int k, double* C,
+                               int64_t ldc, cudaStream_t st);
+cudaError_t launch_gather_rows(const double* A, int64_t lda, int64_t n, const int64_t* I, int k, double* R,
+                               int64_t ldr, double* Rt, int64_t ldt, cudaStream_t st);
+size_t zq_partial_bytes(int k, int num_sms);
+cudaError_t launch_zq(const double* Z, int64_t ldz, const double* Q, int64_t ldq, int64_t n, int k, double* partial,
+                      double* W, int ldw, int num_sms, cudaStream_t st);
+cudaError_t launch_rtsolve(const double* W, int ldw, const double* S, int lds, int k, double* U, int64_t ldu,
+                           cudaStream_t st);
 
 // ---- IALM (ialm.cu), FP64, reading R17-R23 of DESIGN.md
 // M = A - S + Z * inv_mu ;  optional: norms of A (||A||_F^2 partials, max|A|)

@@ -93,25 +93,6 @@ __device__ __forceinline__ void digits_a4(const double (&v)[4], double scale, ui
   }
 }
 
-// X digits: N = rn(v 2^{8S-2-F}) (|N| < 2^{8S-2}) as S balanced signed bytes
-// d_u in [-128, 127] (d_0 in [-64, 64]), N = sum_u d_u 256^{S-1-u}
-template <int S>
-__device__ __forceinline__ void digits_x4(const double (&v)[4], double scale, uint32_t (&w)[S]) {
-#pragma unroll
-  for (int t = 0; t < S; ++t) w[t] = 0u;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    long long q = __double2ll_rn(v[e] * scale);
-#pragma unroll
-    for (int t = S - 1; t >= 1; --t) {
-      const int d = (int)(signed char)(q & 0xff);
-      q = (q - d) >> 8;                                   // exact
-      w[t] |= ((uint32_t)d & 0xffu) << (8 * e);
-    }
-    w[0] |= ((uint32_t)q & 0xffu) << (8 * e);
-  }
-}
-
 // f(a) = (a - c_j) * rs_j when c / rs are given (rpca centring / scaling, Alg. 6)
 __device__ __forceinline__ double fval(const double* A, int64_t lda, const double* c, const double* rs, int64_t r,
                                        int64_t cc) {
@@ -186,49 +167,68 @@ ozaki_slice_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64
 }
 
 // X (K x Np, ldx) -> xs[u][j][k] (u < S, j < Np, ld ldk bytes) and
-// xf[sb * Np + j] = 2^E(sb, j) for 1024-row super-blocks sb.
-// (1) column maxima per super-block: one thread per (16-row chunk, column),
-// combined with an integer atomicMax on the bit pattern (monotone for
-// non-negative doubles, order-independent => deterministic) into a zeroed
-// array; (2) one thread per (16-row chunk, column) slices.
-__global__ void __launch_bounds__(256)
-ozaki_xmax_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, double* __restrict__ smax) {
-  const int j = threadIdx.x % 32 + 32 * blockIdx.y, r = threadIdx.x / 32;
-  const int64_t kc = (int64_t)blockIdx.x * 8 + r;           // 16-row chunk
-  if (j >= Np || kc * 16 >= K) return;
-  double mx = 0.0;
-#pragma unroll
-  for (int k = 0; k < 16; ++k)
-    if (kc * 16 + k < K) mx = fmax(mx, fabs(X[(kc * 16 + k) * ldx + j]));
-  atomicMax(reinterpret_cast<unsigned long long*>(smax) + (kc * 16 / ET) * Np + j,
-            (unsigned long long)__double_as_longlong(mx));
-}
+// xf[sb * Np + j] = 2^E(sb, j) for 1024-row super-blocks sb, in one kernel:
+// a CTA (512 threads) owns one super-block x 8 columns, 16 values per thread
+// kept in registers; (1) column maxima by a fixed-order reduction, (2) the
+// digits into a shared tile [u][column][row] (row stride XT_LD bytes), (3)
+// the tile written out as 1024-byte rows (16-byte stores).  Rows >= K are
+// zero digits.
+constexpr int XT_COLS = 8, XT_THREADS = 512, XT_G = XT_THREADS / XT_COLS, XT_V = ET / XT_G, XT_LD = ET + 16;
+__host__ __device__ constexpr int xt_smem(int S) { return S * XT_COLS * XT_LD; }
 
 template <int S>
-__global__ void __launch_bounds__(256)
-ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, const double* __restrict__ cmax,
-                     int8_t* __restrict__ xs, int64_t ldk, double* __restrict__ xf) {
-  const int j = threadIdx.x % 32 + 32 * blockIdx.y, r = threadIdx.x / 32;
-  const int64_t kc = (int64_t)blockIdx.x * 8 + r;
-  if (j >= Np || kc * 16 >= ldk) return;
-  const int64_t sb = kc / (ET / 16);
-  const int E = block_exp(cmax[sb * Np + j]);
-  if (kc % (ET / 16) == 0) xf[sb * Np + j] = ldexp(1.0, E);
-  const double scale = ldexp(1.0, 8 * S - 2 - E);
-  uint32_t w[4][S];
+__global__ void __launch_bounds__(XT_THREADS)
+ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, int8_t* __restrict__ xs,
+                     int64_t ldk, double* __restrict__ xf) {
+  extern __shared__ __align__(16) unsigned char xt[];      // S x XT_COLS x XT_LD
+  __shared__ double red[XT_G][XT_COLS];
+  __shared__ double escale[XT_COLS];
+  const int tid = threadIdx.x, c = tid & (XT_COLS - 1), g = tid / XT_COLS;
+  const int64_t sb = blockIdx.x, k0 = sb * ET;
+  const int j = blockIdx.y * XT_COLS + c;
+  const bool jv = j < Np;
+  double v[XT_V];
+  double mx = 0.0;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    double v[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t kk = kc * 16 + 4 * q + e;
-      v[e] = kk < K ? X[kk * ldx + j] : 0.0;
-    }
-    digits_x4<S>(v, scale, w[q]);
+  for (int i = 0; i < XT_V; ++i) {
+    const int64_t k = k0 + g + XT_G * i;
+    v[i] = (jv && k < K) ? X[k * ldx + j] : 0.0;
+    mx = fmax(mx, fabs(v[i]));
   }
+  red[g][c] = mx;
+  __syncthreads();
+  if (g == 0) {
+    double m2 = red[0][c];
+    for (int r = 1; r < XT_G; ++r) m2 = fmax(m2, red[r][c]);
+    const int E = block_exp(m2);
+    if (jv) xf[sb * Np + j] = ldexp(1.0, E);
+    escale[c] = ldexp(1.0, 8 * S - 2 - E);
+  }
+  __syncthreads();
+  const double scale = escale[c];
 #pragma unroll
-  for (int t = 0; t < S; ++t)
-    *reinterpret_cast<uint4*>(xs + ((int64_t)t * Np + j) * ldk + kc * 16) = make_uint4(w[0][t], w[1][t], w[2][t], w[3][t]);
+  for (int i = 0; i < XT_V; ++i) {
+    const int r = g + XT_G * i;
+    long long q = __double2ll_rn(v[i] * scale);
+#pragma unroll
+    for (int t = S - 1; t >= 1; --t) {
+      const int d = (int)(signed char)(q & 0xff);
+      q = (q - d) >> 8;                                      // exact
+      xt[(t * XT_COLS + c) * XT_LD + r] = (unsigned char)d;
+    }
+    xt[c * XT_LD + r] = (unsigned char)q;
+  }
+  __syncthreads();
+  const int64_t kend = min((int64_t)ET, ldk - k0);          // multiple of 16
+  const int chunks = (int)(kend / 16);
+  for (int e = tid; e < S * XT_COLS * chunks; e += XT_THREADS) {
+    const int row = e / chunks, ch = e - row * chunks;
+    const int t = row / XT_COLS, cc = row - t * XT_COLS;
+    const int jj = blockIdx.y * XT_COLS + cc;
+    if (jj >= Np) continue;
+    *reinterpret_cast<uint4*>(xs + ((int64_t)t * Np + jj) * ldk + k0 + 16 * ch) =
+        *reinterpret_cast<const uint4*>(xt + row * XT_LD + 16 * ch);
+  }
 }
 
 // ---------------------------------------------------------------- pass kernel
@@ -500,7 +500,7 @@ size_t ozaki_a_bytes(int64_t m, int64_t n) {
 
 size_t ozaki_x_bytes(int64_t K, int Np) {
   const int64_t ldk = round_up(K, 16);
-  return (size_t)OZ_S * Np * ldk + 256 + (size_t)(round_up(ceil_div(K, oz::ET) * Np, 32) + ceil_div(K, 16) * Np) * sizeof(double) + 256;
+  return (size_t)OZ_S * Np * ldk + 256 + (size_t)round_up(ceil_div(K, oz::ET) * Np, 32) * sizeof(double) + 256;
 }
 
 cudaError_t ozaki_slice_a(const OzakiA& a, const double* A, int64_t lda, const double* c, const double* rs, int* flag,
@@ -523,42 +523,58 @@ OzakiA ozaki_layout_a(void* buf, int64_t m, int64_t n) {
   return a;
 }
 
+static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st);
 static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st);
 
+// X slicing of every column block first, then the pass kernel(s): c.mark (if
+// set) separates the two in time for the per-kernel profile.
 cudaError_t ozaki_pass(const OzakiCall& c, cudaStream_t st) {
   if (!ozaki_supported(c.N) || c.M <= 0 || c.K <= 0) return cudaErrorInvalidValue;
-  if (c.N <= 64) return ozaki_pass_cols(c, st);
-  OzakiCall h = c;                                   // columns [0, 64): B, C with their own leading dimensions
-  h.N = 64; h.Nout = c.Nout < 64 ? c.Nout : 64;
-  cudaError_t e = ozaki_pass_cols(h, st);
+  OzakiCall h0 = c, h1 = c;
+  const bool two = c.N > 64;
+  if (two) {
+    h0.N = 64; h0.Nout = c.Nout < 64 ? c.Nout : 64;   // columns [0, 64): B, C with their own leading dimensions
+    h1.B = c.B + 64; h1.C = c.C + 64; h1.N = c.N - 64; h1.Nout = c.Nout - 64; h1.epoch = c.epoch2;
+    h1.xscratch = c.xscratch2;
+    if (!c.xscratch2) return cudaErrorInvalidValue;
+  }
+  cudaError_t e = ozaki_slice_cols(h0, st);
+  if (e == cudaSuccess && two) e = ozaki_slice_cols(h1, st);
   if (e != cudaSuccess) return e;
-  h = c;                                             // columns [64, N)
-  h.B = c.B + 64; h.C = c.C + 64; h.N = c.N - 64; h.Nout = c.Nout - 64; h.epoch = c.epoch2;
-  if (h.Nout <= 0) return cudaSuccess;
-  return ozaki_pass_cols(h, st);
+  if (c.mark) cudaEventRecord(c.mark, st);
+  if (c.mark2) cudaEventRecord(c.mark2, st);
+  e = ozaki_pass_cols(h0, st);
+  if (e == cudaSuccess && two && h1.Nout > 0) e = ozaki_pass_cols(h1, st);
+  return e;
+}
+
+static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st) {
+  using namespace oz;
+  const int N = c.N;
+  const int64_t ldk = round_up(c.K, 16);
+  int8_t* xs = reinterpret_cast<int8_t*>(c.xscratch);
+  double* xf = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(ozaki_slice_x_kernel<OZ_S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               xt_smem(OZ_S));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const dim3 gs((unsigned)ceil_div(ldk, ET), (unsigned)ceil_div(N, XT_COLS));
+  ozaki_slice_x_kernel<OZ_S><<<gs, XT_THREADS, xt_smem(OZ_S), st>>>(c.B, c.ldb, c.K, N, xs, ldk, xf);
+  ++g_kernel_launches;
+  return cudaGetLastError();
 }
 
 static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
   using namespace oz;
   const OzakiA& a = *c.a;
   const int N = c.N;
-  // 1) X slices
+  // X slices (ozaki_slice_cols) are in c.xscratch
   const int64_t ldk = round_up(c.K, 16);
   int8_t* xs = reinterpret_cast<int8_t*>(c.xscratch);
   double* xf = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
-  const int64_t KB = ceil_div(c.K, BKO);
-  double* cmax = xf + round_up(ceil_div(c.K, ET) * N, 32);
-  {
-    cudaMemsetAsync(cmax, 0, (size_t)ceil_div(c.K, ET) * N * sizeof(double), st);
-    const dim3 gx((unsigned)ceil_div(ceil_div(c.K, 16), 8), (unsigned)ceil_div(N, 32));
-    ozaki_xmax_kernel<<<gx, 256, 0, st>>>(c.B, c.ldb, c.K, N, cmax);
-    const dim3 gs((unsigned)ceil_div(ldk / 16, 8), (unsigned)ceil_div(N, 32));
-    ozaki_slice_x_kernel<OZ_S><<<gs, 256, 0, st>>>(c.B, c.ldb, c.K, N, cmax, xs, ldk, xf);
-#ifdef OZ_DEBUG
-    { cudaError_t ee = cudaGetLastError(); if (ee) printf("x slicing: %s (N %d K %lld gx %u %u gs %u %u)\n", cudaGetErrorString(ee), N, (long long)c.K, gx.x, gx.y, gs.x, gs.y); }
-#endif
-    g_kernel_launches += 2;
-  }
   // 2) tensor maps: A slices as (cols = n, rows = m, S); X slices as (cols = K, rows = S * N)
   CUtensorMap mA, mX;
   if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, OZ_S, c.trans)) return cudaErrorInvalidValue;

@@ -249,6 +249,61 @@ def test_rsvd_power_param_rejected(rb):
         rb.rsvd(A, 5, power=2)
 
 
+# ----------------------------------------------------------------------------- rid / rcur (§8(f) f3)
+@pytest.mark.parametrize("m,n,k", [(3000, 500, 20), (2049, 777, 40)])
+def test_rid_parity(rb, m, n, k):
+    """Alg. rid with Alg. id on B, reading R31:
+    the pivot order J equals the oracle's (distinct column norms), C = A(:, J)
+    bit-exact, Z within 1e-9 of the oracle's, Z(:, J) = I, and the ID error
+    matches the oracle's."""
+    A = _decay_matrix(m, n, seed=m + k, noise=1e-6)
+    An = A.numpy()
+    r = rb.rid(A.cuda(), k, p=10, q=2, seed=7)
+    o = oracle.oracle_rid(An, k, p=10, q=2, seed=7)
+    J = r["J"].cpu().numpy()
+    assert list(J) == list(o["J"])
+    C, Z = _np(r["C"]), _np(r["Z"])
+    assert np.array_equal(C, An[:, J])
+    assert np.abs(Z - o["Z"]).max() < 1e-9 * max(1.0, np.abs(o["Z"]).max())
+    assert np.abs(Z[:, J] - np.eye(k)).max() == 0.0
+    e_gpu = np.linalg.norm(An - C @ Z) / np.linalg.norm(An)
+    e_orc = np.linalg.norm(An - o["C"] @ o["Z"]) / np.linalg.norm(An)
+    assert e_gpu <= 1.0001 * e_orc + 1e-13
+
+
+def test_rid_exact_rank_and_rank_deficiency(rb):
+    """Exact rank k: C Z = A to rounding (the ID is exact); asking for more
+    columns than the rank is reported as RSVD_ENUMERIC (S(1:k,1:k) singular)."""
+    g = torch.Generator().manual_seed(5)
+    A = (torch.randn(1500, 12, generator=g, dtype=torch.float64) @
+         torch.randn(12, 400, generator=g, dtype=torch.float64))
+    r = rb.rid(A.cuda(), 12, p=8, q=1, seed=2)
+    C, Z = _np(r["C"]), _np(r["Z"])
+    An = A.numpy()
+    assert np.abs(C @ Z - An).max() < 1e-11 * np.abs(An).max()
+    with pytest.raises(rb.RsvdError):
+        rb.rid(A.cuda(), 14, p=8, q=1, seed=2)
+
+
+@pytest.mark.parametrize("m,n,k", [(2500, 400, 16), (4000, 1000, 30)])
+def test_rcur_parity(rb, m, n, k):
+    """Alg. rcur: J and I equal the oracle's, C = A(:, J) and
+    R = A(I, :) bit-exact, U within 1e-8 relative, and the CUR error matches
+    the oracle's."""
+    A = _decay_matrix(m, n, seed=3 * m + k, noise=1e-6)
+    An = A.numpy()
+    r = rb.rcur(A.cuda(), k, p=10, q=2, seed=9)
+    o = oracle.oracle_rcur(An, k, p=10, q=2, seed=9)
+    J, I = r["J"].cpu().numpy(), r["I"].cpu().numpy()
+    assert list(J) == list(o["J"]) and list(I) == list(o["I"])
+    C, U, R = _np(r["C"]), _np(r["U"]), _np(r["R"])
+    assert np.array_equal(C, An[:, J]) and np.array_equal(R, An[I, :])
+    assert np.abs(U - o["U"]).max() < 1e-8 * np.abs(o["U"]).max()
+    e_gpu = np.linalg.norm(An - C @ U @ R) / np.linalg.norm(An)
+    e_orc = np.linalg.norm(An - o["C"] @ o["U"] @ o["R"]) / np.linalg.norm(An)
+    assert e_gpu <= 1.0001 * e_orc + 1e-12
+
+
 # ----------------------------------------------------------------------------- rrpca
 def test_rrpca_parity_small(rb):
     A, L0, S0 = synthetic.sparse_plus_lowrank(4000, 300, rank=5, frac=0.05, seed=12)

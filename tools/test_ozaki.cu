@@ -38,13 +38,13 @@ int main(int argc, char** argv) {
       if (mode == 2) v = (i == j) ? 1.0 / 128 : 0.0;
       A[i * n + j] = v;
     }
-  double *dA, *dC, *dB, *dP; int* flag; unsigned* flags; void *abuf, *xbuf;
+  double *dA, *dC, *dB, *dP; int* flag; unsigned* flags; void *abuf, *xbuf, *xbuf2;
   CK(cudaMalloc(&dA, m * n * 8)); CK(cudaMemcpy(dA, A.data(), m * n * 8, cudaMemcpyHostToDevice));
   CK(cudaMalloc(&abuf, ozaki_a_bytes(m, n))); CK(cudaMalloc(&flag, 64)); CK(cudaMemset(flag, 0, 64));
   CK(cudaMalloc(&flags, 4096 * 4)); CK(cudaMemset(flags, 0, 4096 * 4));
   const int64_t big = m > n ? m : n;
   CK(cudaMalloc(&dB, big * 128 * 8)); CK(cudaMalloc(&dC, big * 128 * 8)); CK(cudaMalloc(&dP, (size_t)nsm * 128 * 64 * 8));
-  CK(cudaMalloc(&xbuf, ozaki_x_bytes(big, 64)));
+  CK(cudaMalloc(&xbuf, ozaki_x_bytes(big, 64))); CK(cudaMalloc(&xbuf2, ozaki_x_bytes(big, 64)));
   OzakiA oa = ozaki_layout_a(abuf, m, n);
   CK(ozaki_slice_a(oa, dA, n, nullptr, nullptr, flag, 0));
   CK(cudaDeviceSynchronize());
@@ -81,7 +81,7 @@ int main(int argc, char** argv) {
       CK(cudaMemcpy(dB, B.data(), K * N * 8, cudaMemcpyHostToDevice));
       OzakiCall c{};
       c.a = &oa; c.trans = trans; c.B = dB; c.ldb = N; c.C = dC; c.ldc = N; c.Nout = N; c.P = dP; c.flags = flags;
-      c.epoch = ++epoch; c.epoch2 = ++epoch; c.xscratch = xbuf; c.M = M; c.K = K; c.N = N; c.grid = nsm;
+      c.epoch = ++epoch; c.epoch2 = ++epoch; c.xscratch = xbuf; c.xscratch2 = xbuf2; c.M = M; c.K = K; c.N = N; c.grid = nsm;
       { cudaError_t e0 = ozaki_pass(c, 0); cudaError_t e1 = cudaDeviceSynchronize(); if (e0 || e1) { printf("ozaki_pass N=%d trans=%d: ret %s sync %s\n", N, trans, cudaGetErrorString(e0), cudaGetErrorString(e1)); continue; } }
       CK(cudaDeviceSynchronize());
       CK(cudaMemcpy(C.data(), dC, M * N * 8, cudaMemcpyDeviceToHost));
