@@ -167,7 +167,8 @@ rsvd_status rsvd_rpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* pr
  *           0: adaptive target rank -- k = 2 at step (1), then step (7)
  *           predict_rank (Remark 1): l = max(1, #{sigma_i > 1/mu}),
  *           k <- l + 1 if l < k else min(l + ceil(0.05 min(m, n)), min(m, n)),
- *           capped at min(min(m, n), 120 - p) (no deterministic-SVD switch, R30)
+ *           capped at min(min(m, n), 120 - p); the deterministic SVD of
+ *           Remark 2 is used while k > min(m, n)/4 if min(m, n) <= 120 (R30)
  * FP64 only.  L, S: DEVICE m_local x n (ld == n), caller-owned; A contiguous.
  *   iters, final_residual: HOST out-params (nullable)
  *   trace: HOST, nullable, 4*maxiter doubles per iteration: (residual, l, mu,
@@ -180,6 +181,12 @@ typedef struct {
   int32_t k, p, q;
   int32_t sdist;
   uint64_t seed;
+  int32_t rand;   /* 1 (default): randomized SVD in step (6); 0: the deterministic
+                     truncated SVD (P:1743-1744 rand = FALSE), computed as rsvd with
+                     l = min(m, n), q = 0 (Q spans the whole column space, so the
+                     SVD of B is the exact SVD); needs min(m, n) <= 120.  With k = 0
+                     the same switch happens whenever the predicted k > min(m, n)/4
+                     (Remark 2). */
 } rsvd_rrpca_params;
 void rsvd_rrpca_params_default(rsvd_rrpca_params* prm);
 rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_rrpca_params* prm,

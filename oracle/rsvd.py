@@ -156,7 +156,7 @@ def predict_rank(d, mu_inv, k, minmn):
 
 
 def oracle_rrpca(A, lam=None, maxiter=100, tol=1e-7, k=20, p=10, q=2,
-                 sdist="normal", seed=0, trace=False, kmax=None, det_switch=True):
+                 sdist="normal", seed=0, trace=False, kmax=None, det_switch=True, rand=True):
     """Alg. 7 rrpca, the inexact ALM loop, readings R17-R23, R30.
 
     lambda = max(m,n)^-1/2;  ||A||_2 = sigma_1 of rsvd(A, 1, p, q,
@@ -173,7 +173,8 @@ def oracle_rrpca(A, lam=None, maxiter=100, tol=1e-7, k=20, p=10, q=2,
       until ||A - L - S||_F / ||A||_F < tol  (R21; evaluated after step 11)
     Adaptive mode: predicted k is capped at kmax (default min(m, n)); with
     det_switch the truncated SVD of step (6) is the deterministic one (numpy
-    SVD) whenever k > min(m, n)/4 (Remark 2).
+    SVD) whenever k > min(m, n)/4 (Remark 2).  rand=False: the
+    deterministic truncated SVD in every iteration.
     Returns dict(L, S, iters, residual, trace=[(res, l, mu, k)...]).
     """
     A = np.asarray(A, dtype=np.float64)
@@ -199,7 +200,7 @@ def oracle_rrpca(A, lam=None, maxiter=100, tol=1e-7, k=20, p=10, q=2,
     it = 0
     for it in range(1, maxiter + 1):
         M = A - S + Z / mu
-        if adaptive and det_switch and k > minmn / 4:
+        if (not rand) or (adaptive and det_switch and k > minmn / 4):
             uu, dd, vt = np.linalg.svd(M, full_matrices=False)
             r = dict(u=uu[:, :k], d=dd[:k], v=vt[:k].T)
         else:

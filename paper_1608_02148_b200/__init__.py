@@ -55,7 +55,7 @@ POWER = {"subspace": 0, "direct": 1}
 class RrpcaParams(ctypes.Structure):
     _fields_ = [("lam", ctypes.c_double), ("tol", ctypes.c_double), ("maxiter", ctypes.c_int32),
                 ("k", ctypes.c_int32), ("p", ctypes.c_int32), ("q", ctypes.c_int32), ("sdist", ctypes.c_int32),
-                ("seed", ctypes.c_uint64)]
+                ("seed", ctypes.c_uint64), ("rand", ctypes.c_int32)]
 
 
 _lib = None
@@ -328,11 +328,12 @@ def rpca(A, k, center=True, scale=False, retx=True, p=10, q=2, sdist="normal", s
 
 
 def rrpca(A, lam=None, maxiter=50, tol=1e-5, p=10, q=2, k=20, sdist="normal", seed=0, trace=False, ctx=None,
-          m_global=None, row_offset=0):
+          m_global=None, row_offset=0, rand=True):
     """Randomized robust PCA by inexact ALM (Alg. 7; interface P:1736).
 
     k > 0 fixes the target rank; k = 0 selects the adaptive target rank of
     Alg. 7 steps (1) and (7) (k = 2, then predict_rank; R30).
+    rand=False: the deterministic truncated SVD in step (6).
     trace: per iteration (residual, l, mu, k)."""
     ctx = ctx or default_context(A.device)
     mat = _matrix(A, m_global, row_offset)
@@ -342,6 +343,7 @@ def rrpca(A, lam=None, maxiter=50, tol=1e-5, p=10, q=2, k=20, sdist="normal", se
     prm.tol, prm.maxiter, prm.k, prm.p, prm.q = float(tol), int(maxiter), int(k), int(p), int(q)
     prm.sdist = SDIST[sdist] if isinstance(sdist, str) else int(sdist)
     prm.seed = int(seed)
+    prm.rand = 1 if rand else 0
     L = torch.empty_like(A)
     S = torch.empty_like(A)
     it = ctypes.c_int32()

@@ -22,6 +22,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <functional>
 #include <cmath>
 #include <string>
@@ -63,6 +64,7 @@ struct rsvd_ctx {
   int nranks = 1, rank = 0;
   // profiling
   int prof = 0;                   // 0 off, 1 every kind, 2 the pass kernels only (kinds 0, 1, 6)
+  bool debug = getenv("RSVD_DEBUG") != nullptr;
   std::vector<ProfRec> pending;
   std::vector<cudaEvent_t> pool;
   double prof_ms[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -364,6 +366,7 @@ rsvd_status tsqr_local(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, double* 
     while (Mc > cap) {
       int64_t P = ceil_div(Mc, cap);
       if (Mc / P < l) P = Mc / l;
+      if (P * l >= Mc) return fail(ctx, RSVD_EUNSUPPORTED, "TSQR cannot reduce %lld rows at l = %d", (long long)Mc, l);
       need += (size_t)P * l * l * 8 + 256;
       Mc = P * l;
     }
@@ -375,6 +378,7 @@ rsvd_status tsqr_local(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, double* 
   while (Mc > cap) {
     int64_t P = ceil_div(Mc, cap);
     if (Mc / P < l) P = Mc / l;
+    if (P * l >= Mc) return fail(ctx, RSVD_EUNSUPPORTED, "TSQR cannot reduce %lld rows at l = %d", (long long)Mc, l);
     double* stack = (double*)wp;
     wp += align256((size_t)P * l * l * 8);
     CK(launch_hqr_leaves(cur, ld, Mc, l, P, stack, ctx->stream));
@@ -711,6 +715,7 @@ void rsvd_rrpca_params_default(rsvd_rrpca_params* prm) {
   memset(prm, 0, sizeof *prm);
   prm->lambda = 0.0; prm->tol = 1e-5; prm->maxiter = 50; prm->k = 20; prm->p = 10; prm->q = 2;
   prm->sdist = RSVD_NORMAL;
+  prm->rand = 1;
 }
 
 rsvd_status rsvd_run(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm_in, void* u, int64_t ldu,
@@ -970,7 +975,8 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
   const int64_t minmn = std::min(mg, n);
   // library envelope: l = k + p <= kMaxL (the deterministic-SVD switch of
   // Remark 2, is not part of this library; R30)
-  const int kcap = (int)std::min<int64_t>(minmn, kMaxL - rp.p);
+  // (the deterministic path has l = min(m, n) <= kMaxL, so k may reach min(m, n) there)
+  const int kcap = (int)(minmn <= kMaxL ? minmn : std::min<int64_t>(minmn, kMaxL - rp.p));
   if (kcap < 1) return fail(ctx, RSVD_EUNSUPPORTED, "p = %d leaves no room for k under l <= %d", rp.p, kMaxL);
   if (!adaptive && prm->k > kcap)
     return fail(ctx, RSVD_EUNSUPPORTED, "k = %d exceeds min(m, n) or l = k + p <= %d", prm->k, kMaxL);
@@ -1037,6 +1043,15 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
     rsvd_params ri = rp;
     ri.k = ri.nu = ri.nv = k;
     ri.stream = (uint64_t)it;                               // fresh Omega per iteration (R23)
+    // deterministic SVD (rand = FALSE, or Remark 2's switch for k > min(m, n)/4):
+    // l = min(m, n), q = 0 -> Q Q^T M = M, the SVD of B is the exact SVD
+    const bool det = !prm->rand || (adaptive && 4 * (int64_t)k > minmn);
+    if (det) {
+      if (minmn > kMaxL)
+        return fail(ctx, RSVD_EUNSUPPORTED, "deterministic SVD in rrpca needs min(m, n) <= %d", kMaxL);
+      ri.p = (int)(minmn - k);
+      ri.q = 0;
+    }
     CKS(rsvd_device(ctx, &Mdesc, &ri, U, k, dd, V, k));      // step (6)
     CK(launch_ialm_threshold(dd, k, 1.0 / mu, dl, scal + 2, ctx->stream));   // steps (7)-(8)
     const double mu_next = std::min(1.5 * mu, 1e7 * mu0);  // step (12), R20
@@ -1049,6 +1064,9 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
     res = sqrt(h[128]) / normF;
     const int nl = (int)h[130];
     kused = k;
+    if (ctx->debug)
+      fprintf(stderr, "rrpca it %d k %d l %d det %d res %.3e mu %.3e t %.3f ms\n", it, k, nl, (int)det, res, mu,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count());
     if (trace) {
       double* tr = trace + 4 * (it - 1);
       tr[0] = res; tr[1] = nl; tr[2] = mu; tr[3] = k;

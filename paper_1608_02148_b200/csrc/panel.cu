@@ -308,8 +308,10 @@ cudaError_t launch_small_matmul(const double* A, const double* B, double* C, int
 // ------------------------------------------------------------------ Householder leaves
 constexpr int HQR_THREADS = 512;
 
+// rows of one leaf held in shared memory: b l + l (tau) + 32 (reduction / sign
+// bits) doubles; at l = 120 this is 240 = 2 l, so two R factors always combine
 int leaf_rows_cap(int l) {
-  const int64_t avail = (SMEM_OPTIN - 1024) / (int64_t)sizeof(double) - 2 * l - 32;
+  const int64_t avail = SMEM_OPTIN / (int64_t)sizeof(double) - l - 32;
   return (int)(avail / l);
 }
 
@@ -323,8 +325,8 @@ __global__ void __launch_bounds__(HQR_THREADS) hqr_leaves_kernel(double* __restr
   const int64_t r0 = leaf * rb + (leaf < rem ? leaf : rem);
   double* Ys = sm;                 // column-major, ld = b
   double* tau = Ys + (int64_t)l * b;
-  double* w = tau + l;
-  double* red = w + l;             // 32
+  double* red = tau + l;           // 32 (block sums; then the R-diagonal sign bits)
+  unsigned* sgn = reinterpret_cast<unsigned*>(red);
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
 
   for (int64_t e = tid; e < (int64_t)b * l; e += nt) {
@@ -366,13 +368,18 @@ __global__ void __launch_bounds__(HQR_THREADS) hqr_leaves_kernel(double* __restr
     }
   }
 
-  // ---- R (upper l x l) with diag >= 0 to the stack; remember the signs in w
-  for (int j = tid; j < l; j += nt) w[j] = (Ys[(int64_t)j * b + j] < 0.0) ? -1.0 : 1.0;
+  // ---- R (upper l x l) with diag >= 0 to the stack; remember the signs as bits
   __syncthreads();
+  if (tid < 8) sgn[tid] = 0u;
+  __syncthreads();
+  for (int j = tid; j < l; j += nt)
+    if (Ys[(int64_t)j * b + j] < 0.0) atomicOr(&sgn[j >> 5], 1u << (j & 31));
+  __syncthreads();
+  auto w = [&](int c) { return ((sgn[c >> 5] >> (c & 31)) & 1u) ? -1.0 : 1.0; };
   double* Rl = Rstack + leaf * (int64_t)l * l;
   for (int e = tid; e < l * l; e += nt) {
     const int i = e / l, c = e % l;
-    Rl[e] = (c >= i) ? w[i] * Ys[(int64_t)c * b + i] : 0.0;
+    Rl[e] = (c >= i) ? w(i) * Ys[(int64_t)c * b + i] : 0.0;
   }
   __syncthreads();
 
@@ -399,15 +406,15 @@ __global__ void __launch_bounds__(HQR_THREADS) hqr_leaves_kernel(double* __restr
   }
   for (int64_t e = tid; e < (int64_t)b * l; e += nt) {
     const int r = (int)(e / l), c = (int)(e % l);
-    Y[(r0 + r) * ldy + c] = w[c] * Ys[(int64_t)c * b + r];
+    Y[(r0 + r) * ldy + c] = w(c) * Ys[(int64_t)c * b + r];
   }
 }
 
 cudaError_t launch_hqr_leaves(double* Y, int64_t ldy, int64_t M, int l, int64_t nleaves, double* Rstack,
                               cudaStream_t st) {
   const int64_t bmax = ceil_div(M, nleaves);
-  const size_t smem = ((size_t)bmax * l + 2 * l + 32) * sizeof(double);
-  if (smem > (size_t)SMEM_OPTIN - 1024 || bmax < l) return cudaErrorInvalidValue;
+  const size_t smem = ((size_t)bmax * l + l + 32) * sizeof(double);
+  if (smem > (size_t)SMEM_OPTIN || bmax < l) return cudaErrorInvalidValue;
   cudaError_t e = set_smem((const void*)hqr_leaves_kernel, smem);
   if (e != cudaSuccess) return e;
   hqr_leaves_kernel<<<(unsigned)nleaves, HQR_THREADS, smem, st>>>(Y, ldy, M, l, nleaves, Rstack); ++g_kernel_launches;

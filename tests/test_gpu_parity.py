@@ -249,6 +249,26 @@ def test_rsvd_power_param_rejected(rb):
         rb.rsvd(A, 5, power=2)
 
 
+@pytest.mark.timeout(300)
+def test_rsvd_robust_tsqr_at_l120(rb):
+    """CholeskyQR breakdown at the largest sketch width (l = 120): the robust
+    Householder TSQR must reduce a 240-row stack of two R factors in one leaf
+    (regression: it once looped forever there).  Exact rank 50 < l, so the
+    top 50 singular values match the oracle's and U stays orthonormal."""
+    g = torch.Generator().manual_seed(8)
+    A = (torch.randn(3000, 50, generator=g, dtype=torch.float64) *
+         torch.exp(-torch.arange(50, dtype=torch.float64) / 10)) @ torch.randn(50, 500, generator=g, dtype=torch.float64)
+    An = A.numpy()
+    ctx = rb.Context(0)
+    r = rb.rsvd(A.cuda(), 100, p=20, q=1, seed=3, ctx=ctx)
+    assert ctx.stats()["robust_rerun"]
+    o = oracle.oracle_rsvd(An, 100, p=20, q=1, seed=3)
+    d = _np(r.d)
+    assert np.max(np.abs(d[:50] - o["d"][:50]) / o["d"][:50]) < 1e-10
+    u = _np(r.u)[:, :50]
+    assert np.abs(u.T @ u - np.eye(50)).max() < 1e-12
+
+
 # ----------------------------------------------------------------------------- rid / rcur (§8(f) f3)
 @pytest.mark.parametrize("m,n,k", [(3000, 500, 20), (2049, 777, 40)])
 def test_rid_parity(rb, m, n, k):
@@ -345,6 +365,30 @@ def test_rrpca_adaptive_and_large_rank_parity(rb, m, n, rank, k):
     assert np.linalg.norm(L - L0n) / np.linalg.norm(L0n) < 1e-6
     assert ((np.abs(S) > 1e-6) == (S0n != 0)).mean() > 0.999
     assert out["residual"] < 1e-7
+
+
+@pytest.mark.parametrize("rank,k,rand", [(5, 10, False), (32, 0, True)])
+def test_rrpca_deterministic_svd(rb, rank, k, rand):
+    """rand = FALSE and Remark 2's switch (adaptive k >
+    min(m, n)/4 -> deterministic SVD): the GPU's deterministic SVD (rsvd with
+    l = min(m, n), q = 0) against the oracle's numpy SVD, same rank trajectory,
+    L and S within 1e-10 when the iteration counts agree; the rank-5 case also
+    recovers the planted L0 (rank 32 of 120 is beyond exact recovery)."""
+    A, L0, S0 = synthetic.sparse_plus_lowrank(3000, 120, rank=rank, frac=0.05, seed=rank + 100)
+    An = A.numpy()
+    out = rb.rrpca(A.cuda(), k=k, p=10, q=2, tol=1e-7, maxiter=100, seed=4, trace=True, rand=rand)
+    o = oracle.oracle_rrpca(An, k=k, p=10, q=2, tol=1e-7, maxiter=100, seed=4, rand=rand)
+    if k == 0:
+        assert any(t[3] > 120 / 4 for t in o["trace"])               # the switch is exercised
+    nt = min(out["iters"], o["iters"])
+    assert [(t[1], t[3]) for t in out["trace"][:nt]] == [(t[1], t[3]) for t in o["trace"][:nt]]
+    assert abs(out["iters"] - o["iters"]) <= 1
+    L, S = _np(out["L"]), _np(out["S"])
+    if out["iters"] == o["iters"]:
+        assert np.linalg.norm(L - o["L"]) / np.linalg.norm(o["L"]) < 1e-10
+        assert np.linalg.norm(S - o["S"]) / np.linalg.norm(o["S"]) < 1e-10
+    if rank == 5:
+        assert np.linalg.norm(L - L0.numpy()) / np.linalg.norm(L0.numpy()) < 1e-6
 
 
 # ----------------------------------------------------------------------------- full-size configs 3, 5

@@ -70,7 +70,7 @@ int main(int argc, char** argv) {
   }
   unsigned epoch = 0;
   for (int trans = 0; trans < 2; ++trans)
-    for (int N : {16, 32, 64, 96, 128}) {
+    for (int N : {16, 32, 48, 64, 80, 96, 112, 128}) {
       if (argc > 5 && N != atoi(argv[5])) continue;
       const int64_t M = trans ? n : m, K = trans ? m : n;
       std::vector<double> B(K * N), C(M * N, -7.0);
