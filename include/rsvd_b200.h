@@ -92,8 +92,9 @@ typedef struct {
  *   power   power scheme between the sketch and the final QR: 0 = subspace
  *           iterations with QR (Alg. 2, default), 1 = the direct
  *           scheme Y = (A A^T)^q A Omega without normalisation (Alg. 1,
- *           P:343-362; "not recommended in practice"); RSVD_EINVAL
- *           otherwise */
+ *           P:343-362; "not recommended in practice"), 2 = normalized
+ *           power iterations with pivoted LU (Alg. 3; single GPU);
+ *           RSVD_EINVAL otherwise */
 typedef struct {
   int32_t k, nu, nv, p, q;
   int32_t sdist;          /* rsvd_sdist */

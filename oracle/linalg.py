@@ -9,6 +9,9 @@
   economic SVD" (reading R7).
 * ``soft_threshold``: shrink(x, tau) = sign(x) max(|x| - tau, 0)
   (Alg. 7 steps (8) and (10)).
+* ``lu_pp``: LU with partial pivoting, "[L, ~] = lu(Y)  pivoted LU" (Alg. 3
+  norm_iterations steps (2)-(3)): returns the permuted unit lower
+  factor L (Y = L U with L = P^T L_unit).
 * ``qrcp``: QR with column pivoting, "[~, S, P] = qr(A)  pivoted QR
   decomposition" (Alg. id step (1); "stopped after k iterations to
   obtain only the k dominant pivots"): Businger-Golub largest
@@ -165,3 +168,34 @@ def qrcp(A, steps=None):
         R[j + 1:, j] = 0.0
         R[j, j] = alpha
     return R, P
+
+
+def lu_pp(Y):
+    """Gaussian elimination with partial pivoting on Y (m x l, m >= l).
+
+    Step j: the unpivoted row with the largest |y_ij| (first on ties) is the
+    pivot p_j; every other unpivoted row i gets l_ij = y_ij / y_pj and
+    y_i,c -= l_ij y_pj,c for c > j.  Returns L (m x l) with L[p_j, j] = 1,
+    L[p_j, c] = 0 for c > j and the multipliers elsewhere (so Y = L U with U
+    the pivot rows' upper triangle; L is unit lower triangular up to the row
+    permutation), and the pivot rows.  A zero pivot column is skipped
+    (multipliers 0)."""
+    W = np.array(Y, dtype=np.float64)
+    m, l = W.shape
+    done = np.zeros(m, dtype=bool)
+    piv = np.zeros(l, dtype=np.int64)
+    L = np.zeros((m, l))
+    for j in range(l):
+        cand = np.where(~done)[0]
+        p = cand[int(np.argmax(np.abs(W[cand, j])))]
+        piv[j] = p
+        done[p] = True
+        L[p, j] = 1.0
+        u = W[p, j]
+        rest = np.where(~done)[0]
+        if u == 0.0:
+            continue
+        lij = W[rest, j] / u
+        L[rest, j] = lij
+        W[np.ix_(rest, np.arange(j + 1, l))] -= np.outer(lij, W[p, j + 1:])
+    return L, piv

@@ -22,7 +22,7 @@ the QR and SVD are written out in oracle/linalg.py.
 """
 import numpy as np
 
-from .linalg import hqr, jacobi_svd_bt, qrcp, soft_threshold
+from .linalg import hqr, jacobi_svd_bt, lu_pp, qrcp, soft_threshold
 from .philox import omega
 
 
@@ -75,9 +75,9 @@ def _prepare(A, center=False, scale=False):
 
 def oracle_rqb(A, l, q=2, sdist="normal", seed=0, stream=0, omega_dtype=np.float64,
                power="subspace"):
-    """Alg. 4 rqb with Alg. 2 sub_iterations (power="subspace") or the direct
-    power scheme of Alg. 1 (power="direct"): returns Q (m x l),
-    B^T (n x l)."""
+    """Alg. 4 rqb with Alg. 2 sub_iterations (power="subspace"), the direct
+    power scheme of Alg. 1 (power="direct") or the normalized power
+    iterations of Alg. 3 (power="lu"): returns Q (m x l), B^T (n x l)."""
     X = np.asarray(A, dtype=np.float64)
     m, n = X.shape
     Om = omega(n, l, sdist, seed, stream, dtype=omega_dtype)   # step (2)
@@ -86,6 +86,11 @@ def oracle_rqb(A, l, q=2, sdist="normal", seed=0, stream=0, omega_dtype=np.float
         if power == "direct":                                   # Alg. 1
             Y = X.T @ Y                                         #   (2)
             Y = X @ Y                                           #   (3)
+            continue
+        if power == "lu":                                       # Alg. 3
+            Lq, _p = lu_pp(Y)                                   #   (2) [L,~] = lu(Y)
+            Lz, _p = lu_pp(X.T @ Lq)                            #   (3) [L,~] = lu(A^T L)
+            Y = X @ Lz                                          #   (4)
             continue
         Q, _r = hqr(Y)                                          # Alg. 2 (2)
         Qz, _r = hqr(X.T @ Q)                                   #   (3)

@@ -49,7 +49,7 @@ class Params(ctypes.Structure):
                 ("stream", ctypes.c_uint64), ("center", ctypes.c_int32), ("scale", ctypes.c_int32),
                 ("power", ctypes.c_int32)]
 
-POWER = {"subspace": 0, "direct": 1}
+POWER = {"subspace": 0, "direct": 1, "lu": 2}
 
 
 class RrpcaParams(ctypes.Structure):
@@ -228,7 +228,8 @@ def rsvd(A, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0, stream=0, ct
          m_global=None, row_offset=0, out=None, power="subspace"):
     """Randomized SVD (Alg. 5; interface P:708).
 
-    power: "subspace" (Alg. 2, QR between passes) or "direct" (Alg. 1).
+    power: "subspace" (Alg. 2, QR between passes), "direct" (Alg. 1) or "lu"
+    (Alg. 3, pivoted-LU normalisation).
     A: CUDA tensor (m x n, float64 or float32, row-major).  Returns (d, u, v)
     with d (k,), u (m x nu) and v (n x nv, not transposed).  In distributed
     mode (ctx.init_comm) A holds this rank's rows and u this rank's rows.

@@ -36,7 +36,8 @@ using namespace rsvd;
 
 namespace {
 
-constexpr int kFlagCholBreak = 1, kFlagJacobiCap = 2, kFlagNonFinite = 4, kFlagRankDef = 8;
+constexpr int kFlagCholBreak = 1, kFlagJacobiCap = 2, kFlagNonFinite = 4, kFlagRankDef = 8,
+              kFlagLuZero = 16;   // informational: an exactly zero LU pivot (multipliers set to 0)
 constexpr int kMaxL = 120;       // Jacobi + leaf QR shared-memory envelope
 
 struct ProfRec { int kind; double bytes; cudaEvent_t a, b; };
@@ -473,7 +474,8 @@ rsvd_status validate(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm
   if (prm->p < 0 || prm->q < 0) return fail(ctx, RSVD_EINVAL, "p and q must be >= 0");
   if (prm->sdist < 0 || prm->sdist > 2) return fail(ctx, RSVD_EINVAL, "sdist must be normal, unif or rademacher");
   if (prm->nu < 0 || prm->nv < 0) return fail(ctx, RSVD_EINVAL, "nu, nv must be >= 0");
-  if (prm->power < 0 || prm->power > 1) return fail(ctx, RSVD_EINVAL, "power must be 0 (Alg. 2) or 1 (Alg. 1)");
+  if (prm->power < 0 || prm->power > 2) return fail(ctx, RSVD_EINVAL, "power must be 0 (Alg. 2), 1 (Alg. 1) or 2 (Alg. 3)");
+  if (prm->power == 2 && ctx->nranks > 1) return fail(ctx, RSVD_EUNSUPPORTED, "Alg. 3 (pivoted LU) is single-GPU");
   *m_out = mg;
   *n_out = A->n;
   return RSVD_OK;
@@ -517,6 +519,20 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool robus
     if (prm->power == 1) {                                           // Alg. 1 (direct)
       CKS(pass_atx(ctx, p, p.Y, p.Z, centred));                      //   (2) Y = A^T Y
       CKS(pass_ax(ctx, p, p.Z, p.Y, centred));                       //   (3) Y = A Y
+      continue;
+    }
+    if (prm->power == 2) {                                           // Alg. 3 (normalized, pivoted LU)
+      CKS(ensure_ws2(ctx, lu_scratch_bytes(std::max(p.M, p.n), ctx->num_sms)));
+      {
+        Prof pr(ctx, 2, (double)p.M * Np * 8 * 2);
+        CK(launch_lu_rows(p.Y, Np, p.M, l, ctx->ws2, ctx->flags_dev, kFlagLuZero, ctx->num_sms, ctx->stream));
+      }                                                              //   (2) [L,~] = lu(Y)
+      CKS(pass_atx(ctx, p, p.Y, p.Z, centred));                      //   A^T L
+      {
+        Prof pr(ctx, 2, (double)p.n * Np * 8 * 2);
+        CK(launch_lu_rows(p.Z, Np, p.n, l, ctx->ws2, ctx->flags_dev, kFlagLuZero, ctx->num_sms, ctx->stream));
+      }                                                              //   (3) [L,~] = lu(A^T L)
+      CKS(pass_ax(ctx, p, p.Z, p.Y, centred));                       //   (4) Y = A L
       continue;
     }
     CKS(orth(ctx, p, p.Y, p.M, dist, robust, nullptr, false));      // Alg. 2 (2) [Q,~] = qr(Y)

@@ -155,6 +155,11 @@ cudaError_t launch_gather_cols(const double* A, int64_t lda, int64_t m, const in
                                int64_t ldc, cudaStream_t st);
 cudaError_t launch_gather_rows(const double* A, int64_t lda, int64_t n, const int64_t* I, int k, double* R,
                                int64_t ldr, double* Rt, int64_t ldt, cudaStream_t st);
+// In-place GEPP of a tall row-contiguous panel (m x l, ld): Y <- the permuted unit
+// lower factor L of Y = L U (Alg. 3 "[L, ~] = lu(Y)"); flag |= flag_bit on a zero pivot.
+size_t lu_scratch_bytes(int64_t m, int num_sms);
+cudaError_t launch_lu_rows(double* Y, int64_t ld, int64_t m, int l, void* scratch, int* flag, int flag_bit,
+                           int num_sms, cudaStream_t st);
 size_t zq_partial_bytes(int k, int num_sms);
 cudaError_t launch_zq(const double* Z, int64_t ldz, const double* Q, int64_t ldq, int64_t n, int k, double* partial,
                       double* W, int ldw, int num_sms, cudaStream_t st);

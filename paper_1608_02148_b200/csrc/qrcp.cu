@@ -208,6 +208,101 @@ __global__ void __launch_bounds__(QC_THREADS, 1) qrcp_kernel(QrcpArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- pivoted LU
+// "[L, ~] = lu(Y)  pivoted LU" of Alg. 3 (norm_iterations):
+// Gaussian elimination with partial pivoting of a tall row-contiguous panel
+// (row i = l doubles at Y + i * ld), in place, overwritten by the permuted
+// unit lower factor L (L[p_j][j] = 1, L[p_j][c > j] = 0, multipliers
+// elsewhere).  Same cooperative structure as qrcp_kernel with rows in place
+// of columns: per step a per-CTA largest |y_ij| among unpivoted rows, one
+// grid barrier, the same fixed-order pivot choice in every CTA, then each CTA
+// eliminates its own rows against the (never again written) pivot row.
+struct LuArgs {
+  double* Y; int64_t ld; int64_t m; int l;
+  double* cval; int64_t* cidx;             // [2][grid]
+  int* stepof;                             // [m] step at which a row was pivoted, -1 before
+  int* flag; int flag_bit;
+};
+
+__global__ void __launch_bounds__(QC_THREADS, 1) lu_rows_kernel(LuArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double u[QC_RMAX];
+  __shared__ double wv[QC_WARPS];
+  __shared__ int64_t wi[QC_WARPS];
+  __shared__ int64_t s_piv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x;
+  const int64_t r0 = a.m * blockIdx.x / G, r1 = a.m * (blockIdx.x + 1) / G;
+  const int l = a.l;
+  for (int64_t i = r0 + tid; i < r1; i += QC_THREADS) a.stepof[i] = -1;
+  __syncthreads();
+  for (int j = 0; j < l; ++j) {
+    double bv = -1.0;
+    int64_t bi = INT64_MAX;
+    for (int64_t i = r0 + tid; i < r1; i += QC_THREADS) {
+      if (a.stepof[i] >= 0) continue;
+      const double v = fabs(a.Y[i * a.ld + j]);
+      if (better(v, i, bv, bi)) { bv = v; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double vo = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int64_t io = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(vo, io, bv, bi)) { bv = vo; bi = io; }
+    }
+    if (lane == 0) { wv[warp] = bv; wi[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double v = wv[0];
+      int64_t i = wi[0];
+      for (int w = 1; w < QC_WARPS; ++w)
+        if (better(wv[w], wi[w], v, i)) { v = wv[w]; i = wi[w]; }
+      a.cval[(j & 1) * G + blockIdx.x] = v;
+      a.cidx[(j & 1) * G + blockIdx.x] = i;
+    }
+    grid.sync();
+    if (warp == 0) {
+      double v = -1.0;
+      int64_t i = INT64_MAX;
+      for (int b = lane; b < G; b += 32) {
+        const double vb = __ldcg(a.cval + (j & 1) * G + b);
+        const int64_t ib = __ldcg(a.cidx + (j & 1) * G + b);
+        if (better(vb, ib, v, i)) { v = vb; i = ib; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double vo = __shfl_xor_sync(0xffffffffu, v, o);
+        const int64_t io = __shfl_xor_sync(0xffffffffu, i, o);
+        if (better(vo, io, v, i)) { v = vo; i = io; }
+      }
+      if (lane == 0) s_piv = i;
+    }
+    __syncthreads();
+    const int64_t p = s_piv;
+    for (int c = j + tid; c < l; c += QC_THREADS) u[c - j] = __ldcg(a.Y + p * a.ld + c);
+    if (p >= r0 && p < r1 && tid == 0) a.stepof[p] = j;
+    __syncthreads();
+    const double u0 = u[0];
+    if (blockIdx.x == 0 && tid == 0 && !(u0 != 0.0)) atomicOr(a.flag, a.flag_bit);
+    const double inv = u0 != 0.0 ? 1.0 / u0 : 0.0;
+    for (int64_t i = r0 + warp; i < r1; i += QC_WARPS) {
+      if (i == p || a.stepof[i] >= 0) continue;
+      double* y = a.Y + i * a.ld;
+      const double lij = y[j] * inv;
+      for (int c = j + 1 + lane; c < l; c += 32) y[c] = fma(-lij, u[c - j], y[c]);
+      if (lane == 0) y[j] = lij;
+    }
+    __syncthreads();
+  }
+  // pivot rows: unit diagonal, zeros to the right
+  for (int64_t i = r0 + warp; i < r1; i += QC_WARPS) {
+    const int s = a.stepof[i];
+    if (s < 0) continue;
+    double* y = a.Y + i * a.ld;
+    for (int c = s + lane; c < l; c += 32) y[c] = (c == s) ? 1.0 : 0.0;
+  }
+}
+
 // C[r][i] = A[r][J[i]] (column gather, m x k) / R[i][c] = A[I[i]][c] (row gather, k x n)
 // Rt[c][i] = A[I[i]][c] (row gather, transposed into an n x ldt panel)
 __global__ void gather_cols_kernel(const double* __restrict__ A, int64_t lda, int64_t m, const int64_t* __restrict__ J,
@@ -346,6 +441,33 @@ cudaError_t launch_rtsolve(const double* W, int ldw, const double* S, int lds, i
   if (k > 128) return cudaErrorInvalidValue;
   rtsolve_kernel<<<(unsigned)ceil_div(k, 4), 128, 0, st>>>(W, ldw, S, lds, k, U, ldu); ++g_kernel_launches;
   return cudaGetLastError();
+}
+
+size_t lu_scratch_bytes(int64_t m, int num_sms) {
+  return (size_t)2 * num_sms * (sizeof(double) + sizeof(int64_t)) + 256 + (size_t)round_up(m, 64) * sizeof(int);
+}
+
+cudaError_t launch_lu_rows(double* Y, int64_t ld, int64_t m, int l, void* scratch, int* flag, int flag_bit,
+                           int num_sms, cudaStream_t st) {
+  if (l < 1 || l > QC_RMAX || m < l) return cudaErrorInvalidValue;
+  LuArgs a{};
+  a.Y = Y; a.ld = ld; a.m = m; a.l = l;
+  char* p = reinterpret_cast<char*>(scratch);
+  a.cval = reinterpret_cast<double*>(p); p += 2 * num_sms * sizeof(double);
+  a.cidx = reinterpret_cast<int64_t*>(p); p += 2 * num_sms * sizeof(int64_t);
+  p = reinterpret_cast<char*>(round_up((int64_t)(uintptr_t)p, 256));
+  a.stepof = reinterpret_cast<int*>(p);
+  a.flag = flag; a.flag_bit = flag_bit;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_rows_kernel, QC_THREADS, 0);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+  int grid = num_sms;
+  if ((int64_t)grid > m) grid = (int)m;
+  void* args[] = {&a};
+  e = cudaLaunchCooperativeKernel((void*)lu_rows_kernel, dim3(grid), dim3(QC_THREADS), args, 0, st);
+  ++g_kernel_launches;
+  return e;
 }
 
 }  // namespace rsvd

@@ -448,3 +448,25 @@ def test_rid_rcur_exact_rank_reconstruct():
     full = oracle_rid(small, 5, p=20, q=0, seed=1)     # l = 25 = min(m, n)
     det = oracle_id(small, 5)
     assert list(full["J"]) == list(det["J"])
+
+
+def test_lu_pp_matches_scipy_and_normalized_iterations():
+    """Alg. 3: the pivoted LU written out equals scipy's (LAPACK
+    getrf) permuted L on random inputs; the normalized power iterations span
+    the same space as Alg. 2 (Eq. Aq), so rsvd agrees on a well-conditioned
+    input."""
+    import scipy.linalg as sl
+    from oracle.linalg import lu_pp
+    rng = np.random.default_rng(24)
+    Y = rng.standard_normal((50, 8))
+    L, piv = lu_pp(Y)
+    PL, U = sl.lu(Y, permute_l=True)
+    assert np.abs(L - PL).max() < 1e-13
+    Ut = np.triu(np.linalg.solve(L[piv, :], Y[piv, :]))
+    assert np.abs(L @ Ut - Y).max() < 1e-12
+    U_, _ = np.linalg.qr(rng.standard_normal((90, 60)))
+    V_, _ = np.linalg.qr(rng.standard_normal((60, 60)))
+    A = (U_ * np.linspace(2.0, 1.0, 60)) @ V_.T
+    r1 = oracle_rsvd(A, 5, p=3, q=2, seed=6, power="lu")
+    r2 = oracle_rsvd(A, 5, p=3, q=2, seed=6)
+    assert np.abs(r1["d"] - r2["d"]).max() < 1e-12
