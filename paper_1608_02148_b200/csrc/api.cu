@@ -280,12 +280,15 @@ rsvd_status pass_ozaki(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, doub
     CK(ozaki_pass(o, ctx->stream));
     return RSVD_OK;
   }
-  cudaEvent_t e0 = take_event(ctx), e1 = take_event(ctx), e1b = take_event(ctx), e2 = take_event(ctx);
-  cudaEventRecord(e0, ctx->stream);
+  // level 2: only the pass kernel(s) (2 events); level 1 also the X slicing
+  const bool all = ctx->prof == 1;
+  cudaEvent_t e0 = all ? take_event(ctx) : nullptr, e1 = all ? take_event(ctx) : nullptr;
+  cudaEvent_t e1b = take_event(ctx), e2 = take_event(ctx);
+  if (all) cudaEventRecord(e0, ctx->stream);
   o.mark = e1; o.mark2 = e1b;
   CK(ozaki_pass(o, ctx->stream));
   cudaEventRecord(e2, ctx->stream);
-  ctx->pending.push_back({6, 0.0, e0, e1});
+  if (all) ctx->pending.push_back({6, 0.0, e0, e1});
   ctx->pending.push_back({kind, (double)p.M * p.n * 8, e1b, e2});
   return RSVD_OK;
 }
