@@ -31,13 +31,14 @@ struct Tf32Call {
   const float* A; int64_t lda; bool trans;   // A row-major FP32 (16-byte aligned rows)
   const double* B; int64_t ldb;              // K x N panel, FP64 (split to TF32 hi/lo inside)
   double* C; int64_t ldc;                    // M x Nout output, FP64
-  double* P;                                 // stream-K partials (grid * 128 * tf32_n(N) doubles)
+  double* P;                                 // stream-K partials + FP64 drain sums (tf32_partial_bytes)
   unsigned* flags; unsigned epoch;           // as GemmCall
   float* split;                              // 2 * K * tf32_n(N) floats scratch
   int64_t M, K; int N, Nout; int grid;
 };
 bool tf32_pass_supported(const void* A, int64_t lda);
 int tf32_n(int Np);
+size_t tf32_partial_bytes(int Np, int num_sms);   // 2 x grid x 128 x tf32_n(Np) doubles
 size_t tf32_split_bytes(int64_t K, int Np);
 cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st);
 

@@ -8,8 +8,12 @@
 // Precision (reading R12): every FP32 operand x is
 // split as x = hi + lo with hi = x truncated to TF32 (the bits kind::tf32
 // consumes) and lo = rna_tf32(x - hi) (x - hi is exact in FP32); the product is
-// A_hi B_hi + A_lo B_hi + A_hi B_lo, accumulated in FP32 in TMEM for one
-// row-block segment and then summed across segments in FP64.  The panel (X or
+// A_hi B_hi + A_lo B_hi + A_hi B_lo, accumulated in FP32 in TMEM for at most
+// TF_DRAIN units (2048 k) and then summed in FP64: the tensor core's FP32
+// accumulation truncates, and over the 10^6-row reductions of config 4 an
+// undrained TMEM accumulator drifted by ~2e-3 relative (full-size property
+// test); two TMEM accumulator buffers alternate so the MMAs never wait for a
+// drain.  Drains inside a row-block segment add into a per-CTA FP64 buffer.  The panel (X or
 // Q) is split once per pass into global hi/lo FP32 copies by prep_split_b;
 // the A tile is split in shared memory by the 4 epilogue warps.
 //
@@ -29,12 +33,14 @@ namespace tf32 {
 using namespace tc;
 
 constexpr int BM = 128, BK = 32, STAGES = 3, THREADS = 256;
+constexpr int TF_DRAIN = 64;                  // units (of BK = 32 k) per TMEM accumulation run
 constexpr int A_BYTES = BM * BK * 4;          // 16 KB
 constexpr int B_BOX_BYTES = 32 * BK * 4;      // 4 KB per 32-column box
 
 struct Args {
   double* C; int64_t ldc;
   double* P;                                  // [grid][BM][N] partial of a CTA's leading segment
+  double* Pacc;                               // [grid][BM][N] FP64 running sum between drains
   unsigned* flags; unsigned epoch;
   int64_t M, K; int N, Nout;
   int64_t KT, units;
@@ -56,7 +62,7 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   const int nbox = g.N / 32;
   const int b_bytes = nbox * B_BOX_BYTES;
   const int stage_bytes = 2 * A_BYTES + 2 * b_bytes;
-  __shared__ uint64_t full[STAGES], splitd[STAGES], empty_[STAGES], accf, acce;
+  __shared__ uint64_t full[STAGES], splitd[STAGES], empty_[STAGES], accf[2], acce[2];
   __shared__ uint32_t tmem_base;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -67,12 +73,11 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&splitd[s], 4); mbar_init(&empty_[s], 1); }
-    mbar_init(&accf, 1);
-    mbar_init(&acce, 4);
+    for (int b = 0; b < 2; ++b) { mbar_init(&accf[b], 1); mbar_init(&acce[b], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(128));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(256));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -111,13 +116,20 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     if (lane == 0) {
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((TRANS ? 1u : 0u) << 15) | (1u << 16) |
                              ((uint32_t)(g.N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-      int64_t seg = 0;
-      bool first_in_seg = true;
+      int64_t run = 0;                                // accumulation runs (drains) so far
+      bool first = true;
+      int in_run = 0;
+      uint32_t acc_t = tmem;
       for (int64_t it = 0; it < nun; ++it) {
         const int s = (int)(it % STAGES);
         const uint32_t ph = (uint32_t)((it / STAGES) & 1);
-        const int64_t u = u_lo + it, mb = u / KT, kt = u - mb * KT;
-        if (first_in_seg && seg > 0) { mbar_wait(&acce, (uint32_t)((seg - 1) & 1)); tc_fence_after(); }
+        const int64_t u = u_lo + it, kt = u % KT;
+        const bool run_end = (kt == KT - 1) || (it == nun - 1) || (in_run == TF_DRAIN - 1);
+        if (first) {
+          const int b = (int)(run & 1);
+          if (run >= 2) { mbar_wait(&acce[b], (uint32_t)(((run - 2) >> 1) & 1)); }
+          acc_t = tmem + (uint32_t)(b * g.N);
+        }
         mbar_wait(&splitd[s], ph);
         tc_fence_after();
         const uint32_t aH = smem_u32(stageA(s)), aL = smem_u32(stageAlo(s));
@@ -134,24 +146,29 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           }
           const uint64_t dBh = sdesc(bH + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
           const uint64_t dBl = sdesc(bL + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
-          const uint32_t acc0 = (first_in_seg && kk == 0) ? 0u : 1u;
-          mma_tf32(tmem, dAh, dBh, idesc, acc0);
-          mma_tf32(tmem, dAl, dBh, idesc, 1u);
-          mma_tf32(tmem, dAh, dBl, idesc, 1u);
+          const uint32_t acc0 = (first && kk == 0) ? 0u : 1u;
+          mma_tf32(acc_t, dAh, dBh, idesc, acc0);
+          mma_tf32(acc_t, dAl, dBh, idesc, 1u);
+          mma_tf32(acc_t, dAh, dBl, idesc, 1u);
         }
         mma_commit(&empty_[s]);                       // smem stage free when these MMAs complete
-        first_in_seg = false;
-        if (kt == KT - 1 || it == nun - 1) {
-          mma_commit(&accf);                          // accumulator of this segment complete
-          ++seg;
-          first_in_seg = true;
+        first = false;
+        ++in_run;
+        if (run_end) {
+          mma_commit(&accf[run & 1]);                 // this accumulation run complete
+          ++run;
+          first = true;
+          in_run = 0;
         }
       }
     }
   } else if (warp >= 4) {
     // ---------------- A-tile split + epilogue (warps 4..7)
     const int et = tid - 128;                         // 0..127
-    int64_t seg = 0;
+    int64_t run = 0;
+    int in_run = 0, sub = 0;                          // sub: drains so far in this row-block segment
+    const int row = 32 * (warp & 3) + lane;
+    double* pacc = g.Pacc + ((int64_t)blockIdx.x * BM + row) * g.N;
     for (int64_t it = 0; it < nun; ++it) {
       const int s = (int)(it % STAGES);
       const uint32_t ph = (uint32_t)((it / STAGES) & 1);
@@ -173,32 +190,57 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       __syncwarp();
       if (lane == 0) mbar_arrive(&splitd[s]);
       const int64_t u = u_lo + it, mb = u / KT, kt = u - mb * KT;
-      if (kt == KT - 1 || it == nun - 1) {
-        mbar_wait(&accf, (uint32_t)(seg & 1));
-        tc_fence_after();
+      const bool seg_end = (kt == KT - 1) || (it == nun - 1);
+      const bool run_end = seg_end || (in_run == TF_DRAIN - 1);
+      ++in_run;
+      if (!run_end) continue;
+      in_run = 0;
+      const int b = (int)(run & 1);
+      mbar_wait(&accf[b], (uint32_t)((run >> 1) & 1));
+      tc_fence_after();
+      const uint32_t tbase = tmem + (uint32_t)(b * g.N) + ((uint32_t)(32 * (warp & 3)) << 16);
+      if (!seg_end) {
+        // intermediate drain: FP64 running sum of this row-block segment
+        for (int c0 = 0; c0 < g.N; c0 += 32) {
+          uint32_t v[32];
+          TMEM_LD32(tbase + (uint32_t)c0, v);
+          TMEM_WAIT_LD(v);
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            double2* pp = reinterpret_cast<double2*>(pacc + c0 + j);
+            const double2 o = sub ? *pp : make_double2(0.0, 0.0);
+            *pp = make_double2(o.x + (double)__uint_as_float(v[j]), o.y + (double)__uint_as_float(v[j + 1]));
+          }
+        }
+        ++sub;
+      } else {
         // in-kernel stream-K fix-up (see gemm_pass.cu): continuation -> partial +
         // release flag; head of a spanning row block -> acquire later partials
         const int64_t rb_lo = mb * KT, rb_hi = rb_lo + KT;
         const int64_t seg_start = (rb_lo > u_lo) ? rb_lo : u_lo;
         const bool cont = seg_start > rb_lo;
         const bool head = !cont && (u + 1 < rb_hi);
-        const int row = 32 * (warp & 3) + lane;
         const int64_t gm = mb * BM + row;
         for (int c0 = 0; c0 < g.N; c0 += 32) {
           uint32_t v[32];
-          const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)c0;
-          TMEM_LD32(taddr, v);
+          TMEM_LD32(tbase + (uint32_t)c0, v);
           TMEM_WAIT_LD(v);    // the registers are defined only after wait::ld
+          double a[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) a[j] = (double)__uint_as_float(v[j]);
+          if (sub) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const double2 o = *reinterpret_cast<const double2*>(pacc + c0 + j);
+              a[j] += o.x;
+              a[j + 1] += o.y;
+            }
+          }
           if (cont) {
             double* dst = g.P + ((int64_t)blockIdx.x * BM + row) * g.N + c0;
 #pragma unroll
-            for (int j = 0; j < 32; j += 2)
-              *reinterpret_cast<double2*>(dst + j) = make_double2((double)__uint_as_float(v[j]),
-                                                                  (double)__uint_as_float(v[j + 1]));
+            for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(a[j], a[j + 1]);
           } else {
-            double a[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) a[j] = (double)__uint_as_float(v[j]);
             if (head) {
               for (int c = blockIdx.x + 1; c < g.grid && unit_lo(g.units, g.grid, c) < rb_hi; ++c) {
                 unsigned f;
@@ -227,18 +269,19 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           asm volatile("bar.sync 1, 128;" ::: "memory");     // the four epilogue warps
           if (et == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(g.epoch) : "memory");
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acce);
-        ++seg;
+        sub = 0;
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[b]);
+      ++run;
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(128));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256));
   }
 }
 
@@ -297,6 +340,8 @@ bool tf32_pass_supported(const void* A, int64_t lda) {
 
 int tf32_n(int Np) { return (int)round_up(Np, 32); }
 
+size_t tf32_partial_bytes(int Np, int num_sms) { return 2 * (size_t)num_sms * 128 * tf32_n(Np) * sizeof(double); }
+
 size_t tf32_split_bytes(int64_t K, int Np) { return 2 * (size_t)K * tf32_n(Np) * sizeof(float); }
 
 cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st) {
@@ -332,6 +377,7 @@ cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st) {
   if (grid > c.grid) grid = c.grid;
   if (grid < 1) grid = 1;
   g.grid = (int)grid;
+  g.Pacc = c.P + (size_t)c.grid * BM * N;            // second half of the partial buffer (tf32_partial_bytes)
   const size_t smem = (size_t)STAGES * (2 * A_BYTES + 2 * (N / 32) * B_BOX_BYTES) + 1024;
   cudaError_t e;
   if (!c.trans) {

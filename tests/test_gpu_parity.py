@@ -127,6 +127,38 @@ def test_rsvd_parity_cases(rb, m, n, k, p, q, sdist, nu, nv):
     _check_parity(An, r, o, k)
 
 
+@pytest.mark.parametrize("m,n,k,p,q", [(2, 2, 1, 0, 0), (17, 1, 1, 3, 1), (40, 33, 33, 0, 2),
+                                         (33, 40, 5, 100, 1), (1, 9, 1, 2, 0), (129, 128, 120, 0, 1)])
+def test_rsvd_tiny_and_degenerate_shapes(rb, m, n, k, p, q):
+    """Degenerate shapes: 2 x 2, a single column / row, k = min(m, n) (exact
+    SVD), oversampling clamped to min(m, n) (R10), a wide input worked on A^T,
+    and l = 120 = k + 0 on a barely tall matrix."""
+    g = torch.Generator().manual_seed(m * 131 + n)
+    # column scales decay over at most e^-3, so every requested singular value is
+    # well above eps * sigma_1 (relative parity is meaningful for all k of them)
+    A = torch.randn(m, n, generator=g, dtype=torch.float64) * torch.exp(-torch.arange(n, dtype=torch.float64) / max(7.0, n / 3))
+    An = A.numpy()
+    r = rb.rsvd(A.cuda(), k, p=p, q=q, seed=2)
+    o = oracle.oracle_rsvd(An, k, p=p, q=q, seed=2)
+    _check_parity(An, r, o, k, tol_d=1e-10, gap_tol=1e-6, cos_tol=1e-8)
+
+
+@pytest.mark.parametrize("k", [1, 40])
+def test_rid_extreme_k(rb, k):
+    """rid with a single column and with k = n (every column is a skeleton
+    column: Z is a permutation of I and C Z = A exactly up to rounding)."""
+    A = _decay_matrix(500, 40, seed=k + 9, noise=1e-3)
+    An = A.numpy()
+    r = rb.rid(A.cuda(), k, p=5, q=1, seed=4)
+    o = oracle.oracle_rid(An, k, p=5, q=1, seed=4)
+    J = r["J"].cpu().numpy()
+    assert list(J) == list(o["J"])
+    Z = _np(r["Z"])
+    assert np.abs(Z - o["Z"]).max() < 1e-9 * max(1.0, np.abs(o["Z"]).max())
+    if k == 40:
+        assert np.abs(_np(r["C"]) @ Z - An).max() < 1e-12 * np.abs(An).max()
+
+
 def test_rsvd_unaligned_lda(rb):
     """Odd leading dimension (non-16-byte rows) takes the element-wise staging path."""
     A = _decay_matrix(1001, 301, seed=5)
@@ -425,6 +457,39 @@ def test_config3_full_size_rpca(rb):
     sep = np.array([min([abs(dd[i] - dd[j]) for j in range(100) if j != i]) > 1e-6 * dd[0] for i in range(100)])
     c = _cos_cols(rot, o["rotation"])[sep]
     assert np.all(c > 1 - 1e-8)
+
+
+@pytest.mark.timeout(1200)
+def test_config4_full_size_properties(rb):
+    """Config 4 (J:10) at full size -- 10^6 x 10^4 FP32 (40 GB), k = 100,
+    p = 20, q = 3, Gaussian Omega, the launch configuration bench.py times --
+    checked on properties that hold at any size (the oracle cannot run it).
+    B^T = A^T Q, so A^T u_i = d_i v_i (Alg. 5 / Eq. UQU) up to the FP32
+    accumulation of the pass over 10^6 rows (R12): for sampled i the FP64
+    matvec w = A^T u_i (chunked, on the device) gives ||w|| = d_i within the
+    J:5 FP32 tolerance 1e-4 and a direction within 1e-4 of v_i; the vector
+    residual ||w - d_i v_i|| / d_i stays below 1e-2 (FP32 sums of 10^6
+    products).  U, V orthonormal to 1e-5; d descending."""
+    A, meta = synthetic.make_config(4, device="cuda")
+    r = rb.rsvd(A, 100, p=20, q=3, sdist=meta["sdist"], seed=meta["seed_omega"])
+    d = r.d.double()
+    assert bool(torch.all(d[:-1] >= d[1:]))
+    U, V = r.u, r.v
+    eye = torch.eye(100, dtype=torch.float64, device="cuda")
+    assert float((U.double().T @ U.double() - eye).abs().max()) < 1e-5
+    assert float((V.double().T @ V.double() - eye).abs().max()) < 1e-5
+    idx = [0, 1, 10, 50, 99]
+    W = torch.zeros(A.shape[1], len(idx), dtype=torch.float64, device="cuda")
+    Us = U[:, idx].double()
+    for r0 in range(0, A.shape[0], 100000):
+        W += A[r0:r0 + 100000].double().T @ Us[r0:r0 + 100000]
+    for j, i in enumerate(idx):
+        w, v = W[:, j], V[:, i].double()
+        nw = float(torch.linalg.norm(w))
+        assert abs(nw - float(d[i])) / float(d[i]) < 1e-4, (i, nw, float(d[i]))
+        assert 1.0 - float(w @ v) / nw < 1e-4, (i, float(w @ v) / nw)
+        assert float(torch.linalg.norm(w - d[i] * v)) / float(d[i]) < 1e-2
+    del A
 
 
 def test_config5_full_size_rrpca(rb):

@@ -22,7 +22,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&dA, M * K * 4)); fill<<<4096, 256>>>(dA, M * K);
   const int64_t big = M > K ? M : K;
   CK(cudaMalloc(&dB, big * Np * 8)); filld<<<1024, 256>>>(dB, big * Np);
-  CK(cudaMalloc(&dC, big * Np * 8)); CK(cudaMalloc(&dP, (size_t)nsm * 128 * 128 * 8));
+  CK(cudaMalloc(&dC, big * Np * 8)); CK(cudaMalloc(&dP, tf32_partial_bytes(128, nsm)));
   CK(cudaMalloc(&split, tf32_split_bytes(big, Np))); CK(cudaMalloc(&flags, 4096 * 4)); CK(cudaMemset(flags, 0, 4096 * 4));
   unsigned epoch = 0;
   for (int trans = 0; trans < 2; ++trans) {
