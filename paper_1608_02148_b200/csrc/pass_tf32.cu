@@ -17,9 +17,10 @@
 // Q) is split once per pass into global hi/lo FP32 copies by prep_split_b;
 // the A tile is split in shared memory by the 4 epilogue warps.
 //
-// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one
-// thread), warp 2 = TMEM allocator, warps 4..7 = A-tile split + epilogue
-// (warp w reads TMEM lanes 32*(w%4)..+32).  Shared memory per stage:
+// Roles (384 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one
+// thread), warp 2 = TMEM allocator, warps 4..7 = A-tile split, warps 8..11 =
+// drains / epilogue (warp w reads TMEM lanes 32*(w%4)..+32), so a drain never
+// delays the split of the next units.  Shared memory per stage:
 // A (16 KB, SWIZZLE_128B; K-major for NN, MN-major for TN), A_lo (16 KB),
 // B_hi, B_lo (N/32 boxes of 4 KB, MN-major).  3 stages.
 #include <cuda.h>
@@ -32,7 +33,7 @@ namespace rsvd {
 namespace tf32 {
 using namespace tc;
 
-constexpr int BM = 128, BK = 32, STAGES = 3, THREADS = 256;
+constexpr int BM = 128, BK = 32, STAGES = 3, THREADS = 384;
 constexpr int TF_DRAIN = 64;                  // units (of BK = 32 k) per TMEM accumulation run
 constexpr int A_BYTES = BM * BK * 4;          // 16 KB
 constexpr int B_BOX_BYTES = 32 * BK * 4;      // 4 KB per 32-column box
@@ -162,13 +163,9 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         }
       }
     }
-  } else if (warp >= 4) {
-    // ---------------- A-tile split + epilogue (warps 4..7)
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- A-tile split (warps 4..7)
     const int et = tid - 128;                         // 0..127
-    int64_t run = 0;
-    int in_run = 0, sub = 0;                          // sub: drains so far in this row-block segment
-    const int row = 32 * (warp & 3) + lane;
-    double* pacc = g.Pacc + ((int64_t)blockIdx.x * BM + row) * g.N;
     for (int64_t it = 0; it < nun; ++it) {
       const int s = (int)(it % STAGES);
       const uint32_t ph = (uint32_t)((it / STAGES) & 1);
@@ -189,6 +186,15 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       fence_proxy_async();                            // generic-proxy writes -> async proxy (MMA)
       __syncwarp();
       if (lane == 0) mbar_arrive(&splitd[s]);
+    }
+  } else if (warp >= 8) {
+    // ---------------- drains + epilogue (warps 8..11)
+    const int et = tid - 256;                         // 0..127
+    int64_t run = 0;
+    int in_run = 0, sub = 0;                          // sub: drains so far in this row-block segment
+    const int row = 32 * (warp & 3) + lane;
+    double* pacc = g.Pacc + ((int64_t)blockIdx.x * BM + row) * g.N;
+    for (int64_t it = 0; it < nun; ++it) {
       const int64_t u = u_lo + it, mb = u / KT, kt = u - mb * KT;
       const bool seg_end = (kt == KT - 1) || (it == nun - 1);
       const bool run_end = seg_end || (in_run == TF_DRAIN - 1);
