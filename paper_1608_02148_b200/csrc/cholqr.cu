@@ -34,6 +34,8 @@ template <int TJ>
 __global__ void __launch_bounds__(CQ_THREADS, 1)
 gram_partial_kernel(const double* __restrict__ S, int64_t lds, int64_t rows, int Np, int64_t rows_per_cta,
                     double* __restrict__ partial) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int TI = 2 * TJ, NG = 32 * TJ;
   constexpr int LDT = NG + ((4 - NG) & 15);
   extern __shared__ __align__(16) double sm[];
@@ -111,6 +113,8 @@ gram_partial_kernel(const double* __restrict__ S, int64_t lds, int64_t rows, int
 // they are in flight together), then a fixed xor tree.
 __global__ void gram_reduce_kernel(const double* __restrict__ partial, int P, int Ng, int Np,
                                    double* __restrict__ G, int ldg) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int T = 8, B = 8;
   const int e = blockIdx.x * (blockDim.x / T) + threadIdx.x / T;
   const int t = threadIdx.x % T;
@@ -161,7 +165,8 @@ cudaError_t launch_gram(const double* S, int64_t lds, int64_t rows, int Np, doub
       if (e != cudaSuccess) return e;                                                                    \
       attr = true;                                                                                       \
     }                                                                                                    \
-    gram_partial_kernel<TJ><<<P, CQ_THREADS, smem, st>>>(S, lds, rows, Np, rpc, partial);               \
+    e = launch_pdl(gram_partial_kernel<TJ>, dim3(P), dim3(CQ_THREADS), smem, st, S, lds, rows, Np, rpc, partial); \
+    if (e != cudaSuccess) return e;                                                                      \
   }
   const size_t smem_max = (size_t)GR_STAGES * GR_BK * ldpad(128) * sizeof(double);
   switch (ng / 32) {
@@ -175,7 +180,9 @@ cudaError_t launch_gram(const double* S, int64_t lds, int64_t rows, int Np, doub
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int per_block = 256 / 8;
-  gram_reduce_kernel<<<(unsigned)ceil_div((int64_t)Np * Np, per_block), 256, 0, st>>>(partial, P, ng, Np, G, ldg);
+  e = launch_pdl(gram_reduce_kernel, dim3((unsigned)ceil_div((int64_t)Np * Np, per_block)), dim3(256), 0, st,
+                 (const double*)partial, P, ng, Np, G, ldg);
+  if (e != cudaSuccess) return e;
   ++g_kernel_launches;
   return cudaGetLastError();
 }
@@ -261,6 +268,8 @@ template <int NBLK>
 __global__ void __launch_bounds__(256, 1)
 chol_blk_kernel(const double* __restrict__ G, int ldg, int l, int npad, double* __restrict__ R,
                 double* __restrict__ Rinv, int* flag, int flag_bit) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NG = 16 * NBLK, LDM = NG + 4;
   extern __shared__ __align__(16) double smc[];
   double* M = smc;                          // NG x LDM
@@ -391,7 +400,8 @@ cudaError_t launch_chol_aug(const double* G, int ldg, int l, int npad, double* R
       if (e != cudaSuccess) return e;                                                                    \
       attr = true;                                                                                       \
     }                                                                                                    \
-    chol_blk_kernel<NBK><<<1, 256, smem, st>>>(G, ldg, l, npad, R, Rinv, flag, flag_bit);               \
+    e = launch_pdl(chol_blk_kernel<NBK>, dim3(1), dim3(256), smem, st, G, ldg, l, npad, R, Rinv, flag, flag_bit); \
+    if (e != cudaSuccess) return e;                                                                      \
   }
   switch (nblk) {
     case 1: RSVD_CB(1) break;
@@ -421,6 +431,8 @@ template <int TJ, int NBUF>
 __global__ void __launch_bounds__(CQ_THREADS)
 panel_apply_kernel(const double* S, int64_t lds, int64_t rows, int Np, const double* __restrict__ T, int64_t ldt,
                    double* C, int64_t ldc, int Nout, int upper) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NG = 32 * TJ;
   constexpr int LDX = NG + ((4 - NG) & 15);
   extern __shared__ __align__(16) double sm[];
@@ -520,7 +532,8 @@ cudaError_t launch_panel_apply(const double* S, int64_t lds, int64_t rows, int N
       if (e != cudaSuccess) return e;                                                                    \
       attr = true;                                                                                       \
     }                                                                                                    \
-    panel_apply_kernel<TJ, (TJ == 4 ? 1 : 2)><<<(unsigned)grid, CQ_THREADS, smem, st>>>(S, lds, rows, Np, T, ldt, C, ldc, Nout, upper ? 1 : 0); \
+    e = launch_pdl(panel_apply_kernel<TJ, (TJ == 4 ? 1 : 2)>, dim3((unsigned)grid), dim3(CQ_THREADS), smem, st, S, lds, rows, Np, T, ldt, C, ldc, Nout, upper ? 1 : 0); \
+    if (e != cudaSuccess) return e; \
   }
   switch (ng / 32) {
     case 1: RSVD_APPLY(1) break;

@@ -93,6 +93,8 @@ template <int JG, int EPL>
 __global__ void __launch_bounds__(512, 1)
 jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict__ sigma, double* __restrict__ Wo,
                 int ldo, double2* __restrict__ rlog, int* __restrict__ rank_out, int* flag, int* sweeps_out) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) double Xs[];           // L columns x LDX (column p: Xs + p * LDX)
   const int L = jac_L(l);
   constexpr int LDX = JG * EPL + 4;                      // consecutive columns 4 doubles apart mod 32 banks
@@ -228,6 +230,8 @@ constexpr int JA_CH = 16;
 __global__ void __launch_bounds__(128)
 jacobi_apply_j(const double2* __restrict__ rlog, const int* __restrict__ rank, int l, double* __restrict__ Jo,
                int ldo) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double rows[4][129];
   __shared__ __align__(16) double2 buf[2][JA_CH * 64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -300,7 +304,8 @@ cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double
       if (e != cudaSuccess) return e;                                                                     \
       attr = true;                                                                                        \
     }                                                                                                     \
-    jacobi_x_kernel<JG, EPL><<<1, threads, smem, st>>>(R, ldr, l, sigma, W, ldo, rlog, rank, flag, sweeps); \
+    e = launch_pdl(jacobi_x_kernel<JG, EPL>, dim3(1), dim3(threads), smem, st, R, ldr, l, sigma, W, ldo, rlog, rank, flag, sweeps); \
+    if (e != cudaSuccess) return e; \
   }
 #define RSVD_JX_EPL(JG)                  \
   if (epl_need <= 1) RSVD_JX(JG, 1)      \
@@ -317,7 +322,8 @@ cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double
   ++g_kernel_launches;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  jacobi_apply_j<<<(unsigned)ceil_div(l, 4), 128, 0, st>>>(rlog, rank, l, J, ldo);
+  e = launch_pdl(jacobi_apply_j, dim3((unsigned)ceil_div(l, 4)), dim3(128), 0, st, (const double2*)rlog, (const int*)rank, l, J, ldo);
+  if (e != cudaSuccess) return e;
   ++g_kernel_launches;
   return cudaGetLastError();
 }

@@ -17,6 +17,7 @@
 namespace rsvd {
 
 int64_t g_kernel_launches = 0;
+int g_pdl = [] { const char* e = getenv("RSVD_PDL"); return (e && e[0] == '0') ? 0 : 1; }();
 
 __device__ __forceinline__ uint4 philox_round(uint4 c, uint32_t k0, uint32_t k1) {
   const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
@@ -42,6 +43,8 @@ __device__ __forceinline__ double u01(uint64_t x) {
 template <typename TO>
 __global__ void omega_kernel(int64_t n, int64_t l, int64_t ldo, int64_t ncz, int sdist, uint64_t seed,
                              uint64_t stream, bool f32_round, TO* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = n * ncz;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -70,12 +73,15 @@ cudaError_t launch_omega(int64_t n, int64_t l, int64_t ldo, int64_t ncols_zero, 
   int blocks = (int)ceil_div(total, 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
+  cudaError_t e;
   if (out_f32)
-    omega_kernel<float><<<blocks, 256, 0, st>>>(n, l, ldo, ncols_zero, sdist, seed, stream, f32_round,
-                                                 static_cast<float*>(out));
+    e = launch_pdl(omega_kernel<float>, dim3(blocks), dim3(256), 0, st, n, l, ldo, ncols_zero, sdist, seed, stream,
+                   f32_round, static_cast<float*>(out));
   else
-    omega_kernel<double><<<blocks, 256, 0, st>>>(n, l, ldo, ncols_zero, sdist, seed, stream, f32_round,
-                                                  static_cast<double*>(out)); ++g_kernel_launches;
+    e = launch_pdl(omega_kernel<double>, dim3(blocks), dim3(256), 0, st, n, l, ldo, ncols_zero, sdist, seed, stream,
+                   f32_round, static_cast<double*>(out));
+  ++g_kernel_launches;
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -457,6 +457,8 @@ cudaError_t launch_tsqr_combine(double* Y, int64_t ldy, int64_t M, int l, int64_
 
 // ------------------------------------------------------------------ signs / copies
 __global__ void sign_from_v_kernel(const double* __restrict__ V, int64_t ldv, int64_t n, double* sgn) {
+  pdl_wait();
+  pdl_trigger();
   const int col = blockIdx.x;
   __shared__ double bv[256];
   __shared__ int64_t bi[256];
@@ -484,11 +486,13 @@ __global__ void sign_from_v_kernel(const double* __restrict__ V, int64_t ldv, in
 }
 
 cudaError_t launch_sign_from_v(const double* V, int64_t ldv, int64_t n, int l, double* sgn, cudaStream_t st) {
-  sign_from_v_kernel<<<l, 256, 0, st>>>(V, ldv, n, sgn); ++g_kernel_launches;
+  CUDA_TRY(launch_pdl(sign_from_v_kernel, dim3(l), dim3(256), 0, st, V, ldv, n, sgn)); ++g_kernel_launches;
   return cudaGetLastError();
 }
 
 __global__ void scale_cols_kernel(double* X, int64_t ldx, int64_t rows, int l, const double* sgn) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = rows * l;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / l;
@@ -505,13 +509,15 @@ static int grid_for(int64_t total) {
 }
 
 cudaError_t launch_scale_cols(double* X, int64_t ldx, int64_t rows, int l, const double* sgn, cudaStream_t st) {
-  scale_cols_kernel<<<grid_for(rows * l), 256, 0, st>>>(X, ldx, rows, l, sgn); ++g_kernel_launches;
+  CUDA_TRY(launch_pdl(scale_cols_kernel, dim3(grid_for(rows * l)), dim3(256), 0, st, X, ldx, rows, l, sgn)); ++g_kernel_launches;
   return cudaGetLastError();
 }
 
 template <typename TO>
 __global__ void copy_out_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int cols,
                                 TO* __restrict__ dst, int64_t ldd, const double* colfac) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = rows * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / cols;
@@ -526,23 +532,27 @@ cudaError_t launch_copy_out(const double* src, int64_t lds, int64_t rows, int co
                             bool dst_f32, const double* colfac, cudaStream_t st) {
   if (rows * cols == 0) return cudaSuccess;
   if (dst_f32)
-    copy_out_kernel<float><<<grid_for(rows * cols), 256, 0, st>>>(src, lds, rows, cols, (float*)dst, ldd, colfac);
+    CUDA_TRY(launch_pdl(copy_out_kernel<float>, dim3(grid_for(rows * cols)), dim3(256), 0, st, src, lds, rows, cols, (float*)dst, ldd, colfac));
   else
-    copy_out_kernel<double><<<grid_for(rows * cols), 256, 0, st>>>(src, lds, rows, cols, (double*)dst, ldd, colfac); ++g_kernel_launches;
+    CUDA_TRY(launch_pdl(copy_out_kernel<double>, dim3(grid_for(rows * cols)), dim3(256), 0, st, src, lds, rows, cols, (double*)dst, ldd, colfac)); ++g_kernel_launches;
   return cudaGetLastError();
 }
 
 __global__ void fill_kernel(double* p, int64_t n, double v) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) p[e] = v;
 }
 
 cudaError_t launch_fill(double* p, int64_t count, double v, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
-  fill_kernel<<<grid_for(count), 256, 0, st>>>(p, count, v); ++g_kernel_launches;
+  CUDA_TRY(launch_pdl(fill_kernel, dim3(grid_for(count)), dim3(256), 0, st, p, count, v)); ++g_kernel_launches;
   return cudaGetLastError();
 }
 
 __global__ void zero_cols_kernel(double* Y, int64_t ld, int64_t rows, int l, int npad) {
+  pdl_wait();
+  pdl_trigger();
   const int w = npad - l;
   const int64_t total = rows * w;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
@@ -551,7 +561,7 @@ __global__ void zero_cols_kernel(double* Y, int64_t ld, int64_t rows, int l, int
 
 cudaError_t launch_zero_cols(double* Y, int64_t ld, int64_t rows, int l, int npad, cudaStream_t st) {
   if (npad <= l || rows == 0) return cudaSuccess;
-  zero_cols_kernel<<<grid_for(rows * (npad - l)), 256, 0, st>>>(Y, ld, rows, l, npad); ++g_kernel_launches;
+  CUDA_TRY(launch_pdl(zero_cols_kernel, dim3(grid_for(rows * (npad - l))), dim3(256), 0, st, Y, ld, rows, l, npad)); ++g_kernel_launches;
   return cudaGetLastError();
 }
 
@@ -569,13 +579,15 @@ cudaError_t launch_pca_eig(const double* d, int k, double m, void* eig, bool f32
 }
 
 __global__ void check_finite_kernel(const double* v, int64_t n, int* flag) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     if (!isfinite(v[e])) { atomicOr(flag, 4); return; }
 }
 
 cudaError_t launch_check_finite(const double* v, int64_t n, int* flag, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  check_finite_kernel<<<grid_for(n), 256, 0, st>>>(v, n, flag); ++g_kernel_launches;
+  CUDA_TRY(launch_pdl(check_finite_kernel, dim3(grid_for(n)), dim3(256), 0, st, v, n, flag)); ++g_kernel_launches;
   return cudaGetLastError();
 }
 

@@ -106,6 +106,8 @@ __device__ __forceinline__ double fval(const double* A, int64_t lda, const doubl
 __global__ void __launch_bounds__(256)
 ozaki_amax_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, const double* __restrict__ c,
                   const double* __restrict__ rs, double* __restrict__ tmax, int* flag) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[8];
   const int64_t r0 = (int64_t)blockIdx.y * BM, c0 = (int64_t)blockIdx.x * BKO;
   const int tid = threadIdx.x;
@@ -139,6 +141,8 @@ __global__ void __launch_bounds__(256)
 ozaki_slice_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, const double* __restrict__ c,
                      const double* __restrict__ rs, const double* __restrict__ tmax, int8_t* __restrict__ slices,
                      int64_t ldn, double* __restrict__ ea, int nsx) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t r0 = (int64_t)blockIdx.y * BM, c0 = (int64_t)blockIdx.x * BKO;
   const int tid = threadIdx.x;
   const int sy = blockIdx.y / KSUP, sx = blockIdx.x / KSUP;
@@ -180,6 +184,8 @@ template <int S>
 __global__ void __launch_bounds__(XT_THREADS)
 ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, int8_t* __restrict__ xs,
                      int64_t ldk, double* __restrict__ xf) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char xt[];      // S x XT_COLS x XT_LD
   __shared__ double red[XT_G][XT_COLS];
   __shared__ double escale[XT_COLS];
@@ -254,6 +260,8 @@ __host__ __device__ constexpr int oz_nbuf(int S, int N) { return 3 * oz_ubuf(S, 
 template <bool TRANS, int S, int N>
 __global__ void __launch_bounds__(THREADS, 1)
 ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapX, Args g) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int XSL = N * BKU;                      // bytes of one X slice tile (N rows x 64 k)
@@ -506,8 +514,11 @@ size_t ozaki_x_bytes(int64_t K, int Np) {
 cudaError_t ozaki_slice_a(const OzakiA& a, const double* A, int64_t lda, const double* c, const double* rs, int* flag,
                           cudaStream_t st) {
   dim3 grid((unsigned)ceil_div(a.n, oz::BKO), (unsigned)ceil_div(a.m, oz::BM));
-  oz::ozaki_amax_kernel<<<grid, 256, 0, st>>>(A, lda, a.m, a.n, c, rs, a.tmax, flag);
-  oz::ozaki_slice_a_kernel<OZ_S><<<grid, 256, 0, st>>>(A, lda, a.m, a.n, c, rs, a.tmax, a.slices, a.ldn, a.ea, a.ntiles);
+  cudaError_t e = launch_pdl(oz::ozaki_amax_kernel, grid, dim3(256), 0, st, A, lda, a.m, a.n, c, rs, a.tmax, flag);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(oz::ozaki_slice_a_kernel<OZ_S>, grid, dim3(256), 0, st, A, lda, a.m, a.n, c, rs,
+                 (const double*)a.tmax, a.slices, a.ldn, a.ea, a.ntiles);
+  if (e != cudaSuccess) return e;
   g_kernel_launches += 2;
   return cudaGetLastError();
 }
@@ -562,7 +573,8 @@ static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st) {
     attr = true;
   }
   const dim3 gs((unsigned)ceil_div(ldk, ET), (unsigned)ceil_div(N, XT_COLS));
-  ozaki_slice_x_kernel<OZ_S><<<gs, XT_THREADS, xt_smem(OZ_S), st>>>(c.B, c.ldb, c.K, N, xs, ldk, xf);
+  const cudaError_t el = launch_pdl(ozaki_slice_x_kernel<OZ_S>, gs, dim3(XT_THREADS), (size_t)xt_smem(OZ_S), st, c.B, c.ldb, c.K, N, xs, ldk, xf);
+  if (el != cudaSuccess) return el;
   ++g_kernel_launches;
   return cudaGetLastError();
 }
@@ -607,7 +619,8 @@ static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
       if (e != cudaSuccess) return e;                                                                    \
       attr = true;                                                                                       \
     }                                                                                                    \
-    ozaki_pass_kernel<TR, OZ_S, NN><<<g.grid, THREADS, smem, st>>>(mA, mX, g);                           \
+    e = launch_pdl(ozaki_pass_kernel<TR, OZ_S, NN>, dim3(g.grid), dim3(THREADS), smem, st, mA, mX, g);      \
+    if (e != cudaSuccess) return e;                                                                      \
   }
   if (!c.trans) {
     switch (N) { case 16: RSVD_OZ(false, 16) break; case 32: RSVD_OZ(false, 32) break;

@@ -12,7 +12,7 @@ __device__ unsigned long long g_jp[6];
 #define JAC_PROBE(slot) if (threadIdx.x == 0) { long long _t = clock64(); _jt[slot] += _t - _jl; _jl = _t; }
 #define JAC_PROBE_OUT if (threadIdx.x == 0) { for (int q = 0; q < 5; ++q) atomicAdd(&g_jp[q], (unsigned long long)_jt[q]); atomicAdd(&g_jp[5], (unsigned long long)gstep); }
 #include "../paper_1608_02148_b200/csrc/jacobi.cu"
-namespace rsvd { int64_t g_kernel_launches = 0; }
+namespace rsvd { int64_t g_kernel_launches = 0; int g_pdl = 1; }
 using namespace rsvd;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s @%d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
 

@@ -18,7 +18,7 @@ __device__ unsigned long long g_oz2[4], g_oz3[4];
 #define OZ_PROBE3_OUT if (lane == 0) for (int q = 0; q < 4; ++q) atomicAdd(&g_oz3[q], (unsigned long long)_p3[q]);
 #include "../paper_1608_02148_b200/csrc/pass_tf32.cu"
 #include "../paper_1608_02148_b200/csrc/pass_ozaki.cu"
-namespace rsvd { int64_t g_kernel_launches = 0; }
+namespace rsvd { int64_t g_kernel_launches = 0; int g_pdl = 1; }
 using namespace rsvd;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s @%d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
 
