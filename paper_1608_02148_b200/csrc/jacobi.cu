@@ -13,11 +13,15 @@
 // highest differing index bit), and only half of X crosses shared memory per
 // step.  Four lanes own a pair.
 //
-// J is not accumulated here: each step's rotations (c, s) go to a log in
-// global memory, and jacobi_apply_j replays the log on the rows of J (rows
-// are independent: the rotations act on columns) in parallel across CTAs, so
-// the sequential kernel moves only X.
+// J is not accumulated by the sweeping CTA: each step's rotations (c, s) go to
+// a log in global memory, and the other CTAs of the same launch replay the log
+// on the rows of J (rows are independent: the rotations act on columns) while
+// the sweeps run -- the log is published in chunks of JA_CH steps with
+// release/acquire counters tagged by a per-launch epoch -- so the replay adds
+// only its last chunk to the critical path.
 #include <math.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -88,13 +92,97 @@ size_t jacobi_log_bytes(int l) {
   return (size_t)31 * (L - 1) * (L / 2) * 2 * sizeof(double);
 }
 
+constexpr int JA_CH = 16;   // rotation-log chunk (steps) published / replayed at once
+
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Replay of the rotation log on rows [row0, row0 + nw) of J (one warp per row,
+// identity start): chunk c of JA_CH steps is read once prog (epoch-tagged step
+// count) covers it; after `done` (epoch-tagged final step count) the rest.
+// Jo(i, rank[p]) = J(i, p).
+__device__ void jacobi_replay(const double2* __restrict__ rlog, const int* __restrict__ rank, int l,
+                              double* __restrict__ Jo, int ldo, int row0, const unsigned long long* prog,
+                              const unsigned long long* done, unsigned epoch, unsigned char* sm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5, nt = blockDim.x;
+  const int i = row0 + warp;
+  const int L = jac_L(l), npairs = L / 2;
+  double2* buf = reinterpret_cast<double2*>(sm);                       // [JA_CH * 64]
+  double* row = reinterpret_cast<double*>(sm + JA_CH * 64 * sizeof(double2)) + warp * 129;
+  for (int p = lane; p < L; p += 32) row[p] = (p == i) ? 1.0 : 0.0;
+  int levels = 0;
+  while ((1 << levels) < L) ++levels;
+  __shared__ long long s_avail;
+  __shared__ int s_fin;
+  int lh = levels - 1, s = 0;
+  for (int64_t ch = 0;; ++ch) {
+    if (threadIdx.x == 0) {
+      long long avail = -1;
+      int fin = 0;
+      for (;;) {
+        const unsigned long long d = ld_acquire_u64(done);
+        if ((unsigned)(d >> 32) == epoch) { avail = (long long)(d & 0xffffffffu); fin = 1; break; }
+        const unsigned long long pg = ld_acquire_u64(prog);
+        if ((unsigned)(pg >> 32) == epoch && (long long)(pg & 0xffffffffu) >= (ch + 1) * JA_CH) {
+          avail = (long long)(pg & 0xffffffffu);
+          break;
+        }
+        __nanosleep(256);
+      }
+      s_avail = avail;
+      s_fin = fin;
+    }
+    __syncthreads();
+    const long long avail = s_avail;
+    const int fin = s_fin;
+    const int64_t s0 = ch * JA_CH;
+    if (s0 >= avail) {
+      if (fin) break;
+      continue;                                        // (not reached: prog covered the chunk)
+    }
+    const int nst = (int)min((int64_t)JA_CH, (int64_t)avail - s0);
+    for (int e = threadIdx.x; e < nst * npairs; e += nt) buf[e] = __ldcg(rlog + s0 * npairs + e);
+    __syncthreads();
+    for (int st = 0; st < nst; ++st) {
+      for (int k = lane; k < npairs; k += 32) {
+        int p, q;
+        jac_pair(lh, s, k, p, q);
+        const double2 cs = buf[st * npairs + k];
+        const double u = row[p], v = row[q];
+        row[p] = cs.x * u - cs.y * v;
+        row[q] = cs.y * u + cs.x * v;
+      }
+      __syncwarp();
+      if (++s == (1 << lh)) {
+        s = 0;
+        if (--lh < 0) lh = levels - 1;
+      }
+    }
+    __syncthreads();                                   // buf reused by the next chunk
+  }
+  if (i < l)
+    for (int p = lane; p < l; p += 32) Jo[i * ldo + __ldcg(rank + p)] = row[p];
+}
+
 // JG lanes own a column pair; EPL = elements of a column per lane (l <= JG * EPL)
 template <int JG, int EPL>
 __global__ void __launch_bounds__(512, 1)
 jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict__ sigma, double* __restrict__ Wo,
-                int ldo, double2* __restrict__ rlog, int* __restrict__ rank_out, int* flag, int* sweeps_out) {
+                int ldo, double2* __restrict__ rlog, int* __restrict__ rank_out, int* flag, int* sweeps_out,
+                double* __restrict__ Jo, unsigned long long* prog, unsigned long long* done, unsigned epoch) {
   pdl_wait();
   pdl_trigger();
+  if (blockIdx.x > 0) {                                  // J-replay CTAs
+    extern __shared__ __align__(16) unsigned char jsm[];
+    jacobi_replay(rlog, rank_out, l, Jo, ldo, (blockIdx.x - 1) * (int)(blockDim.x >> 5), prog, done, epoch, jsm);
+    return;
+  }
   extern __shared__ __align__(16) double Xs[];           // L columns x LDX (column p: Xs + p * LDX)
   const int L = jac_L(l);
   constexpr int LDX = JG * EPL + 4;                      // consecutive columns 4 doubles apart mod 32 banks
@@ -178,6 +266,10 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
           JAC_PROBE(3)
         }
         __syncthreads();                                 // travelling columns published
+        if (tid == 0 && ((gstep + 1) % JA_CH) == 0) {
+          __threadfence();
+          st_release_u64(prog, ((unsigned long long)epoch << 32) | (unsigned long long)(gstep + 1));
+        }
         JAC_PROBE(4)
       }
       if (act) {
@@ -213,73 +305,15 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
     const double inv = sp > 0.0 ? 1.0 / sp : 1.0;
     for (int i = lane; i < l; i += 32) Wo[i * ldo + rk] = Xs[p * LDX + i] * inv;
   }
+  __syncthreads();                                     // rank_out complete
   if (tid == 0) {
     if (!converged) atomicOr(flag, 2);
     if (bad) atomicOr(flag, 4);
     if (sweeps_out) *sweeps_out = sweeps;
-    rank_out[128] = sweeps;                              // rotations logged for `sweeps` sweeps
+    rank_out[128] = sweeps;
+    __threadfence();
+    st_release_u64(done, ((unsigned long long)epoch << 32) | (unsigned long long)gstep);   // every logged step
   }
-}
-
-// J = product of the logged rotations (identity start), one warp per row of J
-// (4 rows per CTA); the log is staged through shared memory in chunks of
-// JA_CH steps (cp.async, double-buffered) shared by the CTA's warps.
-// Jo(i, rank[p]) = J(i, p).
-constexpr int JA_CH = 16;
-
-__global__ void __launch_bounds__(128)
-jacobi_apply_j(const double2* __restrict__ rlog, const int* __restrict__ rank, int l, double* __restrict__ Jo,
-               int ldo) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ double rows[4][129];
-  __shared__ __align__(16) double2 buf[2][JA_CH * 64];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * 4 + warp;
-  const int L = jac_L(l), npairs = L / 2;
-  double* row = rows[warp];
-  for (int p = lane; p < L; p += 32) row[p] = (p == i) ? 1.0 : 0.0;
-  const int nsweeps = rank[128];
-  int levels = 0;
-  while ((1 << levels) < L) ++levels;
-  const int64_t total = (int64_t)nsweeps * (L - 1);
-  const int64_t nch = ceil_div(total, JA_CH);
-  auto load = [&](int b, int64_t ch) {
-    const int64_t s0 = ch * JA_CH;
-    const int64_t n = min((int64_t)JA_CH, total - s0) * npairs;
-    const double2* src = rlog + s0 * npairs;
-    for (int e = threadIdx.x; e < n; e += 128) cp_async16(&buf[b][e], src + e, 16);
-  };
-  if (nch > 0) load(0, 0);
-  cp_async_commit();
-  int lh = levels - 1, s = 0;
-  for (int64_t ch = 0; ch < nch; ++ch) {
-    if (ch + 1 < nch) load((int)((ch + 1) & 1), ch + 1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const double2* cb = buf[ch & 1];
-    const int nst = (int)min((int64_t)JA_CH, total - ch * JA_CH);
-    for (int st = 0; st < nst; ++st) {
-      for (int k = lane; k < npairs; k += 32) {
-        int p, q;
-        jac_pair(lh, s, k, p, q);
-        const double2 cs = cb[st * npairs + k];
-        const double u = row[p], v = row[q];
-        row[p] = cs.x * u - cs.y * v;
-        row[q] = cs.y * u + cs.x * v;
-      }
-      __syncwarp();
-      if (++s == (1 << lh)) {
-        s = 0;
-        if (--lh < 0) lh = levels - 1;
-      }
-    }
-    __syncthreads();                                     // buffer reused by chunk ch + 2
-  }
-  cp_async_wait<0>();
-  if (i < l)
-    for (int p = lane; p < l; p += 32) Jo[i * ldo + rank[p]] = row[p];
 }
 
 int g_jacobi_lanes = 0;   // lanes per column pair (4, 8, 16; 0: 4 for L <= 64, else 8; tools/bench_jacobi)
@@ -290,6 +324,10 @@ cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double
   const int L = jac_L(l);
   double2* rlog = reinterpret_cast<double2*>(scratch);
   int* rank = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + jacobi_log_bytes(l));
+  unsigned long long* prog = reinterpret_cast<unsigned long long*>(rank + 192);   // 8-byte aligned, after rank[0..128]
+  unsigned long long* done = prog + 1;
+  static unsigned epoch_ctr = 0;
+  const unsigned epoch = ++epoch_ctr;
   const int JGv = g_jacobi_lanes ? g_jacobi_lanes : (L <= 64 ? 4 : 8);
   const int threads = (int)round_up((int64_t)(L / 2) * JGv, 32);
   const int epl_need = (l + JGv - 1) / JGv;
@@ -297,14 +335,16 @@ cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double
 #define RSVD_JX(JG, EPL)                                                                                   \
   {                                                                                                       \
     const int ldx = JG * EPL + 4;                                                                         \
-    const size_t smem = (size_t)L * ldx * sizeof(double);                                                 \
+    const size_t smem = std::max((size_t)L * ldx * sizeof(double),                                        \
+                                 (size_t)JA_CH * 64 * sizeof(double2) + (size_t)(threads / 32) * 129 * sizeof(double)); \
     static bool attr = false;                                                                             \
     if (!attr) {                                                                                          \
       e = cudaFuncSetAttribute(jacobi_x_kernel<JG, EPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
       if (e != cudaSuccess) return e;                                                                     \
       attr = true;                                                                                        \
     }                                                                                                     \
-    e = launch_pdl(jacobi_x_kernel<JG, EPL>, dim3(1), dim3(threads), smem, st, R, ldr, l, sigma, W, ldo, rlog, rank, flag, sweeps); \
+    e = launch_pdl(jacobi_x_kernel<JG, EPL>, dim3(1 + (unsigned)ceil_div(l, threads / 32)), dim3(threads), smem, st, \
+                   R, ldr, l, sigma, W, ldo, rlog, rank, flag, sweeps, J, prog, done, epoch);               \
     if (e != cudaSuccess) return e; \
   }
 #define RSVD_JX_EPL(JG)                  \
@@ -320,14 +360,9 @@ cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double
 #undef RSVD_JX_EPL
 #undef RSVD_JX
   ++g_kernel_launches;
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  e = launch_pdl(jacobi_apply_j, dim3((unsigned)ceil_div(l, 4)), dim3(128), 0, st, (const double2*)rlog, (const int*)rank, l, J, ldo);
-  if (e != cudaSuccess) return e;
-  ++g_kernel_launches;
   return cudaGetLastError();
 }
 
-size_t jacobi_scratch_bytes(int l) { return jacobi_log_bytes(l) + 256 * sizeof(int); }
+size_t jacobi_scratch_bytes(int l) { return jacobi_log_bytes(l) + 256 * sizeof(int); }   // rank[129], prog, done
 
 }  // namespace rsvd
