@@ -552,10 +552,7 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool robus
     Prof pr(ctx, 3, 0);
     CK(launch_jacobi(p.RB, Np, l, p.sigma, p.W, p.J, Np, ctx->flags_dev, ctx->sweeps_dev, p.jlog, ctx->stream));
   }
-  CK(launch_zero_cols(p.J, Np, l, l, Np, ctx->stream));       // keep padding exact zeros
-  CK(launch_fill(p.J + (size_t)l * Np, (int64_t)(Np - l) * Np, 0.0, ctx->stream));
-  CK(launch_zero_cols(p.W, Np, l, l, Np, ctx->stream));
-  CK(launch_fill(p.W + (size_t)l * Np, (int64_t)(Np - l) * Np, 0.0, ctx->stream));
+  // (launch_jacobi leaves the padding of W and J exact zeros)
   // V = Q_B J  (n x Np) into X
   CKS(small_k(ctx, p, p.Z, p.n, p.J, p.X, Np, Np));
   if (!p.trans_input) {

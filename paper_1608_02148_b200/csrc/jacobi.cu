@@ -166,8 +166,12 @@ __device__ void jacobi_replay(const double2* __restrict__ rlog, const int* __res
     }
     __syncthreads();                                   // buf reused by the next chunk
   }
-  if (i < l)
+  if (i < l) {
     for (int p = lane; p < l; p += 32) Jo[i * ldo + __ldcg(rank + p)] = row[p];
+    for (int c = l + lane; c < ldo; c += 32) Jo[i * ldo + c] = 0.0;      // padded columns
+  } else if (i < ldo) {
+    for (int c = lane; c < ldo; c += 32) Jo[i * ldo + c] = 0.0;          // padded rows
+  }
 }
 
 // JG lanes own a column pair; EPL = elements of a column per lane (l <= JG * EPL)
@@ -305,6 +309,11 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
     const double inv = sp > 0.0 ? 1.0 / sp : 1.0;
     for (int i = lane; i < l; i += 32) Wo[i * ldo + rk] = Xs[p * LDX + i] * inv;
   }
+  // padding of the ldo x ldo W outside its leading l x l block: exact zeros
+  for (int e = tid; e < ldo * ldo; e += nt) {
+    const int i = e / ldo, c = e - (e / ldo) * ldo;
+    if (i >= l || c >= l) Wo[e] = 0.0;
+  }
   __syncthreads();                                     // rank_out complete
   if (tid == 0) {
     if (!converged) atomicOr(flag, 2);
@@ -320,7 +329,7 @@ int g_jacobi_lanes = 0;   // lanes per column pair (4, 8, 16; 0: 4 for L <= 64, 
 
 cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double* W, double* J, int ldo,
                           int* flag, int* sweeps, void* scratch, cudaStream_t st) {
-  if (l < 1 || l > 128) return cudaErrorInvalidValue;
+  if (l < 1 || l > 128 || ldo < l || ldo > 128) return cudaErrorInvalidValue;
   const int L = jac_L(l);
   double2* rlog = reinterpret_cast<double2*>(scratch);
   int* rank = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + jacobi_log_bytes(l));
@@ -343,7 +352,7 @@ cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double
       if (e != cudaSuccess) return e;                                                                     \
       attr = true;                                                                                        \
     }                                                                                                     \
-    e = launch_pdl(jacobi_x_kernel<JG, EPL>, dim3(1 + (unsigned)ceil_div(l, threads / 32)), dim3(threads), smem, st, \
+    e = launch_pdl(jacobi_x_kernel<JG, EPL>, dim3(1 + (unsigned)ceil_div(ldo, threads / 32)), dim3(threads), smem, st, \
                    R, ldr, l, sigma, W, ldo, rlog, rank, flag, sweeps, J, prog, done, epoch);               \
     if (e != cudaSuccess) return e; \
   }

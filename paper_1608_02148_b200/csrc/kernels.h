@@ -119,7 +119,8 @@ cudaError_t launch_tsqr_combine(double* Y, int64_t ldy, int64_t M, int l, int64_
                                 const double* S, int64_t lds, cudaStream_t st);
 
 // One-sided Jacobi SVD of X = R^T (R upper l x l, ld ldr): X J = W Sigma (jacobi.cu).
-// Outputs: sigma (l, descending), W (l x l, ld ldo) = U~, J (l x l, ld ldo).
+// Outputs: sigma (l, descending), W (ldo x ldo) = U~, J (ldo x ldo), zero outside
+// their leading l x l blocks (l <= ldo <= 128).
 // flag |= 2 if the sweep cap was hit, 4 on non-finite input.  scratch: device
 // buffer of jacobi_scratch_bytes(l) (rotation log + ranks).
 size_t jacobi_scratch_bytes(int l);
