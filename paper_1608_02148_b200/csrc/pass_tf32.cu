@@ -24,6 +24,7 @@
 // A (16 KB, SWIZZLE_128B; K-major for NN, MN-major for TN), A_lo (16 KB),
 // B_hi, B_lo (N/32 boxes of 4 KB, MN-major).  3 stages.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -291,6 +292,234 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   }
 }
 
+// ---------------------------------------------------------------- TN as Q^T A
+// C^T (N x M) = Q^T (N x K) A (K x M): the panel Q is the M-side operand (its
+// hi / lo FP32 copies, 128 columns, zero-filled beyond N) and 256-column
+// chunks of A are the N side, so the panel is re-read once per 256 columns of
+// A instead of once per 128 (ncu, config 4: 136 GB of DRAM reads per launch
+// for 40 GB of A with the A^T Q form).  Same roles, drains and stream-K
+// fix-up as pass_tf32_kernel; D (128 x 256) double-buffered in all 512 TMEM
+// columns; TMEM lane i = output column i, TMEM column j = output row c0 + j.
+constexpr int TN_BN = 256, TN_STAGES = 2;
+constexpr int TN_Q_BYTES = 128 * BK * 4;             // 16 KB: 4 boxes of 32 columns x 32 k
+constexpr int TN_A_BYTES = TN_BN * BK * 4;           // 32 KB: 8 boxes
+constexpr int TN_STAGE = 2 * TN_Q_BYTES + 2 * TN_A_BYTES;
+
+__global__ void __launch_bounds__(THREADS, 1)
+pass_tf32_tn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapQhi,
+                    const __grid_constant__ CUtensorMap mapQlo, Args g) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[TN_STAGES], splitd[TN_STAGES], empty_[TN_STAGES], accf[2], acce[2];
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t KT = g.KT;
+  const int64_t u_lo = unit_lo(g.units, g.grid, blockIdx.x);
+  const int64_t u_hi = unit_lo(g.units, g.grid, blockIdx.x + 1);
+  const int64_t nun = u_hi - u_lo;
+  if (tid == 0) {
+    for (int s = 0; s < TN_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&splitd[s], 4); mbar_init(&empty_[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&accf[b], 1); mbar_init(&acce[b], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  auto stQh = [&](int s) { return base + (size_t)s * TN_STAGE; };
+  auto stQl = [&](int s) { return base + (size_t)s * TN_STAGE + TN_Q_BYTES; };
+  auto stA = [&](int s) { return base + (size_t)s * TN_STAGE + 2 * TN_Q_BYTES; };
+  auto stAl = [&](int s) { return base + (size_t)s * TN_STAGE + 2 * TN_Q_BYTES + TN_A_BYTES; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int64_t it = 0; it < nun; ++it) {
+        const int s = (int)(it % TN_STAGES);
+        const uint32_t ph = (uint32_t)((it / TN_STAGES) & 1);
+        mbar_wait(&empty_[s], ph ^ 1);
+        const int64_t u = u_lo + it, ct = u / KT, kt = u - ct * KT;
+        const int c0 = (int)(ct * TN_BN), k0 = (int)(kt * BK);
+        mbar_expect_tx(&full[s], (uint32_t)(2 * TN_Q_BYTES + TN_A_BYTES));
+        for (int j = 0; j < 8; ++j) tma_2d(stA(s) + j * B_BOX_BYTES, &mapA, c0 + 32 * j, k0, &full[s]);
+        for (int j = 0; j < 4; ++j) {
+          tma_2d(stQh(s) + j * B_BOX_BYTES, &mapQhi, 32 * j, k0, &full[s]);
+          tma_2d(stQl(s) + j * B_BOX_BYTES, &mapQlo, 32 * j, k0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // D f32, A (= Q^T) tf32 MN-major, B (= A chunk) tf32 MN-major, N = 256, M = 128
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
+                             ((uint32_t)(TN_BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      int64_t run = 0;
+      bool first = true;
+      int in_run = 0;
+      uint32_t acc_t = tmem;
+      for (int64_t it = 0; it < nun; ++it) {
+        const int s = (int)(it % TN_STAGES);
+        const uint32_t ph = (uint32_t)((it / TN_STAGES) & 1);
+        const int64_t u = u_lo + it, kt = u % KT;
+        const bool run_end = (kt == KT - 1) || (it == nun - 1) || (in_run == TF_DRAIN - 1);
+        if (first) {
+          const int b = (int)(run & 1);
+          if (run >= 2) mbar_wait(&acce[b], (uint32_t)(((run - 2) >> 1) & 1));
+          acc_t = tmem + (uint32_t)(b * TN_BN);
+        }
+        mbar_wait(&splitd[s], ph);
+        tc_fence_after();
+        const uint32_t qH = smem_u32(stQh(s)), qL = smem_u32(stQl(s));
+        const uint32_t aH = smem_u32(stA(s)), aL = smem_u32(stAl(s));
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t dQh = sdesc(qH + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
+          const uint64_t dQl = sdesc(qL + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
+          const uint64_t dAh = sdesc(aH + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
+          const uint64_t dAl = sdesc(aL + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
+          const uint32_t acc0 = (first && kk == 0) ? 0u : 1u;
+          mma_tf32(acc_t, dQh, dAh, idesc, acc0);
+          mma_tf32(acc_t, dQl, dAh, idesc, 1u);
+          mma_tf32(acc_t, dQh, dAl, idesc, 1u);
+        }
+        mma_commit(&empty_[s]);
+        first = false;
+        ++in_run;
+        if (run_end) {
+          mma_commit(&accf[run & 1]);
+          ++run;
+          first = true;
+          in_run = 0;
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // A-chunk split (32 KB per unit) into hi (in place) / lo
+    const int et = tid - 128;
+    for (int64_t it = 0; it < nun; ++it) {
+      const int s = (int)(it % TN_STAGES);
+      const uint32_t ph = (uint32_t)((it / TN_STAGES) & 1);
+      mbar_wait(&full[s], ph);
+      float4* a4 = reinterpret_cast<float4*>(stA(s));
+      float4* l4 = reinterpret_cast<float4*>(stAl(s));
+#pragma unroll 4
+      for (int q = et; q < TN_A_BYTES / 16; q += 128) {
+        float4 a = a4[q], hi, lo;
+        hi.x = tf32_trunc(a.x); lo.x = tf32_rna(a.x - hi.x);
+        hi.y = tf32_trunc(a.y); lo.y = tf32_rna(a.y - hi.y);
+        hi.z = tf32_trunc(a.z); lo.z = tf32_rna(a.z - hi.z);
+        hi.w = tf32_trunc(a.w); lo.w = tf32_rna(a.w - hi.w);
+        a4[q] = hi;
+        l4[q] = lo;
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&splitd[s]);
+    }
+  } else if (warp >= 8) {
+    // drains + epilogue: lane i of the TMEM quadrant = output column i
+    const int et = tid - 256;
+    int64_t run = 0;
+    int in_run = 0, sub = 0;
+    const int col = 32 * (warp & 3) + lane;            // output column (< 128)
+    double* pacc = g.Pacc + ((int64_t)blockIdx.x * 128 + col) * TN_BN;
+    for (int64_t it = 0; it < nun; ++it) {
+      const int64_t u = u_lo + it, ct = u / KT, kt = u - ct * KT;
+      const bool seg_end = (kt == KT - 1) || (it == nun - 1);
+      const bool run_end = seg_end || (in_run == TF_DRAIN - 1);
+      ++in_run;
+      if (!run_end) continue;
+      in_run = 0;
+      const int b = (int)(run & 1);
+      mbar_wait(&accf[b], (uint32_t)((run >> 1) & 1));
+      tc_fence_after();
+      const uint32_t tbase = tmem + (uint32_t)(b * TN_BN) + ((uint32_t)(32 * (warp & 3)) << 16);
+      if (!seg_end) {
+        for (int j0 = 0; j0 < TN_BN; j0 += 32) {
+          uint32_t v[32];
+          TMEM_LD32(tbase + (uint32_t)j0, v);
+          TMEM_WAIT_LD(v);
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            double2* pp = reinterpret_cast<double2*>(pacc + j0 + j);
+            const double2 o = sub ? *pp : make_double2(0.0, 0.0);
+            *pp = make_double2(o.x + (double)__uint_as_float(v[j]), o.y + (double)__uint_as_float(v[j + 1]));
+          }
+        }
+        ++sub;
+      } else {
+        const int64_t rb_lo = ct * KT, rb_hi = rb_lo + KT;
+        const int64_t seg_start = (rb_lo > u_lo) ? rb_lo : u_lo;
+        const bool cont = seg_start > rb_lo;
+        const bool head = !cont && (u + 1 < rb_hi);
+        for (int j0 = 0; j0 < TN_BN; j0 += 32) {
+          uint32_t v[32];
+          TMEM_LD32(tbase + (uint32_t)j0, v);
+          TMEM_WAIT_LD(v);
+          double a[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) a[j] = (double)__uint_as_float(v[j]);
+          if (sub) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const double2 o = *reinterpret_cast<const double2*>(pacc + j0 + j);
+              a[j] += o.x;
+              a[j + 1] += o.y;
+            }
+          }
+          if (cont) {
+            double* dst = g.P + ((int64_t)blockIdx.x * 128 + col) * TN_BN + j0;
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(a[j], a[j + 1]);
+          } else {
+            if (head) {
+              for (int c = blockIdx.x + 1; c < g.grid && unit_lo(g.units, g.grid, c) < rb_hi; ++c) {
+                unsigned f;
+                do {
+                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(g.flags + c) : "memory");
+                } while (f != g.epoch);
+                const double* src = g.P + ((int64_t)c * 128 + col) * TN_BN + j0;
+#pragma unroll
+                for (int j = 0; j < 32; j += 2) {
+                  const double2 pv = *reinterpret_cast<const double2*>(src + j);
+                  a[j] += pv.x;
+                  a[j + 1] += pv.y;
+                }
+              }
+            }
+            if (col < g.Nout) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int64_t r = ct * TN_BN + j0 + j;
+                if (r < g.M) g.C[r * g.ldc + col] = a[j];
+              }
+            }
+          }
+        }
+        if (cont) {
+          __threadfence();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (et == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(g.epoch) : "memory");
+        }
+        sub = 0;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[b]);
+      ++run;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+  }
+}
+
 // X (K x Np, FP64, ld ldx) -> Xhi, Xlo (K x N, FP32, row-major, zero-padded columns)
 __global__ void prep_split_b(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, int N,
                              float* __restrict__ hi, float* __restrict__ lo) {
@@ -346,7 +575,10 @@ bool tf32_pass_supported(const void* A, int64_t lda) {
 
 int tf32_n(int Np) { return (int)round_up(Np, 32); }
 
-size_t tf32_partial_bytes(int Np, int num_sms) { return 2 * (size_t)num_sms * 128 * tf32_n(Np) * sizeof(double); }
+size_t tf32_partial_bytes(int Np, int num_sms) {
+  // NN: [grid][128][N] partials + drain sums; TN (Q^T A form): [grid][128][256] each
+  return 2 * (size_t)num_sms * 128 * (tf32_n(Np) > 256 ? tf32_n(Np) : 256) * sizeof(double);
+}
 
 size_t tf32_split_bytes(int64_t K, int Np) { return 2 * (size_t)K * tf32_n(Np) * sizeof(float); }
 
@@ -376,6 +608,24 @@ cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st) {
   g.flags = c.flags; g.epoch = c.epoch;
   if (c.flags == nullptr) return cudaErrorInvalidValue;
   g.KT = ceil_div(c.K, BK);
+  static const bool tn_qta = [] { const char* e = getenv("RSVD_TF32_TN"); return !(e && e[0] == '0'); }();
+  if (c.trans && tn_qta) {
+    // C^T = Q^T A with 256-column chunks of A (pass_tf32_tn_kernel)
+    const int64_t ctiles = ceil_div(c.M, (int64_t)TN_BN);
+    g.units = ctiles * g.KT;
+    int64_t grid = g.units / 8;
+    if (grid < ctiles) grid = ctiles;
+    if (grid > c.grid) grid = c.grid;
+    if (grid < 1) grid = 1;
+    g.grid = (int)grid;
+    g.Pacc = c.P + (size_t)c.grid * 128 * TN_BN;
+    const size_t smem = (size_t)TN_STAGES * TN_STAGE + 1024;
+    cudaError_t e = cudaFuncSetAttribute(pass_tf32_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    pass_tf32_tn_kernel<<<g.grid, THREADS, smem, st>>>(mA, mBh, mBl, g);
+    ++g_kernel_launches;
+    return cudaGetLastError();
+  }
   const int64_t mblocks = ceil_div(c.M, BM);
   g.units = mblocks * g.KT;
   int64_t grid = g.units / 8;
