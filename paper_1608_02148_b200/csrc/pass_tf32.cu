@@ -305,6 +305,9 @@ constexpr int TN_Q_BYTES = 128 * BK * 4;             // 16 KB: 4 boxes of 32 col
 constexpr int TN_A_BYTES = TN_BN * BK * 4;           // 32 KB: 8 boxes
 constexpr int TN_STAGE = 2 * TN_Q_BYTES + 2 * TN_A_BYTES;
 
+// NN = true: the same with C^T = X^T A^T -- 256-row chunks of A (K-major, one
+// TMA box) as the N-side operand, so the panel tile is shared by 256 rows.
+template <bool NN>
 __global__ void __launch_bounds__(THREADS, 1)
 pass_tf32_tn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapQhi,
                     const __grid_constant__ CUtensorMap mapQlo, Args g) {
@@ -344,7 +347,9 @@ pass_tf32_tn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         const int64_t u = u_lo + it, ct = u / KT, kt = u - ct * KT;
         const int c0 = (int)(ct * TN_BN), k0 = (int)(kt * BK);
         mbar_expect_tx(&full[s], (uint32_t)(2 * TN_Q_BYTES + TN_A_BYTES));
-        for (int j = 0; j < 8; ++j) tma_2d(stA(s) + j * B_BOX_BYTES, &mapA, c0 + 32 * j, k0, &full[s]);
+        if (NN) tma_2d(stA(s), &mapA, k0, c0, &full[s]);                      // box {32 k, 256 rows}, K-major
+        else
+          for (int j = 0; j < 8; ++j) tma_2d(stA(s) + j * B_BOX_BYTES, &mapA, c0 + 32 * j, k0, &full[s]);
         for (int j = 0; j < 4; ++j) {
           tma_2d(stQh(s) + j * B_BOX_BYTES, &mapQhi, 32 * j, k0, &full[s]);
           tma_2d(stQl(s) + j * B_BOX_BYTES, &mapQlo, 32 * j, k0, &full[s]);
@@ -354,7 +359,7 @@ pass_tf32_tn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
   } else if (warp == 1) {
     if (lane == 0) {
       // D f32, A (= Q^T) tf32 MN-major, B (= A chunk) tf32 MN-major, N = 256, M = 128
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | ((NN ? 0u : 1u) << 16) |
                              ((uint32_t)(TN_BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       int64_t run = 0;
       bool first = true;
@@ -378,8 +383,14 @@ pass_tf32_tn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         for (int kk = 0; kk < BK / 8; ++kk) {
           const uint64_t dQh = sdesc(qH + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
           const uint64_t dQl = sdesc(qL + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
-          const uint64_t dAh = sdesc(aH + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
-          const uint64_t dAl = sdesc(aL + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
+          uint64_t dAh, dAl;
+          if (NN) {   // K-major chunk: 32 B per 8-wide k step inside the 128 B swizzle row
+            dAh = sdesc(aH + kk * 32, 16, 1024);
+            dAl = sdesc(aL + kk * 32, 16, 1024);
+          } else {
+            dAh = sdesc(aH + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
+            dAl = sdesc(aL + kk * 1024, B_BOX_BYTES, 512, LAYOUT_SW128_BASE32B);
+          }
           const uint32_t acc0 = (first && kk == 0) ? 0u : 1u;
           mma_tf32(acc_t, dQh, dAh, idesc, acc0);
           mma_tf32(acc_t, dQl, dAh, idesc, 1u);
@@ -609,8 +620,10 @@ cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st) {
   if (c.flags == nullptr) return cudaErrorInvalidValue;
   g.KT = ceil_div(c.K, BK);
   static const bool tn_qta = [] { const char* e = getenv("RSVD_TF32_TN"); return !(e && e[0] == '0'); }();
-  if (c.trans && tn_qta) {
-    // C^T = Q^T A with 256-column chunks of A (pass_tf32_tn_kernel)
+  static const bool nn_xta = [] { const char* e = getenv("RSVD_TF32_NN"); return !(e && e[0] == '0'); }();
+  if ((c.trans && tn_qta) || (!c.trans && nn_xta)) {
+    // C^T = Q^T A (TN) / X^T A^T (NN) with 256-column (row) chunks of A (pass_tf32_tn_kernel)
+    if (!c.trans && !make_map(&mA, c.A, c.M, c.K, c.lda, 32, TN_BN, false)) return cudaErrorInvalidValue;
     const int64_t ctiles = ceil_div(c.M, (int64_t)TN_BN);
     g.units = ctiles * g.KT;
     int64_t grid = g.units / 8;
@@ -620,9 +633,16 @@ cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st) {
     g.grid = (int)grid;
     g.Pacc = c.P + (size_t)c.grid * 128 * TN_BN;
     const size_t smem = (size_t)TN_STAGES * TN_STAGE + 1024;
-    cudaError_t e = cudaFuncSetAttribute(pass_tf32_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    pass_tf32_tn_kernel<<<g.grid, THREADS, smem, st>>>(mA, mBh, mBl, g);
+    cudaError_t e;
+    if (c.trans) {
+      e = cudaFuncSetAttribute(pass_tf32_tn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      pass_tf32_tn_kernel<false><<<g.grid, THREADS, smem, st>>>(mA, mBh, mBl, g);
+    } else {
+      e = cudaFuncSetAttribute(pass_tf32_tn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      pass_tf32_tn_kernel<true><<<g.grid, THREADS, smem, st>>>(mA, mBh, mBl, g);
+    }
     ++g_kernel_launches;
     return cudaGetLastError();
   }
