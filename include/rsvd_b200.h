@@ -201,8 +201,8 @@ rsvd_status rsvd_omega(rsvd_ctx* ctx, int64_t n, int64_t l, int32_t sdist, uint6
                        uint64_t stream, int32_t dtype, void* out, int64_t ldo);
 
 /* Per-kernel timing of the last calls (CUDA events on the context stream,
- * enabled by rsvd_set_profiling(ctx, 1); 2 = only the pass kernels, kinds
- * 0, 1, 6, for the least event overhead).  kind: 0 = sketch/power pass A.X,
+ * enabled by rsvd_set_profiling(ctx, 1); 2 = only the pass kernels, kind 0
+ * on one call and kind 1 on the next, for the least event overhead).  kind: 0 = sketch/power pass A.X,
  * 1 = transposed pass A^T.X (incl. its split reduction), 2 = panel
  * orthonormalisation, 3 = small SVD, 4 = other, 5 = Ozaki slicing of A
  * (FP64 inputs on the tensor-core path, once per call), 6 = Ozaki slicing of

@@ -65,6 +65,7 @@ struct rsvd_ctx {
   int nranks = 1, rank = 0;
   // profiling
   int prof = 0;                   // 0 off, 1 every kind, 2 the pass kernels only (kinds 0, 1, 6)
+  int prof_phase = 0;             // level 2: the pass kind (0 / 1) timed in this call, alternating per call
   bool debug = getenv("RSVD_DEBUG") != nullptr;
   std::vector<ProfRec> pending;
   std::vector<cudaEvent_t> pool;
@@ -125,7 +126,7 @@ struct Prof {
   Prof(rsvd_ctx* c_, int k, double b) : c(c_), kind(k), bytes(b) {
     if (on()) { a = take_event(c); cudaEventRecord(a, c->stream); }
   }
-  bool on() const { return c->prof == 1 || (c->prof == 2 && (kind == 0 || kind == 1 || kind == 6)); }
+  bool on() const { return c->prof == 1 || (c->prof == 2 && kind == c->prof_phase); }
   ~Prof() {
     if (on()) {
       cudaEvent_t b2 = take_event(c);
@@ -276,7 +277,7 @@ rsvd_status pass_ozaki(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, doub
   o.xscratch = p.ozx; o.xscratch2 = p.ozx2;
   o.M = M; o.K = K; o.N = p.Np; o.grid = ctx->num_sms;
   ++ctx->ozaki_calls;
-  if (!ctx->prof) {
+  if (!ctx->prof || (ctx->prof == 2 && kind != ctx->prof_phase)) {
     CK(ozaki_pass(o, ctx->stream));
     return RSVD_OK;
   }
@@ -488,6 +489,7 @@ rsvd_status validate(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm
 // p.W (= U~ diag(sgn), Np x Np), p.sigma.  Returns flags via ctx->flags_dev.
 rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool robust, bool want_svd) {
   const int l = p.l, Np = p.Np;
+  ctx->prof_phase ^= 1;           // level-2 profiling samples A.X and A^T.X passes on alternate calls
   const bool dist = ctx->nranks > 1;
   const bool centred = prm->center != 0 || prm->scale != 0;
   CK(cudaMemsetAsync(ctx->flags_dev, 0, sizeof(int) * 4, ctx->stream));
