@@ -211,17 +211,21 @@ def main():
     is_rrpca = bool(meta.get("rrpca"))
     rr_state = {}
 
-    def step():
+    def step(Ain=A):
+        """One call of the public API on Ain; returns the result tensors (device)."""
         if is_rrpca:
-            out = rb.rrpca(A, k=k, p=p, q=q, tol=meta["tol"], maxiter=100, sdist=meta["sdist"],
+            out = rb.rrpca(Ain, k=k, p=p, q=q, tol=meta["tol"], maxiter=100, sdist=meta["sdist"],
                            seed=meta["seed_omega"], ctx=ctx, m_global=m, row_offset=meta["row_offset"])
             rr_state["iters"] = out["iters"]
             rr_state["residual"] = out["residual"]
+            return [out["L"], out["S"]]
         elif center:
-            rb.rpca(A, k, center=True, p=p, q=q, sdist=meta["sdist"], seed=meta["seed_omega"], ctx=ctx,
-                    m_global=m, row_offset=meta["row_offset"])
+            out = rb.rpca(Ain, k, center=True, p=p, q=q, sdist=meta["sdist"], seed=meta["seed_omega"], ctx=ctx,
+                          m_global=m, row_offset=meta["row_offset"])
+            return [out["rotation"], out["eigvals"], out["x"]]
         else:
-            rb.rsvd(A, k, out=(d, u, v), **kw)
+            rb.rsvd(Ain, k, out=(d, u, v), **kw)
+            return [d, u, v]
 
     for _ in range(args.warmup):
         step()
@@ -342,20 +346,21 @@ def main():
             "diagnostics": diag}
 
     # end-to-end: host A (pinned) -> device, rsvd, d/u/v -> host, through the same API
-    if not args.no_e2e and world == 1 and not center and not is_rrpca:
+    # (rsvd: d, u, v; rpca: rotation, eigenvalues, scores; rrpca: L and S)
+    if not args.no_e2e and world == 1:
         A_host = A.cpu().pin_memory()
         stage = torch.empty_like(A)
-        d_h = torch.empty(k, dtype=A.dtype).pin_memory()
-        u_h = torch.empty(m_loc, k, dtype=A.dtype).pin_memory()
-        v_h = torch.empty(n, k, dtype=A.dtype).pin_memory()
+        res_h = []
         e2e_steps = max(3, min(args.steps, 20))
 
         def e2e_step():
             stage.copy_(A_host, non_blocking=True)
-            rb.rsvd(stage, k, out=(d, u, v), **kw)
-            d_h.copy_(d, non_blocking=True)
-            u_h.copy_(u, non_blocking=True)
-            v_h.copy_(v, non_blocking=True)
+            res = step(stage)
+            if not res_h:
+                res_h.extend(torch.empty(r.shape, dtype=r.dtype).pin_memory() for r in res)
+            for h, r in zip(res_h, res):
+                h.copy_(r, non_blocking=True)
+            return res
 
         for _ in range(2):
             e2e_step()
@@ -366,10 +371,12 @@ def main():
         e1.record(st)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1) / e2e_steps
-        line["e2e"] = {"value": round(passes * a_bytes / (ems * 1e-3) / 1e9, 2), "unit": "GB/s",
+        line["e2e"] = {"value": round(step_bytes / (ems * 1e-3) / 1e9, 2), "unit": "GB/s",
                        "ms_per_step": round(ems, 3), "steps": e2e_steps,
                        "h2d_bytes_per_step": int(a_bytes),
-                       "d2h_bytes_per_step": int((k + m_loc * k + n * k) * es)}
+                       "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in res_h)),
+                       "results": "rrpca L, S" if is_rrpca else ("rpca rotation, eigvals, x" if center
+                                                                else "rsvd d, u, v")}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not is_rrpca and m * n <= 2e8:
         t_cpu, b_cpu, reps, shape = cpu_baseline_run(A.cpu().numpy(), meta)
