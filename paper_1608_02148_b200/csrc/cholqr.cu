@@ -281,22 +281,32 @@ chol_blk_kernel(const double* __restrict__ G, int ldg, int l, int npad, double* 
   CB_PROBE_DECL
   if (tid == 0) bad = 0;
   // load: upper blocks of G (mirrored from the upper triangle), identity padding;
-  // two consecutive columns per thread
-#pragma unroll 8
-  for (int e = tid; e < NG * NG / 2; e += 256) {
+  // two consecutive columns per thread.  All of a thread's loads are issued
+  // before its first shared store (one L2 round trip, not one per element pair).
+  constexpr int NLD = (NG * NG / 2 + 255) / 256;
+  double v0[NLD], v1[NLD];
+#pragma unroll
+  for (int r = 0; r < NLD; ++r) {
+    const int e = tid + 256 * r;
     const int i = e / (NG / 2), j = 2 * (e - i * (NG / 2));
-    double v0 = 0.0, v1 = 0.0;
-    if ((i >> 4) <= (j >> 4)) {
+    v0[r] = 0.0; v1[r] = 0.0;
+    if (e < NG * NG / 2 && (i >> 4) <= (j >> 4)) {
       if (i < l) {
-        if (j < l) v0 = (j >= i) ? G[i * ldg + j] : G[j * ldg + i];
-        if (j + 1 < l) v1 = (j + 1 >= i) ? G[i * ldg + j + 1] : G[(j + 1) * ldg + i];
+        if (j < l) v0[r] = (j >= i) ? G[i * ldg + j] : G[j * ldg + i];
+        if (j + 1 < l) v1[r] = (j + 1 >= i) ? G[i * ldg + j + 1] : G[(j + 1) * ldg + i];
       }
-      if (i >= l && i == j) v0 = 1.0;
-      if (i >= l && i == j + 1) v1 = 1.0;
+      if (i >= l && i == j) v0[r] = 1.0;
+      if (i >= l && i == j + 1) v1[r] = 1.0;
     }
-    *reinterpret_cast<double2*>(M + i * LDM + j) = make_double2(v0, v1);
-    if (i == j) d0[i] = (i < l) ? v0 : 1.0;
-    if (i == j + 1) d0[i] = (i < l) ? v1 : 1.0;
+  }
+#pragma unroll
+  for (int r = 0; r < NLD; ++r) {
+    const int e = tid + 256 * r;
+    if (e >= NG * NG / 2) break;
+    const int i = e / (NG / 2), j = 2 * (e - i * (NG / 2));
+    *reinterpret_cast<double2*>(M + i * LDM + j) = make_double2(v0[r], v1[r]);
+    if (i == j) d0[i] = (i < l) ? v0[r] : 1.0;
+    if (i == j + 1) d0[i] = (i < l) ? v1[r] : 1.0;
   }
   __syncthreads();
   if (warp == 0) chol_diag16(M, LDM, Ld, CB_LDB, d0, lane, &bad);

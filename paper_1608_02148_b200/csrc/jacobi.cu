@@ -199,12 +199,22 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
   if (tid == 0) { rotated = 0; bad = 0; }
   __syncthreads();
   // X = R^T: column p of X = row p of R (upper: entries i >= p); rows/columns >= l are zero
-  for (int e = tid; e < L * LDX; e += nt) {
-    const int p = e / LDX, i = e - p * LDX;
-    double v = 0.0;
-    if (p < l && i < l && i >= p) v = R[p * ldr + i];
-    if (!isfinite(v)) bad = 1;
-    Xs[e] = v;
+  // (eight independent loads in flight per thread before the shared stores)
+  for (int e0 = tid; e0 < L * LDX; e0 += 8 * nt) {
+    double v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = e0 + r * nt, p = e / LDX, i = e - p * LDX;
+      v[r] = (e < L * LDX && p < l && i < l && i >= p) ? R[p * ldr + i] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = e0 + r * nt;
+      if (e < L * LDX) {
+        if (!isfinite(v[r])) bad = 1;
+        Xs[e] = v[r];
+      }
+    }
   }
   __syncthreads();
   const double tol = (double)l * 0x1.0p-52, tol2 = tol * tol;
