@@ -73,7 +73,7 @@ cudaError_t ozaki_slice_a(const OzakiA& a, const double* A, int64_t lda, const d
                           cudaStream_t st);
 struct OzakiCall {
   const OzakiA* a; bool trans;                   // trans: C = f(A)^T B (M = n, K = m), else C = f(A) B
-  const double* B; int64_t ldb;                  // K x N panel (FP64), N = Np <= 128 (two launches above 64)
+  const double* B; int64_t ldb;                  // K x N panel (FP64), N = Np <= 128 (two 64-column halves above 64)
   double* C; int64_t ldc; int Nout;
   double* P; unsigned* flags; unsigned epoch;    // stream-K partials / flags as GemmCall
   unsigned epoch2;                               // second column block (N > 64)

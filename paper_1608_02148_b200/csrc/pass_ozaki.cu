@@ -66,6 +66,22 @@ __device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c0
       ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
+// A-slice tile multicast into both CTAs of a 2-CTA cluster (same smem offset;
+// each CTA's mbarrier at the same offset receives the bytes)
+__device__ __forceinline__ void tma_4d_mc(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar,
+                                          uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -245,6 +261,8 @@ struct Args {
   const double* xf;                                 // 2^E per (k-block, column) of X
   int64_t M, K; int N, Nout, Np;
   int64_t KB, units; int grid;
+  // CL = 2 (Np = 128): the second CTA of each pair computes columns [64, 128)
+  double* C2; const double* xf2; int Nout2;
 };
 
 // One unit = (128-row output block, 64-k block): 8 A-slice tiles (128 x 64 B)
@@ -257,9 +275,15 @@ constexpr int A_UT = BM * BKU;                      // bytes of one A-slice tile
 __host__ __device__ constexpr int oz_ubuf(int S, int N) { return (S * A_UT + S * N * BKU + 1023) / 1024 * 1024; }
 __host__ __device__ constexpr int oz_nbuf(int S, int N) { return 3 * oz_ubuf(S, N) + 1024 <= 219 * 1024 ? 3 : 2; }
 
-template <bool TRANS, int S, int N>
+// CL = 2 (Np = 128 as two 64-column halves in one launch): the CTAs of a
+// 2-CTA cluster take the same units in lock step, CTA r computing columns
+// [64 r, 64 r + 64) from its own X slices; each loads half of the unit's A
+// slice tiles and multicasts them to both, so A's slices are read once per
+// pass instead of once per column half.  Stream-K runs over the pairs.
+template <bool TRANS, int S, int N, int CL>
 __global__ void __launch_bounds__(THREADS, 1)
-ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapX, Args g) {
+ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapX,
+                  const __grid_constant__ CUtensorMap mapX2, Args g) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -273,12 +297,17 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t KB = g.KB;                          // 64-k blocks
-  const int64_t u_lo = unit_lo(g.units, g.grid, blockIdx.x);
-  const int64_t u_hi = unit_lo(g.units, g.grid, blockIdx.x + 1);
+  const int crank = CL == 2 ? (int)(blockIdx.x & 1) : 0;   // rank in the cluster = column half
+  const int pid = (int)blockIdx.x / CL, npair = g.grid / CL;
+  const int64_t u_lo = unit_lo(g.units, npair, pid);
+  const int64_t u_hi = unit_lo(g.units, npair, pid + 1);
   const int64_t nun = u_hi - u_lo;
+  double* const Cout = crank ? g.C2 : g.C;
+  const double* const xfh = crank ? g.xf2 : g.xf;
+  const int Nout = crank ? g.Nout2 : g.Nout;
 
   if (tid == 0) {
-    for (int s = 0; s < NB; ++s) { mbar_init(&ufull[s], 1); mbar_init(&uempty[s], 1); }
+    for (int s = 0; s < NB; ++s) { mbar_init(&ufull[s], 1); mbar_init(&uempty[s], CL); }
     mbar_init(&accf, 1);
     mbar_init(&acce, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -288,7 +317,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  if (CL == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base;
 
@@ -304,12 +333,25 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         mbar_wait(&uempty[ub], (uint32_t)(((it / NB) & 1) ^ 1));
         OZ_PROBE2(1)
         mbar_expect_tx(&ufull[ub], (uint32_t)(S * A_UT + S * XSL));
-        for (int t = 0; t < S; ++t) {
-          if (!TRANS) tma_4d(ubuf + t * A_UT, &mapA, (int)((kb & 1) * BKU), t, (int)(kb >> 1), (int)(mb * BM), &ufull[ub]);
-          else tma_4d(ubuf + t * A_UT, &mapA, 0, t, (int)mb, (int)(kb * BKU), &ufull[ub]);
+        if (CL == 1) {
+          for (int t = 0; t < S; ++t) {
+            if (!TRANS) tma_4d(ubuf + t * A_UT, &mapA, (int)((kb & 1) * BKU), t, (int)(kb >> 1), (int)(mb * BM), &ufull[ub]);
+            else tma_4d(ubuf + t * A_UT, &mapA, 0, t, (int)mb, (int)(kb * BKU), &ufull[ub]);
+          }
+        } else {
+          for (int t = crank; t < S; t += 2) {
+            if (!TRANS)
+              tma_4d_mc(ubuf + t * A_UT, &mapA, (int)((kb & 1) * BKU), t, (int)(kb >> 1), (int)(mb * BM), &ufull[ub], (uint16_t)3);
+            else tma_4d_mc(ubuf + t * A_UT, &mapA, 0, t, (int)mb, (int)(kb * BKU), &ufull[ub], (uint16_t)3);
+          }
         }
-        for (int t = 0; t < S; ++t) tma_2d(ubuf + S * A_UT + t * XSL, &mapX, (int)(kb * BKU), t * g.Np, &ufull[ub]);
+        const CUtensorMap* mx = crank ? &mapX2 : &mapX;
+        for (int t = 0; t < S; ++t) tma_2d(ubuf + S * A_UT + t * XSL, mx, (int)(kb * BKU), t * g.Np, &ufull[ub]);
         OZ_PROBE2(2)
+      }
+      if (CL == 2) {
+        // the peer's commits for the last units must have landed before this CTA exits
+        for (int64_t it = nun > NB ? nun - NB : 0; it < nun; ++it) mbar_wait(&uempty[it % NB], (uint32_t)((it / NB) & 1));
       }
       OZ_PROBE2(0)
       OZ_PROBE2_OUT
@@ -358,7 +400,8 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
           }
         }
         OZ_PROBE(4)
-        mma_commit(&uempty[ub]);
+        if (CL == 1) mma_commit(&uempty[ub]);
+        else mma_commit_mc(&uempty[ub], (uint16_t)3);
         if (drain) { mma_commit(&accf); ++ndrain; }
         fresh = drain;
       }
@@ -380,7 +423,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       if (!((kb % KSU == KSU - 1) || kb == KB - 1 || it == nun - 1)) continue;
       const int64_t sb = kb / KSU, sm_ = mb * BM / ET;      // super-block along k, super-tile along m
       const double eaf = TRANS ? g.ea[sb * g.ea_ld + sm_] : g.ea[sm_ * g.ea_ld + sb];
-      for (int j = lane; j < N; j += 32) xfs[j] = eaf * g.xf[sb * g.Np + j];
+      for (int j = lane; j < N; j += 32) xfs[j] = eaf * xfh[sb * g.Np + j];
       __syncwarp();
       OZ_PROBE3(0)
       mbar_wait(&accf, (uint32_t)(ndrain & 1));
@@ -427,7 +470,8 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
           if (et == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(g.epoch) : "memory");
         } else {
           if (head) {
-            for (int cc = blockIdx.x + 1; cc < g.grid && unit_lo(g.units, g.grid, cc) < rb_hi; ++cc) {
+            for (int pc = pid + 1; pc < npair && unit_lo(g.units, npair, pc) < rb_hi; ++pc) {
+              const int cc = pc * CL + crank;
               unsigned f;
               do {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(g.flags + cc) : "memory");
@@ -442,10 +486,10 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
             }
           }
           if (gm < g.M) {
-            double* dst = g.C + gm * g.ldc;
+            double* dst = Cout + gm * g.ldc;
 #pragma unroll
             for (int j = 0; j < N; ++j)
-              if (j < g.Nout) dst[j] = acc[j];
+              if (j < Nout) dst[j] = acc[j];
           }
         }
 #pragma unroll
@@ -457,7 +501,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
     OZ_PROBE3_OUT
   }
   tc_fence_before();
-  __syncthreads();
+  if (CL == 2) cluster_sync_all(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
@@ -496,8 +540,8 @@ static bool map_i8_2d(CUtensorMap* mp, const int8_t* p, int64_t cols, int64_t ro
 
 int ozaki_slices() { return OZ_S; }
 
-// Np <= 64 in one launch; 64 < Np <= 128 as two column blocks (64, Np - 64),
-// each its own launch over the same A slices (TMEM holds 8 groups x 64 columns)
+// Np <= 64 in one launch; 64 < Np <= 128 as two column blocks (64, Np - 64):
+// at Np = 128 one launch of CTA pairs (ozaki_pass_pair), else two launches over the same A slices (TMEM holds 8 groups x 64 columns)
 bool ozaki_supported(int Np) { return Np <= 128 && Np % 16 == 0 && tc::get_encode() != nullptr; }
 
 size_t ozaki_a_bytes(int64_t m, int64_t n) {
@@ -536,6 +580,7 @@ OzakiA ozaki_layout_a(void* buf, int64_t m, int64_t n) {
 
 static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st);
 static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st);
+static cudaError_t ozaki_pass_pair(const OzakiCall& h0, const OzakiCall& h1, cudaStream_t st);
 
 // X slicing of every column block first, then the pass kernel(s): c.mark (if
 // set) separates the two in time for the per-kernel profile.
@@ -554,6 +599,9 @@ cudaError_t ozaki_pass(const OzakiCall& c, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   if (c.mark) cudaEventRecord(c.mark, st);
   if (c.mark2) cudaEventRecord(c.mark2, st);
+  // Np = 128: both halves in one launch of CTA pairs sharing A (RSVD_OZ_PAIR=0: two launches)
+  static const int env_pair = [] { const char* v = getenv("RSVD_OZ_PAIR"); return v ? atoi(v) : 1; }();
+  if (two && c.N == 128 && h1.Nout > 0 && env_pair != 0 && c.grid >= 2) return ozaki_pass_pair(h0, h1, st);
   e = ozaki_pass_cols(h0, st);
   if (e == cudaSuccess && two && h1.Nout > 0) e = ozaki_pass_cols(h1, st);
   return e;
@@ -615,11 +663,11 @@ static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
   {                                                                                                      \
     static bool attr = false;                                                                            \
     if (!attr) {                                                                                         \
-      e = cudaFuncSetAttribute(ozaki_pass_kernel<TR, OZ_S, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); \
+      e = cudaFuncSetAttribute(ozaki_pass_kernel<TR, OZ_S, NN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); \
       if (e != cudaSuccess) return e;                                                                    \
       attr = true;                                                                                       \
     }                                                                                                    \
-    e = launch_pdl(ozaki_pass_kernel<TR, OZ_S, NN>, dim3(g.grid), dim3(THREADS), smem, st, mA, mX, g);      \
+    e = launch_pdl(ozaki_pass_kernel<TR, OZ_S, NN, 1>, dim3(g.grid), dim3(THREADS), smem, st, mA, mX, mX, g); \
     if (e != cudaSuccess) return e;                                                                      \
   }
   if (!c.trans) {
@@ -630,6 +678,53 @@ static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
                  case 48: RSVD_OZ(true, 48) break; default: RSVD_OZ(true, 64) break; }
   }
 #undef RSVD_OZ
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+// Np = 128: one launch of 2-CTA clusters, CTA r of a pair computing column
+// half r (h0 / h1, each sliced into its own X scratch) over the same units.
+static cudaError_t ozaki_pass_pair(const OzakiCall& h0, const OzakiCall& h1, cudaStream_t st) {
+  using namespace oz;
+  const OzakiA& a = *h0.a;
+  constexpr int N = 64;
+  const int64_t ldk = round_up(h0.K, 16);
+  int8_t* xs0 = reinterpret_cast<int8_t*>(h0.xscratch);
+  int8_t* xs1 = reinterpret_cast<int8_t*>(h1.xscratch);
+  const double* xf0 = reinterpret_cast<const double*>(reinterpret_cast<char*>(h0.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
+  const double* xf1 = reinterpret_cast<const double*>(reinterpret_cast<char*>(h1.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
+  CUtensorMap mA, mX0, mX1;
+  if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, OZ_S, h0.trans)) return cudaErrorInvalidValue;
+  if (!map_i8_2d(&mX0, xs0, h0.K, (int64_t)OZ_S * N, ldk, N) || !map_i8_2d(&mX1, xs1, h1.K, (int64_t)OZ_S * N, ldk, N))
+    return cudaErrorInvalidValue;
+  Args g{};
+  g.C = h0.C; g.ldc = h0.ldc; g.P = h0.P; g.flags = h0.flags; g.epoch = h0.epoch;
+  g.ea = a.ea; g.ea_ld = a.ntiles; g.xf = xf0;
+  g.C2 = h1.C; g.xf2 = xf1; g.Nout2 = h1.Nout;
+  g.M = h0.M; g.K = h0.K; g.N = N; g.Nout = h0.Nout; g.Np = N;
+  g.KB = ceil_div(h0.K, BKU);
+  const int64_t mblocks = ceil_div(h0.M, BM);
+  g.units = mblocks * g.KB;
+  int64_t npair = g.units / 4;
+  if (npair < mblocks) npair = mblocks;
+  if (npair > h0.grid / 2) npair = h0.grid / 2;
+  if (npair < 1) npair = 1;
+  g.grid = (int)(2 * npair);
+  const size_t smem = (size_t)oz_nbuf(OZ_S, N) * oz_ubuf(OZ_S, N) + 1024;
+  cudaError_t e = cudaSuccess;
+#define RSVD_OZP(TR)                                                                                      \
+  {                                                                                                      \
+    static bool attr = false;                                                                            \
+    if (!attr) {                                                                                         \
+      e = cudaFuncSetAttribute(ozaki_pass_kernel<TR, OZ_S, N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); \
+      if (e != cudaSuccess) return e;                                                                    \
+      attr = true;                                                                                       \
+    }                                                                                                    \
+    e = launch_pdl_cluster(ozaki_pass_kernel<TR, OZ_S, N, 2>, dim3(g.grid), dim3(THREADS), smem, st, 2u, mA, mX0, mX1, g); \
+    if (e != cudaSuccess) return e;                                                                      \
+  }
+  if (!h0.trans) RSVD_OZP(false) else RSVD_OZP(true)
+#undef RSVD_OZP
   ++g_kernel_launches;
   return cudaGetLastError();
 }
