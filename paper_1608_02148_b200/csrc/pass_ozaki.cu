@@ -541,7 +541,7 @@ static bool map_i8_2d(CUtensorMap* mp, const int8_t* p, int64_t cols, int64_t ro
 int ozaki_slices() { return OZ_S; }
 
 // Np <= 64 in one launch; 64 < Np <= 128 as two column blocks (64, Np - 64):
-// at Np = 128 one launch of CTA pairs (ozaki_pass_pair), else two launches over the same A slices (TMEM holds 8 groups x 64 columns)
+// at Np = 128 one launch of CTA pairs (ozaki_pass_pair), else two launches over the same A slices (TMEM holds 7 groups x 64 columns)
 bool ozaki_supported(int Np) { return Np <= 128 && Np % 16 == 0 && tc::get_encode() != nullptr; }
 
 size_t ozaki_a_bytes(int64_t m, int64_t n) {
