@@ -1,6 +1,7 @@
 """CPU-side checks of the C-ABI library: it builds for sm_100a, loads, and
 exports every function include/rsvd_b200.h declares (no compute calls: there
-is no GPU here).  Plus the SASS evidence that the passes use DMMA."""
+is no GPU here).  Plus the SASS evidence for the tensor-core (tcgen05 i8 /
+tf32, DMMA) and TMA paths, and that a missing library is an error."""
 import ctypes
 import os
 import re
@@ -70,9 +71,13 @@ int main(void) {
     assert got == want
 
 
-def test_sass_uses_fp64_tensor_mma(so_path):
+def test_sass_uses_tensor_cores_and_tma(so_path):
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", so_path], capture_output=True, text=True).stdout
-    assert "DMMA.8x8x4" in out
+    assert "UTCIMMA" in out                  # tcgen05.mma kind::i8 (Ozaki FP64 passes)
+    assert "UTCHMMA" in out                  # tcgen05.mma kind::tf32 (3xTF32 FP32 passes)
+    assert "UTMALDG.4D" in out and "UTMALDG.2D" in out            # TMA tile loads
+    assert "UTMALDG.4D.MULTICAST" in out and "UTCBAR.MULTICAST" in out   # 2-CTA paired pass (Np = 128)
+    assert "DMMA.8x8x4" in out               # FP64 DMMA (Cholesky blocks, panel products)
     assert "LDGSTS" in out
     assert "sm_100a" in subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", so_path],
                                        capture_output=True, text=True).stdout
@@ -86,3 +91,17 @@ def test_product_path_does_not_import_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"(#.*|//.*)", "", txt).lower() or f == "__init__.py" and \
                     "import oracle" not in txt, f
+
+
+def test_missing_library_raises(tmp_path):
+    """No CPU fallback: without the built library the binding refuses to run."""
+    code = ("import paper_1608_02148_b200 as rb\n"
+            "rb.LIB_PATH = %r\n"
+            "rb._lib = None\n"
+            "try:\n"
+            "    rb.lib()\n"
+            "except ImportError as e:\n"
+            "    print('raised', e)\n" % str(tmp_path / "missing.so"))
+    out = subprocess.run(["python", "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "raised" in out.stdout and "not built" in out.stdout
