@@ -306,7 +306,7 @@ cudaError_t launch_small_matmul(const double* A, const double* B, double* C, int
 }
 
 // ------------------------------------------------------------------ Householder leaves
-constexpr int HQR_THREADS = 512;
+constexpr int HQR_THREADS = 1024;
 
 // rows of one leaf held in shared memory: b l + l (tau) + 32 (reduction / sign
 // bits) doubles; at l = 120 this is 240 = 2 l, so two R factors always combine
