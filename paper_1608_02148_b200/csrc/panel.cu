@@ -329,9 +329,20 @@ __global__ void __launch_bounds__(HQR_THREADS) hqr_leaves_kernel(double* __restr
   unsigned* sgn = reinterpret_cast<unsigned*>(red);
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
 
-  for (int64_t e = tid; e < (int64_t)b * l; e += nt) {
-    const int r = (int)(e / l), c = (int)(e % l);
-    Ys[(int64_t)c * b + r] = Y[(r0 + r) * ldy + c];
+  // eight independent loads in flight per thread before the shared stores
+  const int bl = b * l;                               // <= SMEM_OPTIN / 8
+  for (int e0 = tid; e0 < bl; e0 += 8 * nt) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * nt, r = e / l, c = e - r * l;
+      v[q] = e < bl ? Y[(r0 + r) * ldy + c] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * nt, r = e / l, c = e - r * l;
+      if (e < bl) Ys[c * b + r] = v[q];
+    }
   }
   __syncthreads();
 
