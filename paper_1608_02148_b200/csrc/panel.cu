@@ -318,6 +318,8 @@ int leaf_rows_cap(int l) {
 __global__ void __launch_bounds__(HQR_THREADS) hqr_leaves_kernel(double* __restrict__ Y, int64_t ldy,
                                                                  int64_t M, int l, int64_t nleaves,
                                                                  double* __restrict__ Rstack) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double sm[];
   const int64_t leaf = blockIdx.x;
   const int64_t rb = M / nleaves, rem = M % nleaves;
@@ -428,12 +430,16 @@ cudaError_t launch_hqr_leaves(double* Y, int64_t ldy, int64_t M, int l, int64_t 
   if (smem > (size_t)SMEM_OPTIN || bmax < l) return cudaErrorInvalidValue;
   cudaError_t e = set_smem((const void*)hqr_leaves_kernel, smem);
   if (e != cudaSuccess) return e;
-  hqr_leaves_kernel<<<(unsigned)nleaves, HQR_THREADS, smem, st>>>(Y, ldy, M, l, nleaves, Rstack); ++g_kernel_launches;
+  e = launch_pdl(hqr_leaves_kernel, dim3((unsigned)nleaves), dim3(HQR_THREADS), smem, st, Y, ldy, M, l, nleaves, Rstack);
+  if (e != cudaSuccess) return e;
+  ++g_kernel_launches;
   return cudaGetLastError();
 }
 
 __global__ void tsqr_combine_kernel(double* __restrict__ Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
                                     const double* __restrict__ S, int64_t lds) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double sm[];
   double* Ss = sm;                 // l x l
   double* rows = Ss + l * l;       // 16 x l
@@ -462,7 +468,9 @@ cudaError_t launch_tsqr_combine(double* Y, int64_t ldy, int64_t M, int l, int64_
   const size_t smem = ((size_t)l * l + 16 * (size_t)l) * sizeof(double);
   cudaError_t e = set_smem((const void*)tsqr_combine_kernel, smem);
   if (e != cudaSuccess) return e;
-  tsqr_combine_kernel<<<(unsigned)nleaves, 512, smem, st>>>(Y, ldy, M, l, nleaves, S, lds); ++g_kernel_launches;
+  e = launch_pdl(tsqr_combine_kernel, dim3((unsigned)nleaves), dim3(512), smem, st, Y, ldy, M, l, nleaves, S, lds);
+  if (e != cudaSuccess) return e;
+  ++g_kernel_launches;
   return cudaGetLastError();
 }
 
