@@ -159,12 +159,7 @@ cudaError_t launch_gram(const double* S, int64_t lds, int64_t rows, int Np, doub
   cudaError_t e = cudaSuccess;
 #define RSVD_GRAM(TJ)                                                                                     \
   {                                                                                                      \
-    static bool attr = false;                                                                            \
-    if (!attr) {                                                                                         \
-      e = cudaFuncSetAttribute(gram_partial_kernel<TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max); \
-      if (e != cudaSuccess) return e;                                                                    \
-      attr = true;                                                                                       \
-    }                                                                                                    \
+    e = smem_optin(gram_partial_kernel<TJ>); if (e != cudaSuccess) return e;                                                                                                     \
     e = launch_pdl(gram_partial_kernel<TJ>, dim3(P), dim3(CQ_THREADS), smem, st, S, lds, rows, Np, rpc, partial); \
     if (e != cudaSuccess) return e;                                                                      \
   }
@@ -404,12 +399,7 @@ cudaError_t launch_chol_aug(const double* G, int ldg, int l, int npad, double* R
   cudaError_t e = cudaSuccess;
 #define RSVD_CB(NBK)                                                                                      \
   {                                                                                                      \
-    static bool attr = false;                                                                            \
-    if (!attr) {                                                                                         \
-      e = cudaFuncSetAttribute(chol_blk_kernel<NBK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-      if (e != cudaSuccess) return e;                                                                    \
-      attr = true;                                                                                       \
-    }                                                                                                    \
+    e = smem_optin(chol_blk_kernel<NBK>); if (e != cudaSuccess) return e;                                                                                                     \
     e = launch_pdl(chol_blk_kernel<NBK>, dim3(1), dim3(256), smem, st, G, ldg, l, npad, R, Rinv, flag, flag_bit); \
     if (e != cudaSuccess) return e;                                                                      \
   }
@@ -535,13 +525,7 @@ cudaError_t launch_panel_apply(const double* S, int64_t lds, int64_t rows, int N
   cudaError_t e = cudaSuccess;
 #define RSVD_APPLY(TJ)                                                                                    \
   {                                                                                                      \
-    static bool attr = false;                                                                            \
-    if (!attr) {                                                                                         \
-      e = cudaFuncSetAttribute(panel_apply_kernel<TJ, (TJ == 4 ? 1 : 2)>,                                  \
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);              \
-      if (e != cudaSuccess) return e;                                                                    \
-      attr = true;                                                                                       \
-    }                                                                                                    \
+    e = smem_optin(panel_apply_kernel<TJ, (TJ == 4 ? 1 : 2)>); if (e != cudaSuccess) return e;                                                                                                     \
     e = launch_pdl(panel_apply_kernel<TJ, (TJ == 4 ? 1 : 2)>, dim3((unsigned)grid), dim3(CQ_THREADS), smem, st, S, lds, rows, Np, T, ldt, C, ldc, Nout, upper ? 1 : 0); \
     if (e != cudaSuccess) return e; \
   }

@@ -16,6 +16,13 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 #define CUDA_TRY(x) do { const cudaError_t _e = (x); if (_e != cudaSuccess) return _e; } while (0)
 extern int g_pdl;   // 1: launch_pdl sets programmatic stream serialization (RSVD_PDL=0 disables)
 
+// Raise `fn`'s dynamic shared-memory limit to the device's opt-in maximum
+// (minus its static shared memory) on the CURRENT device, once per (kernel,
+// device); thread-safe (omega.cu).
+cudaError_t smem_optin_fn(const void* fn);
+template <typename... KArgs>
+inline cudaError_t smem_optin(void (*kernel)(KArgs...)) { return smem_optin_fn(reinterpret_cast<const void*>(kernel)); }
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {

@@ -304,12 +304,8 @@ static cudaError_t launch_one(const GemmArgs& g, cudaStream_t st) {
   const bool cent = g.c != nullptr || g.rs != nullptr;
   auto kfn = cent ? gemm_pass_kernel<TA, TRANS, TMAX, true> : gemm_pass_kernel<TA, TRANS, TMAX, false>;
   const size_t smem = GemmSmem<TA>::bytes;
-  static bool attr_set[2] = {false, false};   // per instantiation (centred or not)
-  if (!attr_set[cent]) {
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set[cent] = true;
-  }
+  const cudaError_t e = smem_optin(kfn);
+  if (e != cudaSuccess) return e;
   kfn<<<g.grid, GEMM_THREADS, smem, st>>>(g);
   return cudaGetLastError();
 }

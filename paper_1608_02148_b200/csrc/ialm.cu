@@ -167,8 +167,10 @@ static cudaError_t launch_tile(const double* A, double* S, double* Z, double* Mn
 #define IALM_CASE(RR)                                                                                         \
   if (r <= RR) {                                                                                              \
     const int dsm = RR <= 32 ? RR * IALM_THREADS * 8 : 0;                                                     \
-    if (dsm > 48 * 1024)                                                                                      \
-      cudaFuncSetAttribute(ialm_tile_kernel<RR, UPDATE>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);   \
+    if (dsm > 48 * 1024) {                                                                                    \
+      const cudaError_t ea = smem_optin(ialm_tile_kernel<RR, UPDATE>);                                        \
+      if (ea != cudaSuccess) return ea;                                                                       \
+    }                                                                                                         \
     ialm_tile_kernel<RR, UPDATE><<<grid, IALM_THREADS, dsm, st>>>(A, S, Z, Mn, ld, m, n, U, ldu, V, ldv, dl, r, \
                                                                 inv_mu, tshr, mu, inv_mu_next, rows_per,      \
                                                                 partial);                                     \

@@ -23,6 +23,8 @@
 
 #include <algorithm>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -345,7 +347,7 @@ cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double
   int* rank = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + jacobi_log_bytes(l));
   unsigned long long* prog = reinterpret_cast<unsigned long long*>(rank + 192);   // 8-byte aligned, after rank[0..128]
   unsigned long long* done = prog + 1;
-  static unsigned epoch_ctr = 0;
+  static std::atomic<unsigned> epoch_ctr{0};   // unique per launch (the scratch is per context; threads may share the counter)
   const unsigned epoch = ++epoch_ctr;
   const int JGv = g_jacobi_lanes ? g_jacobi_lanes : (L <= 64 ? 4 : 8);
   const int threads = (int)round_up((int64_t)(L / 2) * JGv, 32);
@@ -356,12 +358,7 @@ cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double
     const int ldx = JG * EPL + 4;                                                                         \
     const size_t smem = std::max((size_t)L * ldx * sizeof(double),                                        \
                                  (size_t)JA_CH * 64 * sizeof(double2) + (size_t)(threads / 32) * 129 * sizeof(double)); \
-    static bool attr = false;                                                                             \
-    if (!attr) {                                                                                          \
-      e = cudaFuncSetAttribute(jacobi_x_kernel<JG, EPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-      if (e != cudaSuccess) return e;                                                                     \
-      attr = true;                                                                                        \
-    }                                                                                                     \
+    e = smem_optin(jacobi_x_kernel<JG, EPL>); if (e != cudaSuccess) return e;                                                                                                      \
     e = launch_pdl(jacobi_x_kernel<JG, EPL>, dim3(1 + (unsigned)ceil_div(ldo, threads / 32)), dim3(threads), smem, st, \
                    R, ldr, l, sigma, W, ldo, rlog, rank, flag, sweeps, J, prog, done, epoch);               \
     if (e != cudaSuccess) return e; \

@@ -11,12 +11,35 @@
 // Integer work only (one Philox per entry); <= 1.2 M entries for the configs,
 // so this is a few microseconds and L2-resident.  Output row-major, ldo >= l;
 // columns [l, ncols_zero) are zero-filled (the GEMM N padding).
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace rsvd {
 
 int64_t g_kernel_launches = 0;
+
+cudaError_t smem_optin_fn(const void* fn) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({fn, dev})) return cudaSuccess;
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  int optin = 0;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  if (e == cudaSuccess) done.insert({fn, dev});
+  return e;
+}
 int g_pdl = [] { const char* e = getenv("RSVD_PDL"); return (e && e[0] == '0') ? 0 : 1; }();
 
 __device__ __forceinline__ uint4 philox_round(uint4 c, uint32_t k0, uint32_t k1) {

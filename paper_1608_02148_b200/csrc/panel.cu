@@ -21,19 +21,10 @@ namespace rsvd {
 constexpr int SMEM_OPTIN = 232448;   // B200 per-block opt-in shared memory (profiles/peaks_box.json)
 
 // cudaFuncSetAttribute is a slow host call: raise each kernel's dynamic
-// shared-memory limit to the opt-in maximum once, on first use.
+// shared-memory limit to the opt-in maximum once per device (smem_optin_fn).
 static cudaError_t set_smem(const void* fn, size_t bytes) {
-  static const void* done[32];
-  static int ndone = 0;
-  for (int i = 0; i < ndone; ++i)
-    if (done[i] == fn) return cudaSuccess;
   (void)bytes;
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_OPTIN - (int)fa.sharedSizeBytes);
-  if (e == cudaSuccess && ndone < 32) done[ndone++] = fn;
-  return e;
+  return smem_optin_fn(fn);
 }
 
 // ------------------------------------------------------------------ column statistics

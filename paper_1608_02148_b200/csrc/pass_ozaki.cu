@@ -29,9 +29,12 @@
 // A is sliced once per rsvd call (ozaki_slice_a) and read by every pass (S
 // bytes per element instead of 8); X is sliced before each pass.
 //
-// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 =
-// TMEM allocator, warps 4..7 = epilogue (TMEM lanes = output rows).  Stream-K
-// over (row block, k-block) units with the in-kernel fix-up of gemm_pass.cu.
+// Roles (384 threads): warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 =
+// TMEM allocator, warps 4..11 = epilogue (TMEM lanes = output rows, two warps
+// per lane quadrant splitting the columns, so the FP64 accumulators stay in
+// registers).  Stream-K over (row block, k-block) units with an in-kernel
+// fix-up (column-major partials; the last segment of a CTA stages its rows
+// through the idle unit buffers for coalesced stores).
 #include <cuda.h>
 
 #include "common.cuh"
@@ -42,7 +45,10 @@ namespace rsvd {
 namespace oz {
 using namespace tc;
 
-constexpr int BM = 128, BKO = 128, THREADS = 256;
+// 384 threads: warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator,
+// warps 4..11 epilogue (two per TMEM lane quadrant, each owning half of the N
+// columns, so the FP64 accumulators stay in registers: <= 168 per thread)
+constexpr int BM = 128, BKO = 128, THREADS = 384, EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
 constexpr int A_TILE = BM * BKO;                    // bytes of one slice tile
 constexpr int KSUP = 8, ET = KSUP * BKO;            // exponent super-tiles: 1024 x 1024 of A, 1024-row blocks of X;
                                                     // int32 accumulation over 1024 k: <= 7 pairs * 1024 * 255 * 128 < 2^28
@@ -58,6 +64,9 @@ __host__ __device__ inline int64_t unit_lo(int64_t units, int grid, int c) { ret
 #define OZ_PROBE3_DECL
 #define OZ_PROBE3(slot)
 #define OZ_PROBE3_OUT
+#endif
+#ifndef OZ_TL
+#define OZ_TL(slot) {}                              // probe builds: per-CTA timeline (tools/test_ozaki.cu)
 #endif
 
 __device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
@@ -265,35 +274,48 @@ struct Args {
   double* C2; const double* xf2; int Nout2;
 };
 
-// One unit = (128-row output block, 64-k block): 8 A-slice tiles (128 x 64 B)
-// + the S X-slice tiles (N x 64 B), 64 + 8N KB, loaded as one transaction
-// into one of two unit buffers, so the whole next unit streams in while the
-// current one is multiplied.
-constexpr int BKU = 64;                             // k per unit
-constexpr int KSU = ET / BKU;                       // units per exponent super-block (16)
-constexpr int A_UT = BM * BKU;                      // bytes of one A-slice tile of a unit
-__host__ __device__ constexpr int oz_ubuf(int S, int N) { return (S * A_UT + S * N * BKU + 1023) / 1024 * 1024; }
-__host__ __device__ constexpr int oz_nbuf(int S, int N) { return 3 * oz_ubuf(S, N) + 1024 <= 219 * 1024 ? 3 : 2; }
+// One unit = (128-row output block, BK-k block): S A-slice tiles (128 x BK B)
+// + the S X-slice tiles (N x BK B), loaded as one transaction into one of NB
+// unit buffers (as many as fit in 219 KB, at most 6).  BK = 64 (default: 2
+// buffers at N = 64); BK = 32 (RSVD_OZ_BK=32) fits 5 buffers but its 32-byte
+// box rows stream slower (measured: DESIGN.md §9).
+constexpr int kMaxBuf = 6;
+__host__ __device__ constexpr int oz_ubuf(int S, int N, int BK) { return (S * BM * BK + S * N * BK + 1023) / 1024 * 1024; }
+__host__ __device__ constexpr int oz_nbuf(int S, int N, int BK) {
+  return (219 * 1024 - 1024) / oz_ubuf(S, N, BK) < kMaxBuf ? (219 * 1024 - 1024) / oz_ubuf(S, N, BK) : kMaxBuf;
+}
 
 // CL = 2 (Np = 128 as two 64-column halves in one launch): the CTAs of a
 // 2-CTA cluster take the same units in lock step, CTA r computing columns
 // [64 r, 64 r + 64) from its own X slices; each loads half of the unit's A
 // slice tiles and multicasts them to both, so A's slices are read once per
 // pass instead of once per column half.  Stream-K runs over the pairs.
-template <bool TRANS, int S, int N, int CL>
+template <bool TRANS, int S, int N, int CL, int BK>
 __global__ void __launch_bounds__(THREADS, 1)
 ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapX,
                   const __grid_constant__ CUtensorMap mapX2, Args g) {
   pdl_wait();
+  if (threadIdx.x == 0) OZ_TL(0)
   pdl_trigger();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int XSL = N * BKU;                      // bytes of one X slice tile (N rows x 64 k)
-  constexpr int UBUF = ((S * A_UT + S * XSL) + 1023) / 1024 * 1024;
-  constexpr int NB = oz_nbuf(S, N);                 // unit buffers (3 when they fit, else 2)
-  __shared__ uint64_t ufull[3], uempty[3], accf, acce;
+  constexpr int BKU = BK;                           // k per unit
+#ifdef OZ_KSU_OVERRIDE                               // probe builds only: drain interval in units (wrong numerics)
+  constexpr int KSU = OZ_KSU_OVERRIDE;
+#else
+  constexpr int KSU = ET / BKU;                     // units per exponent super-block
+#endif
+  constexpr int A_UT = BM * BKU;                    // bytes of one A-slice tile of a unit
+  constexpr int XSL = N * BKU;                      // bytes of one X slice tile (N rows x BK k)
+  constexpr int UBUF = oz_ubuf(S, N, BK);
+  constexpr int NB = oz_nbuf(S, N, BK);             // unit buffers
+  constexpr int KPB = BKO / BKU;                    // units per 128-column slice block
+  // NN: K-major tiles with BK-byte rows (SW64 / SW32); TN: MN-major 128 B rows (SW128)
+  constexpr uint32_t LAY_K = BK == 64 ? LAYOUT_SW64 : LAYOUT_SW32;
+  constexpr uint32_t SBO_K = BK == 64 ? 512 : 256;
+  __shared__ uint64_t ufull[kMaxBuf], uempty[kMaxBuf], accf, acce;
   __shared__ uint32_t tmem_base;
-  __shared__ double xfsm[4 * 64];
+  __shared__ double xfsm[EPI_WARPS * 32];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t KB = g.KB;                          // 64-k blocks
@@ -309,7 +331,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   if (tid == 0) {
     for (int s = 0; s < NB; ++s) { mbar_init(&ufull[s], 1); mbar_init(&uempty[s], CL); }
     mbar_init(&accf, 1);
-    mbar_init(&acce, 4);
+    mbar_init(&acce, EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -332,21 +354,31 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         OZ_PROBE2(0)
         mbar_wait(&uempty[ub], (uint32_t)(((it / NB) & 1) ^ 1));
         OZ_PROBE2(1)
+#if defined(OZ_NO_A_TMA)            // probe builds only (tools/test_ozaki.cu): no A-slice loads
+        mbar_expect_tx(&ufull[ub], (uint32_t)(S * XSL));
+        if (false) {
+#elif defined(OZ_NO_X_TMA)          // probe builds only: no X-slice loads
+        mbar_expect_tx(&ufull[ub], (uint32_t)(S * A_UT));
+        if (CL == 1) {
+#else
         mbar_expect_tx(&ufull[ub], (uint32_t)(S * A_UT + S * XSL));
         if (CL == 1) {
+#endif
           for (int t = 0; t < S; ++t) {
-            if (!TRANS) tma_4d(ubuf + t * A_UT, &mapA, (int)((kb & 1) * BKU), t, (int)(kb >> 1), (int)(mb * BM), &ufull[ub]);
+            if (!TRANS) tma_4d(ubuf + t * A_UT, &mapA, (int)((kb % KPB) * BKU), t, (int)(kb / KPB), (int)(mb * BM), &ufull[ub]);
             else tma_4d(ubuf + t * A_UT, &mapA, 0, t, (int)mb, (int)(kb * BKU), &ufull[ub]);
           }
         } else {
           for (int t = crank; t < S; t += 2) {
             if (!TRANS)
-              tma_4d_mc(ubuf + t * A_UT, &mapA, (int)((kb & 1) * BKU), t, (int)(kb >> 1), (int)(mb * BM), &ufull[ub], (uint16_t)3);
+              tma_4d_mc(ubuf + t * A_UT, &mapA, (int)((kb % KPB) * BKU), t, (int)(kb / KPB), (int)(mb * BM), &ufull[ub], (uint16_t)3);
             else tma_4d_mc(ubuf + t * A_UT, &mapA, 0, t, (int)mb, (int)(kb * BKU), &ufull[ub], (uint16_t)3);
           }
         }
         const CUtensorMap* mx = crank ? &mapX2 : &mapX;
+#ifndef OZ_NO_X_TMA
         for (int t = 0; t < S; ++t) tma_2d(ubuf + S * A_UT + t * XSL, mx, (int)(kb * BKU), t * g.Np, &ufull[ub]);
+#endif
         OZ_PROBE2(2)
       }
       if (CL == 2) {
@@ -355,6 +387,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       }
       OZ_PROBE2(0)
       OZ_PROBE2_OUT
+      OZ_TL(1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer
@@ -375,16 +408,18 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         OZ_PROBE(0)
         mbar_wait(&ufull[ub], (uint32_t)((it / NB) & 1));
         OZ_PROBE(3)
+#ifndef OZ_NO_EPI
         if (fresh && ndrain > 0) mbar_wait(&acce, (uint32_t)((ndrain - 1) & 1));
+#endif
         OZ_PROBE(2)
         tc_fence_after();
         const uint32_t ua = smem_u32(base + ub * UBUF);
-        const uint64_t dx0 = sdesc(ua + S * A_UT, 16, 512, LAYOUT_SW64);
+        const uint64_t dx0 = sdesc(ua + S * A_UT, 16, SBO_K, LAY_K);
         const uint32_t acc0 = fresh ? 0u : 1u;
 #pragma unroll
         for (int t = 0; t < S; ++t) {
           // NN: A tile K-major, 64 B rows (SW64, k-step +32 B); TN: MN-major, 128 B rows (SW128, k-step +32 rows)
-          const uint64_t da0 = TRANS ? sdesc(ua + t * A_UT, 16, 1024, LAYOUT_SW128) : sdesc(ua + t * A_UT, 16, 512, LAYOUT_SW64);
+          const uint64_t da0 = TRANS ? sdesc(ua + t * A_UT, 16, 1024, LAYOUT_SW128) : sdesc(ua + t * A_UT, 16, SBO_K, LAY_K);
 #pragma unroll
           for (int kk = 0; kk < BKU / 32; ++kk) {
             const uint64_t da = da0 + (uint64_t)(TRANS ? kk * 256 : kk * 2);
@@ -406,16 +441,25 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         fresh = drain;
       }
       OZ_PROBE_OUT
+      OZ_TL(2)
     }
   } else if (warp >= 4) {
+#ifdef OZ_NO_EPI                    // probe builds only: no epilogue at all
+    if (true) {} else
+#endif
+    {
     // ---------------- epilogue: TMEM groups -> FP64, scale, accumulate; segment write-out
-    const int et = tid - 128;
+    // thread (row, hf) owns columns [hf * NC, hf * NC + NC) of output row `row`
+    constexpr int NC = N / 2;
+    const int et = tid - 128;                         // 0 .. EPI_THREADS - 1
     const int row = 32 * (warp & 3) + lane;
+    const int hf = (warp - 4) >> 2;                   // column half
+    const int c0 = hf * NC;
     const uint32_t tlane = (uint32_t)(32 * (warp & 3)) << 16;
-    double acc[N];
+    double acc[NC];
 #pragma unroll
-    for (int j = 0; j < N; ++j) acc[j] = 0.0;
-    double* xfs = xfsm + (warp & 3) * 64;             // per-warp copy of this super-block's column factors
+    for (int j = 0; j < NC; ++j) acc[j] = 0.0;
+    double* xfs = xfsm + (warp - 4) * 32;             // per-warp copy of this super-block's column factors
     int64_t ndrain = 0;
     OZ_PROBE3_DECL
     for (int64_t it = 0; it < nun; ++it) {
@@ -423,38 +467,57 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       if (!((kb % KSU == KSU - 1) || kb == KB - 1 || it == nun - 1)) continue;
       const int64_t sb = kb / KSU, sm_ = mb * BM / ET;      // super-block along k, super-tile along m
       const double eaf = TRANS ? g.ea[sb * g.ea_ld + sm_] : g.ea[sm_ * g.ea_ld + sb];
-      for (int j = lane; j < N; j += 32) xfs[j] = eaf * xfh[sb * g.Np + j];
+      if (lane < NC) xfs[lane] = eaf * xfh[sb * g.Np + c0 + lane];
       __syncwarp();
       OZ_PROBE3(0)
-      mbar_wait(&accf, (uint32_t)(ndrain & 1));
+      // one thread waits (sleeping), the other epilogue warps block on a named barrier
+      if (et == 0) mbar_wait_sleep(&accf, (uint32_t)(ndrain & 1));
+      asm volatile("bar.sync 2, %0;" ::"n"(EPI_THREADS) : "memory");
       OZ_PROBE3(1)
       ++ndrain;
       tc_fence_after();
       // 8 columns at a time: the S group loads are issued back to back, one wait
 #pragma unroll
-      for (int c = 0; c < N / 8; ++c) {
+      for (int c = 0; c < NC / 8; ++c) {
         uint32_t v[S][8];
 #pragma unroll
-        for (int gg = 0; gg < S; ++gg) TMEM_LD8(tmem + tlane + (uint32_t)(gg * N + 8 * c), v[gg]);
+#if defined(OZ_EPI_V) && (OZ_EPI_V & 1)   // probe builds only: no TMEM loads
+        for (int gg = 0; gg < S; ++gg) for (int i = 0; i < 8; ++i) v[gg][i] = (uint32_t)(gg + i + c) * (uint32_t)row;
+#else
+        for (int gg = 0; gg < S; ++gg) TMEM_LD8(tmem + tlane + (uint32_t)(gg * N + c0 + 8 * c), v[gg]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        double part[8];
+#endif
+        // group g = t + u weighs 2^{-13-8g}; |v_g| < 7 * 1024 * 255 * 128 < 2^28, so the
+        // groups 0..3 and 4..6 combine EXACTLY in int64 (< 2^53 and < 2^45): two
+        // int -> FP64 conversions and one rounding per column instead of seven
+        static_assert(S == 7, "group combination assumes 7 digit groups");
 #pragma unroll
-        for (int i = 0; i < 8; ++i) part[i] = 0.0;
-        double w = 0x1.0p-13;                         // group g = t + u: weight 2^{-13-8g}
-#pragma unroll
-        for (int gg = 0; gg < S; ++gg) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) part[i] = fma((double)(int)v[gg][i], w, part[i]);
-          w *= 0x1.0p-8;
+        for (int i = 0; i < 8; ++i) {
+          const long long s0 = (((long long)(int)v[0][i] * 256 + (int)v[1][i]) * 256 + (int)v[2][i]) * 256 + (int)v[3][i];
+          const long long s1 = ((long long)(int)v[4][i] * 256 + (int)v[5][i]) * 256 + (int)v[6][i];
+          const double part = fma((double)s0, 0x1.0p-37, (double)s1 * 0x1.0p-61);
+          acc[8 * c + i] = fma(part, xfs[8 * c + i], acc[8 * c + i]);
         }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[8 * c + i] = fma(part[i], xfs[8 * c + i], acc[8 * c + i]);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acce);
       OZ_PROBE3(2)
+#if defined(OZ_EPI_V) && (OZ_EPI_V & 4)   // probe builds only: one store of the row sum, no fix-up
       if (kb == KB - 1 || it == nun - 1) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) sacc += acc[j];
+        g.P[(int64_t)blockIdx.x * BM + row] = sacc;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc[j] = 0.0;
+      }
+      if (false) {
+#elif defined(OZ_EPI_V) && (OZ_EPI_V & 2)   // probe builds only: no write-out / fix-up
+      if (false) {
+#else
+      if (kb == KB - 1 || it == nun - 1) {
+#endif
         // stream-K fix-up (see gemm_pass.cu)
         const int64_t rb_lo = mb * KB, rb_hi = rb_lo + KB;
         const int64_t seg_start = (rb_lo > u_lo) ? rb_lo : u_lo;
@@ -462,46 +525,65 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         const bool head = !cont && (u + 1 < rb_hi);
         const int64_t gm = mb * BM + row;
         if (cont) {
-          double* dst = g.P + ((int64_t)blockIdx.x * BM + row) * N;
+          // partial, column-major per CTA ([j][row]): each warp store is 256 contiguous bytes
+          double* dst = g.P + ((int64_t)blockIdx.x * N + c0) * BM + row;
 #pragma unroll
-          for (int j = 0; j < N; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(acc[j], acc[j + 1]);
+          for (int j = 0; j < NC; ++j) dst[(int64_t)j * BM] = acc[j];
+#if !(defined(OZ_EPI_V) && (OZ_EPI_V & 16))
           __threadfence();
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+#endif
+          asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
           if (et == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(g.epoch) : "memory");
         } else {
           if (head) {
             for (int pc = pid + 1; pc < npair && unit_lo(g.units, npair, pc) < rb_hi; ++pc) {
               const int cc = pc * CL + crank;
               unsigned f;
+#if defined(OZ_EPI_V) && (OZ_EPI_V & 8)   // probe builds only: no flag wait (wrong results)
+              (void)f;
+#else
               do {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(g.flags + cc) : "memory");
               } while (f != g.epoch);
-              const double* src = g.P + ((int64_t)cc * BM + row) * N;
+#endif
+              const double* src = g.P + ((int64_t)cc * N + c0) * BM + row;
 #pragma unroll
-              for (int j = 0; j < N; j += 2) {
-                const double2 pv = *reinterpret_cast<const double2*>(src + j);
-                acc[j] += pv.x;
-                acc[j + 1] += pv.y;
-              }
+              for (int j = 0; j < NC; ++j) acc[j] += src[(int64_t)j * BM];
             }
           }
-          if (gm < g.M) {
-            double* dst = Cout + gm * g.ldc;
+          if (it == nun - 1) {
+            // the CTA's last segment: every MMA and TMA load is complete, so the unit
+            // buffers stage the 128 x N block for row-contiguous (coalesced) stores
+            constexpr int LDS = N + 1;
+            double* stg = reinterpret_cast<double*>(base);
 #pragma unroll
-            for (int j = 0; j < N; ++j)
-              if (j < Nout) dst[j] = acc[j];
+            for (int j = 0; j < NC; ++j) stg[row * LDS + c0 + j] = acc[j];
+            asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+            for (int r = warp - 4; r < BM; r += EPI_WARPS) {
+              const int64_t grow = mb * BM + r;
+              if (grow >= g.M) break;
+              for (int j = lane; j < Nout; j += 32) Cout[grow * g.ldc + j] = stg[r * LDS + j];
+            }
+          } else if (gm < g.M) {
+            double* dst = Cout + gm * g.ldc + c0;
+#pragma unroll
+            for (int j = 0; j < NC; ++j)
+              if (c0 + j < Nout) dst[j] = acc[j];
           }
         }
 #pragma unroll
-        for (int j = 0; j < N; ++j) acc[j] = 0.0;
+        for (int j = 0; j < NC; ++j) acc[j] = 0.0;
       }
       OZ_PROBE3(3)
     }
     OZ_PROBE3(0)
     OZ_PROBE3_OUT
+    if (et == 0) OZ_TL(3)
+    }
   }
   tc_fence_before();
   if (CL == 2) cluster_sync_all(); else __syncthreads();
+  if (threadIdx.x == 0) OZ_TL(4)
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
@@ -513,26 +595,28 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
 // interleaved layout.  NN unit tile: 128 rows x 64 B (box {64, 1, 1, 128},
 // SW64, K-major); TN unit tile: 64 rows x 128 B (box {128, 1, 1, 64}, SW128,
 // MN-major operand).
-static bool map_slices(CUtensorMap* mp, const int8_t* p, int64_t rows, int64_t nblk, int S, bool trans) {
+static bool map_slices(CUtensorMap* mp, const int8_t* p, int64_t rows, int64_t nblk, int S, bool trans, int bk) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[4] = {128, (cuuint64_t)S, (cuuint64_t)nblk, (cuuint64_t)rows};
   cuuint64_t strides[3] = {128, (cuuint64_t)(128 * S), (cuuint64_t)(128 * S * nblk)};
-  cuuint32_t box[4] = {trans ? 128u : 64u, 1, 1, trans ? 64u : 128u};
+  cuuint32_t box[4] = {trans ? 128u : (cuuint32_t)bk, 1, 1, trans ? (cuuint32_t)bk : 128u};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(p), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, trans ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             trans ? CU_TENSOR_MAP_SWIZZLE_128B : (bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-static bool map_i8_2d(CUtensorMap* mp, const int8_t* p, int64_t cols, int64_t rows, int64_t ld, int box_rows) {
+static bool map_i8_2d(CUtensorMap* mp, const int8_t* p, int64_t cols, int64_t rows, int64_t ld, int box_rows, int bk) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld};
-  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)bk, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   return enc(mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(p), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -579,6 +663,11 @@ OzakiA ozaki_layout_a(void* buf, int64_t m, int64_t n) {
 }
 
 static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st);
+// k per unit of the pass kernels: 64 (default) or 32 (RSVD_OZ_BK=32)
+static int oz_bk() {
+  static const int v = [] { const char* e = getenv("RSVD_OZ_BK"); return (e && atoi(e) == 32) ? 32 : 64; }();
+  return v;
+}
 static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st);
 static cudaError_t ozaki_pass_pair(const OzakiCall& h0, const OzakiCall& h1, cudaStream_t st);
 
@@ -613,13 +702,8 @@ static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st) {
   const int64_t ldk = round_up(c.K, 16);
   int8_t* xs = reinterpret_cast<int8_t*>(c.xscratch);
   double* xf = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
-  static bool attr = false;
-  if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(ozaki_slice_x_kernel<OZ_S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               xt_smem(OZ_S));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  const cudaError_t ea = smem_optin(ozaki_slice_x_kernel<OZ_S>);
+  if (ea != cudaSuccess) return ea;
   const dim3 gs((unsigned)ceil_div(ldk, ET), (unsigned)ceil_div(N, XT_COLS));
   const cudaError_t el = launch_pdl(ozaki_slice_x_kernel<OZ_S>, gs, dim3(XT_THREADS), (size_t)xt_smem(OZ_S), st, c.B, c.ldb, c.K, N, xs, ldk, xf);
   if (el != cudaSuccess) return el;
@@ -636,9 +720,10 @@ static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
   int8_t* xs = reinterpret_cast<int8_t*>(c.xscratch);
   double* xf = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
   // 2) tensor maps: A slices as (cols = n, rows = m, S); X slices as (cols = K, rows = S * N)
+  const int bk = oz_bk();
   CUtensorMap mA, mX;
-  if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, OZ_S, c.trans)) return cudaErrorInvalidValue;
-  if (!map_i8_2d(&mX, xs, c.K, (int64_t)OZ_S * N, ldk, N)) {
+  if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, OZ_S, c.trans, bk)) return cudaErrorInvalidValue;
+  if (!map_i8_2d(&mX, xs, c.K, (int64_t)OZ_S * N, ldk, N, bk)) {
 #ifdef OZ_DEBUG
     printf("map X failed: xs %p K %lld rows %lld ldk %lld box %d\n", (void*)xs, (long long)c.K, (long long)OZ_S * N, (long long)ldk, N);
 #endif
@@ -648,26 +733,23 @@ static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
   g.C = c.C; g.ldc = c.ldc; g.P = c.P; g.flags = c.flags; g.epoch = c.epoch;
   g.ea = a.ea; g.ea_ld = a.ntiles; g.xf = xf;
   g.M = c.M; g.K = c.K; g.N = N; g.Nout = c.Nout; g.Np = N;
-  g.KB = ceil_div(c.K, BKU);
+  g.KB = ceil_div(c.K, bk);
   const int64_t mblocks = ceil_div(c.M, BM);
   g.units = mblocks * g.KB;
-  int64_t grid = g.units / 4;
+  int64_t grid = g.units / (256 / bk);
   if (grid < mblocks) grid = mblocks;
   if (grid > c.grid) grid = c.grid;
   if (grid < 1) grid = 1;
   g.grid = (int)grid;
-  const int nbuf = N <= 16 ? oz_nbuf(OZ_S, 16) : N <= 32 ? oz_nbuf(OZ_S, 32) : N <= 48 ? oz_nbuf(OZ_S, 48) : oz_nbuf(OZ_S, 64);
-  const size_t smem = (size_t)nbuf * oz_ubuf(OZ_S, N <= 16 ? 16 : N <= 32 ? 32 : N <= 48 ? 48 : 64) + 1024;
+  const int Nt = N <= 16 ? 16 : N <= 32 ? 32 : N <= 48 ? 48 : 64;
+  const size_t smem = (size_t)oz_nbuf(OZ_S, Nt, bk) * oz_ubuf(OZ_S, Nt, bk) + 1024;
   cudaError_t e = cudaSuccess;
 #define RSVD_OZ(TR, NN)                                                                                   \
+  if (bk == 64) RSVD_OZB(TR, NN, 64) else RSVD_OZB(TR, NN, 32)
+#define RSVD_OZB(TR, NN, BK)                                                                              \
   {                                                                                                      \
-    static bool attr = false;                                                                            \
-    if (!attr) {                                                                                         \
-      e = cudaFuncSetAttribute(ozaki_pass_kernel<TR, OZ_S, NN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); \
-      if (e != cudaSuccess) return e;                                                                    \
-      attr = true;                                                                                       \
-    }                                                                                                    \
-    e = launch_pdl(ozaki_pass_kernel<TR, OZ_S, NN, 1>, dim3(g.grid), dim3(THREADS), smem, st, mA, mX, mX, g); \
+    e = smem_optin(ozaki_pass_kernel<TR, OZ_S, NN, 1, BK>); if (e != cudaSuccess) return e;                                                                                                     \
+    e = launch_pdl(ozaki_pass_kernel<TR, OZ_S, NN, 1, BK>, dim3(g.grid), dim3(THREADS), smem, st, mA, mX, mX, g); \
     if (e != cudaSuccess) return e;                                                                      \
   }
   if (!c.trans) {
@@ -678,6 +760,7 @@ static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
                  case 48: RSVD_OZ(true, 48) break; default: RSVD_OZ(true, 64) break; }
   }
 #undef RSVD_OZ
+#undef RSVD_OZB
   ++g_kernel_launches;
   return cudaGetLastError();
 }
@@ -693,38 +776,37 @@ static cudaError_t ozaki_pass_pair(const OzakiCall& h0, const OzakiCall& h1, cud
   int8_t* xs1 = reinterpret_cast<int8_t*>(h1.xscratch);
   const double* xf0 = reinterpret_cast<const double*>(reinterpret_cast<char*>(h0.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
   const double* xf1 = reinterpret_cast<const double*>(reinterpret_cast<char*>(h1.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
+  const int bk = oz_bk();
   CUtensorMap mA, mX0, mX1;
-  if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, OZ_S, h0.trans)) return cudaErrorInvalidValue;
-  if (!map_i8_2d(&mX0, xs0, h0.K, (int64_t)OZ_S * N, ldk, N) || !map_i8_2d(&mX1, xs1, h1.K, (int64_t)OZ_S * N, ldk, N))
+  if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, OZ_S, h0.trans, bk)) return cudaErrorInvalidValue;
+  if (!map_i8_2d(&mX0, xs0, h0.K, (int64_t)OZ_S * N, ldk, N, bk) || !map_i8_2d(&mX1, xs1, h1.K, (int64_t)OZ_S * N, ldk, N, bk))
     return cudaErrorInvalidValue;
   Args g{};
   g.C = h0.C; g.ldc = h0.ldc; g.P = h0.P; g.flags = h0.flags; g.epoch = h0.epoch;
   g.ea = a.ea; g.ea_ld = a.ntiles; g.xf = xf0;
   g.C2 = h1.C; g.xf2 = xf1; g.Nout2 = h1.Nout;
   g.M = h0.M; g.K = h0.K; g.N = N; g.Nout = h0.Nout; g.Np = N;
-  g.KB = ceil_div(h0.K, BKU);
+  g.KB = ceil_div(h0.K, bk);
   const int64_t mblocks = ceil_div(h0.M, BM);
   g.units = mblocks * g.KB;
-  int64_t npair = g.units / 4;
+  int64_t npair = g.units / (256 / bk);
   if (npair < mblocks) npair = mblocks;
   if (npair > h0.grid / 2) npair = h0.grid / 2;
   if (npair < 1) npair = 1;
   g.grid = (int)(2 * npair);
-  const size_t smem = (size_t)oz_nbuf(OZ_S, N) * oz_ubuf(OZ_S, N) + 1024;
+  const size_t smem = (size_t)oz_nbuf(OZ_S, N, bk) * oz_ubuf(OZ_S, N, bk) + 1024;
   cudaError_t e = cudaSuccess;
 #define RSVD_OZP(TR)                                                                                      \
+  if (bk == 64) RSVD_OZPB(TR, 64) else RSVD_OZPB(TR, 32)
+#define RSVD_OZPB(TR, BK)                                                                                 \
   {                                                                                                      \
-    static bool attr = false;                                                                            \
-    if (!attr) {                                                                                         \
-      e = cudaFuncSetAttribute(ozaki_pass_kernel<TR, OZ_S, N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); \
-      if (e != cudaSuccess) return e;                                                                    \
-      attr = true;                                                                                       \
-    }                                                                                                    \
-    e = launch_pdl_cluster(ozaki_pass_kernel<TR, OZ_S, N, 2>, dim3(g.grid), dim3(THREADS), smem, st, 2u, mA, mX0, mX1, g); \
+    e = smem_optin(ozaki_pass_kernel<TR, OZ_S, N, 2, BK>); if (e != cudaSuccess) return e;                                                                                                     \
+    e = launch_pdl_cluster(ozaki_pass_kernel<TR, OZ_S, N, 2, BK>, dim3(g.grid), dim3(THREADS), smem, st, 2u, mA, mX0, mX1, g); \
     if (e != cudaSuccess) return e;                                                                      \
   }
   if (!h0.trans) RSVD_OZP(false) else RSVD_OZP(true)
 #undef RSVD_OZP
+#undef RSVD_OZPB
   ++g_kernel_launches;
   return cudaGetLastError();
 }

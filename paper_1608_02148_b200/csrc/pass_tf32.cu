@@ -170,7 +170,8 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     for (int64_t it = 0; it < nun; ++it) {
       const int s = (int)(it % STAGES);
       const uint32_t ph = (uint32_t)((it / STAGES) & 1);
-      mbar_wait(&full[s], ph);
+      if (et == 0) mbar_wait_sleep(&full[s], ph);    // one thread sleeps; the split warps block on a named barrier
+      asm volatile("bar.sync 3, 128;" ::: "memory");
       float4* a4 = reinterpret_cast<float4*>(stageA(s));
       float4* l4 = reinterpret_cast<float4*>(stageAlo(s));
 #pragma unroll 4
@@ -203,7 +204,8 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       if (!run_end) continue;
       in_run = 0;
       const int b = (int)(run & 1);
-      mbar_wait(&accf[b], (uint32_t)((run >> 1) & 1));
+      if (et == 0) mbar_wait_sleep(&accf[b], (uint32_t)((run >> 1) & 1));
+      asm volatile("bar.sync 2, 128;" ::: "memory");
       tc_fence_after();
       const uint32_t tbase = tmem + (uint32_t)(b * g.N) + ((uint32_t)(32 * (warp & 3)) << 16);
       if (!seg_end) {
@@ -413,7 +415,8 @@ pass_tf32_tn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     for (int64_t it = 0; it < nun; ++it) {
       const int s = (int)(it % TN_STAGES);
       const uint32_t ph = (uint32_t)((it / TN_STAGES) & 1);
-      mbar_wait(&full[s], ph);
+      if (et == 0) mbar_wait_sleep(&full[s], ph);    // one thread sleeps; the split warps block on a named barrier
+      asm volatile("bar.sync 3, 128;" ::: "memory");
       float4* a4 = reinterpret_cast<float4*>(stA(s));
       float4* l4 = reinterpret_cast<float4*>(stAl(s));
 #pragma unroll 4
@@ -445,7 +448,8 @@ pass_tf32_tn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
       if (!run_end) continue;
       in_run = 0;
       const int b = (int)(run & 1);
-      mbar_wait(&accf[b], (uint32_t)((run >> 1) & 1));
+      if (et == 0) mbar_wait_sleep(&accf[b], (uint32_t)((run >> 1) & 1));
+      asm volatile("bar.sync 2, 128;" ::: "memory");
       tc_fence_after();
       const uint32_t tbase = tmem + (uint32_t)(b * TN_BN) + ((uint32_t)(32 * (warp & 3)) << 16);
       if (!seg_end) {
@@ -635,11 +639,11 @@ cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st) {
     const size_t smem = (size_t)TN_STAGES * TN_STAGE + 1024;
     cudaError_t e;
     if (c.trans) {
-      e = cudaFuncSetAttribute(pass_tf32_tn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = smem_optin(pass_tf32_tn_kernel<false>);
       if (e != cudaSuccess) return e;
       pass_tf32_tn_kernel<false><<<g.grid, THREADS, smem, st>>>(mA, mBh, mBl, g);
     } else {
-      e = cudaFuncSetAttribute(pass_tf32_tn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = smem_optin(pass_tf32_tn_kernel<true>);
       if (e != cudaSuccess) return e;
       pass_tf32_tn_kernel<true><<<g.grid, THREADS, smem, st>>>(mA, mBh, mBl, g);
     }
@@ -657,11 +661,11 @@ cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st) {
   const size_t smem = (size_t)STAGES * (2 * A_BYTES + 2 * (N / 32) * B_BOX_BYTES) + 1024;
   cudaError_t e;
   if (!c.trans) {
-    e = cudaFuncSetAttribute(pass_tf32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = smem_optin(pass_tf32_kernel<false>);
     if (e != cudaSuccess) return e;
     pass_tf32_kernel<false><<<g.grid, THREADS, smem, st>>>(mA, mBh, mBl, g);
   } else {
-    e = cudaFuncSetAttribute(pass_tf32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = smem_optin(pass_tf32_kernel<true>);
     if (e != cudaSuccess) return e;
     pass_tf32_kernel<true><<<g.grid, THREADS, smem, st>>>(mA, mBh, mBl, g);
   }

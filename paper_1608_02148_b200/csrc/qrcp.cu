@@ -397,7 +397,7 @@ cudaError_t launch_qrcp(double* W, int64_t ld, int rows, int64_t ncols, int step
   if (e != cudaSuccess) return e;
   const size_t smem = Z ? (size_t)steps * steps * sizeof(double) : 0;
   if (smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = smem_optin(qrcp_kernel);
     if (e != cudaSuccess) return e;
   }
   int per_sm = 0;

@@ -27,6 +27,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
 }
+// Wait with a suspend-time hint: the thread sleeps in hardware until the phase
+// completes (or the hint elapses) instead of spinning, so waiting warps do not
+// take issue slots from the producer / MMA threads of the same sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  const uint32_t a = smem_u32(b);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAITS_%=;\n\t}" ::"r"(a), "r"(parity), "r"(10000000u) : "memory");
+}
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
@@ -41,7 +52,7 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 // SWIZZLE_128B (K-major operands); layout 1 = SWIZZLE_128B_BASE32B, the only
 // swizzled layout tcgen05 accepts for MN-major 32-bit (tf32) operands; its TMA
 // counterpart is CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B (4-row 512 B K atoms).
-constexpr uint32_t LAYOUT_SW128 = 2, LAYOUT_SW128_BASE32B = 1, LAYOUT_SW64 = 4;
+constexpr uint32_t LAYOUT_SW128 = 2, LAYOUT_SW128_BASE32B = 1, LAYOUT_SW64 = 4, LAYOUT_SW32 = 6;
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout = LAYOUT_SW128) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFF);

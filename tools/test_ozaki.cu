@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
 __device__ unsigned long long g_oz[8];
 #define OZ_PROBE_DECL long long _ozt[5] = {0, 0, 0, 0, 0}; long long _ozl = clock64();
 #define OZ_PROBE(slot) { long long _t = clock64(); _ozt[slot] += _t - _ozl; _ozl = _t; }
@@ -16,9 +17,19 @@ __device__ unsigned long long g_oz2[4], g_oz3[4];
 #define OZ_PROBE3_DECL long long _p3[4] = {0, 0, 0, 0}; long long _p3l = clock64();
 #define OZ_PROBE3(slot) if (lane == 0) { long long _t = clock64(); _p3[slot] += _t - _p3l; _p3l = _t; }
 #define OZ_PROBE3_OUT if (lane == 0) for (int q = 0; q < 4; ++q) atomicAdd(&g_oz3[q], (unsigned long long)_p3[q]);
+__device__ unsigned long long g_tl[1024][5];
+#define OZ_TL(slot) { unsigned long long _g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_g)); g_tl[blockIdx.x][slot] = _g; }
 #include "../paper_1608_02148_b200/csrc/pass_tf32.cu"
 #include "../paper_1608_02148_b200/csrc/pass_ozaki.cu"
-namespace rsvd { int64_t g_kernel_launches = 0; int g_pdl = 1; }
+namespace rsvd {
+int64_t g_kernel_launches = 0; int g_pdl = getenv("RSVD_PDL") ? atoi(getenv("RSVD_PDL")) : 1;
+cudaError_t smem_optin_fn(const void* fn) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - (int)fa.sharedSizeBytes);
+}
+}
 using namespace rsvd;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s @%d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
 
@@ -110,6 +121,22 @@ int main(int argc, char** argv) {
         const double t2 = p2[0] + p2[1] + p2[2], t3 = p3[0] + p3[1] + p3[2] + p3[3];
         printf("  producer: issue %.1f%%  wait xempty %.1f%%  wait aempty %.1f%% | epilogue: other %.1f%%  wait accf %.1f%%  drain %.1f%%  write-out %.1f%%\n",
                100 * p2[0] / t2, 100 * p2[1] / t2, 100 * p2[2] / t2, 100 * p3[0] / t3, 100 * p3[1] / t3, 100 * p3[2] / t3, 100 * p3[3] / t3);
+      }
+      if (getenv("OZ_TIMELINE")) {
+        static unsigned long long tl[1024][5];
+        cudaMemcpyFromSymbol(tl, g_tl, sizeof tl);
+        unsigned long long t0 = ~0ull; int nc = 0;
+        for (int b = 0; b < 1024; ++b) if (tl[b][0]) { t0 = tl[b][0] < t0 ? tl[b][0] : t0; ++nc; }
+        std::vector<double> col[5];
+        for (int b = 0; b < nc; ++b) for (int q = 0; q < 5; ++q) col[q].push_back((tl[b][q] - t0) * 1e-3);
+        const char* nm[5] = {"start", "producer-end", "mma-end", "epi-end", "cta-end"};
+        for (int q = 0; q < 5; ++q) {
+          std::sort(col[q].begin(), col[q].end());
+          printf("  %-13s us: min %.1f p10 %.1f med %.1f p90 %.1f max %.1f\n", nm[q], col[q][0], col[q][nc / 10], col[q][nc / 2],
+                 col[q][nc * 9 / 10], col[q][nc - 1]);
+        }
+        cudaMemset(g_tl, 0, 0);
+        unsigned long long z[1024][5] = {}; cudaMemcpyToSymbol(g_tl, z, sizeof z);
       }
       float us = 0;
       if (reps > 0) {
