@@ -186,6 +186,7 @@ size_t plan_bytes(rsvd_ctx* ctx, Plan& p) {
   upd(p.M, p.n, Np);       // Y = A X
   upd(p.n, p.M, Np);       // Z = A^T Q
   if (p.use_tf32) part = std::max(part, tf32_partial_bytes(Np, ctx->num_sms));
+  if (p.use_ozaki) part = std::max(part, ozaki_partial_bytes(Np, ctx->num_sms));
   part = std::max(part, gram_partial_bytes(Np, ctx->num_sms));
   p.part_bytes = part;
   const int64_t big = std::max(p.M, p.n);

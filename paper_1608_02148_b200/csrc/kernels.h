@@ -83,6 +83,8 @@ struct OzakiCall {
   cudaEvent_t mark, mark2;                       // nullable: both recorded after X slicing, before the pass kernel(s)
 };
 bool ozaki_supported(int Np);
+// stream-K partials of the pass kernels: 2 slots (first / last segment) per CTA
+size_t ozaki_partial_bytes(int Np, int grid);
 size_t ozaki_x_bytes(int64_t K, int Np);
 cudaError_t ozaki_pass(const OzakiCall& c, cudaStream_t st);
 

@@ -315,7 +315,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   constexpr uint32_t SBO_K = BK == 64 ? 512 : 256;
   __shared__ uint64_t ufull[kMaxBuf], uempty[kMaxBuf], accf, acce;
   __shared__ uint32_t tmem_base;
-  __shared__ double xfsm[EPI_WARPS * 32];
+  __shared__ double xfsm[EPI_WARPS * 32 + 1];     // + 1: last-arriver broadcast slot
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t KB = g.KB;                          // 64-k blocks
@@ -502,6 +502,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acce);
+      if (et == 0 && it == nun - 1) OZ_TL(5)
       OZ_PROBE3(2)
 #if defined(OZ_EPI_V) && (OZ_EPI_V & 4)   // probe builds only: one store of the row sum, no fix-up
       if (kb == KB - 1 || it == nun - 1) {
@@ -518,39 +519,55 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
 #else
       if (kb == KB - 1 || it == nun - 1) {
 #endif
-        // stream-K fix-up (see gemm_pass.cu)
+        // stream-K fix-up, wait-free: a row block split over several CTAs (pairs)
+        // gets one column-major partial per segment (slot 0 = the CTA's first
+        // segment, 1 = its last) and an epoch-tagged arrival counter; the last
+        // arriver sums the partials in CTA order (the same order whoever arrives
+        // last, so results are bitwise reproducible) and writes the rows.
         const int64_t rb_lo = mb * KB, rb_hi = rb_lo + KB;
         const int64_t seg_start = (rb_lo > u_lo) ? rb_lo : u_lo;
-        const bool cont = seg_start > rb_lo;
-        const bool head = !cont && (u + 1 < rb_hi);
-        const int64_t gm = mb * BM + row;
-        if (cont) {
-          // partial, column-major per CTA ([j][row]): each warp store is 256 contiguous bytes
-          double* dst = g.P + ((int64_t)blockIdx.x * N + c0) * BM + row;
+        const bool full = seg_start == rb_lo && u + 1 == rb_hi;
+        bool write = full;
+        if (!full) {
+          int pf = pid, pl = pid;                    // pairs covering this row block
+          while (pf > 0 && unit_lo(g.units, npair, pf) > rb_lo) --pf;
+          while (pl + 1 < npair && unit_lo(g.units, npair, pl + 1) < rb_hi) ++pl;
+          const int slot = seg_start == u_lo ? 0 : 1;
+          double* dst = g.P + (((int64_t)blockIdx.x * 2 + slot) * N + c0) * BM + row;
 #pragma unroll
           for (int j = 0; j < NC; ++j) dst[(int64_t)j * BM] = acc[j];
-#if !(defined(OZ_EPI_V) && (OZ_EPI_V & 16))
-          __threadfence();
-#endif
           asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
-          if (et == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(g.epoch) : "memory");
-        } else {
-          if (head) {
-            for (int pc = pid + 1; pc < npair && unit_lo(g.units, npair, pc) < rb_hi; ++pc) {
-              const int cc = pc * CL + crank;
-              unsigned f;
-#if defined(OZ_EPI_V) && (OZ_EPI_V & 8)   // probe builds only: no flag wait (wrong results)
-              (void)f;
-#else
-              do {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(g.flags + cc) : "memory");
-              } while (f != g.epoch);
-#endif
-              const double* src = g.P + ((int64_t)cc * N + c0) * BM + row;
-#pragma unroll
-              for (int j = 0; j < NC; ++j) acc[j] += src[(int64_t)j * BM];
+          if (et == 0) {
+            unsigned long long* cnt = reinterpret_cast<unsigned long long*>(g.flags + 2048) + (pf * CL + crank);
+            __threadfence();                         // this CTA's partial before its arrival
+            unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(cnt), nw;
+            for (;;) {
+              nw = ((old >> 32) == g.epoch) ? old + 1 : (((unsigned long long)g.epoch << 32) | 1ull);
+              const unsigned long long seen = atomicCAS(cnt, old, nw);
+              if (seen == old) break;
+              old = seen;
             }
+            const bool last = (int)(nw & 0xffffffffu) == pl - pf + 1;
+            if (last) __threadfence();               // the other partials are visible after the last arrival
+            xfsm[EPI_WARPS * 32] = last ? 1.0 : 0.0;  // broadcast to the epilogue warps
           }
+          asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+          write = xfsm[EPI_WARPS * 32] != 0.0;
+          if (write) {
+#pragma unroll
+            for (int j = 0; j < NC; ++j) acc[j] = 0.0;
+            for (int pc = pf; pc <= pl; ++pc) {
+              const int cc = pc * CL + crank;
+              const int64_t ps = (rb_lo > unit_lo(g.units, npair, pc)) ? rb_lo : unit_lo(g.units, npair, pc);
+              const int sl = ps == unit_lo(g.units, npair, pc) ? 0 : 1;
+              const double* src = g.P + (((int64_t)cc * 2 + sl) * N + c0) * BM + row;
+#pragma unroll
+              for (int j = 0; j < NC; ++j) acc[j] += __ldcg(src + (int64_t)j * BM);
+            }
+            if (et == 0) OZ_TL(6)
+          }
+        }
+        if (write) {
           if (it == nun - 1) {
             // the CTA's last segment: every MMA and TMA load is complete, so the unit
             // buffers stage the 128 x N block for row-contiguous (coalesced) stores
@@ -564,11 +581,14 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
               if (grow >= g.M) break;
               for (int j = lane; j < Nout; j += 32) Cout[grow * g.ldc + j] = stg[r * LDS + j];
             }
-          } else if (gm < g.M) {
-            double* dst = Cout + gm * g.ldc + c0;
+          } else {
+            const int64_t gm = mb * BM + row;
+            if (gm < g.M) {
+              double* dsto = Cout + gm * g.ldc + c0;
 #pragma unroll
-            for (int j = 0; j < NC; ++j)
-              if (c0 + j < Nout) dst[j] = acc[j];
+              for (int j = 0; j < NC; ++j)
+                if (c0 + j < Nout) dsto[j] = acc[j];
+            }
           }
         }
 #pragma unroll
@@ -627,6 +647,10 @@ int ozaki_slices() { return OZ_S; }
 // Np <= 64 in one launch; 64 < Np <= 128 as two column blocks (64, Np - 64):
 // at Np = 128 one launch of CTA pairs (ozaki_pass_pair), else two launches over the same A slices (TMEM holds 7 groups x 64 columns)
 bool ozaki_supported(int Np) { return Np <= 128 && Np % 16 == 0 && tc::get_encode() != nullptr; }
+
+size_t ozaki_partial_bytes(int Np, int grid) {
+  return (size_t)grid * 2 * oz::BM * (size_t)(Np < 64 ? Np : 64) * sizeof(double);
+}
 
 size_t ozaki_a_bytes(int64_t m, int64_t n) {
   const int64_t ldn = round_up(n, oz::BKO);

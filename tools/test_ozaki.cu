@@ -17,7 +17,7 @@ __device__ unsigned long long g_oz2[4], g_oz3[4];
 #define OZ_PROBE3_DECL long long _p3[4] = {0, 0, 0, 0}; long long _p3l = clock64();
 #define OZ_PROBE3(slot) if (lane == 0) { long long _t = clock64(); _p3[slot] += _t - _p3l; _p3l = _t; }
 #define OZ_PROBE3_OUT if (lane == 0) for (int q = 0; q < 4; ++q) atomicAdd(&g_oz3[q], (unsigned long long)_p3[q]);
-__device__ unsigned long long g_tl[1024][5];
+__device__ unsigned long long g_tl[1024][8];
 #define OZ_TL(slot) { unsigned long long _g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_g)); g_tl[blockIdx.x][slot] = _g; }
 #include "../paper_1608_02148_b200/csrc/pass_tf32.cu"
 #include "../paper_1608_02148_b200/csrc/pass_ozaki.cu"
@@ -54,7 +54,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&abuf, ozaki_a_bytes(m, n))); CK(cudaMalloc(&flag, 64)); CK(cudaMemset(flag, 0, 64));
   CK(cudaMalloc(&flags, 4096 * 4)); CK(cudaMemset(flags, 0, 4096 * 4));
   const int64_t big = m > n ? m : n;
-  CK(cudaMalloc(&dB, big * 128 * 8)); CK(cudaMalloc(&dC, big * 128 * 8)); CK(cudaMalloc(&dP, (size_t)nsm * 128 * 64 * 8));
+  CK(cudaMalloc(&dB, big * 128 * 8)); CK(cudaMalloc(&dC, big * 128 * 8)); CK(cudaMalloc(&dP, (size_t)nsm * 2 * 128 * 64 * 8));
   CK(cudaMalloc(&xbuf, ozaki_x_bytes(big, 64))); CK(cudaMalloc(&xbuf2, ozaki_x_bytes(big, 64)));
   OzakiA oa = ozaki_layout_a(abuf, m, n);
   CK(ozaki_slice_a(oa, dA, n, nullptr, nullptr, flag, 0));
@@ -123,20 +123,22 @@ int main(int argc, char** argv) {
                100 * p2[0] / t2, 100 * p2[1] / t2, 100 * p2[2] / t2, 100 * p3[0] / t3, 100 * p3[1] / t3, 100 * p3[2] / t3, 100 * p3[3] / t3);
       }
       if (getenv("OZ_TIMELINE")) {
-        static unsigned long long tl[1024][5];
+        static unsigned long long tl[1024][8];
         cudaMemcpyFromSymbol(tl, g_tl, sizeof tl);
         unsigned long long t0 = ~0ull; int nc = 0;
         for (int b = 0; b < 1024; ++b) if (tl[b][0]) { t0 = tl[b][0] < t0 ? tl[b][0] : t0; ++nc; }
-        std::vector<double> col[5];
-        for (int b = 0; b < nc; ++b) for (int q = 0; q < 5; ++q) col[q].push_back((tl[b][q] - t0) * 1e-3);
-        const char* nm[5] = {"start", "producer-end", "mma-end", "epi-end", "cta-end"};
-        for (int q = 0; q < 5; ++q) {
+        std::vector<double> col[8];
+        for (int b = 0; b < nc; ++b) for (int q = 0; q < 8; ++q) if (tl[b][q]) col[q].push_back((tl[b][q] - t0) * 1e-3);
+        const char* nm[8] = {"start", "producer-end", "mma-end", "epi-end", "cta-end", "last-drain", "head-added", "-"};
+        for (int q = 0; q < 7; ++q) {
+          if (col[q].empty()) continue;
+          const int nc = (int)col[q].size();
           std::sort(col[q].begin(), col[q].end());
           printf("  %-13s us: min %.1f p10 %.1f med %.1f p90 %.1f max %.1f\n", nm[q], col[q][0], col[q][nc / 10], col[q][nc / 2],
                  col[q][nc * 9 / 10], col[q][nc - 1]);
         }
         cudaMemset(g_tl, 0, 0);
-        unsigned long long z[1024][5] = {}; cudaMemcpyToSymbol(g_tl, z, sizeof z);
+        static unsigned long long z[1024][8] = {}; cudaMemcpyToSymbol(g_tl, z, sizeof z);
       }
       float us = 0;
       if (reps > 0) {
