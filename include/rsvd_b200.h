@@ -13,9 +13,17 @@
  *  * "device" = memory of the context's CUDA device (cudaMalloc / torch).
  *    The library never frees caller memory; it owns only its workspace.
  *  * All work is enqueued on the context's stream (the one given to
- *    rsvd_create).  Calls that return a status read a small device status
- *    word at the end (one stream synchronisation); outputs are valid when
- *    the call returns RSVD_OK.
+ *    rsvd_create) and the calls return as soon as it is enqueued: no host
+ *    synchronisation, so a call can be captured into a CUDA graph.  Outputs
+ *    are valid once the stream has reached the end of the call.  Numerical
+ *    failures found on the device (non-finite values, the Jacobi sweep cap,
+ *    a rank-deficient pivoted QR in rid/rcur) are recorded in the context's
+ *    status word and reported by rsvd_sync().  The CholeskyQR breakdown of
+ *    a rank-deficient sketch is handled on the device (Householder TSQR
+ *    fallback), never reported as an error.  Exceptions:
+ *    rsvd_rrpca (its IALM loop decides on the host, one read per iteration)
+ *    and rsvd_run_host (host buffers) return after a stream synchronisation
+ *    with the numerical status of the call.
  *  * Validation errors (RSVD_EINVAL / RSVD_EUNSUPPORTED) are returned BEFORE
  *    any launch and write nothing.  rsvd_last_error() gives the message for
  *    the last non-OK status, or a warning (e.g. nu > k clamped).
@@ -62,12 +70,31 @@ rsvd_status rsvd_destroy(rsvd_ctx* ctx);
 const char* rsvd_last_error(const rsvd_ctx* ctx);
 const char* rsvd_version(void);
 
+/* Wait for the context's stream, then return (and clear) the numerical status
+ * accumulated by the calls completed since the last rsvd_sync: RSVD_OK, or
+ * RSVD_ENUMERIC with the reason in rsvd_last_error (non-finite input or
+ * intermediate, Jacobi sweep cap, numerical rank < k in rid / rcur). */
+rsvd_status rsvd_sync(rsvd_ctx* ctx);
+
 /* NCCL plumbing (multi-GPU, one process per GPU).  rank 0 calls
  * rsvd_nccl_unique_id (writes 128 bytes to host memory `out`), the caller
  * broadcasts them (e.g. torch.distributed), and every rank calls
  * rsvd_comm_init.  nranks == 1 is accepted and means single-GPU. */
 rsvd_status rsvd_nccl_unique_id(void* out128);
 rsvd_status rsvd_comm_init(rsvd_ctx* ctx, const void* nccl_unique_id128, int nranks, int rank);
+
+/* In-process rank groups: `nranks` contexts (2 <= nranks <= 16, on the same
+ * device or on devices with peer access), one host thread each, run the
+ * row-sharded path together with the collectives replaced by fixed-rank-order
+ * device reductions over the group's staging buffers (every rank gets
+ * bitwise the same sums).  Same semantics as rsvd_comm_init; used to run the
+ * distributed algorithm on one GPU (tests) and for multi-GPU without NCCL.
+ * rsvd_group_destroy after every member context is destroyed.  A member that
+ * fails inside a call aborts the group: the others return RSVD_ENCCL. */
+typedef struct rsvd_group rsvd_group;
+rsvd_status rsvd_group_create(rsvd_group** group, int nranks);
+rsvd_status rsvd_group_destroy(rsvd_group* group);
+rsvd_status rsvd_comm_init_group(rsvd_ctx* ctx, rsvd_group* group, int rank);
 
 /* Input matrix descriptor.  `A` is caller-owned DEVICE memory, read-only,
  * row-major m_local x n with leading dimension lda >= n; it must stay valid
@@ -118,6 +145,19 @@ void rsvd_params_default(rsvd_params* prm, int32_t k);
 rsvd_status rsvd_run(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm,
                      void* u, int64_t ldu, void* d, void* v, int64_t ldv);
 
+/* Device workspace (bytes) the library will own for rsvd_run on this matrix
+ * and these parameters (panels, Ozaki slices of A, TSQR fallback scratch);
+ * HOST out-param.  Validation as rsvd_run; nothing is allocated. */
+rsvd_status rsvd_workspace_bytes(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, size_t* bytes);
+
+/* rsvd_run on HOST buffers (end to end): A is read from host memory (pinned
+ * or pageable; m x n row-major, lda), copied to a device staging buffer the
+ * context owns, factored, and u, d, v are copied back to HOST memory
+ * (layouts as rsvd_run).  Single GPU only.  Blocks until the results are in
+ * host memory; returns the numerical status of the call (as rsvd_sync). */
+rsvd_status rsvd_run_host(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm,
+                          void* u, int64_t ldu, void* d, void* v, int64_t ldv);
+
 /* Randomized QB decomposition, Alg. 4, with the final QR
  * of reading R3.  Q: DEVICE m_local x l (ldq >= l), this rank's rows;
  * Bt: DEVICE n x l (ldb >= l), B^T = A^T Q, replicated.  l = min(k+p, min(m,n)).
@@ -147,17 +187,51 @@ rsvd_status rsvd_rcur(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* pr
                       void* C, int64_t ldc, void* U, int64_t ldu, void* R, int64_t ldr,
                       int64_t* J, int64_t* I);
 
-/* Randomized PCA, Alg. 6, interface P:1381-1398:
- * rsvd on X = (A - 1 c^T) diag(1/s) (centring/scaling never materialised).
- *   rotation DEVICE n x k (ldr >= k)       = V
- *   eigvals  DEVICE k                      = d^2 / (m - 1)   (Eq. P:1322)
- *   x        DEVICE m_local x k (ldx >= k) = U diag(d) scores, NULL = retx FALSE
- *   center   DEVICE n column means (NULL = not returned; prm->center selects)
- *   scale    DEVICE n column s.d. (NULL = not returned)
- * Outputs in the dtype of A. */
-rsvd_status rsvd_rpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm,
-                      void* rotation, int64_t ldr, void* eigvals, void* x, int64_t ldx,
-                      void* center, void* scale);
+/* Randomized PCA, Alg. 6, interface
+ * rpca(A, k, center = TRUE, scale = TRUE, retx = TRUE, p = 10, q = 2)
+ * (P:1381-1398): rsvd on X = (A - 1 c^T) diag(1/s) (centring / scaling never
+ * materialised; prm->center, prm->scale select them, rsvd_rpca_params_default
+ * sets both as the paper does).  Every output is DEVICE memory in the dtype
+ * of A, caller-owned, and NULL = not computed:
+ *   rotation  n x k (ldr >= k)        W = V, the principal directions
+ *   eigvals   k                       Lambda = d^2 / (m - 1)          (Eq. P:1322)
+ *   sdev      k                       sqrt(eigvals)
+ *   x         m_local x k (ldx >= k)  scores Z = X W = U diag(d)      (Eq. PCs; retx)
+ *   center    n                       column means c
+ *   scale     n                       column s.d. s (1 for constant columns)
+ *   loadings  n x k (ldl >= k)        L = W Lambda^{1/2}
+ *   x_white   m_local x k (ldw >= k)  whitened PCs z_i / sqrt(lambda_i) (
+ *                                     reading R32: the text's X L is taken as Z Lambda^{-1/2})
+ *   var_ratio k                       lambda_i / sum_{all} lambda
+ *   var_cum   k                       cumulative proportion of variance (summary())
+ *   total_var 1                       sum of all eigenvalues = trace of the
+ *                                     covariance (correlation) matrix, from the
+ *                                     column sums of squares (one extra pass over
+ *                                     A when scale is FALSE) */
+typedef struct {
+  void* rotation; int64_t ldr;
+  void* eigvals;
+  void* sdev;
+  void* x; int64_t ldx;
+  void* center;
+  void* scale;
+  void* loadings; int64_t ldl;
+  void* x_white; int64_t ldw;
+  void* var_ratio;
+  void* var_cum;
+  void* total_var;
+} rsvd_pca_out;
+void rsvd_rpca_params_default(rsvd_params* prm, int32_t k);   /* rsvd defaults + center = scale = 1 */
+rsvd_status rsvd_rpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, const rsvd_pca_out* out);
+
+/* Out-of-sample projection, predict() of the rpca object: the
+ * scores of new rows, out = ((Anew - 1 c^T) diag(1/s)) W, computed by the same
+ * pass kernels as the sketch.  Anew: rsvd_matrix (DEVICE, m_new x n, dtype of
+ * the outputs); rotation DEVICE n x k (ldr); center, scale DEVICE n (nullable
+ * = no centring / scaling; scale entries must be nonzero); out DEVICE
+ * m_new x k (ldo >= k).  1 <= k <= 128. */
+rsvd_status rsvd_rpca_predict(rsvd_ctx* ctx, const rsvd_matrix* Anew, int32_t k, const void* rotation, int64_t ldr,
+                              const void* center, const void* scale, void* out, int64_t ldo);
 
 /* Randomized robust PCA by inexact ALM, Alg. 7, with the
  * readings R17-R23, R30 of DESIGN.md (mu_0 = 1.25/||A||_2, fresh Omega stream t per
@@ -217,8 +291,8 @@ rsvd_status rsvd_profile_reset(rsvd_ctx* ctx);
 int64_t rsvd_launch_count(const rsvd_ctx* ctx);
 
 /* Diagnostics of the last rsvd-family call (HOST out-param, n <= 4 slots):
- * out[0] = one-sided Jacobi sweeps, out[1] = 1 if the CholeskyQR2 breakdown
- * re-run in robust (Householder / TSQR) mode was taken, out[2] = kernel
+ * out[0] = one-sided Jacobi sweeps, out[1] = 1 if the Householder TSQR
+ * fallback after a CholeskyQR breakdown ran (as of the last rsvd_sync), out[2] = kernel
  * launches since the last rsvd_profile_reset, out[3] = passes run on the
  * FP64 Ozaki tensor-core path since the context was created (RSVD_FP64_PATH=dmma
  * in the environment at rsvd_create selects the FP64 DMMA path instead). */

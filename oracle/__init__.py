@@ -17,7 +17,9 @@ Passages followed (PAPER.md line numbers, "P:n"):
   * Alg. 5 ``rsvd``                P:616-637, Eq. UQU
   * random test matrices          P:417-430 (§2.3)
   * ``rsvd()`` interface           P:706-724 (§3.6)
-  * Alg. 6 ``rpca``                P:1336-1361, Eq. P:1322 (§4.2)
+  * Alg. 6 ``rpca``                P:1336-1361, Eq. P:1322 (§4.2); loadings,
+                                  whitening, explained variance P:1239-1302;
+                                  predict() P:1570
   * Alg. 7 ``rrpca`` (IALM)        P:1655-1723 (§5.3)
   * Alg. id / rid / rcur           P:2059-2127, Alg. rcur P:1975-2010 (§6)
 
@@ -29,9 +31,9 @@ are not available), see DESIGN.md §Readings.
 """
 from .philox import philox4x32_10, omega, u01
 from .linalg import hqr, jacobi_svd_bt, qrcp, soft_threshold
-from .rsvd import (oracle_rqb, oracle_rsvd, oracle_rpca, oracle_rrpca, oracle_id, oracle_rid, oracle_rcur, predict_rank,
-                   resolve_params, sign_fix)
+from .rsvd import (oracle_rqb, oracle_rsvd, oracle_rpca, oracle_rpca_predict, oracle_rrpca, oracle_id, oracle_rid,
+                   oracle_rcur, predict_rank, resolve_params, sign_fix)
 
 __all__ = ["philox4x32_10", "omega", "u01", "hqr", "jacobi_svd_bt",
-           "soft_threshold", "oracle_rqb", "oracle_rsvd", "oracle_rpca",
+           "soft_threshold", "oracle_rqb", "oracle_rsvd", "oracle_rpca", "oracle_rpca_predict",
            "oracle_rrpca", "resolve_params", "sign_fix"]

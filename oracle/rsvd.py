@@ -128,23 +128,48 @@ def oracle_rsvd(A, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0,
     return out
 
 
-def oracle_rpca(A, k, center=True, scale=False, retx=True, p=10, q=2,
+def oracle_rpca(A, k, center=True, scale=True, retx=True, p=10, q=2,
                 sdist="normal", seed=0, stream=0):
-    """Alg. 6 rpca / interface P:1381-1398.
+    """Alg. 6 rpca / interface P:1381-1398 (defaults
+    center = TRUE, scale = TRUE as in P:1381).
 
     rsvd on the centred (and optionally scaled) X; eigenvalues
-    Lambda = Sigma^2 / (m-1) (Eq. P:1322), rotation = V, sdev = sqrt(Lambda),
-    scores x = U Sigma (= X V).
+    Lambda = Sigma^2 / (m-1) (Eq. P:1322), rotation W = V, sdev = sqrt(Lambda)
+    (P:1396), scores x = U Sigma (= X W, Eq. PCs).  Also the quantities of
+    Sections 4.1-4.2 and summary():
+      loadings  L = W Lambda^{1/2}
+      x_white   z_i / sqrt(lambda_i), i.e. Z Lambda^{-1/2} (P:1262-1266;
+                reading R32: the printed "X L" contradicts the line after it,
+                which whitening by 1/sqrt(lambda_i) defines)
+      total_var sum of ALL n eigenvalues = trace of the covariance
+                (correlation) matrix = sum of the column variances of X
+      var_ratio lambda_i / total_var, var_cum its cumulative sum
     """
     r = oracle_rsvd(A, k, p=p, q=q, sdist=sdist, seed=seed, stream=stream,
                     center=center, scale=scale)
-    m = np.asarray(A).shape[0]
+    X, _c, _s = _prepare(A, center, scale)
+    m = X.shape[0]
     eig = r["d"] ** 2 / (m - 1)
-    out = dict(rotation=r["v"], eigvals=eig, sdev=np.sqrt(eig), center=r["center"],
-               scale=r["scale"], d=r["d"])
+    sdev = np.sqrt(eig)
+    total = float(np.sum(X * X) / (m - 1))          # the column variances of X, summed
+    out = dict(rotation=r["v"], eigvals=eig, sdev=sdev, center=r["center"],
+               scale=r["scale"], d=r["d"], loadings=r["v"] * sdev[None, :],
+               total_var=total, var_ratio=eig / total, var_cum=np.cumsum(eig) / total)
     if retx:
         out["x"] = r["u"] * r["d"][None, :]
+        out["x_white"] = out["x"] / sdev[None, :]
     return out
+
+
+def oracle_rpca_predict(Anew, rotation, center=None, scale=None):
+    """predict() of an rpca object: the new rows centred and
+    scaled with the training statistics, then rotated: ((Anew - c) / s) W."""
+    X = np.array(Anew, dtype=np.float64)
+    if center is not None:
+        X = X - np.asarray(center, dtype=np.float64)[None, :]
+    if scale is not None:
+        X = X / np.asarray(scale, dtype=np.float64)[None, :]
+    return X @ np.asarray(rotation, dtype=np.float64)
 
 
 def predict_rank(d, mu_inv, k, minmn):

@@ -10,9 +10,16 @@ raises on import of the library.
 Paper interfaces mirrored:
   rsvd(A, k, nu=NULL, nv=NULL, p=10, q=2, sdist="normal")     P:708   (§3.6)
   rpca(A, k, center=TRUE, scale=TRUE, retx=TRUE, p=10, q=2)   P:1381  (§4.4)
+  predict(rpca object, newdata)
   rrpca(A, lambda=NULL, maxiter=50, tol=1e-5, p=10, q=2, ...) P:1736  (§5.4)
   rqb(A, k, p, q)                                             Alg. 4, P:585
+  rid / rcur
+
+The library's calls only enqueue work on the context's stream; every wrapper
+here calls ``rsvd_sync`` afterwards (and raises on a numerical failure)
+unless ``sync=False`` is passed, in which case ``Context.sync()`` reports it.
 """
+import threading
 import ctypes
 import os
 from collections import namedtuple
@@ -25,8 +32,10 @@ LIB_PATH = os.path.join(_HERE, "_lib", "librsvd_b200.so")
 SDIST = {"normal": 0, "unif": 1, "rademacher": 2}
 STATUS = {0: "RSVD_OK", 1: "RSVD_EINVAL", 2: "RSVD_ENOMEM", 3: "RSVD_ECUDA", 4: "RSVD_ENCCL",
           5: "RSVD_ENUMERIC", 6: "RSVD_EUNSUPPORTED"}
-EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_last_error", "rsvd_version", "rsvd_nccl_unique_id",
-           "rsvd_comm_init", "rsvd_params_default", "rsvd_run", "rsvd_rqb", "rsvd_rpca",
+EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_last_error", "rsvd_version", "rsvd_sync", "rsvd_nccl_unique_id",
+           "rsvd_comm_init", "rsvd_group_create", "rsvd_group_destroy", "rsvd_comm_init_group",
+           "rsvd_params_default", "rsvd_workspace_bytes", "rsvd_run", "rsvd_run_host", "rsvd_rqb",
+           "rsvd_rpca_params_default", "rsvd_rpca", "rsvd_rpca_predict",
            "rsvd_rrpca_params_default", "rsvd_rrpca", "rsvd_omega", "rsvd_set_profiling", "rsvd_profile",
            "rsvd_profile_reset", "rsvd_launch_count", "rsvd_stats", "rsvd_rid", "rsvd_rcur"]
 
@@ -50,6 +59,14 @@ class Params(ctypes.Structure):
                 ("power", ctypes.c_int32)]
 
 POWER = {"subspace": 0, "direct": 1, "lu": 2}
+
+
+class PcaOut(ctypes.Structure):
+    _fields_ = [("rotation", ctypes.c_void_p), ("ldr", ctypes.c_int64), ("eigvals", ctypes.c_void_p),
+                ("sdev", ctypes.c_void_p), ("x", ctypes.c_void_p), ("ldx", ctypes.c_int64),
+                ("center", ctypes.c_void_p), ("scale", ctypes.c_void_p), ("loadings", ctypes.c_void_p),
+                ("ldl", ctypes.c_int64), ("x_white", ctypes.c_void_p), ("ldw", ctypes.c_int64),
+                ("var_ratio", ctypes.c_void_p), ("var_cum", ctypes.c_void_p), ("total_var", ctypes.c_void_p)]
 
 
 class RrpcaParams(ctypes.Structure):
@@ -76,12 +93,20 @@ def lib():
         "rsvd_destroy": ([vp], ctypes.c_int),
         "rsvd_last_error": ([vp], ctypes.c_char_p),
         "rsvd_version": ([], ctypes.c_char_p),
+        "rsvd_sync": ([vp], ctypes.c_int),
         "rsvd_nccl_unique_id": ([vp], ctypes.c_int),
         "rsvd_comm_init": ([vp, vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+        "rsvd_group_create": ([ctypes.POINTER(vp), ctypes.c_int], ctypes.c_int),
+        "rsvd_group_destroy": ([vp], ctypes.c_int),
+        "rsvd_comm_init_group": ([vp, vp, ctypes.c_int], ctypes.c_int),
         "rsvd_params_default": ([PP, i32], None),
+        "rsvd_rpca_params_default": ([PP, i32], None),
+        "rsvd_workspace_bytes": ([vp, MP, PP, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
         "rsvd_run": ([vp, MP, PP, vp, i64, vp, vp, i64], ctypes.c_int),
+        "rsvd_run_host": ([vp, MP, PP, vp, i64, vp, vp, i64], ctypes.c_int),
         "rsvd_rqb": ([vp, MP, PP, vp, i64, vp, i64], ctypes.c_int),
-        "rsvd_rpca": ([vp, MP, PP, vp, i64, vp, vp, i64, vp, vp], ctypes.c_int),
+        "rsvd_rpca": ([vp, MP, PP, ctypes.POINTER(PcaOut)], ctypes.c_int),
+        "rsvd_rpca_predict": ([vp, MP, i32, vp, i64, vp, vp, vp, i64], ctypes.c_int),
         "rsvd_rrpca_params_default": ([ctypes.POINTER(RrpcaParams)], None),
         "rsvd_rid": ([vp, MP, PP, vp, i64, vp, i64, vp], i32),
         "rsvd_rcur": ([vp, MP, PP, vp, i64, vp, i64, vp, i64, vp, vp], i32),
@@ -130,8 +155,32 @@ class Context:
         if st != 0:
             raise RsvdError(st, lib().rsvd_last_error(self.h).decode())
 
+    def sync(self):
+        """Wait for this context's stream; raise on a numerical failure recorded by
+        the calls completed since the last sync (rsvd_sync)."""
+        self.check(lib().rsvd_sync(self.h))
+
+    def finish(self, st, sync):
+        self.check(st)
+        if sync:
+            self.sync()
+
     def last_error(self):
         return lib().rsvd_last_error(self.h).decode()
+
+    def init_group(self, group, rank):
+        """Join an in-process RankGroup as `rank` (collectives as fixed-order
+        device reductions; one host thread per member context)."""
+        self.check(lib().rsvd_comm_init_group(self.h, group.h, int(rank)))
+        self.rank, self.world = int(rank), group.n
+
+    def workspace_bytes(self, A, k, p=10, q=2, m_global=None, row_offset=0, center=False, scale=False):
+        """Device workspace the library will own for rsvd(A, k, p, q) (rsvd_workspace_bytes)."""
+        mat = _matrix(A, m_global, row_offset)
+        prm = _params(k, k, k, p, q, "normal", 0, 0, center, scale)
+        out = ctypes.c_size_t()
+        self.check(lib().rsvd_workspace_bytes(self.h, ctypes.byref(mat), ctypes.byref(prm), ctypes.byref(out)))
+        return int(out.value)
 
     def init_comm(self, rank, world, group=None):
         """NCCL communicator owned by the library: rank 0 makes the unique id,
@@ -167,7 +216,7 @@ class Context:
         """(Jacobi sweeps, robust re-run taken, kernel launches, Ozaki passes) of the last call."""
         buf = (ctypes.c_int64 * 4)()
         self.check(lib().rsvd_stats(self.h, buf, 4))
-        return dict(jacobi_sweeps=int(buf[0]), robust_rerun=bool(buf[1]), launches=int(buf[2]),
+        return dict(jacobi_sweeps=int(buf[0]), tsqr_fallback=bool(buf[1]), launches=int(buf[2]),
                     ozaki_passes=int(buf[3]))
 
     def close(self):
@@ -180,6 +229,66 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+class RankGroup:
+    """In-process rank group (rsvd_group): `n` member contexts, each driven by
+    its own host thread, run the row-sharded algorithm together; the
+    collectives are fixed-rank-order device reductions."""
+
+    def __init__(self, n):
+        h = ctypes.c_void_p()
+        st = lib().rsvd_group_create(ctypes.byref(h), int(n))
+        if st != 0:
+            raise RsvdError(st, "rsvd_group_create(%d) failed" % n)
+        self.h, self.n = h, int(n)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().rsvd_group_destroy(self.h)
+            self.h = None
+
+
+def row_partition(m, world):
+    """Contiguous row blocks of m rows over `world` ranks: [(offset, rows), ...]."""
+    bounds = [(m * r) // world for r in range(world + 1)]
+    return [(bounds[r], bounds[r + 1] - bounds[r]) for r in range(world)]
+
+
+def run_ranks(fn, world, device=None):
+    """Run fn(ctx, rank) for rank = 0..world-1 on one device as an in-process
+    rank group (one thread and one stream per rank).  Returns the results in
+    rank order; re-raises the first exception."""
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index
+    group = RankGroup(world)
+    streams = [torch.cuda.Stream(dev) for _ in range(world)]
+    ctxs = []
+    for r in range(world):
+        c = Context(dev, streams[r])
+        c.init_group(group, r)
+        ctxs.append(c)
+    out, err = [None] * world, [None] * world
+
+    def body(r):
+        try:
+            with torch.cuda.stream(streams[r]):
+                out[r] = fn(ctxs[r], r)
+                ctxs[r].sync()
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            err[r] = e
+
+    threads = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for c in ctxs:
+        c.close()
+    group.close()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
 
 
 _default_ctx = {}
@@ -225,7 +334,7 @@ RsvdResult = namedtuple("RsvdResult", ["d", "u", "v"])
 
 
 def rsvd(A, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None,
-         m_global=None, row_offset=0, out=None, power="subspace"):
+         m_global=None, row_offset=0, out=None, power="subspace", sync=True):
     """Randomized SVD (Alg. 5; interface P:708).
 
     power: "subspace" (Alg. 2, QR between passes), "direct" (Alg. 1) or "lu"
@@ -241,31 +350,45 @@ def rsvd(A, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0, stream=0, ct
     nu_ = kk if nu is None else min(int(nu), kk)
     nv_ = kk if nv is None else min(int(nv), kk)
     prm = _params(k, nu, nv, p, q, sdist, seed, stream, power=power)
-    if not (1 <= kk <= min(mg, A.shape[1])):
-        raise RsvdError(1, "k must satisfy 1 <= k <= min(m, n)")
     if out is None:
-        d = torch.empty(kk, dtype=A.dtype, device=A.device)
+        d = torch.empty(max(kk, 0), dtype=A.dtype, device=A.device)
         u = torch.empty(A.shape[0], max(nu_, 0), dtype=A.dtype, device=A.device)
         v = torch.empty(A.shape[1], max(nv_, 0), dtype=A.dtype, device=A.device)
     else:
         d, u, v = out
-    ctx.check(lib().rsvd_run(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(u) if nu_ else ctypes.c_void_p(0),
-                             max(nu_, 1), _ptr(d), _ptr(v) if nv_ else ctypes.c_void_p(0), max(nv_, 1)))
+    ctx.finish(lib().rsvd_run(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(u) if nu_ else ctypes.c_void_p(0),
+                              max(nu_, 1), _ptr(d), _ptr(v) if nv_ else ctypes.c_void_p(0), max(nv_, 1)), sync)
     return RsvdResult(d, u, v)
 
 
 def rsvd_host(A_host, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None,
-              device="cuda", staging=None):
-    """End-to-end call on a HOST matrix: H2D copy of A, rsvd, D2H of (d, u, v)."""
+              device="cuda", out=None):
+    """End to end on HOST memory (rsvd_run_host): the library copies A (a CPU
+    tensor, pinned for full copy bandwidth) to its device staging buffer,
+    factors it and copies (d, u, v) back into CPU tensors (`out` to reuse them)."""
     ctx = ctx or default_context(device)
-    if staging is None or staging.shape != A_host.shape or staging.dtype != A_host.dtype:
-        staging = torch.empty(A_host.shape, dtype=A_host.dtype, device=device)
-    staging.copy_(A_host, non_blocking=True)
-    r = rsvd(staging, k, nu, nv, p, q, sdist, seed, stream, ctx=ctx)
-    return RsvdResult(r.d.to("cpu", non_blocking=False), r.u.to("cpu"), r.v.to("cpu"))
+    if A_host.is_cuda or A_host.dim() != 2 or A_host.stride(1) != 1:
+        raise ValueError("A_host must be a 2-D row-major CPU tensor")
+    m, n = A_host.shape
+    kk = int(k)
+    nu_ = kk if nu is None else min(int(nu), kk)
+    nv_ = kk if nv is None else min(int(nv), kk)
+    dt = 0 if A_host.dtype == torch.float64 else 1
+    mat = Matrix(dt, A_host.data_ptr(), m, n, A_host.stride(0), m, 0)
+    prm = _params(k, nu_, nv_, p, q, sdist, seed, stream)
+    if out is None:
+        pin = torch.cuda.is_available()
+        d = torch.empty(kk, dtype=A_host.dtype, pin_memory=pin)
+        u = torch.empty(m, max(nu_, 0), dtype=A_host.dtype, pin_memory=pin)
+        v = torch.empty(n, max(nv_, 0), dtype=A_host.dtype, pin_memory=pin)
+    else:
+        d, u, v = out
+    ctx.check(lib().rsvd_run_host(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(u) if nu_ else ctypes.c_void_p(0),
+                                  max(nu_, 1), _ptr(d), _ptr(v) if nv_ else ctypes.c_void_p(0), max(nv_, 1)))
+    return RsvdResult(d, u, v)
 
 
-def rqb(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None, m_global=None, row_offset=0):
+def rqb(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None, m_global=None, row_offset=0, sync=True):
     """Randomized QB (Alg. 4): returns (Q (m x l), B (l x n))."""
     ctx = ctx or default_context(A.device)
     mat = _matrix(A, m_global, row_offset)
@@ -273,11 +396,11 @@ def rqb(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None, m_global=No
     Q = torch.empty(A.shape[0], l, dtype=A.dtype, device=A.device)
     Bt = torch.empty(A.shape[1], l, dtype=A.dtype, device=A.device)
     prm = _params(k, 0, 0, p, q, sdist, seed, stream)
-    ctx.check(lib().rsvd_rqb(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(Q), l, _ptr(Bt), l))
+    ctx.finish(lib().rsvd_rqb(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(Q), l, _ptr(Bt), l), sync)
     return Q, Bt.T
 
 
-def rid(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None, m_global=None, row_offset=0):
+def rid(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None, m_global=None, row_offset=0, sync=True):
     """Randomized column ID (Alg. rid; Alg. id):
     returns dict(C (m x k) = A[:, J], Z (k x n), J (k,) int64 pivot order)."""
     ctx = ctx or default_context(A.device)
@@ -288,11 +411,11 @@ def rid(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None, m_global=No
     Z = torch.empty(kk, n, dtype=A.dtype, device=A.device)
     J = torch.empty(kk, dtype=torch.int64, device=A.device)
     prm = _params(k, 0, 0, p, q, sdist, seed, stream)
-    ctx.check(lib().rsvd_rid(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(C), kk, _ptr(Z), n, _ptr(J)))
+    ctx.finish(lib().rsvd_rid(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(C), kk, _ptr(Z), n, _ptr(J)), sync)
     return dict(C=C, Z=Z, J=J)
 
 
-def rcur(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None):
+def rcur(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None, sync=True):
     """Randomized CUR (Alg. rcur): A ~ C U R; returns
     dict(C (m x k), U (k x k), R (k x n), J (column indices), I (row indices))."""
     ctx = ctx or default_context(A.device)
@@ -305,27 +428,65 @@ def rcur(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None):
     J = torch.empty(kk, dtype=torch.int64, device=A.device)
     I = torch.empty(kk, dtype=torch.int64, device=A.device)
     prm = _params(k, 0, 0, p, q, sdist, seed, stream)
-    ctx.check(lib().rsvd_rcur(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(C), kk, _ptr(U), kk, _ptr(R), n,
-                              _ptr(J), _ptr(I)))
+    ctx.finish(lib().rsvd_rcur(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(C), kk, _ptr(U), kk, _ptr(R), n,
+                               _ptr(J), _ptr(I)), sync)
     return dict(C=C, U=U, R=R, J=J, I=I)
 
 
-def rpca(A, k, center=True, scale=False, retx=True, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None,
-         m_global=None, row_offset=0):
-    """Randomized PCA (Alg. 6; interface P:1381-1398)."""
+def rpca(A, k, center=True, scale=True, retx=True, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None,
+         m_global=None, row_offset=0, loadings=False, whiten=False, explained=False, sync=True):
+    """Randomized PCA (Alg. 6; interface
+    rpca(A, k, center=TRUE, scale=TRUE, retx=TRUE, p=10, q=2), P:1381-1398).
+
+    Returns dict(rotation, eigvals, sdev, x (retx), center, scale) and, on
+    request, loadings = W Lambda^1/2, x_white = the whitened PCs
+    (P:1262-1266), var_ratio / var_cum / total_var = the explained variance of
+    summary().  Every value is computed by the library."""
     ctx = ctx or default_context(A.device)
     mat = _matrix(A, m_global, row_offset)
     m, n = A.shape
     kk = int(k)
-    rot = torch.empty(n, kk, dtype=A.dtype, device=A.device)
-    eig = torch.empty(kk, dtype=A.dtype, device=A.device)
-    x = torch.empty(m, kk, dtype=A.dtype, device=A.device) if retx else None
-    c = torch.empty(n, dtype=A.dtype, device=A.device) if center else None
-    s = torch.empty(n, dtype=A.dtype, device=A.device) if scale else None
+    dev, dt = A.device, A.dtype
+    res = dict(rotation=torch.empty(n, kk, dtype=dt, device=dev), eigvals=torch.empty(kk, dtype=dt, device=dev),
+               sdev=torch.empty(kk, dtype=dt, device=dev),
+               x=torch.empty(m, kk, dtype=dt, device=dev) if retx else None,
+               center=torch.empty(n, dtype=dt, device=dev) if center else None,
+               scale=torch.empty(n, dtype=dt, device=dev) if scale else None)
+    if loadings:
+        res["loadings"] = torch.empty(n, kk, dtype=dt, device=dev)
+    if whiten:
+        res["x_white"] = torch.empty(m, kk, dtype=dt, device=dev)
+    if explained:
+        res["var_ratio"] = torch.empty(kk, dtype=dt, device=dev)
+        res["var_cum"] = torch.empty(kk, dtype=dt, device=dev)
+        res["total_var"] = torch.empty(1, dtype=dt, device=dev)
+    o = PcaOut()
+    o.rotation, o.ldr = _ptr(res["rotation"]), kk
+    o.eigvals, o.sdev = _ptr(res["eigvals"]), _ptr(res["sdev"])
+    o.x, o.ldx = _ptr(res["x"]), kk
+    o.center, o.scale = _ptr(res["center"]), _ptr(res["scale"])
+    o.loadings, o.ldl = _ptr(res.get("loadings")), kk
+    o.x_white, o.ldw = _ptr(res.get("x_white")), kk
+    o.var_ratio, o.var_cum, o.total_var = _ptr(res.get("var_ratio")), _ptr(res.get("var_cum")), _ptr(res.get("total_var"))
     prm = _params(k, k, k, p, q, sdist, seed, stream, center, scale)
-    ctx.check(lib().rsvd_rpca(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(rot), kk, _ptr(eig), _ptr(x), kk,
-                              _ptr(c), _ptr(s)))
-    return dict(rotation=rot, eigvals=eig, sdev=eig.sqrt(), x=x, center=c, scale=s)
+    ctx.finish(lib().rsvd_rpca(ctx.h, ctypes.byref(mat), ctypes.byref(prm), ctypes.byref(o)), sync)
+    if explained:
+        res["total_var"] = res["total_var"][0]
+    return res
+
+
+def predict(obj, Anew, ctx=None, sync=True):
+    """Out-of-sample projection of an rpca result (predict()):
+    ((Anew - center) / scale) @ rotation, by the library's pass kernels."""
+    ctx = ctx or default_context(Anew.device)
+    mat = _matrix(Anew)
+    rot = obj["rotation"]
+    kk = rot.shape[1]
+    out = torch.empty(Anew.shape[0], kk, dtype=Anew.dtype, device=Anew.device)
+    c, s = obj.get("center"), obj.get("scale")
+    ctx.finish(lib().rsvd_rpca_predict(ctx.h, ctypes.byref(mat), kk, _ptr(rot), rot.stride(0), _ptr(c), _ptr(s),
+                                       _ptr(out), kk), sync)
+    return out
 
 
 def rrpca(A, lam=None, maxiter=50, tol=1e-5, p=10, q=2, k=20, sdist="normal", seed=0, trace=False, ctx=None,
@@ -364,8 +525,8 @@ def omega(n, l, sdist="normal", seed=0, stream=0, dtype=torch.float64, device="c
     ctx = ctx or default_context(device)
     out = torch.empty(n, l, dtype=dtype, device=device)
     sd = SDIST[sdist] if isinstance(sdist, str) else int(sdist)
-    ctx.check(lib().rsvd_omega(ctx.h, n, l, sd, int(seed), int(stream), 1 if dtype == torch.float32 else 0,
-                               _ptr(out), l))
+    ctx.finish(lib().rsvd_omega(ctx.h, n, l, sd, int(seed), int(stream), 1 if dtype == torch.float32 else 0,
+                                _ptr(out), l), True)
     return out
 
 

@@ -1,6 +1,7 @@
 // api.cu -- C ABI (include/rsvd_b200.h) and the host orchestrator of the
 // randomized SVD hot path.  Host code only; every numerical step runs in the
-// kernels of gemm_pass.cu / omega.cu / panel.cu / ialm.cu on ctx->stream.
+// kernels of pass_ozaki.cu / pass_tf32.cu / gemm_pass.cu / omega.cu /
+// cholqr.cu / panel.cu / jacobi.cu / qrcp.cu / ialm.cu on ctx->stream.
 //
 // Pass schedule of one rsvd (Alg. 4 + Alg. 2 + Alg. 5):
 //   K1 Omega -> X                                   (Alg. 4 step 2)
@@ -9,11 +10,12 @@
 //   orth(Y) -> Q ; K3 B^T = A^T Q (+allreduce)      (steps 9, 10; pass 2q+2)
 //   orth(B^T) -> Q_B, R_B ; Jacobi(R_B^T) -> Sigma, U~ (= W), J
 //   V = Q_B J ; signs from V (reading R9) ; U = Q (U~ diag(sgn))   (Alg. 5 steps 2-3)
-// orth = CholeskyQR2 (Gram by K3, l x l Cholesky, Y R^-1 by K2) with a
-// breakdown flag, or Householder (one CTA) when the panel fits in shared
-// memory, or TSQR (Householder leaves + combine) in robust mode.  A CholQR2
-// breakdown anywhere re-runs the whole call in robust mode (one status read
-// per call, no per-panel host synchronisation).
+// orth = CholeskyQR (intermediate) / CholeskyQR2 (final) with a breakdown bit
+// in the call's status word; the Householder TSQR fallback kernels are
+// enqueued behind every CholeskyQR and run only once that bit is set (device
+// predicate).  Panels that fit one CTA use Householder QR
+// directly.  No call synchronises with the host except rsvd_sync, rsvd_rrpca
+// and rsvd_run_host.
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdarg.h>
@@ -23,8 +25,10 @@
 
 #include <algorithm>
 #include <chrono>
-#include <functional>
 #include <cmath>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -36,13 +40,66 @@ using namespace rsvd;
 
 namespace {
 
-constexpr int kFlagCholBreak = 1, kFlagJacobiCap = 2, kFlagNonFinite = 4, kFlagRankDef = 8,
-              kFlagLuZero = 16;   // informational: an exactly zero LU pivot (multipliers set to 0)
+// bits of the call's status word flags_dev[0] (flags_dev[8] = Jacobi sweeps)
+constexpr int kFlagCholBreak = 1,   // a CholeskyQR broke down: the TSQR fallback runs (not an error)
+              kFlagJacobiCap = 2,   // one-sided Jacobi hit the sweep cap (error)
+              kFlagNonFinite = 4,   // non-finite input / intermediate (error)
+              kFlagRankDef = 8,     // rid / rcur: numerical rank of the pivoted QR < k (error)
+              kFlagLuZero = 16,     // informational: an exactly zero LU pivot (multipliers set to 0)
+              kFlagNoFallback = 32; // a breakdown with no TSQR fallback possible for the shape (error)
 constexpr int kMaxL = 120;       // Jacobi + leaf QR shared-memory envelope
 
 struct ProfRec { int kind; double bytes; cudaEvent_t a, b; };
 
 }  // namespace
+
+// ----------------------------------------------------------------- collectives
+// The row-sharded path needs sum / max allreduces and one allgather; they are
+// behind this interface so that the same orchestration runs over NCCL (one
+// process per GPU) or over an in-process rank group (rsvd_group).
+struct Comm {
+  virtual ~Comm() {}
+  virtual int nranks() const = 0;
+  virtual int rank() const = 0;
+  virtual rsvd_status allreduce(rsvd_ctx* ctx, double* buf, size_t n, bool op_max) = 0;
+  virtual rsvd_status allgather(rsvd_ctx* ctx, const double* send, double* recv, size_t n) = 0;
+  // a member returns an error from a call: peers must not wait for it
+  virtual void on_error() {}
+};
+
+struct rsvd_group {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool aborted = false;
+  struct Slot {
+    double* stage = nullptr; size_t cap = 0; int device = 0;
+    cudaEvent_t ready = nullptr, done = nullptr; bool done_valid = false;
+    bool joined = false;
+  };
+  std::vector<Slot> slots;
+  // host barrier over the n member threads; false if the group was aborted
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (aborted) return false;
+    const uint64_t g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    cv.wait(lk, [&] { return gen != g || aborted; });
+    return !aborted;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
+  }
+};
 
 struct rsvd_ctx {
   int device = 0;
@@ -52,16 +109,19 @@ struct rsvd_ctx {
   // workspace (grown on demand; kept between calls)
   char* ws = nullptr;
   size_t ws_bytes = 0;
-  char* ws2 = nullptr;            // robust-mode TSQR stacks / rrpca buffers
+  char* ws2 = nullptr;            // TSQR stacks, LU / pivoted-QR scratch
   size_t ws2_bytes = 0;
-  int* flags_dev = nullptr;
+  int* flags_dev = nullptr;       // the call's status word (16 ints)
+  int* sticky_dev = nullptr;      // accumulated status for rsvd_sync (4 ints)
   int* flags_host = nullptr;      // pinned
   int* sweeps_dev = nullptr;
   double* hbuf = nullptr;         // pinned host scratch (small D2H/H2D transfers)
   char* ws3 = nullptr;            // rrpca buffers
   size_t ws3_bytes = 0;
+  char* ws5 = nullptr;            // rsvd_run_host device staging
+  size_t ws5_bytes = 0;
   // comm
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;
   int nranks = 1, rank = 0;
   // profiling
   int prof = 0;                   // 0 off, 1 every kind, 2 the pass kernels only (kinds 0, 1, 6)
@@ -72,7 +132,6 @@ struct rsvd_ctx {
   double prof_ms[7] = {0, 0, 0, 0, 0, 0, 0};
   double prof_bytes[7] = {0, 0, 0, 0, 0, 0, 0};
   int64_t prof_count[7] = {0, 0, 0, 0, 0, 0, 0};
-  int64_t launches = 0;
   int last_sweeps = 0;
   bool fp32_tcgen05 = true;       // RSVD_FP32_PATH=dmma selects the FP64-DMMA path for FP32 inputs
   bool fp64_ozaki = true;         // RSVD_FP64_PATH=dmma selects the DMMA path for FP64 inputs
@@ -80,7 +139,7 @@ struct rsvd_ctx {
   size_t ws4_bytes = 0;
   int64_t ozaki_calls = 0;
   int last_robust = 0;
-  unsigned* gemm_flags = nullptr; // stream-K fix-up flags (kMaxGrid, zeroed at creation)
+  unsigned* gemm_flags = nullptr; // stream-K fix-up flags / counters (4096, zeroed at creation)
   unsigned gemm_epoch = 0;
 };
 
@@ -92,7 +151,10 @@ rsvd_status fail(rsvd_ctx* c, rsvd_status s, const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(buf, sizeof buf, fmt, ap);
   va_end(ap);
-  if (c) c->err = buf;
+  if (c) {
+    c->err = buf;
+    if (c->comm) c->comm->on_error();   // an in-process rank group is aborted (its peers return RSVD_ENCCL)
+  }
   return s;
 }
 
@@ -109,6 +171,93 @@ rsvd_status fail(rsvd_ctx* c, rsvd_status s, const char* fmt, ...) {
     rsvd_status s_ = (expr);              \
     if (s_ != RSVD_OK) return s_;         \
   } while (0)
+
+// ----------------------------------------------------------------- NCCL / group communicators
+struct NcclComm : Comm {
+  ncclComm_t c = nullptr;
+  int n = 1, r = 0;
+  ~NcclComm() override { if (c) ncclCommDestroy(c); }
+  int nranks() const override { return n; }
+  int rank() const override { return r; }
+  rsvd_status allreduce(rsvd_ctx* ctx, double* buf, size_t cnt, bool op_max) override {
+    ncclResult_t e = ncclAllReduce(buf, buf, cnt, ncclDouble, op_max ? ncclMax : ncclSum, c, ctx->stream);
+    ncclResult_t async = ncclSuccess;
+    if (e == ncclSuccess && ncclCommGetAsyncError(c, &async) == ncclSuccess && async != ncclSuccess &&
+        async != ncclInProgress)
+      e = async;
+    if (e != ncclSuccess) return fail(ctx, RSVD_ENCCL, "ncclAllReduce: %s", ncclGetErrorString(e));
+    return RSVD_OK;
+  }
+  rsvd_status allgather(rsvd_ctx* ctx, const double* send, double* recv, size_t cnt) override {
+    const ncclResult_t e = ncclAllGather(send, recv, cnt, ncclDouble, c, ctx->stream);
+    if (e != ncclSuccess) return fail(ctx, RSVD_ENCCL, "ncclAllGather: %s", ncclGetErrorString(e));
+    return RSVD_OK;
+  }
+};
+
+// In-process rank group: rank r stages its buffer, every rank then reduces all
+// the stages in rank order into its own buffer (identical bits everywhere).
+// Two host barriers per collective; a rank's stage is rewritten only after
+// every rank's reduction that read it (the previous `done` events) finished.
+struct GroupComm : Comm {
+  rsvd_group* g = nullptr;
+  int r = 0;
+  void on_error() override { g->abort(); }
+  int nranks() const override { return g->n; }
+  int rank() const override { return r; }
+  rsvd_status stage(rsvd_ctx* ctx, const double* src, size_t cnt) {
+    rsvd_group::Slot& me = g->slots[r];
+    if (me.cap < cnt) {
+      // every member's reduction of the previous collective may still read this
+      // stage: wait for all of them (their `done` events precede the last barrier)
+      for (int s = 0; s < g->n; ++s)
+        if (g->slots[s].done_valid) cudaEventSynchronize(g->slots[s].done);
+      cudaStreamSynchronize(ctx->stream);
+      if (me.stage) cudaFree(me.stage);
+      me.stage = nullptr; me.cap = 0;
+      const size_t cap = std::max(cnt, (size_t)1 << 16);   // >= 512 KB: few regrowths
+      if (cudaMalloc(&me.stage, cap * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        g->abort();
+        return fail(ctx, RSVD_ENOMEM, "rank group staging of %zu doubles failed", cap);
+      }
+      me.cap = cap;
+    }
+    for (int s = 0; s < g->n; ++s)
+      if (g->slots[s].done_valid) CK(cudaStreamWaitEvent(ctx->stream, g->slots[s].done, 0));
+    CK(cudaMemcpyAsync(me.stage, src, cnt * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaEventRecord(me.ready, ctx->stream));
+    if (!g->barrier()) return fail(ctx, RSVD_ENCCL, "rank group aborted by another member");
+    for (int s = 0; s < g->n; ++s) CK(cudaStreamWaitEvent(ctx->stream, g->slots[s].ready, 0));
+    return RSVD_OK;
+  }
+  rsvd_status finish(rsvd_ctx* ctx) {
+    rsvd_group::Slot& me = g->slots[r];
+    CK(cudaEventRecord(me.done, ctx->stream));
+    me.done_valid = true;
+    if (!g->barrier()) return fail(ctx, RSVD_ENCCL, "rank group aborted by another member");
+    return RSVD_OK;
+  }
+  rsvd_status allreduce(rsvd_ctx* ctx, double* buf, size_t cnt, bool op_max) override {
+    rsvd_status s = stage(ctx, buf, cnt);
+    if (s != RSVD_OK) { g->abort(); return s; }
+    GroupPtrs in{};
+    for (int q = 0; q < g->n; ++q) in.p[q] = g->slots[q].stage;
+    const cudaError_t e = launch_group_reduce(in, g->n, (int64_t)cnt, op_max ? 1 : 0, buf, ctx->stream);
+    if (e != cudaSuccess) { g->abort(); return fail(ctx, RSVD_ECUDA, "group reduce: %s", cudaGetErrorString(e)); }
+    return finish(ctx);
+  }
+  rsvd_status allgather(rsvd_ctx* ctx, const double* send, double* recv, size_t cnt) override {
+    rsvd_status s = stage(ctx, send, cnt);
+    if (s != RSVD_OK) { g->abort(); return s; }
+    for (int q = 0; q < g->n; ++q) {
+      const cudaError_t e = cudaMemcpyAsync(recv + (size_t)q * cnt, g->slots[q].stage, cnt * sizeof(double),
+                                            cudaMemcpyDeviceToDevice, ctx->stream);
+      if (e != cudaSuccess) { g->abort(); return fail(ctx, RSVD_ECUDA, "group allgather: %s", cudaGetErrorString(e)); }
+    }
+    return finish(ctx);
+  }
+};
 
 cudaEvent_t take_event(rsvd_ctx* c) {
   if (!c->pool.empty()) {
@@ -155,24 +304,26 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // ----------------------------------------------------------------- workspace plan
 struct Plan {
   int64_t M, n;      // local rows, columns (after the m < n transpose swap: M x n "A")
-  int l, Np;         // sketch width, padded width (multiple of 8)
+  int l, Np;         // sketch width, padded width (multiple of 16)
   bool f32;
   bool trans_input;  // single-GPU m < n: work on A^T without copying
   bool scaled = false;  // implicit column scaling active (rpca scale = TRUE)
   const void* A; int64_t lda;
   int64_t m_global;
   // workspace offsets
-  size_t oX, oY, oT, oZ, oPart, oSmall, oColc, oColr, oColp, oSplit, oJlog, total;
+  size_t oX, oY, oT, oZ, oPart, oSmall, oColc, oColr, oColp, oColss, oSplit, oJlog, total;
   bool use_tf32 = false;          // FP32 A on tcgen05 (3-term TF32 split)
   bool use_ozaki = false;         // FP64 A on tcgen05 (Ozaki int8 slices)
   OzakiA oz{};
   void* ozx = nullptr;            // X slice scratch
   void* ozx2 = nullptr;           // second 64-column block (Np > 64)
+  size_t oz_bytes = 0;            // Ozaki slices + X scratch
   float* split = nullptr;
   void* jlog = nullptr;
   size_t part_bytes;
   // small-buffer offsets (doubles from oSmall)
-  double *X, *Y, *T, *Z, *part, *G, *Rinv, *R1, *R2, *RB, *W, *J, *sigma, *sgn, *colc, *colr, *cols, *colp, *Rsm;
+  double *X, *Y, *T, *Z, *part, *G, *Rinv, *R1, *R2, *RB, *W, *J, *sigma, *sgn, *colc, *colr, *cols, *colp, *colss,
+      *Rsm, *tv;
 };
 
 bool small_panel(int64_t rows, int l) { return rows <= leaf_rows_cap(l); }
@@ -196,37 +347,29 @@ size_t plan_bytes(rsvd_ctx* ctx, Plan& p) {
   p.oT = o; o = align256(o + (size_t)big * Np * 8);
   p.oZ = o; o = align256(o + (size_t)p.n * Np * 8);
   p.oPart = o; o = align256(o + part);
-  p.oSmall = o; o = align256(o + (size_t)(9 * Np * Np + 4 * Np) * 8);
+  p.oSmall = o; o = align256(o + (size_t)(9 * Np * Np + 4 * Np + 8) * 8);
   p.oColc = o; o = align256(o + (size_t)p.n * 8);
   p.oColr = o; o = align256(o + (size_t)p.n * 16);
   p.oColp = o; o = align256(o + colsum_partial_bytes(p.M, p.n) + 256);
+  p.oColss = o; o = align256(o + (size_t)p.n * 8);
   p.oSplit = o; o = align256(o + (p.use_tf32 ? tf32_split_bytes(big, Np) : 0));
   p.oJlog = o; o = align256(o + jacobi_scratch_bytes(p.l));
   p.total = o;
   return o;
 }
 
-rsvd_status ensure_ws(rsvd_ctx* ctx, size_t bytes) {
-  if (bytes <= ctx->ws_bytes) return RSVD_OK;
-  if (ctx->ws) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->ws); ctx->ws = nullptr; ctx->ws_bytes = 0; }
-  if (cudaMalloc(&ctx->ws, bytes) != cudaSuccess) {
+rsvd_status ensure_buf(rsvd_ctx* ctx, char** buf, size_t* have, size_t bytes, const char* what) {
+  if (bytes <= *have) return RSVD_OK;
+  if (*buf) { cudaStreamSynchronize(ctx->stream); cudaFree(*buf); *buf = nullptr; *have = 0; }
+  if (cudaMalloc(buf, bytes) != cudaSuccess) {
     cudaGetLastError();
-    return fail(ctx, RSVD_ENOMEM, "workspace allocation of %zu bytes failed", bytes);
+    return fail(ctx, RSVD_ENOMEM, "%s allocation of %zu bytes failed", what, bytes);
   }
-  ctx->ws_bytes = bytes;
+  *have = bytes;
   return RSVD_OK;
 }
-
-rsvd_status ensure_ws2(rsvd_ctx* ctx, size_t bytes) {
-  if (bytes <= ctx->ws2_bytes) return RSVD_OK;
-  if (ctx->ws2) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->ws2); ctx->ws2 = nullptr; ctx->ws2_bytes = 0; }
-  if (cudaMalloc(&ctx->ws2, bytes) != cudaSuccess) {
-    cudaGetLastError();
-    return fail(ctx, RSVD_ENOMEM, "workspace allocation of %zu bytes failed", bytes);
-  }
-  ctx->ws2_bytes = bytes;
-  return RSVD_OK;
-}
+rsvd_status ensure_ws(rsvd_ctx* ctx, size_t bytes) { return ensure_buf(ctx, &ctx->ws, &ctx->ws_bytes, bytes, "workspace"); }
+rsvd_status ensure_ws2(rsvd_ctx* ctx, size_t bytes) { return ensure_buf(ctx, &ctx->ws2, &ctx->ws2_bytes, bytes, "TSQR / scratch workspace"); }
 
 void bind(rsvd_ctx* ctx, Plan& p) {
   char* b = ctx->ws;
@@ -236,24 +379,23 @@ void bind(rsvd_ctx* ctx, Plan& p) {
   double* s = (double*)(b + p.oSmall);
   p.G = s; s += Np * Np; p.Rinv = s; s += Np * Np; p.R1 = s; s += Np * Np; p.R2 = s; s += Np * Np;
   p.RB = s; s += Np * Np; p.W = s; s += Np * Np; p.J = s; s += Np * Np; p.Rsm = s; s += 2 * Np * Np;
-  p.sigma = s; s += Np; p.sgn = s; s += Np;
+  p.sigma = s; s += Np; p.sgn = s; s += Np; p.tv = s; s += 8;
   p.colc = (double*)(b + p.oColc); p.colr = (double*)(b + p.oColr); p.cols = p.colr + p.n; p.colp = (double*)(b + p.oColp);
+  p.colss = (double*)(b + p.oColss);
   p.split = (float*)(b + p.oSplit);
   p.jlog = (void*)(b + p.oJlog);
 }
 
-// ----------------------------------------------------------------- collectives
 rsvd_status allreduce_sum(rsvd_ctx* ctx, double* buf, size_t count) {
-  if (ctx->nranks <= 1 || count == 0) return RSVD_OK;
-  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream);
-  if (r != ncclSuccess) return fail(ctx, RSVD_ENCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
-  return RSVD_OK;
+  if (!ctx->comm || ctx->nranks <= 1 || count == 0) return RSVD_OK;
+  return ctx->comm->allreduce(ctx, buf, count, false);
 }
-
+rsvd_status allreduce_max(rsvd_ctx* ctx, double* buf, size_t count) {
+  if (!ctx->comm || ctx->nranks <= 1 || count == 0) return RSVD_OK;
+  return ctx->comm->allreduce(ctx, buf, count, true);
+}
 rsvd_status allgather(rsvd_ctx* ctx, const double* send, double* recv, size_t count) {
-  ncclResult_t r = ncclAllGather(send, recv, count, ncclDouble, ctx->comm, ctx->stream);
-  if (r != ncclSuccess) return fail(ctx, RSVD_ENCCL, "ncclAllGather: %s", ncclGetErrorString(r));
-  return RSVD_OK;
+  return ctx->comm->allgather(ctx, send, recv, count);
 }
 
 // ----------------------------------------------------------------- passes over A
@@ -346,119 +488,139 @@ rsvd_status pass_atx(rsvd_ctx* ctx, Plan& p, const double* Q, double* Z, bool ce
 
 // C (rows x Nout) = S (rows x Np) * Bsm (Np x Np) (small-K product, panel_apply)
 rsvd_status small_k(rsvd_ctx* ctx, Plan& p, const double* S, int64_t rows, const double* Bsm, double* C,
-                    int64_t ldc, int Nout, bool upper = false) {
-  CK(launch_panel_apply(S, p.Np, rows, p.Np, Bsm, p.Np, C, ldc, Nout, upper, ctx->num_sms, ctx->stream));
+                    int64_t ldc, int Nout, bool upper = false, Pred pr = Pred{}) {
+  CK(launch_panel_apply(S, p.Np, rows, p.Np, Bsm, p.Np, C, ldc, Nout, upper, ctx->num_sms, ctx->stream, pr));
   return RSVD_OK;
 }
 
 // G (Np x Np) = S^T S (gram_partial + fixed-order reduce), allreduce when the
-// rows are distributed.
-rsvd_status gram(rsvd_ctx* ctx, Plan& p, const double* S, int64_t rows, bool dist) {
-  CK(launch_gram(S, p.Np, rows, p.Np, p.part, p.G, p.Np, ctx->num_sms, ctx->stream));
+// rows are distributed (always enqueued: every rank takes part in every collective).
+rsvd_status gram(rsvd_ctx* ctx, Plan& p, const double* S, int64_t rows, bool dist, Pred pr) {
+  CK(launch_gram(S, p.Np, rows, p.Np, p.part, p.G, p.Np, ctx->num_sms, ctx->stream, pr));
   if (dist) return allreduce_sum(ctx, p.G, (size_t)p.Np * p.Np);
   return RSVD_OK;
 }
 
-// TSQR on `rows` x l panel S (ld Np), single device; R (l x l, ld l) to Rout.
-rsvd_status tsqr_local(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, double* Rout) {
-  const int l = p.l;
+// TSQR level structure of a rows x l panel: leaves of <= leaf_rows_cap(l) rows,
+// their R factors stacked, repeated until one leaf remains.  Returns false if
+// the panel cannot be reduced (fewer than l rows per leaf).
+bool tsqr_levels(int64_t rows, int l, std::vector<int64_t>* leaves, size_t* stack_bytes) {
   const int cap = leaf_rows_cap(l);
-  struct Lev { double* buf; int64_t ld, M, P; };
-  std::vector<Lev> levs;
-  // stack sizes
+  int64_t Mc = rows;
   size_t need = 0;
-  {
-    int64_t Mc = rows;
-    while (Mc > cap) {
-      int64_t P = ceil_div(Mc, cap);
-      if (Mc / P < l) P = Mc / l;
-      if (P * l >= Mc) return fail(ctx, RSVD_EUNSUPPORTED, "TSQR cannot reduce %lld rows at l = %d", (long long)Mc, l);
-      need += (size_t)P * l * l * 8 + 256;
-      Mc = P * l;
-    }
-  }
-  CKS(ensure_ws2(ctx, need + 256));
-  char* wp = ctx->ws2;
-  double* cur = S;
-  int64_t ld = p.Np, Mc = rows;
   while (Mc > cap) {
     int64_t P = ceil_div(Mc, cap);
     if (Mc / P < l) P = Mc / l;
-    if (P * l >= Mc) return fail(ctx, RSVD_EUNSUPPORTED, "TSQR cannot reduce %lld rows at l = %d", (long long)Mc, l);
+    if (P < 1 || P * l >= Mc) return false;
+    need += align256((size_t)P * l * l * 8);
+    if (leaves) leaves->push_back(P);
+    Mc = P * l;
+  }
+  if (stack_bytes) *stack_bytes = need + 256;
+  return true;
+}
+
+// TSQR on the rows x l panel S (ld ld_s) on this device, every kernel predicated
+// by `pr`; R (l x l, ld l) to Rout.
+rsvd_status tsqr_local(rsvd_ctx* ctx, const Plan& p, double* S, int64_t ld_s, int64_t rows, double* Rout, Pred pr) {
+  const int l = p.l;
+  std::vector<int64_t> leaves;
+  size_t need = 0;
+  if (!tsqr_levels(rows, l, &leaves, &need))
+    return fail(ctx, RSVD_EUNSUPPORTED, "TSQR cannot reduce %lld rows at l = %d", (long long)rows, l);
+  CKS(ensure_ws2(ctx, need + 256));
+  struct Lev { double* buf; int64_t ld, M, P; };
+  std::vector<Lev> levs;
+  char* wp = ctx->ws2;
+  double* cur = S;
+  int64_t ld = ld_s, Mc = rows;
+  for (const int64_t P : leaves) {
     double* stack = (double*)wp;
     wp += align256((size_t)P * l * l * 8);
-    CK(launch_hqr_leaves(cur, ld, Mc, l, P, stack, ctx->stream));
+    CK(launch_hqr_leaves(cur, ld, Mc, l, P, stack, ctx->stream, pr));
     levs.push_back({cur, ld, Mc, P});
     cur = stack; ld = l; Mc = P * l;
   }
-  CK(launch_hqr_leaves(cur, ld, Mc, l, 1, Rout, ctx->stream));
+  CK(launch_hqr_leaves(cur, ld, Mc, l, 1, Rout, ctx->stream, pr));
   for (int i = (int)levs.size() - 1; i >= 0; --i) {
     const double* Sq = (i + 1 < (int)levs.size()) ? levs[i + 1].buf : cur;
-    CK(launch_tsqr_combine(levs[i].buf, levs[i].ld, levs[i].M, l, levs[i].P, Sq, l, ctx->stream));
+    CK(launch_tsqr_combine(levs[i].buf, levs[i].ld, levs[i].M, l, levs[i].P, Sq, l, ctx->stream, pr));
   }
+  return RSVD_OK;
+}
+
+// Householder TSQR of the first l columns of S (rows x Np, ld Np), run only
+// when the call's breakdown bit is set (pr).  Distributed: local TSQR, then
+// the allgather of the R factors (always enqueued: every rank takes part), the
+// redundant QR of the stack and Q_local <- Q_local S_rank.  R to Rout (ld Np).
+rsvd_status orth_fallback(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool dist, double* Rout, Pred pr) {
+  const int l = p.l, Np = p.Np;
+  const size_t rr = (size_t)l * l;
+  if (rows < l || !tsqr_levels(rows, l, nullptr, nullptr)) {
+    // no Householder fallback for this shape: a breakdown becomes an error
+    CK(launch_flag_or(ctx->flags_dev, kFlagNoFallback, ctx->stream, pr));
+    if (dist) {   // keep the collective sequence identical on every rank
+      double* stack = p.T;
+      CKS(allgather(ctx, p.Rsm, stack, rr));
+    }
+    return RSVD_OK;
+  }
+  CKS(tsqr_local(ctx, p, S, Np, rows, p.Rsm, pr));
+  if (!dist) {
+    if (Rout) CK(launch_copy_out(p.Rsm, l, l, l, Rout, Np, false, nullptr, ctx->stream, pr));
+    return RSVD_OK;
+  }
+  const int64_t srows = (int64_t)ctx->nranks * l;
+  if ((size_t)srows * l > (size_t)std::max(p.M, p.n) * Np)
+    return fail(ctx, RSVD_EUNSUPPORTED, "too many ranks for the robust panel QR workspace");
+  double* stack = p.T;
+  CKS(allgather(ctx, p.Rsm, stack, rr));
+  double* Rg = p.Rsm + rr;
+  if (srows <= leaf_rows_cap(l)) {
+    CK(launch_hqr_leaves(stack, l, srows, l, 1, Rg, ctx->stream, pr));
+  } else {
+    CKS(tsqr_local(ctx, p, stack, l, srows, Rg, pr));
+  }
+  // Q_local <- Q_local S_rank (the rank's l x l block of the stack's Q), zero padded to Np x Np
+  CK(launch_fill(p.Rinv, (int64_t)Np * Np, 0.0, ctx->stream));
+  CK(launch_copy_in(stack + (size_t)ctx->rank * rr, false, l, l, l, l, p.Rinv, Np, ctx->stream));
+  CKS(small_k(ctx, p, S, rows, p.Rinv, S, Np, Np, false, pr));
+  if (Rout) CK(launch_copy_out(Rg, l, l, l, Rout, Np, false, nullptr, ctx->stream, pr));
   return RSVD_OK;
 }
 
 // Orthonormalise the first l columns of S (rows x Np, ld Np) in place.
 // dist: rows are distributed over ranks.  R (l x l, ld Np) to Rout if non-null.
-rsvd_status orth(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool dist, bool robust, double* Rout,
-                 bool exact = true) {
+// exact = false: one CholeskyQR pass (intermediate subspace bases, Alg. 2
+// steps 2-3: only span(Y) matters downstream); true: CholeskyQR2.  The
+// CholeskyQR kernels run while the breakdown bit is clear, the Householder
+// TSQR fallback once it is set (a breakdown in this or an earlier panel of
+// the call): decided on the device, no host round trip.
+rsvd_status orth(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool dist, double* Rout, bool exact = true) {
   const int l = p.l, Np = p.Np;
-  Prof pr(ctx, 2, (double)rows * Np * 8 * 4);
+  Prof pr_(ctx, 2, (double)rows * Np * 8 * 4);
   if (!dist && small_panel(rows, l)) {
     CK(launch_hqr_leaves(S, Np, rows, l, 1, p.Rsm, ctx->stream));
-    if (Rout) { CK(launch_copy_out(p.Rsm, l, l, l, Rout, Np, false, nullptr, ctx->stream));  }
+    if (Rout) CK(launch_copy_out(p.Rsm, l, l, l, Rout, Np, false, nullptr, ctx->stream));
     return RSVD_OK;
   }
-  if (!robust && !exact) {
-    // intermediate subspace-iteration basis (Alg. 2 steps 2-3): only span(Y)
-    // matters downstream, so one CholeskyQR pass suffices (breakdown-checked)
-    CKS(gram(ctx, p, S, rows, dist));
-    CK(launch_chol_aug(p.G, Np, l, Np, p.R1, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream));
-    // in place: each output row of S R^-1 depends only on the same input row,
-    // and stream-K writes a shared row block only in the fix-up after all reads
-    CKS(small_k(ctx, p, S, rows, p.Rinv, S, Np, Np, true));
-    return RSVD_OK;
+  const Pred ok{ctx->flags_dev, kFlagCholBreak, 0}, bad{ctx->flags_dev, kFlagCholBreak, 1};
+  if (!exact) {
+    CKS(gram(ctx, p, S, rows, dist, ok));
+    CK(launch_chol_aug(p.G, Np, l, Np, p.R1, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream, ok));
+    // in place: each output row of S R^-1 depends only on the same input row
+    CKS(small_k(ctx, p, S, rows, p.Rinv, S, Np, Np, true, ok));
+  } else {
+    // CholeskyQR2: S -> T = S R1^-1 -> S = T R2^-1 (S intact until the last step)
+    CKS(gram(ctx, p, S, rows, dist, ok));
+    CK(launch_chol_aug(p.G, Np, l, Np, p.R1, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream, ok));
+    CKS(small_k(ctx, p, S, rows, p.Rinv, p.T, Np, Np, true, ok));
+    CKS(gram(ctx, p, p.T, rows, dist, ok));
+    CK(launch_chol_aug(p.G, Np, l, Np, p.R2, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream, ok));
+    CKS(small_k(ctx, p, p.T, rows, p.Rinv, S, Np, Np, true, ok));
+    if (Rout) CK(launch_panel_apply(p.R2, Np, Np, Np, p.R1, Np, Rout, Np, Np, true, ctx->num_sms, ctx->stream, ok));
   }
-  if (!robust) {
-    // CholeskyQR2
-    CKS(gram(ctx, p, S, rows, dist));
-    CK(launch_chol_aug(p.G, Np, l, Np, p.R1, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream));
-    CKS(small_k(ctx, p, S, rows, p.Rinv, p.T, Np, Np, true));
-    CKS(gram(ctx, p, p.T, rows, dist));
-    CK(launch_chol_aug(p.G, Np, l, Np, p.R2, p.Rinv, ctx->flags_dev, kFlagCholBreak, ctx->stream));
-    CKS(small_k(ctx, p, p.T, rows, p.Rinv, S, Np, Np, true));
-    if (Rout) { CK(launch_panel_apply(p.R2, Np, Np, Np, p.R1, Np, Rout, Np, Np, true, ctx->num_sms, ctx->stream));  }
-    return RSVD_OK;
-  }
-  // robust: TSQR (local), then across ranks
-  if (rows < l) return fail(ctx, RSVD_EUNSUPPORTED, "robust panel QR needs >= l rows per rank");
-  CKS(tsqr_local(ctx, p, S, rows, p.Rsm));
-  if (dist) {
-    // allgather the local R factors, QR of the stack (redundant per rank), combine
-    const size_t rr = (size_t)l * l;
-    const int64_t srows = (int64_t)ctx->nranks * l;
-    // reuse T as the gathered stack (big enough: max(M, n) * Np >= nranks * l * l? check)
-    if ((size_t)srows * l > (size_t)std::max(p.M, p.n) * Np)
-      return fail(ctx, RSVD_EUNSUPPORTED, "too many ranks for the robust panel QR workspace");
-    double* stack = p.T;
-    CKS(allgather(ctx, p.Rsm, stack, rr));
-    double* Rg = p.Rsm + rr;
-    if (srows <= leaf_rows_cap(l)) {
-      CK(launch_hqr_leaves(stack, l, srows, l, 1, Rg, ctx->stream));
-    } else {
-      Plan q = p; q.Np = l;
-      CKS(tsqr_local(ctx, q, stack, srows, Rg));
-    }
-    // local Q <- local Q * S_rank : treat the local panel as nleaves = 1 block
-    // (combine kernel reads S rows [leaf*l, ...) so offset the pointer)
-    const int64_t nleaves = std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 256), 1));
-    CK(launch_tsqr_combine(S, Np, rows, l, nleaves, stack + (size_t)ctx->rank * l * l, l, ctx->stream));
-    if (Rout) { CK(launch_copy_out(Rg, l, l, l, Rout, Np, false, nullptr, ctx->stream));  }
-  } else if (Rout) {
-    CK(launch_copy_out(p.Rsm, l, l, l, Rout, Np, false, nullptr, ctx->stream));
-  }
-  return RSVD_OK;
+  return orth_fallback(ctx, p, S, rows, dist, Rout, bad);
 }
 
 rsvd_status validate(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, int64_t* m_out,
@@ -486,30 +648,34 @@ rsvd_status validate(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm
   return RSVD_OK;
 }
 
+// Column statistics of rpca (Alg. 6): c (means), ss (sums of squares of
+// the centred columns, when scaling or the total variance is needed), rs = 1/s.d.
+rsvd_status column_stats(rsvd_ctx* ctx, Plan& p, bool centred, bool want_ss) {
+  if (centred) {
+    CK(launch_colsum(p.A, p.lda, p.f32, p.M, p.n, 0, nullptr, p.colp, p.colc, ctx->stream, nullptr));
+    CKS(allreduce_sum(ctx, p.colc, (size_t)p.n));
+    CK(launch_colstat_finish(p.colc, p.n, (double)p.m_global, 0, nullptr, ctx->stream));
+  } else {
+    CK(launch_fill(p.colc, p.n, 0.0, ctx->stream));
+  }
+  if (p.scaled || want_ss) {
+    CK(launch_colsum(p.A, p.lda, p.f32, p.M, p.n, 1, p.colc, p.colp, p.colss, ctx->stream, nullptr));
+    CKS(allreduce_sum(ctx, p.colss, (size_t)p.n));
+  }
+  if (p.scaled) CK(launch_colstat_scale(p.colss, p.n, (double)p.m_global, p.colr, p.cols, ctx->stream));
+  return RSVD_OK;
+}
+
 // Core of rsvd: fills p.Y (= Q, M x Np), p.X (= V, n x Np, sign-fixed),
-// p.W (= U~ diag(sgn), Np x Np), p.sigma.  Returns flags via ctx->flags_dev.
-rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool robust, bool want_svd) {
+// p.W (= U~ diag(sgn), Np x Np), p.sigma.  Status bits in ctx->flags_dev.
+rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool want_svd, bool want_ss = false) {
   const int l = p.l, Np = p.Np;
   ctx->prof_phase ^= 1;           // level-2 profiling samples A.X and A^T.X passes on alternate calls
   const bool dist = ctx->nranks > 1;
   const bool centred = prm->center != 0 || prm->scale != 0;
-  CK(cudaMemsetAsync(ctx->flags_dev, 0, sizeof(int) * 4, ctx->stream));
+  CK(cudaMemsetAsync(ctx->flags_dev, 0, sizeof(int) * 16, ctx->stream));
   p.scaled = prm->scale != 0;
-  if (centred || p.scaled) {
-    // column means c (and 1/s.d. for scaling): Alg. 6, "center and scale"
-    if (centred) {
-      CK(launch_colsum(p.A, p.lda, p.f32, p.M, p.n, 0, nullptr, p.colp, p.colc, ctx->stream, nullptr));
-      CKS(allreduce_sum(ctx, p.colc, (size_t)p.n));
-      CK(launch_colstat_finish(p.colc, p.n, (double)p.m_global, 0, nullptr, ctx->stream));
-    } else {
-      CK(launch_fill(p.colc, p.n, 0.0, ctx->stream));
-    }
-    if (p.scaled) {
-      CK(launch_colsum(p.A, p.lda, p.f32, p.M, p.n, 1, p.colc, p.colp, p.colr, ctx->stream, nullptr));
-      CKS(allreduce_sum(ctx, p.colr, (size_t)p.n));
-      CK(launch_colstat_finish(p.colr, p.n, (double)p.m_global, 1, p.cols, ctx->stream));
-    }
-  }
+  if (centred || p.scaled || want_ss) CKS(column_stats(ctx, p, prm->center != 0, want_ss));
   if (p.use_ozaki) {
     // slices of f(A) once per call; every pass below reads them (pass_ozaki.cu)
     Prof pr(ctx, 5, (double)p.M * p.n * 8);
@@ -541,16 +707,16 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool robus
       CKS(pass_ax(ctx, p, p.Z, p.Y, centred));                       //   (4) Y = A L
       continue;
     }
-    CKS(orth(ctx, p, p.Y, p.M, dist, robust, nullptr, false));      // Alg. 2 (2) [Q,~] = qr(Y)
+    CKS(orth(ctx, p, p.Y, p.M, dist, nullptr, false));              // Alg. 2 (2) [Q,~] = qr(Y)
     CKS(pass_atx(ctx, p, p.Y, p.Z, centred));                        //   A^T Q
-    CKS(orth(ctx, p, p.Z, p.n, false, robust, nullptr, false));     //   (3) [Q,~] = qr(A^T Q)
+    CKS(orth(ctx, p, p.Z, p.n, false, nullptr, false));             //   (3) [Q,~] = qr(A^T Q)
     CKS(pass_ax(ctx, p, p.Z, p.Y, centred));                         //   (4) Y = A Q
   }
-  CKS(orth(ctx, p, p.Y, p.M, dist, robust, nullptr));               // Alg. 4 step 9
+  CKS(orth(ctx, p, p.Y, p.M, dist, nullptr));                       // Alg. 4 step 9
   CKS(pass_atx(ctx, p, p.Y, p.Z, centred));                          // step 10: B^T = A^T Q
   if (!want_svd) return RSVD_OK;
   // economic SVD of B via B^T = Q_B R_B and Jacobi on R_B^T (Alg. 5 step 2)
-  CKS(orth(ctx, p, p.Z, p.n, false, robust, p.RB));
+  CKS(orth(ctx, p, p.Z, p.n, false, p.RB));
   {
     Prof pr(ctx, 3, 0);
     CK(launch_jacobi(p.RB, Np, l, p.sigma, p.W, p.J, Np, ctx->flags_dev, ctx->sweeps_dev, p.jlog, ctx->stream));
@@ -574,17 +740,24 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool robus
   return RSVD_OK;
 }
 
-rsvd_status finish_flags(rsvd_ctx* ctx, int* flags) {
-  CK(cudaMemcpyAsync(ctx->flags_host, ctx->flags_dev, sizeof(int) * 16, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  if (ctx->prof) prof_collect(ctx);
-  *flags = ctx->flags_host[0];
-  ctx->last_sweeps = ctx->flags_host[8];
+// Ozaki slices of A (and X slice scratch) for the plan
+rsvd_status plan_ozaki(rsvd_ctx* ctx, Plan& p, int64_t m_local, int64_t n_stored, bool alloc) {
+  const size_t sa = align256(ozaki_a_bytes(m_local, n_stored));
+  const size_t sx = align256(ozaki_x_bytes(std::max(p.M, p.n), std::min(p.Np, 64)));
+  const size_t nx = p.Np > 64 ? 2 : 1;
+  p.oz_bytes = sa + nx * sx;
+  if (!alloc) return RSVD_OK;
+  CKS(ensure_buf(ctx, &ctx->ws4, &ctx->ws4_bytes, p.oz_bytes, "Ozaki slice workspace"));
+  p.oz = ozaki_layout_a(ctx->ws4, m_local, n_stored);
+  p.ozx = ctx->ws4 + sa;
+  p.ozx2 = nx > 1 ? ctx->ws4 + sa + sx : nullptr;
   return RSVD_OK;
 }
 
 // Build the plan for A (handles the single-GPU m < n case by working on A^T).
-rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bool center_or_scale, Plan& p) {
+// alloc = false: sizes only (rsvd_workspace_bytes).
+rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bool center_or_scale, Plan& p,
+                      bool alloc = true) {
   const int64_t mg = ctx->nranks > 1 ? A->m_global : A->m_local;
   p.f32 = A->dtype == RSVD_F32;
   p.A = A->A; p.lda = A->lda;
@@ -602,46 +775,49 @@ rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bo
   if (ctx->nranks > 1 && p.M < p.l)
     return fail(ctx, RSVD_EUNSUPPORTED, "each rank needs at least l = %d rows", p.l);
   const size_t bytes = plan_bytes(ctx, p);
-  CKS(ensure_ws(ctx, bytes));
-  bind(ctx, p);
-  if (p.use_ozaki) {
-    // slices of the stored matrix (A->m_local x A->n), then the X slice scratch
-    const size_t sa = align256(ozaki_a_bytes(A->m_local, A->n));
-    const size_t sx = align256(ozaki_x_bytes(std::max(p.M, p.n), std::min(p.Np, 64)));
-    const size_t nx = p.Np > 64 ? 2 : 1;
-    if (sa + nx * sx > ctx->ws4_bytes) {
-      if (ctx->ws4) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->ws4); ctx->ws4 = nullptr; ctx->ws4_bytes = 0; }
-      if (cudaMalloc(&ctx->ws4, sa + nx * sx) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(ctx, RSVD_ENOMEM, "Ozaki slice workspace of %zu bytes failed", sa + nx * sx);
-      }
-      ctx->ws4_bytes = sa + nx * sx;
-    }
-    p.oz = ozaki_layout_a(ctx->ws4, A->m_local, A->n);
-    p.ozx = ctx->ws4 + sa;
-    p.ozx2 = nx > 1 ? ctx->ws4 + sa + sx : nullptr;
+  if (alloc) {
+    CKS(ensure_ws(ctx, bytes));
+    bind(ctx, p);
   }
+  if (p.use_ozaki) CKS(plan_ozaki(ctx, p, A->m_local, A->n, alloc));
   return RSVD_OK;
 }
 
-// The caller's output kernels (`emit`) are enqueued right behind the core, so
-// the one host synchronisation per call (reading the status word) also covers
-// them; on a CholeskyQR breakdown the robust core and the outputs run again.
-rsvd_status run_with_retry(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool want_svd,
-                           const std::function<rsvd_status()>& emit = nullptr) {
-  int flags = 0;
-  ctx->last_robust = 0;
-  CKS(rsvd_core(ctx, p, prm, false, want_svd));
+// TSQR fallback scratch for the panels of a plan (rows M and n)
+size_t plan_tsqr_bytes(const Plan& p, int nranks) {
+  size_t a = 0, b = 0, c = 0;
+  tsqr_levels(p.M, p.l, nullptr, &a);
+  tsqr_levels(p.n, p.l, nullptr, &b);
+  tsqr_levels((int64_t)nranks * p.l, p.l, nullptr, &c);
+  return std::max(std::max(a, b), c) + 512;
+}
+
+// One call: the core, then the caller's output kernels (`emit`), then the
+// end-of-call status kernel (flags OR-ed into the sticky word for rsvd_sync).
+rsvd_status run_call(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool want_svd,
+                     const std::function<rsvd_status()>& emit = nullptr, bool want_ss = false) {
+  ctx->err.clear();
+  CKS(ensure_ws2(ctx, plan_tsqr_bytes(p, ctx->nranks)));   // before any launch: no reallocation mid-call
+  CKS(rsvd_core(ctx, p, prm, want_svd, want_ss));
   if (emit) CKS(emit());
-  CKS(finish_flags(ctx, &flags));
-  if (flags & kFlagCholBreak) {
-    ctx->last_robust = 1;
-    CKS(rsvd_core(ctx, p, prm, true, want_svd));
-    if (emit) CKS(emit());
-    CKS(finish_flags(ctx, &flags));
-  }
-  if (flags & kFlagNonFinite) return fail(ctx, RSVD_ENUMERIC, "non-finite intermediate (input contains Inf/NaN?)");
-  if (flags & kFlagJacobiCap) return fail(ctx, RSVD_ENUMERIC, "one-sided Jacobi hit the 30-sweep cap");
+  CK(launch_status_finish(ctx->flags_dev, ctx->sticky_dev, kFlagCholBreak, ctx->stream));
+  return RSVD_OK;
+}
+
+// Wait for the stream and turn the sticky status into a return code.
+rsvd_status sync_status(rsvd_ctx* ctx) {
+  CK(cudaMemcpyAsync(ctx->flags_host, ctx->sticky_dev, sizeof(int) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemsetAsync(ctx->sticky_dev, 0, sizeof(int) * 4, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->prof) prof_collect(ctx);
+  const int f = ctx->flags_host[0];
+  ctx->last_sweeps = ctx->flags_host[1];
+  ctx->last_robust = ctx->flags_host[2];
+  if (f & kFlagNonFinite) return fail(ctx, RSVD_ENUMERIC, "non-finite intermediate (input contains Inf/NaN?)");
+  if (f & kFlagJacobiCap) return fail(ctx, RSVD_ENUMERIC, "one-sided Jacobi hit the 30-sweep cap");
+  if (f & kFlagRankDef) return fail(ctx, RSVD_ENUMERIC, "pivoted QR: numerical rank < k");
+  if (f & kFlagNoFallback)
+    return fail(ctx, RSVD_ENUMERIC, "CholeskyQR breakdown on a panel with fewer rows than l (no TSQR fallback)");
   return RSVD_OK;
 }
 
@@ -650,7 +826,7 @@ rsvd_status run_with_retry(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool 
 // =================================================================== C ABI
 extern "C" {
 
-const char* rsvd_version(void) { return "rsvd_b200 0.1 (sm_100a)"; }
+const char* rsvd_version(void) { return "rsvd_b200 0.2 (sm_100a)"; }
 
 rsvd_status rsvd_create(rsvd_ctx** out, int device, void* stream) {
   if (!out) return RSVD_EINVAL;
@@ -660,12 +836,14 @@ rsvd_status rsvd_create(rsvd_ctx** out, int device, void* stream) {
   ctx->stream = (cudaStream_t)stream;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (e == cudaSuccess) e = cudaMalloc(&ctx->flags_dev, 16 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->flags_dev, 32 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(ctx->flags_dev, 0, 32 * sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->flags_host, 16 * sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->hbuf, 1024 * sizeof(double));
-  if (e == cudaSuccess) ctx->sweeps_dev = ctx->flags_dev + 8;
+  if (e == cudaSuccess) { ctx->sweeps_dev = ctx->flags_dev + 8; ctx->sticky_dev = ctx->flags_dev + 16; }
   if (e == cudaSuccess) e = cudaMalloc(&ctx->gemm_flags, 4096 * sizeof(unsigned));
   if (e == cudaSuccess) e = cudaMemset(ctx->gemm_flags, 0, 4096 * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
   {
     const char* fp = getenv("RSVD_FP32_PATH");
     if (fp && strcmp(fp, "dmma") == 0) ctx->fp32_tcgen05 = false;
@@ -682,8 +860,9 @@ rsvd_status rsvd_create(rsvd_ctx** out, int device, void* stream) {
 
 rsvd_status rsvd_destroy(rsvd_ctx* ctx) {
   if (!ctx) return RSVD_EINVAL;
+  cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  delete ctx->comm;
   for (auto& r : ctx->pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : ctx->pool) cudaEventDestroy(e);
   cudaFree(ctx->ws);
@@ -692,6 +871,7 @@ rsvd_status rsvd_destroy(rsvd_ctx* ctx) {
   cudaFreeHost(ctx->flags_host);
   cudaFreeHost(ctx->hbuf);
   cudaFree(ctx->ws3);
+  cudaFree(ctx->ws5);
   cudaFree(ctx->gemm_flags);
   cudaFree(ctx->ws4);
   delete ctx;
@@ -699,6 +879,12 @@ rsvd_status rsvd_destroy(rsvd_ctx* ctx) {
 }
 
 const char* rsvd_last_error(const rsvd_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+rsvd_status rsvd_sync(rsvd_ctx* ctx) {
+  if (!ctx) return RSVD_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  return sync_status(ctx);
+}
 
 rsvd_status rsvd_nccl_unique_id(void* out128) {
   if (!out128) return RSVD_EINVAL;
@@ -710,14 +896,59 @@ rsvd_status rsvd_nccl_unique_id(void* out128) {
 
 rsvd_status rsvd_comm_init(rsvd_ctx* ctx, const void* id128, int nranks, int rank) {
   if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, RSVD_EINVAL, "bad comm args");
+  if (ctx->comm) return fail(ctx, RSVD_EINVAL, "context already has a communicator");
   if (nranks == 1) { ctx->nranks = 1; ctx->rank = 0; return RSVD_OK; }
   if (!id128) return fail(ctx, RSVD_EINVAL, "null unique id");
   ncclUniqueId id;
   memcpy(&id, id128, sizeof id);
   cudaSetDevice(ctx->device);
-  ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
-  if (r != ncclSuccess) return fail(ctx, RSVD_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  NcclComm* c = new NcclComm();
+  ncclResult_t r = ncclCommInitRank(&c->c, nranks, id, rank);
+  if (r != ncclSuccess) { delete c; return fail(ctx, RSVD_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)); }
+  c->n = nranks; c->r = rank;
+  ctx->comm = c;
   ctx->nranks = nranks;
+  ctx->rank = rank;
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_group_create(rsvd_group** out, int nranks) {
+  if (!out || nranks < 2 || nranks > kMaxGroup) return RSVD_EINVAL;
+  rsvd_group* g = new rsvd_group();
+  g->n = nranks;
+  g->slots.resize(nranks);
+  *out = g;
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_group_destroy(rsvd_group* g) {
+  if (!g) return RSVD_EINVAL;
+  for (auto& s : g->slots) {
+    if (!s.joined) continue;
+    cudaSetDevice(s.device);
+    if (s.stage) cudaFree(s.stage);
+    if (s.ready) cudaEventDestroy(s.ready);
+    if (s.done) cudaEventDestroy(s.done);
+  }
+  delete g;
+  return RSVD_OK;
+}
+
+rsvd_status rsvd_comm_init_group(rsvd_ctx* ctx, rsvd_group* g, int rank) {
+  if (!ctx) return RSVD_EINVAL;
+  if (!g || rank < 0 || rank >= g->n) return fail(ctx, RSVD_EINVAL, "bad group or rank");
+  if (ctx->comm) return fail(ctx, RSVD_EINVAL, "context already has a communicator");
+  CK(cudaSetDevice(ctx->device));
+  rsvd_group::Slot& s = g->slots[rank];
+  if (s.joined) return fail(ctx, RSVD_EINVAL, "rank %d of the group is already taken", rank);
+  CK(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+  s.device = ctx->device;
+  s.joined = true;
+  GroupComm* c = new GroupComm();
+  c->g = g; c->r = rank;
+  ctx->comm = c;
+  ctx->nranks = g->n;
   ctx->rank = rank;
   return RSVD_OK;
 }
@@ -729,6 +960,13 @@ void rsvd_params_default(rsvd_params* prm, int32_t k) {
   prm->sdist = RSVD_NORMAL;
 }
 
+void rsvd_rpca_params_default(rsvd_params* prm, int32_t k) {
+  rsvd_params_default(prm, k);
+  if (!prm) return;
+  prm->center = 1;
+  prm->scale = 1;                 // rpca(..., center = TRUE, scale = TRUE, ...)
+}
+
 void rsvd_rrpca_params_default(rsvd_rrpca_params* prm) {
   if (!prm) return;
   memset(prm, 0, sizeof *prm);
@@ -737,16 +975,29 @@ void rsvd_rrpca_params_default(rsvd_rrpca_params* prm) {
   prm->rand = 1;
 }
 
+rsvd_status rsvd_workspace_bytes(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, size_t* bytes) {
+  int64_t mg, n;
+  CKS(validate(ctx, A, prm, &mg, &n));
+  if (!bytes) return fail(ctx, RSVD_EINVAL, "bytes is null");
+  Plan p{};
+  CKS(make_plan(ctx, A, prm->k, prm->p, prm->center || prm->scale, p, false));
+  size_t tot = p.total + p.oz_bytes + plan_tsqr_bytes(p, ctx->nranks);
+  if (prm->power == 2) tot += lu_scratch_bytes(std::max(p.M, p.n), ctx->num_sms);
+  *bytes = tot;
+  return RSVD_OK;
+}
+
 rsvd_status rsvd_run(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm_in, void* u, int64_t ldu,
                      void* d, void* v, int64_t ldv) {
   int64_t mg, n;
   CKS(validate(ctx, A, prm_in, &mg, &n));
   rsvd_params prm = *prm_in;
   ctx->err.clear();
+  std::string warn;
   if (prm.nu > prm.k || prm.nv > prm.k) {
     prm.nu = std::min(prm.nu, prm.k);
     prm.nv = std::min(prm.nv, prm.k);
-    ctx->err = "warning: nu/nv > k clamped to k";
+    warn = "warning: nu/nv > k clamped to k";
   }
   if (!d) return fail(ctx, RSVD_EINVAL, "d is null");
   if (prm.nu > 0 && (!u || ldu < prm.nu)) return fail(ctx, RSVD_EINVAL, "u null or ldu < nu");
@@ -777,8 +1028,41 @@ rsvd_status rsvd_run(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm
     CK(launch_copy_out(p.sigma, 1, prm.k, 1, d, 1, f32, nullptr, ctx->stream));
     return RSVD_OK;
   };
-  CKS(run_with_retry(ctx, p, &prm, true, emit));
+  CKS(run_call(ctx, p, &prm, true, emit));
+  if (!warn.empty()) ctx->err = warn;
   return RSVD_OK;
+}
+
+rsvd_status rsvd_run_host(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, void* u, int64_t ldu,
+                          void* d, void* v, int64_t ldv) {
+  int64_t mg, n;
+  CKS(validate(ctx, A, prm, &mg, &n));
+  if (ctx->nranks > 1) return fail(ctx, RSVD_EUNSUPPORTED, "rsvd_run_host is single-GPU");
+  if (!d) return fail(ctx, RSVD_EINVAL, "d is null");
+  const int k = prm->k, nu = std::min(prm->nu, k), nv = std::min(prm->nv, k);
+  if (nu > 0 && (!u || ldu < nu)) return fail(ctx, RSVD_EINVAL, "u null or ldu < nu");
+  if (nv > 0 && (!v || ldv < nv)) return fail(ctx, RSVD_EINVAL, "v null or ldv < nv");
+  CK(cudaSetDevice(ctx->device));
+  const size_t es = A->dtype == RSVD_F32 ? 4 : 8;
+  const int64_t m = A->m_local;
+  const size_t bA = align256((size_t)m * n * es), bU = align256((size_t)m * std::max(nu, 1) * es),
+               bD = align256((size_t)k * es), bV = align256((size_t)n * std::max(nv, 1) * es);
+  CKS(ensure_buf(ctx, &ctx->ws5, &ctx->ws5_bytes, bA + bU + bD + bV, "host-call staging"));
+  char* dA = ctx->ws5;
+  char* dU = dA + bA;
+  char* dD = dU + bU;
+  char* dV = dD + bD;
+  // A: host (lda) -> device (ld n)
+  CK(cudaMemcpy2DAsync(dA, n * es, A->A, A->lda * es, n * es, m, cudaMemcpyHostToDevice, ctx->stream));
+  rsvd_matrix Ad = *A;
+  Ad.A = dA; Ad.lda = n; Ad.m_global = m; Ad.row_offset = 0;
+  rsvd_params pr = *prm;
+  pr.nu = nu; pr.nv = nv;
+  CKS(rsvd_run(ctx, &Ad, &pr, nu ? dU : nullptr, std::max(nu, 1), dD, nv ? dV : nullptr, std::max(nv, 1)));
+  if (nu > 0) CK(cudaMemcpy2DAsync(u, ldu * es, dU, nu * es, nu * es, m, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(d, dD, k * es, cudaMemcpyDeviceToHost, ctx->stream));
+  if (nv > 0) CK(cudaMemcpy2DAsync(v, ldv * es, dV, nv * es, nv * es, n, cudaMemcpyDeviceToHost, ctx->stream));
+  return sync_status(ctx);
 }
 
 rsvd_status rsvd_rqb(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, void* Q, int64_t ldq, void* Bt,
@@ -791,11 +1075,12 @@ rsvd_status rsvd_rqb(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm
   CKS(make_plan(ctx, A, prm->k, prm->p, prm->center || prm->scale, p));
   if (p.trans_input) return fail(ctx, RSVD_EUNSUPPORTED, "rqb needs m >= n");
   if (!Q || !Bt || ldq < p.l || ldb < p.l) return fail(ctx, RSVD_EINVAL, "Q/Bt null or ld < l");
-  CKS(run_with_retry(ctx, p, prm, false));
-  CK(launch_copy_out(p.Y, p.Np, p.M, p.l, Q, ldq, p.f32, nullptr, ctx->stream));
-  CK(launch_copy_out(p.Z, p.Np, p.n, p.l, Bt, ldb, p.f32, nullptr, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  return RSVD_OK;
+  auto emit = [&]() -> rsvd_status {
+    CK(launch_copy_out(p.Y, p.Np, p.M, p.l, Q, ldq, p.f32, nullptr, ctx->stream));
+    CK(launch_copy_out(p.Z, p.Np, p.n, p.l, Bt, ldb, p.f32, nullptr, ctx->stream));
+    return RSVD_OK;
+  };
+  return run_call(ctx, p, prm, false, emit);
 }
 
 // Alg. rid: [~, B] = rqb(A, k, p, q); [~, Z, J] = id(B, k) (Alg. id,
@@ -814,16 +1099,14 @@ rsvd_status rsvd_rid(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm
   CKS(make_plan(ctx, A, k, prm->p, false, p));
   if (p.trans_input) return fail(ctx, RSVD_EUNSUPPORTED, "rid needs m >= n");
   if (p.l > 128) return fail(ctx, RSVD_EUNSUPPORTED, "rid needs l <= 128");
+  CKS(ensure_ws2(ctx, std::max(plan_tsqr_bytes(p, ctx->nranks), qrcp_scratch_bytes(p.n, k, ctx->num_sms))));
   auto emit = [&]() -> rsvd_status {
-    CKS(ensure_ws2(ctx, qrcp_scratch_bytes(p.n, k, ctx->num_sms)));
     CK(launch_qrcp(p.Z, p.Np, p.l, p.n, k, J, (double*)Z, ldz, ctx->ws2, ctx->flags_dev, kFlagRankDef,
                    ctx->num_sms, ctx->stream));
     CK(launch_gather_cols((const double*)A->A, A->lda, A->m_local, J, k, (double*)C, ldc, ctx->stream));
     return RSVD_OK;
   };
-  CKS(run_with_retry(ctx, p, prm, false, emit));
-  if (ctx->flags_host[0] & kFlagRankDef) return fail(ctx, RSVD_ENUMERIC, "pivoted QR: numerical rank of B < k");
-  return RSVD_OK;
+  return run_call(ctx, p, prm, false, emit);
 }
 
 // Alg. rcur: [C, Z, J] = rid(A, k, p, q); [~, S, P] = qr(C^T)
@@ -852,8 +1135,11 @@ rsvd_status rsvd_rcur(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* pr
   double* Ct = p.T;                        // m x k copy of C for the pivoted QR of C^T
   double* Rt = p.Y;                        // n x Np2 panel R^T -> Q_R
   double* Sr = p.RB;                       // S_R (k x k, ld Np2)
+  Plan q = p;
+  q.l = k; q.Np = Np2;
+  CKS(ensure_ws2(ctx, std::max({plan_tsqr_bytes(p, 1), plan_tsqr_bytes(q, 1), qrcp_scratch_bytes(p.n, k, ctx->num_sms),
+                                qrcp_scratch_bytes(m, k, ctx->num_sms)})));
   auto emit = [&]() -> rsvd_status {
-    CKS(ensure_ws2(ctx, std::max(qrcp_scratch_bytes(p.n, k, ctx->num_sms), qrcp_scratch_bytes(m, k, ctx->num_sms))));
     CK(launch_qrcp(p.Z, p.Np, p.l, p.n, k, J, Zs, p.n, ctx->ws2, ctx->flags_dev, kFlagRankDef, ctx->num_sms,
                    ctx->stream));                                        // rid: Z, J
     CK(launch_gather_cols(Ad, A->lda, m, J, k, (double*)C, ldc, ctx->stream));   // C = A(:, J)
@@ -862,40 +1148,96 @@ rsvd_status rsvd_rcur(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* pr
                    ctx->stream));                                        // I = P(1:k) of qr(C^T)
     CK(cudaMemsetAsync(Rt, 0, (size_t)p.n * Np2 * sizeof(double), ctx->stream));
     CK(launch_gather_rows(Ad, A->lda, p.n, I, k, (double*)R, ldr, Rt, Np2, ctx->stream));   // R = A(I, :), R^T
-    Plan q = p;
-    q.l = k; q.Np = Np2;
-    CKS(orth(ctx, q, Rt, p.n, false, true, Sr));                         // R^T = Q_R S_R (TSQR)
+    // R^T = Q_R S_R by Householder TSQR (always: R^T may be rank deficient)
+    CKS(tsqr_local(ctx, q, Rt, Np2, p.n, p.Rsm, Pred{}));
+    CK(launch_copy_out(p.Rsm, k, k, k, Sr, Np2, false, nullptr, ctx->stream));
     CK(launch_zq(Zs, p.n, Rt, Np2, p.n, k, p.part, p.G, k, ctx->num_sms, ctx->stream));   // W = Z Q_R
     CK(launch_rtsolve(p.G, k, Sr, Np2, k, (double*)U, ldu, ctx->stream));              // U = W S_R^-T
     return RSVD_OK;
   };
-  CKS(run_with_retry(ctx, p, prm, false, emit));
-  if (ctx->flags_host[0] & kFlagRankDef) return fail(ctx, RSVD_ENUMERIC, "pivoted QR: numerical rank < k");
-  return RSVD_OK;
+  return run_call(ctx, p, prm, false, emit);
 }
 
-rsvd_status rsvd_rpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm_in, void* rotation, int64_t ldr,
-                      void* eigvals, void* x, int64_t ldx, void* center, void* scale) {
+rsvd_status rsvd_rpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm_in, const rsvd_pca_out* o) {
   int64_t mg, n;
   CKS(validate(ctx, A, prm_in, &mg, &n));
+  if (!o) return fail(ctx, RSVD_EINVAL, "null output descriptor");
   rsvd_params prm = *prm_in;
-  if (!rotation || ldr < prm.k || !eigvals) return fail(ctx, RSVD_EINVAL, "rotation/eigvals null or ldr < k");
-  if (x && ldx < prm.k) return fail(ctx, RSVD_EINVAL, "ldx < k");
+  const int k = prm.k;
+  if (o->rotation && o->ldr < k) return fail(ctx, RSVD_EINVAL, "ldr < k");
+  if (o->x && o->ldx < k) return fail(ctx, RSVD_EINVAL, "ldx < k");
+  if (o->loadings && o->ldl < k) return fail(ctx, RSVD_EINVAL, "ldl < k");
+  if (o->x_white && o->ldw < k) return fail(ctx, RSVD_EINVAL, "ldw < k");
   CK(cudaSetDevice(ctx->device));
   Plan p{};
-  CKS(make_plan(ctx, A, prm.k, prm.p, prm.center || prm.scale, p));
+  CKS(make_plan(ctx, A, k, prm.p, prm.center || prm.scale, p));
   if (p.trans_input) return fail(ctx, RSVD_EUNSUPPORTED, "rpca needs m >= n");
-  CKS(run_with_retry(ctx, p, &prm, true));
-  const int k = prm.k, Np = p.Np;
-  CK(launch_copy_out(p.X, Np, p.n, k, rotation, ldr, p.f32, nullptr, ctx->stream));
-  CK(launch_pca_eig(p.sigma, k, (double)p.m_global, eigvals, p.f32, ctx->stream));
-  if (x) {
-    CKS(small_k(ctx, p, p.Y, p.M, p.W, p.T, Np, k));
-    CK(launch_copy_out(p.T, Np, p.M, k, x, ldx, p.f32, p.sigma, ctx->stream));   // scores U diag(d)
-  }
-  if (center && prm.center) CK(launch_copy_out(p.colc, 1, p.n, 1, center, 1, p.f32, nullptr, ctx->stream));
-  if (scale && prm.scale) CK(launch_copy_out(p.cols, 1, p.n, 1, scale, 1, p.f32, nullptr, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
+  const bool want_total = o->var_ratio || o->var_cum || o->total_var;
+  auto emit = [&]() -> rsvd_status {
+    const int Np = p.Np;
+    const bool f32 = p.f32;
+    const double mgd = (double)p.m_global;
+    if (want_total) CK(launch_total_var(p.colss, p.scaled ? p.colr : nullptr, p.n, mgd, p.tv, ctx->stream));
+    CK(launch_pca_stats(p.sigma, k, mgd, want_total ? p.tv : nullptr, o->eigvals, o->sdev, o->var_ratio,
+                        o->var_cum, f32, ctx->stream));
+    if (o->total_var) CK(launch_copy_out(p.tv, 1, 1, 1, o->total_var, 1, f32, nullptr, ctx->stream));
+    if (o->rotation) CK(launch_copy_out(p.X, Np, p.n, k, o->rotation, o->ldr, f32, nullptr, ctx->stream));
+    if (o->loadings) {                     // L = W Lambda^{1/2}: rotation columns times sdev
+      CK(launch_vec_map(p.sigma, false, k, 2, mgd, p.sgn, ctx->stream));
+      CK(launch_copy_out(p.X, Np, p.n, k, o->loadings, o->ldl, f32, p.sgn, ctx->stream));
+    }
+    if (o->x || o->x_white) {
+      CKS(small_k(ctx, p, p.Y, p.M, p.W, p.T, Np, k));                   // U (this rank's rows)
+      if (o->x) CK(launch_copy_out(p.T, Np, p.M, k, o->x, o->ldx, f32, p.sigma, ctx->stream));   // Z = U diag(d)
+      if (o->x_white) {                    // z_i / sqrt(lambda_i) = u_i sqrt(m - 1)
+        CK(launch_vec_map(nullptr, false, k, 3, sqrt(mgd - 1.0), p.sgn, ctx->stream));
+        CK(launch_copy_out(p.T, Np, p.M, k, o->x_white, o->ldw, f32, p.sgn, ctx->stream));
+      }
+    }
+    if (o->center && prm.center) CK(launch_copy_out(p.colc, 1, p.n, 1, o->center, 1, f32, nullptr, ctx->stream));
+    if (o->scale && prm.scale) CK(launch_copy_out(p.cols, 1, p.n, 1, o->scale, 1, f32, nullptr, ctx->stream));
+    return RSVD_OK;
+  };
+  return run_call(ctx, p, &prm, true, emit, want_total && !p.scaled);
+}
+
+rsvd_status rsvd_rpca_predict(rsvd_ctx* ctx, const rsvd_matrix* Anew, int32_t k, const void* rotation, int64_t ldr,
+                              const void* center, const void* scale, void* out, int64_t ldo) {
+  if (!ctx) return RSVD_EINVAL;
+  if (!Anew || !Anew->A || !rotation || !out) return fail(ctx, RSVD_EINVAL, "null argument");
+  if (Anew->dtype != RSVD_F64 && Anew->dtype != RSVD_F32) return fail(ctx, RSVD_EINVAL, "dtype must be F64 or F32");
+  if (Anew->m_local < 1 || Anew->n < 1 || Anew->lda < Anew->n) return fail(ctx, RSVD_EINVAL, "bad shape or lda < n");
+  if (k < 1 || k > 128 || ldr < k || ldo < k) return fail(ctx, RSVD_EINVAL, "need 1 <= k <= 128, ldr >= k, ldo >= k");
+  CK(cudaSetDevice(ctx->device));
+  ctx->err.clear();
+  rsvd_matrix Am = *Anew;
+  Am.m_global = Am.m_local; Am.row_offset = 0;
+  // a plan with l = k over the new rows, never transposed (the projection is row-wise)
+  Plan p{};
+  const bool cs = center || scale;
+  p.f32 = Am.dtype == RSVD_F32;
+  p.A = Am.A; p.lda = Am.lda;
+  p.trans_input = false;
+  p.M = Am.m_local; p.n = Am.n; p.m_global = Am.m_local;
+  p.l = k; p.Np = (int)round_up(k, 16);
+  p.use_tf32 = p.f32 && !cs && ctx->fp32_tcgen05 && tf32_pass_supported(p.A, p.lda);
+  p.use_ozaki = !p.f32 && ctx->fp64_ozaki && ozaki_supported(p.Np);
+  CKS(ensure_ws(ctx, plan_bytes(ctx, p)));
+  bind(ctx, p);
+  if (p.use_ozaki) CKS(plan_ozaki(ctx, p, Am.m_local, Am.n, true));
+  const bool f32 = p.f32;
+  CK(cudaMemsetAsync(ctx->flags_dev, 0, sizeof(int) * 16, ctx->stream));
+  CK(launch_copy_in(rotation, f32, ldr, p.n, k, p.Np, p.X, p.Np, ctx->stream));       // W, zero padded
+  if (center) CK(launch_vec_map(center, f32, p.n, 0, 0.0, p.colc, ctx->stream));
+  else CK(launch_fill(p.colc, p.n, 0.0, ctx->stream));
+  p.scaled = scale != nullptr;
+  if (scale) CK(launch_vec_map(scale, f32, p.n, 1, 0.0, p.colr, ctx->stream));          // 1 / s
+  if (p.use_ozaki)
+    CK(ozaki_slice_a(p.oz, (const double*)p.A, p.lda, center ? p.colc : nullptr, scale ? p.colr : nullptr,
+                     ctx->flags_dev, ctx->stream));
+  CKS(pass_ax(ctx, p, p.X, p.Y, cs));                                                   // f(Anew) W
+  CK(launch_copy_out(p.Y, p.Np, p.M, k, out, ldo, f32, nullptr, ctx->stream));
+  CK(launch_status_finish(ctx->flags_dev, ctx->sticky_dev, kFlagCholBreak, ctx->stream));
   return RSVD_OK;
 }
 
@@ -906,7 +1248,6 @@ rsvd_status rsvd_omega(rsvd_ctx* ctx, int64_t n, int64_t l, int32_t sdist, uint6
   CK(cudaSetDevice(ctx->device));
   const bool f32 = dtype == RSVD_F32;
   CK(launch_omega(n, l, ldo, l, sdist, seed, stream, f32, f32, out, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
   return RSVD_OK;
 }
 
@@ -936,11 +1277,11 @@ rsvd_status rsvd_profile_reset(rsvd_ctx* ctx) {
   return RSVD_OK;
 }
 
-int64_t rsvd_launch_count(const rsvd_ctx* ctx) { return ctx ? rsvd::g_kernel_launches : 0; }
+int64_t rsvd_launch_count(const rsvd_ctx* ctx) { return ctx ? rsvd::g_kernel_launches.load() : 0; }
 
 rsvd_status rsvd_stats(const rsvd_ctx* ctx, int64_t* out, int n) {
   if (!ctx || !out || n < 0) return RSVD_EINVAL;
-  const int64_t v[4] = {ctx->last_sweeps, ctx->last_robust, rsvd::g_kernel_launches, ctx->ozaki_calls};
+  const int64_t v[4] = {ctx->last_sweeps, ctx->last_robust, rsvd::g_kernel_launches.load(), ctx->ozaki_calls};
   for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
   return RSVD_OK;
 }
@@ -950,6 +1291,7 @@ rsvd_status rsvd_stats(const rsvd_ctx* ctx, int64_t* out, int n) {
 // =================================================================== rrpca (Alg. 7)
 namespace {
 
+// rsvd into device buffers (enqueued; step (6) of Alg. 7)
 rsvd_status rsvd_device(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, double* U, int64_t ldu,
                         double* d, double* V, int64_t ldv) {
   int64_t mg, n;
@@ -957,18 +1299,13 @@ rsvd_status rsvd_device(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* 
   Plan p{};
   CKS(make_plan(ctx, A, prm->k, prm->p, false, p));
   if (p.trans_input) return fail(ctx, RSVD_EUNSUPPORTED, "rrpca needs m >= n");
-  CKS(run_with_retry(ctx, p, prm, true));
-  if (U) CKS(small_k(ctx, p, p.Y, p.M, p.W, U, ldu, prm->k));
-  if (V) CK(launch_copy_out(p.X, p.Np, p.n, prm->k, V, ldv, false, nullptr, ctx->stream));
-  CK(launch_copy_out(p.sigma, 1, prm->k, 1, d, 1, false, nullptr, ctx->stream));
-  return RSVD_OK;
-}
-
-rsvd_status allreduce_max(rsvd_ctx* ctx, double* buf, size_t count) {
-  if (ctx->nranks <= 1) return RSVD_OK;
-  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclMax, ctx->comm, ctx->stream);
-  if (r != ncclSuccess) return fail(ctx, RSVD_ENCCL, "ncclAllReduce(max): %s", ncclGetErrorString(r));
-  return RSVD_OK;
+  auto emit = [&]() -> rsvd_status {
+    if (U) CKS(small_k(ctx, p, p.Y, p.M, p.W, U, ldu, prm->k));
+    if (V) CK(launch_copy_out(p.X, p.Np, p.n, prm->k, V, ldv, false, nullptr, ctx->stream));
+    CK(launch_copy_out(p.sigma, 1, prm->k, 1, d, 1, false, nullptr, ctx->stream));
+    return RSVD_OK;
+  };
+  return run_call(ctx, p, prm, true, emit);
 }
 
 }  // namespace
@@ -992,9 +1329,10 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
   CK(cudaSetDevice(ctx->device));
   const int64_t m = A->m_local;
   const int64_t minmn = std::min(mg, n);
-  // library envelope: l = k + p <= kMaxL (the deterministic-SVD switch of
-  // Remark 2, is not part of this library; R30)
-  // (the deterministic path has l = min(m, n) <= kMaxL, so k may reach min(m, n) there)
+  // library envelope: l = k + p <= kMaxL.  The deterministic SVD of Remark 2
+  // and rand = FALSE is rsvd with l = min(m, n), q = 0 (reading R30),
+  // available while min(m, n) <= kMaxL; above that the randomized SVD is kept
+  // (warning in rsvd_last_error) and the adaptive k is capped at kMaxL - p.
   const int kcap = (int)(minmn <= kMaxL ? minmn : std::min<int64_t>(minmn, kMaxL - rp.p));
   if (kcap < 1) return fail(ctx, RSVD_EUNSUPPORTED, "p = %d leaves no room for k under l <= %d", rp.p, kMaxL);
   if (!adaptive && prm->k > kcap)
@@ -1058,16 +1396,22 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
   int it = 0;
   double res = INFINITY;
   int kused = k;
+  std::string warn;
   for (it = 1; it <= prm->maxiter; ++it) {
     rsvd_params ri = rp;
     ri.k = ri.nu = ri.nv = k;
     ri.stream = (uint64_t)it;                               // fresh Omega per iteration (R23)
     // deterministic SVD (rand = FALSE, or Remark 2's switch for k > min(m, n)/4):
     // l = min(m, n), q = 0 -> Q Q^T M = M, the SVD of B is the exact SVD
-    const bool det = !prm->rand || (adaptive && 4 * (int64_t)k > minmn);
+    const bool want_det = !prm->rand || (adaptive && 4 * (int64_t)k > minmn);
+    const bool det = want_det && minmn <= kMaxL;
+    if (want_det && !det) {
+      char b[200];
+      snprintf(b, sizeof b, "warning: deterministic SVD needs min(m, n) <= %d; the randomized SVD is kept (iteration %d, k = %d)",
+               kMaxL, it, k);
+      warn = b;
+    }
     if (det) {
-      if (minmn > kMaxL)
-        return fail(ctx, RSVD_EUNSUPPORTED, "deterministic SVD in rrpca needs min(m, n) <= %d", kMaxL);
       ri.p = (int)(minmn - k);
       ri.q = 0;
     }
@@ -1093,6 +1437,11 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
     if (adaptive) {                                         // step (7) predict_rank (R30)
       const int l1 = std::max(nl, 1);
       int64_t kn = l1 < k ? l1 + 1 : std::min<int64_t>(l1 + (int64_t)ceil(0.05 * (double)minmn), minmn);
+      if (kn > kcap) {
+        char b[200];
+        snprintf(b, sizeof b, "warning: predicted rank %lld capped at %d (l = k + p <= %d)", (long long)kn, kcap, kMaxL);
+        warn = b;
+      }
       k = (int)std::min<int64_t>(kn, kcap);
     }
     mu = mu_next;
@@ -1100,8 +1449,9 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
   }
   if (it > prm->maxiter) it = prm->maxiter;
   CK(launch_lowrank_materialise(U, kused, V, kused, dl, kused, m, n, Lm, ld, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
   if (iters_out) *iters_out = it;
   if (res_out) *res_out = res;
+  CKS(sync_status(ctx));
+  if (!warn.empty()) ctx->err = warn;
   return RSVD_OK;
 }

@@ -33,9 +33,10 @@ int cq_ng(int Np) { return (int)round_up(Np, 32); }
 template <int TJ>
 __global__ void __launch_bounds__(CQ_THREADS, 1)
 gram_partial_kernel(const double* __restrict__ S, int64_t lds, int64_t rows, int Np, int64_t rows_per_cta,
-                    double* __restrict__ partial) {
+                    double* __restrict__ partial, Pred pr) {
   pdl_wait();
   pdl_trigger();
+  if (pred_skip(pr)) return;
   constexpr int TI = 2 * TJ, NG = 32 * TJ;
   constexpr int LDT = NG + ((4 - NG) & 15);
   extern __shared__ __align__(16) double sm[];
@@ -112,9 +113,10 @@ gram_partial_kernel(const double* __restrict__ S, int64_t lds, int64_t rows, int
 // element each sum p = t, t+T, ... ascending (loads issued in batches of 8 so
 // they are in flight together), then a fixed xor tree.
 __global__ void gram_reduce_kernel(const double* __restrict__ partial, int P, int Ng, int Np,
-                                   double* __restrict__ G, int ldg) {
+                                   double* __restrict__ G, int ldg, Pred pr) {
   pdl_wait();
   pdl_trigger();
+  if (pred_skip(pr)) return;
   constexpr int T = 8, B = 8;
   const int e = blockIdx.x * (blockDim.x / T) + threadIdx.x / T;
   const int t = threadIdx.x % T;
@@ -150,7 +152,7 @@ size_t gram_partial_bytes(int Np, int num_sms) {
 }
 
 cudaError_t launch_gram(const double* S, int64_t lds, int64_t rows, int Np, double* partial, double* G, int ldg,
-                        int num_sms, cudaStream_t st) {
+                        int num_sms, cudaStream_t st, Pred pr) {
   if (Np % 2 || Np > 128 || rows < 1) return cudaErrorInvalidValue;
   const int ng = cq_ng(Np);
   const int P = gram_ctas(rows, num_sms);
@@ -160,7 +162,7 @@ cudaError_t launch_gram(const double* S, int64_t lds, int64_t rows, int Np, doub
 #define RSVD_GRAM(TJ)                                                                                     \
   {                                                                                                      \
     e = smem_optin(gram_partial_kernel<TJ>); if (e != cudaSuccess) return e;                                                                                                     \
-    e = launch_pdl(gram_partial_kernel<TJ>, dim3(P), dim3(CQ_THREADS), smem, st, S, lds, rows, Np, rpc, partial); \
+    e = launch_pdl(gram_partial_kernel<TJ>, dim3(P), dim3(CQ_THREADS), smem, st, S, lds, rows, Np, rpc, partial, pr); \
     if (e != cudaSuccess) return e;                                                                      \
   }
   const size_t smem_max = (size_t)GR_STAGES * GR_BK * ldpad(128) * sizeof(double);
@@ -176,7 +178,7 @@ cudaError_t launch_gram(const double* S, int64_t lds, int64_t rows, int Np, doub
   if (e != cudaSuccess) return e;
   const int per_block = 256 / 8;
   e = launch_pdl(gram_reduce_kernel, dim3((unsigned)ceil_div((int64_t)Np * Np, per_block)), dim3(256), 0, st,
-                 (const double*)partial, P, ng, Np, G, ldg);
+                 (const double*)partial, P, ng, Np, G, ldg, pr);
   if (e != cudaSuccess) return e;
   ++g_kernel_launches;
   return cudaGetLastError();
@@ -262,9 +264,10 @@ __device__ __forceinline__ void chol_diag16(double* D, int ldd, double* Lk, int 
 template <int NBLK>
 __global__ void __launch_bounds__(256, 1)
 chol_blk_kernel(const double* __restrict__ G, int ldg, int l, int npad, double* __restrict__ R,
-                double* __restrict__ Rinv, int* flag, int flag_bit) {
+                double* __restrict__ Rinv, int* flag, int flag_bit, Pred pr) {
   pdl_wait();
   pdl_trigger();
+  if (pred_skip(pr)) return;
   constexpr int NG = 16 * NBLK, LDM = NG + 4;
   extern __shared__ __align__(16) double smc[];
   double* M = smc;                          // NG x LDM
@@ -392,7 +395,7 @@ chol_blk_kernel(const double* __restrict__ G, int ldg, int l, int npad, double* 
 }
 
 cudaError_t launch_chol_aug(const double* G, int ldg, int l, int npad, double* R, double* Rinv, int* flag,
-                            int flag_bit, cudaStream_t st) {
+                            int flag_bit, cudaStream_t st, Pred pr) {
   if (l < 1 || l > 128 || npad > 128 || npad < l) return cudaErrorInvalidValue;
   const int nblk = (npad + 15) / 16;
   const size_t smem = ((size_t)16 * nblk * (16 * nblk + 4) + (size_t)nblk * 16 * CB_LDB) * sizeof(double);
@@ -400,7 +403,7 @@ cudaError_t launch_chol_aug(const double* G, int ldg, int l, int npad, double* R
 #define RSVD_CB(NBK)                                                                                      \
   {                                                                                                      \
     e = smem_optin(chol_blk_kernel<NBK>); if (e != cudaSuccess) return e;                                                                                                     \
-    e = launch_pdl(chol_blk_kernel<NBK>, dim3(1), dim3(256), smem, st, G, ldg, l, npad, R, Rinv, flag, flag_bit); \
+    e = launch_pdl(chol_blk_kernel<NBK>, dim3(1), dim3(256), smem, st, G, ldg, l, npad, R, Rinv, flag, flag_bit, pr); \
     if (e != cudaSuccess) return e;                                                                      \
   }
   switch (nblk) {
@@ -430,9 +433,10 @@ constexpr int AP_BM = 64;
 template <int TJ, int NBUF>
 __global__ void __launch_bounds__(CQ_THREADS)
 panel_apply_kernel(const double* S, int64_t lds, int64_t rows, int Np, const double* __restrict__ T, int64_t ldt,
-                   double* C, int64_t ldc, int Nout, int upper) {
+                   double* C, int64_t ldc, int Nout, int upper, Pred pr) {
   pdl_wait();
   pdl_trigger();
+  if (pred_skip(pr)) return;
   constexpr int NG = 32 * TJ;
   constexpr int LDX = NG + ((4 - NG) & 15);
   extern __shared__ __align__(16) double sm[];
@@ -509,7 +513,7 @@ panel_apply_kernel(const double* S, int64_t lds, int64_t rows, int Np, const dou
 }
 
 cudaError_t launch_panel_apply(const double* S, int64_t lds, int64_t rows, int Np, const double* T, int64_t ldt,
-                               double* C, int64_t ldc, int Nout, bool upper, int num_sms, cudaStream_t st) {
+                               double* C, int64_t ldc, int Nout, bool upper, int num_sms, cudaStream_t st, Pred pr) {
   if (Np % 4 || Np > 128 || (lds & 1) || (ldt & 1) || rows < 1) return cudaErrorInvalidValue;
   const int ng = cq_ng(Np);
   const int ldx = ldpad(ng), ldss = Np + ((4 - Np) & 15);
@@ -526,7 +530,7 @@ cudaError_t launch_panel_apply(const double* S, int64_t lds, int64_t rows, int N
 #define RSVD_APPLY(TJ)                                                                                    \
   {                                                                                                      \
     e = smem_optin(panel_apply_kernel<TJ, (TJ == 4 ? 1 : 2)>); if (e != cudaSuccess) return e;                                                                                                     \
-    e = launch_pdl(panel_apply_kernel<TJ, (TJ == 4 ? 1 : 2)>, dim3((unsigned)grid), dim3(CQ_THREADS), smem, st, S, lds, rows, Np, T, ldt, C, ldc, Nout, upper ? 1 : 0); \
+    e = launch_pdl(panel_apply_kernel<TJ, (TJ == 4 ? 1 : 2)>, dim3((unsigned)grid), dim3(CQ_THREADS), smem, st, S, lds, rows, Np, T, ldt, C, ldc, Nout, upper ? 1 : 0, pr); \
     if (e != cudaSuccess) return e; \
   }
   switch (ng / 32) {

@@ -60,6 +60,16 @@ inline cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
 }
 
+// Device-side predicate on a status word (the call's flags): a predicated
+// kernel returns at entry (after releasing its dependents) unless
+// ((*flag & mask) != 0) == want.  flag == nullptr: always run.  Used for the
+// CholeskyQR -> TSQR breakdown fallback, decided on the device so that a call
+// never waits on the host (api.cu orth()).
+struct Pred { const int* flag; int mask; int want; };
+__device__ __forceinline__ bool pred_skip(const Pred p) {
+  return p.flag != nullptr && (((*reinterpret_cast<const volatile int*>(p.flag) & p.mask) != 0) != (p.want != 0));
+}
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 

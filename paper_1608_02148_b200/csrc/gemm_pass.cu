@@ -64,8 +64,11 @@ __host__ __device__ inline int64_t unit_lo(int64_t units, int grid, int c) {
   return (units * (int64_t)c) / grid;
 }
 
+__global__ void epoch_bump_kernel(unsigned* ctr) { ++*ctr; }   // the next pass's stream-K epoch (kernels.h)
+
 template <typename TA, bool TRANS, int TMAX, bool CENT>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) {
+  const unsigned epoch = g.flags ? *reinterpret_cast<const volatile unsigned*>(g.flags + kEpochSlot) : 0u;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   using S = GemmSmem<TA>;
   TA* As = reinterpret_cast<TA*>(smem_raw);
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
       }
       __threadfence();
       __syncthreads();
-      if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(g.epoch) : "memory");
+      if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(epoch) : "memory");
       return;
     }
     if (seg_end < rb_hi) {
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_pass_kernel(GemmArgs g) 
         unsigned f;
         do {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(g.flags + c) : "memory");
-        } while (f != g.epoch);
+        } while (f != epoch);
         const double* pb = g.P + (int64_t)c * BM * N;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -346,7 +349,7 @@ cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st) {
   GemmArgs g;
   g.A = c.A; g.lda = c.lda; g.B = c.B; g.ldb = c.ldb; g.C = c.C; g.ldc = c.ldc; g.P = c.P;
   g.c = c.center; g.rs = c.rscale; g.M = c.M; g.K = c.K; g.N = c.N; g.Nout = c.Nout;
-  g.flags = c.flags; g.epoch = c.epoch;
+  g.flags = c.flags;
   g.KT = ceil_div(c.K, BK);
   g.units = ceil_div(c.M, BM) * g.KT;
   g.grid = gemm_choose_grid(c.M, c.K, c.grid > 0 ? c.grid : 148);
@@ -355,6 +358,10 @@ cudaError_t gemm_pass(const GemmCall& c, cudaStream_t st) {
     g.a_vec = ((uintptr_t)c.A % 16 == 0) && ((c.lda * es) % 16 == 0);
   }
   if (g.grid > 1 && (c.P == nullptr || c.flags == nullptr)) return cudaErrorInvalidValue;
+  if (c.flags) {
+    epoch_bump_kernel<<<1, 1, 0, st>>>(c.flags + kEpochSlot);
+    ++g_kernel_launches;
+  }
   cudaError_t e;
   if (c.a_f32) e = c.trans ? dispatch_tmax<float, true>(g, st) : dispatch_tmax<float, false>(g, st);
   else e = c.trans ? dispatch_tmax<double, true>(g, st) : dispatch_tmax<double, false>(g, st);

@@ -4,10 +4,21 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <atomic>
+
+#include "common.cuh"
+
 namespace rsvd {
 
-// Kernels launched by this library (all launchers add to it).
-extern int64_t g_kernel_launches;
+// Kernels launched by this library (all launchers add to it; rank-group threads share it).
+extern std::atomic<int64_t> g_kernel_launches;
+
+// Stream-K bookkeeping in the context's 4096-word flag array: [0, grid) the
+// DMMA / TF32 passes' "partial published" flags, [2048, 2048 + 4 grid) the
+// Ozaki passes' arrival counters, kEpochSlot the device-side launch epoch
+// (advanced by the kernel that precedes each pass, so CUDA-graph replays of a
+// captured call see a new epoch every time).
+constexpr int kEpochSlot = 4095;
 
 // ---- K2/K3 streaming passes (gemm_pass.cu)
 struct GemmCall {
@@ -15,7 +26,7 @@ struct GemmCall {
   const double* B; int64_t ldb;          // K x N, N % 16 == 0, zero-padded columns
   double* C; int64_t ldc;                // output M x Nout
   double* P;                             // split partials (>= gemm_partial_bytes)
-  unsigned* flags; unsigned epoch;       // >= grid flags, zero-initialised once; epoch unique per launch
+  unsigned* flags; unsigned epoch;       // >= 4096 flag words, zero-initialised once (epoch: unused, see kEpochSlot)
   const double* center;                  // per A-column mean (nullable)
   const double* rscale;                  // per A-column 1/s.d. (nullable)
   int64_t M, K; int N, Nout;
@@ -48,16 +59,17 @@ cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st);
 int gram_ctas(int64_t rows, int num_sms);
 size_t gram_partial_bytes(int Np, int num_sms);
 cudaError_t launch_gram(const double* S, int64_t lds, int64_t rows, int Np, double* partial, double* G, int ldg,
-                        int num_sms, cudaStream_t st);
+                        int num_sms, cudaStream_t st, Pred pr = Pred{});
 // G = R^T R (l x l leading block of G, ld ldg) and R^-1, by symmetric elimination
 // on [G | I]; R, Rinv npad x npad (ld npad, zero padded; R nullable); flag |= flag_bit
 // on breakdown (pivot <= 1e-13 of its original diagonal, or non-finite).
 cudaError_t launch_chol_aug(const double* G, int ldg, int l, int npad, double* R, double* Rinv, int* flag,
-                            int flag_bit, cudaStream_t st);
+                            int flag_bit, cudaStream_t st, Pred pr = Pred{});
 // C (rows x Nout, ld ldc) = S (rows x Np, ld lds) * T (Np x Np, ld ldt); C may alias S.
 // upper: T is upper triangular (skips the zero blocks).
 cudaError_t launch_panel_apply(const double* S, int64_t lds, int64_t rows, int Np, const double* T, int64_t ldt,
-                               double* C, int64_t ldc, int Nout, bool upper, int num_sms, cudaStream_t st);
+                               double* C, int64_t ldc, int Nout, bool upper, int num_sms, cudaStream_t st,
+                               Pred pr = Pred{});
 
 // ---- FP64 passes by Ozaki-scheme int8 slices on tcgen05 (pass_ozaki.cu)
 #define OZ_S 7                                   // 8-bit digits per element (A: 56-bit two's complement, X: 54-bit balanced)
@@ -115,10 +127,10 @@ cudaError_t launch_small_matmul(const double* A, const double* B, double* C, int
 // Rstack + leaf*l*l (ld l).
 int leaf_rows_cap(int l);
 cudaError_t launch_hqr_leaves(double* Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
-                              double* Rstack, cudaStream_t st);
+                              double* Rstack, cudaStream_t st, Pred pr = Pred{});
 // Q rows of each leaf <- Q rows * S_leaf, S_leaf = rows [leaf*l, leaf*l+l) of S (ld lds).
 cudaError_t launch_tsqr_combine(double* Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
-                                const double* S, int64_t lds, cudaStream_t st);
+                                const double* S, int64_t lds, cudaStream_t st, Pred pr = Pred{});
 
 // One-sided Jacobi SVD of X = R^T (R upper l x l, ld ldr): X J = W Sigma (jacobi.cu).
 // Outputs: sigma (l, descending), W (ldo x ldo) = U~, J (ldo x ldo), zero outside
@@ -138,12 +150,31 @@ cudaError_t launch_scale_cols(double* X, int64_t ldx, int64_t rows, int l, const
                               cudaStream_t st);
 // dst (rows x cols, ldd, f32 or f64) = src (ld lds) ; optional per-column factor
 cudaError_t launch_copy_out(const double* src, int64_t lds, int64_t rows, int cols, void* dst,
-                            int64_t ldd, bool dst_f32, const double* colfac, cudaStream_t st);
+                            int64_t ldd, bool dst_f32, const double* colfac, cudaStream_t st,
+                            Pred pr = Pred{});
 cudaError_t launch_fill(double* p, int64_t count, double v, cudaStream_t st);
 // Y (rows x ld) columns [l, npad) set to zero
 cudaError_t launch_zero_cols(double* Y, int64_t ld, int64_t rows, int l, int npad, cudaStream_t st);
 // rpca: eig[i] = d[i]^2 / (m-1)
 cudaError_t launch_pca_eig(const double* d, int k, double m, void* eig, bool f32, cudaStream_t st);
+// rpca outputs (Alg. 6; reading R32 of DESIGN.md)
+cudaError_t launch_colstat_scale(const double* ss, int64_t n, double m_global, double* rs, double* s, cudaStream_t st);
+cudaError_t launch_total_var(const double* ss, const double* rs, int64_t n, double m_global, double* out,
+                             cudaStream_t st);
+cudaError_t launch_pca_stats(const double* d, int k, double m_global, const double* total, void* eig, void* sdev,
+                             void* ratio, void* cum, bool f32, cudaStream_t st);
+// dst[j] = src[j] (mode 0), 1/src[j] (1), src[j]/sqrt(v-1) (2), v (3)
+cudaError_t launch_vec_map(const void* src, bool src_f32, int64_t n, int mode, double v, double* dst, cudaStream_t st);
+// X (rows x npad, FP64, zero padded) = src (rows x cols)
+cudaError_t launch_copy_in(const void* src, bool src_f32, int64_t lds, int64_t rows, int cols, int npad, double* X,
+                           int64_t ldx, cudaStream_t st);
+// status words: *flag |= bits (predicated); end-of-call sticky status
+cudaError_t launch_flag_or(int* flag, int bits, cudaStream_t st, Pred pr);
+cudaError_t launch_status_finish(const int* flag, int* sticky, int fallback_bit, cudaStream_t st);
+// in-process rank groups: out = in[0] op in[1] ... (fixed rank order)
+constexpr int kMaxGroup = 16;
+struct GroupPtrs { const double* p[kMaxGroup]; };
+cudaError_t launch_group_reduce(const GroupPtrs& in, int nranks, int64_t n, int op_max, double* out, cudaStream_t st);
 // Finite check of flags: flag |= 4 if any non-finite among v[0..n)
 cudaError_t launch_check_finite(const double* v, int64_t n, int* flag, cudaStream_t st);
 

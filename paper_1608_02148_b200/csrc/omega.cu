@@ -20,7 +20,7 @@
 
 namespace rsvd {
 
-int64_t g_kernel_launches = 0;
+std::atomic<int64_t> g_kernel_launches{0};
 
 cudaError_t smem_optin_fn(const void* fn) {
   static std::mutex mu;

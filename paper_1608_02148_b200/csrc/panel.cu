@@ -13,6 +13,8 @@
 //  * sign / copy / column statistics helpers.
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -308,9 +310,10 @@ int leaf_rows_cap(int l) {
 
 __global__ void __launch_bounds__(HQR_THREADS) hqr_leaves_kernel(double* __restrict__ Y, int64_t ldy,
                                                                  int64_t M, int l, int64_t nleaves,
-                                                                 double* __restrict__ Rstack) {
+                                                                 double* __restrict__ Rstack, Pred pr) {
   pdl_wait();
   pdl_trigger();
+  if (pred_skip(pr)) return;
   extern __shared__ double sm[];
   const int64_t leaf = blockIdx.x;
   const int64_t rb = M / nleaves, rem = M % nleaves;
@@ -415,22 +418,23 @@ __global__ void __launch_bounds__(HQR_THREADS) hqr_leaves_kernel(double* __restr
 }
 
 cudaError_t launch_hqr_leaves(double* Y, int64_t ldy, int64_t M, int l, int64_t nleaves, double* Rstack,
-                              cudaStream_t st) {
+                              cudaStream_t st, Pred pr) {
   const int64_t bmax = ceil_div(M, nleaves);
   const size_t smem = ((size_t)bmax * l + l + 32) * sizeof(double);
   if (smem > (size_t)SMEM_OPTIN || bmax < l) return cudaErrorInvalidValue;
   cudaError_t e = set_smem((const void*)hqr_leaves_kernel, smem);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(hqr_leaves_kernel, dim3((unsigned)nleaves), dim3(HQR_THREADS), smem, st, Y, ldy, M, l, nleaves, Rstack);
+  e = launch_pdl(hqr_leaves_kernel, dim3((unsigned)nleaves), dim3(HQR_THREADS), smem, st, Y, ldy, M, l, nleaves, Rstack, pr);
   if (e != cudaSuccess) return e;
   ++g_kernel_launches;
   return cudaGetLastError();
 }
 
 __global__ void tsqr_combine_kernel(double* __restrict__ Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
-                                    const double* __restrict__ S, int64_t lds) {
+                                    const double* __restrict__ S, int64_t lds, Pred pr) {
   pdl_wait();
   pdl_trigger();
+  if (pred_skip(pr)) return;
   extern __shared__ double sm[];
   double* Ss = sm;                 // l x l
   double* rows = Ss + l * l;       // 16 x l
@@ -455,11 +459,11 @@ __global__ void tsqr_combine_kernel(double* __restrict__ Y, int64_t ldy, int64_t
 }
 
 cudaError_t launch_tsqr_combine(double* Y, int64_t ldy, int64_t M, int l, int64_t nleaves, const double* S,
-                                int64_t lds, cudaStream_t st) {
+                                int64_t lds, cudaStream_t st, Pred pr) {
   const size_t smem = ((size_t)l * l + 16 * (size_t)l) * sizeof(double);
   cudaError_t e = set_smem((const void*)tsqr_combine_kernel, smem);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(tsqr_combine_kernel, dim3((unsigned)nleaves), dim3(512), smem, st, Y, ldy, M, l, nleaves, S, lds);
+  e = launch_pdl(tsqr_combine_kernel, dim3((unsigned)nleaves), dim3(512), smem, st, Y, ldy, M, l, nleaves, S, lds, pr);
   if (e != cudaSuccess) return e;
   ++g_kernel_launches;
   return cudaGetLastError();
@@ -525,9 +529,10 @@ cudaError_t launch_scale_cols(double* X, int64_t ldx, int64_t rows, int l, const
 
 template <typename TO>
 __global__ void copy_out_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int cols,
-                                TO* __restrict__ dst, int64_t ldd, const double* colfac) {
+                                TO* __restrict__ dst, int64_t ldd, const double* colfac, Pred pr) {
   pdl_wait();
   pdl_trigger();
+  if (pred_skip(pr)) return;
   const int64_t total = rows * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / cols;
@@ -539,12 +544,13 @@ __global__ void copy_out_kernel(const double* __restrict__ src, int64_t lds, int
 }
 
 cudaError_t launch_copy_out(const double* src, int64_t lds, int64_t rows, int cols, void* dst, int64_t ldd,
-                            bool dst_f32, const double* colfac, cudaStream_t st) {
+                            bool dst_f32, const double* colfac, cudaStream_t st, Pred pr) {
   if (rows * cols == 0) return cudaSuccess;
   if (dst_f32)
-    CUDA_TRY(launch_pdl(copy_out_kernel<float>, dim3(grid_for(rows * cols)), dim3(256), 0, st, src, lds, rows, cols, (float*)dst, ldd, colfac));
+    CUDA_TRY(launch_pdl(copy_out_kernel<float>, dim3(grid_for(rows * cols)), dim3(256), 0, st, src, lds, rows, cols, (float*)dst, ldd, colfac, pr));
   else
-    CUDA_TRY(launch_pdl(copy_out_kernel<double>, dim3(grid_for(rows * cols)), dim3(256), 0, st, src, lds, rows, cols, (double*)dst, ldd, colfac)); ++g_kernel_launches;
+    CUDA_TRY(launch_pdl(copy_out_kernel<double>, dim3(grid_for(rows * cols)), dim3(256), 0, st, src, lds, rows, cols, (double*)dst, ldd, colfac, pr));
+  ++g_kernel_launches;
   return cudaGetLastError();
 }
 
@@ -598,6 +604,183 @@ __global__ void check_finite_kernel(const double* v, int64_t n, int* flag) {
 cudaError_t launch_check_finite(const double* v, int64_t n, int* flag, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   CUDA_TRY(launch_pdl(check_finite_kernel, dim3(grid_for(n)), dim3(256), 0, st, v, n, flag)); ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace rsvd
+
+namespace rsvd {
+
+// ------------------------------------------------------------------ rpca outputs (Alg. 6)
+// rs = 1 / s.d. and s = s.d. from the column sums of squares ss of the centred
+// data (non-destructive: ss stays for the total variance); constant columns
+// get s = 1 (no scaling)
+__global__ void colstat_scale_kernel(const double* ss, int64_t n, double mg, double* rs, double* s) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double sd = sqrt(ss[j] / (mg - 1.0));
+  if (!(sd > 0.0)) sd = 1.0;
+  s[j] = sd;
+  rs[j] = 1.0 / sd;
+}
+
+cudaError_t launch_colstat_scale(const double* ss, int64_t n, double m_global, double* rs, double* s, cudaStream_t st) {
+  CUDA_TRY(launch_pdl(colstat_scale_kernel, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, st, ss, n, m_global, rs, s));
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+// total variance sum_j var(X_j) = sum_j ss_j rs_j^2 / (m - 1) (the trace of the
+// covariance / correlation matrix = sum of ALL its eigenvalues);
+// one CTA, fixed-order partial sums then a fixed tree (deterministic)
+__global__ void total_var_kernel(const double* ss, const double* rs, int64_t n, double mg, double* out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const double f = rs ? rs[j] : 1.0;
+    s += ss[j] * f * f;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s / (mg - 1.0);
+}
+
+cudaError_t launch_total_var(const double* ss, const double* rs, int64_t n, double m_global, double* out, cudaStream_t st) {
+  CUDA_TRY(launch_pdl(total_var_kernel, dim3(1), dim3(256), 0, st, ss, rs, n, m_global, out));
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+// eigvals = d^2 / (m-1), sdev = sqrt(eigvals), the proportion of
+// variance eigvals / total and its cumulative sum (summary());
+// every output nullable; one thread per value, the cumulative sum in index order
+template <typename TO>
+__global__ void pca_stats_kernel(const double* d, int k, double mg, const double* total, TO* eig, TO* sdev, TO* ratio,
+                                 TO* cum) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = threadIdx.x;
+  if (i < k) {
+    const double e = d[i] * d[i] / (mg - 1.0);
+    if (eig) eig[i] = (TO)e;
+    if (sdev) sdev[i] = (TO)sqrt(e);
+    if (ratio && total) ratio[i] = (TO)(e / *total);
+  }
+  if (cum && total && i == 0) {
+    double c = 0.0;
+    for (int t = 0; t < k; ++t) {
+      c += d[t] * d[t] / (mg - 1.0);
+      cum[t] = (TO)(c / *total);
+    }
+  }
+}
+
+cudaError_t launch_pca_stats(const double* d, int k, double m_global, const double* total, void* eig, void* sdev,
+                             void* ratio, void* cum, bool f32, cudaStream_t st) {
+  if (k > 1024) return cudaErrorInvalidValue;
+  if (f32)
+    CUDA_TRY(launch_pdl(pca_stats_kernel<float>, dim3(1), dim3(1024), 0, st, d, k, m_global, total, (float*)eig,
+                        (float*)sdev, (float*)ratio, (float*)cum));
+  else
+    CUDA_TRY(launch_pdl(pca_stats_kernel<double>, dim3(1), dim3(1024), 0, st, d, k, m_global, total, (double*)eig,
+                        (double*)sdev, (double*)ratio, (double*)cum));
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+// dst[j] = f(src[j]) for a small vector: mode 0 copy, 1 reciprocal, 2 sqrt(src / (m - 1)) (= sdev from d), 3 = constant v
+template <typename TI>
+__global__ void vec_map_kernel(const TI* src, int64_t n, int mode, double v, double* dst) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double x = src ? (double)src[j] : 0.0;
+  dst[j] = mode == 0 ? x : mode == 1 ? 1.0 / x : mode == 2 ? x / sqrt(v - 1.0) : v;
+}
+
+cudaError_t launch_vec_map(const void* src, bool src_f32, int64_t n, int mode, double v, double* dst, cudaStream_t st) {
+  const dim3 g((unsigned)ceil_div(n, 256));
+  if (src_f32) CUDA_TRY(launch_pdl(vec_map_kernel<float>, g, dim3(256), 0, st, (const float*)src, n, mode, v, dst));
+  else CUDA_TRY(launch_pdl(vec_map_kernel<double>, g, dim3(256), 0, st, (const double*)src, n, mode, v, dst));
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+// X (rows x npad, ld ldx, FP64) = src (rows x cols, ld lds, f32 or f64), columns [cols, npad) zero
+template <typename TI>
+__global__ void copy_in_kernel(const TI* __restrict__ src, int64_t lds, int64_t rows, int cols, int npad,
+                               double* __restrict__ X, int64_t ldx) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t total = rows * npad;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / npad;
+    const int c = (int)(e % npad);
+    X[r * ldx + c] = c < cols ? (double)src[r * lds + c] : 0.0;
+  }
+}
+
+cudaError_t launch_copy_in(const void* src, bool src_f32, int64_t lds, int64_t rows, int cols, int npad, double* X,
+                           int64_t ldx, cudaStream_t st) {
+  const int64_t total = rows * npad;
+  const unsigned g = (unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+  if (src_f32) CUDA_TRY(launch_pdl(copy_in_kernel<float>, dim3(g), dim3(256), 0, st, (const float*)src, lds, rows, cols, npad, X, ldx));
+  else CUDA_TRY(launch_pdl(copy_in_kernel<double>, dim3(g), dim3(256), 0, st, (const double*)src, lds, rows, cols, npad, X, ldx));
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ status words
+__global__ void flag_or_kernel(int* flag, int bits, Pred pr) {
+  pdl_wait();
+  pdl_trigger();
+  if (pred_skip(pr)) return;
+  atomicOr(flag, bits);
+}
+
+cudaError_t launch_flag_or(int* flag, int bits, cudaStream_t st, Pred pr) {
+  CUDA_TRY(launch_pdl(flag_or_kernel, dim3(1), dim3(1), 0, st, flag, bits, pr));
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+// end of a call: the call's flags (flag[0]) are OR-ed into the context's sticky
+// status (read and cleared by rsvd_sync); sticky[1] = Jacobi sweeps, sticky[2] =
+// 1 if the TSQR fallback ran in this call
+__global__ void status_finish_kernel(const int* flag, int* sticky, int fallback_bit) {
+  pdl_wait();
+  pdl_trigger();
+  atomicOr(sticky, flag[0]);
+  sticky[1] = flag[8];
+  sticky[2] = (flag[0] & fallback_bit) ? 1 : 0;
+}
+
+cudaError_t launch_status_finish(const int* flag, int* sticky, int fallback_bit, cudaStream_t st) {
+  CUDA_TRY(launch_pdl(status_finish_kernel, dim3(1), dim3(1), 0, st, flag, sticky, fallback_bit));
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ in-process rank groups
+// out[i] = stage[0][i] (+ / max) stage[1][i] ... stage[R-1][i], ranks in order
+// (every rank computes the identical result: the stand-in for ncclAllReduce)
+__global__ void group_reduce_kernel(GroupPtrs in, int nranks, int64_t n, int op_max, double* out) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = in.p[0][i];
+    for (int r = 1; r < nranks; ++r) s = op_max ? fmax(s, in.p[r][i]) : s + in.p[r][i];
+    out[i] = s;
+  }
+}
+
+cudaError_t launch_group_reduce(const GroupPtrs& in, int nranks, int64_t n, int op_max, double* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 8);
+  CUDA_TRY(launch_pdl(group_reduce_kernel, dim3(g), dim3(256), 0, st, in, nranks, n, op_max, out));
+  ++g_kernel_launches;
   return cudaGetLastError();
 }
 

@@ -208,9 +208,12 @@ __host__ __device__ constexpr int xt_smem(int S) { return S * XT_COLS * XT_LD; }
 template <int S>
 __global__ void __launch_bounds__(XT_THREADS)
 ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, int8_t* __restrict__ xs,
-                     int64_t ldk, double* __restrict__ xf) {
+                     int64_t ldk, double* __restrict__ xf, unsigned* epoch_ctr) {
   pdl_wait();
   pdl_trigger();
+  // the next pass kernel's stream-K epoch (read by it after its griddepcontrol.wait):
+  // advanced on the device so that CUDA-graph replays get fresh epochs too
+  if (epoch_ctr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) ++*epoch_ctr;
   extern __shared__ __align__(16) unsigned char xt[];      // S x XT_COLS x XT_LD
   __shared__ double red[XT_G][XT_COLS];
   __shared__ double escale[XT_COLS];
@@ -297,6 +300,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   pdl_wait();
   if (threadIdx.x == 0) OZ_TL(0)
   pdl_trigger();
+  const unsigned epoch = *reinterpret_cast<const volatile unsigned*>(g.flags + kEpochSlot);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int BKU = BK;                           // k per unit
@@ -542,7 +546,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
             __threadfence();                         // this CTA's partial before its arrival
             unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(cnt), nw;
             for (;;) {
-              nw = ((old >> 32) == g.epoch) ? old + 1 : (((unsigned long long)g.epoch << 32) | 1ull);
+              nw = ((old >> 32) == epoch) ? old + 1 : (((unsigned long long)epoch << 32) | 1ull);
               const unsigned long long seen = atomicCAS(cnt, old, nw);
               if (seen == old) break;
               old = seen;
@@ -729,7 +733,8 @@ static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st) {
   const cudaError_t ea = smem_optin(ozaki_slice_x_kernel<OZ_S>);
   if (ea != cudaSuccess) return ea;
   const dim3 gs((unsigned)ceil_div(ldk, ET), (unsigned)ceil_div(N, XT_COLS));
-  const cudaError_t el = launch_pdl(ozaki_slice_x_kernel<OZ_S>, gs, dim3(XT_THREADS), (size_t)xt_smem(OZ_S), st, c.B, c.ldb, c.K, N, xs, ldk, xf);
+  const cudaError_t el = launch_pdl(ozaki_slice_x_kernel<OZ_S>, gs, dim3(XT_THREADS), (size_t)xt_smem(OZ_S), st, c.B, c.ldb, c.K, N, xs, ldk, xf,
+                                   c.flags ? c.flags + kEpochSlot : nullptr);
   if (el != cudaSuccess) return el;
   ++g_kernel_launches;
   return cudaGetLastError();

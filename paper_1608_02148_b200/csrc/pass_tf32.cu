@@ -58,6 +58,7 @@ template <bool TRANS>
 __global__ void __launch_bounds__(THREADS, 1)
 pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBhi,
                  const __grid_constant__ CUtensorMap mapBlo, Args g) {
+  const unsigned epoch = *reinterpret_cast<const volatile unsigned*>(g.flags + kEpochSlot);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned carve-up (SWIZZLE_128B atoms)
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -255,7 +256,7 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                 unsigned f;
                 do {
                   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(g.flags + c) : "memory");
-                } while (f != g.epoch);
+                } while (f != epoch);
                 const double* src = g.P + ((int64_t)c * BM + row) * g.N + c0;
 #pragma unroll
                 for (int j = 0; j < 32; j += 2) {
@@ -276,7 +277,7 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         if (cont) {
           __threadfence();
           asm volatile("bar.sync 1, 128;" ::: "memory");     // the four epilogue warps
-          if (et == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(g.epoch) : "memory");
+          if (et == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(epoch) : "memory");
         }
         sub = 0;
       }
@@ -313,6 +314,7 @@ template <bool NN>
 __global__ void __launch_bounds__(THREADS, 1)
 pass_tf32_tn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapQhi,
                     const __grid_constant__ CUtensorMap mapQlo, Args g) {
+  const unsigned epoch = *reinterpret_cast<const volatile unsigned*>(g.flags + kEpochSlot);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[TN_STAGES], splitd[TN_STAGES], empty_[TN_STAGES], accf[2], acce[2];
@@ -495,7 +497,7 @@ pass_tf32_tn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 unsigned f;
                 do {
                   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(g.flags + c) : "memory");
-                } while (f != g.epoch);
+                } while (f != epoch);
                 const double* src = g.P + ((int64_t)c * 128 + col) * TN_BN + j0;
 #pragma unroll
                 for (int j = 0; j < 32; j += 2) {
@@ -517,7 +519,7 @@ pass_tf32_tn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         if (cont) {
           __threadfence();
           asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (et == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(g.epoch) : "memory");
+          if (et == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(g.flags + blockIdx.x), "r"(epoch) : "memory");
         }
         sub = 0;
       }
@@ -537,7 +539,8 @@ pass_tf32_tn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
 
 // X (K x Np, FP64, ld ldx) -> Xhi, Xlo (K x N, FP32, row-major, zero-padded columns)
 __global__ void prep_split_b(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, int N,
-                             float* __restrict__ hi, float* __restrict__ lo) {
+                             float* __restrict__ hi, float* __restrict__ lo, unsigned* epoch_ctr) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) ++*epoch_ctr;   // the pass kernel's stream-K epoch (kernels.h)
   const int64_t total = K * N;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = e / N;
@@ -608,7 +611,7 @@ cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st) {
     int64_t total = c.K * N;
     int blocks = (int)ceil_div(total, 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
-    prep_split_b<<<blocks, 256, 0, st>>>(c.B, c.ldb, c.K, c.N, N, hi, lo);
+    prep_split_b<<<blocks, 256, 0, st>>>(c.B, c.ldb, c.K, c.N, N, hi, lo, c.flags + kEpochSlot);
     ++g_kernel_launches;
   }
   // 2) tensor maps
@@ -620,7 +623,7 @@ cudaError_t tf32_pass(const Tf32Call& c, cudaStream_t st) {
   if (!ok) return cudaErrorInvalidValue;
   Args g;
   g.C = c.C; g.ldc = c.ldc; g.P = c.P; g.M = c.M; g.K = c.K; g.N = N; g.Nout = c.Nout;
-  g.flags = c.flags; g.epoch = c.epoch;
+  g.flags = c.flags;
   if (c.flags == nullptr) return cudaErrorInvalidValue;
   g.KT = ceil_div(c.K, BK);
   static const bool tn_qta = [] { const char* e = getenv("RSVD_TF32_TN"); return !(e && e[0] == '0'); }();

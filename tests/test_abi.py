@@ -54,8 +54,9 @@ def test_struct_layouts_match_header(so_path):
 #include <stddef.h>
 #include "rsvd_b200.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu\n", sizeof(rsvd_matrix), sizeof(rsvd_params), sizeof(rsvd_rrpca_params),
-         offsetof(rsvd_params, seed), offsetof(rsvd_rrpca_params, seed));
+  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(rsvd_matrix), sizeof(rsvd_params), sizeof(rsvd_rrpca_params),
+         offsetof(rsvd_params, seed), offsetof(rsvd_rrpca_params, seed), sizeof(rsvd_pca_out),
+         offsetof(rsvd_pca_out, x_white));
   return 0;
 }
 '''
@@ -67,7 +68,7 @@ int main(void) {
         subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
         got = [int(x) for x in subprocess.check_output([exe]).split()]
     want = [ctypes.sizeof(rb.Matrix), ctypes.sizeof(rb.Params), ctypes.sizeof(rb.RrpcaParams),
-            rb.Params.seed.offset, rb.RrpcaParams.seed.offset]
+            rb.Params.seed.offset, rb.RrpcaParams.seed.offset, ctypes.sizeof(rb.PcaOut), rb.PcaOut.x_white.offset]
     assert got == want
 
 

@@ -1,0 +1,160 @@
+"""The library's row-sharded (nranks > 1) path, executed on ONE GPU through an
+in-process rank group (rsvd_group): R contexts, one host thread
+and one stream each, rank r holding rows [offset_r, offset_r + m_r) of A; the
+collectives (the n x l allreduce of A^T Q, the l x l Gram allreduce of
+CholeskyQR, the column sums of rpca, the allgather of the TSQR fallback, the
+IALM scalars) are fixed-rank-order device reductions.  Alg. 4 steps (3) and
+(10) computed per row block and summed.
+
+Checks: d equal to the 1-rank run within 1e-12 relative and to the oracle
+within 1e-10 (BASELINE.json north_star FP64 tolerance); U (gathered rows) and V
+orthonormal to 1e-12; the rank-deficient config 1 exercises the distributed
+TSQR fallback."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthetic
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1608_02148_b200 as rb
+    return rb
+
+
+def _np(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def _sharded_rsvd(rb, A, k, world, **kw):
+    """rsvd of the device matrix A split into `world` row blocks; returns
+    (d, U gathered in row order, V, fallback flags per rank)."""
+    m = A.shape[0]
+    parts = rb.row_partition(m, world)
+
+    def fn(ctx, r):
+        off, rows = parts[r]
+        res = rb.rsvd(A[off:off + rows], k, ctx=ctx, m_global=m, row_offset=off, sync=False, **kw)
+        ctx.sync()
+        return res, ctx.stats()["tsqr_fallback"]
+
+    out = rb.run_ranks(fn, world)
+    d0 = out[0][0].d
+    for res, _ in out[1:]:
+        assert torch.equal(res.d, d0), "ranks disagree on d"
+        assert torch.equal(res.v, out[0][0].v), "ranks disagree on V"
+    U = torch.cat([res.u for res, _ in out], dim=0)
+    return _np(d0), _np(U), _np(out[0][0].v), [f for _, f in out]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_config1_sharded_exact_rank(rb, world):
+    """Config 1 (exact rank 10, l = 20) row-sharded: every rank's CholeskyQR of
+    the rank-deficient sketch breaks down, the distributed TSQR fallback
+    (local TSQR, allgather of the R factors, QR of the stack) runs, and the
+    planted singular values come back to 1e-12 (J:7)."""
+    A, meta = synthetic.make_config(1)
+    Ad = A.cuda()
+    d, U, V, fb = _sharded_rsvd(rb, Ad, 10, world, p=10, q=2, sdist="normal", seed=meta["seed_omega"])
+    s = meta["s"].numpy()
+    assert np.max(np.abs(d - s) / s) <= 1e-12
+    assert all(fb), "the TSQR fallback should have run on every rank"
+    assert np.abs(U.T @ U - np.eye(10)).max() <= 1e-12
+    assert np.abs(V.T @ V - np.eye(10)).max() <= 1e-12
+    o = oracle.oracle_rsvd(A.numpy(), 10, p=10, q=2, sdist="normal", seed=meta["seed_omega"])
+    assert np.max(np.abs(d - o["d"]) / o["d"]) <= 1e-10
+    r1 = rb.rsvd(Ad, 10, p=10, q=2, sdist="normal", seed=meta["seed_omega"])
+    assert np.max(np.abs(d - _np(r1.d)) / _np(r1.d)) <= 1e-12
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_config2_sharded(rb, world):
+    """Config 2 (J:8, 10000 x 5000, Rademacher Omega) row-sharded over 2/4/8
+    ranks: d within 1e-12 of the 1-rank run and 1e-10 of the oracle, the
+    reconstruction error within 1.0001 x the oracle's (+1e-13, R24)."""
+    A, meta = synthetic.make_config(2)
+    Ad = A.cuda()
+    kw = dict(p=10, q=2, sdist="rademacher", seed=meta["seed_omega"])
+    d, U, V, _ = _sharded_rsvd(rb, Ad, 50, world, **kw)
+    r1 = rb.rsvd(Ad, 50, **kw)
+    d1 = _np(r1.d)
+    assert np.max(np.abs(d - d1) / d1) <= 1e-12
+    o = oracle.oracle_rsvd(A.numpy(), 50, **kw)
+    assert np.max(np.abs(d - o["d"]) / o["d"]) <= 1e-10
+    assert np.abs(U.T @ U - np.eye(50)).max() <= 1e-12
+    An = A.numpy()
+    e = np.linalg.norm(An - (U * d) @ V.T) / np.linalg.norm(An)
+    eo = np.linalg.norm(An - (o["u"] * o["d"]) @ o["v"].T) / np.linalg.norm(An)
+    assert e <= 1.0001 * eo + 1e-13
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rpca_sharded_matches_single_rank(rb, world):
+    """rpca with centring and scaling row-sharded: the column means and s.d. are
+    allreduced, everything else matches the 1-rank run and the oracle."""
+    g = torch.Generator().manual_seed(4)
+    A = (torch.randn(6000, 300, generator=g, dtype=torch.float64) *
+         torch.exp(-torch.arange(300, dtype=torch.float64) / 40) + torch.linspace(0, 5, 300, dtype=torch.float64))
+    Ad = A.cuda()
+    parts = rb.row_partition(A.shape[0], world)
+
+    def fn(ctx, r):
+        off, rows = parts[r]
+        return rb.rpca(Ad[off:off + rows], 20, center=True, scale=True, p=10, q=2, seed=3, ctx=ctx,
+                       m_global=A.shape[0], row_offset=off, explained=True)
+
+    out = rb.run_ranks(fn, world)
+    one = rb.rpca(Ad, 20, center=True, scale=True, p=10, q=2, seed=3, explained=True)
+    o = oracle.oracle_rpca(A.numpy(), 20, center=True, scale=True, p=10, q=2, seed=3)
+    for key in ("eigvals", "center", "scale", "var_ratio"):
+        got = _np(out[0][key])
+        assert np.max(np.abs(got - _np(one[key])) / np.abs(_np(one[key]))) <= 1e-12, key
+        assert np.max(np.abs(got - o[key]) / np.abs(o[key])) <= 1e-10, key
+    x = np.concatenate([_np(res["x"]) for res in out], axis=0)
+    assert np.linalg.norm(x - o["x"]) / np.linalg.norm(o["x"]) < 1e-9
+
+
+def test_rrpca_sharded(rb):
+    """rrpca (Alg. 7) over 2 ranks: the IALM scalars (||A||_F^2 partials, max|A|,
+    the residual) are allreduced; same iterations and L, S as the 1-rank run."""
+    A, L0, S0 = synthetic.sparse_plus_lowrank(4000, 300, rank=5, frac=0.05, seed=12)
+    Ad = A.cuda()
+    parts = rb.row_partition(A.shape[0], 2)
+
+    def fn(ctx, r):
+        off, rows = parts[r]
+        return rb.rrpca(Ad[off:off + rows].contiguous(), k=10, p=10, q=2, tol=1e-7, maxiter=100, seed=3, ctx=ctx,
+                        m_global=A.shape[0], row_offset=off)
+
+    out = rb.run_ranks(fn, 2)
+    one = rb.rrpca(Ad, k=10, p=10, q=2, tol=1e-7, maxiter=100, seed=3)
+    assert out[0]["iters"] == out[1]["iters"] == one["iters"]
+    L = np.concatenate([_np(o["L"]) for o in out], axis=0)
+    S = np.concatenate([_np(o["S"]) for o in out], axis=0)
+    assert np.linalg.norm(L - _np(one["L"])) / np.linalg.norm(_np(one["L"])) < 1e-10
+    assert np.linalg.norm(S - _np(one["S"])) / np.linalg.norm(_np(one["S"])) < 1e-10
+    assert np.linalg.norm(L - L0.numpy()) / np.linalg.norm(L0.numpy()) < 1e-6
+
+
+def test_group_abort_releases_peers(rb):
+    """A member failing inside a call (bad argument after the group formed) must
+    not hang the others: they see RSVD_ENCCL / an exception, not a deadlock."""
+    A = torch.randn(2000, 100, dtype=torch.float64, device="cuda")
+    parts = rb.row_partition(2000, 2)
+
+    def fn(ctx, r):
+        off, rows = parts[r]
+        if r == 1:
+            # rank 1 asks for an impossible k: it fails validation before any
+            # collective, which aborts the group, so rank 0 is released
+            rb.rsvd(A[off:off + rows], 500, ctx=ctx, m_global=2000, row_offset=off)
+        return rb.rsvd(A[off:off + rows], 10, ctx=ctx, m_global=2000, row_offset=off)
+
+    with pytest.raises(Exception):
+        rb.run_ranks(fn, 2)

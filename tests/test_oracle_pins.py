@@ -14,6 +14,7 @@ import pytest
 import oracle
 from oracle.linalg import hqr, jacobi_svd_bt, soft_threshold
 from oracle.philox import omega, omega_words, philox4x32_10
+from oracle.rsvd import oracle_rpca_predict
 from oracle.rsvd import oracle_rpca, oracle_rqb, oracle_rrpca, oracle_rsvd, predict_rank, resolve_params
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -350,6 +351,48 @@ def test_rpca_eigenvalues_are_covariance_eigenvalues():
     out_s = oracle_rpca(X, 12, center=True, scale=True, p=5, q=1, seed=2)
     evs = np.sort(np.linalg.eigvalsh(np.corrcoef(X, rowvar=False)))[::-1]
     assert np.abs(out_s["eigvals"] - evs).max() < 1e-12
+
+
+@pytest.mark.parametrize("scale", [False, True])
+def test_rpca_loadings_whitening_explained_variance(scale):
+    """Full-rank case k = n (l = min(m, n): the exact SVD), checked against what
+    the paper and linear algebra fix, not against the oracle's own formulas:
+    * loadings L = W Lambda^1/2 factor the covariance (correlation) matrix,
+      C = L L^T, the squared column sums are the eigenvalues and the squared
+      row sums the variables' variances (P:1241-1252);
+    * the whitened PCs have unit variance and are uncorrelated (P:1262-1266,
+      Fig. 4b "uncorrelated and have unit variance"): cov(Z_white) = I;
+    * the proportions of variance sum to 1 over all n components, and the
+      total variance is the trace of np.cov / np.corrcoef."""
+    rng = np.random.default_rng(17)
+    X = rng.standard_normal((120, 9)) @ rng.standard_normal((9, 9)) * np.arange(1, 10) + 3.0
+    out = oracle_rpca(X, 9, center=True, scale=scale, p=0, q=1, seed=4)
+    C = np.corrcoef(X, rowvar=False) if scale else np.cov(X, rowvar=False)
+    L = out["loadings"]
+    assert np.abs(L @ L.T - C).max() < 1e-11 * np.abs(C).max()
+    assert np.abs((L * L).sum(axis=0) - out["eigvals"]).max() < 1e-11 * out["eigvals"][0]
+    assert np.abs((L * L).sum(axis=1) - np.diag(C)).max() < 1e-11 * np.abs(C).max()
+    Zw = out["x_white"]
+    assert np.abs(np.cov(Zw, rowvar=False) - np.eye(9)).max() < 1e-10
+    assert abs(out["total_var"] - np.trace(C)) < 1e-12 * np.trace(C)
+    assert abs(out["var_cum"][-1] - 1.0) < 1e-12
+    assert np.all(np.diff(out["var_cum"]) >= 0)
+    assert np.abs(out["var_ratio"] - np.linalg.eigvalsh(C)[::-1] / np.trace(C)).max() < 1e-12
+
+
+def test_rpca_predict_reproduces_training_scores():
+    """predict() on the training rows gives back the scores of Alg. 6
+    step (3), Z = U Sigma, when the range is captured exactly (k = n, so
+    Q Q^T X = X and X W = U Sigma V^T W = U Sigma, Eq. PCs); rows equal to
+    the column means map to the origin."""
+    rng = np.random.default_rng(23)
+    X = rng.standard_normal((200, 30)) @ np.diag(np.exp(-np.arange(30) / 6.0)) + 2.0
+    for scale in (False, True):
+        out = oracle_rpca(X, 30, center=True, scale=scale, p=0, q=1, seed=7)
+        P = oracle_rpca_predict(X, out["rotation"], out["center"], out["scale"])
+        assert np.abs(P - out["x"]).max() < 1e-10 * np.abs(out["x"]).max()
+        origin = oracle_rpca_predict(out["center"][None, :], out["rotation"], out["center"], out["scale"])
+        assert np.abs(origin).max() == 0.0
 
 
 # ----------------------------------------------------------------------------- rrpca

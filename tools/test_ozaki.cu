@@ -22,7 +22,7 @@ __device__ unsigned long long g_tl[1024][8];
 #include "../paper_1608_02148_b200/csrc/pass_tf32.cu"
 #include "../paper_1608_02148_b200/csrc/pass_ozaki.cu"
 namespace rsvd {
-int64_t g_kernel_launches = 0; int g_pdl = getenv("RSVD_PDL") ? atoi(getenv("RSVD_PDL")) : 1;
+std::atomic<int64_t> g_kernel_launches{0}; int g_pdl = getenv("RSVD_PDL") ? atoi(getenv("RSVD_PDL")) : 1;
 cudaError_t smem_optin_fn(const void* fn) {
   cudaFuncAttributes fa;
   cudaError_t e = cudaFuncGetAttributes(&fa, fn);
