@@ -1,15 +1,22 @@
 #!/usr/bin/env python
-"""Benchmark: randomized SVD (arXiv 1608.02148, Alg. 5) on B200.
+"""Benchmark: randomized SVD (arXiv 1608.02148, Alg. 5 / Alg. 6 / Alg. 7) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
-A step is one full rsvd (Alg. 4 + 2 + 5: Omega, 2q+2 passes over A, panel
-orthonormalisations, Jacobi SVD of B, U = Q U~) on device-resident A.  The
-default workload is BASELINE.json configs[1] (config 2): FP64 10000 x 5000,
-s_i = exp(-i/20) + N(0, 1e-6), k=50, p=10, q=2, Rademacher Omega.
-metric = A-bytes streamed per second = (2q+2) * m * n * 8 / t_rsvd (whole job,
-all ranks); ms_per_step = the rsvd wall time.  N > 1: A row-sharded over the
-ranks (strong scaling), NCCL allreduce of the n x l partials inside the library.
+A step is one call of the library's public API on one batch of the workload
+(BASELINE.json configs): config 3 (default, the largest single-GPU FP64
+workload) = rpca of the FP64 200000 x 4000 image-like matrix, column-centred,
+k=100, p=20, q=2, uniform Omega (Alg. 6: colsum, Omega, 2q+2 passes over A,
+panel orthonormalisations, Jacobi SVD of B, scores); configs 1, 2, 4 = rsvd
+(Alg. 5); config 5 = rrpca (Alg. 7, the whole IALM loop).  Inputs are
+synthetic (synthetic/__init__.py) and resident in HBM when the timed region
+starts.  metric = A-bytes streamed per second = the step's algorithmic passes
+over A (2q+2 per rsvd, +1 column-mean pass for rpca, + the fused IALM update
+for rrpca) x m x n x sizeof / time (whole job, all ranks).  N > 1: A is
+row-sharded over the ranks (strong scaling), the library's NCCL communicator
+sums the n x l partials.  Steps are enqueued back to back (the calls do not
+synchronise with the host); the timed region is bracketed by a barrier and a
+device synchronisation, and is timed with CUDA events (max over ranks).
 
 --impl reference times the CPU oracle (oracle/, numpy FP64) on the host cores
 on a bounded row sample of the same workload (rank 0 only).
@@ -17,6 +24,7 @@ on a bounded row sample of the same workload (rank 0 only).
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -31,17 +39,19 @@ import synthetic  # noqa: E402
 
 PEAKS_BOX = os.path.join(ROOT, "profiles", "peaks_box.json")
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "rsvd_A_bytes_per_s"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     return ap.parse_args()
 
 
@@ -52,6 +62,18 @@ def dist_env():
     return rank, world, local
 
 
+def relaunch_under_torchrun(n):
+    """--gpus N without a torchrun environment: start N ranks (one per GPU) on
+    this node through torch.distributed.run and exit with its status."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def peaks():
     hbm, src_hbm = 6650.0, "fallback (B200_PROFILING.md)"
     if os.path.exists(MEASURED):
@@ -60,13 +82,13 @@ def peaks():
             src_hbm = "MEASURED_PEAKS.json hbm_gbs"
         except Exception:
             pass
-    fp64, src64 = 37.1, "profiles/peaks_box.json (tools/peaks.cu DMMA)"
+    box = {}
     if os.path.exists(PEAKS_BOX):
         try:
-            fp64 = float(json.load(open(PEAKS_BOX))["dmma_m8n8k4_tflops_w8"])
+            box = json.load(open(PEAKS_BOX))
         except Exception:
-            pass
-    return hbm, src_hbm, fp64, src64
+            box = {}
+    return hbm, src_hbm, box
 
 
 class ClockSampler:
@@ -114,67 +136,86 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(loaded)}
 
 
-def make_input(cfg, device, rank, world):
-    A, meta = synthetic.make_config(cfg, device=device)
-    m = A.shape[0]
-    if world > 1:
-        rows = [(m * r) // world for r in range(world + 1)]
-        A = A[rows[rank]:rows[rank + 1]].contiguous()
-        meta["row_offset"] = rows[rank]
-    else:
-        meta["row_offset"] = 0
-    meta["m_global"] = m
-    return A, meta
+def step_bytes_for(meta, m, n, es, iters=None):
+    """Algorithmic A-bytes of one step: 2q+2 passes per rsvd,
+    +1 column-mean pass for rpca; rrpca: (iters + 1) rsvds (||A||_2 and one per
+    IALM iteration) + the fused update per iteration (reads A, S, Z; writes S,
+    Z, M: 6 m x n arrays)."""
+    passes = 2 * meta["q"] + 2
+    a_bytes = m * n * es
+    if meta.get("rrpca"):
+        it = iters or 1
+        return (it + 1) * passes * a_bytes + it * 6 * a_bytes
+    return passes * a_bytes + (a_bytes if meta["center"] else 0)
 
 
-def cpu_baseline_run(A_host, meta, budget_s=12.0, max_reps=5, rows=None):
-    """The oracle as it stands, on the host cores, on a bounded sample."""
+def oracle_step(meta, An):
+    """One step of the workload by the oracle (the same call the product arm makes)."""
     import oracle
-    An = A_host if rows is None else A_host[:rows]
-    q = meta["q"]
-    times = []
-    t_end = time.perf_counter() + budget_s
-    while len(times) < max_reps:
-        t0 = time.perf_counter()
-        oracle.oracle_rsvd(An, meta["k"], p=meta["p"], q=q, sdist=meta["sdist"], seed=meta["seed_omega"],
-                           center=meta["center"])
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() > t_end:
-            break
-    t = float(np.median(times))
-    bytes_ = (2 * q + 2) * An.shape[0] * An.shape[1] * An.itemsize
-    return t, bytes_, len(times), An.shape
+    k, p, q = meta["k"], meta["p"], meta["q"]
+    if meta.get("rrpca"):
+        o = oracle.oracle_rrpca(An, k=k, p=p, q=q, tol=meta["tol"], maxiter=100, sdist=meta["sdist"],
+                                seed=meta["seed_omega"])
+        return o["iters"]
+    if meta["center"]:
+        oracle.oracle_rpca(An, k, center=True, scale=False, p=p, q=q, sdist=meta["sdist"], seed=meta["seed_omega"])
+        return None
+    oracle.oracle_rsvd(An, k, p=p, q=q, sdist=meta["sdist"], seed=meta["seed_omega"])
+    return None
+
+
+def sample_rows(meta, A, budget_s):
+    """A row sample of the workload sized for about `budget_s` seconds of oracle
+    work: time a small sample, scale linearly in rows (the oracle is O(m n l))."""
+    m = A.shape[0]
+    l = meta["k"] + meta["p"]
+    r0 = int(min(m, max(4 * l, 2000)))
+    t0 = time.perf_counter()
+    oracle_step(meta, np.ascontiguousarray(A[:r0]))
+    t = max(time.perf_counter() - t0, 1e-3)
+    rows = int(min(m, max(r0, r0 * budget_s / t)))
+    return np.ascontiguousarray(A[:rows]) if rows < m else A
+
+
+def cpu_baseline_run(meta, A_host, budget_s):
+    """The oracle as it stands, on the host cores, on a bounded row sample."""
+    An = sample_rows(meta, A_host, budget_s)
+    t0 = time.perf_counter()
+    iters = oracle_step(meta, An)
+    t = time.perf_counter() - t0
+    b = step_bytes_for(meta, An.shape[0], An.shape[1], An.itemsize, iters)
+    sample = "one oracle %s call on the first %d of %d rows of %s (full n = %d), numpy FP64, %d host threads%s" % (
+        "rrpca" if meta.get("rrpca") else ("rpca" if meta["center"] else "rsvd"), An.shape[0], A_host.shape[0],
+        meta["name"], An.shape[1], os.cpu_count(), (", %d IALM iterations" % iters) if iters else "")
+    return {"value": round(b / t / 1e9, 4), "unit": "GB/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": sample, "ms_per_call": round(t * 1e3, 1)}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    meta = dict(synthetic.CONFIGS[args.config])
     A, meta = synthetic.make_config(args.config)
     An = A.numpy()
-    l = meta["k"] + meta["p"]
-    total = args.steps + args.warmup
-    rows = int(min(An.shape[0], max(2 * l, An.shape[0] * 10 // max(total, 1))))
-    Ans = np.ascontiguousarray(An[:rows])
-    import oracle
+    total = max(args.steps + args.warmup, 1)
+    Ans = sample_rows(meta, An, 60.0 / total)
     for _ in range(args.warmup):
-        oracle.oracle_rsvd(Ans, meta["k"], p=meta["p"], q=meta["q"], sdist=meta["sdist"],
-                           seed=meta["seed_omega"], center=meta["center"])
+        oracle_step(meta, Ans)
     t0 = time.perf_counter()
+    iters = None
     for _ in range(args.steps):
-        oracle.oracle_rsvd(Ans, meta["k"], p=meta["p"], q=meta["q"], sdist=meta["sdist"],
-                           seed=meta["seed_omega"], center=meta["center"])
+        iters = oracle_step(meta, Ans)
     dt = (time.perf_counter() - t0) / max(args.steps, 1)
-    bytes_ = (2 * meta["q"] + 2) * rows * An.shape[1] * 8
-    val = bytes_ / dt / 1e9
-    cores = os.cpu_count()
-    sample = "oracle rsvd on the first %d of %d rows of %s (full n=%d), k=%d p=%d q=%d" % (
-        rows, An.shape[0], meta["name"], An.shape[1], meta["k"], meta["p"], meta["q"])
-    line = {"impl": "reference", "metric": "rsvd_A_bytes_per_s", "value": round(val, 4), "unit": "GB/s",
+    b = step_bytes_for(meta, Ans.shape[0], An.shape[1], An.itemsize, iters)
+    val = b / dt / 1e9
+    sample = "oracle %s on the first %d of %d rows of %s (full n = %d), k=%d p=%d q=%d" % (
+        "rrpca" if meta.get("rrpca") else ("rpca" if meta["center"] else "rsvd"), Ans.shape[0], An.shape[0],
+        meta["name"], An.shape[1], meta["k"], meta["p"], meta["q"])
+    line = {"impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": meta["name"], "rows_sampled": rows},
-            "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if An.itemsize == 8 else "f32",
+            "data": "synthetic", "config": {"workload": meta["name"], "rows_sampled": int(Ans.shape[0])},
+            "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": os.cpu_count(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -186,50 +227,51 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
     import paper_1608_02148_b200 as rb
+    if world > torch.cuda.device_count():
+        raise SystemExit("bench.py: %d ranks but only %d CUDA devices" % (world, torch.cuda.device_count()))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    A, meta = make_input(args.config, dev, rank, world)
+    A_full, meta = synthetic.make_config(args.config, device=dev)
+    m, n = A_full.shape
+    offset, m_loc = rb.row_partition(m, world)[rank]
+    A = A_full[offset:offset + m_loc].contiguous() if world > 1 else A_full
+    del A_full
     torch.cuda.synchronize()
-    ctx = rb.Context(local)
+    st = torch.cuda.current_stream(dev)
+    ctx = rb.Context(local, st)
     if world > 1:
         ctx.init_comm(rank, world)
-    m, n = meta["m_global"], meta["n"]
     k, p, q = meta["k"], meta["p"], meta["q"]
     l = min(k + p, min(m, n))
     es = A.element_size()
-    m_loc = A.shape[0]
-    kw = dict(p=p, q=q, sdist=meta["sdist"], seed=meta["seed_omega"], ctx=ctx, m_global=m,
-              row_offset=meta["row_offset"])
+    center = meta["center"]
+    is_rrpca = bool(meta.get("rrpca"))
+    kw = dict(p=p, q=q, sdist=meta["sdist"], seed=meta["seed_omega"], ctx=ctx, m_global=m, row_offset=offset)
     d = torch.empty(k, dtype=A.dtype, device=dev)
     u = torch.empty(m_loc, k, dtype=A.dtype, device=dev)
     v = torch.empty(n, k, dtype=A.dtype, device=dev)
-    center = meta["center"]
-    is_rrpca = bool(meta.get("rrpca"))
     rr_state = {}
 
-    def step(Ain=A):
-        """One call of the public API on Ain; returns the result tensors (device)."""
+    def step():
+        """One call of the public API (enqueued; no host synchronisation except rrpca's loop)."""
         if is_rrpca:
-            out = rb.rrpca(Ain, k=k, p=p, q=q, tol=meta["tol"], maxiter=100, sdist=meta["sdist"],
-                           seed=meta["seed_omega"], ctx=ctx, m_global=m, row_offset=meta["row_offset"])
-            rr_state["iters"] = out["iters"]
-            rr_state["residual"] = out["residual"]
-            return [out["L"], out["S"]]
+            out = rb.rrpca(A, k=k, p=p, q=q, tol=meta["tol"], maxiter=100, sdist=meta["sdist"],
+                           seed=meta["seed_omega"], ctx=ctx, m_global=m, row_offset=offset)
+            rr_state["iters"], rr_state["residual"] = out["iters"], out["residual"]
         elif center:
-            out = rb.rpca(Ain, k, center=True, p=p, q=q, sdist=meta["sdist"], seed=meta["seed_omega"], ctx=ctx,
-                          m_global=m, row_offset=meta["row_offset"])
-            return [out["rotation"], out["eigvals"], out["x"]]
+            rb.rpca(A, k, center=True, scale=False, sync=False, **kw)
         else:
-            rb.rsvd(Ain, k, out=(d, u, v), **kw)
-            return [d, u, v]
+            rb.rsvd(A, k, out=(d, u, v), sync=False, **kw)
 
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
+    ctx.sync()
 
     def barrier():
         if world > 1:
@@ -243,7 +285,6 @@ def main():
         time.sleep(0.3)
     ctx.profile_reset()
     ctx.set_profiling(2)            # the pass kernels (dominant-kernel roofline) timed live, least overhead
-    st = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     e0.record(st)
@@ -252,6 +293,7 @@ def main():
     e1.record(st)
     barrier()
     ctx.set_profiling(False)
+    ctx.sync()                      # numerical status of every timed call
     clocks = sampler.stop() if sampler else None
     ms = e0.elapsed_time(e1) / max(args.steps, 1)
     launches = ctx.launch_count()
@@ -259,10 +301,10 @@ def main():
     # per-kind breakdown (every kernel class) from a short separate profiled run
     ctx.profile_reset()
     ctx.set_profiling(1)
-    n_diag = min(args.steps, 10)
+    n_diag = min(args.steps, 5)
     for _ in range(n_diag):
         step()
-    torch.cuda.synchronize(dev)
+    ctx.sync()
     ctx.set_profiling(False)
     prof_all = {kind: ctx.profile(kind) for kind in range(7)}
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -272,17 +314,11 @@ def main():
     ms = float(t.item())
     passes = 2 * q + 2
     a_bytes = m * n * es
-    if is_rrpca:
-        # per IALM iteration: one rsvd (2q+2 passes over M) + the fused update
-        # (reads A, S, Z; writes S, Z, M = 6 m x n arrays); plus the ||A||_2 rsvd
-        it = rr_state.get("iters", 1)
-        step_bytes = (it + 1) * passes * a_bytes + it * 6 * a_bytes
-    else:
-        step_bytes = passes * a_bytes + (a_bytes if center else 0)     # + the column-mean pass
+    step_bytes = step_bytes_for(meta, m, n, es, rr_state.get("iters"))
     value = step_bytes / (ms * 1e-3) / 1e9
 
-    # roofline of the dominant kernel (the streaming passes; kinds 0 = A.X, 1 = A^T.X)
-    hbm_peak, hbm_src, fp64_peak, fp64_src = peaks()
+    # roofline of the dominant kernel: the streaming pass (kinds 0 = A.X, 1 = A^T.X)
+    hbm_peak, hbm_src, box = peaks()
     diag = ctx.stats()
     if es == 8 and diag.get("ozaki_passes", 0) > 0:
         path = "ozaki"
@@ -290,40 +326,50 @@ def main():
                  1: "pass_AtX (ozaki_pass_kernel TN: int8 slices on tcgen05)"}
     elif es == 4:
         path = "tf32"
-        kinds = {0: "pass_AX (pass_tf32_kernel NN: 3xTF32 on tcgen05)", 1: "pass_AtX (pass_tf32_kernel TN: 3xTF32 on tcgen05)"}
+        kinds = {0: "pass_AX (pass_tf32_tn_kernel as X^T A^T: 3xTF32 on tcgen05)",
+                 1: "pass_AtX (pass_tf32_tn_kernel as Q^T A: 3xTF32 on tcgen05)"}
     else:
         path = "dmma"
         kinds = {0: "pass_AX (gemm_pass_kernel NN, FP64 DMMA)", 1: "pass_AtX (gemm_pass_kernel TN, FP64 DMMA)"}
     dom = max((0, 1), key=lambda kk: prof[kk][0])
-    tot_ms, cnt, by = prof[dom]
+    tot_ms, cnt, _ = prof[dom]
     avg_ms = tot_ms / max(cnt, 1)
+    # algorithmic bytes of one pass: A once + the n x l and m_loc x l panels
+    bytes_launch = (m_loc * n + n * l + m_loc * l) * es
     flops_launch = 2.0 * m_loc * n * l
-    bytes_launch = m_loc * n * es          # algorithmic: A read once per pass (FP64 / FP32 bytes)
-    tf = flops_launch / (avg_ms * 1e-3) / 1e12
     gbs = bytes_launch / (avg_ms * 1e-3) / 1e9
+    tf = flops_launch / (avg_ms * 1e-3) / 1e12
     tot_all = max(sum(prof_all[kk][0] for kk in range(7)), 1e-12)
     share = {"A.X": prof_all[0][0] / tot_all, "At.X": prof_all[1][0] / tot_all}
     per_kind = {name: round(prof_all[kk][0] / max(n_diag, 1), 4) for kk, name in
                 enumerate(["pass_AX", "pass_AtX", "panel_orth", "jacobi_svd", "omega", "ozaki_slice_A",
                            "ozaki_slice_X"])}
     if path == "dmma":
-        roof = {"bound": "tensor", "kernel": kinds[dom], "achieved": round(tf, 3), "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": round(tf / fp64_peak, 4), "traffic": None,
-                "peak_source": fp64_src + " (FP64 DMMA; tcgen05 has no f64 kind)",
-                "hbm": {"achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-                        "frac": round(gbs / hbm_peak, 4), "peak_source": hbm_src}}
+        fp64 = float(box.get("dmma_m8n8k4_tflops_w8", 37.1))
+        roof = {"bound": "tensor", "kernel": kinds[dom], "achieved": round(tf, 3), "peak": fp64,
+                "unit": "TFLOP/s", "frac": round(tf / fp64, 4), "traffic": None,
+                "peak_source": "profiles/peaks_box.json dmma_m8n8k4_tflops_w8 (FP64 DMMA)"}
     else:
-        # tensor-core passes: the target roof is HBM (A read once per pass); the
-        # FP64-equivalent flop rate is reported alongside
         roof = {"bound": "hbm", "kernel": kinds[dom], "achieved": round(gbs, 1), "peak": hbm_peak,
-                "unit": "GB/s", "frac": round(gbs / hbm_peak, 4), "traffic": None, "peak_source": hbm_src,
-                "fp64_equivalent": {"achieved_tflops": round(tf, 3), "dmma_peak_tflops": fp64_peak,
-                                    "frac_of_dmma_peak": round(tf / fp64_peak, 4)}}
-    roof.update({"path": path, "algorithmic_per_launch": {"flops": flops_launch, "bytes": bytes_launch},
-                 "avg_launch_ms": round(avg_ms, 5), "step_share": {kk: round(vv, 4) for kk, vv in share.items()},
+                "unit": "GB/s", "frac": round(gbs / hbm_peak, 4), "traffic": None, "peak_source": hbm_src}
+        if path == "ozaki" and box.get("tcgen05_i8_tops"):
+            # the binding alternative: 28 int8 slice products per FP64 product on the tensor pipe
+            i8 = 28.0 * flops_launch / (avg_ms * 1e-3) / 1e12
+            roof["tensor_i8"] = {"achieved_tops": round(i8, 1), "peak_tops": box["tcgen05_i8_tops"],
+                                 "frac": round(i8 / box["tcgen05_i8_tops"], 4),
+                                 "peak_source": "profiles/peaks_box.json tcgen05_i8_tops (tools/peaks_tc.cu)"}
+        if path == "tf32" and box.get("tcgen05_tf32_tflops"):
+            t3 = 3.0 * flops_launch / (avg_ms * 1e-3) / 1e12
+            roof["tensor_tf32"] = {"achieved_tflops": round(t3, 1), "peak_tflops": box["tcgen05_tf32_tflops"],
+                                   "frac": round(t3 / box["tcgen05_tf32_tflops"], 4),
+                                   "peak_source": "profiles/peaks_box.json tcgen05_tf32_tflops (tools/peaks_tc.cu)"}
+    roof.update({"path": path, "algorithmic_per_launch": {"bytes": bytes_launch, "flops": flops_launch,
+                                                          "recipe": "sizeof * (m_loc n + n l + m_loc l)"},
+                 "avg_launch_ms": round(avg_ms, 5), "launches_timed": int(cnt),
+                 "step_share": {kk: round(vv, 4) for kk, vv in share.items()},
                  "per_kind_ms_per_step": per_kind})
     traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic_cfg%d_%s.json" % (args.config, path))
-    if os.path.exists(traffic_file):
+    if os.path.exists(traffic_file) and world == 1:
         try:
             tr = json.load(open(traffic_file))
             roof["traffic"] = tr.get("AX" if dom == 0 else "AtX")
@@ -331,61 +377,56 @@ def main():
         except Exception:
             pass
 
-    line = {"metric": "rsvd_A_bytes_per_s", "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+    line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64" if es == 8 else "f32",
-            "data": "synthetic",
-            "config": {"workload": meta["name"], "m": m, "n": n, "k": k, "p": p, "q": q, "l": l,
-                       "sdist": meta["sdist"], "center": bool(center), "passes_per_step": passes,
+            "data": "synthetic (seeded, synthetic/__init__.py)",
+            "config": {"workload": meta["name"], "call": "rrpca" if is_rrpca else ("rpca" if center else "rsvd"),
+                       "m": m, "n": n, "k": k, "p": p, "q": q, "l": l,
+                       "sdist": meta["sdist"], "center": bool(center), "passes_per_rsvd": passes,
                        "A_bytes": a_bytes, "bytes_per_step": step_bytes,
                        "rrpca_iters": rr_state.get("iters"), "rrpca_residual": rr_state.get("residual"),
-                       "l2_policy": "A (%d MB) > L2 (126 MB): no flush" % (a_bytes >> 20)
-                       if a_bytes > 126e6 else "A L2-resident (latency-bound config)",
-                       "parallelism": "row-sharded dp%d" % world},
-            "roofline": roof, "gpu_launches": int(launches), "clocks": clocks,
-            "diagnostics": diag}
+                       "l2_policy": ("A (%d MB) > L2 (126 MB): no flush" % (a_bytes >> 20)) if a_bytes > 126e6
+                       else "A L2-resident (latency-bound config)",
+                       "parallelism": "row-sharded dp%d" % world, "rows_per_rank": m_loc},
+            "roofline": roof, "gpu_launches": int(launches), "clocks": clocks, "diagnostics": diag}
 
-    # end-to-end: host A (pinned) -> device, rsvd, d/u/v -> host, through the same API
-    # (rsvd: d, u, v; rpca: rotation, eigenvalues, scores; rrpca: L and S)
+    # end to end through the host-buffer C-ABI calls (rsvd_run_host / rsvd_rpca_host /
+    # rsvd_rrpca_host): A copied in from pinned host memory, results copied out, per step
     if not args.no_e2e and world == 1:
         A_host = A.cpu().pin_memory()
-        stage = torch.empty_like(A)
-        res_h = []
-        e2e_steps = max(3, min(args.steps, 20))
+        e2e_steps = max(2, min(args.steps, 10 if not is_rrpca else 2))
+        d2h = {}
 
         def e2e_step():
-            stage.copy_(A_host, non_blocking=True)
-            res = step(stage)
-            if not res_h:
-                res_h.extend(torch.empty(r.shape, dtype=r.dtype).pin_memory() for r in res)
-            for h, r in zip(res_h, res):
-                h.copy_(r, non_blocking=True)
-            return res
+            if is_rrpca:
+                out = rb.rrpca(A_host, k=k, p=p, q=q, tol=meta["tol"], maxiter=100, sdist=meta["sdist"],
+                               seed=meta["seed_omega"], ctx=ctx)
+                res = [out["L"], out["S"]]
+            elif center:
+                out = rb.rpca(A_host, k, center=True, scale=False, p=p, q=q, sdist=meta["sdist"],
+                              seed=meta["seed_omega"], ctx=ctx)
+                res = [out["rotation"], out["eigvals"], out["sdev"], out["x"], out["center"]]
+            else:
+                r = rb.rsvd_host(A_host, k, p=p, q=q, sdist=meta["sdist"], seed=meta["seed_omega"], ctx=ctx)
+                res = [r.d, r.u, r.v]
+            d2h["bytes"] = int(sum(t.numel() * t.element_size() for t in res))
 
-        for _ in range(2):
-            e2e_step()
+        e2e_step()
         torch.cuda.synchronize()
-        e0.record(st)
+        t0 = time.perf_counter()
         for _ in range(e2e_steps):
             e2e_step()
-        e1.record(st)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / e2e_steps
+        ems = (time.perf_counter() - t0) * 1e3 / e2e_steps
         line["e2e"] = {"value": round(step_bytes / (ems * 1e-3) / 1e9, 2), "unit": "GB/s",
                        "ms_per_step": round(ems, 3), "steps": e2e_steps,
-                       "h2d_bytes_per_step": int(a_bytes),
-                       "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in res_h)),
-                       "results": "rrpca L, S" if is_rrpca else ("rpca rotation, eigvals, x" if center
-                                                                else "rsvd d, u, v")}
+                       "h2d_bytes_per_step": int(a_bytes), "d2h_bytes_per_step": d2h["bytes"],
+                       "call": "rsvd_rrpca_host" if is_rrpca else ("rsvd_rpca_host" if center else "rsvd_run_host"),
+                       "timing": "host wall clock around blocking calls (each returns after its D2H copy)"}
 
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not is_rrpca and m * n <= 2e8:
-        t_cpu, b_cpu, reps, shape = cpu_baseline_run(A.cpu().numpy(), meta)
-        line["cpu_baseline"] = {"value": round(b_cpu / t_cpu / 1e9, 4), "unit": "GB/s",
-                                "cores": os.cpu_count(), "kind": "oracle",
-                                "sample": "median of %d full oracle rsvd calls on %s (%dx%d), numpy FP64, "
-                                          "%d host threads" % (reps, meta["name"], shape[0], shape[1],
-                                                               os.cpu_count()),
-                                "ms_per_rsvd": round(t_cpu * 1e3, 1)}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_run(meta, A.cpu().numpy(), args.cpu_budget)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -224,6 +224,12 @@ typedef struct {
 void rsvd_rpca_params_default(rsvd_params* prm, int32_t k);   /* rsvd defaults + center = scale = 1 */
 rsvd_status rsvd_rpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, const rsvd_pca_out* out);
 
+/* rsvd_rpca on HOST buffers (end to end, single GPU): A and every non-NULL
+ * output of `out` are HOST memory (layouts as rsvd_rpca); A is staged into a
+ * device buffer the context owns and the outputs are copied back.  Blocks;
+ * returns the numerical status of the call (as rsvd_sync). */
+rsvd_status rsvd_rpca_host(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, const rsvd_pca_out* out);
+
 /* Out-of-sample projection, predict() of the rpca object: the
  * scores of new rows, out = ((Anew - 1 c^T) diag(1/s)) W, computed by the same
  * pass kernels as the sketch.  Anew: rsvd_matrix (DEVICE, m_new x n, dtype of
@@ -267,6 +273,12 @@ void rsvd_rrpca_params_default(rsvd_rrpca_params* prm);
 rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_rrpca_params* prm,
                        void* L, void* S, int64_t ld, int32_t* iters, double* final_residual,
                        double* trace);
+
+/* rsvd_rrpca on HOST buffers (end to end, single GPU): A, L, S HOST memory
+ * (m x n, ld == n); staged through device buffers the context owns. */
+rsvd_status rsvd_rrpca_host(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_rrpca_params* prm,
+                            void* L, void* S, int64_t ld, int32_t* iters, double* final_residual,
+                            double* trace);
 
 /* Random test matrix alone (K1): writes the n x l matrix
  * Omega to DEVICE `out` (row-major, ldo >= l) in `dtype` (FP32 = round to

@@ -35,8 +35,8 @@ STATUS = {0: "RSVD_OK", 1: "RSVD_EINVAL", 2: "RSVD_ENOMEM", 3: "RSVD_ECUDA", 4: 
 EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_last_error", "rsvd_version", "rsvd_sync", "rsvd_nccl_unique_id",
            "rsvd_comm_init", "rsvd_group_create", "rsvd_group_destroy", "rsvd_comm_init_group",
            "rsvd_params_default", "rsvd_workspace_bytes", "rsvd_run", "rsvd_run_host", "rsvd_rqb",
-           "rsvd_rpca_params_default", "rsvd_rpca", "rsvd_rpca_predict",
-           "rsvd_rrpca_params_default", "rsvd_rrpca", "rsvd_omega", "rsvd_set_profiling", "rsvd_profile",
+           "rsvd_rpca_params_default", "rsvd_rpca", "rsvd_rpca_host", "rsvd_rpca_predict",
+           "rsvd_rrpca_params_default", "rsvd_rrpca", "rsvd_rrpca_host", "rsvd_omega", "rsvd_set_profiling", "rsvd_profile",
            "rsvd_profile_reset", "rsvd_launch_count", "rsvd_stats", "rsvd_rid", "rsvd_rcur"]
 
 
@@ -106,12 +106,15 @@ def lib():
         "rsvd_run_host": ([vp, MP, PP, vp, i64, vp, vp, i64], ctypes.c_int),
         "rsvd_rqb": ([vp, MP, PP, vp, i64, vp, i64], ctypes.c_int),
         "rsvd_rpca": ([vp, MP, PP, ctypes.POINTER(PcaOut)], ctypes.c_int),
+        "rsvd_rpca_host": ([vp, MP, PP, ctypes.POINTER(PcaOut)], ctypes.c_int),
         "rsvd_rpca_predict": ([vp, MP, i32, vp, i64, vp, vp, vp, i64], ctypes.c_int),
         "rsvd_rrpca_params_default": ([ctypes.POINTER(RrpcaParams)], None),
         "rsvd_rid": ([vp, MP, PP, vp, i64, vp, i64, vp], i32),
         "rsvd_rcur": ([vp, MP, PP, vp, i64, vp, i64, vp, i64, vp, vp], i32),
         "rsvd_rrpca": ([vp, MP, ctypes.POINTER(RrpcaParams), vp, vp, i64, ctypes.POINTER(i32),
                         ctypes.POINTER(dp), ctypes.POINTER(dp)], ctypes.c_int),
+        "rsvd_rrpca_host": ([vp, MP, ctypes.POINTER(RrpcaParams), vp, vp, i64, ctypes.POINTER(i32),
+                             ctypes.POINTER(dp), ctypes.POINTER(dp)], ctypes.c_int),
         "rsvd_omega": ([vp, i64, i64, i32, u64, u64, i32, vp, i64], ctypes.c_int),
         "rsvd_set_profiling": ([vp, ctypes.c_int], ctypes.c_int),
         "rsvd_profile": ([vp, ctypes.c_int, ctypes.POINTER(dp), ctypes.POINTER(i64), ctypes.POINTER(dp)],
@@ -433,6 +436,27 @@ def rcur(A, k, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None, sync=True)
     return dict(C=C, U=U, R=R, J=J, I=I)
 
 
+def _pca_outputs(m, n, k, dt, dev, retx, center, scale, loadings, whiten, explained, pin=False):
+    mk = lambda *shape: torch.empty(*shape, dtype=dt, device=dev, pin_memory=pin)  # noqa: E731
+    res = dict(rotation=mk(n, k), eigvals=mk(k), sdev=mk(k), x=mk(m, k) if retx else None,
+               center=mk(n) if center else None, scale=mk(n) if scale else None)
+    if loadings:
+        res["loadings"] = mk(n, k)
+    if whiten:
+        res["x_white"] = mk(m, k)
+    if explained:
+        res["var_ratio"], res["var_cum"], res["total_var"] = mk(k), mk(k), mk(1)
+    o = PcaOut()
+    o.rotation, o.ldr = _ptr(res["rotation"]), k
+    o.eigvals, o.sdev = _ptr(res["eigvals"]), _ptr(res["sdev"])
+    o.x, o.ldx = _ptr(res["x"]), k
+    o.center, o.scale = _ptr(res["center"]), _ptr(res["scale"])
+    o.loadings, o.ldl = _ptr(res.get("loadings")), k
+    o.x_white, o.ldw = _ptr(res.get("x_white")), k
+    o.var_ratio, o.var_cum, o.total_var = _ptr(res.get("var_ratio")), _ptr(res.get("var_cum")), _ptr(res.get("total_var"))
+    return res, o
+
+
 def rpca(A, k, center=True, scale=True, retx=True, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None,
          m_global=None, row_offset=0, loadings=False, whiten=False, explained=False, sync=True):
     """Randomized PCA (Alg. 6; interface
@@ -441,35 +465,32 @@ def rpca(A, k, center=True, scale=True, retx=True, p=10, q=2, sdist="normal", se
     Returns dict(rotation, eigvals, sdev, x (retx), center, scale) and, on
     request, loadings = W Lambda^1/2, x_white = the whitened PCs
     (P:1262-1266), var_ratio / var_cum / total_var = the explained variance of
-    summary().  Every value is computed by the library."""
+    summary().  Every value is computed by the library.
+    A CPU tensor runs end to end through rsvd_rpca_host (outputs on the CPU)."""
+    if not A.is_cuda:
+        return _rpca_host(A, k, center, scale, retx, p, q, sdist, seed, stream, ctx, loadings, whiten, explained)
     ctx = ctx or default_context(A.device)
     mat = _matrix(A, m_global, row_offset)
     m, n = A.shape
-    kk = int(k)
-    dev, dt = A.device, A.dtype
-    res = dict(rotation=torch.empty(n, kk, dtype=dt, device=dev), eigvals=torch.empty(kk, dtype=dt, device=dev),
-               sdev=torch.empty(kk, dtype=dt, device=dev),
-               x=torch.empty(m, kk, dtype=dt, device=dev) if retx else None,
-               center=torch.empty(n, dtype=dt, device=dev) if center else None,
-               scale=torch.empty(n, dtype=dt, device=dev) if scale else None)
-    if loadings:
-        res["loadings"] = torch.empty(n, kk, dtype=dt, device=dev)
-    if whiten:
-        res["x_white"] = torch.empty(m, kk, dtype=dt, device=dev)
-    if explained:
-        res["var_ratio"] = torch.empty(kk, dtype=dt, device=dev)
-        res["var_cum"] = torch.empty(kk, dtype=dt, device=dev)
-        res["total_var"] = torch.empty(1, dtype=dt, device=dev)
-    o = PcaOut()
-    o.rotation, o.ldr = _ptr(res["rotation"]), kk
-    o.eigvals, o.sdev = _ptr(res["eigvals"]), _ptr(res["sdev"])
-    o.x, o.ldx = _ptr(res["x"]), kk
-    o.center, o.scale = _ptr(res["center"]), _ptr(res["scale"])
-    o.loadings, o.ldl = _ptr(res.get("loadings")), kk
-    o.x_white, o.ldw = _ptr(res.get("x_white")), kk
-    o.var_ratio, o.var_cum, o.total_var = _ptr(res.get("var_ratio")), _ptr(res.get("var_cum")), _ptr(res.get("total_var"))
+    res, o = _pca_outputs(m, n, int(k), A.dtype, A.device, retx, center, scale, loadings, whiten, explained)
     prm = _params(k, k, k, p, q, sdist, seed, stream, center, scale)
     ctx.finish(lib().rsvd_rpca(ctx.h, ctypes.byref(mat), ctypes.byref(prm), ctypes.byref(o)), sync)
+    if explained:
+        res["total_var"] = res["total_var"][0]
+    return res
+
+
+def _rpca_host(A, k, center, scale, retx, p, q, sdist, seed, stream, ctx, loadings, whiten, explained):
+    ctx = ctx or default_context()
+    if A.dim() != 2 or A.stride(1) != 1:
+        raise ValueError("A must be a 2-D row-major tensor")
+    m, n = A.shape
+    dt = 0 if A.dtype == torch.float64 else 1
+    mat = Matrix(dt, A.data_ptr(), m, n, A.stride(0), m, 0)
+    res, o = _pca_outputs(m, n, int(k), A.dtype, "cpu", retx, center, scale, loadings, whiten, explained,
+                          pin=torch.cuda.is_available())
+    prm = _params(k, k, k, p, q, sdist, seed, stream, center, scale)
+    ctx.check(lib().rsvd_rpca_host(ctx.h, ctypes.byref(mat), ctypes.byref(prm), ctypes.byref(o)))
     if explained:
         res["total_var"] = res["total_var"][0]
     return res
@@ -497,8 +518,15 @@ def rrpca(A, lam=None, maxiter=50, tol=1e-5, p=10, q=2, k=20, sdist="normal", se
     Alg. 7 steps (1) and (7) (k = 2, then predict_rank; R30).
     rand=False: the deterministic truncated SVD in step (6).
     trace: per iteration (residual, l, mu, k)."""
-    ctx = ctx or default_context(A.device)
-    mat = _matrix(A, m_global, row_offset)
+    host = not A.is_cuda
+    ctx = ctx or default_context(None if host else A.device)
+    if host:
+        if A.dim() != 2 or not A.is_contiguous():
+            raise ValueError("A must be a contiguous 2-D tensor")
+        mat = Matrix(0 if A.dtype == torch.float64 else 1, A.data_ptr(), A.shape[0], A.shape[1], A.shape[1],
+                     A.shape[0], 0)
+    else:
+        mat = _matrix(A, m_global, row_offset)
     prm = RrpcaParams()
     lib().rsvd_rrpca_params_default(ctypes.byref(prm))
     prm.lam = 0.0 if lam is None else float(lam)
@@ -506,13 +534,15 @@ def rrpca(A, lam=None, maxiter=50, tol=1e-5, p=10, q=2, k=20, sdist="normal", se
     prm.sdist = SDIST[sdist] if isinstance(sdist, str) else int(sdist)
     prm.seed = int(seed)
     prm.rand = 1 if rand else 0
-    L = torch.empty_like(A)
-    S = torch.empty_like(A)
+    pin = host and torch.cuda.is_available()
+    L = torch.empty(A.shape, dtype=A.dtype, device=A.device, pin_memory=pin)
+    S = torch.empty(A.shape, dtype=A.dtype, device=A.device, pin_memory=pin)
     it = ctypes.c_int32()
     res = ctypes.c_double()
     tr = (ctypes.c_double * (4 * int(maxiter)))()
-    ctx.check(lib().rsvd_rrpca(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(L), _ptr(S), A.shape[1],
-                               ctypes.byref(it), ctypes.byref(res), tr))
+    fn = lib().rsvd_rrpca_host if host else lib().rsvd_rrpca
+    ctx.check(fn(ctx.h, ctypes.byref(mat), ctypes.byref(prm), _ptr(L), _ptr(S), A.shape[1],
+                 ctypes.byref(it), ctypes.byref(res), tr))
     hist = [(tr[4 * i], int(tr[4 * i + 1]), tr[4 * i + 2], int(tr[4 * i + 3])) for i in range(it.value)]
     out = dict(L=L, S=S, iters=it.value, residual=res.value)
     if trace:

@@ -1201,6 +1201,49 @@ rsvd_status rsvd_rpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* pr
   return run_call(ctx, p, &prm, true, emit, want_total && !p.scaled);
 }
 
+rsvd_status rsvd_rpca_host(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, const rsvd_pca_out* o) {
+  int64_t mg, n;
+  CKS(validate(ctx, A, prm, &mg, &n));
+  if (!o) return fail(ctx, RSVD_EINVAL, "null output descriptor");
+  if (ctx->nranks > 1) return fail(ctx, RSVD_EUNSUPPORTED, "rsvd_rpca_host is single-GPU");
+  CK(cudaSetDevice(ctx->device));
+  const size_t es = A->dtype == RSVD_F32 ? 4 : 8;
+  const int64_t m = A->m_local, k = prm->k;
+  // device staging: A, then every requested output (dense, ld = its column count)
+  struct Out { void* host; int64_t ldh, rows, cols; size_t off; } outs[12];
+  int no = 0;
+  size_t off = align256((size_t)m * n * es);
+  auto add = [&](void* h, int64_t ldh, int64_t rows, int64_t cols) {
+    if (!h) return;
+    outs[no++] = {h, ldh, rows, cols, off};
+    off += align256((size_t)rows * cols * es);
+  };
+  add(o->rotation, o->ldr, n, k); add(o->eigvals, 1, k, 1); add(o->sdev, 1, k, 1); add(o->x, o->ldx, m, k);
+  add(o->center, 1, n, 1); add(o->scale, 1, n, 1); add(o->loadings, o->ldl, n, k); add(o->x_white, o->ldw, m, k);
+  add(o->var_ratio, 1, k, 1); add(o->var_cum, 1, k, 1); add(o->total_var, 1, 1, 1);
+  CKS(ensure_buf(ctx, &ctx->ws5, &ctx->ws5_bytes, off, "host-call staging"));
+  char* dA = ctx->ws5;
+  CK(cudaMemcpy2DAsync(dA, n * es, A->A, A->lda * es, n * es, m, cudaMemcpyHostToDevice, ctx->stream));
+  rsvd_matrix Ad = *A;
+  Ad.A = dA; Ad.lda = n; Ad.m_global = m; Ad.row_offset = 0;
+  rsvd_pca_out od = *o;
+  auto dptr = [&](void* h) -> void* {
+    for (int i = 0; i < no; ++i) if (outs[i].host == h) return ctx->ws5 + outs[i].off;
+    return nullptr;
+  };
+  od.rotation = dptr(o->rotation); od.ldr = k; od.eigvals = dptr(o->eigvals); od.sdev = dptr(o->sdev);
+  od.x = dptr(o->x); od.ldx = k; od.center = dptr(o->center); od.scale = dptr(o->scale);
+  od.loadings = dptr(o->loadings); od.ldl = k; od.x_white = dptr(o->x_white); od.ldw = k;
+  od.var_ratio = dptr(o->var_ratio); od.var_cum = dptr(o->var_cum); od.total_var = dptr(o->total_var);
+  CKS(rsvd_rpca(ctx, &Ad, prm, &od));
+  for (int i = 0; i < no; ++i) {
+    const Out& q = outs[i];
+    CK(cudaMemcpy2DAsync(q.host, q.ldh * es, ctx->ws5 + q.off, q.cols * es, q.cols * es, q.rows,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  return sync_status(ctx);
+}
+
 rsvd_status rsvd_rpca_predict(rsvd_ctx* ctx, const rsvd_matrix* Anew, int32_t k, const void* rotation, int64_t ldr,
                               const void* center, const void* scale, void* out, int64_t ldo) {
   if (!ctx) return RSVD_EINVAL;
@@ -1309,6 +1352,29 @@ rsvd_status rsvd_device(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* 
 }
 
 }  // namespace
+
+extern "C" rsvd_status rsvd_rrpca_host(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_rrpca_params* prm, void* L,
+                                       void* S, int64_t ld, int32_t* iters_out, double* res_out, double* trace) {
+  if (!ctx) return RSVD_EINVAL;
+  if (!A || !A->A || !prm || !L || !S) return fail(ctx, RSVD_EINVAL, "null argument");
+  if (A->dtype != RSVD_F64) return fail(ctx, RSVD_EUNSUPPORTED, "rrpca is FP64 only");
+  if (ctx->nranks > 1) return fail(ctx, RSVD_EUNSUPPORTED, "rsvd_rrpca_host is single-GPU");
+  if (A->m_local < 1 || A->n < 1 || A->lda != A->n || ld != A->n)
+    return fail(ctx, RSVD_EUNSUPPORTED, "rrpca needs contiguous A, L, S (lda == ld == n)");
+  CK(cudaSetDevice(ctx->device));
+  const size_t bytes = (size_t)A->m_local * A->n * 8, b = align256(bytes);
+  CKS(ensure_buf(ctx, &ctx->ws5, &ctx->ws5_bytes, 3 * b, "host-call staging"));
+  char* dA = ctx->ws5;
+  char* dL = dA + b;
+  char* dS = dL + b;
+  CK(cudaMemcpyAsync(dA, A->A, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  rsvd_matrix Ad = *A;
+  Ad.A = dA; Ad.m_global = A->m_local; Ad.row_offset = 0;
+  CKS(rsvd_rrpca(ctx, &Ad, prm, dL, dS, ld, iters_out, res_out, trace));
+  CK(cudaMemcpyAsync(L, dL, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(S, dS, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return sync_status(ctx);
+}
 
 extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_rrpca_params* prm, void* Lout,
                                   void* Sout, int64_t ld, int32_t* iters_out, double* res_out, double* trace) {

@@ -1,8 +1,9 @@
 """The bench.py JSON line the driver consumes: keys, types and units.
 
 CPU: the reference arm (`--impl reference`, the oracle on host cores) on the
-small config.  GPU: the product arm on the bench default (config 2) with a
-short run -- roofline, e2e, launch count and clocks present and consistent.
+small config.  GPU: the product arm on the bench default (config 3, rpca) with
+a short run -- roofline, e2e through the host-buffer C-ABI call, launch count,
+clocks and the cpu_baseline present and consistent.
 """
 import json
 import os
@@ -42,7 +43,7 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_product_arm_line():
-    d = _run(["--steps", "3", "--warmup", "3", "--no-cpu-baseline"], timeout=900)
+    d = _run(["--steps", "3", "--warmup", "3", "--cpu-budget", "3"], timeout=900)
     assert BASE_KEYS <= set(d)
     assert d["metric"] == "rsvd_A_bytes_per_s" and d["dtype"] == "f64" and d["n_gpus"] == 1
     # value = bytes of A streamed per step / time
@@ -56,3 +57,24 @@ def test_product_arm_line():
     assert e["h2d_bytes_per_step"] == d["config"]["A_bytes"] and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert d["clocks"] is not None and d["clocks"]["sm_mhz"] > 0
+    assert d["config"]["workload"].startswith("cfg3") and d["config"]["call"] == "rpca"
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+    # the roofline counts the algorithmic bytes of one pass: A + the two panels
+    c = d["config"]
+    assert r["algorithmic_per_launch"]["bytes"] == 8 * (c["m"] * c["n"] + c["n"] * c["l"] + c["m"] * c["l"])
+
+
+def test_gpus_flag_relaunches_under_torchrun(monkeypatch):
+    """--gpus N without a torchrun environment re-executes bench.py under
+    torch.distributed.run with N processes (the command is checked, not run)."""
+    import bench
+    seen = {}
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2"])
+    with pytest.raises(SystemExit):
+        bench.relaunch_under_torchrun(4)
+    cmd = seen["cmd"]
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert cmd[cmd.index("--nproc-per-node") + 1] == "4" and "127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "2"]
