@@ -37,14 +37,31 @@ def _flags():
                 "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nr, "include")] + ARCH
 
 
+HASH_FILE = os.path.join(OUT_DIR, "build.sha256")
+
+
+def _content_hash(deps, flags):
+    """sha256 over every source / header, this script and the compiler flags:
+    the library is rebuilt whenever its inputs change (not by mtime, which a
+    copied tree -- e.g. the GPU box's snapshot -- does not preserve)."""
+    import hashlib
+    h = hashlib.sha256()
+    for d in sorted(deps):
+        h.update(os.path.relpath(d, ROOT).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(flags).encode())
+    return h.hexdigest()
+
+
 def build(force=False, verbose=False):
     nr, flags = _flags()
     os.makedirs(os.path.join(OUT_DIR, "obj"), exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     deps = srcs + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         [os.path.join(ROOT, "include", "rsvd_b200.h"), __file__]
-    newest = max(os.path.getmtime(d) for d in deps)
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
+    digest = _content_hash(deps, flags)
+    if not force and os.path.exists(LIB) and os.path.exists(HASH_FILE) and open(HASH_FILE).read().strip() == digest:
         return LIB
 
     def compile_one(src):
@@ -63,10 +80,13 @@ def build(force=False, verbose=False):
     objs = [o for o, _ in results]
     libdir = os.path.join(nr, "lib")
     cmd = [NVCC, "-shared", "-o", LIB] + objs + ARCH + [
-        "-L" + libdir, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + libdir, "-lcudart"]
+        "-L" + libdir, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + libdir, "-lcudart", "-lcuda",
+        "-Xlinker", "--no-undefined"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stderr[-4000:])
+    with open(HASH_FILE, "w") as f:
+        f.write(digest + "\n")
     return LIB
 
 

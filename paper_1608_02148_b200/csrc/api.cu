@@ -180,6 +180,12 @@ struct NcclComm : Comm {
   int nranks() const override { return n; }
   int rank() const override { return r; }
   rsvd_status allreduce(rsvd_ctx* ctx, double* buf, size_t cnt, bool op_max) override {
+    const rsvd_status s = allreduce_(ctx, buf, cnt, op_max);
+    if (s != RSVD_OK) return s;
+    CK(launch_stream_fence(ctx->stream));
+    return RSVD_OK;
+  }
+  rsvd_status allreduce_(rsvd_ctx* ctx, double* buf, size_t cnt, bool op_max) {
     ncclResult_t e = ncclAllReduce(buf, buf, cnt, ncclDouble, op_max ? ncclMax : ncclSum, c, ctx->stream);
     ncclResult_t async = ncclSuccess;
     if (e == ncclSuccess && ncclCommGetAsyncError(c, &async) == ncclSuccess && async != ncclSuccess &&
@@ -191,6 +197,7 @@ struct NcclComm : Comm {
   rsvd_status allgather(rsvd_ctx* ctx, const double* send, double* recv, size_t cnt) override {
     const ncclResult_t e = ncclAllGather(send, recv, cnt, ncclDouble, c, ctx->stream);
     if (e != ncclSuccess) return fail(ctx, RSVD_ENCCL, "ncclAllGather: %s", ncclGetErrorString(e));
+    CK(launch_stream_fence(ctx->stream));
     return RSVD_OK;
   }
 };
@@ -255,6 +262,7 @@ struct GroupComm : Comm {
                                             cudaMemcpyDeviceToDevice, ctx->stream);
       if (e != cudaSuccess) { g->abort(); return fail(ctx, RSVD_ECUDA, "group allgather: %s", cudaGetErrorString(e)); }
     }
+    CK(launch_stream_fence(ctx->stream));
     return finish(ctx);
   }
 };
@@ -673,7 +681,7 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool want_
   ctx->prof_phase ^= 1;           // level-2 profiling samples A.X and A^T.X passes on alternate calls
   const bool dist = ctx->nranks > 1;
   const bool centred = prm->center != 0 || prm->scale != 0;
-  CK(cudaMemsetAsync(ctx->flags_dev, 0, sizeof(int) * 16, ctx->stream));
+  CK(launch_zero_words(ctx->flags_dev, 16, ctx->stream));
   p.scaled = prm->scale != 0;
   if (centred || p.scaled || want_ss) CKS(column_stats(ctx, p, prm->center != 0, want_ss));
   if (p.use_ozaki) {
@@ -1146,7 +1154,7 @@ rsvd_status rsvd_rcur(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* pr
     CK(launch_gather_cols(Ad, A->lda, m, J, k, Ct, k, ctx->stream));
     CK(launch_qrcp(Ct, k, k, m, k, I, nullptr, 0, ctx->ws2, ctx->flags_dev, kFlagRankDef, ctx->num_sms,
                    ctx->stream));                                        // I = P(1:k) of qr(C^T)
-    CK(cudaMemsetAsync(Rt, 0, (size_t)p.n * Np2 * sizeof(double), ctx->stream));
+    CK(launch_fill(Rt, p.n * Np2, 0.0, ctx->stream));
     CK(launch_gather_rows(Ad, A->lda, p.n, I, k, (double*)R, ldr, Rt, Np2, ctx->stream));   // R = A(I, :), R^T
     // R^T = Q_R S_R by Householder TSQR (always: R^T may be rank deficient)
     CKS(tsqr_local(ctx, q, Rt, Np2, p.n, p.Rsm, Pred{}));
@@ -1269,7 +1277,7 @@ rsvd_status rsvd_rpca_predict(rsvd_ctx* ctx, const rsvd_matrix* Anew, int32_t k,
   bind(ctx, p);
   if (p.use_ozaki) CKS(plan_ozaki(ctx, p, Am.m_local, Am.n, true));
   const bool f32 = p.f32;
-  CK(cudaMemsetAsync(ctx->flags_dev, 0, sizeof(int) * 16, ctx->stream));
+  CK(launch_zero_words(ctx->flags_dev, 16, ctx->stream));
   CK(launch_copy_in(rotation, f32, ldr, p.n, k, p.Np, p.X, p.Np, ctx->stream));       // W, zero padded
   if (center) CK(launch_vec_map(center, f32, p.n, 0, 0.0, p.colc, ctx->stream));
   else CK(launch_fill(p.colc, p.n, 0.0, ctx->stream));

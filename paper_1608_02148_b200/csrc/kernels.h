@@ -74,9 +74,10 @@ cudaError_t launch_panel_apply(const double* S, int64_t lds, int64_t rows, int N
 // ---- FP64 passes by Ozaki-scheme int8 slices on tcgen05 (pass_ozaki.cu)
 #define OZ_S 7                                   // 8-bit digits per element (A: 56-bit two's complement, X: 54-bit balanced)
 struct OzakiA {                                  // A sliced once per call: m x (ldn/128) x S x 128 int8 + exponents
-  int8_t* slices; double* ea;                    // ea[row][col super-tile] = 2^E (512 x 512 super-tiles)
-  double* tmax;                                  // scratch: max |f(a)| per 128 x 128 tile
-  int64_t m, n, ldn; int ntiles;
+  int8_t* slices;
+  int* erow;                                     // E_r: max_j |f(a_rj)| < 2^{E_r}, one per row
+  unsigned* emax;                                // max_r E_r + 4096 (biased, atomicMax)
+  int64_t m, n, ldn;
 };
 size_t ozaki_a_bytes(int64_t m, int64_t n);
 OzakiA ozaki_layout_a(void* buf, int64_t m, int64_t n);
@@ -171,6 +172,9 @@ cudaError_t launch_copy_in(const void* src, bool src_f32, int64_t lds, int64_t r
 // status words: *flag |= bits (predicated); end-of-call sticky status
 cudaError_t launch_flag_or(int* flag, int bits, cudaStream_t st, Pred pr);
 cudaError_t launch_status_finish(const int* flag, int* sticky, int fallback_bit, cudaStream_t st);
+// plain-launched helpers that order later PDL kernels behind non-kernel stream work
+cudaError_t launch_zero_words(int* p, int n, cudaStream_t st);
+cudaError_t launch_stream_fence(cudaStream_t st);
 // in-process rank groups: out = in[0] op in[1] ... (fixed rank order)
 constexpr int kMaxGroup = 16;
 struct GroupPtrs { const double* p[kMaxGroup]; };

@@ -616,6 +616,8 @@ namespace rsvd {
 // data (non-destructive: ss stays for the total variance); constant columns
 // get s = 1 (no scaling)
 __global__ void colstat_scale_kernel(const double* ss, int64_t n, double mg, double* rs, double* s) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
   double sd = sqrt(ss[j] / (mg - 1.0));
@@ -758,7 +760,29 @@ __global__ void status_finish_kernel(const int* flag, int* sticky, int fallback_
 }
 
 cudaError_t launch_status_finish(const int* flag, int* sticky, int fallback_bit, cudaStream_t st) {
-  CUDA_TRY(launch_pdl(status_finish_kernel, dim3(1), dim3(1), 0, st, flag, sticky, fallback_bit));
+  CUDA_TRY(launch_plain(status_finish_kernel, dim3(1), dim3(1), 0, st, flag, sticky, fallback_bit));
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+// p[0..n) = 0 by a plain launch (instead of cudaMemsetAsync, so that the
+// following PDL kernels are ordered behind it), then nothing else
+__global__ void zero_words_kernel(int* p, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
+}
+
+cudaError_t launch_zero_words(int* p, int n, cudaStream_t st) {
+  CUDA_TRY(launch_plain(zero_words_kernel, dim3(1), dim3(64), 0, st, p, n));
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+// an empty plain kernel: orders the following PDL kernels behind preceding
+// non-kernel stream work (collective copies, NCCL)
+__global__ void stream_fence_kernel() {}
+
+cudaError_t launch_stream_fence(cudaStream_t st) {
+  CUDA_TRY(launch_plain(stream_fence_kernel, dim3(1), dim3(1), 0, st));
   ++g_kernel_launches;
   return cudaGetLastError();
 }
@@ -779,7 +803,8 @@ __global__ void group_reduce_kernel(GroupPtrs in, int nranks, int64_t n, int op_
 cudaError_t launch_group_reduce(const GroupPtrs& in, int nranks, int64_t n, int op_max, double* out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 8);
-  CUDA_TRY(launch_pdl(group_reduce_kernel, dim3(g), dim3(256), 0, st, in, nranks, n, op_max, out));
+  // plain launch: it follows the staging copies and the cross-stream event waits
+  CUDA_TRY(launch_plain(group_reduce_kernel, dim3(g), dim3(256), 0, st, in, nranks, n, op_max, out));
   ++g_kernel_launches;
   return cudaGetLastError();
 }

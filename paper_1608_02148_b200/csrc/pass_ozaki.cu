@@ -8,15 +8,19 @@
 // int8 tensor throughput is ~60x higher, so an exact slice decomposition
 // moves the pass to the HBM roof.
 //
-// Representation: A is cut into 1024 x 1024 super-tiles; with max |a| < 2^E
-// over the super-tile, a is rounded to the 56-bit integer N = rn(a 2^{55-E})
-// (exact for every a >= 2^{E-3}; error <= 2^{E-56} otherwise) and N is stored
-// as S = 7 two's-complement bytes: digit 0 signed (s8), digits 1..6 unsigned
-// (u8), weight of digit t = 2^{E-7-8t}.  X (the panel, K x Np) is cut per
-// (1024-row block, column) with exponent F into S balanced signed digits
-// (s8, N = rn(x 2^{54-F}) < 2^54 in magnitude, weight of digit u = 2^{F-6-8u}).
-// Then
-//   (A X)_ij = sum_sb 2^{E + F} sum_{t,u} 2^{-13-8(t+u)} (D_t X_u)_ij
+// Representation: every row r of A gets one exponent E_r with max_j |a_rj| <
+// 2^{E_r}; a is rounded to the 56-bit integer N = rn(a 2^{55-E_r}) (exact for
+// every a >= 2^{E_r-3}; error <= 2^{E_r-56} otherwise) and N is stored as S = 7
+// two's-complement bytes: digit 0 signed (s8), digits 1..6 unsigned (u8),
+// weight of digit t = 2^{E_r-7-8t}.  The row exponents are found and applied
+// in ONE read of A (ozaki_slice_rows_kernel: a warp per row, the row re-read
+// from L1/L2 for the digits).  X (the panel, K x Np) is cut per (1024-row
+// block, column) with exponent F into S balanced signed digits (s8, N =
+// rn(x 2^{54-F}) < 2^54 in magnitude, weight of digit u = 2^{F-6-8u}).  The
+// NN pass applies 2^{E_r} to output row r at write-out; the TN pass (A^T X,
+// reducing over rows) slices X' = X diag(2^{E_k - E_max}) instead (exact
+// power-of-two row scaling) and applies 2^{E_max} at write-out.  Then
+//   (A X)_ij = 2^{E_i} sum_sb 2^{F} sum_{t,u} 2^{-13-8(t+u)} (D_t X_u)_ij
 // where D_t X_u over one super-block is an exact int32 dot product
 // (|.| <= 1024 * 255 * 128 < 2^25).  Products with t + u > S - 1 are dropped
 // (weight <= 2^{-69} relative to 2^{E+F}: below FP64 rounding of the sum).
@@ -50,7 +54,7 @@ using namespace tc;
 // columns, so the FP64 accumulators stay in registers: <= 168 per thread)
 constexpr int BM = 128, BKO = 128, THREADS = 384, EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
 constexpr int A_TILE = BM * BKO;                    // bytes of one slice tile
-constexpr int KSUP = 8, ET = KSUP * BKO;            // exponent super-tiles: 1024 x 1024 of A, 1024-row blocks of X;
+constexpr int ET = 1024;                            // exponent blocks of X: 1024 rows x 1 column;
                                                     // int32 accumulation over 1024 k: <= 7 pairs * 1024 * 255 * 128 < 2^28
 
 __host__ __device__ inline int64_t unit_lo(int64_t units, int grid, int c) { return (units * (int64_t)c) / grid; }
@@ -107,12 +111,14 @@ __device__ __forceinline__ int block_exp(double mx) { return mx > 0.0 ? ilogb(mx
 // most significant first (byte 0 read as s8, the others as u8); packed 4
 // elements per word
 template <int S>
-__device__ __forceinline__ void digits_a4(const double (&v)[4], double scale, uint32_t (&w)[S]) {
+__device__ __forceinline__ void digits_a4(const double (&v)[4], double s1, double s2, uint32_t (&w)[S]) {
 #pragma unroll
   for (int t = 0; t < S; ++t) w[t] = 0u;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const long long q = __double2ll_rn(v[e] * scale);   // exact power-of-two scaling, then round
+    // exact power-of-two scaling in two steps (2^{55-E} alone over/underflows
+    // at the ends of the exponent range), then round
+    const long long q = __double2ll_rn(v[e] * s1 * s2);
 #pragma unroll
     for (int t = 0; t < S; ++t) w[t] |= ((uint32_t)(q >> (8 * (S - 1 - t))) & 0xffu) << (8 * e);
   }
@@ -127,71 +133,91 @@ __device__ __forceinline__ double fval(const double* A, int64_t lda, const doubl
   return a;
 }
 
-// max |f(a)| per 128 x 128 tile (bx = column tile, by = row tile); flag |= 4 on non-finite
-__global__ void __launch_bounds__(256)
-ozaki_amax_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, const double* __restrict__ c,
-                  const double* __restrict__ rs, double* __restrict__ tmax, int* flag) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ double red[8];
-  const int64_t r0 = (int64_t)blockIdx.y * BM, c0 = (int64_t)blockIdx.x * BKO;
-  const int tid = threadIdx.x;
-  double mx = 0.0;
-  bool nf = false;
-  for (int e = tid; e < BM * BKO; e += 256) {
-    const int64_t r = r0 + e / BKO, cc = c0 + e % BKO;
-    if (r < m && cc < n) {
-      const double a = fval(A, lda, c, rs, r, cc);
-      if (!isfinite(a)) nf = true;
-      mx = fmax(mx, fabs(a));
-    }
+// 2^e as two exactly representable factors (e in about [-2200, 2200])
+__device__ __forceinline__ void pow2_split(int e, double& p1, double& p2) {
+  const int h = e / 2;
+  p1 = ldexp(1.0, h);
+  p2 = ldexp(1.0, e - h);
+}
+
+// four consecutive f(a) of one row starting at column j0 (zeros beyond n);
+// 16-byte loads when the row is 16-byte aligned
+__device__ __forceinline__ void load_f4(const double* row, int64_t j0, int64_t n, bool vec, const double* c,
+                                        const double* rs, double (&v)[4]) {
+  if (vec && j0 + 3 < n) {
+    const double2 a = __ldcs(reinterpret_cast<const double2*>(row + j0));
+    const double2 b = __ldcs(reinterpret_cast<const double2*>(row + j0 + 2));
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = j0 + q < n ? row[j0 + q] : 0.0;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((tid & 31) == 0) red[tid >> 5] = mx;
-  if (nf) atomicOr(flag, 4);
-  __syncthreads();
-  if (tid == 0) {
-    for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
-    tmax[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = fmax(mx, red[0]);
+  for (int q = 0; q < 4; ++q) {
+    if (j0 + q >= n) { v[q] = 0.0; continue; }
+    if (c) v[q] -= c[j0 + q];
+    if (rs) v[q] *= rs[j0 + q];
   }
 }
 
-// 128 x 128 tile -> slices, interleaved as [row][col block][t][128 bytes] so that
-// one unit's S slice boxes read one contiguous S * 128 B run per row (DRAM
-// locality for both pass orientations); digits relative to the
-// 1024 x 1024 super-tile exponent; ea[sy * nsx + sx] = 2^E
+// Slices of f(A) = (A - 1 c^T) diag(rs) with one exponent per row, in one HBM
+// read of A: a warp per row finds max_j |f(a_rj)| (pass 1, the row streamed
+// from HBM), then writes the S digit bytes of every 128-column block (pass 2,
+// the row re-read from L1 / L2); layout [row][col block][t][128 B] (one
+// unit's S slice boxes = one contiguous S x 128 B run per row).  erow[r] =
+// E_r; *emax = max_r E_r + kEBias (atomicMax, zeroed by the launcher); flag
+// |= 4 on a non-finite f(a).
+constexpr int kEBias = 4096;
 template <int S>
 __global__ void __launch_bounds__(256)
-ozaki_slice_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, const double* __restrict__ c,
-                     const double* __restrict__ rs, const double* __restrict__ tmax, int8_t* __restrict__ slices,
-                     int64_t ldn, double* __restrict__ ea, int nsx) {
+ozaki_slice_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, const double* __restrict__ c,
+                        const double* __restrict__ rs, int8_t* __restrict__ slices, int64_t ldn, int* __restrict__ erow,
+                        unsigned* emax, int* flag) {
   pdl_wait();
   pdl_trigger();
-  const int64_t r0 = (int64_t)blockIdx.y * BM, c0 = (int64_t)blockIdx.x * BKO;
-  const int tid = threadIdx.x;
-  const int sy = blockIdx.y / KSUP, sx = blockIdx.x / KSUP;
-  double mx = 0.0;
-  for (int yy = sy * KSUP; yy < min((int)gridDim.y, (sy + 1) * KSUP); ++yy)
-    for (int xx = sx * KSUP; xx < min((int)gridDim.x, (sx + 1) * KSUP); ++xx) mx = fmax(mx, tmax[(int64_t)yy * gridDim.x + xx]);
-  const int E = block_exp(mx);
-  if (tid == 0 && blockIdx.y % KSUP == 0 && blockIdx.x % KSUP == 0) ea[(int64_t)sy * nsx + sx] = ldexp(1.0, E);
-  const double scale = ldexp(1.0, 8 * S - 1 - E);
-  // 4 consecutive columns per thread-iteration; columns >= n of the last block are zero
+  __shared__ unsigned wm[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t nblk = ldn / BKO;
-  for (int e = tid; e < BM * (BKO / 4); e += 256) {
-    const int64_t r = r0 + e / (BKO / 4);
-    const int jj = 4 * (e % (BKO / 4));
-    const int64_t cc = c0 + jj;
-    if (r >= m) continue;
-    double v[4];
+  const bool vec = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  unsigned mymax = 0;
+  bool nf = false;
+  for (int64_t r = (int64_t)blockIdx.x * 8 + wid; r < m; r += (int64_t)gridDim.x * 8) {
+    const double* row = A + r * lda;
+    double mx = 0.0;
+    for (int64_t j0 = 4 * lane; j0 < n; j0 += 128) {
+      double v[4];
+      load_f4(row, j0, n, vec, c, rs, v);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = (cc + q < n) ? fval(A, lda, c, rs, r, cc + q) : 0.0;
-    uint32_t w[S];
-    digits_a4<S>(v, scale, w);
-    int8_t* dst = slices + ((r * nblk + blockIdx.x) * S) * BKO + jj;
+      for (int q = 0; q < 4; ++q) {
+        if (!isfinite(v[q])) nf = true;
+        mx = fmax(mx, fabs(v[q]));
+      }
+    }
 #pragma unroll
-    for (int t = 0; t < S; ++t) *reinterpret_cast<uint32_t*>(dst + t * BKO) = w[t];
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int E = isfinite(mx) ? block_exp(mx) : 0;
+    if (lane == 0) erow[r] = E;
+    mymax = max(mymax, (unsigned)(E + kEBias));
+    double s1, s2;
+    pow2_split(8 * S - 1 - E, s1, s2);
+    for (int64_t b = 0; b < nblk; ++b) {
+      const int64_t j0 = b * BKO + 4 * lane;
+      double v[4];
+      load_f4(row, j0, n, vec, c, rs, v);
+      uint32_t w[S];
+      digits_a4<S>(v, s1, s2, w);
+      int8_t* dst = slices + ((r * nblk + b) * S) * BKO + 4 * lane;
+#pragma unroll
+      for (int t = 0; t < S; ++t) *reinterpret_cast<uint32_t*>(dst + t * BKO) = w[t];
+    }
+  }
+  if (nf) atomicOr(flag, 4);
+  if (lane == 0) wm[wid] = mymax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int q = 0; q < 8; ++q) t = max(t, wm[q]);
+    if (t) atomicMax(emax, t);
   }
 }
 
@@ -208,7 +234,8 @@ __host__ __device__ constexpr int xt_smem(int S) { return S * XT_COLS * XT_LD; }
 template <int S>
 __global__ void __launch_bounds__(XT_THREADS)
 ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int Np, int8_t* __restrict__ xs,
-                     int64_t ldk, double* __restrict__ xf, unsigned* epoch_ctr) {
+                     int64_t ldk, double* __restrict__ xf, unsigned* epoch_ctr, const int* __restrict__ erow,
+                     const unsigned* __restrict__ emax) {
   pdl_wait();
   pdl_trigger();
   // the next pass kernel's stream-K epoch (read by it after its griddepcontrol.wait):
@@ -216,7 +243,7 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
   if (epoch_ctr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) ++*epoch_ctr;
   extern __shared__ __align__(16) unsigned char xt[];      // S x XT_COLS x XT_LD
   __shared__ double red[XT_G][XT_COLS];
-  __shared__ double escale[XT_COLS];
+  __shared__ double escale[XT_COLS][2];
   const int tid = threadIdx.x, c = tid & (XT_COLS - 1), g = tid / XT_COLS;
   const int64_t sb = blockIdx.x, k0 = sb * ET;
   const int j = blockIdx.y * XT_COLS + c;
@@ -227,6 +254,8 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
   for (int i = 0; i < XT_V; ++i) {
     const int64_t k = k0 + g + XT_G * i;
     v[i] = (jv && k < K) ? X[k * ldx + j] : 0.0;
+    // TN passes: X' = diag(2^{E_k - E_max}) X folds A's row exponents into the panel
+    if (erow && k < K) v[i] = ldexp(v[i], erow[k] - ((int)*emax - kEBias));
     mx = fmax(mx, fabs(v[i]));
   }
   red[g][c] = mx;
@@ -236,14 +265,14 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
     for (int r = 1; r < XT_G; ++r) m2 = fmax(m2, red[r][c]);
     const int E = block_exp(m2);
     if (jv) xf[sb * Np + j] = ldexp(1.0, E);
-    escale[c] = ldexp(1.0, 8 * S - 2 - E);
+    pow2_split(8 * S - 2 - E, escale[c][0], escale[c][1]);
   }
   __syncthreads();
-  const double scale = escale[c];
+  const double sc1 = escale[c][0], sc2 = escale[c][1];
 #pragma unroll
   for (int i = 0; i < XT_V; ++i) {
     const int r = g + XT_G * i;
-    long long q = __double2ll_rn(v[i] * scale);
+    long long q = __double2ll_rn(v[i] * sc1 * sc2);
 #pragma unroll
     for (int t = S - 1; t >= 1; --t) {
       const int d = (int)(signed char)(q & 0xff);
@@ -269,7 +298,7 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
 struct Args {
   double* C; int64_t ldc;
   double* P; unsigned* flags; unsigned epoch;
-  const double* ea; int ea_ld;                      // 2^E per A tile [row tile][col tile]
+  const int* erow; const unsigned* emax;            // A's row exponents E_r, max_r E_r + kEBias
   const double* xf;                                 // 2^E per (k-block, column) of X
   int64_t M, K; int N, Nout, Np;
   int64_t KB, units; int grid;
@@ -469,9 +498,8 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
     for (int64_t it = 0; it < nun; ++it) {
       const int64_t u = u_lo + it, mb = u / KB, kb = u - mb * KB;
       if (!((kb % KSU == KSU - 1) || kb == KB - 1 || it == nun - 1)) continue;
-      const int64_t sb = kb / KSU, sm_ = mb * BM / ET;      // super-block along k, super-tile along m
-      const double eaf = TRANS ? g.ea[sb * g.ea_ld + sm_] : g.ea[sm_ * g.ea_ld + sb];
-      if (lane < NC) xfs[lane] = eaf * xfh[sb * g.Np + c0 + lane];
+      const int64_t sb = kb / KSU;                          // super-block along k (X exponent block)
+      if (lane < NC) xfs[lane] = xfh[sb * g.Np + c0 + lane];
       __syncwarp();
       OZ_PROBE3(0)
       // one thread waits (sleeping), the other epilogue warps block on a named barrier
@@ -552,7 +580,10 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
               old = seen;
             }
             const bool last = (int)(nw & 0xffffffffu) == pl - pf + 1;
-            if (last) __threadfence();               // the other partials are visible after the last arrival
+            if (last) {
+              __threadfence();                       // the other partials are visible after the last arrival
+              atomicExch(cnt, 0ull);                 // back to zero: a later launch with the same epoch starts clean
+            }
             xfsm[EPI_WARPS * 32] = last ? 1.0 : 0.0;  // broadcast to the epilogue warps
           }
           asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
@@ -572,6 +603,15 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
           }
         }
         if (write) {
+          // A's exponent: 2^{E_row} for NN, 2^{E_max} for TN (exact, two factors)
+          {
+            const int64_t gmr = mb * BM + row;
+            const int e = TRANS ? (int)*g.emax - kEBias : (gmr < g.M ? g.erow[gmr] : 0);
+            double p1, p2;
+            pow2_split(e, p1, p2);
+#pragma unroll
+            for (int j = 0; j < NC; ++j) acc[j] = acc[j] * p1 * p2;
+          }
           if (it == nun - 1) {
             // the CTA's last segment: every MMA and TMA load is complete, so the unit
             // buffers stage the 128 x N block for row-contiguous (coalesced) stores
@@ -658,8 +698,7 @@ size_t ozaki_partial_bytes(int Np, int grid) {
 
 size_t ozaki_a_bytes(int64_t m, int64_t n) {
   const int64_t ldn = round_up(n, oz::BKO);
-  const int64_t tiles = ceil_div(m, oz::BM) * ceil_div(n, oz::BKO);
-  return (size_t)OZ_S * m * ldn + 256 + 2 * (size_t)tiles * sizeof(double) + 512;
+  return (size_t)OZ_S * m * ldn + 256 + (size_t)round_up(m, 64) * sizeof(int) + 512;
 }
 
 size_t ozaki_x_bytes(int64_t K, int Np) {
@@ -669,13 +708,14 @@ size_t ozaki_x_bytes(int64_t K, int Np) {
 
 cudaError_t ozaki_slice_a(const OzakiA& a, const double* A, int64_t lda, const double* c, const double* rs, int* flag,
                           cudaStream_t st) {
-  dim3 grid((unsigned)ceil_div(a.n, oz::BKO), (unsigned)ceil_div(a.m, oz::BM));
-  cudaError_t e = launch_pdl(oz::ozaki_amax_kernel, grid, dim3(256), 0, st, A, lda, a.m, a.n, c, rs, a.tmax, flag);
+  cudaError_t e = cudaMemsetAsync(a.emax, 0, sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(oz::ozaki_slice_a_kernel<OZ_S>, grid, dim3(256), 0, st, A, lda, a.m, a.n, c, rs,
-                 (const double*)a.tmax, a.slices, a.ldn, a.ea, a.ntiles);
+  const int64_t grid = std::min<int64_t>(ceil_div(a.m, 8), 148 * 8);
+  // plain launch: it follows the memset of emax
+  e = launch_plain(oz::ozaki_slice_rows_kernel<OZ_S>, dim3((unsigned)grid), dim3(256), 0, st, A, lda, a.m, a.n, c, rs,
+                   a.slices, a.ldn, a.erow, a.emax, flag);
   if (e != cudaSuccess) return e;
-  g_kernel_launches += 2;
+  ++g_kernel_launches;
   return cudaGetLastError();
 }
 
@@ -683,10 +723,8 @@ OzakiA ozaki_layout_a(void* buf, int64_t m, int64_t n) {
   OzakiA a{};
   a.m = m; a.n = n; a.ldn = round_up(n, oz::BKO);
   a.slices = reinterpret_cast<int8_t*>(buf);
-  a.ea = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + round_up((int64_t)OZ_S * m * a.ldn, 256));
-  const int64_t tiles = ceil_div(m, oz::BM) * ceil_div(n, oz::BKO);
-  a.tmax = a.ea + round_up(tiles, 32);
-  a.ntiles = (int)ceil_div(n, oz::ET);               // super-tile columns (ea row stride)
+  a.erow = reinterpret_cast<int*>(reinterpret_cast<char*>(buf) + round_up((int64_t)OZ_S * m * a.ldn, 256));
+  a.emax = reinterpret_cast<unsigned*>(a.erow + round_up(m, 64));
   return a;
 }
 
@@ -734,7 +772,8 @@ static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st) {
   if (ea != cudaSuccess) return ea;
   const dim3 gs((unsigned)ceil_div(ldk, ET), (unsigned)ceil_div(N, XT_COLS));
   const cudaError_t el = launch_pdl(ozaki_slice_x_kernel<OZ_S>, gs, dim3(XT_THREADS), (size_t)xt_smem(OZ_S), st, c.B, c.ldb, c.K, N, xs, ldk, xf,
-                                   c.flags ? c.flags + kEpochSlot : nullptr);
+                                   c.flags ? c.flags + kEpochSlot : nullptr,
+                                   c.trans ? (const int*)c.a->erow : nullptr, (const unsigned*)c.a->emax);
   if (el != cudaSuccess) return el;
   ++g_kernel_launches;
   return cudaGetLastError();
@@ -760,7 +799,7 @@ static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
   }
   Args g{};
   g.C = c.C; g.ldc = c.ldc; g.P = c.P; g.flags = c.flags; g.epoch = c.epoch;
-  g.ea = a.ea; g.ea_ld = a.ntiles; g.xf = xf;
+  g.erow = a.erow; g.emax = a.emax; g.xf = xf;
   g.M = c.M; g.K = c.K; g.N = N; g.Nout = c.Nout; g.Np = N;
   g.KB = ceil_div(c.K, bk);
   const int64_t mblocks = ceil_div(c.M, BM);
@@ -812,7 +851,7 @@ static cudaError_t ozaki_pass_pair(const OzakiCall& h0, const OzakiCall& h1, cud
     return cudaErrorInvalidValue;
   Args g{};
   g.C = h0.C; g.ldc = h0.ldc; g.P = h0.P; g.flags = h0.flags; g.epoch = h0.epoch;
-  g.ea = a.ea; g.ea_ld = a.ntiles; g.xf = xf0;
+  g.erow = a.erow; g.emax = a.emax; g.xf = xf0;
   g.C2 = h1.C; g.xf2 = xf1; g.Nout2 = h1.Nout;
   g.M = h0.M; g.K = h0.K; g.N = N; g.Nout = h0.Nout; g.Np = N;
   g.KB = ceil_div(h0.K, bk);

@@ -106,3 +106,24 @@ def test_missing_library_raises(tmp_path):
     out = subprocess.run(["python", "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "raised" in out.stdout and "not built" in out.stdout
+
+
+def test_every_pdl_kernel_waits_on_its_predecessor():
+    """Programmatic dependent launch lets a kernel start while its predecessor
+    runs: every kernel launched with launch_pdl must execute griddepcontrol.wait
+    (pdl_wait) at entry before it touches global memory.  (A kernel that did not
+    read a column-statistics buffer before the reduction producing it finished.)"""
+    import glob
+    src = {f: open(f).read() for f in glob.glob(os.path.join(ROOT, "paper_1608_02148_b200", "csrc", "*.cu"))}
+    launched = set()
+    for s in src.values():
+        launched |= set(re.findall(r"launch_pdl(?:_cluster)?\((?:oz::|tf32::)?([A-Za-z_0-9]+)", s))
+    assert len(launched) >= 15
+    missing = []
+    for f, s in src.items():
+        for m in re.finditer(r"__global__\s+void\s+(?:__launch_bounds__\([^)]*\)\s*)?([A-Za-z_0-9]+)\s*\(", s):
+            if m.group(1) in launched:
+                body = s[s.index("{", m.end()):][:400]
+                if "pdl_wait()" not in body:
+                    missing.append(m.group(1))
+    assert not missing, missing
