@@ -142,11 +142,13 @@ __device__ __forceinline__ void pow2_split(int e, double& p1, double& p2) {
 
 // four consecutive f(a) of one row starting at column j0 (zeros beyond n);
 // 16-byte loads when the row is 16-byte aligned
+template <bool LAST>
 __device__ __forceinline__ void load_f4(const double* row, int64_t j0, int64_t n, bool vec, const double* c,
                                         const double* rs, double (&v)[4]) {
   if (vec && j0 + 3 < n) {
-    const double2 a = __ldcs(reinterpret_cast<const double2*>(row + j0));
-    const double2 b = __ldcs(reinterpret_cast<const double2*>(row + j0 + 2));
+    // first read: default caching (the row is read again right after); second: evict-first
+    const double2 a = LAST ? __ldcs(reinterpret_cast<const double2*>(row + j0)) : *reinterpret_cast<const double2*>(row + j0);
+    const double2 b = LAST ? __ldcs(reinterpret_cast<const double2*>(row + j0 + 2)) : *reinterpret_cast<const double2*>(row + j0 + 2);
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
   } else {
 #pragma unroll
@@ -184,9 +186,10 @@ ozaki_slice_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t m, in
   for (int64_t r = (int64_t)blockIdx.x * 8 + wid; r < m; r += (int64_t)gridDim.x * 8) {
     const double* row = A + r * lda;
     double mx = 0.0;
+#pragma unroll 4
     for (int64_t j0 = 4 * lane; j0 < n; j0 += 128) {
       double v[4];
-      load_f4(row, j0, n, vec, c, rs, v);
+      load_f4<false>(row, j0, n, vec, c, rs, v);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (!isfinite(v[q])) nf = true;
@@ -203,7 +206,7 @@ ozaki_slice_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t m, in
     for (int64_t b = 0; b < nblk; ++b) {
       const int64_t j0 = b * BKO + 4 * lane;
       double v[4];
-      load_f4(row, j0, n, vec, c, rs, v);
+      load_f4<true>(row, j0, n, vec, c, rs, v);
       uint32_t w[S];
       digits_a4<S>(v, s1, s2, w);
       int8_t* dst = slices + ((r * nblk + b) * S) * BKO + 4 * lane;
@@ -217,6 +220,98 @@ ozaki_slice_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t m, in
   if (threadIdx.x == 0) {
     unsigned t = 0;
     for (int q = 0; q < 8; ++q) t = max(t, wm[q]);
+    if (t) atomicMax(emax, t);
+  }
+}
+
+// The same slices with the rows staged in shared memory: one CTA per SM made
+// of G groups of SR_W warps, each group owning one row buffer; the group's
+// first thread bulk-copies the group's next row (cp.async.bulk, one
+// transaction, the group's mbarrier), the group reduces max |f(a)| (shuffles +
+// a named barrier of the group only) and writes the digits from shared memory.
+// Groups never wait for each other, so copies and arithmetic overlap with up
+// to 32 warps per SM.  One HBM read of A.  Needs 16-byte aligned rows (lda and
+// n even) of at most SR_SMEM / 2 bytes.
+constexpr int SR_SMEM = 200 * 1024, SR_W = 4, SR_MAX_G = 8;
+template <int S>
+__global__ void __launch_bounds__(32 * SR_W * SR_MAX_G, 1)
+ozaki_slice_rows_smem_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                             const double* __restrict__ c, const double* __restrict__ rs, int8_t* __restrict__ slices,
+                             int64_t ldn, int* __restrict__ erow, unsigned* emax, int* flag) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(128) unsigned char srow_raw[];
+  __shared__ uint64_t full[SR_MAX_G];
+  __shared__ double redm[SR_MAX_G][SR_W];
+  __shared__ unsigned wmx[SR_MAX_G * SR_W];
+  constexpr int GT = 32 * SR_W;                     // threads per group
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int grp = wid / SR_W, gw = wid % SR_W, gt = threadIdx.x % GT;
+  const int ng = blockDim.x / GT;
+  const int64_t nblk = ldn / BKO;
+  const uint32_t row_bytes = (uint32_t)(n * 8);
+  const int64_t stride = (row_bytes + 127) / 128 * 16;          // doubles per group buffer (128-byte aligned)
+  double* row = reinterpret_cast<double*>(srow_raw) + grp * stride;
+  if (gt == 0) mbar_init(&full[grp], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  unsigned mymax = 0;
+  bool nf = false;
+  uint32_t phase = 0;
+  const int64_t gstride = (int64_t)gridDim.x * ng;
+  for (int64_t r = (int64_t)blockIdx.x * ng + grp; r < m; r += gstride, phase ^= 1u) {
+    if (gt == 0) {
+      mbar_expect_tx(&full[grp], row_bytes);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(row)), "l"(A + r * lda), "r"(row_bytes), "r"(smem_u32(&full[grp])) : "memory");
+    }
+    mbar_wait(&full[grp], phase);
+    double mx = 0.0;
+    for (int64_t j = gt; j < n; j += GT) {
+      double v = row[j];
+      if (c) v -= c[j];
+      if (rs) v *= rs[j];
+      if (!isfinite(v)) nf = true;
+      mx = fmax(mx, fabs(v));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) redm[grp][gw] = mx;
+    asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "n"(GT) : "memory");
+#pragma unroll
+    for (int w = 0; w < SR_W; ++w) mx = fmax(mx, redm[grp][w]);
+    const int E = isfinite(mx) ? block_exp(mx) : 0;
+    if (gt == 0) erow[r] = E;
+    mymax = max(mymax, (unsigned)(E + kEBias));
+    double s1, s2;
+    pow2_split(8 * S - 1 - E, s1, s2);
+    // 32 threads per 128-column block, 4 consecutive columns per thread
+    for (int64_t q = gt; q < nblk * 32; q += GT) {
+      const int64_t blk = q >> 5;
+      const int64_t j0 = blk * BKO + 4 * (q & 31);
+      double v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t jj = j0 + e;
+        double a = jj < n ? row[jj] : 0.0;
+        if (jj < n && c) a -= c[jj];
+        if (jj < n && rs) a *= rs[jj];
+        v[e] = a;
+      }
+      uint32_t w[S];
+      digits_a4<S>(v, s1, s2, w);
+      int8_t* dst = slices + ((r * nblk + blk) * S) * BKO + 4 * (q & 31);
+#pragma unroll
+      for (int t = 0; t < S; ++t) *reinterpret_cast<uint32_t*>(dst + t * BKO) = w[t];
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "n"(GT) : "memory");   // the buffer and redm are reused
+  }
+  if (nf) atomicOr(flag, 4);
+  if (lane == 0) wmx[wid] = mymax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = max(t, wmx[w]);
     if (t) atomicMax(emax, t);
   }
 }
@@ -250,12 +345,16 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
   const bool jv = j < Np;
   double v[XT_V];
   double mx = 0.0;
+  const int eoff = erow ? (int)*emax - kEBias : 0;
 #pragma unroll
   for (int i = 0; i < XT_V; ++i) {
     const int64_t k = k0 + g + XT_G * i;
     v[i] = (jv && k < K) ? X[k * ldx + j] : 0.0;
     // TN passes: X' = diag(2^{E_k - E_max}) X folds A's row exponents into the panel
-    if (erow && k < K) v[i] = ldexp(v[i], erow[k] - ((int)*emax - kEBias));
+    if (erow && k < K) {
+      const int d = __ldg(erow + k) - eoff;                   // <= 0
+      v[i] *= d >= -1022 ? __hiloint2double((d + 1023) << 20, 0) : ldexp(1.0, d);
+    }
     mx = fmax(mx, fabs(v[i]));
   }
   red[g][c] = mx;
@@ -710,7 +809,25 @@ cudaError_t ozaki_slice_a(const OzakiA& a, const double* A, int64_t lda, const d
                           cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(a.emax, 0, sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
-  const int64_t grid = std::min<int64_t>(ceil_div(a.m, 8), 148 * 8);
+  // shared-memory staged rows (one buffer per warp, bulk copies) when 16-byte aligned rows fit
+  const int64_t rbuf = (a.n * 8 + 127) / 128 * 128;
+  const int ngroups = (int)std::min<int64_t>(oz::SR_MAX_G, oz::SR_SMEM / rbuf);
+  if (ngroups >= 2 && (a.n % 2 == 0) && (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0)) {
+    e = smem_optin(oz::ozaki_slice_rows_smem_kernel<OZ_S>);
+    if (e != cudaSuccess) return e;
+    e = launch_plain(oz::ozaki_slice_rows_smem_kernel<OZ_S>,
+                     dim3((unsigned)std::min<int64_t>(ceil_div(a.m, (int64_t)ngroups), 148)),
+                     dim3(32 * oz::SR_W * ngroups), (size_t)ngroups * rbuf, st, A, lda, a.m, a.n, c, rs, a.slices,
+                     a.ldn, a.erow, a.emax, flag);
+    if (e != cudaSuccess) return e;
+    ++g_kernel_launches;
+    return cudaGetLastError();
+  }
+  // otherwise one warp per row, rows in flight bounded so that the second read of
+  // each row hits L1 / L2: at most ~256 KB of rows per SM
+  const int64_t row_bytes = std::max<int64_t>(a.n * 8, 1);
+  const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(8, (256 << 10) / (8 * row_bytes)));
+  const int64_t grid = std::min<int64_t>(ceil_div(a.m, 8), 148 * per_sm);
   // plain launch: it follows the memset of emax
   e = launch_plain(oz::ozaki_slice_rows_kernel<OZ_S>, dim3((unsigned)grid), dim3(256), 0, st, A, lda, a.m, a.n, c, rs,
                    a.slices, a.ldn, a.erow, a.emax, flag);
