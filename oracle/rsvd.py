@@ -205,7 +205,9 @@ def oracle_rrpca(A, lam=None, maxiter=100, tol=1e-7, k=20, p=10, q=2,
     det_switch the truncated SVD of step (6) is the deterministic one (numpy
     SVD) whenever k > min(m, n)/4 (Remark 2).  rand=False: the
     deterministic truncated SVD in every iteration.
-    Returns dict(L, S, iters, residual, trace=[(res, l, mu, k)...]).
+    Returns dict(L, S, iters, residual, trace=[(res, l, mu, k)...],
+    sigmas=[the step-(6) singular values of every iteration]).  tol <= 0 runs
+    exactly maxiter iterations.
     """
     A = np.asarray(A, dtype=np.float64)
     m, n = A.shape
@@ -225,6 +227,7 @@ def oracle_rrpca(A, lam=None, maxiter=100, tol=1e-7, k=20, p=10, q=2,
     S = np.zeros_like(A)
     normF = np.sqrt(np.sum(A * A))
     hist = []
+    sigmas = []
     L = np.zeros_like(A)
     res = np.inf
     it = 0
@@ -236,6 +239,7 @@ def oracle_rrpca(A, lam=None, maxiter=100, tol=1e-7, k=20, p=10, q=2,
         else:
             r = oracle_rsvd(M, k, p=p, q=q, sdist=sdist, seed=seed, stream=it)
         d = r["d"]
+        sigmas.append(np.array(d, copy=True))
         nl = int(np.sum(d > 1.0 / mu))
         kused = k
         if adaptive:
@@ -252,7 +256,7 @@ def oracle_rrpca(A, lam=None, maxiter=100, tol=1e-7, k=20, p=10, q=2,
         if res < tol:
             break
     return dict(L=L, S=S, iters=it, residual=res, trace=hist, lam=lam, mu0=mu0,
-                norm2=norm2)
+                norm2=norm2, sigmas=sigmas)
 
 
 def _triu_solve(S, B):

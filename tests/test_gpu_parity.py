@@ -36,7 +36,48 @@ def _cos_cols(X, Y):
     return np.abs(np.sum(X * Y, axis=0)) / (np.linalg.norm(X, axis=0) * np.linalg.norm(Y, axis=0))
 
 
-def _check_parity(A, r, o, k, tol_d=1e-10, tol_orth=1e-12, floor=1e-13, gap_tol=1e-6, cos_tol=1e-8):
+def _clusters(dd, gap_tol):
+    """Groups of consecutive singular values whose neighbours are closer than
+    gap_tol * d_0 (singular vectors defined only up to a rotation inside a
+    group, reading R29 / SURVEY c29)."""
+    groups, cur = [], [0]
+    for i in range(1, len(dd)):
+        if abs(dd[i - 1] - dd[i]) <= gap_tol * dd[0]:
+            cur.append(i)
+        else:
+            groups.append(cur)
+            cur = [i]
+    groups.append(cur)
+    return groups
+
+
+def _sin_max_angle(X, Y):
+    """sin of the largest principal angle between span(X) and span(Y) (both
+    with orthonormal columns): ||(I - Y Y^T) X||_2."""
+    R = X - Y @ (Y.T @ X)
+    return float(np.linalg.norm(R, 2)) if R.size else 0.0
+
+
+def _check_vectors(Vg, Vo, dd, gap_tol, cos_tol, ang_tol):
+    """Separated singular vectors column by column (|cos| > 1 - cos_tol, same
+    sign, reading R9); clusters of near-equal values by principal angles
+    (sin theta_max <= ang_tol); a cluster cut by the last compared column is
+    not determined by the first columns alone and is skipped."""
+    nv = min(Vg.shape[1], Vo.shape[1], len(dd))
+    for grp in _clusters(dd, gap_tol):
+        if grp[0] >= nv:
+            break
+        if len(grp) == 1:
+            i = grp[0]
+            c = abs(float(Vg[:, i] @ Vo[:, i])) / (np.linalg.norm(Vg[:, i]) * np.linalg.norm(Vo[:, i]))
+            assert c > 1 - cos_tol, (i, c)
+            assert float(Vg[:, i] @ Vo[:, i]) > 0, ("sign", i)
+        elif grp[-1] < nv:
+            sa = _sin_max_angle(Vg[:, grp], Vo[:, grp])
+            assert sa <= ang_tol, (grp, sa)
+
+
+def _check_parity(A, r, o, k, tol_d=1e-10, tol_orth=1e-12, floor=1e-13, gap_tol=1e-6, cos_tol=1e-8, ang_tol=1e-8):
     d, U, V = _np(r.d), _np(r.u), _np(r.v)
     assert np.all(np.isfinite(d)) and np.all(np.isfinite(U)) and np.all(np.isfinite(V))
     rel = np.abs(d - o["d"]) / np.maximum(np.abs(o["d"]), 1e-300)
@@ -49,20 +90,11 @@ def _check_parity(A, r, o, k, tol_d=1e-10, tol_orth=1e-12, floor=1e-13, gap_tol=
         e_gpu = _recon_err(A, d, U, V)
         e_or = _recon_err(A, o["d"], o["u"], o["v"])
         assert e_gpu <= 1.0001 * e_or + floor, (e_gpu, e_or)
-    # singular vectors: column-wise where the spectrum is separated (reading R29)
-    dd = o["d"]
-    sep = np.ones(len(dd), dtype=bool)
-    for i in range(len(dd)):
-        for j in range(len(dd)):
-            if i != j and abs(dd[i] - dd[j]) <= gap_tol * dd[0]:
-                sep[i] = False
-    nv = min(V.shape[1], o["v"].shape[1])
-    if nv:
-        c = _cos_cols(V[:, :nv], o["v"][:, :nv])[sep[:nv]]
-        assert np.all(c > 1 - cos_tol), c.min()
-        # sign convention (R9): same signs as the oracle for separated columns
-        s = np.sign(np.sum(V[:, :nv] * o["v"][:, :nv], axis=0))[sep[:nv]]
-        assert np.all(s > 0)
+    # singular vectors: column-wise where separated, principal angles in clusters (R29)
+    if V.shape[1]:
+        _check_vectors(V, o["v"], o["d"], gap_tol, cos_tol, ang_tol)
+    if U.shape[1]:
+        _check_vectors(U, o["u"], o["d"], gap_tol, cos_tol, ang_tol)
 
 
 # ----------------------------------------------------------------------------- Omega (K1)
@@ -176,7 +208,8 @@ def test_rsvd_fp32(rb):
     r = rb.rsvd(A.cuda(), 30, p=10, q=2, seed=4)
     assert r.d.dtype == torch.float32
     o = oracle.oracle_rsvd(An, 30, p=10, q=2, seed=4)
-    _check_parity(An.astype(np.float64), r, o, 30, tol_d=1e-4, tol_orth=1e-5, floor=1e-6, cos_tol=1e-5)
+    _check_parity(An.astype(np.float64), r, o, 30, tol_d=1e-4, tol_orth=1e-5, floor=1e-6, cos_tol=1e-5, ang_tol=1e-3,
+                  gap_tol=1e-3)
 
 
 def test_rsvd_rank_deficient_large_panel(rb):
@@ -374,46 +407,80 @@ def test_rcur_parity(rb, m, n, k):
 
 
 # ----------------------------------------------------------------------------- rrpca
+def _rrpca_trajectory(out, o, margin=0.05):
+    """Compare the GPU's per-iteration (l, k) of Alg. 7 with the oracle's.
+    Returns the first iteration where they differ (None if never).  A
+    difference is only accepted where it is ill-posed: every oracle singular
+    value between the two counts lies within `margin` of the threshold 1/mu
+    (the tail of a randomized SVD is not determined to rounding level, so a
+    count can flip there; reading R30)."""
+    nt = min(len(out["trace"]), len(o["trace"]))
+    for t in range(nt):
+        g, w = out["trace"][t], o["trace"][t]
+        assert g[3] == w[3], ("target rank differs before any count did", t)
+        if g[1] != w[1]:
+            thr = 1.0 / w[2]
+            lo, hi = sorted((g[1], w[1]))
+            band = np.asarray(o["sigmas"][t][lo:hi])
+            assert band.size and np.all(np.abs(band - thr) <= margin * thr), (t, g[1], w[1], band, thr)
+            return t
+    return None
+
+
+def _rrpca_same_iterations(An, out, kw):
+    """An oracle run of exactly the GPU's number of iterations (tol <= 0 never
+    stops early), for the L / S comparison when the natural counts differ."""
+    kw = dict(kw, maxiter=out["iters"], tol=0.0)
+    return oracle.oracle_rrpca(An, **kw)
+
+
+def _check_rrpca(rb, A, L0=None, S0=None, recover=True, **kw):
+    """GPU rrpca vs the oracle on the same A and Omega streams: the rank
+    trajectory, the residual trace (1e-6 relative), and L and S within 1e-10
+    of an oracle run with the SAME number of iterations (rerun with maxiter =
+    the GPU's count when the natural counts differ) whenever the trajectories
+    agree; planted components recovered (1e-6, support 0.999)."""
+    An = A.numpy()
+    out = rb.rrpca(A.cuda(), trace=True, **{key: val for key, val in kw.items() if key != "kmax"})
+    okw = {key: val for key, val in kw.items() if key != "rand"}
+    o = oracle.oracle_rrpca(An, rand=kw.get("rand", True), **okw)
+    div = _rrpca_trajectory(out, o)
+    nt = min(out["iters"], o["iters"]) if div is None else div
+    for t in range(nt):
+        assert abs(out["trace"][t][0] - o["trace"][t][0]) <= 1e-6 * o["trace"][t][0] + 1e-15, t
+    L, S = _np(out["L"]), _np(out["S"])
+    if div is None:
+        ref = o if out["iters"] == o["iters"] else _rrpca_same_iterations(An, out, dict(okw, rand=kw.get("rand", True)))
+        assert np.linalg.norm(L - ref["L"]) / np.linalg.norm(ref["L"]) < 1e-10
+        assert np.linalg.norm(S - ref["S"]) / np.linalg.norm(ref["S"]) < 1e-10
+        assert abs(out["iters"] - o["iters"]) <= 1
+    if recover and L0 is not None:
+        L0n, S0n = L0.numpy(), S0.numpy()
+        assert np.linalg.norm(L - L0n) / np.linalg.norm(L0n) < 1e-6
+        assert ((np.abs(S) > 1e-6) == (S0n != 0)).mean() > 0.999
+    assert out["residual"] < kw["tol"]
+    return out, o, div
+
+
 def test_rrpca_parity_small(rb):
     A, L0, S0 = synthetic.sparse_plus_lowrank(4000, 300, rank=5, frac=0.05, seed=12)
-    An = A.numpy()
-    out = rb.rrpca(A.cuda(), k=10, p=10, q=2, tol=1e-7, maxiter=100, seed=3, trace=True)
-    o = oracle.oracle_rrpca(An, k=10, p=10, q=2, tol=1e-7, maxiter=100, seed=3)
-    assert abs(out["iters"] - o["iters"]) <= 1
-    L, S = _np(out["L"]), _np(out["S"])
-    if out["iters"] == o["iters"]:
-        assert np.linalg.norm(L - o["L"]) / np.linalg.norm(o["L"]) < 1e-10
-        assert np.linalg.norm(S - o["S"]) / np.linalg.norm(o["S"]) < 1e-10
-    L0n, S0n = L0.numpy(), S0.numpy()
-    assert np.linalg.norm(L - L0n) / np.linalg.norm(L0n) < 1e-6
-    assert ((np.abs(S) > 1e-6) == (S0n != 0)).mean() > 0.999
-    assert out["residual"] < 1e-7
+    _, _, div = _check_rrpca(rb, A, L0, S0, k=10, p=10, q=2, tol=1e-7, maxiter=100, seed=3)
+    assert div is None
 
 
 @pytest.mark.parametrize("m,n,rank,k", [(4000, 300, 5, 0), (3000, 400, 40, 0), (3000, 400, 40, 60)])
 def test_rrpca_adaptive_and_large_rank_parity(rb, m, n, rank, k):
     """Alg. 7 with the adaptive target rank of steps (1), (7) (k = 0, R30) and a
     fixed rank above 32 (the R = 64 update kernel): the rank trajectory (l, k)
-    per iteration matches the oracle's exactly, L and S within 1e-10 when the
-    iteration counts agree, and the planted L0, S0 are recovered."""
+    per iteration matches the oracle's (a count may differ only where the
+    oracle's values sit at 1/mu), L and S within 1e-10 of the oracle at the
+    same iteration count, and the planted L0, S0 are recovered."""
     A, L0, S0 = synthetic.sparse_plus_lowrank(m, n, rank=rank, frac=0.05, seed=rank + 11)
-    An = A.numpy()
-    out = rb.rrpca(A.cuda(), k=k, p=10, q=2, tol=1e-7, maxiter=100, seed=4, trace=True)
-    o = oracle.oracle_rrpca(An, k=k, p=10, q=2, tol=1e-7, maxiter=100, seed=4, kmax=min(m, n, 110))
+    out, o, div = _check_rrpca(rb, A, L0, S0, k=k, p=10, q=2, tol=1e-7, maxiter=100, seed=4, kmax=min(m, n, 110))
     assert all(t[3] <= min(m, n) / 4 for t in o["trace"])          # no Remark-2 switch on either side
-    nt = min(out["iters"], o["iters"])
-    assert [(t[1], t[3]) for t in out["trace"][:nt]] == [(t[1], t[3]) for t in o["trace"][:nt]]
     if k == 0:
         assert out["trace"][0][3] == 2 and out["trace"][-1][3] == rank + 1
-    assert abs(out["iters"] - o["iters"]) <= 1
-    L, S = _np(out["L"]), _np(out["S"])
-    if out["iters"] == o["iters"]:
-        assert np.linalg.norm(L - o["L"]) / np.linalg.norm(o["L"]) < 1e-10
-        assert np.linalg.norm(S - o["S"]) / np.linalg.norm(o["S"]) < 1e-10
-    L0n, S0n = L0.numpy(), S0.numpy()
-    assert np.linalg.norm(L - L0n) / np.linalg.norm(L0n) < 1e-6
-    assert ((np.abs(S) > 1e-6) == (S0n != 0)).mean() > 0.999
-    assert out["residual"] < 1e-7
+        assert div is None
 
 
 @pytest.mark.parametrize("rank,k,rand", [(5, 10, False), (32, 0, True)])
@@ -421,42 +488,51 @@ def test_rrpca_deterministic_svd(rb, rank, k, rand):
     """rand = FALSE and Remark 2's switch (adaptive k >
     min(m, n)/4 -> deterministic SVD): the GPU's deterministic SVD (rsvd with
     l = min(m, n), q = 0) against the oracle's numpy SVD, same rank trajectory,
-    L and S within 1e-10 when the iteration counts agree; the rank-5 case also
+    L and S within 1e-10 at the same iteration count; the rank-5 case also
     recovers the planted L0 (rank 32 of 120 is beyond exact recovery)."""
     A, L0, S0 = synthetic.sparse_plus_lowrank(3000, 120, rank=rank, frac=0.05, seed=rank + 100)
-    An = A.numpy()
-    out = rb.rrpca(A.cuda(), k=k, p=10, q=2, tol=1e-7, maxiter=100, seed=4, trace=True, rand=rand)
-    o = oracle.oracle_rrpca(An, k=k, p=10, q=2, tol=1e-7, maxiter=100, seed=4, rand=rand)
+    out, o, div = _check_rrpca(rb, A, L0, S0, recover=rank == 5, k=k, p=10, q=2, tol=1e-7, maxiter=100, seed=4,
+                               rand=rand)
     if k == 0:
         assert any(t[3] > 120 / 4 for t in o["trace"])               # the switch is exercised
-    nt = min(out["iters"], o["iters"])
-    assert [(t[1], t[3]) for t in out["trace"][:nt]] == [(t[1], t[3]) for t in o["trace"][:nt]]
-    assert abs(out["iters"] - o["iters"]) <= 1
-    L, S = _np(out["L"]), _np(out["S"])
-    if out["iters"] == o["iters"]:
-        assert np.linalg.norm(L - o["L"]) / np.linalg.norm(o["L"]) < 1e-10
-        assert np.linalg.norm(S - o["S"]) / np.linalg.norm(o["S"]) < 1e-10
-    if rank == 5:
-        assert np.linalg.norm(L - L0.numpy()) / np.linalg.norm(L0.numpy()) < 1e-6
+    assert div is None
 
 
 # ----------------------------------------------------------------------------- full-size configs 3, 5
 def test_config3_full_size_rpca(rb):
-    """Config 3 (J:9): 200000 x 4000 column-centred PCA, k=100, p=20, q=2, uniform Omega."""
+    """Config 3 (J:9): 200000 x 4000 column-centred PCA (scale = FALSE, reading
+    R15), k=100, p=20, q=2, uniform Omega: eigenvalues (2e-10, the d^2 of the
+    1e-10 d tolerance), column means, rotation and scores x = U Sigma
+    (Alg. 6 step (3)) column-wise where separated and by principal angles in
+    clusters, orthonormality, and the centred reconstruction error within
+    1.0001 x the oracle's (computed in row chunks on the device)."""
     A, meta = synthetic.make_config(3)
-    out = rb.rpca(A.cuda(), 100, center=True, p=20, q=2, sdist="unif", seed=meta["seed_omega"])
+    Ad = A.cuda()
+    out = rb.rpca(Ad, 100, center=True, scale=False, p=20, q=2, sdist="unif", seed=meta["seed_omega"])
     An = A.numpy()
-    o = oracle.oracle_rpca(An, 100, center=True, p=20, q=2, sdist="unif", seed=meta["seed_omega"])
+    o = oracle.oracle_rpca(An, 100, center=True, scale=False, p=20, q=2, sdist="unif", seed=meta["seed_omega"])
     ev = _np(out["eigvals"])
-    assert np.max(np.abs(ev - o["eigvals"]) / o["eigvals"]) < 2e-10       # d^2: twice the d tolerance
+    assert np.max(np.abs(ev - o["eigvals"]) / o["eigvals"]) < 2e-10
     assert np.abs(_np(out["center"]) - o["center"]).max() < 1e-12
-    rot = _np(out["rotation"])
+    rot, x = _np(out["rotation"]), _np(out["x"])
     assert np.abs(rot.T @ rot - np.eye(100)).max() < 1e-12
-    # separated eigenpairs agree column-wise with the oracle
-    dd = np.sqrt(o["eigvals"])
-    sep = np.array([min([abs(dd[i] - dd[j]) for j in range(100) if j != i]) > 1e-6 * dd[0] for i in range(100)])
-    c = _cos_cols(rot, o["rotation"])[sep]
-    assert np.all(c > 1 - 1e-8)
+    d = np.sqrt(o["eigvals"] * (An.shape[0] - 1))
+    _check_vectors(rot, o["rotation"], d, 1e-6, 1e-8, 1e-8)
+    U, Uo = x / d[None, :], o["x"] / d[None, :]
+    assert np.abs(U.T @ U - np.eye(100)).max() < 1e-11
+    _check_vectors(U, Uo, d, 1e-6, 1e-8, 1e-8)
+    # centred reconstruction error ||X - x W^T||_F / ||X||_F, X = A - 1 c^T
+    c = torch.as_tensor(o["center"], device="cuda")
+    xg, rg = out["x"], out["rotation"]
+    xo, ro = torch.as_tensor(o["x"], device="cuda"), torch.as_tensor(o["rotation"], device="cuda")
+    num_g = num_o = den = 0.0
+    for r0 in range(0, A.shape[0], 20000):
+        X = Ad[r0:r0 + 20000] - c[None, :]
+        den += float((X * X).sum())
+        num_g += float(((X - xg[r0:r0 + 20000] @ rg.T) ** 2).sum())
+        num_o += float(((X - xo[r0:r0 + 20000] @ ro.T) ** 2).sum())
+    eg, eo = np.sqrt(num_g / den), np.sqrt(num_o / den)
+    assert eg <= 1.0001 * eo + 1e-13, (eg, eo)
 
 
 @pytest.mark.timeout(1200)
@@ -492,20 +568,55 @@ def test_config4_full_size_properties(rb):
     del A
 
 
+@pytest.mark.timeout(1800)
+def test_config4_full_size_vs_oracle(rb):
+    """Config 4 (J:10) at full size against the oracle's FP64 rsvd of the same
+    FP32 A (tests/golden/cfg4_oracle.npz, written on the GPU box's host by
+    tools/make_cfg4_golden.py, which calls only oracle/ and synthetic/):
+    d within the FP32 tolerance 1e-4 (J:5), V column-wise / by principal
+    angles within 1e-3 (reading R29 FP32), U and V orthonormal to 1e-5, and
+    the reconstruction error (row chunks, FP64, on the device) within
+    1.0001 x the oracle's + 1e-6 (R24)."""
+    import os
+    gold = os.path.join(os.path.dirname(__file__), "golden", "cfg4_oracle.npz")
+    g = np.load(gold)
+    A, meta = synthetic.make_config(4, device="cuda")
+    r = rb.rsvd(A, 100, p=20, q=3, sdist=meta["sdist"], seed=meta["seed_omega"])
+    d, V = _np(r.d), _np(r.v)
+    assert np.max(np.abs(d - g["d"]) / g["d"]) <= 1e-4
+    _check_vectors(V, g["v"], g["d"], 1e-3, 1e-4, 1e-3)
+    eye = torch.eye(100, dtype=torch.float64, device="cuda")
+    Ud = r.u.double()
+    assert float((Ud.T @ Ud - eye).abs().max()) < 1e-5
+    assert np.abs(V.T @ V - np.eye(100)).max() < 1e-5
+    ur = g["u_rows"]                                   # the oracle's first 2000 rows of U
+    ug = _np(r.u[:ur.shape[0]])
+    for grp in _clusters(g["d"], 1e-3):               # separated columns: same direction and sign
+        if len(grp) == 1:
+            i = grp[0]
+            c = float(ug[:, i] @ ur[:, i]) / (np.linalg.norm(ug[:, i]) * np.linalg.norm(ur[:, i]))
+            assert c > 1 - 1e-2, (i, c)
+    num = den = 0.0
+    Vd, dd = r.v.double(), r.d.double()
+    for r0 in range(0, A.shape[0], 50000):
+        X = A[r0:r0 + 50000].double()
+        den += float((X * X).sum())
+        num += float(((X - (Ud[r0:r0 + 50000] * dd[None, :]) @ Vd.T) ** 2).sum())
+    err = np.sqrt(num / den)
+    assert err <= 1.0001 * float(g["recon_err"]) + 1e-6, (err, float(g["recon_err"]))
+    del A
+
+
 def test_config5_full_size_rrpca(rb):
-    """Config 5 (J:11): 100000 x 1000 robust PCA by IALM, rsvd(k=20, p=10, q=2), tol 1e-7."""
+    """Config 5 (J:11): 100000 x 1000 robust PCA by IALM, rsvd(k=20, p=10, q=2),
+    tol 1e-7: the residual trace of every iteration, L and S against the oracle
+    run of the SAME number of iterations (unconditionally: an oracle rerun
+    with maxiter = the GPU's count when the natural counts differ), and the
+    planted L0, S0 (ground truth, R21 / SURVEY X5)."""
     A, meta = synthetic.make_config(5)
-    out = rb.rrpca(A.cuda(), k=20, p=10, q=2, tol=1e-7, maxiter=100, seed=meta["seed_omega"], trace=True)
-    L, S = _np(out["L"]), _np(out["S"])
-    L0, S0 = meta["L0"].numpy(), meta["S0"].numpy()
-    assert out["residual"] < 1e-7
-    assert np.linalg.norm(L - L0) / np.linalg.norm(L0) < 1e-6                  # ground truth (R21, X5)
-    assert ((np.abs(S) > 1e-6) == (S0 != 0)).mean() > 0.999
-    o = oracle.oracle_rrpca(A.numpy(), k=20, p=10, q=2, tol=1e-7, maxiter=100, seed=meta["seed_omega"])
-    assert abs(out["iters"] - o["iters"]) <= 1
-    if out["iters"] == o["iters"]:
-        assert np.linalg.norm(L - o["L"]) / np.linalg.norm(o["L"]) < 1e-10
-        assert np.linalg.norm(S - o["S"]) / np.linalg.norm(o["S"]) < 1e-10
+    out, o, div = _check_rrpca(rb, A, meta["L0"], meta["S0"], k=20, p=10, q=2, tol=1e-7, maxiter=100,
+                               seed=meta["seed_omega"])
+    assert div is None                       # fixed rank 20 of a rank-20 signal: no borderline counts
 
 
 # ----------------------------------------------------------------------------- FP32 on tcgen05
@@ -517,7 +628,8 @@ def test_rsvd_fp32_tcgen05_parity(rb, m, n, k, p, q):
     An = A.numpy()
     r = rb.rsvd(A.cuda(), k, p=p, q=q, seed=12)
     o = oracle.oracle_rsvd(An, k, p=p, q=q, seed=12)
-    _check_parity(An.astype(np.float64), r, o, k, tol_d=1e-4, tol_orth=1e-5, floor=1e-6, gap_tol=1e-3, cos_tol=1e-5)
+    _check_parity(An.astype(np.float64), r, o, k, tol_d=1e-4, tol_orth=1e-5, floor=1e-6, gap_tol=1e-3, cos_tol=1e-5,
+                  ang_tol=1e-3)
 
 
 # ----------------------------------------------------------------------------- FP64 pass paths
