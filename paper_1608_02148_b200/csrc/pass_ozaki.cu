@@ -455,7 +455,11 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   const int pid = (int)blockIdx.x / CL, npair = g.grid / CL;
   const int64_t u_lo = unit_lo(g.units, npair, pid);
   const int64_t u_hi = unit_lo(g.units, npair, pid + 1);
-  const int64_t nun = u_hi - u_lo;
+  const int nun = (int)(u_hi - u_lo);
+  // (row block, k-block) of the first unit; the loops advance them incrementally
+  // (no 64-bit division per unit on the single-thread producer / MMA paths)
+  const int mb0 = (int)(u_lo / KB), kb0 = (int)(u_lo - (int64_t)mb0 * KB);
+  const int KBi = (int)KB;
   double* const Cout = crank ? g.C2 : g.C;
   const double* const xfh = crank ? g.xf2 : g.xf;
   const int Nout = crank ? g.Nout2 : g.Nout;
@@ -479,12 +483,12 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
     // ---------------- TMA producer: one transaction per unit
     if (lane == 0) {
       OZ_PROBE2_DECL
-      for (int64_t it = 0; it < nun; ++it) {
-        const int64_t u = u_lo + it, mb = u / KB, kb = u - mb * KB;
-        const int ub = (int)(it % NB);
+      int mb = mb0, kb = kb0, ub = 0;
+      uint32_t ph = 0;
+      for (int it = 0; it < nun; ++it, (++kb == KBi ? (kb = 0, ++mb) : 0), (++ub == NB ? (ub = 0, ph ^= 1u) : 0u)) {
         unsigned char* ubuf = base + ub * UBUF;
         OZ_PROBE2(0)
-        mbar_wait(&uempty[ub], (uint32_t)(((it / NB) & 1) ^ 1));
+        mbar_wait(&uempty[ub], ph ^ 1u);
         OZ_PROBE2(1)
 #if defined(OZ_NO_A_TMA)            // probe builds only (tools/test_ozaki.cu): no A-slice loads
         mbar_expect_tx(&ufull[ub], (uint32_t)(S * XSL));
@@ -497,13 +501,13 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         if (CL == 1) {
 #endif
           for (int t = 0; t < S; ++t) {
-            if (!TRANS) tma_4d(ubuf + t * A_UT, &mapA, (int)((kb % KPB) * BKU), t, (int)(kb / KPB), (int)(mb * BM), &ufull[ub]);
+            if (!TRANS) tma_4d(ubuf + t * A_UT, &mapA, (int)((kb % KPB) * BKU), t, (int)(kb / KPB), (int)((int64_t)mb * BM), &ufull[ub]);
             else tma_4d(ubuf + t * A_UT, &mapA, 0, t, (int)mb, (int)(kb * BKU), &ufull[ub]);
           }
         } else {
           for (int t = crank; t < S; t += 2) {
             if (!TRANS)
-              tma_4d_mc(ubuf + t * A_UT, &mapA, (int)((kb % KPB) * BKU), t, (int)(kb / KPB), (int)(mb * BM), &ufull[ub], (uint16_t)3);
+              tma_4d_mc(ubuf + t * A_UT, &mapA, (int)((kb % KPB) * BKU), t, (int)(kb / KPB), (int)((int64_t)mb * BM), &ufull[ub], (uint16_t)3);
             else tma_4d_mc(ubuf + t * A_UT, &mapA, 0, t, (int)mb, (int)(kb * BKU), &ufull[ub], (uint16_t)3);
           }
         }
@@ -515,7 +519,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       }
       if (CL == 2) {
         // the peer's commits for the last units must have landed before this CTA exits
-        for (int64_t it = nun > NB ? nun - NB : 0; it < nun; ++it) mbar_wait(&uempty[it % NB], (uint32_t)((it / NB) & 1));
+        for (int it = nun > NB ? nun - NB : 0; it < nun; ++it) mbar_wait(&uempty[it % NB], (uint32_t)((it / NB) & 1));
       }
       OZ_PROBE2(0)
       OZ_PROBE2_OUT
@@ -531,14 +535,15 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
                               ((uint32_t)(BM >> 4) << 24);
       constexpr int CMAX = 256 / N;
       OZ_PROBE_DECL
-      int64_t ndrain = 0;
+      int ndrain = 0;
       bool fresh = true;
-      for (int64_t it = 0; it < nun; ++it) {
-        const int64_t u = u_lo + it, kb = u % KB;
-        const bool drain = (kb % KSU == KSU - 1) || kb == KB - 1 || it == nun - 1;
-        const int ub = (int)(it % NB);
+      int kb = kb0, ub = 0, ks = kb0 % KSU;
+      uint32_t ph = 0;
+      for (int it = 0; it < nun; ++it, (++kb == KBi ? (kb = 0, ks = 0) : (++ks == KSU ? (ks = 0) : 0)),
+                                       (++ub == NB ? (ub = 0, ph ^= 1u) : 0u)) {
+        const bool drain = (ks == KSU - 1) || kb == KBi - 1 || it == nun - 1;
         OZ_PROBE(0)
-        mbar_wait(&ufull[ub], (uint32_t)((it / NB) & 1));
+        mbar_wait(&ufull[ub], ph);
         OZ_PROBE(3)
 #ifndef OZ_NO_EPI
         if (fresh && ndrain > 0) mbar_wait(&acce, (uint32_t)((ndrain - 1) & 1));
@@ -594,9 +599,10 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
     double* xfs = xfsm + (warp - 4) * 32;             // per-warp copy of this super-block's column factors
     int64_t ndrain = 0;
     OZ_PROBE3_DECL
-    for (int64_t it = 0; it < nun; ++it) {
-      const int64_t u = u_lo + it, mb = u / KB, kb = u - mb * KB;
-      if (!((kb % KSU == KSU - 1) || kb == KB - 1 || it == nun - 1)) continue;
+    int mb = mb0, kb = kb0;
+    for (int it = 0; it < nun; ++it, (++kb == KBi ? (kb = 0, ++mb) : 0)) {
+      const int64_t u = u_lo + it;
+      if (!((kb % KSU == KSU - 1) || kb == KBi - 1 || it == nun - 1)) continue;
       const int64_t sb = kb / KSU;                          // super-block along k (X exponent block)
       if (lane < NC) xfs[lane] = xfh[sb * g.Np + c0 + lane];
       __syncwarp();
@@ -655,7 +661,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         // segment, 1 = its last) and an epoch-tagged arrival counter; the last
         // arriver sums the partials in CTA order (the same order whoever arrives
         // last, so results are bitwise reproducible) and writes the rows.
-        const int64_t rb_lo = mb * KB, rb_hi = rb_lo + KB;
+        const int64_t rb_lo = (int64_t)mb * KB, rb_hi = rb_lo + KB;
         const int64_t seg_start = (rb_lo > u_lo) ? rb_lo : u_lo;
         const bool full = seg_start == rb_lo && u + 1 == rb_hi;
         bool write = full;
@@ -704,7 +710,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         if (write) {
           // A's exponent: 2^{E_row} for NN, 2^{E_max} for TN (exact, two factors)
           {
-            const int64_t gmr = mb * BM + row;
+            const int64_t gmr = (int64_t)mb * BM + row;
             const int e = TRANS ? (int)*g.emax - kEBias : (gmr < g.M ? g.erow[gmr] : 0);
             double p1, p2;
             pow2_split(e, p1, p2);
@@ -720,12 +726,12 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
             for (int j = 0; j < NC; ++j) stg[row * LDS + c0 + j] = acc[j];
             asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
             for (int r = warp - 4; r < BM; r += EPI_WARPS) {
-              const int64_t grow = mb * BM + r;
+              const int64_t grow = (int64_t)mb * BM + r;
               if (grow >= g.M) break;
               for (int j = lane; j < Nout; j += 32) Cout[grow * g.ldc + j] = stg[r * LDS + j];
             }
           } else {
-            const int64_t gm = mb * BM + row;
+            const int64_t gm = (int64_t)mb * BM + row;
             if (gm < g.M) {
               double* dsto = Cout + gm * g.ldc + c0;
 #pragma unroll
