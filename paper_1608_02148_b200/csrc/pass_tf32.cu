@@ -182,7 +182,9 @@ pass_tf32_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         hi.y = tf32_trunc(a.y); lo.y = tf32_rna(a.y - hi.y);
         hi.z = tf32_trunc(a.z); lo.z = tf32_rna(a.z - hi.z);
         hi.w = tf32_trunc(a.w); lo.w = tf32_rna(a.w - hi.w);
-        a4[q] = hi;
+#ifdef TF32_STORE_HI
+        a4[q] = hi;                                   // (kind::tf32 ignores the low 13 bits anyway)
+#endif
         l4[q] = lo;
       }
       TF32_DEBUG_SPLIT
@@ -428,7 +430,9 @@ pass_tf32_tn_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         hi.y = tf32_trunc(a.y); lo.y = tf32_rna(a.y - hi.y);
         hi.z = tf32_trunc(a.z); lo.z = tf32_rna(a.z - hi.z);
         hi.w = tf32_trunc(a.w); lo.w = tf32_rna(a.w - hi.w);
-        a4[q] = hi;
+#ifdef TF32_STORE_HI
+        a4[q] = hi;                                   // (kind::tf32 ignores the low 13 bits anyway)
+#endif
         l4[q] = lo;
       }
       fence_proxy_async();
