@@ -111,7 +111,7 @@ struct rsvd_ctx {
   size_t ws_bytes = 0;
   char* ws2 = nullptr;            // TSQR stacks, LU / pivoted-QR scratch
   size_t ws2_bytes = 0;
-  int* flags_dev = nullptr;       // the call's status word (16 ints)
+  int* flags_dev = nullptr;       // the call's status word (16 ints); [64, 128): launch_tsqr_fused's words
   int* sticky_dev = nullptr;      // accumulated status for rsvd_sync (4 ints)
   int* flags_host = nullptr;      // pinned
   int* sweeps_dev = nullptr;
@@ -528,32 +528,34 @@ bool tsqr_levels(int64_t rows, int l, std::vector<int64_t>* leaves, size_t* stac
   return true;
 }
 
-// TSQR on the rows x l panel S (ld ld_s) on this device, every kernel predicated
-// by `pr`; R (l x l, ld l) to Rout.
-rsvd_status tsqr_local(rsvd_ctx* ctx, const Plan& p, double* S, int64_t ld_s, int64_t rows, double* Rout, Pred pr) {
+// TSQR on the rows x l panel S (ld ld_s) on this device, one predicated
+// cooperative launch (launch_tsqr_fused); R (l x l, ld l) to Rout, and also to
+// Rout2 (ld ldo2) if non-null.
+rsvd_status tsqr_local(rsvd_ctx* ctx, const Plan& p, double* S, int64_t ld_s, int64_t rows, double* Rout, Pred pr,
+                       double* Rout2 = nullptr, int64_t ldo2 = 0) {
   const int l = p.l;
   std::vector<int64_t> leaves;
   size_t need = 0;
   if (!tsqr_levels(rows, l, &leaves, &need))
     return fail(ctx, RSVD_EUNSUPPORTED, "TSQR cannot reduce %lld rows at l = %d", (long long)rows, l);
+  if ((int)leaves.size() > kTsqrMaxLev)
+    return fail(ctx, RSVD_EUNSUPPORTED, "TSQR of %lld rows needs more than %d levels", (long long)rows, kTsqrMaxLev);
   CKS(ensure_ws2(ctx, need + 256));
-  struct Lev { double* buf; int64_t ld, M, P; };
-  std::vector<Lev> levs;
+  TsqrArgs a = {};
   char* wp = ctx->ws2;
   double* cur = S;
   int64_t ld = ld_s, Mc = rows;
   for (const int64_t P : leaves) {
     double* stack = (double*)wp;
     wp += align256((size_t)P * l * l * 8);
-    CK(launch_hqr_leaves(cur, ld, Mc, l, P, stack, ctx->stream, pr));
-    levs.push_back({cur, ld, Mc, P});
+    a.lev[a.nlev++] = TsqrLevel{cur, ld, Mc, P};
     cur = stack; ld = l; Mc = P * l;
   }
-  CK(launch_hqr_leaves(cur, ld, Mc, l, 1, Rout, ctx->stream, pr));
-  for (int i = (int)levs.size() - 1; i >= 0; --i) {
-    const double* Sq = (i + 1 < (int)levs.size()) ? levs[i + 1].buf : cur;
-    CK(launch_tsqr_combine(levs[i].buf, levs[i].ld, levs[i].M, l, levs[i].P, Sq, l, ctx->stream, pr));
-  }
+  a.l = l;
+  a.cur = cur; a.ldc = ld; a.Mc = Mc;
+  a.R = Rout; a.Rout = Rout2; a.ldro = ldo2;
+  a.bar = reinterpret_cast<unsigned*>(ctx->flags_dev + 64);
+  CK(launch_tsqr_fused(a, ctx->num_sms, ctx->stream, pr));
   return RSVD_OK;
 }
 
@@ -573,11 +575,8 @@ rsvd_status orth_fallback(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool 
     }
     return RSVD_OK;
   }
+  if (!dist) return tsqr_local(ctx, p, S, Np, rows, p.Rsm, pr, Rout, Np);
   CKS(tsqr_local(ctx, p, S, Np, rows, p.Rsm, pr));
-  if (!dist) {
-    if (Rout) CK(launch_copy_out(p.Rsm, l, l, l, Rout, Np, false, nullptr, ctx->stream, pr));
-    return RSVD_OK;
-  }
   const int64_t srows = (int64_t)ctx->nranks * l;
   if ((size_t)srows * l > (size_t)std::max(p.M, p.n) * Np)
     return fail(ctx, RSVD_EUNSUPPORTED, "too many ranks for the robust panel QR workspace");
@@ -844,8 +843,8 @@ rsvd_status rsvd_create(rsvd_ctx** out, int device, void* stream) {
   ctx->stream = (cudaStream_t)stream;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (e == cudaSuccess) e = cudaMalloc(&ctx->flags_dev, 32 * sizeof(int));
-  if (e == cudaSuccess) e = cudaMemset(ctx->flags_dev, 0, 32 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->flags_dev, 128 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(ctx->flags_dev, 0, 128 * sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->flags_host, 16 * sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->hbuf, 1024 * sizeof(double));
   if (e == cudaSuccess) { ctx->sweeps_dev = ctx->flags_dev + 8; ctx->sticky_dev = ctx->flags_dev + 16; }

@@ -133,6 +133,24 @@ cudaError_t launch_hqr_leaves(double* Y, int64_t ldy, int64_t M, int l, int64_t 
 cudaError_t launch_tsqr_combine(double* Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
                                 const double* S, int64_t lds, cudaStream_t st, Pred pr = Pred{});
 
+// The whole local TSQR of an M x l panel in one cooperative launch (panel.cu):
+// level i reduces lev[i].buf (lev[i].M rows, ld lev[i].ld) in lev[i].P leaves,
+// stacking their R factors in lev[i+1].buf (cur for the last level, ld l);
+// the final leaf factors cur (Mc rows, ld ldc) into R (l x l, ld l), copied to
+// Rout (ld ldro) if non-null; then Q is formed downwards in every level's buf.
+// bar: 2 kTsqrMaxLev + 2 device words, zero before the first launch; the
+// kernel leaves them zero (ticket + per-phase completion counters).
+constexpr int kTsqrMaxLev = 24;
+struct TsqrLevel { double* buf; int64_t ld, M, P; };
+struct TsqrArgs {
+  TsqrLevel lev[kTsqrMaxLev];
+  int nlev, l;
+  double* cur; int64_t ldc, Mc;
+  double* R; double* Rout; int64_t ldro;
+  unsigned* bar;
+};
+cudaError_t launch_tsqr_fused(const TsqrArgs& a, int num_sms, cudaStream_t st, Pred pr = Pred{});
+
 // One-sided Jacobi SVD of X = R^T (R upper l x l, ld ldr): X J = W Sigma (jacobi.cu).
 // Outputs: sigma (l, descending), W (ldo x ldo) = U~, J (ldo x ldo), zero outside
 // their leading l x l blocks (l <= ldo <= 128).

@@ -308,14 +308,11 @@ int leaf_rows_cap(int l) {
   return (int)(avail / l);
 }
 
-__global__ void __launch_bounds__(HQR_THREADS) hqr_leaves_kernel(double* __restrict__ Y, int64_t ldy,
-                                                                 int64_t M, int l, int64_t nleaves,
-                                                                 double* __restrict__ Rstack, Pred pr) {
-  pdl_wait();
-  pdl_trigger();
-  if (pred_skip(pr)) return;
+// Householder QR of leaf `leaf` of the M x l panel Y (nleaves near-equal row
+// blocks): R (diag >= 0) to Rstack + leaf l^2, the explicit Q over the leaf's rows.
+__device__ void hqr_leaf(double* __restrict__ Y, int64_t ldy, int64_t M, int l, int64_t nleaves, int64_t leaf,
+                         double* __restrict__ Rstack) {
   extern __shared__ double sm[];
-  const int64_t leaf = blockIdx.x;
   const int64_t rb = M / nleaves, rem = M % nleaves;
   const int b = (int)(rb + (leaf < rem ? 1 : 0));
   const int64_t r0 = leaf * rb + (leaf < rem ? leaf : rem);
@@ -415,6 +412,16 @@ __global__ void __launch_bounds__(HQR_THREADS) hqr_leaves_kernel(double* __restr
     const int r = (int)(e / l), c = (int)(e % l);
     Y[(r0 + r) * ldy + c] = w(c) * Ys[(int64_t)c * b + r];
   }
+  __syncthreads();   // the shared buffers are reused by the caller's next leaf
+}
+
+__global__ void __launch_bounds__(HQR_THREADS) hqr_leaves_kernel(double* __restrict__ Y, int64_t ldy,
+                                                                 int64_t M, int l, int64_t nleaves,
+                                                                 double* __restrict__ Rstack, Pred pr) {
+  pdl_wait();
+  pdl_trigger();
+  if (pred_skip(pr)) return;
+  hqr_leaf(Y, ldy, M, l, nleaves, blockIdx.x, Rstack);
 }
 
 cudaError_t launch_hqr_leaves(double* Y, int64_t ldy, int64_t M, int l, int64_t nleaves, double* Rstack,
@@ -430,15 +437,12 @@ cudaError_t launch_hqr_leaves(double* Y, int64_t ldy, int64_t M, int l, int64_t 
   return cudaGetLastError();
 }
 
-__global__ void tsqr_combine_kernel(double* __restrict__ Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
-                                    const double* __restrict__ S, int64_t lds, Pred pr) {
-  pdl_wait();
-  pdl_trigger();
-  if (pred_skip(pr)) return;
+// Q rows of leaf `leaf` <- Q rows * S_leaf (S_leaf = rows [leaf l, leaf l + l) of S)
+__device__ void tsqr_combine_leaf(double* __restrict__ Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
+                                  int64_t leaf, const double* __restrict__ S, int64_t lds) {
   extern __shared__ double sm[];
   double* Ss = sm;                 // l x l
   double* rows = Ss + l * l;       // 16 x l
-  const int64_t leaf = blockIdx.x;
   const int64_t rb = M / nleaves, rem = M % nleaves;
   const int b = (int)(rb + (leaf < rem ? 1 : 0));
   const int64_t r0 = leaf * rb + (leaf < rem ? leaf : rem);
@@ -456,6 +460,15 @@ __global__ void tsqr_combine_kernel(double* __restrict__ Y, int64_t ldy, int64_t
       Y[(r0 + rc + r) * ldy + c] = s;
     }
   }
+  __syncthreads();
+}
+
+__global__ void tsqr_combine_kernel(double* __restrict__ Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
+                                    const double* __restrict__ S, int64_t lds, Pred pr) {
+  pdl_wait();
+  pdl_trigger();
+  if (pred_skip(pr)) return;
+  tsqr_combine_leaf(Y, ldy, M, l, nleaves, blockIdx.x, S, lds);
 }
 
 cudaError_t launch_tsqr_combine(double* Y, int64_t ldy, int64_t M, int l, int64_t nleaves, const double* S,
@@ -465,6 +478,107 @@ cudaError_t launch_tsqr_combine(double* Y, int64_t ldy, int64_t M, int l, int64_
   if (e != cudaSuccess) return e;
   e = launch_pdl(tsqr_combine_kernel, dim3((unsigned)nleaves), dim3(512), smem, st, Y, ldy, M, l, nleaves, S, lds, pr);
   if (e != cudaSuccess) return e;
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ whole TSQR, one launch
+// The complete local TSQR of launch_hqr_leaves / launch_tsqr_combine as ONE
+// persistent launch: the upward levels (Householder leaves, their R factors
+// stacked), the final leaf (R, also copied to Rout), the downward combines.  It
+// is the CholeskyQR breakdown fallback, so on the happy path it is enqueued
+// predicated and exits at once: one launch per orthonormalisation instead of
+// one per level.
+//
+// Scheduling without a co-residency assumption (no cooperative launch, which
+// serialises the stream): CTAs take work items from an atomic ticket in
+// dependency order -- level 0 leaves, level 1 leaves, ..., the final leaf, the
+// combines of level nlev-1 down to 0.  An item waits only for the completion
+// counter of the phase before it, whose items hold lower tickets and so are
+// owned by CTAs already running: progress never depends on a CTA that has not
+// started.  Every CTA ends with one failed fetch; the last of those (all work
+// done, nobody waiting) returns the ticket and counters to zero.
+// Words: bar[0] ticket, bar[1 + ph] completion count of phase ph.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(HQR_THREADS, 1) tsqr_fused_kernel(TsqrArgs a, Pred pr) {
+  pdl_wait();
+  if (pred_skip(pr)) return;
+  __shared__ int64_t s_item;
+  const int l = a.l, L = a.nlev;
+  // phases: 0..L-1 leaves of level i; L the final leaf; L+1+j combines of level L-1-j
+  int64_t total = 1;
+  for (int i = 0; i < L; ++i) total += 2 * a.lev[i].P;
+  unsigned* ticket = a.bar;
+  unsigned* done = a.bar + 1;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = (int64_t)atomicAdd(ticket, 1u);
+    __syncthreads();
+    int64_t t = s_item;
+    __syncthreads();
+    if (t >= total) {
+      if (threadIdx.x == 0 && t == total + gridDim.x - 1) {   // the last CTA to leave
+        for (int ph = 0; ph < 2 * L + 1; ++ph) done[ph] = 0u;
+        *ticket = 0u;
+        __threadfence();
+      }
+      return;
+    }
+    int ph = 0;
+    int64_t idx = t;
+    for (; ph < L && idx >= a.lev[ph].P; ++ph) idx -= a.lev[ph].P;
+    if (ph == L && idx >= 1) {
+      idx -= 1;
+      ph = L + 1;
+      while (idx >= a.lev[2 * L - ph].P) { idx -= a.lev[2 * L - ph].P; ++ph; }
+    }
+    // wait for the phase this one reads
+    if (ph > 0 && threadIdx.x == 0) {
+      const unsigned need = (ph <= L) ? (unsigned)a.lev[ph - 1].P                    // leaves / final leaf
+                                      : (ph == L + 1 ? 1u : (unsigned)a.lev[2 * L - ph + 1].P);   // combines
+      while (ld_acquire_u32(done + ph - 1) < need) __nanosleep(128);
+    }
+    __syncthreads();
+    if (ph < L) {
+      const TsqrLevel& V = a.lev[ph];
+      hqr_leaf(V.buf, V.ld, V.M, l, V.P, idx, (ph + 1 < L) ? a.lev[ph + 1].buf : a.cur);
+    } else if (ph == L) {
+      hqr_leaf(a.cur, a.ldc, a.Mc, l, 1, 0, a.R);
+      if (a.Rout)
+        for (int e = threadIdx.x; e < l * l; e += blockDim.x) a.Rout[(int64_t)(e / l) * a.ldro + e % l] = a.R[e];
+      __syncthreads();
+    } else {
+      const int i = 2 * L - ph;
+      const TsqrLevel& V = a.lev[i];
+      tsqr_combine_leaf(V.buf, V.ld, V.M, l, V.P, idx, (i + 1 < L) ? a.lev[i + 1].buf : a.cur, l);
+    }
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(done + ph, 1u);
+    }
+  }
+}
+
+cudaError_t launch_tsqr_fused(const TsqrArgs& a, int num_sms, cudaStream_t st, Pred pr) {
+  const int l = a.l;
+  size_t smem = ((size_t)a.Mc * l + l + 32) * sizeof(double);
+  int64_t pmax = 1;
+  for (int i = 0; i < a.nlev; ++i) {
+    const int64_t bmax = ceil_div(a.lev[i].M, a.lev[i].P);
+    if (bmax < l) return cudaErrorInvalidValue;
+    smem = std::max(smem, ((size_t)bmax * l + l + 32) * sizeof(double));
+    pmax = std::max(pmax, a.lev[i].P);
+  }
+  smem = std::max(smem, ((size_t)l * l + 16 * (size_t)l) * sizeof(double));
+  if (smem > (size_t)SMEM_OPTIN || a.nlev > kTsqrMaxLev || a.Mc < l || pmax >= (int64_t)1 << 30)
+    return cudaErrorInvalidValue;
+  CUDA_TRY(set_smem((const void*)tsqr_fused_kernel, smem));
+  const int grid = (int)std::min<int64_t>(pmax, num_sms);
+  CUDA_TRY(launch_pdl(tsqr_fused_kernel, dim3((unsigned)grid), dim3(HQR_THREADS), smem, st, a, pr));
   ++g_kernel_launches;
   return cudaGetLastError();
 }

@@ -223,6 +223,30 @@ def test_rsvd_rank_deficient_large_panel(rb):
     _check_parity(An, r, o, 5)
 
 
+@pytest.mark.timeout(300)
+def test_rsvd_fallback_many_leaves_and_concurrent(rb):
+    """The single-launch TSQR fallback with more leaves than SMs (200000 rows at
+    l = 120: ~830 leaves, ~10 levels, grid-stride over the leaves) on an exactly
+    rank-12 input, and two contexts on two streams running it at the same time
+    (ticket-ordered work items: no wait depends on a CTA that is not running).
+    Exact rank 12 < l: the top 12 singular values are the generator's."""
+    s = torch.as_tensor(2.0 ** -np.arange(12.0))
+    A, _ = synthetic.lowrank(200000, 300, s, seed=21)
+    Ad = A.cuda()
+    ctxs = [rb.Context(0, torch.cuda.Stream()) for _ in range(2)]
+    ref = rb.rsvd(Ad, 100, p=20, q=1, seed=3, ctx=ctxs[0])
+    assert ctxs[0].stats()["tsqr_fallback"]
+    d = _np(ref.d)
+    assert np.max(np.abs(d[:12] - s.numpy()) / s.numpy()) < 1e-11
+    u = _np(ref.u)[:, :12]
+    assert np.abs(u.T @ u - np.eye(12)).max() < 1e-12
+    outs = [rb.rsvd(Ad, 100, p=20, q=1, seed=3, ctx=c, sync=False) for c in ctxs]
+    for c in ctxs:
+        c.sync()
+    for o in outs:
+        assert torch.equal(o.d, ref.d) and torch.equal(o.u, ref.u)
+
+
 def test_rsvd_deterministic(rb):
     A = _decay_matrix(2000, 500, seed=1).cuda()
     r1 = rb.rsvd(A, 20, seed=5)
