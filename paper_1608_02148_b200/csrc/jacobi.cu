@@ -22,12 +22,16 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include <atomic>
 
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef JB_PROBE
+#define JB_PROBE(slot)                              // probe builds: per-phase cycles of a block round (tools/bench_jacobi)
+#endif
 #ifndef JAC_PROBE
 #define JAC_PROBE_DECL
 #define JAC_PROBE(slot)
@@ -337,6 +341,324 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
   }
 }
 
+// ------------------------------------------------------------------ block ordering
+// The same one-sided Jacobi (rotation formula, threshold, stopping rule, sweep
+// cap) in a block-cyclic order built for one SM's register file.  Columns form
+// NB blocks of B (B = 8 for l > 64, else 4; NB even, padding columns are zero
+// and never rotate).  A sweep is NB block steps: step 0 pairs blocks (2w,
+// 2w+1) and rotates the pairs inside each block (B - 1 round-robin rounds, the
+// B-th round logs identities); step s >= 1 pairs the blocks by a closed-form
+// round-robin tournament (block 0 fixed) and rotates the B^2 cross pairs in B
+// rounds of B disjoint pairs.  Warp w holds its two blocks (2B columns, rows
+// lane + 32e) in registers for the whole step: a round's B dot-product triples
+// are reduce-scattered by shuffles so that lanes 4j.. (B = 8) own pair j's
+// (alpha, beta, gamma), compute its rotation, and broadcast (c, s) to the warp.
+// Shared memory is touched once per block step (load / store of the blocks)
+// and the CTA synchronises once per block step (NB per sweep, not L - 1).
+// Every pair of columns meets once per sweep, as in the cyclic order.
+namespace {
+int blk_B(int l) {
+  static const int force = getenv("RSVD_JACOBI_B") ? atoi(getenv("RSVD_JACOBI_B")) : 0;   // A/B probes
+  if (force == 8 || (force == 4 && l <= 64)) return force;
+  return l > 64 ? 8 : 4;
+}
+__host__ __device__ inline int blk_NB(int l, int B) {
+  int nb = (l + B - 1) / B;
+  if (nb < 2) nb = 2;
+  return nb + (nb & 1);
+}
+// blocks (I, J) of warp w at block step s of a sweep
+__host__ __device__ inline void blk_blocks(int NB, int s, int w, int& I, int& J) {
+  if (s == 0) { I = 2 * w; J = 2 * w + 1; return; }
+  const int m = NB - 1, r = s - 1;
+  if (w == 0) { I = 0; J = r + 1; }
+  else { I = (r + w) % m + 1; J = (r - w + m) % m + 1; }
+}
+// local columns (0..2B-1) of pair j in round rho: cross steps (j, B + (j + rho) % B);
+// the intra step pairs within each block by round robin (block 0 fixed), its
+// last round repeats round 0 (identity rotations)
+__host__ __device__ constexpr int blk_lp(int B, bool intra, int rho, int j) {
+  return !intra ? j
+                : ((j < B / 2 ? 0 : B) + ((j % (B / 2)) == 0 ? 0 : ((rho % (B - 1)) + (j % (B / 2))) % (B - 1) + 1));
+}
+__host__ __device__ constexpr int blk_lq(int B, bool intra, int rho, int j) {
+  return !intra ? B + (j + rho) % B
+                : ((j < B / 2 ? 0 : B) +
+                   ((j % (B / 2)) == 0 ? (rho % (B - 1)) + 1
+                                       : ((rho % (B - 1)) - (j % (B / 2)) + (B - 1)) % (B - 1) + 1));
+}
+}  // namespace
+
+size_t jacobi_blk_log_bytes(int l) {   // either block size
+  size_t mx = 0;
+  for (int B : {4, 8}) {
+    const int NB = blk_NB(l, B);
+    mx = std::max(mx, (size_t)31 * NB * B * (NB / 2) * B * sizeof(double2));
+  }
+  return mx;
+}
+
+constexpr int JB_CHS = 2;   // block steps per published / replayed chunk
+
+// J replay for the block order: one warp per row of J, the log applied chunk by chunk
+template <int B>
+__device__ void jacobi_blk_replay(const double2* __restrict__ rlog, const int* __restrict__ rank, int l, int NB,
+                                  double* __restrict__ Jo, int ldo, int row0, const unsigned long long* prog,
+                                  const unsigned long long* done, unsigned epoch, unsigned char* sm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nt = blockDim.x;
+  const int i = row0 + warp;
+  const int W = NB / 2, NC = NB * B, per_step = B * W * B;
+  double2* buf = reinterpret_cast<double2*>(sm);                         // [JB_CHS * per_step]
+  double* row = reinterpret_cast<double*>(sm + (size_t)JB_CHS * per_step * sizeof(double2)) + warp * (NC + 1);
+  for (int p = lane; p < NC; p += 32) row[p] = (p == i) ? 1.0 : 0.0;
+  __shared__ long long s_avail;
+  __shared__ int s_fin;
+  for (int64_t ch = 0;; ++ch) {
+    if (threadIdx.x == 0) {
+      long long avail = -1;
+      int fin = 0;
+      for (;;) {
+        const unsigned long long d = ld_acquire_u64(done);
+        if ((unsigned)(d >> 32) == epoch) { avail = (long long)(d & 0xffffffffu); fin = 1; break; }
+        const unsigned long long pg = ld_acquire_u64(prog);
+        if ((unsigned)(pg >> 32) == epoch && (long long)(pg & 0xffffffffu) >= (ch + 1) * JB_CHS) {
+          avail = (long long)(pg & 0xffffffffu);
+          break;
+        }
+        __nanosleep(256);
+      }
+      s_avail = avail;
+      s_fin = fin;
+    }
+    __syncthreads();
+    const long long avail = s_avail;
+    const int fin = s_fin;
+    const int64_t g0 = ch * JB_CHS;
+    if (g0 >= avail) {
+      if (fin) break;
+      continue;
+    }
+    const int nst = (int)min((int64_t)JB_CHS, (int64_t)avail - g0);
+    for (int e = threadIdx.x; e < nst * per_step; e += nt) buf[e] = __ldcg(rlog + g0 * per_step + e);
+    __syncthreads();
+    for (int st = 0; st < nst; ++st) {
+      const int s = (int)((g0 + st) % NB);
+      for (int rho = 0; rho < B; ++rho) {
+        for (int k = lane; k < W * B; k += 32) {
+          const int w = k / B, j = k - w * B;
+          int I, J;
+          blk_blocks(NB, s, w, I, J);
+          const int lp = blk_lp(B, s == 0, rho, j), lq = blk_lq(B, s == 0, rho, j);
+          const int p = lp < B ? I * B + lp : J * B + lp - B;
+          const int q = lq < B ? I * B + lq : J * B + lq - B;
+          const double2 cs = buf[(st * B + rho) * W * B + k];
+          const double u = row[p], v = row[q];
+          row[p] = cs.x * u - cs.y * v;
+          row[q] = cs.y * u + cs.x * v;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();                                   // buf reused by the next chunk
+  }
+  if (i < l) {
+    for (int p = lane; p < l; p += 32) Jo[i * ldo + __ldcg(rank + p)] = row[p];
+    for (int c = l + lane; c < ldo; c += 32) Jo[i * ldo + c] = 0.0;
+  } else if (i < ldo) {
+    for (int c = lane; c < ldo; c += 32) Jo[i * ldo + c] = 0.0;
+  }
+}
+
+// one round of B disjoint pairs on the warp's registers x[2B][RPL]: the B
+// dot-product triples are reduce-scattered by shuffles so that lane group j
+// (lanes j G .. j G + G - 1, G = 32 / B) holds pair j's (alpha, beta, gamma),
+// computes its rotation and broadcasts (c, s) to the warp.  (A shared-memory
+// reduction / broadcast was measured slower: tools/bench_jacobi.)
+template <int B, int RPL, bool INTRA, int RHO>
+__device__ __forceinline__ void blk_round(double (&x)[2 * B][RPL], int lane, double tol2, bool& rot,
+                                          double2* __restrict__ logp) {
+  constexpr int LB = B == 8 ? 3 : 2;
+  JB_PROBE(0)
+  double v[3][B];
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    const int p = blk_lp(B, INTRA, RHO, j), q = blk_lq(B, INTRA, RHO, j);
+    double a = 0.0, b = 0.0, g = 0.0;
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) {
+      a = fma(x[p][e], x[p][e], a);
+      b = fma(x[q][e], x[q][e], b);
+      g = fma(x[p][e], x[q][e], g);
+    }
+    v[0][j] = a; v[1][j] = b; v[2][j] = g;
+  }
+  JB_PROBE(1)
+  // reduce-scatter over lane bits 4 .. 5 - LB: lane keeps the pair j = lane >> (5 - LB)
+#pragma unroll
+  for (int k = 0; k < LB; ++k) {
+    const int h = (B >> k) / 2;
+    const bool up = (lane >> (4 - k)) & 1;
+#pragma unroll
+    for (int qv = 0; qv < 3; ++qv)
+#pragma unroll
+      for (int i2 = 0; i2 < h; ++i2) {
+        const double send = up ? v[qv][i2] : v[qv][i2 + h];
+        const double keep = up ? v[qv][i2 + h] : v[qv][i2];
+        v[qv][i2] = keep + __shfl_xor_sync(0xffffffffu, send, 16 >> k);
+      }
+  }
+#pragma unroll
+  for (int o = 16 >> LB; o > 0; o >>= 1) {
+    v[0][0] += __shfl_xor_sync(0xffffffffu, v[0][0], o);
+    v[1][0] += __shfl_xor_sync(0xffffffffu, v[1][0], o);
+    v[2][0] += __shfl_xor_sync(0xffffffffu, v[2][0], o);
+  }
+  JB_PROBE(2)
+  double c = 1.0, sn = 0.0;
+  const double al = v[0][0], be = v[1][0], ga = v[2][0];
+  const bool doit = !(INTRA && RHO == B - 1) && ga * ga > tol2 * (al * be);
+  if (doit) jac_rot(al, be, ga, c, sn);
+  JB_PROBE(3)
+  rot |= __any_sync(0xffffffffu, doit);
+  if ((lane & ((32 >> LB) - 1)) == 0) logp[lane >> (5 - LB)] = make_double2(c, sn);
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    const int p = blk_lp(B, INTRA, RHO, j), q = blk_lq(B, INTRA, RHO, j);
+    const double cj = __shfl_sync(0xffffffffu, c, j << (5 - LB));
+    const double sj = __shfl_sync(0xffffffffu, sn, j << (5 - LB));
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) {
+      const double u = x[p][e], w = x[q][e];
+      x[p][e] = cj * u - sj * w;
+      x[q][e] = sj * u + cj * w;
+    }
+  }
+  JB_PROBE(4)
+}
+
+template <int B, int RPL, bool INTRA, int RHO>
+struct BlkRounds {
+  __device__ __forceinline__ static void run(double (&x)[2 * B][RPL], int lane, double tol2, bool& rot,
+                                             double2* logp, int stride) {
+    blk_round<B, RPL, INTRA, RHO>(x, lane, tol2, rot, logp);
+    BlkRounds<B, RPL, INTRA, RHO + 1>::run(x, lane, tol2, rot, logp + stride, stride);
+  }
+};
+template <int B, int RPL, bool INTRA>
+struct BlkRounds<B, RPL, INTRA, B> {
+  __device__ __forceinline__ static void run(double (&)[2 * B][RPL], int, double, bool&, double2*, int) {}
+};
+
+template <int B, int RPL>
+__global__ void __launch_bounds__(256, 1)
+jacobi_blk_kernel(const double* __restrict__ R, int ldr, int l, int NB, double* __restrict__ sigma,
+                  double* __restrict__ Wo, int ldo, double2* __restrict__ rlog, int* __restrict__ rank_out, int* flag,
+                  int* sweeps_out, double* __restrict__ Jo, unsigned long long* prog, unsigned long long* done,
+                  unsigned epoch) {
+  pdl_wait();
+  pdl_trigger();
+  if (blockIdx.x > 0) {                                  // J-replay CTAs
+    extern __shared__ __align__(16) unsigned char jsm[];
+    jacobi_blk_replay<B>(rlog, rank_out, l, NB, Jo, ldo, (blockIdx.x - 1) * (int)(blockDim.x >> 5), prog, done,
+                         epoch, jsm);
+    return;
+  }
+  extern __shared__ __align__(16) double Xs[];           // NC columns x LDX rows (column p: Xs + p * LDX)
+  constexpr int LDX = 32 * RPL;
+  const int NC = NB * B, W = NB / 2;
+  __shared__ int rotated, bad;
+  __shared__ double sg[128];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) { rotated = 0; bad = 0; }
+  __syncthreads();
+  // X = R^T: column p of X = row p of R (entries i >= p); rows / columns >= l are zero
+  for (int e0 = tid; e0 < NC * LDX; e0 += 8 * nt) {
+    double v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = e0 + r * nt, p = e / LDX, i = e - p * LDX;
+      v[r] = (e < NC * LDX && p < l && i < l && i >= p) ? R[p * ldr + i] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = e0 + r * nt;
+      if (e < NC * LDX) {
+        if (!isfinite(v[r])) bad = 1;
+        Xs[e] = v[r];
+      }
+    }
+  }
+  __syncthreads();
+  const double tol = (double)l * 0x1.0p-52, tol2 = tol * tol;
+  const int per_step = B * W * B;
+  int sweeps = 0;
+  bool converged = bad != 0;
+  int64_t gstep = 0;
+  for (int sweep = 0; sweep <= 30 && !converged; ++sweep) {
+    bool rot = false;
+    for (int s = 0; s < NB; ++s, ++gstep) {
+      int I, J;
+      blk_blocks(NB, s, warp, I, J);
+      double x[2 * B][RPL];
+#pragma unroll
+      for (int c = 0; c < 2 * B; ++c)
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) x[c][e] = Xs[((c < B ? I * B + c : J * B + c - B)) * LDX + lane + 32 * e];
+      double2* logp = rlog + gstep * per_step + warp * B;
+      if (s == 0) BlkRounds<B, RPL, true, 0>::run(x, lane, tol2, rot, logp, W * B);
+      else BlkRounds<B, RPL, false, 0>::run(x, lane, tol2, rot, logp, W * B);
+#pragma unroll
+      for (int c = 0; c < 2 * B; ++c)
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) Xs[((c < B ? I * B + c : J * B + c - B)) * LDX + lane + 32 * e] = x[c][e];
+      __syncthreads();                                   // blocks published for the next step
+      if (tid == 0 && ((gstep + 1) % JB_CHS) == 0) {
+        __threadfence();
+        st_release_u64(prog, ((unsigned long long)epoch << 32) | (unsigned long long)(gstep + 1));
+      }
+    }
+    if (rot && lane == 0) rotated = 1;
+    __syncthreads();
+    const bool any = rotated != 0;
+    __syncthreads();
+    if (tid == 0) rotated = 0;
+    if (!any) converged = true;
+    else ++sweeps;
+  }
+  // sigma_p = ||x_p||, stable descending ranks, W(:, rank) = x_p / sigma_p
+  const int nw = nt >> 5;
+  for (int p = warp; p < l; p += nw) {
+    double s2 = 0.0;
+    for (int i = lane; i < l; i += 32) s2 = fma(Xs[p * LDX + i], Xs[p * LDX + i], s2);
+    s2 = warp_sum(s2);
+    if (lane == 0) sg[p] = sqrt(s2);
+  }
+  __syncthreads();
+  for (int p = warp; p < l; p += nw) {
+    int rk = 0;
+    const double sp = sg[p];
+    for (int q = lane; q < l; q += 32) rk += (sg[q] > sp) || (sg[q] == sp && q < p);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
+    if (lane == 0) { sigma[rk] = sp; rank_out[p] = rk; }
+    const double inv = sp > 0.0 ? 1.0 / sp : 1.0;
+    for (int i = lane; i < l; i += 32) Wo[i * ldo + rk] = Xs[p * LDX + i] * inv;
+  }
+  for (int e = tid; e < ldo * ldo; e += nt) {
+    const int i = e / ldo, c = e - (e / ldo) * ldo;
+    if (i >= l || c >= l) Wo[e] = 0.0;
+  }
+  __syncthreads();                                     // rank_out complete
+  if (tid == 0) {
+    if (!converged) atomicOr(flag, 2);
+    if (bad) atomicOr(flag, 4);
+    if (sweeps_out) *sweeps_out = sweeps;
+    rank_out[128] = sweeps;
+    __threadfence();
+    st_release_u64(done, ((unsigned long long)epoch << 32) | (unsigned long long)gstep);
+  }
+}
+
 int g_jacobi_lanes = 0;   // lanes per column pair (4, 8, 16; 0: 4 for L <= 64, else 8; tools/bench_jacobi)
 
 cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double* W, double* J, int ldo,
@@ -344,11 +666,41 @@ cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double
   if (l < 1 || l > 128 || ldo < l || ldo > 128) return cudaErrorInvalidValue;
   const int L = jac_L(l);
   double2* rlog = reinterpret_cast<double2*>(scratch);
-  int* rank = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + jacobi_log_bytes(l));
+  int* rank = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + std::max(jacobi_log_bytes(l), jacobi_blk_log_bytes(l)));
   unsigned long long* prog = reinterpret_cast<unsigned long long*>(rank + 192);   // 8-byte aligned, after rank[0..128]
   unsigned long long* done = prog + 1;
   static std::atomic<unsigned> epoch_ctr{0};   // unique per launch (the scratch is per context; threads may share the counter)
   const unsigned epoch = ++epoch_ctr;
+  // block order for l <= 32 and l > 64; the cyclic order (measured 2 % faster
+  // at l = 60 on config 2) in between.  RSVD_JACOBI_CYCLIC / _BLOCK force one (A/B).
+  static const bool force_cyc = getenv("RSVD_JACOBI_CYCLIC") != nullptr;
+  static const bool force_blk = getenv("RSVD_JACOBI_BLOCK") != nullptr;
+  const bool use_blk = force_blk || (!force_cyc && (l <= 32 || l > 64));
+  if (use_blk && g_jacobi_lanes == 0) {
+    const int B = blk_B(l), NB = blk_NB(l, B), nwp = NB / 2, NC = NB * B;
+    const int rpl = (l + 31) / 32;
+    const int threads = nwp * 32;
+    const size_t smem = std::max((size_t)NC * 32 * (rpl <= 1 ? 1 : rpl <= 2 ? 2 : 4) * sizeof(double),
+                                 (size_t)JB_CHS * B * nwp * B * sizeof(double2) + (size_t)nwp * (NC + 1) * sizeof(double));
+    const dim3 grid(1 + (unsigned)ceil_div(ldo, nwp));
+    cudaError_t e = cudaSuccess;
+#define RSVD_JB(BB, RP)                                                                                     \
+  {                                                                                                         \
+    e = smem_optin(jacobi_blk_kernel<BB, RP>);                                                              \
+    if (e != cudaSuccess) return e;                                                                         \
+    e = launch_pdl(jacobi_blk_kernel<BB, RP>, grid, dim3(threads), smem, st, R, ldr, l, NB, sigma, W, ldo, \
+                   rlog, rank, flag, sweeps, J, prog, done, epoch);                                         \
+  }
+    if (B == 8) {
+      if (rpl <= 2) RSVD_JB(8, 2) else RSVD_JB(8, 4)
+    } else {
+      if (rpl <= 1) RSVD_JB(4, 1) else RSVD_JB(4, 2)
+    }
+#undef RSVD_JB
+    if (e != cudaSuccess) return e;
+    ++g_kernel_launches;
+    return cudaGetLastError();
+  }
   const int JGv = g_jacobi_lanes ? g_jacobi_lanes : (L <= 64 ? 4 : 8);
   const int threads = (int)round_up((int64_t)(L / 2) * JGv, 32);
   const int epl_need = (l + JGv - 1) / JGv;
@@ -379,6 +731,8 @@ cudaError_t launch_jacobi(const double* R, int ldr, int l, double* sigma, double
   return cudaGetLastError();
 }
 
-size_t jacobi_scratch_bytes(int l) { return jacobi_log_bytes(l) + 256 * sizeof(int); }   // rank[129], prog, done
+size_t jacobi_scratch_bytes(int l) {   // rotation log (either order), rank[129], prog, done
+  return std::max(jacobi_log_bytes(l), jacobi_blk_log_bytes(l)) + 256 * sizeof(int);
+}
 
 }  // namespace rsvd

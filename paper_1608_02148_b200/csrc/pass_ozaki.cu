@@ -73,10 +73,22 @@ __host__ __device__ inline int64_t unit_lo(int64_t units, int grid, int c) { ret
 #define OZ_TL(slot) {}                              // probe builds: per-CTA timeline (tools/test_ozaki.cu)
 #endif
 
+// L2 policies of the loads (the CUTLASS CacheHintSm90 encodings): A's slices
+// are read once per pass (evict first, so the stream does not push X out),
+// X's slices by every row block (evict last).
+constexpr uint64_t kL2EvictFirst = 0x12F0000000000000ull, kL2EvictLast = 0x14F0000000000000ull;
+
 __device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
-      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)),
+        "l"(kL2EvictFirst)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d_keep(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(kL2EvictLast)
       : "memory");
 }
 // A-slice tile multicast into both CTAs of a 2-CTA cluster (same smem offset;
@@ -84,8 +96,9 @@ __device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c0
 __device__ __forceinline__ void tma_4d_mc(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar,
                                           uint16_t mask) {
   asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
-      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "h"(mask)
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7, %8;"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "h"(mask),
+        "l"(kL2EvictFirst)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
@@ -513,7 +526,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         }
         const CUtensorMap* mx = crank ? &mapX2 : &mapX;
 #ifndef OZ_NO_X_TMA
-        for (int t = 0; t < S; ++t) tma_2d(ubuf + S * A_UT + t * XSL, mx, (int)(kb * BKU), t * g.Np, &ufull[ub]);
+        for (int t = 0; t < S; ++t) tma_2d_keep(ubuf + S * A_UT + t * XSL, mx, (int)(kb * BKU), t * g.Np, &ufull[ub]);
 #endif
         OZ_PROBE2(2)
       }

@@ -13,7 +13,7 @@ __device__ long long g_cb[8];
 #define CB_PROBE(slot) if (threadIdx.x == 0) { long long _t = clock64(); _cbt[slot] += _t - _cbl; _cbl = _t; }
 #define CB_PROBE_OUT if (threadIdx.x == 0) { for (int q = 0; q < 5; ++q) atomicAdd((unsigned long long*)&g_cb[q], (unsigned long long)_cbt[q]); atomicAdd((unsigned long long*)&g_cb[5], (unsigned long long)(clock64() - _cb0)); }
 #include "../paper_1608_02148_b200/csrc/cholqr.cu"
-namespace rsvd { int64_t g_kernel_launches = 0; int g_pdl = 1; }
+namespace rsvd { std::atomic<int64_t> g_kernel_launches{0}; int g_pdl = 1; cudaError_t smem_optin_fn(const void* fn) { cudaFuncAttributes a; cudaError_t e = cudaFuncGetAttributes(&a, fn); if (e != cudaSuccess) return e; int o = 0; cudaDeviceGetAttribute(&o, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0); return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, o - (int)a.sharedSizeBytes); } }
 using namespace rsvd;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s @%d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
 

@@ -11,8 +11,11 @@ __device__ unsigned long long g_jp[6];
 #define JAC_PROBE_DECL long long _jt[5] = {0, 0, 0, 0, 0}; long long _jl = clock64();
 #define JAC_PROBE(slot) if (threadIdx.x == 0) { long long _t = clock64(); _jt[slot] += _t - _jl; _jl = _t; }
 #define JAC_PROBE_OUT if (threadIdx.x == 0) { for (int q = 0; q < 5; ++q) atomicAdd(&g_jp[q], (unsigned long long)_jt[q]); atomicAdd(&g_jp[5], (unsigned long long)gstep); }
+__device__ unsigned long long g_jb[8];
+__shared__ long long g_jbl;
+#define JB_PROBE(slot) if (blockIdx.x == 0 && threadIdx.x == 0) { const long long _t = clock64(); if (slot > 0) atomicAdd(&g_jb[slot - 1], (unsigned long long)(_t - g_jbl)); else atomicAdd(&g_jb[5], 1ull); g_jbl = _t; }
 #include "../paper_1608_02148_b200/csrc/jacobi.cu"
-namespace rsvd { int64_t g_kernel_launches = 0; int g_pdl = 1; }
+namespace rsvd { std::atomic<int64_t> g_kernel_launches{0}; int g_pdl = 1; cudaError_t smem_optin_fn(const void* fn) { cudaFuncAttributes a; cudaError_t e = cudaFuncGetAttributes(&a, fn); if (e != cudaSuccess) return e; int o = 0; cudaDeviceGetAttribute(&o, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0); return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, o - (int)a.sharedSizeBytes); } }
 using namespace rsvd;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s @%d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
 
@@ -23,7 +26,41 @@ template <typename F> float timeit(F f, int reps) {
   float ms; cudaEventElapsedTime(&ms, a, b); CK(cudaGetLastError()); return ms * 1000.f / reps;
 }
 
+// host check of the block order: per sweep every column pair meets exactly
+// once (the intra step's last round is the identity round) and the pairs of a
+// round (over all warps) are disjoint
+static bool check_block_order() {
+  bool ok = true;
+  for (int B : {4, 8})
+    for (int NB = 2; NB <= 16; NB += 2) {
+      const int NC = NB * B, W = NB / 2;
+      std::vector<int> met(NC * NC, 0);
+      for (int s = 0; s < NB; ++s)
+        for (int rho = 0; rho < B; ++rho) {
+          if (s == 0 && rho == B - 1) continue;
+          std::vector<int> used(NC, 0);
+          for (int w = 0; w < W; ++w) {
+            int I, J;
+            blk_blocks(NB, s, w, I, J);
+            for (int j = 0; j < B; ++j) {
+              const int lp = blk_lp(B, s == 0, rho, j), lq = blk_lq(B, s == 0, rho, j);
+              const int p = lp < B ? I * B + lp : J * B + lp - B, q = lq < B ? I * B + lq : J * B + lq - B;
+              if (p == q || used[p]++ || used[q]++) ok = false;
+              met[std::min(p, q) * NC + std::max(p, q)]++;
+            }
+          }
+        }
+      for (int p = 0; p < NC; ++p)
+        for (int q = p + 1; q < NC; ++q)
+          if (met[p * NC + q] != 1) ok = false;
+      if (!ok) { printf("block order FAILED at B %d NB %d\n", B, NB); return false; }
+    }
+  printf("block order: every pair once per sweep, rounds disjoint (B 4/8, NB 2..16)\n");
+  return ok;
+}
+
 int main(int argc, char** argv) {
+  if (!check_block_order()) return 1;
   const int only = argc > 1 ? atoi(argv[1]) : -1;
   int* flag; CK(cudaMalloc(&flag, 64));
   int* sw; CK(cudaMalloc(&sw, 64));
@@ -49,6 +86,14 @@ int main(int argc, char** argv) {
              pr[1] / st, pr[2] / st, pr[3] / st, pr[4] / st, pr[0] / st);
     }
     g_jacobi_lanes = 0;
+    {
+      unsigned long long z[8] = {0}; cudaMemcpyToSymbol(g_jb, z, sizeof z);
+      timeit([&] { launch_jacobi(dR, ld, l, sig, W, J, ld, flag, sw, scr, 0); }, 3);
+      unsigned long long pr[8]; cudaMemcpyFromSymbol(pr, g_jb, sizeof pr);
+      const double n = pr[5] ? (double)pr[5] : 1.0;
+      printf("    block order, cycles per round (warp 0): dots %.0f  reduce %.0f  rot %.0f  bcast+apply %.0f  | rounds %.0f\n",
+             pr[0] / n, pr[1] / n, pr[2] / n, pr[3] / n, n / 4);
+    }
     float t = timeit([&] { launch_jacobi(dR, ld, l, sig, W, J, ld, flag, sw, scr, 0); }, 10);
     int sweeps, fl;
     CK(cudaMemcpy(&sweeps, sw, 4, cudaMemcpyDeviceToHost)); CK(cudaMemcpy(&fl, flag, 4, cudaMemcpyDeviceToHost));
