@@ -243,8 +243,9 @@ ozaki_slice_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t m, in
 // transaction, the group's mbarrier), the group reduces max |f(a)| (shuffles +
 // a named barrier of the group only) and writes the digits from shared memory.
 // Groups never wait for each other, so copies and arithmetic overlap with up
-// to 32 warps per SM.  One HBM read of A.  Needs 16-byte aligned rows (lda and
-// n even) of at most SR_SMEM / 2 bytes.
+// to 32 warps per SM.  One HBM read of A.  The centring / scaling vectors (rpca)
+// are staged in shared memory too, in place of row buffers.  Needs 16-byte
+// aligned rows (lda and n even) and room for two row buffers.
 constexpr int SR_SMEM = 200 * 1024, SR_W = 4, SR_MAX_G = 8;
 template <int S>
 __global__ void __launch_bounds__(32 * SR_W * SR_MAX_G, 1)
@@ -265,6 +266,15 @@ ozaki_slice_rows_smem_kernel(const double* __restrict__ A, int64_t lda, int64_t 
   const uint32_t row_bytes = (uint32_t)(n * 8);
   const int64_t stride = (row_bytes + 127) / 128 * 16;          // doubles per group buffer (128-byte aligned)
   double* row = reinterpret_cast<double*>(srow_raw) + grp * stride;
+  // the centring / scaling vectors staged once behind the row buffers: with most
+  // of the SM's L1 given to shared memory they would otherwise come from L2 for
+  // every element (measured: the dominant stall of the centred config-3 slicing)
+  double* cs = reinterpret_cast<double*>(srow_raw) + ng * stride;
+  double* rss = cs + (c ? stride : 0);
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    if (c) cs[j] = c[j];
+    if (rs) rss[j] = rs[j];
+  }
   if (gt == 0) mbar_init(&full[grp], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
@@ -282,8 +292,8 @@ ozaki_slice_rows_smem_kernel(const double* __restrict__ A, int64_t lda, int64_t 
     double mx = 0.0;
     for (int64_t j = gt; j < n; j += GT) {
       double v = row[j];
-      if (c) v -= c[j];
-      if (rs) v *= rs[j];
+      if (c) v -= cs[j];
+      if (rs) v *= rss[j];
       if (!isfinite(v)) nf = true;
       mx = fmax(mx, fabs(v));
     }
@@ -302,15 +312,23 @@ ozaki_slice_rows_smem_kernel(const double* __restrict__ A, int64_t lda, int64_t 
     for (int64_t q = gt; q < nblk * 32; q += GT) {
       const int64_t blk = q >> 5;
       const int64_t j0 = blk * BKO + 4 * (q & 31);
-      double v[4];
+      // two 16-byte reads per thread (n even: a pair is wholly inside or outside
+      // the row); lanes with bit 2 set read their second half first, so each
+      // read instruction of the warp touches every bank group equally
+      const bool h0 = (q >> 2) & 1;
+      double2 a[2];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t jj = j0 + e;
-        double a = jj < n ? row[jj] : 0.0;
-        if (jj < n && c) a -= c[jj];
-        if (jj < n && rs) a *= rs[jj];
-        v[e] = a;
+      for (int hh = 0; hh < 2; ++hh) {
+        const int64_t jj = j0 + 2 * (hh ^ (int)h0);
+        a[hh] = make_double2(0.0, 0.0);
+        if (jj < n) {
+          a[hh] = *reinterpret_cast<const double2*>(row + jj);
+          if (c) { const double2 cc = *reinterpret_cast<const double2*>(cs + jj); a[hh].x -= cc.x; a[hh].y -= cc.y; }
+          if (rs) { const double2 rr = *reinterpret_cast<const double2*>(rss + jj); a[hh].x *= rr.x; a[hh].y *= rr.y; }
+        }
       }
+      const double2 lo = h0 ? a[1] : a[0], hi = h0 ? a[0] : a[1];
+      double v[4] = {lo.x, lo.y, hi.x, hi.y};
       uint32_t w[S];
       digits_a4<S>(v, s1, s2, w);
       int8_t* dst = slices + ((r * nblk + blk) * S) * BKO + 4 * (q & 31);
@@ -830,13 +848,14 @@ cudaError_t ozaki_slice_a(const OzakiA& a, const double* A, int64_t lda, const d
   if (e != cudaSuccess) return e;
   // shared-memory staged rows (one buffer per warp, bulk copies) when 16-byte aligned rows fit
   const int64_t rbuf = (a.n * 8 + 127) / 128 * 128;
-  const int ngroups = (int)std::min<int64_t>(oz::SR_MAX_G, oz::SR_SMEM / rbuf);
+  const int64_t vecs = (int64_t)(c != nullptr) + (rs != nullptr);          // staged c / rs, rbuf bytes each
+  const int ngroups = (int)std::max<int64_t>(0, std::min<int64_t>(oz::SR_MAX_G, (oz::SR_SMEM - vecs * rbuf) / rbuf));
   if (ngroups >= 2 && (a.n % 2 == 0) && (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0)) {
     e = smem_optin(oz::ozaki_slice_rows_smem_kernel<OZ_S>);
     if (e != cudaSuccess) return e;
     e = launch_plain(oz::ozaki_slice_rows_smem_kernel<OZ_S>,
                      dim3((unsigned)std::min<int64_t>(ceil_div(a.m, (int64_t)ngroups), 148)),
-                     dim3(32 * oz::SR_W * ngroups), (size_t)ngroups * rbuf, st, A, lda, a.m, a.n, c, rs, a.slices,
+                     dim3(32 * oz::SR_W * ngroups), (size_t)(ngroups + vecs) * rbuf, st, A, lda, a.m, a.n, c, rs, a.slices,
                      a.ldn, a.erow, a.emax, flag);
     if (e != cudaSuccess) return e;
     ++g_kernel_launches;
