@@ -52,6 +52,33 @@ __global__ void __launch_bounds__(128, 1) burst(int iters, unsigned long long* s
   }
 }
 
+// back-to-back launches for ~secs seconds (clocks settle under the power
+// limit): the sustained figure for kernels timed inside long steps
+template <int KIND>
+static double run_sustained(int nsm, int iters, double secs) {
+  unsigned long long* sink;
+  cudaMalloc(&sink, 8);
+  cudaFuncSetAttribute(burst<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  burst<KIND><<<nsm, 128, 100 * 1024>>>(iters, sink);
+  cudaEventRecord(e0);
+  cudaEventSynchronize(e0);
+  long long launches = 0;
+  float ms = 0.f;
+  while (ms < secs * 1e3) {
+    for (int r = 0; r < 20; ++r) burst<KIND><<<nsm, 128, 100 * 1024>>>(iters, sink);
+    launches += 20;
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+  }
+  cudaFree(sink);
+  const int K = KIND == 0 ? 32 : (KIND == 1 ? 8 : 16);
+  return 2.0 * 128 * 256 * K * (double)iters * nsm * launches / (ms * 1e-3) / 1e12;
+}
+
 template <int KIND>
 static double run(int nsm, int iters) {
   unsigned long long* sink;
@@ -83,7 +110,10 @@ int main() {
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   const int iters = 200000;
   const double i8 = run<0>(nsm, iters), tf32 = run<1>(nsm, iters), bf16 = run<2>(nsm, iters);
-  printf("{\"tcgen05_i8_tops\": %.1f, \"tcgen05_tf32_tflops\": %.1f, \"tcgen05_bf16_tflops\": %.1f, "
+  const double i8s = run_sustained<0>(nsm, iters / 4, 4.0), tf32s = run_sustained<1>(nsm, iters / 4, 4.0);
+  printf("{\"tcgen05_i8_tops_sustained\": %.1f, \"tcgen05_tf32_tflops_sustained\": %.1f, "
+         "\"sustained_how\": \"back-to-back launches for 4 s\", ", i8s, tf32s);
+  printf("\"tcgen05_i8_tops\": %.1f, \"tcgen05_tf32_tflops\": %.1f, \"tcgen05_bf16_tflops\": %.1f, "
          "\"tc_peaks_how\": \"tools/peaks_tc.cu: %d CTAs x back-to-back cta_group::1 M=128 N=256 SS MMAs (%d each), "
          "best of 5 CUDA-event timings, dense\", \"sms\": %d, \"clock_khz_attr\": %d, \"cudaError\": \"%s\"}\n",
          i8, tf32, bf16, nsm, iters, nsm, clk, cudaGetErrorString(cudaGetLastError()));
