@@ -324,6 +324,10 @@ def main():
         path = "ozaki"
         kinds = {0: "pass_AX (ozaki_pass_kernel NN: int8 slices on tcgen05)",
                  1: "pass_AtX (ozaki_pass_kernel TN: int8 slices on tcgen05)"}
+    elif es == 4 and diag.get("ozaki_passes", 0) > 0:
+        path = "ozaki32"
+        kinds = {0: "pass_AX (ozaki_pass_kernel NN: 3-digit int8 slices of FP32 A on tcgen05)",
+                 1: "pass_AtX (ozaki_pass_kernel TN: 3-digit int8 slices of FP32 A on tcgen05)"}
     elif es == 4:
         path = "tf32"
         kinds = {0: "pass_AX (pass_tf32_tn_kernel as X^T A^T: 3xTF32 on tcgen05)",
@@ -353,11 +357,17 @@ def main():
         roof = {"bound": "hbm", "kernel": kinds[dom], "achieved": round(gbs, 1), "peak": hbm_peak,
                 "unit": "GB/s", "frac": round(gbs / hbm_peak, 4), "traffic": None, "peak_source": hbm_src}
         i8_peak = box.get("tcgen05_i8_tops_sustained", box.get("tcgen05_i8_tops"))
-        if path == "ozaki" and i8_peak:
-            # the other roof: 28 int8 slice products per FP64 product on the tensor pipe
-            # (DESIGN.md §6).  The binding roof is the one with the longer floor:
-            # bytes / HBM peak or int8 ops / tcgen05 int8 peak (config 3, l = 120: tensor)
-            ops_launch = 28.0 * flops_launch
+        if path in ("ozaki", "ozaki32") and i8_peak:
+            # the other roof: 28 (FP64 A, 7 digits) or 6 (FP32 A, 3 digits) int8 slice
+            # products per product on the tensor pipe.  The binding roof is
+            # the one with the longer floor: bytes / HBM peak or int8 ops / tcgen05 int8
+            # peak (config 3, l = 120: tensor)
+            ops_launch = (28.0 if path == "ozaki" else 6.0) * flops_launch
+            # what the kernel itself streams: the digit slices of A (7 or 3 bytes per element)
+            digits = 7 if path == "ozaki" else 3
+            kbytes = m_loc * (-(-n // 128) * 128) * digits
+            roof["slice_bytes_per_launch"] = kbytes
+            roof["slice_bytes_frac"] = round(kbytes / (avg_ms * 1e-3) / 1e9 / hbm_peak, 4)
             i8 = ops_launch / (avg_ms * 1e-3) / 1e12
             src = "profiles/peaks_box.json %s (tools/peaks_tc.cu)" % (
                 "tcgen05_i8_tops_sustained" if "tcgen05_i8_tops_sustained" in box else "tcgen05_i8_tops")

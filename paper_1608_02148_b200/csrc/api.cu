@@ -135,6 +135,7 @@ struct rsvd_ctx {
   int last_sweeps = 0;
   bool fp32_tcgen05 = true;       // RSVD_FP32_PATH=dmma selects the FP64-DMMA path for FP32 inputs
   bool fp64_ozaki = true;         // RSVD_FP64_PATH=dmma selects the DMMA path for FP64 inputs
+  bool fp32_ozaki = true;         // FP32 A: 3-digit Ozaki slices (RSVD_FP32_PATH=tf32: 3xTF32 passes, =dmma: CUDA cores)
   char* ws4 = nullptr;            // Ozaki slices of A (+ X slice scratch)
   size_t ws4_bytes = 0;
   int64_t ozaki_calls = 0;
@@ -441,7 +442,7 @@ rsvd_status pass_ozaki(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, doub
   CK(ozaki_pass(o, ctx->stream));
   cudaEventRecord(e2, ctx->stream);
   if (all) ctx->pending.push_back({6, 0.0, e0, e1});
-  ctx->pending.push_back({kind, (double)p.M * p.n * 8, e1b, e2});
+  ctx->pending.push_back({kind, (double)p.M * p.n * (p.f32 ? 4 : 8), e1b, e2});
   return RSVD_OK;
 }
 
@@ -685,8 +686,8 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool want_
   if (centred || p.scaled || want_ss) CKS(column_stats(ctx, p, prm->center != 0, want_ss));
   if (p.use_ozaki) {
     // slices of f(A) once per call; every pass below reads them (pass_ozaki.cu)
-    Prof pr(ctx, 5, (double)p.M * p.n * 8);
-    CK(ozaki_slice_a(p.oz, (const double*)p.A, p.lda, centred ? p.colc : nullptr, p.scaled ? p.colr : nullptr,
+    Prof pr(ctx, 5, (double)p.M * p.n * (p.f32 ? 4 : 8));
+    CK(ozaki_slice_a(p.oz, p.A, p.f32, p.lda, centred ? p.colc : nullptr, p.scaled ? p.colr : nullptr,
                      ctx->flags_dev, ctx->stream));
   }
   {
@@ -749,13 +750,15 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool want_
 
 // Ozaki slices of A (and X slice scratch) for the plan
 rsvd_status plan_ozaki(rsvd_ctx* ctx, Plan& p, int64_t m_local, int64_t n_stored, bool alloc) {
-  const size_t sa = align256(ozaki_a_bytes(m_local, n_stored));
-  const size_t sx = align256(ozaki_x_bytes(std::max(p.M, p.n), std::min(p.Np, 64)));
-  const size_t nx = p.Np > 64 ? 2 : 1;
+  const int s = p.f32 ? OZ_S32 : OZ_S;
+  const size_t sa = align256(ozaki_a_bytes(m_local, n_stored, s));
+  const int xc = ozaki_x_cols(s, p.Np);
+  const size_t sx = align256(ozaki_x_bytes(std::max(p.M, p.n), xc, s));
+  const size_t nx = p.Np > xc ? 2 : 1;
   p.oz_bytes = sa + nx * sx;
   if (!alloc) return RSVD_OK;
   CKS(ensure_buf(ctx, &ctx->ws4, &ctx->ws4_bytes, p.oz_bytes, "Ozaki slice workspace"));
-  p.oz = ozaki_layout_a(ctx->ws4, m_local, n_stored);
+  p.oz = ozaki_layout_a(ctx->ws4, m_local, n_stored, s);
   p.ozx = ctx->ws4 + sa;
   p.ozx2 = nx > 1 ? ctx->ws4 + sa + sx : nullptr;
   return RSVD_OK;
@@ -776,8 +779,8 @@ rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bo
   const int64_t mn = std::min(mg, A->n);
   p.l = (int)std::min<int64_t>((int64_t)k + p_over, mn);
   p.Np = (int)round_up(p.l, 16);      // GEMM N granularity: two warps x n8 tiles
-  p.use_tf32 = p.f32 && !center_or_scale && ctx->fp32_tcgen05 && tf32_pass_supported(p.A, p.lda);
-  p.use_ozaki = !p.f32 && ctx->fp64_ozaki && ozaki_supported(p.Np);
+  p.use_ozaki = (p.f32 ? ctx->fp32_ozaki : ctx->fp64_ozaki) && ozaki_supported(p.Np);
+  p.use_tf32 = !p.use_ozaki && p.f32 && !center_or_scale && ctx->fp32_tcgen05 && tf32_pass_supported(p.A, p.lda);
   if (p.l > kMaxL) return fail(ctx, RSVD_EUNSUPPORTED, "l = k + p = %d exceeds this build's limit %d", p.l, kMaxL);
   if (ctx->nranks > 1 && p.M < p.l)
     return fail(ctx, RSVD_EUNSUPPORTED, "each rank needs at least l = %d rows", p.l);
@@ -853,7 +856,8 @@ rsvd_status rsvd_create(rsvd_ctx** out, int device, void* stream) {
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   {
     const char* fp = getenv("RSVD_FP32_PATH");
-    if (fp && strcmp(fp, "dmma") == 0) ctx->fp32_tcgen05 = false;
+    if (fp && strcmp(fp, "dmma") == 0) ctx->fp32_tcgen05 = ctx->fp32_ozaki = false;
+    if (fp && strcmp(fp, "tf32") == 0) ctx->fp32_ozaki = false;
     const char* f64 = getenv("RSVD_FP64_PATH");
     if (f64 && strcmp(f64, "dmma") == 0) ctx->fp64_ozaki = false;
   }
@@ -1270,8 +1274,8 @@ rsvd_status rsvd_rpca_predict(rsvd_ctx* ctx, const rsvd_matrix* Anew, int32_t k,
   p.trans_input = false;
   p.M = Am.m_local; p.n = Am.n; p.m_global = Am.m_local;
   p.l = k; p.Np = (int)round_up(k, 16);
-  p.use_tf32 = p.f32 && !cs && ctx->fp32_tcgen05 && tf32_pass_supported(p.A, p.lda);
-  p.use_ozaki = !p.f32 && ctx->fp64_ozaki && ozaki_supported(p.Np);
+  p.use_ozaki = (p.f32 ? ctx->fp32_ozaki : ctx->fp64_ozaki) && ozaki_supported(p.Np);
+  p.use_tf32 = !p.use_ozaki && p.f32 && !cs && ctx->fp32_tcgen05 && tf32_pass_supported(p.A, p.lda);
   CKS(ensure_ws(ctx, plan_bytes(ctx, p)));
   bind(ctx, p);
   if (p.use_ozaki) CKS(plan_ozaki(ctx, p, Am.m_local, Am.n, true));
@@ -1283,7 +1287,7 @@ rsvd_status rsvd_rpca_predict(rsvd_ctx* ctx, const rsvd_matrix* Anew, int32_t k,
   p.scaled = scale != nullptr;
   if (scale) CK(launch_vec_map(scale, f32, p.n, 1, 0.0, p.colr, ctx->stream));          // 1 / s
   if (p.use_ozaki)
-    CK(ozaki_slice_a(p.oz, (const double*)p.A, p.lda, center ? p.colc : nullptr, scale ? p.colr : nullptr,
+    CK(ozaki_slice_a(p.oz, p.A, p.f32, p.lda, center ? p.colc : nullptr, scale ? p.colr : nullptr,
                      ctx->flags_dev, ctx->stream));
   CKS(pass_ax(ctx, p, p.X, p.Y, cs));                                                   // f(Anew) W
   CK(launch_copy_out(p.Y, p.Np, p.M, k, out, ldo, f32, nullptr, ctx->stream));

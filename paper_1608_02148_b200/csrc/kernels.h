@@ -71,19 +71,22 @@ cudaError_t launch_panel_apply(const double* S, int64_t lds, int64_t rows, int N
                                double* C, int64_t ldc, int Nout, bool upper, int num_sms, cudaStream_t st,
                                Pred pr = Pred{});
 
-// ---- FP64 passes by Ozaki-scheme int8 slices on tcgen05 (pass_ozaki.cu)
-#define OZ_S 7                                   // 8-bit digits per element (A: 56-bit two's complement, X: 54-bit balanced)
-struct OzakiA {                                  // A sliced once per call: m x (ldn/128) x S x 128 int8 + exponents
+// ---- passes by Ozaki-scheme int8 slices on tcgen05 (pass_ozaki.cu)
+#define OZ_S 7                                   // FP64 A: 8-bit digits per element (A: 56-bit two's complement, X: 54-bit balanced)
+#define OZ_S32 3                                 // FP32 A: 3 digits (A: 24-bit two's complement, X: 22-bit balanced)
+struct OzakiA {                                  // A sliced once per call: m x (ldn/128) x s x 128 int8 + exponents
   int8_t* slices;
   int* erow;                                     // E_r: max_j |f(a_rj)| < 2^{E_r}, one per row
   unsigned* emax;                                // max_r E_r + 4096 (biased, atomicMax)
   int64_t m, n, ldn;
+  int s;                                         // digits per element: OZ_S (FP64 A) or OZ_S32 (FP32 A)
 };
-size_t ozaki_a_bytes(int64_t m, int64_t n);
-OzakiA ozaki_layout_a(void* buf, int64_t m, int64_t n);
-// slices of f(A) = (A - 1 c^T) diag(rs) (c, rs nullable); flag |= 4 on non-finite A
-cudaError_t ozaki_slice_a(const OzakiA& a, const double* A, int64_t lda, const double* c, const double* rs, int* flag,
-                          cudaStream_t st);
+size_t ozaki_a_bytes(int64_t m, int64_t n, int s);
+OzakiA ozaki_layout_a(void* buf, int64_t m, int64_t n, int s);
+// slices of f(A) = (A - 1 c^T) diag(rs) (c, rs nullable; A FP64, or FP32 when f32);
+// flag |= 4 on non-finite A
+cudaError_t ozaki_slice_a(const OzakiA& a, const void* A, bool f32, int64_t lda, const double* c, const double* rs,
+                          int* flag, cudaStream_t st);
 struct OzakiCall {
   const OzakiA* a; bool trans;                   // trans: C = f(A)^T B (M = n, K = m), else C = f(A) B
   const double* B; int64_t ldb;                  // K x N panel (FP64), N = Np <= 128 (two 64-column halves above 64)
@@ -98,7 +101,8 @@ struct OzakiCall {
 bool ozaki_supported(int Np);
 // stream-K partials of the pass kernels: 2 slots (first / last segment) per CTA
 size_t ozaki_partial_bytes(int Np, int grid);
-size_t ozaki_x_bytes(int64_t K, int Np);
+size_t ozaki_x_bytes(int64_t K, int Np, int s);
+int ozaki_x_cols(int s, int Np);                 // columns per X slice scratch (64, or 128 for FP32 A at Np = 128)
 cudaError_t ozaki_pass(const OzakiCall& c, cudaStream_t st);
 
 // ---- K1 Omega (omega.cu)

@@ -53,6 +53,9 @@ using namespace tc;
 // warps 4..11 epilogue (two per TMEM lane quadrant, each owning half of the N
 // columns, so the FP64 accumulators stay in registers: <= 168 per thread)
 constexpr int BM = 128, BKO = 128, THREADS = 384, EPI_WARPS = 8, EPI_THREADS = 32 * EPI_WARPS;
+// N = 128 (FP32 A at Np = 128, one CTA per row block): 16 epilogue warps, 32 columns each
+__host__ __device__ constexpr int oz_epi_warps(int N) { return N > 64 ? 16 : EPI_WARPS; }
+__host__ __device__ constexpr int oz_threads(int N) { return 128 + 32 * oz_epi_warps(N); }
 constexpr int A_TILE = BM * BKO;                    // bytes of one slice tile
 constexpr int ET = 1024;                            // exponent blocks of X: 1024 rows x 1 column;
                                                     // int32 accumulation over 1024 k: <= 7 pairs * 1024 * 255 * 128 < 2^28
@@ -101,6 +104,45 @@ __device__ __forceinline__ void tma_4d_mc(void* dst, const CUtensorMap* map, int
         "l"(kL2EvictFirst)
       : "memory");
 }
+// MODE 3 (row pair, cta_group::2): each CTA loads its own tiles into its own shared
+// memory and signals the LEADER's (rank 0) barrier: the peer bit of the barrier's
+// shared::cluster address cleared (the CUTLASS 2-SM TMA convention)
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;
+__device__ __forceinline__ void tma_4d_2sm(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "r"(smem_u32(bar) & kPeerMask), "l"(kL2EvictFirst)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d_2sm_keep(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & kPeerMask),
+        "l"(kL2EvictLast)
+      : "memory");
+}
+__device__ __forceinline__ void tma_4d_2sm_keep(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "r"(smem_u32(bar) & kPeerMask), "l"(kL2EvictLast)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_2sm(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_2sm_mc(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask) : "memory");
+}
 __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
                ::"r"(smem_u32(bar)), "h"(mask) : "memory");
@@ -131,7 +173,13 @@ __device__ __forceinline__ void digits_a4(const double (&v)[4], double s1, doubl
   for (int e = 0; e < 4; ++e) {
     // exact power-of-two scaling in two steps (2^{55-E} alone over/underflows
     // at the ends of the exponent range), then round
-    const long long q = __double2ll_rn(v[e] * s1 * s2);
+    long long q = __double2ll_rn(v[e] * s1 * s2);
+    if constexpr (S < 7) {
+      // fewer digits than a double's significand: rounding may reach 2^{8S-1}; clamp
+      // (an error of one unit in the last digit, as the rounding itself)
+      constexpr long long lim = (1ll << (8 * S - 1)) - 1;
+      q = q > lim ? lim : (q < -lim ? -lim : q);
+    }
 #pragma unroll
     for (int t = 0; t < S; ++t) w[t] |= ((uint32_t)(q >> (8 * (S - 1 - t))) & 0xffu) << (8 * e);
   }
@@ -154,18 +202,23 @@ __device__ __forceinline__ void pow2_split(int e, double& p1, double& p2) {
 }
 
 // four consecutive f(a) of one row starting at column j0 (zeros beyond n);
-// 16-byte loads when the row is 16-byte aligned
-template <bool LAST>
-__device__ __forceinline__ void load_f4(const double* row, int64_t j0, int64_t n, bool vec, const double* c,
+// 16-byte loads when the row is 16-byte aligned (T = double or float)
+template <bool LAST, typename T>
+__device__ __forceinline__ void load_f4(const T* row, int64_t j0, int64_t n, bool vec, const double* c,
                                         const double* rs, double (&v)[4]) {
   if (vec && j0 + 3 < n) {
     // first read: default caching (the row is read again right after); second: evict-first
-    const double2 a = LAST ? __ldcs(reinterpret_cast<const double2*>(row + j0)) : *reinterpret_cast<const double2*>(row + j0);
-    const double2 b = LAST ? __ldcs(reinterpret_cast<const double2*>(row + j0 + 2)) : *reinterpret_cast<const double2*>(row + j0 + 2);
-    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    if constexpr (sizeof(T) == 8) {
+      const double2 a = LAST ? __ldcs(reinterpret_cast<const double2*>(row + j0)) : *reinterpret_cast<const double2*>(row + j0);
+      const double2 b = LAST ? __ldcs(reinterpret_cast<const double2*>(row + j0 + 2)) : *reinterpret_cast<const double2*>(row + j0 + 2);
+      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
+      const float4 a = LAST ? __ldcs(reinterpret_cast<const float4*>(row + j0)) : *reinterpret_cast<const float4*>(row + j0);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    }
   } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = j0 + q < n ? row[j0 + q] : 0.0;
+    for (int q = 0; q < 4; ++q) v[q] = j0 + q < n ? (double)row[j0 + q] : 0.0;
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -183,9 +236,9 @@ __device__ __forceinline__ void load_f4(const double* row, int64_t j0, int64_t n
 // E_r; *emax = max_r E_r + kEBias (atomicMax, zeroed by the launcher); flag
 // |= 4 on a non-finite f(a).
 constexpr int kEBias = 4096;
-template <int S>
+template <int S, typename T>
 __global__ void __launch_bounds__(256)
-ozaki_slice_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, const double* __restrict__ c,
+ozaki_slice_rows_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n, const double* __restrict__ c,
                         const double* __restrict__ rs, int8_t* __restrict__ slices, int64_t ldn, int* __restrict__ erow,
                         unsigned* emax, int* flag) {
   pdl_wait();
@@ -193,11 +246,11 @@ ozaki_slice_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t m, in
   __shared__ unsigned wm[8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t nblk = ldn / BKO;
-  const bool vec = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  const bool vec = ((lda * (int64_t)sizeof(T)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   unsigned mymax = 0;
   bool nf = false;
   for (int64_t r = (int64_t)blockIdx.x * 8 + wid; r < m; r += (int64_t)gridDim.x * 8) {
-    const double* row = A + r * lda;
+    const T* row = A + r * lda;
     double mx = 0.0;
 #pragma unroll 4
     for (int64_t j0 = 4 * lane; j0 < n; j0 += 128) {
@@ -245,11 +298,12 @@ ozaki_slice_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t m, in
 // Groups never wait for each other, so copies and arithmetic overlap with up
 // to 32 warps per SM.  One HBM read of A.  The centring / scaling vectors (rpca)
 // are staged in shared memory too, in place of row buffers.  Needs 16-byte
-// aligned rows (lda and n even) and room for two row buffers.
+// aligned rows (16-byte row pitch and row length) and room for two row buffers.
+// T = double (FP64 A) or float (FP32 A: the digits of the exactly upcast value).
 constexpr int SR_SMEM = 200 * 1024, SR_W = 4, SR_MAX_G = 8;
-template <int S>
+template <int S, typename T>
 __global__ void __launch_bounds__(32 * SR_W * SR_MAX_G, 1)
-ozaki_slice_rows_smem_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+ozaki_slice_rows_smem_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n,
                              const double* __restrict__ c, const double* __restrict__ rs, int8_t* __restrict__ slices,
                              int64_t ldn, int* __restrict__ erow, unsigned* emax, int* flag) {
   pdl_wait();
@@ -263,14 +317,15 @@ ozaki_slice_rows_smem_kernel(const double* __restrict__ A, int64_t lda, int64_t 
   const int grp = wid / SR_W, gw = wid % SR_W, gt = threadIdx.x % GT;
   const int ng = blockDim.x / GT;
   const int64_t nblk = ldn / BKO;
-  const uint32_t row_bytes = (uint32_t)(n * 8);
-  const int64_t stride = (row_bytes + 127) / 128 * 16;          // doubles per group buffer (128-byte aligned)
-  double* row = reinterpret_cast<double*>(srow_raw) + grp * stride;
+  const uint32_t row_bytes = (uint32_t)(n * sizeof(T));
+  const int64_t rbuf = (row_bytes + 127) / 128 * 128;          // bytes per group buffer (128-byte aligned)
+  const int64_t vstride = (n * 8 + 127) / 128 * 16;            // doubles per staged vector
+  T* row = reinterpret_cast<T*>(srow_raw + grp * rbuf);
   // the centring / scaling vectors staged once behind the row buffers: with most
   // of the SM's L1 given to shared memory they would otherwise come from L2 for
   // every element (measured: the dominant stall of the centred config-3 slicing)
-  double* cs = reinterpret_cast<double*>(srow_raw) + ng * stride;
-  double* rss = cs + (c ? stride : 0);
+  double* cs = reinterpret_cast<double*>(srow_raw + ng * rbuf);
+  double* rss = cs + (c ? vstride : 0);
   for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
     if (c) cs[j] = c[j];
     if (rs) rss[j] = rs[j];
@@ -289,13 +344,33 @@ ozaki_slice_rows_smem_kernel(const double* __restrict__ A, int64_t lda, int64_t 
                    ::"r"(smem_u32(row)), "l"(A + r * lda), "r"(row_bytes), "r"(smem_u32(&full[grp])) : "memory");
     }
     mbar_wait(&full[grp], phase);
+    // FP32 A without centring / scaling: the row in float arithmetic (exact: |a|,
+    // max, and below the power-of-two scaling), 16-byte reads, four chains
+    constexpr bool F32 = sizeof(T) == 4;
+    const bool fast = F32 && !c && !rs;
     double mx = 0.0;
-    for (int64_t j = gt; j < n; j += GT) {
-      double v = row[j];
-      if (c) v -= cs[j];
-      if (rs) v *= rss[j];
-      if (!isfinite(v)) nf = true;
-      mx = fmax(mx, fabs(v));
+    if (fast) {
+      float m4[4] = {0.f, 0.f, 0.f, 0.f};
+      bool bad = false;
+      for (int64_t j = 4 * gt; j < n; j += 4 * GT) {
+        const float4 a = *reinterpret_cast<const float4*>(row + j);
+        const float e[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          bad |= !isfinite(e[q]);
+          m4[q] = fmaxf(m4[q], fabsf(e[q]));
+        }
+      }
+      if (bad) nf = true;
+      mx = bad ? (double)INFINITY : (double)fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+    } else {
+      for (int64_t j = gt; j < n; j += GT) {
+        double v = (double)row[j];
+        if (c) v -= cs[j];
+        if (rs) v *= rss[j];
+        if (!isfinite(v)) nf = true;
+        mx = fmax(mx, fabs(v));
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -308,27 +383,74 @@ ozaki_slice_rows_smem_kernel(const double* __restrict__ A, int64_t lda, int64_t 
     mymax = max(mymax, (unsigned)(E + kEBias));
     double s1, s2;
     pow2_split(8 * S - 1 - E, s1, s2);
+    if constexpr (F32) {
+      // 2^{8S-1-E} as a normal float: N = rn(a 2^{8S-1-E}) in float arithmetic
+      // (the scaling is exact, |N| < 2^{8S-1} <= 2^31)
+      const int se = 8 * S - 1 - E;
+      if (fast && se >= -126 && se <= 127) {
+        const float sf = __int_as_float((se + 127) << 23);
+        for (int64_t q = gt; q < nblk * 32; q += GT) {
+          const int64_t blk = q >> 5;
+          const int64_t j0 = blk * BKO + 4 * (q & 31);
+          uint32_t w[S];
+#pragma unroll
+          for (int t = 0; t < S; ++t) w[t] = 0u;
+          if (j0 < n) {
+            const float4 a = *reinterpret_cast<const float4*>(row + j0);
+            // rounding may reach 2^{8S-1} (a within half a unit below 2^E): clamp
+            constexpr int lim = (int)((1ll << (8 * S - 1)) - 1);
+            const float4 b = make_float4(a.x * sf, a.y * sf, a.z * sf, a.w * sf);
+            const int nq[4] = {max(-lim, min(lim, __float2int_rn(b.x))), max(-lim, min(lim, __float2int_rn(b.y))),
+                               max(-lim, min(lim, __float2int_rn(b.z))), max(-lim, min(lim, __float2int_rn(b.w)))};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+#pragma unroll
+              for (int t = 0; t < S; ++t) w[t] |= ((uint32_t)(nq[e] >> (8 * (S - 1 - t))) & 0xffu) << (8 * e);
+          }
+          int8_t* dst = slices + ((r * nblk + blk) * S) * BKO + 4 * (q & 31);
+#pragma unroll
+          for (int t = 0; t < S; ++t) *reinterpret_cast<uint32_t*>(dst + t * BKO) = w[t];
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "n"(GT) : "memory");   // the buffer and redm are reused
+        continue;
+      }
+    }
     // 32 threads per 128-column block, 4 consecutive columns per thread
     for (int64_t q = gt; q < nblk * 32; q += GT) {
       const int64_t blk = q >> 5;
       const int64_t j0 = blk * BKO + 4 * (q & 31);
-      // two 16-byte reads per thread (n even: a pair is wholly inside or outside
-      // the row); lanes with bit 2 set read their second half first, so each
-      // read instruction of the warp touches every bank group equally
-      const bool h0 = (q >> 2) & 1;
-      double2 a[2];
+      double v[4];
+      if constexpr (sizeof(T) == 8) {
+        // two 16-byte reads per thread (n even: a pair is wholly inside or outside
+        // the row); lanes with bit 2 set read their second half first, so each
+        // read instruction of the warp touches every bank group equally
+        const bool h0 = (q >> 2) & 1;
+        double2 a[2];
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int64_t jj = j0 + 2 * (hh ^ (int)h0);
-        a[hh] = make_double2(0.0, 0.0);
-        if (jj < n) {
-          a[hh] = *reinterpret_cast<const double2*>(row + jj);
-          if (c) { const double2 cc = *reinterpret_cast<const double2*>(cs + jj); a[hh].x -= cc.x; a[hh].y -= cc.y; }
-          if (rs) { const double2 rr = *reinterpret_cast<const double2*>(rss + jj); a[hh].x *= rr.x; a[hh].y *= rr.y; }
+        for (int hh = 0; hh < 2; ++hh) {
+          const int64_t jj = j0 + 2 * (hh ^ (int)h0);
+          a[hh] = make_double2(0.0, 0.0);
+          if (jj < n) {
+            a[hh] = *reinterpret_cast<const double2*>(row + jj);
+            if (c) { const double2 cc = *reinterpret_cast<const double2*>(cs + jj); a[hh].x -= cc.x; a[hh].y -= cc.y; }
+            if (rs) { const double2 rr = *reinterpret_cast<const double2*>(rss + jj); a[hh].x *= rr.x; a[hh].y *= rr.y; }
+          }
+        }
+        const double2 lo = h0 ? a[1] : a[0], hi = h0 ? a[0] : a[1];
+        v[0] = lo.x; v[1] = lo.y; v[2] = hi.x; v[3] = hi.y;
+      } else {
+        // one 16-byte read per thread (n % 4 == 0: a quad is wholly inside or outside the row)
+        v[0] = v[1] = v[2] = v[3] = 0.0;
+        if (j0 < n) {
+          const float4 a = *reinterpret_cast<const float4*>(row + j0);
+          v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (c) v[e] -= cs[j0 + e];
+            if (rs) v[e] *= rss[j0 + e];
+          }
         }
       }
-      const double2 lo = h0 ? a[1] : a[0], hi = h0 ? a[0] : a[1];
-      double v[4] = {lo.x, lo.y, hi.x, hi.y};
       uint32_t w[S];
       digits_a4<S>(v, s1, s2, w);
       int8_t* dst = slices + ((r * nblk + blk) * S) * BKO + 4 * (q & 31);
@@ -452,10 +574,24 @@ __host__ __device__ constexpr int oz_nbuf(int S, int N, int BK) {
 // [64 r, 64 r + 64) from its own X slices; each loads half of the unit's A
 // slice tiles and multicasts them to both, so A's slices are read once per
 // pass instead of once per column half.  Stream-K runs over the pairs.
-template <bool TRANS, int S, int N, int CL, int BK>
-__global__ void __launch_bounds__(THREADS, 1)
+//
+// MODE 3 (row pair, FP32 A at Np = 128): the two CTAs of a cluster own two
+// adjacent 128-row blocks of the SAME unit (256 rows) and one tcgen05.mma
+// .cta_group::2 (M = 256, N = 128) covers both: each CTA streams only its own A
+// rows and HALF of the X tile (64 of the 128 columns; the pair's MMA reads the
+// other half from the peer), so a CTA ingests 1.5 bytes per byte of its A slices
+// instead of 3 (column pair) or 2 (one CTA, N = 128) -- the SM's L2 -> shared
+// ingest (~10 TB/s chip-wide) is what bounds the pass (tools/test_ozaki.cu
+// probes: the kernel with its MMAs removed runs as fast as with them).  The
+// leader (rank 0) arms the stage barriers and issues the MMAs; both CTAs' TMA
+// loads complete on the leader's barriers; commits are multicast to both.
+template <bool TRANS, int S, int N, int MODE, int BK>
+__global__ void __launch_bounds__(oz_threads(N), 1)
 ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapX,
                   const __grid_constant__ CUtensorMap mapX2, Args g) {
+  constexpr int CL = MODE == 1 ? 1 : 2;             // cluster size
+  constexpr bool RP = MODE == 3;                    // row pair (cta_group::2)
+  constexpr int NX = RP ? N / 2 : N;                // X columns (B rows) held per CTA
   pdl_wait();
   if (threadIdx.x == 0) OZ_TL(0)
   pdl_trigger();
@@ -469,20 +605,26 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   constexpr int KSU = ET / BKU;                     // units per exponent super-block
 #endif
   constexpr int A_UT = BM * BKU;                    // bytes of one A-slice tile of a unit
-  constexpr int XSL = N * BKU;                      // bytes of one X slice tile (N rows x BK k)
-  constexpr int UBUF = oz_ubuf(S, N, BK);
-  constexpr int NB = oz_nbuf(S, N, BK);             // unit buffers
+  constexpr int XSL = NX * BKU;                     // bytes of one X slice tile (NX rows x BK k)
+  constexpr int UBUF = oz_ubuf(S, NX, BK);
+  constexpr int NB = oz_nbuf(S, NX, BK);            // unit buffers
   constexpr int KPB = BKO / BKU;                    // units per 128-column slice block
   // NN: K-major tiles with BK-byte rows (SW64 / SW32); TN: MN-major 128 B rows (SW128)
   constexpr uint32_t LAY_K = BK == 64 ? LAYOUT_SW64 : LAYOUT_SW32;
   constexpr uint32_t SBO_K = BK == 64 ? 512 : 256;
-  __shared__ uint64_t ufull[kMaxBuf], uempty[kMaxBuf], accf, acce;
+  // accumulator sets in TMEM: two (at column 0 and 256) when S x N <= 256, so the
+  // MMAs of the next exponent super-block never wait for the epilogue's drain
+  constexpr int NACC = 2 * S * N <= 512 ? 2 : 1;
+  static_assert(!RP || (CL == 2 && N == 128), "row pairs: N = 128");
+  __shared__ uint64_t ufull[kMaxBuf], uempty[kMaxBuf], accf[2], acce[2];
   __shared__ uint32_t tmem_base;
-  __shared__ double xfsm[EPI_WARPS * 32 + 1];     // + 1: last-arriver broadcast slot
+  constexpr int EPI_WARPS = oz_epi_warps(N), EPI_THREADS = 32 * EPI_WARPS;
+  constexpr int XFW = N / (EPI_WARPS / 4) > 32 ? N / (EPI_WARPS / 4) : 32;   // column factors per epilogue warp
+  __shared__ double xfsm[EPI_WARPS * XFW + 1];    // + 1: last-arriver broadcast slot
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t KB = g.KB;                          // 64-k blocks
-  const int crank = CL == 2 ? (int)(blockIdx.x & 1) : 0;   // rank in the cluster = column half
+  const int crank = CL == 2 ? (int)(blockIdx.x & 1) : 0;   // rank in the cluster = column half (MODE 2) / row block (MODE 3)
   const int pid = (int)blockIdx.x / CL, npair = g.grid / CL;
   const int64_t u_lo = unit_lo(g.units, npair, pid);
   const int64_t u_hi = unit_lo(g.units, npair, pid + 1);
@@ -491,19 +633,23 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   // (no 64-bit division per unit on the single-thread producer / MMA paths)
   const int mb0 = (int)(u_lo / KB), kb0 = (int)(u_lo - (int64_t)mb0 * KB);
   const int KBi = (int)KB;
-  double* const Cout = crank ? g.C2 : g.C;
-  const double* const xfh = crank ? g.xf2 : g.xf;
-  const int Nout = crank ? g.Nout2 : g.Nout;
+  double* const Cout = (crank && !RP) ? g.C2 : g.C;
+  const double* const xfh = (crank && !RP) ? g.xf2 : g.xf;
+  const int Nout = (crank && !RP) ? g.Nout2 : g.Nout;
 
   if (tid == 0) {
-    for (int s = 0; s < NB; ++s) { mbar_init(&ufull[s], 1); mbar_init(&uempty[s], CL); }
-    mbar_init(&accf, 1);
-    mbar_init(&acce, EPI_WARPS);
+    for (int s = 0; s < NB; ++s) { mbar_init(&ufull[s], 1); mbar_init(&uempty[s], RP ? 1 : CL); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&accf[s], 1); mbar_init(&acce[s], RP ? 2 * EPI_WARPS : EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (RP) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   if (CL == 2) cluster_sync_all(); else __syncthreads();
@@ -521,6 +667,19 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         OZ_PROBE2(0)
         mbar_wait(&uempty[ub], ph ^ 1u);
         OZ_PROBE2(1)
+        if constexpr (RP) {
+          // own 128 rows of A (row block 2 mb + crank) and own half of the X columns;
+          // the bytes of both CTAs complete on the leader's barrier, which the leader arms
+          if (crank == 0) mbar_expect_tx(&ufull[ub], (uint32_t)(2 * (S * A_UT + S * XSL)));
+          // ONE box per operand and unit: all S digit tiles of A (tensor map dims
+          // {byte, row, digit, column block}: box -> [digit][row][BK]) and all S digit
+          // tiles of this CTA's X half (dims {k, column, half, digit}) -- the TMA
+          // engine streams large boxes faster than many 4-8 KB ones
+          const int orb = 2 * mb + crank;
+          if (!TRANS) tma_4d_2sm(ubuf, &mapA, (int)((kb % KPB) * BKU), (int)((int64_t)orb * BM), 0, (int)(kb / KPB), &ufull[ub]);
+          else tma_4d_2sm(ubuf, &mapA, 0, (int)(kb * BKU), 0, orb, &ufull[ub]);
+          tma_4d_2sm_keep(ubuf + S * A_UT, &mapX, (int)(kb * BKU), 0, crank, 0, &ufull[ub]);
+        } else {
 #if defined(OZ_NO_A_TMA)            // probe builds only (tools/test_ozaki.cu): no A-slice loads
         mbar_expect_tx(&ufull[ub], (uint32_t)(S * XSL));
         if (false) {
@@ -546,6 +705,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
 #ifndef OZ_NO_X_TMA
         for (int t = 0; t < S; ++t) tma_2d_keep(ubuf + S * A_UT + t * XSL, mx, (int)(kb * BKU), t * g.Np, &ufull[ub]);
 #endif
+        }
         OZ_PROBE2(2)
       }
       if (CL == 2) {
@@ -557,14 +717,16 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       OZ_TL(1)
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
+    // ---------------- MMA issuer (MODE 3: the leader only, one MMA for both CTAs)
+    if (lane == 0 && (!RP || crank == 0)) {
       // X slices u0..u0+c-1 are consecutive N-row tiles and their groups t+u0..t+u0+c-1
       // consecutive N-column blocks of TMEM: one MMA with N_mma = c N covers them (<= 256)
       // D s32; B s8; A s8 for digit 0, u8 for the others (bits 7-9, set per t)
       const uint32_t idesc0 = (2u << 4) | (1u << 10) | ((TRANS ? 1u : 0u) << 15) | (0u << 16) |
-                              ((uint32_t)(BM >> 4) << 24);
-      constexpr int CMAX = 256 / N;
+                              ((uint32_t)((RP ? 2 * BM : BM) >> 4) << 24);
+      // MODE 3: one digit per MMA (the pair's B operand is split by columns: digit
+      // batches would put different digits in the two CTAs)
+      constexpr int CMAX = RP ? 1 : 256 / N;
       OZ_PROBE_DECL
       int ndrain = 0;
       bool fresh = true;
@@ -577,13 +739,15 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         mbar_wait(&ufull[ub], ph);
         OZ_PROBE(3)
 #ifndef OZ_NO_EPI
-        if (fresh && ndrain > 0) mbar_wait(&acce, (uint32_t)((ndrain - 1) & 1));
+        // a fresh super-block reuses accumulator set ndrain % NACC: drain ndrain - NACC must be done
+        if (fresh && ndrain >= NACC) mbar_wait(&acce[ndrain % NACC], (uint32_t)((ndrain / NACC - 1) & 1));
 #endif
         OZ_PROBE(2)
         tc_fence_after();
         const uint32_t ua = smem_u32(base + ub * UBUF);
         const uint64_t dx0 = sdesc(ua + S * A_UT, 16, SBO_K, LAY_K);
         const uint32_t acc0 = fresh ? 0u : 1u;
+        const uint32_t tacc = tmem + (uint32_t)((ndrain % NACC) * 256);
 #pragma unroll
         for (int t = 0; t < S; ++t) {
           // NN: A tile K-major, 64 B rows (SW64, k-step +32 B); TN: MN-major, 128 B rows (SW128, k-step +32 rows)
@@ -597,15 +761,21 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
               const uint64_t db = dx0 + (uint64_t)((u0 * XSL + kk * 32) >> 4);
               const uint32_t idesc = idesc0 | ((t == 0 ? 1u : 0u) << 7) | ((uint32_t)((cnt * N) >> 3) << 17);
 #ifndef OZ_SKIP_MMA
-              mma_i8(tmem + (uint32_t)((t + u0) * N), da, db, idesc, (t > 0 || kk > 0) ? 1u : acc0);
+              if constexpr (RP) mma_i8_2sm(tacc + (uint32_t)((t + u0) * N), da, db, idesc, (t > 0 || kk > 0) ? 1u : acc0);
+              else mma_i8(tacc + (uint32_t)((t + u0) * N), da, db, idesc, (t > 0 || kk > 0) ? 1u : acc0);
 #endif
             }
           }
         }
         OZ_PROBE(4)
-        if (CL == 1) mma_commit(&uempty[ub]);
-        else mma_commit_mc(&uempty[ub], (uint16_t)3);
-        if (drain) { mma_commit(&accf); ++ndrain; }
+        if constexpr (RP) {
+          mma_commit_2sm_mc(&uempty[ub]);
+          if (drain) { mma_commit_2sm_mc(&accf[ndrain % NACC]); ++ndrain; }
+        } else {
+          if (CL == 1) mma_commit(&uempty[ub]);
+          else mma_commit_mc(&uempty[ub], (uint16_t)3);
+          if (drain) { mma_commit(&accf[ndrain % NACC]); ++ndrain; }
+        }
         fresh = drain;
       }
       OZ_PROBE_OUT
@@ -618,16 +788,16 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
     {
     // ---------------- epilogue: TMEM groups -> FP64, scale, accumulate; segment write-out
     // thread (row, hf) owns columns [hf * NC, hf * NC + NC) of output row `row`
-    constexpr int NC = N / 2;
+    constexpr int NC = N / (EPI_WARPS / 4);           // columns per thread (32, or 8..24 at N < 64)
     const int et = tid - 128;                         // 0 .. EPI_THREADS - 1
     const int row = 32 * (warp & 3) + lane;
-    const int hf = (warp - 4) >> 2;                   // column half
+    const int hf = (warp - 4) >> 2;                   // column part
     const int c0 = hf * NC;
     const uint32_t tlane = (uint32_t)(32 * (warp & 3)) << 16;
     double acc[NC];
 #pragma unroll
     for (int j = 0; j < NC; ++j) acc[j] = 0.0;
-    double* xfs = xfsm + (warp - 4) * 32;             // per-warp copy of this super-block's column factors
+    double* xfs = xfsm + (warp - 4) * XFW;            // per-warp copy of this super-block's column factors
     int64_t ndrain = 0;
     OZ_PROBE3_DECL
     int mb = mb0, kb = kb0;
@@ -635,11 +805,13 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       const int64_t u = u_lo + it;
       if (!((kb % KSU == KSU - 1) || kb == KBi - 1 || it == nun - 1)) continue;
       const int64_t sb = kb / KSU;                          // super-block along k (X exponent block)
-      if (lane < NC) xfs[lane] = xfh[sb * g.Np + c0 + lane];
+      for (int j = lane; j < NC; j += 32) xfs[j] = xfh[sb * g.Np + c0 + j];
       __syncwarp();
       OZ_PROBE3(0)
       // one thread waits (sleeping), the other epilogue warps block on a named barrier
-      if (et == 0) mbar_wait_sleep(&accf, (uint32_t)(ndrain & 1));
+      const int abuf = (int)(ndrain % NACC);
+      const uint32_t aoff = (uint32_t)(abuf * 256);
+      if (et == 0) mbar_wait_sleep(&accf[abuf], (uint32_t)((ndrain / NACC) & 1));
       asm volatile("bar.sync 2, %0;" ::"n"(EPI_THREADS) : "memory");
       OZ_PROBE3(1)
       ++ndrain;
@@ -652,24 +824,36 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
 #if defined(OZ_EPI_V) && (OZ_EPI_V & 1)   // probe builds only: no TMEM loads
         for (int gg = 0; gg < S; ++gg) for (int i = 0; i < 8; ++i) v[gg][i] = (uint32_t)(gg + i + c) * (uint32_t)row;
 #else
-        for (int gg = 0; gg < S; ++gg) TMEM_LD8(tmem + tlane + (uint32_t)(gg * N + c0 + 8 * c), v[gg]);
+        for (int gg = 0; gg < S; ++gg) TMEM_LD8(tmem + tlane + aoff + (uint32_t)(gg * N + c0 + 8 * c), v[gg]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #endif
-        // group g = t + u weighs 2^{-13-8g}; |v_g| < 7 * 1024 * 255 * 128 < 2^28, so the
-        // groups 0..3 and 4..6 combine EXACTLY in int64 (< 2^53 and < 2^45): two
-        // int -> FP64 conversions and one rounding per column instead of seven
-        static_assert(S == 7, "group combination assumes 7 digit groups");
+        // group g = t + u weighs 2^{-13-8g} (for every S); |v_g| < S * 1024 * 255 * 128 < 2^28
+        static_assert(S == 7 || S == 3, "group combination for 7 (FP64) or 3 (FP32) digit groups");
+        if constexpr (S == 7) {
+          // groups 0..3 and 4..6 combine EXACTLY in int64 (< 2^53 and < 2^45): two
+          // int -> FP64 conversions and one rounding per column instead of seven
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const long long s0 = (((long long)(int)v[0][i] * 256 + (int)v[1][i]) * 256 + (int)v[2][i]) * 256 + (int)v[3][i];
-          const long long s1 = ((long long)(int)v[4][i] * 256 + (int)v[5][i]) * 256 + (int)v[6][i];
-          const double part = fma((double)s0, 0x1.0p-37, (double)s1 * 0x1.0p-61);
-          acc[8 * c + i] = fma(part, xfs[8 * c + i], acc[8 * c + i]);
+          for (int i = 0; i < 8; ++i) {
+            const long long s0 = (((long long)(int)v[0][i] * 256 + (int)v[1][i]) * 256 + (int)v[2][i]) * 256 + (int)v[3][i];
+            const long long s1 = ((long long)(int)v[4][i] * 256 + (int)v[5][i]) * 256 + (int)v[6][i];
+            const double part = fma((double)s0, 0x1.0p-37, (double)s1 * 0x1.0p-61);
+            acc[8 * c + i] = fma(part, xfs[8 * c + i], acc[8 * c + i]);
+          }
+        } else {
+          // groups 0..2 combine exactly in int64 (< 2^45): one conversion per column
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const long long s0 = ((long long)(int)v[0][i] * 256 + (int)v[1][i]) * 256 + (int)v[2][i];
+            acc[8 * c + i] = fma((double)s0 * 0x1.0p-29, xfs[8 * c + i], acc[8 * c + i]);
+          }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acce);
+      if (lane == 0) {
+        if constexpr (RP) mbar_arrive_leader(&acce[abuf]);
+        else mbar_arrive(&acce[abuf]);
+      }
       if (et == 0 && it == nun - 1) OZ_TL(5)
       OZ_PROBE3(2)
 #if defined(OZ_EPI_V) && (OZ_EPI_V & 4)   // probe builds only: one store of the row sum, no fix-up
@@ -720,10 +904,10 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
               __threadfence();                       // the other partials are visible after the last arrival
               atomicExch(cnt, 0ull);                 // back to zero: a later launch with the same epoch starts clean
             }
-            xfsm[EPI_WARPS * 32] = last ? 1.0 : 0.0;  // broadcast to the epilogue warps
+            xfsm[EPI_WARPS * XFW] = last ? 1.0 : 0.0;  // broadcast to the epilogue warps
           }
           asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
-          write = xfsm[EPI_WARPS * 32] != 0.0;
+          write = xfsm[EPI_WARPS * XFW] != 0.0;
           if (write) {
 #pragma unroll
             for (int j = 0; j < NC; ++j) acc[j] = 0.0;
@@ -741,7 +925,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         if (write) {
           // A's exponent: 2^{E_row} for NN, 2^{E_max} for TN (exact, two factors)
           {
-            const int64_t gmr = (int64_t)mb * BM + row;
+            const int64_t gmr = (int64_t)(RP ? 2 * mb + crank : mb) * BM + row;
             const int e = TRANS ? (int)*g.emax - kEBias : (gmr < g.M ? g.erow[gmr] : 0);
             double p1, p2;
             pow2_split(e, p1, p2);
@@ -757,12 +941,12 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
             for (int j = 0; j < NC; ++j) stg[row * LDS + c0 + j] = acc[j];
             asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
             for (int r = warp - 4; r < BM; r += EPI_WARPS) {
-              const int64_t grow = (int64_t)mb * BM + r;
+              const int64_t grow = (int64_t)(RP ? 2 * mb + crank : mb) * BM + r;
               if (grow >= g.M) break;
               for (int j = lane; j < Nout; j += 32) Cout[grow * g.ldc + j] = stg[r * LDS + j];
             }
           } else {
-            const int64_t gm = (int64_t)mb * BM + row;
+            const int64_t gm = (int64_t)(RP ? 2 * mb + crank : mb) * BM + row;
             if (gm < g.M) {
               double* dsto = Cout + gm * g.ldc + c0;
 #pragma unroll
@@ -786,7 +970,8 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   if (threadIdx.x == 0) OZ_TL(4)
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    if constexpr (RP) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
   }
 }
 
@@ -807,6 +992,36 @@ static bool map_slices(CUtensorMap* mp, const int8_t* p, int64_t rows, int64_t n
              trans ? CU_TENSOR_MAP_SWIZZLE_128B : (bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// All S digit tiles of a unit in one box: dims {byte j < 128, row, digit, column
+// block} (strides not increasing: the row stride is the largest) so the box lands
+// as [digit][row][bytes] -- the per-digit tiles the MMA descriptors address.
+// NN: box {bk, 128 rows, S, 1} (K-major, SW64 / SW32); TN: box {128, bk rows, S, 1}
+// (MN-major, SW128).
+static bool map_slices_all(CUtensorMap* mp, const int8_t* p, int64_t rows, int64_t nblk, int S, bool trans, int bk) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {128, (cuuint64_t)rows, (cuuint64_t)S, (cuuint64_t)nblk};
+  cuuint64_t strides[3] = {(cuuint64_t)(128 * S * nblk), 128, (cuuint64_t)(128 * S)};
+  cuuint32_t box[4] = {trans ? 128u : (cuuint32_t)bk, trans ? (cuuint32_t)bk : 128u, (cuuint32_t)S, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             trans ? CU_TENSOR_MAP_SWIZZLE_128B : (bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// X slices xs[(t Np + j) ldk + k] viewed as {k, j < Np / 2, half, digit}: box
+// {bk, Np / 2, 1, S} = one CTA's column half of all S digit tiles, [digit][column][k]
+static bool map_x_halves(CUtensorMap* mp, const int8_t* p, int64_t K, int Np, int64_t ldk, int S, int bk) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)(Np / 2), 2, (cuuint64_t)S};
+  cuuint64_t strides[3] = {(cuuint64_t)ldk, (cuuint64_t)(ldk * (Np / 2)), (cuuint64_t)(ldk * Np)};
+  cuuint32_t box[4] = {(cuuint32_t)bk, (cuuint32_t)(Np / 2), 1, (cuuint32_t)S};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 static bool map_i8_2d(CUtensorMap* mp, const int8_t* p, int64_t cols, int64_t rows, int64_t ld, int box_rows, int bk) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
@@ -825,77 +1040,106 @@ static bool map_i8_2d(CUtensorMap* mp, const int8_t* p, int64_t cols, int64_t ro
 int ozaki_slices() { return OZ_S; }
 
 // Np <= 64 in one launch; 64 < Np <= 128 as two column blocks (64, Np - 64):
-// at Np = 128 one launch of CTA pairs (ozaki_pass_pair), else two launches over the same A slices (TMEM holds 7 groups x 64 columns)
+// at Np = 128 one launch of CTA pairs (ozaki_pass_pair), else two launches over the same A slices (TMEM holds S groups x 64 columns)
 bool ozaki_supported(int Np) { return Np <= 128 && Np % 16 == 0 && tc::get_encode() != nullptr; }
 
+// FP32 A (3 digits) at Np = 128: all 128 columns per CTA (3 groups x 128 TMEM
+// columns) -- MODE 3 row pairs (cta_group::2, default) or MODE 1 one CTA per
+// row block (RSVD_OZ_MODE128=1); RSVD_OZ_MODE128=2: the column-pair launch
+static int oz_mode128_env() {
+  static const int env = [] { const char* v = getenv("RSVD_OZ_MODE128"); return v ? atoi(v) : 3; }();
+  return env;
+}
+static bool oz_single128(int s, int Np) { return oz_mode128_env() != 2 && s == OZ_S32 && Np == 128; }
+int ozaki_x_cols(int s, int Np) { return oz_single128(s, Np) ? 128 : (Np < 64 ? Np : 64); }
+
 size_t ozaki_partial_bytes(int Np, int grid) {
-  return (size_t)grid * 2 * oz::BM * (size_t)(Np < 64 ? Np : 64) * sizeof(double);
+  return (size_t)grid * 2 * oz::BM * (size_t)(Np < 128 ? Np : 128) * sizeof(double);
 }
 
-size_t ozaki_a_bytes(int64_t m, int64_t n) {
+size_t ozaki_a_bytes(int64_t m, int64_t n, int s) {
   const int64_t ldn = round_up(n, oz::BKO);
-  return (size_t)OZ_S * m * ldn + 256 + (size_t)round_up(m, 64) * sizeof(int) + 512;
+  return (size_t)s * m * ldn + 256 + (size_t)round_up(m, 64) * sizeof(int) + 512;
 }
 
-size_t ozaki_x_bytes(int64_t K, int Np) {
+size_t ozaki_x_bytes(int64_t K, int Np, int s) {
   const int64_t ldk = round_up(K, 16);
-  return (size_t)OZ_S * Np * ldk + 256 + (size_t)round_up(ceil_div(K, oz::ET) * Np, 32) * sizeof(double) + 256;
+  return (size_t)s * Np * ldk + 256 + (size_t)round_up(ceil_div(K, oz::ET) * Np, 32) * sizeof(double) + 256;
 }
 
-cudaError_t ozaki_slice_a(const OzakiA& a, const double* A, int64_t lda, const double* c, const double* rs, int* flag,
-                          cudaStream_t st) {
+template <int S, typename T>
+static cudaError_t ozaki_slice_a_t(const OzakiA& a, const T* A, int64_t lda, const double* c, const double* rs,
+                                   int* flag, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(a.emax, 0, sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
-  // shared-memory staged rows (one buffer per warp, bulk copies) when 16-byte aligned rows fit
-  const int64_t rbuf = (a.n * 8 + 127) / 128 * 128;
-  const int64_t vecs = (int64_t)(c != nullptr) + (rs != nullptr);          // staged c / rs, rbuf bytes each
-  const int ngroups = (int)std::max<int64_t>(0, std::min<int64_t>(oz::SR_MAX_G, (oz::SR_SMEM - vecs * rbuf) / rbuf));
-  if (ngroups >= 2 && (a.n % 2 == 0) && (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0)) {
-    e = smem_optin(oz::ozaki_slice_rows_smem_kernel<OZ_S>);
+  // shared-memory staged rows (one buffer per group, bulk copies) when 16-byte aligned rows fit
+  const int64_t rbuf = (a.n * (int64_t)sizeof(T) + 127) / 128 * 128;
+  const int64_t vbuf = (a.n * 8 + 127) / 128 * 128;
+  const int64_t vecs = (int64_t)(c != nullptr) + (rs != nullptr);          // staged c / rs, vbuf bytes each
+  const int ngroups = (int)std::max<int64_t>(0, std::min<int64_t>(oz::SR_MAX_G, (oz::SR_SMEM - vecs * vbuf) / rbuf));
+  const int64_t qa = 16 / (int64_t)sizeof(T);                            // elements per 16 bytes
+  if (ngroups >= 2 && (a.n % qa == 0) && (lda % qa == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0)) {
+    e = smem_optin(oz::ozaki_slice_rows_smem_kernel<S, T>);
     if (e != cudaSuccess) return e;
-    e = launch_plain(oz::ozaki_slice_rows_smem_kernel<OZ_S>,
+    e = launch_plain(oz::ozaki_slice_rows_smem_kernel<S, T>,
                      dim3((unsigned)std::min<int64_t>(ceil_div(a.m, (int64_t)ngroups), 148)),
-                     dim3(32 * oz::SR_W * ngroups), (size_t)(ngroups + vecs) * rbuf, st, A, lda, a.m, a.n, c, rs, a.slices,
-                     a.ldn, a.erow, a.emax, flag);
+                     dim3(32 * oz::SR_W * ngroups), (size_t)(ngroups * rbuf + vecs * vbuf), st, A, lda, a.m, a.n, c, rs,
+                     a.slices, a.ldn, a.erow, a.emax, flag);
     if (e != cudaSuccess) return e;
     ++g_kernel_launches;
     return cudaGetLastError();
   }
   // otherwise one warp per row, rows in flight bounded so that the second read of
   // each row hits L1 / L2: at most ~256 KB of rows per SM
-  const int64_t row_bytes = std::max<int64_t>(a.n * 8, 1);
+  const int64_t row_bytes = std::max<int64_t>(a.n * (int64_t)sizeof(T), 1);
   const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(8, (256 << 10) / (8 * row_bytes)));
   const int64_t grid = std::min<int64_t>(ceil_div(a.m, 8), 148 * per_sm);
   // plain launch: it follows the memset of emax
-  e = launch_plain(oz::ozaki_slice_rows_kernel<OZ_S>, dim3((unsigned)grid), dim3(256), 0, st, A, lda, a.m, a.n, c, rs,
+  e = launch_plain(oz::ozaki_slice_rows_kernel<S, T>, dim3((unsigned)grid), dim3(256), 0, st, A, lda, a.m, a.n, c, rs,
                    a.slices, a.ldn, a.erow, a.emax, flag);
   if (e != cudaSuccess) return e;
   ++g_kernel_launches;
   return cudaGetLastError();
 }
 
-OzakiA ozaki_layout_a(void* buf, int64_t m, int64_t n) {
+cudaError_t ozaki_slice_a(const OzakiA& a, const void* A, bool f32, int64_t lda, const double* c, const double* rs,
+                          int* flag, cudaStream_t st) {
+  if (f32 && a.s == OZ_S32) return ozaki_slice_a_t<OZ_S32>(a, (const float*)A, lda, c, rs, flag, st);
+  if (!f32 && a.s == OZ_S) return ozaki_slice_a_t<OZ_S>(a, (const double*)A, lda, c, rs, flag, st);
+  return cudaErrorInvalidValue;
+}
+
+OzakiA ozaki_layout_a(void* buf, int64_t m, int64_t n, int s) {
   OzakiA a{};
-  a.m = m; a.n = n; a.ldn = round_up(n, oz::BKO);
+  a.m = m; a.n = n; a.ldn = round_up(n, oz::BKO); a.s = s;
   a.slices = reinterpret_cast<int8_t*>(buf);
-  a.erow = reinterpret_cast<int*>(reinterpret_cast<char*>(buf) + round_up((int64_t)OZ_S * m * a.ldn, 256));
+  a.erow = reinterpret_cast<int*>(reinterpret_cast<char*>(buf) + round_up((int64_t)s * m * a.ldn, 256));
   a.emax = reinterpret_cast<unsigned*>(a.erow + round_up(m, 64));
   return a;
 }
 
-static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st);
 // k per unit of the pass kernels: 64 (default) or 32 (RSVD_OZ_BK=32)
 static int oz_bk() {
   static const int v = [] { const char* e = getenv("RSVD_OZ_BK"); return (e && atoi(e) == 32) ? 32 : 64; }();
   return v;
 }
-static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st);
-static cudaError_t ozaki_pass_pair(const OzakiCall& h0, const OzakiCall& h1, cudaStream_t st);
+template <int S> static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st);
+template <int S> static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st);
+template <int S> static cudaError_t ozaki_pass_pair(const OzakiCall& h0, const OzakiCall& h1, cudaStream_t st);
+template <int S> static cudaError_t ozaki_pass_rowpair(const OzakiCall& c, cudaStream_t st);
 
 // X slicing of every column block first, then the pass kernel(s): c.mark (if
 // set) separates the two in time for the per-kernel profile.
-cudaError_t ozaki_pass(const OzakiCall& c, cudaStream_t st) {
-  if (!ozaki_supported(c.N) || c.M <= 0 || c.K <= 0) return cudaErrorInvalidValue;
+template <int S>
+static cudaError_t ozaki_pass_t(const OzakiCall& c, cudaStream_t st) {
+  if (oz_single128(S, c.N)) {
+    cudaError_t e = ozaki_slice_cols<S>(c, st);
+    if (e != cudaSuccess) return e;
+    if (c.mark) cudaEventRecord(c.mark, st);
+    if (c.mark2) cudaEventRecord(c.mark2, st);
+    if (oz_mode128_env() == 3 && c.grid >= 2) return ozaki_pass_rowpair<S>(c, st);
+    return ozaki_pass_cols<S>(c, st);
+  }
   OzakiCall h0 = c, h1 = c;
   const bool two = c.N > 64;
   if (two) {
@@ -904,29 +1148,37 @@ cudaError_t ozaki_pass(const OzakiCall& c, cudaStream_t st) {
     h1.xscratch = c.xscratch2;
     if (!c.xscratch2) return cudaErrorInvalidValue;
   }
-  cudaError_t e = ozaki_slice_cols(h0, st);
-  if (e == cudaSuccess && two) e = ozaki_slice_cols(h1, st);
+  cudaError_t e = ozaki_slice_cols<S>(h0, st);
+  if (e == cudaSuccess && two) e = ozaki_slice_cols<S>(h1, st);
   if (e != cudaSuccess) return e;
   if (c.mark) cudaEventRecord(c.mark, st);
   if (c.mark2) cudaEventRecord(c.mark2, st);
   // Np = 128: both halves in one launch of CTA pairs sharing A (RSVD_OZ_PAIR=0: two launches)
   static const int env_pair = [] { const char* v = getenv("RSVD_OZ_PAIR"); return v ? atoi(v) : 1; }();
-  if (two && c.N == 128 && h1.Nout > 0 && env_pair != 0 && c.grid >= 2) return ozaki_pass_pair(h0, h1, st);
-  e = ozaki_pass_cols(h0, st);
-  if (e == cudaSuccess && two && h1.Nout > 0) e = ozaki_pass_cols(h1, st);
+  if (two && c.N == 128 && h1.Nout > 0 && env_pair != 0 && c.grid >= 2) return ozaki_pass_pair<S>(h0, h1, st);
+  e = ozaki_pass_cols<S>(h0, st);
+  if (e == cudaSuccess && two && h1.Nout > 0) e = ozaki_pass_cols<S>(h1, st);
   return e;
 }
 
+cudaError_t ozaki_pass(const OzakiCall& c, cudaStream_t st) {
+  if (!ozaki_supported(c.N) || c.M <= 0 || c.K <= 0) return cudaErrorInvalidValue;
+  if (c.a->s == OZ_S) return ozaki_pass_t<OZ_S>(c, st);
+  if (c.a->s == OZ_S32) return ozaki_pass_t<OZ_S32>(c, st);
+  return cudaErrorInvalidValue;
+}
+
+template <int S>
 static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st) {
   using namespace oz;
   const int N = c.N;
   const int64_t ldk = round_up(c.K, 16);
   int8_t* xs = reinterpret_cast<int8_t*>(c.xscratch);
-  double* xf = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
-  const cudaError_t ea = smem_optin(ozaki_slice_x_kernel<OZ_S>);
+  double* xf = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xscratch) + round_up((int64_t)S * N * ldk, 256));
+  const cudaError_t ea = smem_optin(ozaki_slice_x_kernel<S>);
   if (ea != cudaSuccess) return ea;
   const dim3 gs((unsigned)ceil_div(ldk, ET), (unsigned)ceil_div(N, XT_COLS));
-  const cudaError_t el = launch_pdl(ozaki_slice_x_kernel<OZ_S>, gs, dim3(XT_THREADS), (size_t)xt_smem(OZ_S), st, c.B, c.ldb, c.K, N, xs, ldk, xf,
+  const cudaError_t el = launch_pdl(ozaki_slice_x_kernel<S>, gs, dim3(XT_THREADS), (size_t)xt_smem(S), st, c.B, c.ldb, c.K, N, xs, ldk, xf,
                                    c.flags ? c.flags + kEpochSlot : nullptr,
                                    c.trans ? (const int*)c.a->erow : nullptr, (const unsigned*)c.a->emax);
   if (el != cudaSuccess) return el;
@@ -934,6 +1186,7 @@ static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int S>
 static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
   using namespace oz;
   const OzakiA& a = *c.a;
@@ -941,17 +1194,12 @@ static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
   // X slices (ozaki_slice_cols) are in c.xscratch
   const int64_t ldk = round_up(c.K, 16);
   int8_t* xs = reinterpret_cast<int8_t*>(c.xscratch);
-  double* xf = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
+  double* xf = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xscratch) + round_up((int64_t)S * N * ldk, 256));
   // 2) tensor maps: A slices as (cols = n, rows = m, S); X slices as (cols = K, rows = S * N)
   const int bk = oz_bk();
   CUtensorMap mA, mX;
-  if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, OZ_S, c.trans, bk)) return cudaErrorInvalidValue;
-  if (!map_i8_2d(&mX, xs, c.K, (int64_t)OZ_S * N, ldk, N, bk)) {
-#ifdef OZ_DEBUG
-    printf("map X failed: xs %p K %lld rows %lld ldk %lld box %d\n", (void*)xs, (long long)c.K, (long long)OZ_S * N, (long long)ldk, N);
-#endif
-    return cudaErrorInvalidValue;
-  }
+  if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, S, c.trans, bk)) return cudaErrorInvalidValue;
+  if (!map_i8_2d(&mX, xs, c.K, (int64_t)S * N, ldk, N, bk)) return cudaErrorInvalidValue;
   Args g{};
   g.C = c.C; g.ldc = c.ldc; g.P = c.P; g.flags = c.flags; g.epoch = c.epoch;
   g.erow = a.erow; g.emax = a.emax; g.xf = xf;
@@ -964,16 +1212,23 @@ static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
   if (grid > c.grid) grid = c.grid;
   if (grid < 1) grid = 1;
   g.grid = (int)grid;
-  const int Nt = N <= 16 ? 16 : N <= 32 ? 32 : N <= 48 ? 48 : 64;
-  const size_t smem = (size_t)oz_nbuf(OZ_S, Nt, bk) * oz_ubuf(OZ_S, Nt, bk) + 1024;
+  const int Nt = N <= 16 ? 16 : N <= 32 ? 32 : N <= 48 ? 48 : N <= 64 ? 64 : 128;
+  const size_t smem = (size_t)oz_nbuf(S, Nt, bk) * oz_ubuf(S, Nt, bk) + 1024;
   cudaError_t e = cudaSuccess;
 #define RSVD_OZ(TR, NN)                                                                                   \
   if (bk == 64) RSVD_OZB(TR, NN, 64) else RSVD_OZB(TR, NN, 32)
 #define RSVD_OZB(TR, NN, BK)                                                                              \
   {                                                                                                      \
-    e = smem_optin(ozaki_pass_kernel<TR, OZ_S, NN, 1, BK>); if (e != cudaSuccess) return e;                                                                                                     \
-    e = launch_pdl(ozaki_pass_kernel<TR, OZ_S, NN, 1, BK>, dim3(g.grid), dim3(THREADS), smem, st, mA, mX, mX, g); \
+    e = smem_optin(ozaki_pass_kernel<TR, S, NN, 1, BK>); if (e != cudaSuccess) return e;                \
+    e = launch_pdl(ozaki_pass_kernel<TR, S, NN, 1, BK>, dim3(g.grid), dim3(oz_threads(NN)), smem, st, mA, mX, mX, g); \
     if (e != cudaSuccess) return e;                                                                      \
+  }
+  if constexpr (S == OZ_S32) {
+    if (N == 128) {
+      if (!c.trans) RSVD_OZ(false, 128) else RSVD_OZ(true, 128)
+      ++g_kernel_launches;
+      return cudaGetLastError();
+    }
   }
   if (!c.trans) {
     switch (N) { case 16: RSVD_OZ(false, 16) break; case 32: RSVD_OZ(false, 32) break;
@@ -990,6 +1245,7 @@ static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
 
 // Np = 128: one launch of 2-CTA clusters, CTA r of a pair computing column
 // half r (h0 / h1, each sliced into its own X scratch) over the same units.
+template <int S>
 static cudaError_t ozaki_pass_pair(const OzakiCall& h0, const OzakiCall& h1, cudaStream_t st) {
   using namespace oz;
   const OzakiA& a = *h0.a;
@@ -997,12 +1253,12 @@ static cudaError_t ozaki_pass_pair(const OzakiCall& h0, const OzakiCall& h1, cud
   const int64_t ldk = round_up(h0.K, 16);
   int8_t* xs0 = reinterpret_cast<int8_t*>(h0.xscratch);
   int8_t* xs1 = reinterpret_cast<int8_t*>(h1.xscratch);
-  const double* xf0 = reinterpret_cast<const double*>(reinterpret_cast<char*>(h0.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
-  const double* xf1 = reinterpret_cast<const double*>(reinterpret_cast<char*>(h1.xscratch) + round_up((int64_t)OZ_S * N * ldk, 256));
+  const double* xf0 = reinterpret_cast<const double*>(reinterpret_cast<char*>(h0.xscratch) + round_up((int64_t)S * N * ldk, 256));
+  const double* xf1 = reinterpret_cast<const double*>(reinterpret_cast<char*>(h1.xscratch) + round_up((int64_t)S * N * ldk, 256));
   const int bk = oz_bk();
   CUtensorMap mA, mX0, mX1;
-  if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, OZ_S, h0.trans, bk)) return cudaErrorInvalidValue;
-  if (!map_i8_2d(&mX0, xs0, h0.K, (int64_t)OZ_S * N, ldk, N, bk) || !map_i8_2d(&mX1, xs1, h1.K, (int64_t)OZ_S * N, ldk, N, bk))
+  if (!map_slices(&mA, a.slices, a.m, a.ldn / BKO, S, h0.trans, bk)) return cudaErrorInvalidValue;
+  if (!map_i8_2d(&mX0, xs0, h0.K, (int64_t)S * N, ldk, N, bk) || !map_i8_2d(&mX1, xs1, h1.K, (int64_t)S * N, ldk, N, bk))
     return cudaErrorInvalidValue;
   Args g{};
   g.C = h0.C; g.ldc = h0.ldc; g.P = h0.P; g.flags = h0.flags; g.epoch = h0.epoch;
@@ -1017,14 +1273,14 @@ static cudaError_t ozaki_pass_pair(const OzakiCall& h0, const OzakiCall& h1, cud
   if (npair > h0.grid / 2) npair = h0.grid / 2;
   if (npair < 1) npair = 1;
   g.grid = (int)(2 * npair);
-  const size_t smem = (size_t)oz_nbuf(OZ_S, N, bk) * oz_ubuf(OZ_S, N, bk) + 1024;
+  const size_t smem = (size_t)oz_nbuf(S, N, bk) * oz_ubuf(S, N, bk) + 1024;
   cudaError_t e = cudaSuccess;
 #define RSVD_OZP(TR)                                                                                      \
   if (bk == 64) RSVD_OZPB(TR, 64) else RSVD_OZPB(TR, 32)
 #define RSVD_OZPB(TR, BK)                                                                                 \
   {                                                                                                      \
-    e = smem_optin(ozaki_pass_kernel<TR, OZ_S, N, 2, BK>); if (e != cudaSuccess) return e;                                                                                                     \
-    e = launch_pdl_cluster(ozaki_pass_kernel<TR, OZ_S, N, 2, BK>, dim3(g.grid), dim3(THREADS), smem, st, 2u, mA, mX0, mX1, g); \
+    e = smem_optin(ozaki_pass_kernel<TR, S, N, 2, BK>); if (e != cudaSuccess) return e;                 \
+    e = launch_pdl_cluster(ozaki_pass_kernel<TR, S, N, 2, BK>, dim3(g.grid), dim3(THREADS), smem, st, 2u, mA, mX0, mX1, g); \
     if (e != cudaSuccess) return e;                                                                      \
   }
   if (!h0.trans) RSVD_OZP(false) else RSVD_OZP(true)
@@ -1032,6 +1288,52 @@ static cudaError_t ozaki_pass_pair(const OzakiCall& h0, const OzakiCall& h1, cud
 #undef RSVD_OZPB
   ++g_kernel_launches;
   return cudaGetLastError();
+}
+
+// MODE 3 (FP32 A at Np = 128): clusters of two CTAs over pairs of 128-row
+// blocks, one cta_group::2 MMA (M = 256, N = 128) per digit product.
+template <int S>
+static cudaError_t ozaki_pass_rowpair(const OzakiCall& c, cudaStream_t st) {
+  using namespace oz;
+  if constexpr (S != OZ_S32) {
+    return cudaErrorInvalidValue;
+  } else {
+    const OzakiA& a = *c.a;
+    constexpr int N = 128;
+    const int64_t ldk = round_up(c.K, 16);
+    int8_t* xs = reinterpret_cast<int8_t*>(c.xscratch);
+    const double* xf = reinterpret_cast<const double*>(reinterpret_cast<char*>(c.xscratch) + round_up((int64_t)S * N * ldk, 256));
+    const int bk = oz_bk();
+    CUtensorMap mA, mX;
+    if (!map_slices_all(&mA, a.slices, a.m, a.ldn / BKO, S, c.trans, bk)) return cudaErrorInvalidValue;
+    if (!map_x_halves(&mX, xs, c.K, N, ldk, S, bk)) return cudaErrorInvalidValue;   // half the columns per CTA
+    Args g{};
+    g.C = c.C; g.ldc = c.ldc; g.P = c.P; g.flags = c.flags; g.epoch = c.epoch;
+    g.erow = a.erow; g.emax = a.emax; g.xf = xf;
+    g.C2 = c.C; g.xf2 = xf; g.Nout2 = c.Nout;
+    g.M = c.M; g.K = c.K; g.N = N; g.Nout = c.Nout; g.Np = N;
+    g.KB = ceil_div(c.K, bk);
+    const int64_t mpairs = ceil_div(c.M, 2 * BM);                    // 256-row unit blocks
+    g.units = mpairs * g.KB;
+    int64_t npair = g.units / (256 / bk);
+    if (npair < mpairs) npair = mpairs;
+    if (npair > c.grid / 2) npair = c.grid / 2;
+    if (npair < 1) npair = 1;
+    g.grid = (int)(2 * npair);
+    const size_t smem = (size_t)oz_nbuf(S, N / 2, bk) * oz_ubuf(S, N / 2, bk) + 1024;
+    cudaError_t e = cudaSuccess;
+#define RSVD_OZR(TR, BK)                                                                                  \
+    {                                                                                                    \
+      e = smem_optin(ozaki_pass_kernel<TR, S, N, 3, BK>); if (e != cudaSuccess) return e;               \
+      e = launch_pdl_cluster(ozaki_pass_kernel<TR, S, N, 3, BK>, dim3(g.grid), dim3(oz_threads(N)), smem, st, 2u, mA, mX, mX, g); \
+      if (e != cudaSuccess) return e;                                                                    \
+    }
+    if (bk == 64) { if (!c.trans) RSVD_OZR(false, 64) else RSVD_OZR(true, 64) }
+    else { if (!c.trans) RSVD_OZR(false, 32) else RSVD_OZR(true, 32) }
+#undef RSVD_OZR
+    ++g_kernel_launches;
+    return cudaGetLastError();
+  }
 }
 
 }  // namespace rsvd

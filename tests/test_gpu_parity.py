@@ -644,16 +644,77 @@ def test_config5_full_size_rrpca(rb):
 
 
 # ----------------------------------------------------------------------------- FP32 on tcgen05
-@pytest.mark.parametrize("m,n,k,p,q", [(3000, 700, 30, 10, 2), (5000, 1200, 100, 20, 3), (777, 2000, 20, 12, 1)])
-def test_rsvd_fp32_tcgen05_parity(rb, m, n, k, p, q):
-    """FP32 A through the tcgen05 3xTF32 passes (TMA + TMEM): singular values within
-    1e-4 of the FP64 oracle on the same FP32 data (J:5), orthonormality 1e-5."""
+def _ctx_fp32_path(rb, path):
+    import os
+    old = os.environ.get("RSVD_FP32_PATH")
+    os.environ["RSVD_FP32_PATH"] = path
+    try:
+        return rb.Context(0)
+    finally:
+        if old is None:
+            del os.environ["RSVD_FP32_PATH"]
+        else:
+            os.environ["RSVD_FP32_PATH"] = old
+
+
+@pytest.mark.parametrize("path", ["ozaki", "tf32"])
+@pytest.mark.parametrize("m,n,k,p,q", [(3000, 700, 30, 10, 2), (5000, 1200, 100, 20, 3), (777, 2000, 20, 12, 1),
+                                       (4099, 1030, 50, 14, 2)])
+def test_rsvd_fp32_tcgen05_parity(rb, m, n, k, p, q, path):
+    """FP32 A through the tcgen05 passes -- 3-digit Ozaki int8 slices (default)
+    or 3xTF32 (RSVD_FP32_PATH=tf32): singular values within 1e-4 of the FP64
+    oracle on the same FP32 data (J:5), orthonormality 1e-5.  (4099, 1030):
+    ragged row block and a row length that is not a multiple of 4 (the
+    warp-per-row slicer)."""
     A = _decay_matrix(m, n, seed=m + 3 * n, noise=1e-5).to(torch.float32)
     An = A.numpy()
-    r = rb.rsvd(A.cuda(), k, p=p, q=q, seed=12)
+    ctx = _ctx_fp32_path(rb, path)
+    r = rb.rsvd(A.cuda(), k, p=p, q=q, seed=12, ctx=ctx)
+    assert (ctx.stats()["ozaki_passes"] > 0) == (path == "ozaki")
     o = oracle.oracle_rsvd(An, k, p=p, q=q, seed=12)
     _check_parity(An.astype(np.float64), r, o, k, tol_d=1e-4, tol_orth=1e-5, floor=1e-6, gap_tol=1e-3, cos_tol=1e-5,
                   ang_tol=1e-3)
+
+
+def test_rsvd_fp32_ozaki_matches_fp64(rb):
+    """The 3-digit slices of FP32 A keep 24 bits per element relative to its
+    row maximum and the X panel 22 bits: the FP32 run agrees with the FP64
+    Ozaki run on the exactly upcast matrix to ~1e-6 (far inside J:5's 1e-4),
+    including rows spanning four decades."""
+    A = _decay_matrix(2600, 900, seed=77, noise=1e-5).numpy()
+    A = A * (10.0 ** np.random.default_rng(3).uniform(-4, 0, size=(A.shape[0], 1)))
+    A32 = torch.from_numpy(A).to(torch.float32)
+    r32 = rb.rsvd(A32.cuda(), 40, p=10, q=2, seed=5)
+    r64 = rb.rsvd(A32.double().cuda(), 40, p=10, q=2, seed=5)
+    d32, d64 = _np(r32.d).astype(np.float64), _np(r64.d)
+    assert np.max(np.abs(d32 - d64) / d64) < 2e-6
+
+
+def test_rsvd_fp32_ozaki_top_binade(rb):
+    """Elements within half a unit below the row's power of two (|a| = 2^E (1 -
+    2^-24)) round to 2^23 at 24 bits: the slicer clamps instead of wrapping
+    the two's-complement top digit.  Rows of +-0.99999994 * 2^e_r plus a
+    rank-3 signal; d within 1e-4 of the oracle."""
+    rng = np.random.default_rng(11)
+    m, n = 2048, 768
+    top = np.float32(1.0) - np.float32(2.0 ** -24)
+    A = np.where(rng.random((m, n)) < 0.5, -top, top).astype(np.float32)
+    A *= (2.0 ** rng.integers(-3, 4, size=(m, 1))).astype(np.float32)
+    A[:, :3] *= np.float32(0.5)
+    r = rb.rsvd(torch.from_numpy(A).cuda(), 10, p=10, q=1, seed=2)
+    o = oracle.oracle_rsvd(A.astype(np.float64), 10, p=10, q=1, seed=2)
+    assert np.max(np.abs(_np(r.d).astype(np.float64) - o["d"]) / o["d"]) < 1e-4
+
+
+def test_rpca_fp32_centred_ozaki(rb):
+    """FP32 rpca: the centring / scaling is applied in FP64 to the upcast FP32
+    elements inside the 3-digit slicer; eigenvalues within 1e-4 of the oracle."""
+    A = (_decay_matrix(3000, 500, seed=8, noise=1e-4).numpy() + 3.0).astype(np.float32)
+    for scale in (False, True):
+        r = rb.rpca(torch.from_numpy(A).cuda(), 20, center=True, scale=scale, p=10, q=2, seed=3)
+        o = oracle.oracle_rpca(A.astype(np.float64), 20, center=True, scale=scale, p=10, q=2, seed=3)
+        ev, eo = _np(r["eigvals"]).astype(np.float64), o["eigvals"]
+        assert np.max(np.abs(ev - eo) / eo) < 1e-4
 
 
 # ----------------------------------------------------------------------------- FP64 pass paths
