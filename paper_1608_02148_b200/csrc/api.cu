@@ -608,7 +608,11 @@ rsvd_status orth(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool dist, dou
   const int l = p.l, Np = p.Np;
   Prof pr_(ctx, 2, (double)rows * Np * 8 * 4);
   if (!dist && small_panel(rows, l)) {
-    CK(launch_hqr_leaves(S, Np, rows, l, 1, p.Rsm, ctx->stream));
+    // register-column Householder when the panel fits (l <= 32, rows <= 1024), else in shared memory
+    static const bool small_regs = [] { const char* v = getenv("RSVD_HQR_REGS"); return !v || atoi(v) != 0; }();
+    const cudaError_t eh = small_regs ? launch_hqr_small(S, Np, rows, l, p.Rsm, ctx->stream) : cudaErrorNotSupported;
+    if (eh == cudaErrorNotSupported) CK(launch_hqr_leaves(S, Np, rows, l, 1, p.Rsm, ctx->stream));
+    else CK(eh);
     if (Rout) CK(launch_copy_out(p.Rsm, l, l, l, Rout, Np, false, nullptr, ctx->stream));
     return RSVD_OK;
   }

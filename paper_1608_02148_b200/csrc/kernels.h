@@ -131,6 +131,9 @@ cudaError_t launch_small_matmul(const double* A, const double* B, double* C, int
 // columns).  Explicit Q overwrites the leaf rows; R (l x l, diag >= 0) goes to
 // Rstack + leaf*l*l (ld l).
 int leaf_rows_cap(int l);
+// Register-column Householder QR of one small panel (M <= 1024 rows, l <= 32):
+// Q in place, R (diag >= 0, row-major l x l); cudaErrorNotSupported if it does not fit.
+cudaError_t launch_hqr_small(double* Y, int64_t ldy, int64_t M, int l, double* R, cudaStream_t st);
 cudaError_t launch_hqr_leaves(double* Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
                               double* Rstack, cudaStream_t st, Pred pr = Pred{});
 // Q rows of each leaf <- Q rows * S_leaf, S_leaf = rows [leaf*l, leaf*l+l) of S (ld lds).

@@ -437,6 +437,134 @@ cudaError_t launch_hqr_leaves(double* Y, int64_t ldy, int64_t M, int l, int64_t 
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ register-column Householder
+// The single-CTA panel QR of hqr_leaf for small panels (b <= 32 RPL rows, l <= 32
+// columns) with the panel held in REGISTERS: warp c owns column c (row r = lane +
+// 32 i in element i), so the trailing update of a column step reads only the
+// Householder vector from shared memory (hqr_leaf re-reads the vector and every
+// trailing column from shared memory twice per step: ~760 KB per step at 1000 x
+// 20, bound by shared-memory bandwidth).  Same LAPACK dgeqr2 /
+// dorg2r arithmetic and conventions (v_j = 1 implicit, sign(0) = +1, tau = 0 for a
+// zero column: R_jj = 0, reading R6), same outputs: Q in place, R (diag >= 0)
+// row-major l x l.  The explicit Q needs no barrier: warp c applies H_c .. H_0 to
+// e_c on its own (the vectors are read-only by then).
+template <int RPL>
+__global__ void __launch_bounds__(RPL >= 32 ? 640 : 1024, 1)
+hqr_cols_kernel(double* __restrict__ Y, int64_t ldy, int b, int l, double* __restrict__ Rout) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int B = 32 * RPL;
+  extern __shared__ double sv[];
+  double* V = sv;                      // l x B, column j = v_j (zeros above row j)
+  double* tau = V + (int64_t)l * B;    // l
+  double* Rs = tau + l;                // l x l row-major (upper part)
+  const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+  double y[RPL];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = lane + 32 * i;
+    y[i] = r < b ? Y[(int64_t)r * ldy + c] : 0.0;
+  }
+  for (int j = 0; j < l; ++j) {
+    if (c == j) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = lane + 32 * i;
+        if (r > j) s += y[i] * y[i];
+      }
+      s = warp_sum(s);
+      double x0 = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i)
+        if (i == (j >> 5)) x0 = y[i];
+      x0 = __shfl_sync(0xffffffffu, x0, j & 31);
+      double t = 0.0, beta = x0, scal = 0.0;
+      if (s != 0.0) {
+        const double nrm = sqrt(x0 * x0 + s);
+        beta = -copysign(nrm, x0);                 // sign(0) = +1 => beta = -||x||
+        t = (beta - x0) / beta;
+        scal = 1.0 / (x0 - beta);
+      }
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = lane + 32 * i;
+        if (r < j) Rs[r * l + j] = y[i];
+        V[(int64_t)j * B + r] = r > j ? y[i] * scal : (r == j ? 1.0 : 0.0);
+      }
+      if (lane == 0) { tau[j] = t; Rs[j * l + j] = beta; }
+    }
+    __syncthreads();
+    if (c > j) {
+      const double t = tau[j];
+      if (t != 0.0) {
+        const double* v = V + (int64_t)j * B + lane;
+        double w = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) w += v[32 * i] * y[i];
+        const double f = t * warp_sum(w);
+        // re-read v (volatile): holding it across the reduction would double the registers
+        const volatile double* vv = v;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) y[i] -= f * vv[32 * i];
+      }
+    }
+  }
+  __syncthreads();
+  // explicit Q column c = H_0 ... H_c e_c (H_i e_c = e_c for i > c), diag(R) >= 0
+  const double sg = Rs[c * l + c] < 0.0 ? -1.0 : 1.0;
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) y[i] = (lane + 32 * i == c) ? 1.0 : 0.0;
+  for (int i = c; i >= 0; --i) {
+    const double t = tau[i];
+    if (t == 0.0) continue;
+    const double* v = V + (int64_t)i * B + lane;
+    double w = 0.0;
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) w += v[32 * e] * y[e];
+    const double f = t * warp_sum(w);
+    const volatile double* vv = v;
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) y[e] -= f * vv[32 * e];
+  }
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = lane + 32 * i;
+    if (r < b) Y[(int64_t)r * ldy + c] = sg * y[i];
+  }
+  // R row c: (diag sign of row c) x upper part; zeros below the diagonal
+  for (int e = lane; e < l; e += 32) Rout[c * l + e] = e >= c ? sg * Rs[c * l + e] : 0.0;
+}
+
+// Register-column Householder for a b x l panel if it fits (l <= 32, b <= 1024 and
+// the registers of 32 l threads); cudaErrorNotSupported otherwise (the caller
+// uses launch_hqr_leaves).
+cudaError_t launch_hqr_small(double* Y, int64_t ldy, int64_t M, int l, double* R, cudaStream_t st) {
+  if (l < 1 || l > 32 || M < l || M > 1024) return cudaErrorNotSupported;
+  int rpl = 4;
+  while (32 * rpl < M) rpl *= 2;
+  // registers: ~2 RPL + 32 per thread within 65536 / (32 l); RPL = 32 needs l <= 20
+  if ((rpl == 32 && l > 20) || 64 * rpl + 1024 > 65536 / l) return cudaErrorNotSupported;
+  const size_t smem = ((size_t)l * 32 * rpl + l + (size_t)l * l) * sizeof(double);
+  cudaError_t e = cudaSuccess;
+#define RSVD_HQC(RP)                                                                                  \
+  {                                                                                                  \
+    e = set_smem((const void*)hqr_cols_kernel<RP>, smem);                                            \
+    if (e != cudaSuccess) return e;                                                                  \
+    e = launch_pdl(hqr_cols_kernel<RP>, dim3(1), dim3(32 * l), smem, st, Y, ldy, (int)M, l, R);      \
+  }
+  switch (rpl) {
+    case 4: RSVD_HQC(4) break;
+    case 8: RSVD_HQC(8) break;
+    case 16: RSVD_HQC(16) break;
+    default: RSVD_HQC(32) break;
+  }
+#undef RSVD_HQC
+  if (e != cudaSuccess) return e;
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
 // Q rows of leaf `leaf` <- Q rows * S_leaf (S_leaf = rows [leaf l, leaf l + l) of S)
 __device__ void tsqr_combine_leaf(double* __restrict__ Y, int64_t ldy, int64_t M, int l, int64_t nleaves,
                                   int64_t leaf, const double* __restrict__ S, int64_t lds) {
