@@ -493,8 +493,11 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
   __shared__ double red[XT_G][XT_COLS];
   __shared__ double escale[XT_COLS][2];
   const int tid = threadIdx.x, c = tid & (XT_COLS - 1), g = tid / XT_COLS;
-  const int64_t sb = blockIdx.x, k0 = sb * ET;
-  const int j = blockIdx.y * XT_COLS + c;
+  // grid: x = column group (fastest), y = super-block, so the CTAs reading the
+  // column groups of the same rows run together (whole rows from DRAM, not
+  // 64-byte pieces of rows read at different times)
+  const int64_t sb = blockIdx.y, k0 = sb * ET;
+  const int j = blockIdx.x * XT_COLS + c;
   const bool jv = j < Np;
   double v[XT_V];
   double mx = 0.0;
@@ -510,11 +513,15 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
     }
     mx = fmax(mx, fabs(v[i]));
   }
-  red[g][c] = mx;
+  // column maxima: the 4 row groups of a warp by shuffles (lane bits 3, 4), then
+  // the 16 warp maxima of a column by one thread (fixed order: deterministic)
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+  if ((threadIdx.x & 31) < XT_COLS) red[threadIdx.x >> 5][c] = mx;
   __syncthreads();
   if (g == 0) {
     double m2 = red[0][c];
-    for (int r = 1; r < XT_G; ++r) m2 = fmax(m2, red[r][c]);
+    for (int r = 1; r < XT_THREADS / 32; ++r) m2 = fmax(m2, red[r][c]);
     const int E = block_exp(m2);
     if (jv) xf[sb * Np + j] = ldexp(1.0, E);
     pow2_split(8 * S - 2 - E, escale[c][0], escale[c][1]);
@@ -539,7 +546,7 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
   for (int e = tid; e < S * XT_COLS * chunks; e += XT_THREADS) {
     const int row = e / chunks, ch = e - row * chunks;
     const int t = row / XT_COLS, cc = row - t * XT_COLS;
-    const int jj = blockIdx.y * XT_COLS + cc;
+    const int jj = blockIdx.x * XT_COLS + cc;
     if (jj >= Np) continue;
     *reinterpret_cast<uint4*>(xs + ((int64_t)t * Np + jj) * ldk + k0 + 16 * ch) =
         *reinterpret_cast<const uint4*>(xt + row * XT_LD + 16 * ch);
@@ -1177,7 +1184,7 @@ static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st) {
   double* xf = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xscratch) + round_up((int64_t)S * N * ldk, 256));
   const cudaError_t ea = smem_optin(ozaki_slice_x_kernel<S>);
   if (ea != cudaSuccess) return ea;
-  const dim3 gs((unsigned)ceil_div(ldk, ET), (unsigned)ceil_div(N, XT_COLS));
+  const dim3 gs((unsigned)ceil_div(N, XT_COLS), (unsigned)ceil_div(ldk, ET));
   const cudaError_t el = launch_pdl(ozaki_slice_x_kernel<S>, gs, dim3(XT_THREADS), (size_t)xt_smem(S), st, c.B, c.ldb, c.K, N, xs, ldk, xf,
                                    c.flags ? c.flags + kEpochSlot : nullptr,
                                    c.trans ? (const int*)c.a->erow : nullptr, (const unsigned*)c.a->emax);
