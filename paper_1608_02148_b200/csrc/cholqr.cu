@@ -512,6 +512,99 @@ panel_apply_kernel(const double* S, int64_t lds, int64_t rows, int Np, const dou
   cp_async_wait<0>();
 }
 
+// Np in (96, 128] (configs 3 and 4): 32-row blocks, double-buffered (T takes 135
+// KB of shared memory, so 64-row blocks fit only once: the load of the next block
+// was exposed), and warps over column PAIRS of 8-column tiles (w, 15 - w): with
+// an upper-triangular T (R^-1) tile j needs k < 8 j + 8, so every warp does the
+// same 17 x 8 k-steps instead of 32 .. 128 (the slowest warp set the pace).
+constexpr int AP2_BM = 32;
+__global__ void __launch_bounds__(CQ_THREADS, 1)
+panel_apply128_kernel(const double* S, int64_t lds, int64_t rows, int Np, const double* __restrict__ T,
+                      int64_t ldt, double* C, int64_t ldc, int Nout, int upper, Pred pr) {
+  pdl_wait();
+  pdl_trigger();
+  if (pred_skip(pr)) return;
+  constexpr int NG = 128, LDX = NG + ((4 - NG) & 15);
+  extern __shared__ __align__(16) double sm[];
+  const int LDSS = Np + ((4 - Np) & 15);
+  double* Ts = sm;                        // Np x LDX
+  double* Ss = sm + Np * LDX;             // 2 x AP2_BM x LDSS
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int cpr = Np / 2;
+  const int64_t nblk = ceil_div(rows, AP2_BM);
+  const int jt[2] = {warp, 15 - warp};                 // the warp's two 8-column tiles
+  const int kend0 = upper ? min(Np, 8 * jt[0] + 8) : Np;
+  const int kend1 = upper ? min(Np, 8 * jt[1] + 8) : Np;   // >= kend0
+  for (int ch = tid; ch < Np * cpr; ch += CQ_THREADS) {
+    const int r = ch / cpr, c = (ch - r * cpr) * 2;
+    cp_async16(Ts + r * LDX + c, T + r * ldt + c, 16);
+  }
+  for (int e = tid; e < Np * (NG - Np); e += CQ_THREADS) {
+    const int r = e / (NG - Np), c = Np + e % (NG - Np);
+    Ts[r * LDX + c] = 0.0;
+  }
+  auto load = [&](int buf, int64_t rb) {
+    double* ss = Ss + buf * AP2_BM * LDSS;
+    const int64_t m0 = rb * AP2_BM;
+    for (int ch = tid; ch < AP2_BM * cpr; ch += CQ_THREADS) {
+      const int r = ch / cpr, c = (ch - r * cpr) * 2;
+      const bool ok = m0 + r < rows;
+      cp_async16(ss + r * LDSS + c, ok ? S + (m0 + r) * lds + c : S, ok ? 16 : 0);
+    }
+  };
+  int64_t rb = blockIdx.x;
+  if (rb < nblk) load(0, rb);
+  cp_async_commit();
+  for (int it = 0; rb < nblk; ++it, rb += gridDim.x) {
+    const int buf = it & 1;
+    if (rb + gridDim.x < nblk) load(buf ^ 1, rb + gridDim.x);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* ss = Ss + buf * AP2_BM * LDSS;
+    double acc[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    int kk = 0;
+    for (; kk < kend0; kk += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = ss[(i * 8 + gq) * LDSS + kk + tq];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = Ts[(kk + tq) * LDX + jt[j] * 8 + gq];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    for (; kk < kend1; kk += 4) {
+      double af[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = ss[(i * 8 + gq) * LDSS + kk + tq];
+      const double bf = Ts[(kk + tq) * LDX + jt[1] * 8 + gq];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dmma884(acc[i][1][0], acc[i][1][1], af[i], bf);
+    }
+    const int64_t m0 = rb * AP2_BM;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t r = m0 + i * 8 + gq;
+      if (r >= rows) continue;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = jt[j] * 8 + 2 * tq;
+        if (c < Nout) C[r * ldc + c] = acc[i][j][0];
+        if (c + 1 < Nout) C[r * ldc + c + 1] = acc[i][j][1];
+      }
+    }
+    __syncthreads();                      // buffer `buf` is refilled in iteration it + 2
+  }
+  cp_async_wait<0>();
+}
+
 cudaError_t launch_panel_apply(const double* S, int64_t lds, int64_t rows, int Np, const double* T, int64_t ldt,
                                double* C, int64_t ldc, int Nout, bool upper, int num_sms, cudaStream_t st, Pred pr) {
   if (Np % 4 || Np > 128 || (lds & 1) || (ldt & 1) || rows < 1) return cudaErrorInvalidValue;
@@ -532,6 +625,19 @@ cudaError_t launch_panel_apply(const double* S, int64_t lds, int64_t rows, int N
     e = smem_optin(panel_apply_kernel<TJ, (TJ == 4 ? 1 : 2)>); if (e != cudaSuccess) return e;                                                                                                     \
     e = launch_pdl(panel_apply_kernel<TJ, (TJ == 4 ? 1 : 2)>, dim3((unsigned)grid), dim3(CQ_THREADS), smem, st, S, lds, rows, Np, T, ldt, C, ldc, Nout, upper ? 1 : 0, pr); \
     if (e != cudaSuccess) return e; \
+  }
+  static const bool bal = [] { const char* v = getenv("RSVD_APPLY128"); return !v || atoi(v) != 0; }();
+  if (ng == 128 && bal) {
+    const size_t sm2 = ((size_t)Np * ldx + 2 * (size_t)AP2_BM * ldss) * sizeof(double);
+    int64_t g2 = ceil_div(rows, AP2_BM);
+    if (g2 > num_sms) g2 = num_sms;
+    e = smem_optin(panel_apply128_kernel);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(panel_apply128_kernel, dim3((unsigned)g2), dim3(CQ_THREADS), sm2, st, S, lds, rows, Np, T, ldt, C, ldc,
+                   Nout, upper ? 1 : 0, pr);
+    if (e != cudaSuccess) return e;
+    ++g_kernel_launches;
+    return cudaGetLastError();
   }
   switch (ng / 32) {
     case 1: RSVD_APPLY(1) break;
