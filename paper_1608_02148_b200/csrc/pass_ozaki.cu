@@ -500,15 +500,23 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
   const int j = blockIdx.x * XT_COLS + c;
   const bool jv = j < Np;
   double v[XT_V];
+  int ev[XT_V];
   double mx = 0.0;
-  const int eoff = erow ? (int)*emax - kEBias : 0;
+  // all loads first (X values and, for TN passes, the row exponents), then the
+  // arithmetic: the exponent-dependent scaling otherwise serialised the loads
+  // (ncu: long-scoreboard stalls on the exponent subtraction dominated)
 #pragma unroll
   for (int i = 0; i < XT_V; ++i) {
     const int64_t k = k0 + g + XT_G * i;
     v[i] = (jv && k < K) ? X[k * ldx + j] : 0.0;
+    ev[i] = (erow && k < K) ? __ldg(erow + k) : 0;
+  }
+  const int eoff = erow ? (int)*emax - kEBias : 0;
+#pragma unroll
+  for (int i = 0; i < XT_V; ++i) {
     // TN passes: X' = diag(2^{E_k - E_max}) X folds A's row exponents into the panel
-    if (erow && k < K) {
-      const int d = __ldg(erow + k) - eoff;                   // <= 0
+    if (erow) {
+      const int d = ev[i] - eoff;                             // <= 0 (rows beyond K: v = 0)
       v[i] *= d >= -1022 ? __hiloint2double((d + 1023) << 20, 0) : ldexp(1.0, d);
     }
     mx = fmax(mx, fabs(v[i]));
