@@ -659,13 +659,15 @@ def _ctx_fp32_path(rb, path):
 
 @pytest.mark.parametrize("path", ["ozaki", "tf32"])
 @pytest.mark.parametrize("m,n,k,p,q", [(3000, 700, 30, 10, 2), (5000, 1200, 100, 20, 3), (777, 2000, 20, 12, 1),
-                                       (4099, 1030, 50, 14, 2)])
+                                       (4099, 1030, 50, 14, 2), (4900, 1030, 100, 20, 2), (1100, 3000, 100, 20, 1)])
 def test_rsvd_fp32_tcgen05_parity(rb, m, n, k, p, q, path):
     """FP32 A through the tcgen05 passes -- 3-digit Ozaki int8 slices (default)
     or 3xTF32 (RSVD_FP32_PATH=tf32): singular values within 1e-4 of the FP64
     oracle on the same FP32 data (J:5), orthonormality 1e-5.  (4099, 1030):
     ragged row block and a row length that is not a multiple of 4 (the
-    warp-per-row slicer)."""
+    warp-per-row slicer).  l = 120 runs the row-pair (cta_group::2) kernel:
+    (4900, 1030) has 39 row blocks of A.X (the last pair's second CTA entirely
+    out of range) and 9 of A^T.X; (1100, 3000) is wide (the roles swapped)."""
     A = _decay_matrix(m, n, seed=m + 3 * n, noise=1e-5).to(torch.float32)
     An = A.numpy()
     ctx = _ctx_fp32_path(rb, path)
