@@ -58,6 +58,10 @@ __host__ __device__ constexpr int oz_epi_warps(int N) { return N > 64 ? 16 : EPI
 __host__ __device__ constexpr int oz_threads(int N) { return 128 + 32 * oz_epi_warps(N); }
 constexpr int A_TILE = BM * BKO;                    // bytes of one slice tile
 constexpr int ET = 1024;                            // exponent blocks of X: 1024 rows x 1 column;
+// the drain interval / X exponent block per digit count: 1024 k at S = 7; 4096 at
+// S = 3 (int32 headroom: 3 pairs x 4096 x 255 x 128 < 2^31), a quarter of the
+// TMEM drains that stall the MMA issuer (probe: 2232 -> 2098 us per FP32 pass)
+__host__ __device__ constexpr int oz_et(int S) { return S == 3 ? 4096 : ET; }
                                                     // int32 accumulation over 1024 k: <= 7 pairs * 1024 * 255 * 128 < 2^28
 
 __host__ __device__ inline int64_t unit_lo(int64_t units, int grid, int c) { return (units * (int64_t)c) / grid; }
@@ -496,6 +500,9 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
   // grid: x = column group (fastest), y = super-block, so the CTAs reading the
   // column groups of the same rows run together (whole rows from DRAM, not
   // 64-byte pieces of rows read at different times)
+  // oz_et(S) > 1024: the CX = oz_et(S) / 1024 CTAs of a cluster (along y) slice one
+  // exponent block together; their column maxima meet in shared memory (DSMEM)
+  constexpr int CX = oz_et(S) / ET;
   const int64_t sb = blockIdx.y, k0 = sb * ET;
   const int j = blockIdx.x * XT_COLS + c;
   const bool jv = j < Np;
@@ -527,7 +534,30 @@ ozaki_slice_x_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N
   mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
   if ((threadIdx.x & 31) < XT_COLS) red[threadIdx.x >> 5][c] = mx;
   __syncthreads();
-  if (g == 0) {
+  if constexpr (CX > 1) {
+    __shared__ double cmax[CX][XT_COLS];
+    const int crk = (int)(blockIdx.y % CX);
+    // every CTA of the cluster must be running before its shared memory is written
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+    if (g == 0) {
+      double m2 = red[0][c];
+      for (int r = 1; r < XT_THREADS / 32; ++r) m2 = fmax(m2, red[r][c]);
+      const uint32_t local = (uint32_t)__cvta_generic_to_shared(&cmax[crk][c]);
+      for (int pr = 0; pr < CX; ++pr) {
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(pr));
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(m2) : "memory");
+      }
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (g == 0) {
+      double m2 = cmax[0][c];
+      for (int pr = 1; pr < CX; ++pr) m2 = fmax(m2, cmax[pr][c]);
+      const int E = block_exp(m2);
+      if (jv && crk == 0) xf[(sb / CX) * Np + j] = ldexp(1.0, E);
+      pow2_split(8 * S - 2 - E, escale[c][0], escale[c][1]);
+    }
+  } else if (g == 0) {
     double m2 = red[0][c];
     for (int r = 1; r < XT_THREADS / 32; ++r) m2 = fmax(m2, red[r][c]);
     const int E = block_exp(m2);
@@ -617,7 +647,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
 #ifdef OZ_KSU_OVERRIDE                               // probe builds only: drain interval in units (wrong numerics)
   constexpr int KSU = OZ_KSU_OVERRIDE;
 #else
-  constexpr int KSU = ET / BKU;                     // units per exponent super-block
+  constexpr int KSU = oz_et(S) / BKU;               // units per exponent super-block
 #endif
   constexpr int A_UT = BM * BKU;                    // bytes of one A-slice tile of a unit
   constexpr int XSL = NX * BKU;                     // bytes of one X slice tile (NX rows x BK k)
@@ -1079,7 +1109,7 @@ size_t ozaki_a_bytes(int64_t m, int64_t n, int s) {
 
 size_t ozaki_x_bytes(int64_t K, int Np, int s) {
   const int64_t ldk = round_up(K, 16);
-  return (size_t)s * Np * ldk + 256 + (size_t)round_up(ceil_div(K, oz::ET) * Np, 32) * sizeof(double) + 256;
+  return (size_t)s * Np * ldk + 256 + (size_t)round_up(ceil_div(K, (int64_t)oz::oz_et(s)) * Np, 32) * sizeof(double) + 256;
 }
 
 template <int S, typename T>
@@ -1192,10 +1222,33 @@ static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st) {
   double* xf = reinterpret_cast<double*>(reinterpret_cast<char*>(c.xscratch) + round_up((int64_t)S * N * ldk, 256));
   const cudaError_t ea = smem_optin(ozaki_slice_x_kernel<S>);
   if (ea != cudaSuccess) return ea;
-  const dim3 gs((unsigned)ceil_div(N, XT_COLS), (unsigned)ceil_div(ldk, ET));
-  const cudaError_t el = launch_pdl(ozaki_slice_x_kernel<S>, gs, dim3(XT_THREADS), (size_t)xt_smem(S), st, c.B, c.ldb, c.K, N, xs, ldk, xf,
-                                   c.flags ? c.flags + kEpochSlot : nullptr,
-                                   c.trans ? (const int*)c.a->erow : nullptr, (const unsigned*)c.a->emax);
+  constexpr int CX = oz_et(S) / ET;
+  const dim3 gs((unsigned)ceil_div(N, XT_COLS), (unsigned)(ceil_div(ceil_div(ldk, (int64_t)ET), (int64_t)CX) * CX));
+  cudaError_t el;
+  if constexpr (CX == 1) {
+    el = launch_pdl(ozaki_slice_x_kernel<S>, gs, dim3(XT_THREADS), (size_t)xt_smem(S), st, c.B, c.ldb, c.K, N, xs, ldk, xf,
+                    c.flags ? c.flags + kEpochSlot : nullptr,
+                    c.trans ? (const int*)c.a->erow : nullptr, (const unsigned*)c.a->emax);
+  } else {
+    // clusters of CX CTAs along y: one exponent block of oz_et(S) rows
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = gs;
+    cfg.blockDim = dim3(XT_THREADS);
+    cfg.dynamicSmemBytes = (size_t)xt_smem(S);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 1;
+    at[1].val.clusterDim.y = CX;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    el = cudaLaunchKernelEx(&cfg, ozaki_slice_x_kernel<S>, c.B, c.ldb, c.K, N, xs, ldk, xf,
+                            c.flags ? c.flags + kEpochSlot : nullptr,
+                            c.trans ? (const int*)c.a->erow : nullptr, (const unsigned*)c.a->emax);
+  }
   if (el != cudaSuccess) return el;
   ++g_kernel_launches;
   return cudaGetLastError();
