@@ -109,6 +109,102 @@ gram_partial_kernel(const double* __restrict__ S, int64_t lds, int64_t rows, int
     }
 }
 
+// Ng = 128 (configs 3 and 4): the upper triangle only, as the 36 upper 16 x 16
+// blocks (I <= J) of the 8 x 8 block grid dealt round-robin to the 8 warps (warps w
+// and w + 4 share an SM sub-partition: 5 + 4 blocks each), i.e. 9 of the 16
+// blocks' DMMAs per sub-partition instead of 16 (gram_partial_kernel<4> skips
+// only the two lower 64 x 32 warp tiles, so its busiest sub-partitions still do
+// 4 of 4 tiles).  Same 3-stage cp.async ring; partial p holds the upper blocks.
+constexpr int GS_MAXB = 5;
+__global__ void __launch_bounds__(CQ_THREADS, 1)
+gram_sym128_kernel(const double* __restrict__ S, int64_t lds, int64_t rows, int Np, int64_t rows_per_cta,
+                   double* __restrict__ partial, Pred pr) {
+  pdl_wait();
+  pdl_trigger();
+  if (pred_skip(pr)) return;
+  constexpr int NG = 128, LDT = NG + ((4 - NG) & 15);
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int64_t r0 = blockIdx.x * rows_per_cta;
+  int64_t r1 = r0 + rows_per_cta;
+  if (r1 > rows) r1 = rows;
+  const int nst = (int)ceil_div(r1 > r0 ? r1 - r0 : 0, GR_BK);
+  const int cpr = Np / 2;
+  // this warp's blocks b = warp + 8 q (b enumerates I <= J row by row; 36 blocks)
+  int bI[GS_MAXB], bJ[GS_MAXB];
+  const int nb = warp < 4 ? 5 : 4;
+#pragma unroll
+  for (int q = 0; q < GS_MAXB; ++q) {
+    int b = warp + 8 * q, I = 0;
+    if (b > 35) b = 35;
+    while (b >= 8 - I) { b -= 8 - I; ++I; }
+    bI[q] = I;
+    bJ[q] = I + b;
+  }
+  auto load = [&](int st, int it) {
+    double* t = sm + st * GR_BK * LDT;
+    const int64_t base = r0 + (int64_t)it * GR_BK;
+    for (int ch = tid; ch < GR_BK * cpr; ch += CQ_THREADS) {
+      const int r = ch / cpr, c = (ch - r * cpr) * 2;
+      const int64_t g = base + r;
+      const bool ok = g < r1;
+      cp_async16(t + r * LDT + c, ok ? S + g * lds + c : S, ok ? 16 : 0);
+    }
+    if (NG > Np)
+      for (int e = tid; e < GR_BK * (NG - Np); e += CQ_THREADS) {
+        const int r = e / (NG - Np), c = Np + e % (NG - Np);
+        t[r * LDT + c] = 0.0;
+      }
+  };
+  double acc[GS_MAXB][2][2][2];
+#pragma unroll
+  for (int q = 0; q < GS_MAXB; ++q)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < GR_STAGES - 1; ++st) {
+    if (st < nst) load(st, st);
+    cp_async_commit();
+  }
+  for (int it = 0; it < nst; ++it) {
+    cp_async_wait<GR_STAGES - 2>();
+    __syncthreads();
+    if (it + GR_STAGES - 1 < nst) load((it + GR_STAGES - 1) % GR_STAGES, it + GR_STAGES - 1);
+    cp_async_commit();
+    const double* t = sm + (it % GR_STAGES) * GR_BK * LDT;
+#pragma unroll
+    for (int kk = 0; kk < GR_BK; kk += 4) {
+      const double* tr = t + (kk + tq) * LDT + gq;
+#pragma unroll
+      for (int q = 0; q < GS_MAXB; ++q) {
+        if (q >= nb) break;
+        const double a0 = tr[bI[q] * 16], a1 = tr[bI[q] * 16 + 8];
+        const double b0 = tr[bJ[q] * 16], b1 = tr[bJ[q] * 16 + 8];
+        dmma884(acc[q][0][0][0], acc[q][0][0][1], a0, b0);
+        dmma884(acc[q][0][1][0], acc[q][0][1][1], a0, b1);
+        dmma884(acc[q][1][0][0], acc[q][1][0][1], a1, b0);
+        dmma884(acc[q][1][1][0], acc[q][1][1][1], a1, b1);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  double* out = partial + (int64_t)blockIdx.x * NG * NG;
+#pragma unroll
+  for (int q = 0; q < GS_MAXB; ++q) {
+    if (q >= nb) break;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int r = bI[q] * 16 + i * 8 + gq, c = bJ[q] * 16 + j * 8 + 2 * tq;
+        *reinterpret_cast<double2*>(out + r * NG + c) = make_double2(acc[q][i][j][0], acc[q][i][j][1]);
+      }
+  }
+}
+
 // upper triangle of G (Np x Np, ld ldg) = sum_{p < P} partial_p (Ng x Ng), fixed order: T lanes per
 // element each sum p = t, t+T, ... ascending (loads issued in batches of 8 so
 // they are in flight together), then a fixed xor tree.
@@ -166,11 +262,19 @@ cudaError_t launch_gram(const double* S, int64_t lds, int64_t rows, int Np, doub
     if (e != cudaSuccess) return e;                                                                      \
   }
   const size_t smem_max = (size_t)GR_STAGES * GR_BK * ldpad(128) * sizeof(double);
-  switch (ng / 32) {
-    case 1: RSVD_GRAM(1) break;
-    case 2: RSVD_GRAM(2) break;
-    case 3: RSVD_GRAM(3) break;
-    default: RSVD_GRAM(4) break;
+  static const bool sym = [] { const char* v = getenv("RSVD_GRAM_SYM"); return !v || atoi(v) != 0; }();
+  if (ng == 128 && sym) {
+    e = smem_optin(gram_sym128_kernel);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(gram_sym128_kernel, dim3(P), dim3(CQ_THREADS), smem, st, S, lds, rows, Np, rpc, partial, pr);
+    if (e != cudaSuccess) return e;
+  } else {
+    switch (ng / 32) {
+      case 1: RSVD_GRAM(1) break;
+      case 2: RSVD_GRAM(2) break;
+      case 3: RSVD_GRAM(3) break;
+      default: RSVD_GRAM(4) break;
+    }
   }
 #undef RSVD_GRAM
   ++g_kernel_launches;

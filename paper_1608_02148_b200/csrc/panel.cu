@@ -448,8 +448,10 @@ cudaError_t launch_hqr_leaves(double* Y, int64_t ldy, int64_t M, int l, int64_t 
 // zero column: R_jj = 0, reading R6), same outputs: Q in place, R (diag >= 0)
 // row-major l x l.  The explicit Q needs no barrier: warp c applies H_c .. H_0 to
 // e_c on its own (the vectors are read-only by then).
-template <int RPL>
-__global__ void __launch_bounds__(RPL >= 32 ? 640 : 1024, 1)
+// VREG: the vector is read once into registers per step (RPL <= 16, l <= 20:
+// 2 x RPL doubles per lane fit 640 threads' registers), else re-read (volatile).
+template <int RPL, bool VREG>
+__global__ void __launch_bounds__((RPL >= 32 || VREG) ? 640 : 1024, 1)
 hqr_cols_kernel(double* __restrict__ Y, int64_t ldy, int b, int l, double* __restrict__ Rout) {
   pdl_wait();
   pdl_trigger();
@@ -503,10 +505,15 @@ hqr_cols_kernel(double* __restrict__ Y, int64_t ldy, int b, int l, double* __res
 #pragma unroll
         for (int i = 0; i < RPL; ++i) w += v[32 * i] * y[i];
         const double f = t * warp_sum(w);
-        // re-read v (volatile): holding it across the reduction would double the registers
-        const volatile double* vv = v;
+        if constexpr (VREG) {
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) y[i] -= f * vv[32 * i];
+          for (int i = 0; i < RPL; ++i) y[i] -= f * v[32 * i];
+        } else {
+          // re-read v (volatile): holding it across the reduction would double the registers
+          const volatile double* vv = v;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) y[i] -= f * vv[32 * i];
+        }
       }
     }
   }
@@ -523,9 +530,14 @@ hqr_cols_kernel(double* __restrict__ Y, int64_t ldy, int b, int l, double* __res
 #pragma unroll
     for (int e = 0; e < RPL; ++e) w += v[32 * e] * y[e];
     const double f = t * warp_sum(w);
-    const volatile double* vv = v;
+    if constexpr (VREG) {
 #pragma unroll
-    for (int e = 0; e < RPL; ++e) y[e] -= f * vv[32 * e];
+      for (int e = 0; e < RPL; ++e) y[e] -= f * v[32 * e];
+    } else {
+      const volatile double* vv = v;
+#pragma unroll
+      for (int e = 0; e < RPL; ++e) y[e] -= f * vv[32 * e];
+    }
   }
 #pragma unroll
   for (int i = 0; i < RPL; ++i) {
@@ -547,17 +559,18 @@ cudaError_t launch_hqr_small(double* Y, int64_t ldy, int64_t M, int l, double* R
   if ((rpl == 32 && l > 20) || 64 * rpl + 1024 > 65536 / l) return cudaErrorNotSupported;
   const size_t smem = ((size_t)l * 32 * rpl + l + (size_t)l * l) * sizeof(double);
   cudaError_t e = cudaSuccess;
-#define RSVD_HQC(RP)                                                                                  \
+#define RSVD_HQC(RP, VR)                                                                              \
   {                                                                                                  \
-    e = set_smem((const void*)hqr_cols_kernel<RP>, smem);                                            \
+    e = set_smem((const void*)hqr_cols_kernel<RP, VR>, smem);                                        \
     if (e != cudaSuccess) return e;                                                                  \
-    e = launch_pdl(hqr_cols_kernel<RP>, dim3(1), dim3(32 * l), smem, st, Y, ldy, (int)M, l, R);      \
+    e = launch_pdl(hqr_cols_kernel<RP, VR>, dim3(1), dim3(32 * l), smem, st, Y, ldy, (int)M, l, R);  \
   }
+  const bool vreg = rpl <= 16 && l <= 20;
   switch (rpl) {
-    case 4: RSVD_HQC(4) break;
-    case 8: RSVD_HQC(8) break;
-    case 16: RSVD_HQC(16) break;
-    default: RSVD_HQC(32) break;
+    case 4: if (vreg) RSVD_HQC(4, true) else RSVD_HQC(4, false) break;
+    case 8: if (vreg) RSVD_HQC(8, true) else RSVD_HQC(8, false) break;
+    case 16: if (vreg) RSVD_HQC(16, true) else RSVD_HQC(16, false) break;
+    default: RSVD_HQC(32, false) break;
   }
 #undef RSVD_HQC
   if (e != cudaSuccess) return e;
