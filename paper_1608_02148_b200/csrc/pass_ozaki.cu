@@ -772,6 +772,9 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       // MODE 3: one digit per MMA (the pair's B operand is split by columns: digit
       // batches would put different digits in the two CTAs)
       constexpr int CMAX = RP ? 1 : 256 / N;
+      const uint32_t ub0 = smem_u32(base);
+      const uint64_t dA0 = TRANS ? sdesc(ub0, 16, 1024, LAYOUT_SW128) : sdesc(ub0, 16, SBO_K, LAY_K);
+      const uint64_t dX0 = sdesc(ub0 + S * A_UT, 16, SBO_K, LAY_K);
       OZ_PROBE_DECL
       int ndrain = 0;
       bool fresh = true;
@@ -789,14 +792,17 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
 #endif
         OZ_PROBE(2)
         tc_fence_after();
-        const uint32_t ua = smem_u32(base + ub * UBUF);
-        const uint64_t dx0 = sdesc(ua + S * A_UT, 16, SBO_K, LAY_K);
+        // descriptors = the buffer-0 descriptors + the 16-byte offset of this unit's
+        // buffer (the start-address field is the low 14 bits, addr >> 4 < 2^14: no
+        // carry) -- no descriptor rebuilt per unit on the single issuing thread
+        const uint64_t uo = (uint64_t)((ub * UBUF) >> 4);
+        const uint64_t dx0 = dX0 + uo;
         const uint32_t acc0 = fresh ? 0u : 1u;
         const uint32_t tacc = tmem + (uint32_t)((ndrain % NACC) * 256);
 #pragma unroll
         for (int t = 0; t < S; ++t) {
           // NN: A tile K-major, 64 B rows (SW64, k-step +32 B); TN: MN-major, 128 B rows (SW128, k-step +32 rows)
-          const uint64_t da0 = TRANS ? sdesc(ua + t * A_UT, 16, 1024, LAYOUT_SW128) : sdesc(ua + t * A_UT, 16, SBO_K, LAY_K);
+          const uint64_t da0 = dA0 + uo + (uint64_t)((t * A_UT) >> 4);
 #pragma unroll
           for (int kk = 0; kk < BKU / 32; ++kk) {
             const uint64_t da = da0 + (uint64_t)(TRANS ? kk * 256 : kk * 2);
