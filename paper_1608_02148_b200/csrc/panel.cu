@@ -52,8 +52,16 @@ __global__ void colsum_finish_kernel(const double* __restrict__ partial, int chu
                                      double* __restrict__ out) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
+  // loads in batches of 8 (in flight together), summed in the same ascending order
   double s = 0.0;
-  for (int t = 0; t < chunks; ++t) s += partial[t * n + j];
+  for (int t0 = 0; t0 < chunks; t0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) v[b] = (t0 + b < chunks) ? partial[(int64_t)(t0 + b) * n + j] : 0.0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (t0 + b < chunks) s += v[b];
+  }
   out[j] = s;
 }
 
