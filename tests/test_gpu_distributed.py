@@ -158,3 +158,27 @@ def test_group_abort_releases_peers(rb):
 
     with pytest.raises(Exception):
         rb.run_ranks(fn, 2)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fp32_sharded_row_pairs(rb, world):
+    """FP32 A (config 4's path: 3-digit Ozaki slices, l = 120 -> the row-pair
+    cta_group::2 pass, 4096-row X exponent blocks) row-sharded over 2 / 3 ranks
+    of unequal row counts: ranks agree bitwise on d and V, d within 1e-5 of
+    the 1-rank run (the slices of each rank's rows carry the same per-row
+    exponents; only the reduction split of A^T Q differs) and within 1e-4 of
+    the FP64 oracle on the same FP32 data (J:5)."""
+    g = torch.Generator().manual_seed(31)
+    m, n = 9001, 1300
+    U = torch.linalg.qr(torch.randn(m, 200, generator=g, dtype=torch.float64))[0]
+    V = torch.linalg.qr(torch.randn(n, 200, generator=g, dtype=torch.float64))[0]
+    s = torch.exp(-torch.arange(200, dtype=torch.float64) / 50.0)
+    A = ((U * s) @ V.T + 1e-4 * torch.randn(m, n, generator=g, dtype=torch.float64)).to(torch.float32)
+    Ad = A.cuda()
+    d, Ug, Vg, _ = _sharded_rsvd(rb, Ad, 100, world, p=20, q=2, sdist="normal", seed=7)
+    assert np.abs(Ug.T @ Ug - np.eye(100)).max() <= 1e-5
+    r1 = rb.rsvd(Ad, 100, p=20, q=2, sdist="normal", seed=7)
+    d1 = _np(r1.d)
+    assert np.max(np.abs(d - d1) / d1) <= 1e-5
+    o = oracle.oracle_rsvd(A.numpy().astype(np.float64), 100, p=20, q=2, sdist="normal", seed=7)
+    assert np.max(np.abs(d - o["d"]) / o["d"]) <= 1e-4
