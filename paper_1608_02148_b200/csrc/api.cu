@@ -18,6 +18,7 @@
 // and rsvd_run_host.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvtx3.hpp>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -279,13 +280,19 @@ cudaEvent_t take_event(rsvd_ctx* c) {
   return e;
 }
 
+// NVTX ranges (header-only nvtx3: no-ops unless a profiler such as nsys is
+// attached) around the enqueue of each phase, named as bench.py's per-kind split
+static const char* const kKindName[7] = {"rsvd:pass_AX", "rsvd:pass_AtX", "rsvd:panel_orth", "rsvd:jacobi_svd",
+                                         "rsvd:omega", "rsvd:ozaki_slice_A", "rsvd:ozaki_slice_X"};
 struct Prof {
   rsvd_ctx* c; int kind; double bytes; cudaEvent_t a = nullptr;
   Prof(rsvd_ctx* c_, int k, double b) : c(c_), kind(k), bytes(b) {
+    nvtxRangePushA(kind >= 0 && kind < 7 ? kKindName[kind] : "rsvd");
     if (on()) { a = take_event(c); cudaEventRecord(a, c->stream); }
   }
   bool on() const { return c->prof == 1 || (c->prof == 2 && kind == c->prof_phase); }
   ~Prof() {
+    nvtxRangePop();
     if (on()) {
       cudaEvent_t b2 = take_event(c);
       cudaEventRecord(b2, c->stream);
@@ -423,6 +430,7 @@ rsvd_status pass_tf32(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, doubl
 // One Ozaki pass: profile kind 6 = X slicing, `kind` (0 / 1) = the pass kernel(s)
 rsvd_status pass_ozaki(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, double* C, int64_t M, int64_t K,
                        int kind) {
+  nvtx3::scoped_range_in<nvtx3::domain::global> nv{kind == 0 ? "rsvd:pass_AX (ozaki)" : "rsvd:pass_AtX (ozaki)"};
   OzakiCall o{};
   o.a = &p.oz; o.trans = trans; o.B = B; o.ldb = p.Np; o.C = C; o.ldc = p.Np; o.Nout = p.Np;
   o.P = p.part; o.flags = ctx->gemm_flags; o.epoch = ++ctx->gemm_epoch; o.epoch2 = ++ctx->gemm_epoch;
