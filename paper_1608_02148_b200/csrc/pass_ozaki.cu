@@ -58,10 +58,12 @@ __host__ __device__ constexpr int oz_epi_warps(int N) { return N > 64 ? 16 : EPI
 __host__ __device__ constexpr int oz_threads(int N) { return 128 + 32 * oz_epi_warps(N); }
 constexpr int A_TILE = BM * BKO;                    // bytes of one slice tile
 constexpr int ET = 1024;                            // exponent blocks of X: 1024 rows x 1 column;
-// the drain interval / X exponent block per digit count: 1024 k at S = 7; 4096 at
-// S = 3 (int32 headroom: 3 pairs x 4096 x 255 x 128 < 2^31), a quarter of the
-// TMEM drains that stall the MMA issuer (probe: 2232 -> 2098 us per FP32 pass)
-__host__ __device__ constexpr int oz_et(int S) { return S == 3 ? 4096 : ET; }
+// the drain interval / X exponent block: 4096 k for both digit counts (int32
+// headroom: 7 pairs x 4096 x 255 x 128 < 2^30): a quarter of the TMEM drains that
+// stall the MMA issuer (probes: FP32 pass 2232 -> 2098 us, config-3 FP64 pass 2235
+// -> 2179 us; config-3 step 21.2 -> 20.3 ms; 8192 at S = 3 gained nothing more).
+// The X slicer reduces a block's column maxima over a cluster of 4 CTAs.
+__host__ __device__ constexpr int oz_et(int S) { return S > 0 ? 4096 : ET; }
                                                     // int32 accumulation over 1024 k: <= 7 pairs * 1024 * 255 * 128 < 2^28
 
 __host__ __device__ inline int64_t unit_lo(int64_t units, int grid, int c) { return (units * (int64_t)c) / grid; }
@@ -881,8 +883,9 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         // group g = t + u weighs 2^{-13-8g} (for every S); |v_g| < S * 1024 * 255 * 128 < 2^28
         static_assert(S == 7 || S == 3, "group combination for 7 (FP64) or 3 (FP32) digit groups");
         if constexpr (S == 7) {
-          // groups 0..3 and 4..6 combine EXACTLY in int64 (< 2^53 and < 2^45): two
-          // int -> FP64 conversions and one rounding per column instead of seven
+          // groups 0..3 and 4..6 combine in int64 (exactly: < 2^55 and < 2^47), then two
+          // int -> FP64 conversions (one rounding of the 55-bit group-0..3 sum, at
+          // FP64 unit roundoff) instead of seven conversions
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const long long s0 = (((long long)(int)v[0][i] * 256 + (int)v[1][i]) * 256 + (int)v[2][i]) * 256 + (int)v[3][i];
