@@ -47,8 +47,10 @@ constexpr int kFlagCholBreak = 1,   // a CholeskyQR broke down: the TSQR fallbac
               kFlagNonFinite = 4,   // non-finite input / intermediate (error)
               kFlagRankDef = 8,     // rid / rcur: numerical rank of the pivoted QR < k (error)
               kFlagLuZero = 16,     // informational: an exactly zero LU pivot (multipliers set to 0)
-              kFlagNoFallback = 32; // a breakdown with no TSQR fallback possible for the shape (error)
+              kFlagNoFallback = 32, // a breakdown with no TSQR fallback possible for the shape (error)
+              kFlagWideBreak = 64;  // CholeskyQR breakdown in a wide plan (l > kMaxL; error, reading R34)
 constexpr int kMaxL = 120;       // Jacobi + leaf QR shared-memory envelope
+constexpr int kMaxWide = 4096;   // wide plans (l > kMaxL, wide.cu): l x l factors in global memory
 
 struct ProfRec { int kind; double bytes; cudaEvent_t a, b; };
 
@@ -330,6 +332,7 @@ struct Plan {
   size_t oX, oY, oT, oZ, oPart, oSmall, oColc, oColr, oColp, oColss, oSplit, oJlog, total;
   bool use_tf32 = false;          // FP32 A on tcgen05 (3-term TF32 split)
   bool use_ozaki = false;         // FP64 A on tcgen05 (Ozaki int8 slices)
+  bool wide = false;              // l > kMaxL: DMMA column blocks, CholeskyQR2, wide Jacobi (wide.cu)
   OzakiA oz{};
   void* ozx = nullptr;            // X slice scratch
   void* ozx2 = nullptr;           // second 64-column block (Np > 64)
@@ -348,13 +351,14 @@ size_t plan_bytes(rsvd_ctx* ctx, Plan& p) {
   const int Np = p.Np;
   size_t part = 0;
   auto upd = [&](int64_t M, int64_t K, int N) {
-    part = std::max(part, gemm_partial_bytes(N, gemm_choose_grid(M, K, ctx->num_sms)));
+    part = std::max(part, gemm_partial_bytes(std::min(N, 128), gemm_choose_grid(M, K, ctx->num_sms)));
   };
   upd(p.M, p.n, Np);       // Y = A X
   upd(p.n, p.M, Np);       // Z = A^T Q
   if (p.use_tf32) part = std::max(part, tf32_partial_bytes(Np, ctx->num_sms));
   if (p.use_ozaki) part = std::max(part, ozaki_partial_bytes(Np, ctx->num_sms));
-  part = std::max(part, gram_partial_bytes(Np, ctx->num_sms));
+  if (!p.wide) part = std::max(part, gram_partial_bytes(Np, ctx->num_sms));
+  else upd(Np, std::max(p.M, p.n), 128);   // the Gram and small-K products of the wide panels
   p.part_bytes = part;
   const int64_t big = std::max(p.M, p.n);
   size_t o = 0;
@@ -369,7 +373,9 @@ size_t plan_bytes(rsvd_ctx* ctx, Plan& p) {
   p.oColp = o; o = align256(o + colsum_partial_bytes(p.M, p.n) + 256);
   p.oColss = o; o = align256(o + (size_t)p.n * 8);
   p.oSplit = o; o = align256(o + (p.use_tf32 ? tf32_split_bytes(big, Np) : 0));
-  p.oJlog = o; o = align256(o + jacobi_scratch_bytes(p.l));
+  p.oJlog = o;
+  o = align256(o + (p.wide ? std::max(jacobi_wide_scratch_bytes(p.l), chol_wide_scratch_bytes(Np))
+                            : jacobi_scratch_bytes(p.l)));
   p.total = o;
   return o;
 }
@@ -454,7 +460,31 @@ rsvd_status pass_ozaki(rsvd_ctx* ctx, Plan& p, bool trans, const double* B, doub
   return RSVD_OK;
 }
 
+// C (M x Nout, ld ldc) = f(Aop) (M x K) * B (K x N, ld ldb) as DMMA gemm_pass
+// launches over column blocks of <= 128 (wide plans; N % 16 == 0).  C must not
+// alias A or B: every block re-reads the whole of A.
+rsvd_status gemm_blocks(rsvd_ctx* ctx, Plan& p, const void* A, int64_t lda, bool a_f32, bool trans,
+                        const double* center, const double* rscale, const double* B, int64_t ldb, int N, double* C,
+                        int64_t ldc, int Nout, int64_t M, int64_t K) {
+  for (int j0 = 0; j0 < N && j0 < Nout; j0 += 128) {
+    GemmCall g{};
+    g.A = A; g.lda = lda; g.a_f32 = a_f32; g.trans = trans;
+    g.B = B + j0; g.ldb = ldb; g.C = C + j0; g.ldc = ldc; g.P = p.part;
+    g.center = center; g.rscale = rscale;
+    g.M = M; g.K = K; g.N = std::min(128, N - j0); g.Nout = std::min(g.N, Nout - j0);
+    g.grid = ctx->num_sms;
+    g.flags = ctx->gemm_flags; g.epoch = ++ctx->gemm_epoch;
+    CK(gemm_pass(g, ctx->stream));
+  }
+  return RSVD_OK;
+}
+
 rsvd_status pass_ax(rsvd_ctx* ctx, Plan& p, const double* X, double* Y, bool centred) {
+  if (p.wide) {
+    Prof pr(ctx, 0, (double)p.M * p.n * (p.f32 ? 4 : 8));
+    return gemm_blocks(ctx, p, p.A, p.lda, p.f32, p.trans_input, centred ? p.colc : nullptr,
+                       p.scaled ? p.colr : nullptr, X, p.Np, p.Np, Y, p.Np, p.Np, p.M, p.n);
+  }
   if (p.use_ozaki) return pass_ozaki(ctx, p, p.trans_input, X, Y, p.M, p.n, 0);
   if (p.use_tf32 && !centred) {
     Prof pr(ctx, 0, (double)p.M * p.n * 4);
@@ -476,6 +506,14 @@ rsvd_status pass_ax(rsvd_ctx* ctx, Plan& p, const double* X, double* Y, bool cen
 
 // Z (n x Np) = f(A)^T Q (K3), then allreduce over ranks.
 rsvd_status pass_atx(rsvd_ctx* ctx, Plan& p, const double* Q, double* Z, bool centred) {
+  if (p.wide) {
+    {
+      Prof pr(ctx, 1, (double)p.M * p.n * (p.f32 ? 4 : 8));
+      CKS(gemm_blocks(ctx, p, p.A, p.lda, p.f32, !p.trans_input, centred ? p.colc : nullptr,
+                      p.scaled ? p.colr : nullptr, Q, p.Np, p.Np, Z, p.Np, p.Np, p.n, p.M));
+    }
+    return allreduce_sum(ctx, Z, (size_t)p.n * p.Np);
+  }
   if (p.use_ozaki) {
     CKS(pass_ozaki(ctx, p, !p.trans_input, Q, Z, p.n, p.M, 1));
     return allreduce_sum(ctx, Z, (size_t)p.n * p.Np);
@@ -506,6 +544,10 @@ rsvd_status pass_atx(rsvd_ctx* ctx, Plan& p, const double* Q, double* Z, bool ce
 // C (rows x Nout) = S (rows x Np) * Bsm (Np x Np) (small-K product, panel_apply)
 rsvd_status small_k(rsvd_ctx* ctx, Plan& p, const double* S, int64_t rows, const double* Bsm, double* C,
                     int64_t ldc, int Nout, bool upper = false, Pred pr = Pred{}) {
+  if (p.wide) {
+    if (C == S) return fail(ctx, RSVD_EINVAL, "internal: in-place small-K product in a wide plan");
+    return gemm_blocks(ctx, p, S, p.Np, false, false, nullptr, nullptr, Bsm, p.Np, p.Np, C, ldc, Nout, rows, p.Np);
+  }
   CK(launch_panel_apply(S, p.Np, rows, p.Np, Bsm, p.Np, C, ldc, Nout, upper, ctx->num_sms, ctx->stream, pr));
   return RSVD_OK;
 }
@@ -612,9 +654,43 @@ rsvd_status orth_fallback(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool 
 // CholeskyQR kernels run while the breakdown bit is clear, the Householder
 // TSQR fallback once it is set (a breakdown in this or an earlier panel of
 // the call): decided on the device, no host round trip.
+// Wide plans (l > kMaxL): shifted CholeskyQR3 in every position (Fukaya et
+// al.: one CholeskyQR of G + s I, s = 11 (m l + l (l + 1)) u ||S||_F^2, then
+// CholeskyQR2), S -> T -> S -> T, copied back to S.  The Gram G = S^T S by
+// gemm_pass (TN form, column blocks), R and R^-1 by the cooperative
+// chol_wide_kernel.  The shift keeps the first factorisation defined for any
+// numerically full-rank panel (kappa up to ~1/u, e.g. the deterministic SVD of
+// a nearly low-rank IALM iterate); a panel that is rank-deficient to working
+// precision breaks the second CholeskyQR and, with no Householder fallback at
+// these widths, is reported as RSVD_ENUMERIC at rsvd_sync (reading R34).
+rsvd_status orth_wide(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool dist, double* Rout) {
+  const int l = p.l, Np = p.Np;
+  double* src = S;
+  double* dst = p.T;
+  double* Rs[3] = {p.Rsm, p.R1, p.R2};
+  const double mrows = dist ? (double)p.m_global : (double)rows;
+  const double shift_c = 11.0 * (mrows * l + (double)l * (l + 1)) * 0x1.0p-53;
+  for (int it = 0; it < 3; ++it) {
+    CKS(gemm_blocks(ctx, p, src, Np, false, true, nullptr, nullptr, src, Np, Np, p.G, Np, Np, Np, rows));
+    if (dist) CKS(allreduce_sum(ctx, p.G, (size_t)Np * Np));
+    CK(launch_chol_wide(p.G, Np, l, Np, Rs[it], p.Rinv, p.jlog, ctx->flags_dev, kFlagWideBreak,
+                        it == 0 ? shift_c : 0.0, ctx->num_sms, ctx->stream));
+    CKS(gemm_blocks(ctx, p, src, Np, false, false, nullptr, nullptr, p.Rinv, Np, Np, dst, Np, Np, rows, Np));
+    std::swap(src, dst);
+  }
+  CK(launch_copy_out(src, Np, rows, Np, S, Np, false, nullptr, ctx->stream));
+  // R = R3 R2 R1 (G is free again)
+  if (Rout) {
+    CKS(gemm_blocks(ctx, p, Rs[1], Np, false, false, nullptr, nullptr, Rs[0], Np, Np, p.G, Np, Np, Np, Np));
+    CKS(gemm_blocks(ctx, p, Rs[2], Np, false, false, nullptr, nullptr, p.G, Np, Np, Rout, Np, Np, Np, Np));
+  }
+  return RSVD_OK;
+}
+
 rsvd_status orth(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool dist, double* Rout, bool exact = true) {
   const int l = p.l, Np = p.Np;
   Prof pr_(ctx, 2, (double)rows * Np * 8 * 4);
+  if (p.wide) return orth_wide(ctx, p, S, rows, dist, Rout);
   if (!dist && small_panel(rows, l)) {
     // register-column Householder when the panel fits (l <= 32, rows <= 1024), else in shared memory
     static const bool small_regs = [] { const char* v = getenv("RSVD_HQR_REGS"); return !v || atoi(v) != 0; }();
@@ -739,7 +815,11 @@ rsvd_status rsvd_core(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool want_
   CKS(orth(ctx, p, p.Z, p.n, false, p.RB));
   {
     Prof pr(ctx, 3, 0);
-    CK(launch_jacobi(p.RB, Np, l, p.sigma, p.W, p.J, Np, ctx->flags_dev, ctx->sweeps_dev, p.jlog, ctx->stream));
+    if (p.wide)
+      CK(launch_jacobi_wide(p.RB, Np, l, p.sigma, p.W, p.J, Np, ctx->flags_dev, ctx->sweeps_dev, p.jlog,
+                            ctx->num_sms, ctx->stream));
+    else
+      CK(launch_jacobi(p.RB, Np, l, p.sigma, p.W, p.J, Np, ctx->flags_dev, ctx->sweeps_dev, p.jlog, ctx->stream));
   }
   // (launch_jacobi leaves the padding of W and J exact zeros)
   // V = Q_B J  (n x Np) into X
@@ -791,9 +871,11 @@ rsvd_status make_plan(rsvd_ctx* ctx, const rsvd_matrix* A, int k, int p_over, bo
   const int64_t mn = std::min(mg, A->n);
   p.l = (int)std::min<int64_t>((int64_t)k + p_over, mn);
   p.Np = (int)round_up(p.l, 16);      // GEMM N granularity: two warps x n8 tiles
-  p.use_ozaki = (p.f32 ? ctx->fp32_ozaki : ctx->fp64_ozaki) && ozaki_supported(p.Np);
-  p.use_tf32 = !p.use_ozaki && p.f32 && !center_or_scale && ctx->fp32_tcgen05 && tf32_pass_supported(p.A, p.lda);
-  if (p.l > kMaxL) return fail(ctx, RSVD_EUNSUPPORTED, "l = k + p = %d exceeds this build's limit %d", p.l, kMaxL);
+  p.wide = p.l > kMaxL;
+  p.use_ozaki = !p.wide && (p.f32 ? ctx->fp32_ozaki : ctx->fp64_ozaki) && ozaki_supported(p.Np);
+  p.use_tf32 = !p.wide && !p.use_ozaki && p.f32 && !center_or_scale && ctx->fp32_tcgen05 &&
+               tf32_pass_supported(p.A, p.lda);
+  if (p.l > kMaxWide) return fail(ctx, RSVD_EUNSUPPORTED, "l = k + p = %d exceeds this build's limit %d", p.l, kMaxWide);
   if (ctx->nranks > 1 && p.M < p.l)
     return fail(ctx, RSVD_EUNSUPPORTED, "each rank needs at least l = %d rows", p.l);
   const size_t bytes = plan_bytes(ctx, p);
@@ -838,6 +920,9 @@ rsvd_status sync_status(rsvd_ctx* ctx) {
   if (f & kFlagNonFinite) return fail(ctx, RSVD_ENUMERIC, "non-finite intermediate (input contains Inf/NaN?)");
   if (f & kFlagJacobiCap) return fail(ctx, RSVD_ENUMERIC, "one-sided Jacobi hit the 30-sweep cap");
   if (f & kFlagRankDef) return fail(ctx, RSVD_ENUMERIC, "pivoted QR: numerical rank < k");
+  if (f & kFlagWideBreak)
+    return fail(ctx, RSVD_ENUMERIC, "CholeskyQR breakdown at l > %d (numerically rank-deficient sketch; no Householder "
+                "fallback at this width)", kMaxL);
   if (f & kFlagNoFallback)
     return fail(ctx, RSVD_ENUMERIC, "CholeskyQR breakdown on a panel with fewer rows than l (no TSQR fallback)");
   return RSVD_OK;
@@ -1418,14 +1503,15 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
   CK(cudaSetDevice(ctx->device));
   const int64_t m = A->m_local;
   const int64_t minmn = std::min(mg, n);
-  // library envelope: l = k + p <= kMaxL.  The deterministic SVD of Remark 2
-  // and rand = FALSE is rsvd with l = min(m, n), q = 0 (reading R30),
-  // available while min(m, n) <= kMaxL; above that the randomized SVD is kept
-  // (warning in rsvd_last_error) and the adaptive k is capped at kMaxL - p.
-  const int kcap = (int)(minmn <= kMaxL ? minmn : std::min<int64_t>(minmn, kMaxL - rp.p));
-  if (kcap < 1) return fail(ctx, RSVD_EUNSUPPORTED, "p = %d leaves no room for k under l <= %d", rp.p, kMaxL);
+  // library envelope: l = k + p <= kMaxWide (l > kMaxL runs as a wide plan,
+  // wide.cu).  The deterministic SVD of Remark 2 and rand = FALSE is
+  // rsvd with l = min(m, n), q = 0 (reading R30), available while
+  // min(m, n) <= kMaxWide; above that the randomized SVD is kept (warning in
+  // rsvd_last_error) and the adaptive k is capped at kMaxWide - p.
+  const int kcap = (int)(minmn <= kMaxWide ? minmn : std::min<int64_t>(minmn, kMaxWide - rp.p));
+  if (kcap < 1) return fail(ctx, RSVD_EUNSUPPORTED, "p = %d leaves no room for k under l <= %d", rp.p, kMaxWide);
   if (!adaptive && prm->k > kcap)
-    return fail(ctx, RSVD_EUNSUPPORTED, "k = %d exceeds min(m, n) or l = k + p <= %d", prm->k, kMaxL);
+    return fail(ctx, RSVD_EUNSUPPORTED, "k = %d exceeds min(m, n) or l = k + p <= %d", prm->k, kMaxWide);
   int k = adaptive ? std::min(2, kcap) : prm->k;
   const int kbuf = adaptive ? kcap : prm->k;
   const double lam = prm->lambda > 0 ? prm->lambda : 1.0 / sqrt((double)std::max(mg, n));
@@ -1440,9 +1526,14 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
   const size_t oM = o; o = align256(o + (size_t)m * n * 8);
   const size_t oU = o; o = align256(o + (size_t)m * kbuf * 8);
   const size_t oV = o; o = align256(o + (size_t)n * kbuf * 8);
-  const size_t od = o; o = align256(o + 128 * 8);
-  const size_t odl = o; o = align256(o + 128 * 8);
+  const size_t od = o; o = align256(o + (size_t)std::max(128, kbuf) * 8);
+  const size_t odl = o; o = align256(o + (size_t)std::max(128, kbuf) * 8);
   const size_t oP = o; o = align256(o + (size_t)2 * nb * 8 + 64);
+  // ranks above 128 (wide): L materialised by gemm_pass from U and diag(dl) V^T (kbuf x npad)
+  const int64_t npad = round_up(n, 16);
+  const bool maybe_wide = kbuf > 128;
+  const size_t oVt = o; o = align256(o + (maybe_wide ? (size_t)kbuf * npad * 8 : 0));
+  const size_t oGP = o; o = align256(o + (maybe_wide ? gemm_partial_bytes(128, ctx->num_sms) : 0));
   if (o > ctx->ws3_bytes) {
     if (ctx->ws3) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->ws3); ctx->ws3 = nullptr; ctx->ws3_bytes = 0; }
     if (cudaMalloc(&ctx->ws3, o) != cudaSuccess) { cudaGetLastError(); return fail(ctx, RSVD_ENOMEM, "rrpca workspace"); }
@@ -1456,6 +1547,8 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
   double* dl = (double*)(ctx->ws3 + odl);
   double* part = (double*)(ctx->ws3 + oP);
   double* scal = part + 2 * nb;   // [0] = sum, [1] = max, [2] = l
+  double* Vt = (double*)(ctx->ws3 + oVt);
+  double* gpart = (double*)(ctx->ws3 + oGP);
   double* h = ctx->hbuf;
 
   // ||A||_2 = sigma_1 of rsvd(A, 1, p, q) with Omega stream 0 (reading R18)
@@ -1493,11 +1586,11 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
     // deterministic SVD (rand = FALSE, or Remark 2's switch for k > min(m, n)/4):
     // l = min(m, n), q = 0 -> Q Q^T M = M, the SVD of B is the exact SVD
     const bool want_det = !prm->rand || (adaptive && 4 * (int64_t)k > minmn);
-    const bool det = want_det && minmn <= kMaxL;
+    const bool det = want_det && minmn <= kMaxWide;
     if (want_det && !det) {
       char b[200];
       snprintf(b, sizeof b, "warning: deterministic SVD needs min(m, n) <= %d; the randomized SVD is kept (iteration %d, k = %d)",
-               kMaxL, it, k);
+               kMaxWide, it, k);
       warn = b;
     }
     if (det) {
@@ -1507,9 +1600,26 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
     CKS(rsvd_device(ctx, &Mdesc, &ri, U, k, dd, V, k));      // step (6)
     CK(launch_ialm_threshold(dd, k, 1.0 / mu, dl, scal + 2, ctx->stream));   // steps (7)-(8)
     const double mu_next = std::min(1.5 * mu, 1e7 * mu0);  // step (12), R20
-    CK(launch_ialm_update(Ad, S, Z, M, n, m, n, U, k, V, k, dl, k, 1.0 / mu, mu, lam, 1.0 / mu_next, part, nb,
-                          ctx->stream));                   // steps (9)-(11) fused
-    CK(launch_reduce_blocks(part, npart, 0, scal, ctx->stream));
+    if (k <= 128) {
+      CK(launch_ialm_update(Ad, S, Z, M, n, m, n, U, k, V, k, dl, k, 1.0 / mu, mu, lam, 1.0 / mu_next, part, nb,
+                            ctx->stream));                 // steps (9)-(11) fused
+      CK(launch_reduce_blocks(part, npart, 0, scal, ctx->stream));
+    } else {
+      // step (9) materialised into the L output: L = U (diag(dl) V^T), column blocks of 128
+      CK(launch_scale_transpose(V, k, n, k, dl, Vt, npad, ctx->stream));
+      for (int64_t j0 = 0; j0 < n; j0 += 128) {
+        GemmCall g{};
+        g.A = U; g.lda = k; g.a_f32 = false; g.trans = false;
+        g.B = Vt + j0; g.ldb = npad; g.C = Lm + j0; g.ldc = ld; g.P = gpart;
+        g.M = m; g.K = k; g.N = (int)std::min<int64_t>(128, npad - j0); g.Nout = (int)std::min<int64_t>(g.N, n - j0);
+        g.grid = ctx->num_sms;
+        g.flags = ctx->gemm_flags; g.epoch = ++ctx->gemm_epoch;
+        CK(gemm_pass(g, ctx->stream));
+      }
+      CK(launch_ialm_update_dense(Ad, S, Z, M, Lm, m * n, 1.0 / mu, mu, lam, 1.0 / mu_next, part, nb,
+                                  ctx->stream));           // steps (10)-(11)
+      CK(launch_reduce_blocks(part, nb, 0, scal, ctx->stream));
+    }
     CKS(allreduce_sum(ctx, scal, 1));
     CK(cudaMemcpyAsync(h + 128, scal, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1528,7 +1638,7 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
       int64_t kn = l1 < k ? l1 + 1 : std::min<int64_t>(l1 + (int64_t)ceil(0.05 * (double)minmn), minmn);
       if (kn > kcap) {
         char b[200];
-        snprintf(b, sizeof b, "warning: predicted rank %lld capped at %d (l = k + p <= %d)", (long long)kn, kcap, kMaxL);
+        snprintf(b, sizeof b, "warning: predicted rank %lld capped at %d (l = k + p <= %d)", (long long)kn, kcap, kMaxWide);
         warn = b;
       }
       k = (int)std::min<int64_t>(kn, kcap);
@@ -1537,7 +1647,8 @@ extern "C" rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsv
     if (res < prm->tol) break;
   }
   if (it > prm->maxiter) it = prm->maxiter;
-  CK(launch_lowrank_materialise(U, kused, V, kused, dl, kused, m, n, Lm, ld, ctx->stream));
+  if (kused <= 128)   // above, the last iteration left L materialised in Lm
+    CK(launch_lowrank_materialise(U, kused, V, kused, dl, kused, m, n, Lm, ld, ctx->stream));
   if (iters_out) *iters_out = it;
   if (res_out) *res_out = res;
   CKS(sync_status(ctx));

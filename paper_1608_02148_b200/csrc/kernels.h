@@ -230,6 +230,25 @@ cudaError_t launch_zq(const double* Z, int64_t ldz, const double* Q, int64_t ldq
 cudaError_t launch_rtsolve(const double* W, int ldw, const double* S, int lds, int k, double* U, int64_t ldu,
                            cudaStream_t st);
 
+// ---- wide plans, l > 120 (wide.cu; reading R34): cooperative launches, one CTA per SM
+// G + s I = R^T R (l x l leading block of G; s = shift_c trace(G), 0 when shift_c <= 0) and
+// R^-1 into npad x npad (ld npad, zero padded); breakdown as launch_chol_aug (flag |= flag_bit;
+// the column is dropped).
+size_t chol_wide_scratch_bytes(int npad);
+cudaError_t launch_chol_wide(const double* G, int ldg, int l, int npad, double* R, double* Rinv, void* scratch,
+                             int* flag, int flag_bit, double shift_c, int num_sms, cudaStream_t st);
+// One-sided Jacobi SVD of X = R^T, X J = W Sigma, for any l (outputs as launch_jacobi, ldo >= l).
+size_t jacobi_wide_scratch_bytes(int l);
+cudaError_t launch_jacobi_wide(const double* R, int ldr, int l, double* sigma, double* W, double* J, int ldo,
+                               int* flag, int* sweeps, void* scratch, int num_sms, cudaStream_t st);
+// Bt (r x ldb) = diag(dl) V^T (V n x r, ld ldv), columns >= n zero
+cudaError_t launch_scale_transpose(const double* V, int64_t ldv, int64_t n, int r, const double* dl, double* Bt,
+                                   int64_t ldb, cudaStream_t st);
+// IALM steps (10)-(11) with L materialised (contiguous m x n, total = m n); partial[b], b < nblocks
+cudaError_t launch_ialm_update_dense(const double* A, double* S, double* Z, double* Mnext, const double* L,
+                                     int64_t total, double inv_mu, double mu, double lam, double inv_mu_next,
+                                     double* partial, int nblocks, cudaStream_t st);
+
 // ---- IALM (ialm.cu), FP64, reading R17-R23 of DESIGN.md
 // M = A - S + Z * inv_mu ;  optional: norms of A (||A||_F^2 partials, max|A|)
 cudaError_t launch_ialm_form_m(const double* A, const double* S, const double* Z, int64_t ld,
