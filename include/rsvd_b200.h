@@ -111,7 +111,14 @@ typedef struct {
  *   k      target rank, 1 <= k <= min(m, n) (reading R10)
  *   nu,nv  number of left/right singular vectors to return; values
  *          > k are clamped to k with a warning; 0 = not formed
- *   p      oversampling, l = min(k + p, min(m, n)) (Alg. 4 step 1)
+ *   p      oversampling, l = min(k + p, min(m, n)) (Alg. 4 step 1);
+ *          l <= 4096 (RSVD_EUNSUPPORTED above).  l <= 120 runs the tcgen05
+ *          Ozaki / TF32 passes and the shared-memory panels and Jacobi;
+ *          120 < l <= 4096 runs a "wide plan" (reading R34): DMMA passes over
+ *          column blocks of 128, shifted CholeskyQR3 panels, a grid-wide
+ *          Jacobi.  A wide plan has no Householder fallback: a sketch that is
+ *          rank-deficient to working precision (k + p > rank(A)) may end in
+ *          RSVD_ENUMERIC at rsvd_sync
  *   q      subspace iterations (Alg. 2)
  *   seed, stream  counter-based Omega (reading R1)
  *   center  1 = implicit column centring of A (rpca, Alg. 6)
@@ -244,12 +251,13 @@ rsvd_status rsvd_rpca_predict(rsvd_ctx* ctx, const rsvd_matrix* Anew, int32_t k,
  * iteration, mu <- min(1.5 mu, 1e7 mu_0)).
  *   lambda  <= 0 selects max(m, n)^-1/2
  *   tol     stop when ||A - L - S||_F / ||A||_F < tol
- *   k       > 0: fixed target rank k (R22), needs k <= min(m, n), k + p <= 120;
+ *   k       > 0: fixed target rank k (R22), needs k <= min(m, n), k + p <= 4096;
  *           0: adaptive target rank -- k = 2 at step (1), then step (7)
  *           predict_rank (Remark 1): l = max(1, #{sigma_i > 1/mu}),
  *           k <- l + 1 if l < k else min(l + ceil(0.05 min(m, n)), min(m, n)),
- *           capped at min(min(m, n), 120 - p); the deterministic SVD of
- *           Remark 2 is used while k > min(m, n)/4 if min(m, n) <= 120 (R30)
+ *           capped at min(m, n) (at 4096 - p when min(m, n) > 4096); the
+ *           deterministic SVD of Remark 2 is used while k > min(m, n)/4 if
+ *           min(m, n) <= 4096, else the randomized SVD is kept with a warning (R30)
  * FP64 only.  L, S: DEVICE m_local x n (ld == n), caller-owned; A contiguous.
  *   iters, final_residual: HOST out-params (nullable)
  *   trace: HOST, nullable, 4*maxiter doubles per iteration: (residual, l, mu,
@@ -265,7 +273,8 @@ typedef struct {
   int32_t rand;   /* 1 (default): randomized SVD in step (6); 0: the deterministic
                      truncated SVD (P:1743-1744 rand = FALSE), computed as rsvd with
                      l = min(m, n), q = 0 (Q spans the whole column space, so the
-                     SVD of B is the exact SVD); needs min(m, n) <= 120.  With k = 0
+                     SVD of B is the exact SVD; a wide plan when min(m, n) > 120); needs
+                     min(m, n) <= 4096.  With k = 0
                      the same switch happens whenever the predicted k > min(m, n)/4
                      (Remark 2). */
 } rsvd_rrpca_params;
