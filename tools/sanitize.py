@@ -22,6 +22,7 @@ rb.rpca(A2, 20, p=10, q=1, seed=3, loadings=True, whiten=True, explained=True)
 rb.rid(A2, 20, p=10, q=1, seed=4)
 rb.rcur(A2, 16, p=10, q=1, seed=5)
 rb.rsvd(A2.float(), 30, p=10, q=1, seed=6)                                 # FP32 tcgen05 passes
+rb.rsvd(A2, 150, p=10, q=1, seed=9)                                        # wide plan (l = 160): cooperative kernels
 As, _, _ = synthetic.sparse_plus_lowrank(2000, 200, rank=5, frac=0.05, seed=7)
 rb.rrpca(As.cuda(), k=10, p=10, q=1, tol=1e-6, maxiter=20, seed=8)
 parts = rb.row_partition(3000, 2)
