@@ -67,6 +67,11 @@ __host__ __device__ constexpr int oz_et(int S) { return S > 0 ? 4096 : ET; }
                                                     // int32 accumulation over 1024 k: <= 7 pairs * 1024 * 255 * 128 < 2^28
 
 __host__ __device__ inline int64_t unit_lo(int64_t units, int grid, int c) { return (units * (int64_t)c) / grid; }
+
+// first k-block of row block mb (Args::krot)
+__device__ __forceinline__ int oz_phi(int64_t krot, int64_t KB, int mb) {
+  return krot > 0 ? (int)((((int64_t)mb * KB) % krot) % KB) : 0;
+}
 #ifndef OZ_PROBE
 #define OZ_PROBE_DECL
 #define OZ_PROBE(slot)
@@ -601,6 +606,12 @@ struct Args {
   const double* xf;                                 // 2^E per (k-block, column) of X
   int64_t M, K; int N, Nout, Np;
   int64_t KB, units; int grid;
+  // k rotation of the Aᵀ·X passes (0 = off): the units of row block mb visit the
+  // k-blocks from phi(mb) = ((mb KB) mod krot) mod KB on (cyclically), krot = the
+  // units per CTA (pair).  Every CTA (pair) then starts its range at one of ~3
+  // k offsets instead of one per CTA, so the CTAs stream the same X-slice rows
+  // at the same time and X (Q's slices, > L2 at config 3) is read ~once from HBM.
+  int64_t krot;
   // CL = 2 (Np = 128): the second CTA of each pair computes columns [64, 128)
   double* C2; const double* xf2; int Nout2;
 };
@@ -676,10 +687,17 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   const int64_t u_lo = unit_lo(g.units, npair, pid);
   const int64_t u_hi = unit_lo(g.units, npair, pid + 1);
   const int nun = (int)(u_hi - u_lo);
-  // (row block, k-block) of the first unit; the loops advance them incrementally
-  // (no 64-bit division per unit on the single-thread producer / MMA paths)
-  const int mb0 = (int)(u_lo / KB), kb0 = (int)(u_lo - (int64_t)mb0 * KB);
+  // (row block, unit index j within it, k-block) of the first unit; the loops
+  // advance them incrementally (no 64-bit division per unit on the single-thread
+  // producer / MMA paths).  kb = (j + phi(mb)) mod KB (Args::krot).
+  const int mb0 = (int)(u_lo / KB), j0 = (int)(u_lo - (int64_t)mb0 * KB);
   const int KBi = (int)KB;
+  const int kb0 = (int)((j0 + oz_phi(g.krot, KB, mb0)) % KBi);
+  // next unit: j wraps into the next row block (kb restarts at its phi), kb wraps at KB
+  auto adv = [&](int& mb, int& j, int& kb) {
+    if (++kb == KBi) kb = 0;
+    if (++j == KBi) { j = 0; ++mb; kb = oz_phi(g.krot, KB, mb); }
+  };
   double* const Cout = (crank && !RP) ? g.C2 : g.C;
   const double* const xfh = (crank && !RP) ? g.xf2 : g.xf;
   const int Nout = (crank && !RP) ? g.Nout2 : g.Nout;
@@ -707,9 +725,9 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
     // ---------------- TMA producer: one transaction per unit
     if (lane == 0) {
       OZ_PROBE2_DECL
-      int mb = mb0, kb = kb0, ub = 0;
+      int mb = mb0, j = j0, kb = kb0, ub = 0;
       uint32_t ph = 0;
-      for (int it = 0; it < nun; ++it, (++kb == KBi ? (kb = 0, ++mb) : 0), (++ub == NB ? (ub = 0, ph ^= 1u) : 0u)) {
+      for (int it = 0; it < nun; ++it, adv(mb, j, kb), (++ub == NB ? (ub = 0, ph ^= 1u) : 0u)) {
         unsigned char* ubuf = base + ub * UBUF;
         OZ_PROBE2(0)
         mbar_wait(&uempty[ub], ph ^ 1u);
@@ -780,11 +798,11 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       OZ_PROBE_DECL
       int ndrain = 0;
       bool fresh = true;
-      int kb = kb0, ub = 0, ks = kb0 % KSU;
+      int mb = mb0, j = j0, kb = kb0, ub = 0;
       uint32_t ph = 0;
-      for (int it = 0; it < nun; ++it, (++kb == KBi ? (kb = 0, ks = 0) : (++ks == KSU ? (ks = 0) : 0)),
-                                       (++ub == NB ? (ub = 0, ph ^= 1u) : 0u)) {
-        const bool drain = (ks == KSU - 1) || kb == KBi - 1 || it == nun - 1;
+      for (int it = 0; it < nun; ++it, adv(mb, j, kb), (++ub == NB ? (ub = 0, ph ^= 1u) : 0u)) {
+        // drain at the end of an X exponent super-block, of K, and of the row block
+        const bool drain = (kb % KSU == KSU - 1) || kb == KBi - 1 || j == KBi - 1 || it == nun - 1;
         OZ_PROBE(0)
         mbar_wait(&ufull[ub], ph);
         OZ_PROBE(3)
@@ -853,10 +871,10 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
     double* xfs = xfsm + (warp - 4) * XFW;            // per-warp copy of this super-block's column factors
     int64_t ndrain = 0;
     OZ_PROBE3_DECL
-    int mb = mb0, kb = kb0;
-    for (int it = 0; it < nun; ++it, (++kb == KBi ? (kb = 0, ++mb) : 0)) {
+    int mb = mb0, j = j0, kb = kb0;
+    for (int it = 0; it < nun; ++it, adv(mb, j, kb)) {
       const int64_t u = u_lo + it;
-      if (!((kb % KSU == KSU - 1) || kb == KBi - 1 || it == nun - 1)) continue;
+      if (!((kb % KSU == KSU - 1) || kb == KBi - 1 || j == KBi - 1 || it == nun - 1)) continue;
       const int64_t sb = kb / KSU;                          // super-block along k (X exponent block)
       for (int j = lane; j < NC; j += 32) xfs[j] = xfh[sb * g.Np + c0 + j];
       __syncwarp();
@@ -911,7 +929,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
       if (et == 0 && it == nun - 1) OZ_TL(5)
       OZ_PROBE3(2)
 #if defined(OZ_EPI_V) && (OZ_EPI_V & 4)   // probe builds only: one store of the row sum, no fix-up
-      if (kb == KB - 1 || it == nun - 1) {
+      if (j == KBi - 1 || it == nun - 1) {
         double sacc = 0.0;
 #pragma unroll
         for (int j = 0; j < NC; ++j) sacc += acc[j];
@@ -923,7 +941,7 @@ ozaki_pass_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
 #elif defined(OZ_EPI_V) && (OZ_EPI_V & 2)   // probe builds only: no write-out / fix-up
       if (false) {
 #else
-      if (kb == KB - 1 || it == nun - 1) {
+      if (j == KBi - 1 || it == nun - 1) {
 #endif
         // stream-K fix-up, wait-free: a row block split over several CTAs (pairs)
         // gets one column-major partial per segment (slot 0 = the CTA's first
@@ -1263,6 +1281,15 @@ static cudaError_t ozaki_slice_cols(const OzakiCall& c, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// k rotation of the TN passes (Args::krot): the units per CTA (pair), or 0 (NN
+// passes: X is L2-resident; RSVD_OZ_KROT=0 disables it for A/B runs)
+static int64_t oz_krot(bool trans, int64_t units, int nctas) {
+  static const bool off = [] { const char* v = getenv("RSVD_OZ_KROT"); return v && atoi(v) == 0; }();
+  if (!trans || off || nctas < 1) return 0;
+  const int64_t u = units / nctas;
+  return u > 0 ? u : 1;
+}
+
 template <int S>
 static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
   using namespace oz;
@@ -1289,6 +1316,7 @@ static cudaError_t ozaki_pass_cols(const OzakiCall& c, cudaStream_t st) {
   if (grid > c.grid) grid = c.grid;
   if (grid < 1) grid = 1;
   g.grid = (int)grid;
+  g.krot = oz_krot(c.trans, g.units, g.grid);
   const int Nt = N <= 16 ? 16 : N <= 32 ? 32 : N <= 48 ? 48 : N <= 64 ? 64 : 128;
   const size_t smem = (size_t)oz_nbuf(S, Nt, bk) * oz_ubuf(S, Nt, bk) + 1024;
   cudaError_t e = cudaSuccess;
@@ -1350,6 +1378,7 @@ static cudaError_t ozaki_pass_pair(const OzakiCall& h0, const OzakiCall& h1, cud
   if (npair > h0.grid / 2) npair = h0.grid / 2;
   if (npair < 1) npair = 1;
   g.grid = (int)(2 * npair);
+  g.krot = oz_krot(h0.trans, g.units, (int)npair);
   const size_t smem = (size_t)oz_nbuf(S, N, bk) * oz_ubuf(S, N, bk) + 1024;
   cudaError_t e = cudaSuccess;
 #define RSVD_OZP(TR)                                                                                      \
@@ -1397,6 +1426,7 @@ static cudaError_t ozaki_pass_rowpair(const OzakiCall& c, cudaStream_t st) {
     if (npair > c.grid / 2) npair = c.grid / 2;
     if (npair < 1) npair = 1;
     g.grid = (int)(2 * npair);
+    g.krot = oz_krot(c.trans, g.units, (int)npair);
     const size_t smem = (size_t)oz_nbuf(S, N / 2, bk) * oz_ubuf(S, N / 2, bk) + 1024;
     cudaError_t e = cudaSuccess;
 #define RSVD_OZR(TR, BK)                                                                                  \
