@@ -182,3 +182,21 @@ def test_fp32_sharded_row_pairs(rb, world):
     assert np.max(np.abs(d - d1) / d1) <= 1e-5
     o = oracle.oracle_rsvd(A.numpy().astype(np.float64), 100, p=20, q=2, sdist="normal", seed=7)
     assert np.max(np.abs(d - o["d"]) / o["d"]) <= 1e-4
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_wide_plan_sharded(rb, world):
+    """A wide plan (l = 170 > 120, reading R34) row-sharded: the Gram of every
+    shifted-CholeskyQR3 panel is allreduced, the cooperative Cholesky and the
+    grid-wide Jacobi run redundantly on every rank (identical bits); d within
+    1e-12 of the 1-rank run and 1e-10 of the oracle, U and V orthonormal."""
+    s = np.exp(-np.arange(600) / 100.0)
+    A, _ = synthetic.lowrank(2500, 600, torch.as_tensor(s), noise=1e-8, seed=44)
+    Ad = A.cuda()
+    d, U, V, _ = _sharded_rsvd(rb, Ad, 150, world, p=20, q=2, seed=8)
+    r1 = rb.rsvd(Ad, 150, p=20, q=2, seed=8)
+    assert np.max(np.abs(d - _np(r1.d)) / _np(r1.d)) <= 1e-12
+    o = oracle.oracle_rsvd(A.numpy(), 150, p=20, q=2, seed=8)
+    assert np.max(np.abs(d - o["d"]) / o["d"]) <= 1e-10
+    assert np.abs(U.T @ U - np.eye(150)).max() <= 1e-12
+    assert np.abs(V.T @ V - np.eye(150)).max() <= 1e-12
