@@ -759,3 +759,23 @@ def test_rsvd_heterogeneous_row_scales(rb):
     r = rb.rsvd(torch.from_numpy(A).cuda(), 30, p=10, q=2, seed=9)
     o = oracle.oracle_rsvd(A, 30, p=10, q=2, seed=9)
     _check_parity(A, r, o, 30)
+
+
+@pytest.mark.parametrize("e", [-450, 450])
+def test_rsvd_power_of_two_scaling(rb, e):
+    """ADVICE r1 (Ozaki exponent range): A scaled by 2^e far from 1.  Every step
+    is equivariant under a power-of-two scaling (the slices keep their digits,
+    the row exponents shift; Gram and Cholesky factors scale exactly while no
+    value leaves the normal range), so d(2^e A) = 2^e d(A) and U, V are the same
+    -- checked to 1e-14, and d against the oracle to 1e-10.  (|A| beyond about
+    2^±500 squares out of range in the Gram of CholeskyQR: DESIGN.md R35.)"""
+    A = _decay_matrix(3000, 700, seed=31)
+    r0 = rb.rsvd(A.cuda(), 40, p=10, q=2, seed=5)
+    As = A * (2.0 ** e)
+    r1 = rb.rsvd(As.cuda(), 40, p=10, q=2, seed=5)
+    d0, d1 = _np(r0.d), _np(r1.d)
+    assert np.max(np.abs(d1 * 2.0 ** -e - d0) / d0) < 1e-14
+    assert np.abs(_np(r1.v) - _np(r0.v)).max() < 1e-12
+    assert np.abs(_np(r1.u) - _np(r0.u)).max() < 1e-12
+    o = oracle.oracle_rsvd(As.numpy(), 40, p=10, q=2, seed=5)
+    assert np.max(np.abs(d1 - o["d"]) / o["d"]) < 1e-10
