@@ -127,7 +127,7 @@ typedef struct {
  *           iterations with QR (Alg. 2, default), 1 = the direct
  *           scheme Y = (A A^T)^q A Omega without normalisation (Alg. 1,
  *           P:343-362; "not recommended in practice"), 2 = normalized
- *           power iterations with pivoted LU (Alg. 3; single GPU);
+ *           power iterations with pivoted LU (Alg. 3; single GPU, l <= 128);
  *           RSVD_EINVAL otherwise */
 typedef struct {
   int32_t k, nu, nv, p, q;

@@ -901,6 +901,8 @@ size_t plan_tsqr_bytes(const Plan& p, int nranks) {
 rsvd_status run_call(rsvd_ctx* ctx, Plan& p, const rsvd_params* prm, bool want_svd,
                      const std::function<rsvd_status()>& emit = nullptr, bool want_ss = false) {
   ctx->err.clear();
+  if (prm->power == 2 && p.l > 128)   // the cooperative GEPP holds a row of the panel per lane group
+    return fail(ctx, RSVD_EUNSUPPORTED, "Alg. 3 (pivoted LU power scheme) needs l = k + p <= 128");
   CKS(ensure_ws2(ctx, plan_tsqr_bytes(p, ctx->nranks)));   // before any launch: no reallocation mid-call
   CKS(rsvd_core(ctx, p, prm, want_svd, want_ss));
   if (emit) CKS(emit());

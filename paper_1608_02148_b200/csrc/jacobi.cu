@@ -93,6 +93,32 @@ __device__ __forceinline__ void jac_rot(double al, double be, double ga, double&
 }
 }  // namespace
 
+// Scale X (count doubles in shared memory) by 2^-E, E the exponent of max |x|
+// (exact: a power of two), so that the squared norms and products of the
+// rotation test stay inside the FP64 range whatever the scale of A (reading
+// R35); every rotation is unchanged (the test and the angle are homogeneous).
+// Returns 2^E, the factor of the singular values (1 for a zero / non-finite X).
+// All threads of the block call it; red: >= 32 doubles of shared scratch.
+__device__ double jac_prescale(double* Xs, int count, double* red, int bad) {
+  double mx = 0.0;
+  for (int e = threadIdx.x; e < count; e += blockDim.x) mx = fmax(mx, fabs(Xs[e]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = 0.0;
+  for (int w = 0; w < nw; ++w) mx = fmax(mx, red[w]);
+  __syncthreads();
+  if (bad || !(mx > 0.0) || !isfinite(mx)) return 1.0;
+  int ex;
+  frexp(mx, &ex);
+  const double sc = ldexp(1.0, -ex);
+  for (int e = threadIdx.x; e < count; e += blockDim.x) Xs[e] *= sc;
+  __syncthreads();
+  return ldexp(1.0, ex);
+}
+
 size_t jacobi_log_bytes(int l) {
   const int L = jac_L(l);
   return (size_t)31 * (L - 1) * (L / 2) * 2 * sizeof(double);
@@ -223,6 +249,7 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
     }
   }
   __syncthreads();
+  const double jscale = jac_prescale(Xs, L * LDX, sg, bad);
   const double tol = (double)l * 0x1.0p-52, tol2 = tol * tol;
   int levels = 0;
   while ((1 << levels) < L) ++levels;
@@ -321,7 +348,7 @@ jacobi_x_kernel(const double* __restrict__ R, int ldr, int l, double* __restrict
     for (int q = lane; q < l; q += 32) rk += (sg[q] > sp) || (sg[q] == sp && q < p);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
-    if (lane == 0) { sigma[rk] = sp; rank_out[p] = rk; }
+    if (lane == 0) { sigma[rk] = sp * jscale; rank_out[p] = rk; }
     const double inv = sp > 0.0 ? 1.0 / sp : 1.0;
     for (int i = lane; i < l; i += 32) Wo[i * ldo + rk] = Xs[p * LDX + i] * inv;
   }
@@ -589,6 +616,7 @@ jacobi_blk_kernel(const double* __restrict__ R, int ldr, int l, int NB, double* 
     }
   }
   __syncthreads();
+  const double jscale = jac_prescale(Xs, NC * LDX, sg, bad);
   const double tol = (double)l * 0x1.0p-52, tol2 = tol * tol;
   const int per_step = B * W * B;
   int sweeps = 0;
@@ -640,7 +668,7 @@ jacobi_blk_kernel(const double* __restrict__ R, int ldr, int l, int NB, double* 
     for (int q = lane; q < l; q += 32) rk += (sg[q] > sp) || (sg[q] == sp && q < p);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
-    if (lane == 0) { sigma[rk] = sp; rank_out[p] = rk; }
+    if (lane == 0) { sigma[rk] = sp * jscale; rank_out[p] = rk; }
     const double inv = sp > 0.0 ? 1.0 / sp : 1.0;
     for (int i = lane; i < l; i += 32) Wo[i * ldo + rk] = Xs[p * LDX + i] * inv;
   }

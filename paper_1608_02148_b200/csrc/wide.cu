@@ -121,6 +121,7 @@ struct JacWideArgs {
   double* sg; int* cnt;            // column norms; per-sweep rotation counters
   double* sigma; double* W; double* J; int ldo;
   int* flag; int* sweeps;
+  unsigned long long* gmax;        // bits of max |x| (zeroed by the launcher)
 };
 
 // pair i of round r of the circle method over n (even) players: the last is
@@ -142,17 +143,39 @@ __global__ void __launch_bounds__(WT) jacobi_wide_kernel(JacWideArgs a) {
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
+  double mx = 0.0;
   for (int64_t e = gt; e < (int64_t)l * l; e += nth) {
     const int j = (int)(e / l), i = (int)(e - (int64_t)j * l);
     const double v = i >= j ? a.R[(int64_t)j * a.ldr + i] : 0.0;
     if (!isfinite(v)) bad = 1;
+    mx = fmax(mx, fabs(v));
     a.Xc[e] = v;
     a.Jc[e] = i == j ? 1.0 : 0.0;
   }
+  // max |x| over the grid (non-negative doubles order as their bit patterns;
+  // the slot is zeroed by the launcher) for the power-of-two prescaling (R35)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0 && mx > 0.0 && isfinite(mx))
+    atomicMax(a.gmax, (unsigned long long)__double_as_longlong(mx));
   for (int64_t e = gt; e < (int64_t)a.ldo * a.ldo; e += nth) { a.W[e] = 0.0; a.J[e] = 0.0; }
   if (gt < 32) a.cnt[gt] = 0;
   __syncthreads();
   if (threadIdx.x == 0 && bad) atomicOr(a.flag, 4);
+  grid.sync();
+  // X <- 2^-E X (exact), sigma <- 2^E sigma at the end: the squared norms of the
+  // rotation test stay in range whatever the scale of A (as jac_prescale, R35)
+  double jscale = 1.0;
+  {
+    const double gm = __longlong_as_double((long long)__ldcg(a.gmax));
+    if (gm > 0.0) {
+      int ex;
+      frexp(gm, &ex);
+      const double sc = ldexp(1.0, -ex);
+      jscale = ldexp(1.0, ex);
+      for (int64_t e = gt; e < (int64_t)l * l; e += nth) a.Xc[e] *= sc;
+    }
+  }
   grid.sync();
   const double tol = (double)l * 0x1.0p-52;
   int sweeps = 0;
@@ -220,7 +243,7 @@ __global__ void __launch_bounds__(WT) jacobi_wide_kernel(JacWideArgs a) {
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
-    if (lane == 0) a.sigma[rk] = sj;
+    if (lane == 0) a.sigma[rk] = sj * jscale;
     const double inv = sj > 0.0 ? 1.0 / sj : 1.0;
     const double* xj = a.Xc + (int64_t)j * l;
     const double* jj = a.Jc + (int64_t)j * l;
@@ -318,6 +341,9 @@ cudaError_t launch_jacobi_wide(const double* R, int ldr, int l, double* sigma, d
   a.sg = a.Jc + (size_t)a.Lp * l;
   a.cnt = reinterpret_cast<int*>(a.sg + a.Lp);
   a.sigma = sigma; a.W = W; a.J = J; a.ldo = ldo; a.flag = flag; a.sweeps = sweeps;
+  a.gmax = reinterpret_cast<unsigned long long*>(a.cnt + 32);
+  const cudaError_t e = cudaMemsetAsync(a.gmax, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
   return coop_launch(jacobi_wide_kernel, &a, num_sms, st);
 }
 

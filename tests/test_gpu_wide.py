@@ -131,3 +131,15 @@ def test_rrpca_rank_above_128_dense_update(rb):
     _, _, div = _check_rrpca(rb, A, L0, S0, recover=False, k=150, p=10, q=2, tol=1e-7, maxiter=100, seed=4,
                              rand=False)
     assert div is None
+
+
+def test_wide_lu_power_scheme_rejected_before_launch(rb):
+    """Alg. 3's cooperative GEPP is limited to l <= 128: a wide Alg. 3 request is
+    refused with RSVD_EUNSUPPORTED before any launch (not a CUDA error mid-call);
+    the context stays usable."""
+    A = _slow_decay(600, 300, seed=3)
+    with pytest.raises(rb.RsvdError) as ei:
+        rb.rsvd(A.cuda(), 150, p=10, q=1, seed=1, power="lu")
+    assert ei.value.status == 6
+    r = rb.rsvd(A.cuda(), 20, p=10, q=1, seed=1)
+    assert np.all(np.isfinite(_np(r.d)))
