@@ -329,6 +329,7 @@ struct Plan {
   const void* A; int64_t lda;
   int64_t m_global;
   // workspace offsets
+  size_t oW0 = 0;
   size_t oX, oY, oT, oZ, oPart, oSmall, oColc, oColr, oColp, oColss, oSplit, oJlog, total;
   bool use_tf32 = false;          // FP32 A on tcgen05 (3-term TF32 split)
   bool use_ozaki = false;         // FP64 A on tcgen05 (Ozaki int8 slices)
@@ -341,6 +342,7 @@ struct Plan {
   void* jlog = nullptr;
   size_t part_bytes;
   // small-buffer offsets (doubles from oSmall)
+  double* W0 = nullptr;           // wide plans: the panel saved for the Householder fallback
   double *X, *Y, *T, *Z, *part, *G, *Rinv, *R1, *R2, *RB, *W, *J, *sigma, *sgn, *colc, *colr, *cols, *colp, *colss,
       *Rsm, *tv;
 };
@@ -373,6 +375,7 @@ size_t plan_bytes(rsvd_ctx* ctx, Plan& p) {
   p.oColp = o; o = align256(o + colsum_partial_bytes(p.M, p.n) + 256);
   p.oColss = o; o = align256(o + (size_t)p.n * 8);
   p.oSplit = o; o = align256(o + (p.use_tf32 ? tf32_split_bytes(big, Np) : 0));
+  p.oW0 = o; o = align256(o + (p.wide ? (size_t)big * Np * 8 : 0));
   p.oJlog = o;
   o = align256(o + (p.wide ? std::max(jacobi_wide_scratch_bytes(p.l), chol_wide_scratch_bytes(Np))
                             : jacobi_scratch_bytes(p.l)));
@@ -406,6 +409,7 @@ void bind(rsvd_ctx* ctx, Plan& p) {
   p.colss = (double*)(b + p.oColss);
   p.split = (float*)(b + p.oSplit);
   p.jlog = (void*)(b + p.oJlog);
+  if (p.wide) p.W0 = (double*)(b + p.oW0);
 }
 
 rsvd_status allreduce_sum(rsvd_ctx* ctx, double* buf, size_t count) {
@@ -661,10 +665,12 @@ rsvd_status orth_fallback(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool 
 // chol_wide_kernel.  The shift keeps the first factorisation defined for any
 // numerically full-rank panel (kappa up to ~1/u, e.g. the deterministic SVD of
 // a nearly low-rank IALM iterate); a panel that is rank-deficient to working
-// precision breaks the second CholeskyQR and, with no Householder fallback at
-// these widths, is reported as RSVD_ENUMERIC at rsvd_sync (reading R34).
+// precision breaks the second CholeskyQR: then (decided on the device) the
+// cooperative Householder QR of the saved panel replaces Q and R (single GPU;
+// row-sharded panels report the breakdown as RSVD_ENUMERIC, reading R34).
 rsvd_status orth_wide(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool dist, double* Rout) {
   const int l = p.l, Np = p.Np;
+  if (!dist) CK(launch_copy_out(S, Np, rows, Np, p.W0, Np, false, nullptr, ctx->stream));
   double* src = S;
   double* dst = p.T;
   double* Rs[3] = {p.Rsm, p.R1, p.R2};
@@ -684,6 +690,9 @@ rsvd_status orth_wide(rsvd_ctx* ctx, Plan& p, double* S, int64_t rows, bool dist
     CKS(gemm_blocks(ctx, p, Rs[1], Np, false, false, nullptr, nullptr, Rs[0], Np, Np, p.G, Np, Np, Np, Np));
     CKS(gemm_blocks(ctx, p, Rs[2], Np, false, false, nullptr, nullptr, p.G, Np, Np, Rout, Np, Np, Np, Np));
   }
+  if (!dist)   // a no-op launch unless a CholeskyQR above broke down
+    CK(launch_hqr_wide(p.W0, rows, l, Np, S, Rout, p.part, p.jlog, ctx->flags_dev, kFlagWideBreak, kFlagCholBreak,
+                       ctx->num_sms, ctx->stream));
   return RSVD_OK;
 }
 

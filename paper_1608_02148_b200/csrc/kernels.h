@@ -241,6 +241,11 @@ cudaError_t launch_chol_wide(const double* G, int ldg, int l, int npad, double* 
 size_t jacobi_wide_scratch_bytes(int l);
 cudaError_t launch_jacobi_wide(const double* R, int ldr, int l, double* sigma, double* W, double* J, int ldo,
                                int* flag, int* sweeps, void* scratch, int num_sms, cudaStream_t st);
+// Householder QR of the saved rows x l panel (ld npad; overwritten) into Q (ld npad) and R
+// (npad x npad upper, diag >= 0, nullable), only when (*flag & bit); clears the bit, sets ran_bit.
+// part: >= num_sms x npad doubles; scratch: >= 3 npad doubles.  Cooperative launch.
+cudaError_t launch_hqr_wide(double* Wsaved, int64_t rows, int l, int npad, double* Q, double* R, double* part,
+                            void* scratch, int* flag, int bit, int ran_bit, int num_sms, cudaStream_t st);
 // Bt (r x ldb) = diag(dl) V^T (V n x r, ld ldv), columns >= n zero
 cudaError_t launch_scale_transpose(const double* V, int64_t ldv, int64_t n, int r, const double* dl, double* Bt,
                                    int64_t ldb, cudaStream_t st);

@@ -258,6 +258,134 @@ __global__ void __launch_bounds__(WT) jacobi_wide_kernel(JacWideArgs a) {
   }
 }
 
+struct HqrWideArgs {
+  double* W; int64_t rows; int l; int np;   // saved panel (rows x np), overwritten by the reflectors
+  double* Q;                                // output Q (rows x np, first l columns)
+  double* R;                                // output R (np x np, upper, zero padded), nullable
+  double* part;                             // grid x np partial sums
+  double* al; double* vt; double* vj;       // per column: alpha, v^T v, v_j
+  int* flag; int bit;                       // runs only if (*flag & bit); clears the bit
+  int ran_bit;                              // set when it ran (informational)
+};
+
+// CTA b's rows: [b rows / G, (b + 1) rows / G)
+__device__ __forceinline__ int64_t hw_row(int64_t rows, int G, int b) { return rows * b / G; }
+
+// Partial sums over this CTA's rows of f(i, c) for columns c in [c0, c1), one
+// warp per column, written to part[blockIdx.x * np + c]; then a grid barrier.
+template <typename F>
+__device__ __forceinline__ void hw_col_sums(const HqrWideArgs& a, int64_t r0, int64_t r1, int c0, int c1, F f,
+                                            cg::grid_group& grid) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = c0 + warp; c < c1; c += nw) {
+    double s = 0.0;
+    for (int64_t i = r0 + lane; i < r1; i += 32) s += f(i, c);
+    s = warp_sum(s);
+    if (lane == 0) a.part[(int64_t)blockIdx.x * a.np + c] = s;
+  }
+  grid.sync();
+}
+
+// The grid's sums of columns [c0, c1) into tot (shared), fixed CTA order:
+// identical in every CTA
+__device__ __forceinline__ void hw_totals(const HqrWideArgs& a, int c0, int c1, double* tot) {
+  for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) s += __ldcg(a.part + (int64_t)b * a.np + c);
+    tot[c] = s;
+  }
+  __syncthreads();
+}
+
+// Householder QR of a wide panel in global memory (the fallback of a wide
+// plan's CholeskyQR, reading R34): column j -- ||x||, alpha = -sgn(x_0)||x||,
+// v = x - alpha e_0 (skipped when ||x|| = 0, R_jj = 0); H = I - 2 v v^T / v^T v
+// applied to the trailing columns; then the explicit Q = H_0 ... H_{l-1} [I; 0]
+// by backward accumulation and diag(R) >= 0 (sign flips of R's rows and Q's
+// columns), as the oracle's hqr.  Grid sums in fixed CTA order
+// (deterministic).  Runs only when the call's breakdown bit is set.
+__global__ void __launch_bounds__(WT) hqr_wide_kernel(HqrWideArgs a) {
+  if ((*(volatile int*)a.flag & a.bit) == 0) return;   // uniform: read before any barrier
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x, l = a.l, np = a.np;
+  const int64_t r0 = hw_row(a.rows, G, blockIdx.x), r1 = hw_row(a.rows, G, blockIdx.x + 1);
+  double* W = a.W;
+  extern __shared__ double tot[];                        // np doubles
+  for (int j = 0; j < l; ++j) {
+    // ||x||^2 over rows >= j
+    hw_col_sums(a, r0 > j ? r0 : j, r1, j, j + 1, [&](int64_t i, int c) { const double w = W[i * np + c]; return w * w; }, grid);
+    hw_totals(a, j, j + 1, tot);
+    const double nx2 = tot[j];
+    const double x0 = __ldcg(W + (int64_t)j * np + j);
+    const double nx = sqrt(nx2);
+    const double alpha = nx == 0.0 ? 0.0 : (x0 >= 0.0 ? -nx : nx);
+    const double v0 = x0 - alpha;
+    const double vtv = nx2 - x0 * x0 + v0 * v0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { a.al[j] = alpha; a.vt[j] = vtv; a.vj[j] = v0; }
+    __syncthreads();                                     // tot[j] read by every thread
+    if (nx == 0.0 || !(vtv > 0.0)) { grid.sync(); continue; }
+    // d_c = v^T W[:, c] for c > j (v_j = v0, v_i = W[i][j] below)
+    hw_col_sums(a, r0 > j ? r0 : j, r1, j + 1, l, [&](int64_t i, int c) {
+      const double vi = i == j ? v0 : W[i * np + j];
+      return vi * W[i * np + c];
+    }, grid);
+    const double f = 2.0 / vtv;
+    hw_totals(a, j + 1, l, tot);
+    for (int c = j + 1; c < l; ++c) {
+      const double dc = tot[c] * f;
+      for (int64_t i = (r0 > j ? r0 : j) + threadIdx.x; i < r1; i += blockDim.x) {
+        const double vi = i == j ? v0 : W[i * np + j];
+        W[i * np + c] -= dc * vi;
+      }
+    }
+    grid.sync();
+  }
+  // R (upper): R_jj = alpha_j, R_jc = W[j][c] (c > j); signs so that diag(R) >= 0
+  if (a.R) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)np * np; e += (int64_t)G * blockDim.x) {
+      const int i = (int)(e / np), c = (int)(e % np);
+      double v = 0.0;
+      if (i < l && c < l && c >= i) {
+        const double sg = __ldcg(a.al + i) < 0.0 ? -1.0 : 1.0;
+        v = sg * (c == i ? __ldcg(a.al + i) : __ldcg(W + (int64_t)i * np + c));
+      }
+      a.R[e] = v;
+    }
+  }
+  // Q = [I; 0], then for j = l-1 .. 0: Q[:, j:] -= (2 / v^T v) v (v^T Q[:, j:])
+  for (int64_t i = r0; i < r1; ++i)
+    for (int c = threadIdx.x; c < l; c += blockDim.x) a.Q[i * np + c] = i == c ? 1.0 : 0.0;
+  grid.sync();
+  for (int j = l - 1; j >= 0; --j) {
+    const double vtv = __ldcg(a.vt + j), v0 = __ldcg(a.vj + j);
+    if (__ldcg(a.al + j) == 0.0 && v0 == 0.0) continue;      // skipped column (H = I)
+    if (!(vtv > 0.0)) continue;
+    hw_col_sums(a, r0 > j ? r0 : j, r1, j, l, [&](int64_t i, int c) {
+      const double vi = i == j ? v0 : W[i * np + j];
+      return vi * a.Q[i * np + c];
+    }, grid);
+    const double f = 2.0 / vtv;
+    hw_totals(a, j, l, tot);
+    for (int c = j; c < l; ++c) {
+      const double dc = tot[c] * f;
+      for (int64_t i = (r0 > j ? r0 : j) + threadIdx.x; i < r1; i += blockDim.x) {
+        const double vi = i == j ? v0 : W[i * np + j];
+        a.Q[i * np + c] -= dc * vi;
+      }
+    }
+    grid.sync();
+  }
+  // diag(R) >= 0: Q(:, j) *= sgn(alpha_j) where alpha_j < 0
+  for (int64_t i = r0; i < r1; ++i)
+    for (int c = threadIdx.x; c < l; c += blockDim.x)
+      if (__ldcg(a.al + c) < 0.0) a.Q[i * np + c] = -a.Q[i * np + c];
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicAnd(a.flag, ~a.bit);
+    atomicOr(a.flag, a.ran_bit);
+  }
+}
+
 template <typename K>
 cudaError_t coop_launch(K kernel, void* arg, int num_sms, cudaStream_t st) {
   int per_sm = 0;
@@ -324,6 +452,29 @@ cudaError_t launch_chol_wide(const double* G, int ldg, int l, int npad, double* 
   a.d0 = a.Wk + (size_t)npad * npad;
   a.R = R; a.Rinv = Rinv; a.flag = flag; a.flag_bit = flag_bit; a.shift_c = shift_c;
   return coop_launch(chol_wide_kernel, &a, num_sms, st);
+}
+
+cudaError_t launch_hqr_wide(double* Wsaved, int64_t rows, int l, int npad, double* Q, double* R, double* part,
+                            void* scratch, int* flag, int bit, int ran_bit, int num_sms, cudaStream_t st) {
+  if (l < 1 || npad < l || rows < l) return cudaErrorInvalidValue;
+  HqrWideArgs a;
+  a.W = Wsaved; a.rows = rows; a.l = l; a.np = npad; a.Q = Q; a.R = R; a.part = part;
+  a.al = reinterpret_cast<double*>(scratch);
+  a.vt = a.al + npad;
+  a.vj = a.vt + npad;
+  a.flag = flag; a.bit = bit; a.ran_bit = ran_bit;
+  const int grid = (int)std::min<int64_t>(num_sms, std::max<int64_t>(1, rows / 32));
+  const size_t smem = (size_t)npad * sizeof(double);
+  cudaError_t e = cudaSuccess;
+  if (smem > 48 * 1024 && (e = smem_optin(hqr_wide_kernel)) != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hqr_wide_kernel, WT, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+  void* args[] = {&a};
+  e = cudaLaunchCooperativeKernel((void*)hqr_wide_kernel, dim3(grid), dim3(WT), args, smem, st);
+  ++g_kernel_launches;
+  return e;
 }
 
 size_t jacobi_wide_scratch_bytes(int l) {
