@@ -116,9 +116,9 @@ typedef struct {
  *          Ozaki / TF32 passes and the shared-memory panels and Jacobi;
  *          120 < l <= 4096 runs a "wide plan" (reading R34): DMMA passes over
  *          column blocks of 128, shifted CholeskyQR3 panels, a grid-wide
- *          Jacobi.  A wide plan has no Householder fallback: a sketch that is
- *          rank-deficient to working precision (k + p > rank(A)) may end in
- *          RSVD_ENUMERIC at rsvd_sync
+ *          Jacobi.  A sketch rank-deficient to working precision (k + p >
+ *          rank(A)) takes a device-side Householder fallback on one GPU; a
+ *          row-sharded wide plan reports it as RSVD_ENUMERIC at rsvd_sync
  *   q      subspace iterations (Alg. 2)
  *   seed, stream  counter-based Omega (reading R1)
  *   center  1 = implicit column centring of A (rpca, Alg. 6)
