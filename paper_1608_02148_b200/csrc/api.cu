@@ -413,11 +413,11 @@ void bind(rsvd_ctx* ctx, Plan& p) {
 }
 
 rsvd_status allreduce_sum(rsvd_ctx* ctx, double* buf, size_t count) {
-  if (!ctx->comm || ctx->nranks <= 1 || count == 0) return RSVD_OK;
+  if (!ctx->comm || count == 0) return RSVD_OK;   // one rank has no communicator (but see RSVD_NCCL_SINGLE)
   return ctx->comm->allreduce(ctx, buf, count, false);
 }
 rsvd_status allreduce_max(rsvd_ctx* ctx, double* buf, size_t count) {
-  if (!ctx->comm || ctx->nranks <= 1 || count == 0) return RSVD_OK;
+  if (!ctx->comm || count == 0) return RSVD_OK;
   return ctx->comm->allreduce(ctx, buf, count, true);
 }
 rsvd_status allgather(rsvd_ctx* ctx, const double* send, double* recv, size_t count) {
@@ -1016,10 +1016,16 @@ rsvd_status rsvd_nccl_unique_id(void* out128) {
 rsvd_status rsvd_comm_init(rsvd_ctx* ctx, const void* id128, int nranks, int rank) {
   if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, RSVD_EINVAL, "bad comm args");
   if (ctx->comm) return fail(ctx, RSVD_EINVAL, "context already has a communicator");
-  if (nranks == 1) { ctx->nranks = 1; ctx->rank = 0; return RSVD_OK; }
-  if (!id128) return fail(ctx, RSVD_EINVAL, "null unique id");
+  // One rank needs no communicator.  RSVD_NCCL_SINGLE=1 (tests) still builds a
+  // one-rank NCCL communicator, so that every allreduce of the call goes through
+  // ncclAllReduce on the context's stream (an identity) on a single GPU.
+  const char* single = getenv("RSVD_NCCL_SINGLE");
+  if (nranks == 1 && !(single && single[0] == '1')) { ctx->nranks = 1; ctx->rank = 0; return RSVD_OK; }
   ncclUniqueId id;
-  memcpy(&id, id128, sizeof id);
+  if (id128) memcpy(&id, id128, sizeof id);
+  else if (nranks == 1) {
+    if (ncclGetUniqueId(&id) != ncclSuccess) return fail(ctx, RSVD_ENCCL, "ncclGetUniqueId failed");
+  } else return fail(ctx, RSVD_EINVAL, "null unique id");
   cudaSetDevice(ctx->device);
   NcclComm* c = new NcclComm();
   ncclResult_t r = ncclCommInitRank(&c->c, nranks, id, rank);

@@ -200,3 +200,37 @@ def test_wide_plan_sharded(rb, world):
     assert np.max(np.abs(d - o["d"]) / o["d"]) <= 1e-10
     assert np.abs(U.T @ U - np.eye(150)).max() <= 1e-12
     assert np.abs(V.T @ V - np.eye(150)).max() <= 1e-12
+
+
+def test_one_rank_nccl_communicator(rb, monkeypatch):
+    """The NCCL communicator itself on ONE GPU (RSVD_NCCL_SINGLE=1: a one-rank
+    ncclCommInitRank; every Gram / A^T X / column-sum / IALM-scalar allreduce of
+    the call is then a real in-stream ncclAllReduce, an identity at one rank,
+    followed by the library's stream fence).  rsvd, rpca and rrpca must equal the
+    communicator-free run bitwise (Alg. 4 steps (3)/(10))."""
+    monkeypatch.setenv("RSVD_NCCL_SINGLE", "1")
+    ctx = rb.Context()
+    ctx.init_comm(0, 1)
+    monkeypatch.delenv("RSVD_NCCL_SINGLE")
+    A, meta = synthetic.make_config(1)
+    Ad = A.cuda()
+    kw = dict(p=10, q=2, sdist="normal", seed=meta["seed_omega"])
+    r0 = rb.rsvd(Ad, 10, **kw)
+    r1 = rb.rsvd(Ad, 10, ctx=ctx, **kw)
+    assert torch.equal(r0.d, r1.d) and torch.equal(r0.u, r1.u) and torch.equal(r0.v, r1.v)
+    g = torch.Generator().manual_seed(5)
+    B = (torch.randn(3000, 40, generator=g, dtype=torch.float64) @ torch.randn(40, 300, generator=g, dtype=torch.float64)
+         + 3.0 + 0.01 * torch.randn(3000, 300, generator=g, dtype=torch.float64)).cuda()
+    p0 = rb.rpca(B, 20, seed=3)
+    p1 = rb.rpca(B, 20, seed=3, ctx=ctx)
+    for key in ("eigvals", "rotation", "x", "center", "scale"):
+        assert torch.equal(p0[key], p1[key]), key
+    L0 = torch.randn(400, 5, generator=g, dtype=torch.float64) @ torch.randn(5, 200, generator=g, dtype=torch.float64)
+    S0 = torch.zeros(400, 200, dtype=torch.float64)
+    idx = torch.rand(400, 200, generator=g) < 0.05
+    S0[idx] = 10.0 * torch.randn(int(idx.sum()), generator=g, dtype=torch.float64)
+    M = (L0 + S0).cuda()
+    q0 = rb.rrpca(M, k=10, maxiter=20, seed=1)
+    q1 = rb.rrpca(M, k=10, maxiter=20, seed=1, ctx=ctx)
+    assert q0["iters"] == q1["iters"]
+    assert torch.equal(q0["L"], q1["L"]) and torch.equal(q0["S"], q1["S"])
