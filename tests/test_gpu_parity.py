@@ -781,3 +781,24 @@ def test_rsvd_power_of_two_scaling(rb, e):
     # unit scale): it runs on the unscaled A, and 2^e d(A) is the scaled answer
     o = oracle.oracle_rsvd(A.numpy(), 40, p=10, q=2, seed=5)
     assert np.max(np.abs(d1 * 2.0 ** -e - o["d"]) / o["d"]) < 1e-10
+
+
+def test_rsvd_repeated_calls_bitwise(rb):
+    """Race check by repetition (compute-sanitizer is closed on the GPU pool):
+    200 config-2 calls (Np = 64 stream-K passes with fix-up flags, the Jacobi
+    rotation log replayed by other CTAs) and 100 calls at l = 120 (2-CTA paired
+    passes) enqueued back to back with no host synchronisation; every result
+    must equal the first call's bit for bit (tools/stress_determinism.py runs
+    the longer version over every kernel family)."""
+    A, meta = synthetic.make_config(2)
+    Ad = A.cuda()
+    for k, p, q, n_rep in ((50, 10, 2, 200), (100, 20, 1, 100)):
+        ref = rb.rsvd(Ad, k, p=p, q=q, sdist="rademacher", seed=meta["seed_omega"])
+        ref = [t.clone() for t in ref]
+        bad = torch.zeros((), dtype=torch.int64, device="cuda")
+        for _ in range(n_rep):
+            r = rb.rsvd(Ad, k, p=p, q=q, sdist="rademacher", seed=meta["seed_omega"], sync=False)
+            for a, b in zip(r, ref):
+                bad += (a != b).sum()
+        torch.cuda.synchronize()
+        assert int(bad.item()) == 0
