@@ -425,7 +425,8 @@ def main():
 
     # end to end through the host-buffer C-ABI calls (rsvd_run_host / rsvd_rpca_host /
     # rsvd_rrpca_host): A copied in from pinned host memory, results copied out, per step
-    if not args.no_e2e and world == 1:
+    # (N > 1: each rank passes its own row block from its pinned host memory)
+    if not args.no_e2e:
         A_host = A.cpu().pin_memory()
         e2e_steps = max(2, min(args.steps, 10 if not is_rrpca else 2))
         d2h = {}
@@ -433,29 +434,40 @@ def main():
         def e2e_step():
             if is_rrpca:
                 out = rb.rrpca(A_host, k=k, p=p, q=q, tol=meta["tol"], maxiter=100, sdist=meta["sdist"],
-                               seed=meta["seed_omega"], ctx=ctx)
+                               seed=meta["seed_omega"], ctx=ctx, m_global=m, row_offset=offset)
                 res = [out["L"], out["S"]]
             elif center:
                 out = rb.rpca(A_host, k, center=True, scale=False, p=p, q=q, sdist=meta["sdist"],
-                              seed=meta["seed_omega"], ctx=ctx)
+                              seed=meta["seed_omega"], ctx=ctx, m_global=m, row_offset=offset)
                 res = [out["rotation"], out["eigvals"], out["sdev"], out["x"], out["center"]]
             else:
-                r = rb.rsvd_host(A_host, k, p=p, q=q, sdist=meta["sdist"], seed=meta["seed_omega"], ctx=ctx)
+                r = rb.rsvd_host(A_host, k, p=p, q=q, sdist=meta["sdist"], seed=meta["seed_omega"], ctx=ctx,
+                                 m_global=m, row_offset=offset)
                 res = [r.d, r.u, r.v]
             d2h["bytes"] = int(sum(t.numel() * t.element_size() for t in res))
 
         e2e_step()
-        torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             e2e_step()
-        torch.cuda.synchronize()
+        barrier()
         ems = (time.perf_counter() - t0) * 1e3 / e2e_steps
+        if world > 1:
+            import torch.distributed as dist
+            te = torch.tensor([ems, float(m_loc * n * es), float(d2h["bytes"])], dtype=torch.float64, device=dev)
+            tmax = te.clone()
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+            dist.all_reduce(te, op=dist.ReduceOp.SUM)
+            ems, a_in, d_out = float(tmax[0].item()), int(te[1].item()), int(te[2].item())
+        else:
+            a_in, d_out = int(a_bytes), d2h["bytes"]
         line["e2e"] = {"value": round(step_bytes / (ems * 1e-3) / 1e9, 2), "unit": "GB/s",
                        "ms_per_step": round(ems, 3), "steps": e2e_steps,
-                       "h2d_bytes_per_step": int(a_bytes), "d2h_bytes_per_step": d2h["bytes"],
+                       "h2d_bytes_per_step": a_in, "d2h_bytes_per_step": d_out,
                        "call": "rsvd_rrpca_host" if is_rrpca else ("rsvd_rpca_host" if center else "rsvd_run_host"),
-                       "timing": "host wall clock around blocking calls (each returns after its D2H copy)"}
+                       "timing": "host wall clock around blocking calls (each returns after its D2H copy)"
+                                 + ("; max over ranks, bytes summed over ranks" if world > 1 else "")}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_run(meta, A.cpu().numpy(), args.cpu_budget)

@@ -160,7 +160,8 @@ rsvd_status rsvd_workspace_bytes(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd
 /* rsvd_run on HOST buffers (end to end): A is read from host memory (pinned
  * or pageable; m x n row-major, lda), copied to a device staging buffer the
  * context owns, factored, and u, d, v are copied back to HOST memory
- * (layouts as rsvd_run).  Single GPU only.  Blocks until the results are in
+ * (layouts as rsvd_run).  With a communicator A holds this rank's m_local
+ * rows (m_global / row_offset as rsvd_run; u gets the same rows).  Blocks until the results are in
  * host memory; returns the numerical status of the call (as rsvd_sync). */
 rsvd_status rsvd_run_host(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm,
                           void* u, int64_t ldu, void* d, void* v, int64_t ldv);
@@ -231,7 +232,7 @@ typedef struct {
 void rsvd_rpca_params_default(rsvd_params* prm, int32_t k);   /* rsvd defaults + center = scale = 1 */
 rsvd_status rsvd_rpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params* prm, const rsvd_pca_out* out);
 
-/* rsvd_rpca on HOST buffers (end to end, single GPU): A and every non-NULL
+/* rsvd_rpca on HOST buffers (end to end; with a communicator A holds this rank's rows and m_global / row_offset place them): A and every non-NULL
  * output of `out` are HOST memory (layouts as rsvd_rpca); A is staged into a
  * device buffer the context owns and the outputs are copied back.  Blocks;
  * returns the numerical status of the call (as rsvd_sync). */
@@ -283,7 +284,7 @@ rsvd_status rsvd_rrpca(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_rrpca_par
                        void* L, void* S, int64_t ld, int32_t* iters, double* final_residual,
                        double* trace);
 
-/* rsvd_rrpca on HOST buffers (end to end, single GPU): A, L, S HOST memory
+/* rsvd_rrpca on HOST buffers (end to end; with a communicator A holds this rank's rows and m_global / row_offset place them): A, L, S HOST memory
  * (m x n, ld == n); staged through device buffers the context owns. */
 rsvd_status rsvd_rrpca_host(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_rrpca_params* prm,
                             void* L, void* S, int64_t ld, int32_t* iters, double* final_residual,

@@ -365,7 +365,7 @@ def rsvd(A, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0, stream=0, ct
 
 
 def rsvd_host(A_host, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0, stream=0, ctx=None,
-              device="cuda", out=None):
+              device="cuda", out=None, m_global=None, row_offset=0):
     """End to end on HOST memory (rsvd_run_host): the library copies A (a CPU
     tensor, pinned for full copy bandwidth) to its device staging buffer,
     factors it and copies (d, u, v) back into CPU tensors (`out` to reuse them)."""
@@ -377,7 +377,7 @@ def rsvd_host(A_host, k, nu=None, nv=None, p=10, q=2, sdist="normal", seed=0, st
     nu_ = kk if nu is None else min(int(nu), kk)
     nv_ = kk if nv is None else min(int(nv), kk)
     dt = 0 if A_host.dtype == torch.float64 else 1
-    mat = Matrix(dt, A_host.data_ptr(), m, n, A_host.stride(0), m, 0)
+    mat = Matrix(dt, A_host.data_ptr(), m, n, A_host.stride(0), m if m_global is None else m_global, row_offset)
     prm = _params(k, nu_, nv_, p, q, sdist, seed, stream)
     if out is None:
         pin = torch.cuda.is_available()
@@ -468,7 +468,8 @@ def rpca(A, k, center=True, scale=True, retx=True, p=10, q=2, sdist="normal", se
     summary().  Every value is computed by the library.
     A CPU tensor runs end to end through rsvd_rpca_host (outputs on the CPU)."""
     if not A.is_cuda:
-        return _rpca_host(A, k, center, scale, retx, p, q, sdist, seed, stream, ctx, loadings, whiten, explained)
+        return _rpca_host(A, k, center, scale, retx, p, q, sdist, seed, stream, ctx, loadings, whiten, explained,
+                          m_global, row_offset)
     ctx = ctx or default_context(A.device)
     mat = _matrix(A, m_global, row_offset)
     m, n = A.shape
@@ -480,13 +481,14 @@ def rpca(A, k, center=True, scale=True, retx=True, p=10, q=2, sdist="normal", se
     return res
 
 
-def _rpca_host(A, k, center, scale, retx, p, q, sdist, seed, stream, ctx, loadings, whiten, explained):
+def _rpca_host(A, k, center, scale, retx, p, q, sdist, seed, stream, ctx, loadings, whiten, explained,
+               m_global=None, row_offset=0):
     ctx = ctx or default_context()
     if A.dim() != 2 or A.stride(1) != 1:
         raise ValueError("A must be a 2-D row-major tensor")
     m, n = A.shape
     dt = 0 if A.dtype == torch.float64 else 1
-    mat = Matrix(dt, A.data_ptr(), m, n, A.stride(0), m, 0)
+    mat = Matrix(dt, A.data_ptr(), m, n, A.stride(0), m if m_global is None else m_global, row_offset)
     res, o = _pca_outputs(m, n, int(k), A.dtype, "cpu", retx, center, scale, loadings, whiten, explained,
                           pin=torch.cuda.is_available())
     prm = _params(k, k, k, p, q, sdist, seed, stream, center, scale)
@@ -524,7 +526,7 @@ def rrpca(A, lam=None, maxiter=50, tol=1e-5, p=10, q=2, k=20, sdist="normal", se
         if A.dim() != 2 or not A.is_contiguous():
             raise ValueError("A must be a contiguous 2-D tensor")
         mat = Matrix(0 if A.dtype == torch.float64 else 1, A.data_ptr(), A.shape[0], A.shape[1], A.shape[1],
-                     A.shape[0], 0)
+                     A.shape[0] if m_global is None else m_global, row_offset)
     else:
         mat = _matrix(A, m_global, row_offset)
     prm = RrpcaParams()

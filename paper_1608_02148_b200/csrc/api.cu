@@ -1162,7 +1162,6 @@ rsvd_status rsvd_run_host(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params
                           void* d, void* v, int64_t ldv) {
   int64_t mg, n;
   CKS(validate(ctx, A, prm, &mg, &n));
-  if (ctx->nranks > 1) return fail(ctx, RSVD_EUNSUPPORTED, "rsvd_run_host is single-GPU");
   if (!d) return fail(ctx, RSVD_EINVAL, "d is null");
   const int k = prm->k, nu = std::min(prm->nu, k), nv = std::min(prm->nv, k);
   if (nu > 0 && (!u || ldu < nu)) return fail(ctx, RSVD_EINVAL, "u null or ldu < nu");
@@ -1180,7 +1179,8 @@ rsvd_status rsvd_run_host(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_params
   // A: host (lda) -> device (ld n)
   CK(cudaMemcpy2DAsync(dA, n * es, A->A, A->lda * es, n * es, m, cudaMemcpyHostToDevice, ctx->stream));
   rsvd_matrix Ad = *A;
-  Ad.A = dA; Ad.lda = n; Ad.m_global = m; Ad.row_offset = 0;
+  Ad.A = dA; Ad.lda = n;                  // this rank's row block keeps its place in the sharded matrix
+  if (ctx->nranks <= 1) { Ad.m_global = m; Ad.row_offset = 0; }
   rsvd_params pr = *prm;
   pr.nu = nu; pr.nv = nv;
   CKS(rsvd_run(ctx, &Ad, &pr, nu ? dU : nullptr, std::max(nu, 1), dD, nv ? dV : nullptr, std::max(nv, 1)));
@@ -1330,7 +1330,6 @@ rsvd_status rsvd_rpca_host(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_param
   int64_t mg, n;
   CKS(validate(ctx, A, prm, &mg, &n));
   if (!o) return fail(ctx, RSVD_EINVAL, "null output descriptor");
-  if (ctx->nranks > 1) return fail(ctx, RSVD_EUNSUPPORTED, "rsvd_rpca_host is single-GPU");
   CK(cudaSetDevice(ctx->device));
   const size_t es = A->dtype == RSVD_F32 ? 4 : 8;
   const int64_t m = A->m_local, k = prm->k;
@@ -1350,7 +1349,8 @@ rsvd_status rsvd_rpca_host(rsvd_ctx* ctx, const rsvd_matrix* A, const rsvd_param
   char* dA = ctx->ws5;
   CK(cudaMemcpy2DAsync(dA, n * es, A->A, A->lda * es, n * es, m, cudaMemcpyHostToDevice, ctx->stream));
   rsvd_matrix Ad = *A;
-  Ad.A = dA; Ad.lda = n; Ad.m_global = m; Ad.row_offset = 0;
+  Ad.A = dA; Ad.lda = n;                  // this rank's row block keeps its place in the sharded matrix
+  if (ctx->nranks <= 1) { Ad.m_global = m; Ad.row_offset = 0; }
   rsvd_pca_out od = *o;
   auto dptr = [&](void* h) -> void* {
     for (int i = 0; i < no; ++i) if (outs[i].host == h) return ctx->ws5 + outs[i].off;
@@ -1483,7 +1483,6 @@ extern "C" rsvd_status rsvd_rrpca_host(rsvd_ctx* ctx, const rsvd_matrix* A, cons
   if (!ctx) return RSVD_EINVAL;
   if (!A || !A->A || !prm || !L || !S) return fail(ctx, RSVD_EINVAL, "null argument");
   if (A->dtype != RSVD_F64) return fail(ctx, RSVD_EUNSUPPORTED, "rrpca is FP64 only");
-  if (ctx->nranks > 1) return fail(ctx, RSVD_EUNSUPPORTED, "rsvd_rrpca_host is single-GPU");
   if (A->m_local < 1 || A->n < 1 || A->lda != A->n || ld != A->n)
     return fail(ctx, RSVD_EUNSUPPORTED, "rrpca needs contiguous A, L, S (lda == ld == n)");
   CK(cudaSetDevice(ctx->device));
@@ -1494,7 +1493,8 @@ extern "C" rsvd_status rsvd_rrpca_host(rsvd_ctx* ctx, const rsvd_matrix* A, cons
   char* dS = dL + b;
   CK(cudaMemcpyAsync(dA, A->A, bytes, cudaMemcpyHostToDevice, ctx->stream));
   rsvd_matrix Ad = *A;
-  Ad.A = dA; Ad.m_global = A->m_local; Ad.row_offset = 0;
+  Ad.A = dA;
+  if (ctx->nranks <= 1) { Ad.m_global = A->m_local; Ad.row_offset = 0; }
   CKS(rsvd_rrpca(ctx, &Ad, prm, dL, dS, ld, iters_out, res_out, trace));
   CK(cudaMemcpyAsync(L, dL, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(S, dS, bytes, cudaMemcpyDeviceToHost, ctx->stream));

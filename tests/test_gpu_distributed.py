@@ -234,3 +234,63 @@ def test_one_rank_nccl_communicator(rb, monkeypatch):
     q1 = rb.rrpca(M, k=10, maxiter=20, seed=1, ctx=ctx)
     assert q0["iters"] == q1["iters"]
     assert torch.equal(q0["L"], q1["L"]) and torch.equal(q0["S"], q1["S"])
+
+
+def test_host_buffer_calls_sharded(rb):
+    """The host-buffer C-ABI calls on a row-sharded matrix (2 ranks): each rank
+    passes its own rows from host memory (m_global / row_offset place them), the
+    library copies them in, runs the sharded path and copies its rows of U / the
+    scores back.  Results equal the device-buffer sharded run bitwise and the
+    1-rank run to 1e-12 (Alg. 4 steps (3)/(10); Alg. 6)."""
+    A, meta = synthetic.make_config(2, scale_rows=3000)
+    A = A[:, :1200].contiguous()
+    Ad = A.cuda()
+    m = A.shape[0]
+    world = 2
+    parts = rb.row_partition(m, world)
+    kw = dict(p=10, q=2, sdist="rademacher", seed=meta["seed_omega"])
+
+    def fn_host(ctx, r):
+        off, rows = parts[r]
+        blk = A[off:off + rows].contiguous().pin_memory()
+        res = rb.rsvd_host(blk, 30, ctx=ctx, m_global=m, row_offset=off, **kw)
+        pca = rb.rpca(blk, 20, ctx=ctx, m_global=m, row_offset=off, seed=3)
+        return res, pca
+
+    def fn_dev(ctx, r):
+        off, rows = parts[r]
+        res = rb.rsvd(Ad[off:off + rows], 30, ctx=ctx, m_global=m, row_offset=off, **kw)
+        pca = rb.rpca(Ad[off:off + rows], 20, ctx=ctx, m_global=m, row_offset=off, seed=3)
+        return res, pca
+
+    oh = rb.run_ranks(fn_host, world)
+    od = rb.run_ranks(fn_dev, world)
+    for (rh, ph), (rd, pd) in zip(oh, od):
+        assert not rh.d.is_cuda and not ph["x"].is_cuda
+        assert torch.equal(rh.d, rd.d.cpu()) and torch.equal(rh.u, rd.u.cpu()) and torch.equal(rh.v, rd.v.cpu())
+        for key in ("eigvals", "rotation", "x", "center", "scale", "sdev"):
+            assert torch.equal(ph[key], pd[key].cpu()), key
+    r1 = rb.rsvd(Ad, 30, **kw)
+    d1 = _np(r1.d)
+    assert np.max(np.abs(_np(oh[0][0].d) - d1) / d1) <= 1e-12
+    p1 = rb.rpca(Ad, 20, seed=3)
+    e1 = _np(p1["eigvals"])
+    assert np.max(np.abs(_np(oh[0][1]["eigvals"]) - e1) / e1) <= 1e-12
+    x = torch.cat([o[1]["x"] for o in oh], 0)
+    assert x.shape == (m, 20)
+    # rrpca through rsvd_rrpca_host on the same two ranks
+    As, _, _ = synthetic.sparse_plus_lowrank(2000, 200, rank=5, frac=0.05, seed=7)
+    Asd = As.cuda()
+    parts2 = rb.row_partition(2000, world)
+
+    def rr(host):
+        def fn(ctx, r):
+            off, rows = parts2[r]
+            blk = As[off:off + rows].contiguous() if host else Asd[off:off + rows]
+            return rb.rrpca(blk, k=10, p=10, q=2, tol=1e-7, maxiter=60, seed=8, ctx=ctx, m_global=2000, row_offset=off)
+        return rb.run_ranks(fn, world)
+
+    qh, qd = rr(True), rr(False)
+    for a, b in zip(qh, qd):
+        assert a["iters"] == b["iters"]
+        assert torch.equal(a["L"], b["L"].cpu()) and torch.equal(a["S"], b["S"].cpu())
