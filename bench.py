@@ -418,8 +418,8 @@ def main():
                        "sdist": meta["sdist"], "center": bool(center), "passes_per_rsvd": passes,
                        "A_bytes": a_bytes, "bytes_per_step": step_bytes,
                        "rrpca_iters": rr_state.get("iters"), "rrpca_residual": rr_state.get("residual"),
-                       "l2_policy": ("A (%d MB) > L2 (126 MB): no flush" % (a_bytes >> 20)) if a_bytes > 126e6
-                       else "A L2-resident (latency-bound config)",
+                       "l2_policy": ("A per rank (%d MB) > L2 (126 MB): no flush" % ((m_loc * n * es) >> 20))
+                       if m_loc * n * es > 126e6 else "A L2-resident per rank (latency-bound config)",
                        "parallelism": "row-sharded dp%d" % world, "rows_per_rank": m_loc},
             "roofline": roof, "gpu_launches": int(launches), "clocks": clocks, "diagnostics": diag}
 
